@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py -- FEM harmonic inpainting hot path on B200 (arXiv 2105.01586).
+
+Workload (default, BASELINE.json configs[4], "C5"): 8192x8192 fp64 synthetic image (bump
+sigma x32), 2 % mask from one densification pass (1 % random + 1 % selected by per-triangle
+error), p = m unknown vertices. Setup (untimed, reported): image generation, the
+densification pass, host mesh_build, assemble. One timed STEP = one full inpainting:
+inpaint_solve (Jacobi-PCG to relative residual 1e-10, x0 = midrange(g)) + rasterise_error
+(u image, e image, per-triangle error and best pixel, SSE). Inputs (f 537 MB) exceed L2,
+so no extra flush is needed between steps.
+
+    value  = whole-job Mpixels/s = ranks * W*H * K / max-over-ranks device time
+    e2e    = the same with f and g copied host->device (pinned) and SSE device->host
+             inside every step
+    roofline: the PCG loop (k_spmv_dot + k_update), algorithmic bytes per iteration
+             12 nnz_uu + 4 (n_u+1) + 80 n_u x iterations over
+             the solve's device time, against MEASURED_PEAKS.json hbm_gbs.
+    cpu_baseline: the fp64 oracle (oracle/, 1 thread) on the same workload, run in a
+             separate process on a host core while the GPU part runs.
+
+--impl reference times the oracle alone (the reference arm of this tier).
+--gpus N (torchrun): replicas only -- every rank runs its own copy.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import make_config, schedule  # noqa: E402
+
+RTOL = 1e-10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5, help="1 or 5 (single-image inpainting configs)")
+    ap.add_argument("--size", type=int, default=0, help="override W=H (scaled variant of the config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def workload_inputs(cfg: int, size: int = 0):
+    """Seeded inputs; for the densify-type config the initial random mask + schedule."""
+    c = make_config(cfg, W=size or None, H=size or None)
+    return c
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+
+def oracle_run(cfg: int, size: int, mode: str, steps: int, warmup: int, q):
+    """Runs in a separate process. mode 'baseline': one full oracle step (solve to 1e-12 +
+    raster + error) timed; mode 'reference': setup + one full step, then steps of a bounded
+    sample (8 CG iterations + full raster+error) extrapolated with the full step's count."""
+    try:
+        import oracle
+        c = workload_inputs(cfg, size)
+        W, H = c["W"], c["H"]
+        f = c["f"].reshape(-1)
+        t0 = time.time()
+        if c["kind"].startswith("densify"):
+            mask, _, _ = oracle.densify(W, H, c["f"], c["mask0"], c["unknowns"], c["schedule"][:2], rtol=1e-12)
+        else:
+            mask = c["mask"]
+        S = oracle.System(W, H, mask, c["unknowns"])
+        t_setup = time.time() - t0
+        g = f[S.mask_px]
+        t0 = time.perf_counter()
+        u, st, iters, rr = S.solve(g, rtol=1e-12)
+        t1 = time.perf_counter()
+        R = S.raster(u, f)
+        t2 = time.perf_counter()
+        full = dict(solve_s=t1 - t0, raster_s=t2 - t1, iters=iters, mse=R["mse"], setup_s=t_setup, n_u=S.n_u,
+                    nnz_uu=S.nnz_uu)
+        out = dict(full=full, samples=[])
+        if mode == "reference":
+            K = 8
+            for s in range(warmup + steps):
+                a = time.perf_counter()
+                S.solve(g, rtol=1e-300, max_iter=K, method=2)
+                b = time.perf_counter()
+                S.raster(u, f)
+                c2 = time.perf_counter()
+                out["samples"].append(dict(t_iter=(b - a) / K, raster_s=c2 - b, warm=s < warmup))
+        q.put(out)
+    except Exception as e:  # report, never hang the bench
+        q.put({"error": repr(e)})
+
+
+def start_oracle(cfg, size, mode, steps=0, warmup=0):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=oracle_run, args=(cfg, size, mode, steps, warmup, q), daemon=True)
+    p.start()
+    return p, q
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    p, q = start_oracle(args.config, args.size, "reference", args.steps, args.warmup)
+    out = q.get()
+    p.join(timeout=60)
+    c = make_config(args.config, W=args.size or None, H=args.size or None)
+    Npx = c["W"] * c["H"]
+    if "error" in out:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle failed: " + out["error"]}))
+        return 0
+    full = out["full"]
+    timed = [s for s in out["samples"] if not s["warm"]]
+    per_step = [s["t_iter"] * full["iters"] + s["raster_s"] for s in timed]
+    ms = 1e3 * float(np.mean(per_step))
+    value = Npx / (ms * 1e-3) / 1e6
+    line = {
+        "impl": "reference", "metric": "FEM inpainting Mpixels/s (solve+raster+error)", "value": value,
+        "unit": "Mpx/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, c),
+        "cpu_baseline": {"value": value, "unit": "Mpx/s", "cores": 1, "kind": "oracle",
+                         "sample": f"setup: oracle densify + mesh + one full solve ({full['iters']} plain-CG "
+                                   f"iterations to 1e-12, {full['solve_s']:.1f} s) + raster ({full['raster_s']:.1f} s);"
+                                   f" each step: 8 CG iterations + full raster+error, extrapolated to "
+                                   f"{full['iters']} iterations"},
+        "e2e": {"value": value, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "oracle_full_step_s": full["solve_s"] + full["raster_s"],
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_dict(args, c):
+    return {"workload": f"C{args.config}: {c['W']}x{c['H']} fp64 synthetic, "
+                        f"{'2% mask from one densification pass (1% random + 1% selected)' if args.config == 5 else '5% random mask'}, "
+                        "p = m unknown vertices; step = PCG solve (rtol 1e-10) + rasterise + error maps + MSE",
+            "W": c["W"], "H": c["H"], "global_batch": 1, "parallelism": f"replicas{args.gpus}",
+            "l2_flush": "inputs larger than L2 (f = 537 MB)" if c["W"] * c["H"] * 8 > 126 * 2**20 else
+                        "L2-resident working set (no flush; latency-bound config)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    from paper_2105_01586_b200 import femi, pipeline
+
+    baseline_proc = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        baseline_proc = start_oracle(args.config, args.size, "baseline")
+
+    # ---- setup (untimed, reported)
+    t0 = time.time()
+    c = workload_inputs(args.config, args.size)
+    W, H = c["W"], c["H"]
+    Npx = W * H
+    f_dev = torch.as_tensor(c["f"], dtype=torch.float64, device=dev).reshape(-1)
+    t_gen = time.time() - t0
+    setup = {"generate_s": t_gen}
+    if c["kind"].startswith("densify"):
+        t0 = time.time()
+        mask, recs, _ = pipeline.densify(W, H, f_dev, c["mask0"], c["unknowns"], c["schedule"][:2], rtol=RTOL)
+        setup["densify_pass_s"] = time.time() - t0
+        setup["densify_mesh_s"] = recs[0]["mesh_seconds"]
+    else:
+        mask = c["mask"]
+    t0 = time.time()
+    mesh = femi.Mesh(W, H, mask, c["unknowns"])
+    setup["mesh_build_s"] = mesh.build_seconds
+    setup["mesh_threads"] = mesh.build_threads
+    torch.cuda.synchronize()
+    t1 = time.time()
+    sysm = femi.System(mesh)
+    torch.cuda.synchronize()
+    setup["assemble_s"] = time.time() - t1
+    vert = mesh.export()["vert_px"]
+    info = mesh.info
+    g_dev = pipeline.mask_values(f_dev, vert, sysm.n_u)
+    u_vert = torch.empty(sysm.nv, dtype=torch.float64, device=dev)
+    u_px = torch.empty(Npx, dtype=torch.float64, device=dev)
+    e_px = torch.empty(Npx, dtype=torch.float64, device=dev)
+    tri_err = torch.empty(sysm.T, dtype=torch.float64, device=dev)
+    best = torch.empty(sysm.T, dtype=torch.int32, device=dev)
+    sse = torch.zeros(1, dtype=torch.float64, device=dev)
+    opts = femi.cg_opts(rtol=RTOL)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        st, it, rel = femi.inpaint_solve_batched([sysm], [g_dev], [u_vert], opts)
+        if ev:
+            ev[1].record(stream)
+        femi.rasterise_error(sysm, u_vert, f_dev, sse, u_px, e_px, tri_err, best)
+        if ev:
+            ev[2].record(stream)
+        return st, int(it[0]), float(rel[0])
+
+    for _ in range(args.warmup):
+        st, iters, rel = step()
+    torch.cuda.synchronize()
+    assert st == 0 and rel <= RTOL, f"solve failed: status {st} relres {rel}"
+
+    # ---- timed region (device events, barrier + sync both sides)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = femi.kernel_launches()
+    it_list = []
+    with Clocks(local) as clk:
+        e_start.record(stream)
+        for k in range(args.steps):
+            st, iters, rel = step(evs[k])
+            it_list.append(iters)
+        e_end.record(stream)
+        torch.cuda.synchronize()
+    launches = femi.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    total_ms = e_start.elapsed_time(e_end)
+    solve_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    raster_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    t_max = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    total_ms = float(t_max.item())
+    ms_per_step = total_ms / args.steps
+    value = world * Npx * args.steps / (total_ms * 1e-3) / 1e6
+    mse = sse.item() / Npx
+
+    # ---- e2e: host buffers (pinned) in, SSE out, every step
+    e2e = None
+    if not args.no_e2e:
+        f_host = torch.empty(Npx, dtype=torch.float64, pin_memory=True)
+        f_host.copy_(torch.as_tensor(c["f"].reshape(-1)))
+        g_host = torch.empty(sysm.m, dtype=torch.float64, pin_memory=True)
+        g_host.copy_(g_dev.cpu())
+        f_d2 = torch.empty_like(f_dev)
+        g_d2 = torch.empty_like(g_dev)
+        sse_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+
+        def step_e2e():
+            f_d2.copy_(f_host, non_blocking=True)
+            g_d2.copy_(g_host, non_blocking=True)
+            femi.inpaint_solve_batched([sysm], [g_d2], [u_vert], opts)
+            femi.rasterise_error(sysm, u_vert, f_d2, sse, u_px, e_px, tri_err, best)
+            sse_host.copy_(sse, non_blocking=True)
+            stream.synchronize()
+            return float(sse_host[0])
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            s_e2e = step_e2e()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        assert abs(s_e2e / Npx - mse) <= 1e-9 * mse
+        e2e = {"value": world * Npx * args.steps / (float(t.item()) * 1e-3) / 1e6, "unit": "Mpx/s",
+               "h2d_bytes_per_step": int(8 * Npx + 8 * sysm.m), "d2h_bytes_per_step": 8}
+
+    # ---- roofline of the PCG loop (SURVEY §8(d) algorithmic bytes)
+    n_u, nnz_uu = info["n_unknown"], info["nnz_uu"]
+    bytes_iter = 12 * nnz_uu + 4 * (n_u + 1) + 80 * n_u
+    iters = int(np.median(it_list))
+    solve_s = float(np.median(solve_ms)) * 1e-3
+    achieved = bytes_iter * iters / solve_s / 1e9
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"C{args.config}", {}).get("pcg_bytes_per_iter")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if baseline_proc is not None:
+        p, q = baseline_proc
+        try:
+            out = q.get(timeout=900)
+        except Exception as e:
+            out = {"error": repr(e)}
+        p.join(timeout=30)
+        if "full" in out:
+            fo = out["full"]
+            t_cpu = fo["solve_s"] + fo["raster_s"]
+            cpu = {"value": Npx / t_cpu / 1e6, "unit": "Mpx/s", "cores": 1, "kind": "oracle",
+                   "sample": f"the whole step once: oracle plain CG to 1e-12 ({fo['iters']} iterations, "
+                             f"{fo['solve_s']:.1f} s) + raster+error ({fo['raster_s']:.1f} s) on the oracle's own "
+                             f"densified mesh of the same seeded input; oracle MSE {fo['mse']:.6f}"}
+        else:
+            cpu = {"value": None, "unit": "Mpx/s", "cores": 1, "kind": "oracle", "sample": out.get("error")}
+
+    if rank == 0:
+        line = {
+            "metric": "FEM inpainting Mpixels/s (solve+raster+error)", "value": value, "unit": "Mpx/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, c),
+            "roofline": {"bound": "hbm", "kernel": "pcg loop (k_spmv_dot + k_update)", "achieved": achieved,
+                         "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "bytes_per_iter": bytes_iter, "iters": iters,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "detail": {"solve_ms": float(np.median(solve_ms)), "raster_ms": float(np.median(raster_ms)),
+                       "cg_iters": iters, "us_per_cg_iter": 1e3 * float(np.median(solve_ms)) / max(iters, 1),
+                       "mse": mse, "n_unknown": n_u, "n_mask": info["n_mask"], "n_tri": info["n_tri"],
+                       "nnz_uu": nnz_uu, "nnz_uk": info["nnz_uk"], "setup": setup, "version": femi.version()},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,222 @@
+/*
+ * femi.h -- C ABI of the B200-native FEM harmonic-inpainting hot path
+ * (Chizhov & Weickert, "Efficient Data Optimisation for Harmonic Inpainting with Finite
+ * Elements", arXiv 2105.01586). Library: paper_2105_01586_b200/libfemi.so (sm_100a).
+ *
+ * Citations "PAPER.md:Lx-y" refer to the paper's LaTeX source; readings A1..A18 are the
+ * interpretations frozen in DESIGN.md where the paper is silent.
+ *
+ * Conventions (all calls):
+ *  - Pixel index pix = y*W + x; pixel centres at integer (x, y); Omega = [0,W-1]x[0,H-1]
+ *    (reading A1). Images are row-major fp64 arrays of W*H values on the 0..255 scale.
+ *  - Vertex numbering is canonical: unknown vertices first (ascending pix), then mask
+ *    vertices (ascending pix). A vertex-value vector u_vert has n_vert = n_unknown +
+ *    n_mask entries in that order; a mask-value vector g has n_mask entries in ascending
+ *    mask-pix order.
+ *  - Handles (femi_mesh, femi_system) are created and freed only by the library and are
+ *    immutable after creation, EXCEPT that a femi_system caches device scratch for its
+ *    solves: at most one call may be in flight per femi_system at a time.
+ *  - Device pointers are caller-owned (e.g. PyTorch tensors); the library never frees
+ *    them; they must stay valid until the enqueued work completes. All device work is
+ *    enqueued on the caller's stream (femi_stream == cudaStream_t; NULL = legacy default
+ *    stream). Calls that return host outputs synchronise that stream before returning.
+ *  - Every call returns a femi_status; on failure femi_last_error() returns a thread-local
+ *    message. No C++ exception crosses the ABI. There is no CPU fallback: without a usable
+ *    sm_100 device the device calls return FEMI_E_CUDA.
+ */
+#ifndef FEMI_H
+#define FEMI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* femi_stream; /* == cudaStream_t */
+
+typedef enum {
+    FEMI_OK = 0,
+    FEMI_E_ARG = 1,           /* invalid argument (NULL, negative size, bad option)      */
+    FEMI_E_DEGENERATE = 2,    /* W < 2 or H < 2: every vertex collinear                  */
+    FEMI_E_NO_MASK = 3,       /* no Dirichlet vertex: A_uu singular  */
+    FEMI_E_NOT_CONVERGED = 4, /* max_iter reached; outputs hold the last iterate          */
+    FEMI_E_NONFINITE = 5,     /* NaN/Inf in inputs or iterates                            */
+    FEMI_E_NEG_CURVATURE = 6, /* p.Ap <= 0 inside CG: matrix not SPD                      */
+    FEMI_E_SIZE = 7,          /* pix out of range, duplicates, mask/unknown overlap, W or H > 16384 */
+    FEMI_E_CUDA = 8,          /* CUDA runtime error (message has the CUDA error string)   */
+    FEMI_E_OOM = 9            /* host or device allocation failed                         */
+} femi_status;
+
+const char* femi_last_error(void);
+const char* femi_version(void);
+/* Number of CUDA kernels this library has launched since it was loaded (all threads). */
+int64_t femi_kernel_launches(void);
+
+typedef struct femi_mesh_s* femi_mesh;
+typedef struct femi_system_s* femi_system;
+
+typedef struct {
+    int64_t width, height;
+    int64_t n_vert, n_unknown, n_mask, n_tri;
+    int64_t nnz_uu; /* A_uu entries incl. the diagonal (reading A5) */
+    int64_t nnz_uk; /* A_uk entries                                  */
+} femi_mesh_info;
+
+/* ---------------------------------------------------------------------------------
+ * S0 mesh_build (HOST setup stage, timed separately).
+ * "Every mask pixel is a vertex in this mesh, and a subset of the
+ * remaining non-mask pixels are chosen as unknowns ... a Delaunay triangulation is
+ * constructed from the point set formed by the vertices". Corners missing from both sets
+ * are added as unknowns (reading A2). Cocircular ties are broken by the symbolic
+ * perturbation of reading A3, so the triangulation is unique and independent of the
+ * input order. Triangles are CCW, rotated so the smallest pix comes first, sorted
+ * lexicographically by pix triple.
+ *   mask_px[m], unknown_px[p]: HOST arrays of distinct pixels, any order, disjoint.
+ *   out: receives a new handle (free with femi_mesh_free).
+ * Errors: FEMI_E_ARG (NULL), FEMI_E_DEGENERATE (W<2 or H<2), FEMI_E_SIZE (range,
+ * duplicates, overlap, W or H > 16384), FEMI_E_NO_MASK (m == 0), FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_mesh_build(int32_t W, int32_t H, const int32_t* mask_px, int64_t m,
+                            const int32_t* unknown_px, int64_t p, femi_mesh* out);
+femi_status femi_mesh_info_get(femi_mesh mesh, femi_mesh_info* info);
+/* Canonical arrays to HOST buffers (any pointer may be NULL to skip it):
+ *   vert_px[n_vert], tri_vert[3*n_tri] (canonical vertex indices),
+ *   uu_rowptr[n_unknown+1], uu_col[nnz_uu] (unknown indices, ascending, diagonal included),
+ *   uk_rowptr[n_unknown+1], uk_col[nnz_uk] (mask indices, ascending). */
+femi_status femi_mesh_export(femi_mesh mesh, int32_t* vert_px, int32_t* tri_vert,
+                             int32_t* uu_rowptr, int32_t* uu_col,
+                             int32_t* uk_rowptr, int32_t* uk_col);
+/* Host seconds spent in the last femi_mesh_build of this handle (triangulation, canonical
+ * ordering, tables) and the host threads it used. */
+femi_status femi_mesh_timing(femi_mesh mesh, double* seconds, int32_t* threads);
+void femi_mesh_free(femi_mesh mesh);
+
+/* ---------------------------------------------------------------------------------
+ * S1 assemble (DEVICE). PAPER.md:L229-237 linear FEM: for each triangle (i,j,k) the entry
+ * A_ij receives -1/2 cot(angle at k); the diagonal makes every row of the full matrix
+ * sum to zero (natural Neumann border, Eq. (3)); Dirichlet elimination of
+ * the mask vertices (Eq. (2)) splits the unknown rows into A_uu and A_uk (reading A6 fixes
+ * the rounding). Also builds the pixel-ownership flags (reading A7) and the Jacobi scaling
+ * used by the solver. Uploads the mesh tables and enqueues the assembly kernels on
+ * `stream`; returns after enqueueing (the handle is usable by later calls on any stream
+ * ordered after it).
+ * Errors: FEMI_E_ARG, FEMI_E_CUDA, FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out);
+femi_status femi_system_info_get(femi_system sys, femi_mesh_info* info);
+/* Unscaled CSR values (pattern of femi_mesh_export) to HOST buffers uu_val[nnz_uu],
+ * uk_val[nnz_uk]; synchronises `stream`. */
+femi_status femi_system_export(femi_system sys, double* uu_val, double* uk_val, femi_stream stream);
+void femi_system_free(femi_system sys);
+
+/* ---------------------------------------------------------------------------------
+ * S2 inpaint_solve_batched (DEVICE). PAPER.md:L236-239: A_uu is SPD given >= 1 mask
+ * pixel; "we can use the conjugate gradient method". Solves A_uu x = -A_uk g for B
+ * right-hand sides with Jacobi-preconditioned CG (preconditioning changes iterates, not
+ * the solution). Stops when the relative residual ||b - A x||_2 / ||b||_2 <= rtol, the
+ * residual being confirmed with a fresh SpMV at exit (reading A11).
+ *   sys[B]: system handles (distinct meshes -> block-diagonal batch; a repeated handle
+ *           shares its matrix).
+ *   g[B]: HOST array of DEVICE pointers, g[b] has n_mask values of sys[b].
+ *   u_vert[B]: HOST array of DEVICE pointers, u_vert[b] has n_vert values: on return the
+ *           unknown entries hold x and the mask entries hold g exactly. With x0 == 2 the
+ *           unknown entries are read as the initial guess.
+ *   opts: rtol (> 0), max_iter (> 0), precond (0 none, 1 Jacobi), x0 (0 zeros, 1
+ *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided),
+ *         check_every (iterations between device->host convergence polls; 0 = default).
+ *   iters[B], relres[B]: HOST outputs (iteration count, final true relative residual).
+ * Special cases: ||b|| == 0 -> x = 0, 0 iterations; n_unknown == 0 -> no-op; an initial
+ * guess that already satisfies rtol exits with 0 iterations and is returned unchanged.
+ * Synchronises `stream`. Errors: FEMI_E_ARG, FEMI_E_NOT_CONVERGED (outputs written),
+ * FEMI_E_NONFINITE, FEMI_E_NEG_CURVATURE, FEMI_E_CUDA, FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    double rtol;
+    int32_t max_iter;
+    int32_t precond;
+    int32_t x0;
+    int32_t check_every;
+} femi_cg_opts;
+
+femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const double* const* g,
+                                       double* const* u_vert, const femi_cg_opts* opts,
+                                       int32_t* iters, double* relres, femi_stream stream);
+
+/* ---------------------------------------------------------------------------------
+ * S3+S4 rasterise_error (DEVICE). PAPER.md:L239-241 "the solution is linearly
+ * interpolated within each triangle"; "error map e_i = (u_i - f_i)^2 ...
+ * the total L2 error in each triangle". Each pixel belongs to the lowest-index closed
+ * triangle containing it (reading A7). A vertex pixel takes its vertex value exactly;
+ * otherwise u = u_a + l_b (u_b - u_a) + l_c (u_c - u_a) with exact-integer barycentric
+ * numerators (S3).
+ *   u_vert[n_vert], f[W*H]: DEVICE inputs.
+ *   u_px[W*H], e_px[W*H]: DEVICE outputs, nullable.
+ *   tri_err[n_tri]: DEVICE output, nullable: sum of e over the triangle's pixels.
+ *   tri_best_px[n_tri]: DEVICE output, nullable: owned non-vertex pixel with the largest
+ *           e (ties: lowest pix), -1 if none (reading A8).
+ *   sse: DEVICE scalar output (sum of e over all pixels; MSE = sse / (W*H)).
+ * Enqueues only (no synchronisation). Errors: FEMI_E_ARG, FEMI_E_CUDA.
+ * The _batched form takes B systems and HOST arrays of DEVICE pointers (entries of the
+ * optional outputs may be NULL); sse[b] are separate device scalars.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_rasterise_error(femi_system sys, const double* u_vert, const double* f,
+                                 double* u_px, double* e_px, double* tri_err, int32_t* tri_best_px,
+                                 double* sse, femi_stream stream);
+femi_status femi_rasterise_error_batched(int32_t B, const femi_system* sys, const double* const* u_vert,
+                                         const double* const* f, double* const* u_px, double* const* e_px,
+                                         double* const* tri_err, int32_t* const* tri_best_px,
+                                         double* const* sse, femi_stream stream);
+
+/* ---------------------------------------------------------------------------------
+ * S5 densify_step (DEVICE + host result). PAPER.md:L262-268: "We insert a single mask
+ * pixel in each triangle, in descending order of the L2 error. The position of the mask
+ * pixel within a triangle is chosen to be at the empty location with the largest
+ * pointwise error." Rasterises u_vert against f, orders triangles by (tri_err desc, index
+ * asc), skips triangles with zero error or no empty pixel, takes the first b, and fills
+ * any shortfall with the globally largest-error empty pixels (ties: lowest pix) (readings
+ * A8-A10).
+ *   f[W*H], u_vert[n_vert]: DEVICE inputs; b >= 0.
+ *   new_mask_px[b]: HOST output, ascending pix; *n_added = number written (== b unless
+ *           fewer than b empty pixels exist).
+ * Synchronises `stream`. Errors: FEMI_E_ARG, FEMI_E_CUDA, FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_densify_step(femi_system sys, const double* f, const double* u_vert, int64_t b,
+                              int32_t* new_mask_px, int64_t* n_added, femi_stream stream);
+
+/* ---------------------------------------------------------------------------------
+ * S6 tonal_optimise (DEVICE + host report). PAPER.md:L280-316, Eqs. (4)-(5):
+ * g* = argmin ||B g - f||^2 solved as B^T B g = B^T f by CG on the normal equations in
+ * CGLS form ("nested conjugate gradient solver"), B g = P_k g + P_u A_uu^-1 (-A_uk g)
+ * applied matrix-free: each outer iteration runs one forward and one adjoint inner
+ * inpainting solve. Starts from g (in), stops when ||B^T(f - B g)|| / ||B^T f|| < outer_rtol
+ * or after outer_max iterations; the reported gradient and MSE are recomputed with fresh
+ * solves at exit (reading A13).
+ *   f[W*H]: DEVICE; g[n_mask]: DEVICE, in = initial values (e.g. f at the mask), out = g*.
+ *   report: HOST output. Synchronises `stream`.
+ * Errors: FEMI_E_ARG, FEMI_E_NOT_CONVERGED (g written), FEMI_E_NONFINITE, FEMI_E_CUDA,
+ * FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    double outer_rtol;
+    int32_t outer_max;
+    femi_cg_opts inner;
+    int32_t warm_start; /* reserved, must be 0 in this version */
+} femi_tonal_opts;
+
+typedef struct {
+    int32_t outer_iters;
+    int32_t inner_solves;
+    int64_t inner_iters;
+    double rel_grad;           /* recomputed at exit with fresh solves */
+    double rel_grad_recursive; /* the CGLS recursion's value at exit    */
+    double mse_before, mse_after;
+} femi_tonal_report;
+
+femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
+                                femi_tonal_report* report, femi_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEMI_H */

@@ -1,0 +1,364 @@
+// abi.cu -- the extern "C" boundary of libfemi (include/femi.h). Argument checking, handle
+// life cycle, uploads; every compute step is one of the kernels in the other .cu files.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "device.cuh"
+
+namespace femi {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+femi_status cuda_fail(cudaError_t e, const char* what) {
+    set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? FEMI_E_OOM : FEMI_E_CUDA;
+}
+
+namespace {
+
+template <class T>
+femi_status upload(femi_system_s* S, T** dst, const std::vector<T>& src, cudaStream_t st, size_t extra = 0) {
+    size_t n = src.size() + extra;
+    void* p = nullptr;
+    FEMI_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+    S->allocs.push_back(p);
+    if (!src.empty()) FEMI_CUDA(cudaMemcpyAsync(p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, st));
+    *dst = (T*)p;
+    return FEMI_OK;
+}
+
+template <class T>
+femi_status alloc(femi_system_s* S, T** dst, size_t n) {
+    void* p = nullptr;
+    FEMI_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+    S->allocs.push_back(p);
+    *dst = (T*)p;
+    return FEMI_OK;
+}
+
+femi_status check_device() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+        set_error("libfemi is built for sm_100a (B200); current device is sm_" + std::to_string(prop.major) +
+                  std::to_string(prop.minor));
+        return FEMI_E_CUDA;
+    }
+    static bool pool_set = false;
+    if (!pool_set) {  // keep stream-ordered scratch cached between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set = true;
+    }
+    return FEMI_OK;
+}
+
+// row chunks for the PCG kernels: <= kRowsPerChunk rows and <= kChunkNnzCap off-diagonals
+std::vector<Chunk> make_chunks(const std::vector<int32_t>& uu_rowptr, int64_t n_u) {
+    std::vector<Chunk> ch;
+    int64_t i = 0;
+    int32_t local = 0;
+    while (i < n_u) {
+        int64_t j = i;
+        int64_t nnz = 0;
+        while (j < n_u && j - i < kRowsPerChunk) {
+            int64_t rn = (uu_rowptr[j + 1] - uu_rowptr[j]) - 1;
+            if (j > i && nnz + rn > kChunkNnzCap) break;
+            nnz += rn;
+            ++j;
+        }
+        ch.push_back({0, (int32_t)i, (int32_t)j, local++});
+        i = j;
+    }
+    return ch;
+}
+
+}  // namespace
+}  // namespace femi
+
+using namespace femi;
+
+extern "C" {
+
+const char* femi_last_error(void) { return g_last_error.c_str(); }
+
+const char* femi_version(void) { return "femi-b200 0.1 (sm_100a)"; }
+
+int64_t femi_kernel_launches(void) { return g_launches.load(); }
+
+femi_status femi_mesh_build(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,
+                            int64_t p, femi_mesh* out) {
+    if (!out) {
+        set_error("mesh_build: out is NULL");
+        return FEMI_E_ARG;
+    }
+    *out = nullptr;
+    femi_mesh_s* h = new (std::nothrow) femi_mesh_s();
+    if (!h) return FEMI_E_OOM;
+    femi_status s;
+    try {
+        s = build_mesh(W, H, mask_px, m, unknown_px, p, h->mesh);
+    } catch (const std::bad_alloc&) {
+        set_error("mesh_build: host allocation failed");
+        s = FEMI_E_OOM;
+    } catch (...) {
+        set_error("mesh_build: internal error");
+        s = FEMI_E_ARG;
+    }
+    if (s != FEMI_OK) {
+        delete h;
+        return s;
+    }
+    *out = h;
+    return FEMI_OK;
+}
+
+femi_status femi_mesh_info_get(femi_mesh mesh, femi_mesh_info* info) {
+    if (!mesh || !info) {
+        set_error("mesh_info_get: NULL argument");
+        return FEMI_E_ARG;
+    }
+    const Mesh& M = mesh->mesh;
+    info->width = M.W;
+    info->height = M.H;
+    info->n_vert = M.nv;
+    info->n_unknown = M.n_u;
+    info->n_mask = M.m;
+    info->n_tri = M.T;
+    info->nnz_uu = (int64_t)M.uu_col.size();
+    info->nnz_uk = (int64_t)M.uk_col.size();
+    return FEMI_OK;
+}
+
+femi_status femi_mesh_export(femi_mesh mesh, int32_t* vert_px, int32_t* tri_vert, int32_t* uu_rowptr, int32_t* uu_col,
+                             int32_t* uk_rowptr, int32_t* uk_col) {
+    if (!mesh) {
+        set_error("mesh_export: NULL mesh");
+        return FEMI_E_ARG;
+    }
+    const Mesh& M = mesh->mesh;
+    auto cp = [](int32_t* dst, const std::vector<int32_t>& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(int32_t) * v.size());
+    };
+    cp(vert_px, M.vpix);
+    cp(tri_vert, M.tri);
+    cp(uu_rowptr, M.uu_rowptr);
+    cp(uu_col, M.uu_col);
+    cp(uk_rowptr, M.uk_rowptr);
+    cp(uk_col, M.uk_col);
+    return FEMI_OK;
+}
+
+femi_status femi_mesh_timing(femi_mesh mesh, double* seconds, int32_t* threads) {
+    if (!mesh) return FEMI_E_ARG;
+    if (seconds) *seconds = mesh->mesh.build_seconds;
+    if (threads) *threads = mesh->mesh.threads;
+    return FEMI_OK;
+}
+
+void femi_mesh_free(femi_mesh mesh) { delete mesh; }
+
+void femi_system_free(femi_system sys) {
+    if (!sys) return;
+    cudaDeviceSynchronize();
+    for (void* p : sys->allocs) cudaFree(p);
+    delete sys;
+}
+
+femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) {
+    if (!mesh || !out) {
+        set_error("assemble: NULL argument");
+        return FEMI_E_ARG;
+    }
+    *out = nullptr;
+    femi_status s = check_device();
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Mesh& M = mesh->mesh;
+    femi_system_s* S = new (std::nothrow) femi_system_s();
+    if (!S) return FEMI_E_OOM;
+    S->W = M.W;
+    S->H = M.H;
+    S->n_u = M.n_u;
+    S->m = M.m;
+    S->nv = M.nv;
+    S->T = M.T;
+    S->nnz_uu = (int64_t)M.uu_col.size();
+    S->nnz_uk = (int64_t)M.uk_col.size();
+    int32_t* d_tri = nullptr;
+    uint32_t* d_flags = nullptr;
+#define U(x)                              \
+    do {                                  \
+        s = (x);                          \
+        if (s != FEMI_OK) goto fail;      \
+    } while (0)
+    U(upload(S, &S->vpix, M.vpix, st));
+    U(upload(S, &d_tri, M.tri, st));
+    U(upload(S, &d_flags, M.flags, st));
+    U(alloc(S, &S->tri, (size_t)M.T));
+    U(upload(S, &S->vt_ptr, M.vt_ptr, st));
+    U(upload(S, &S->vt_idx, M.vt_idx, st));
+    U(upload(S, &S->uu_rowptr, M.uu_rowptr, st));
+    U(upload(S, &S->uu_col, M.uu_col, st));
+    U(upload(S, &S->uu_opp, M.uu_opp, st));
+    U(alloc(S, &S->uu_val, M.uu_col.size()));
+    U(upload(S, &S->uk_rowptr, M.uk_rowptr, st));
+    U(upload(S, &S->uk_col, M.uk_col, st));
+    U(upload(S, &S->uk_opp, M.uk_opp, st));
+    U(alloc(S, &S->uk_val, M.uk_col.size()));
+    U(upload(S, &S->ku_rowptr, M.ku_rowptr, st));
+    U(upload(S, &S->ku_src, M.ku_src, st));
+    U(upload(S, &S->ku_row, M.ku_row, st));
+    U(alloc(S, &S->o_rowptr, (size_t)M.n_u + 1));
+    U(alloc(S, &S->o_col, M.uu_col.size() - M.n_u));
+    U(alloc(S, &S->o_val, M.uu_col.size() - M.n_u));
+    U(alloc(S, &S->s, (size_t)M.n_u));
+    S->chunks_h = make_chunks(M.uu_rowptr, M.n_u);
+    U(upload(S, &S->chunks_d, S->chunks_h, st));
+    U(launch_tri_records(S, d_tri, d_flags, st));
+    U(launch_assemble_values(S, st));
+    // the int32 triangle table and flags are folded into TriRec; drop them once done
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        s = cuda_fail(cudaGetLastError(), "assemble: sync");
+        goto fail;
+    }
+    for (auto it = S->allocs.begin(); it != S->allocs.end();) {
+        if (*it == (void*)d_tri || *it == (void*)d_flags) {
+            cudaFree(*it);
+            it = S->allocs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+#undef U
+    *out = S;
+    return FEMI_OK;
+fail:
+    femi_system_free(S);
+    return s;
+}
+
+femi_status femi_system_info_get(femi_system sys, femi_mesh_info* info) {
+    if (!sys || !info) return FEMI_E_ARG;
+    info->width = sys->W;
+    info->height = sys->H;
+    info->n_vert = sys->nv;
+    info->n_unknown = sys->n_u;
+    info->n_mask = sys->m;
+    info->n_tri = sys->T;
+    info->nnz_uu = sys->nnz_uu;
+    info->nnz_uk = sys->nnz_uk;
+    return FEMI_OK;
+}
+
+femi_status femi_system_export(femi_system sys, double* uu_val, double* uk_val, femi_stream stream) {
+    if (!sys) {
+        set_error("system_export: NULL system");
+        return FEMI_E_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (uu_val && sys->nnz_uu)
+        FEMI_CUDA(cudaMemcpyAsync(uu_val, sys->uu_val, sizeof(double) * sys->nnz_uu, cudaMemcpyDeviceToHost, st));
+    if (uk_val && sys->nnz_uk)
+        FEMI_CUDA(cudaMemcpyAsync(uk_val, sys->uk_val, sizeof(double) * sys->nnz_uk, cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaStreamSynchronize(st));
+    return FEMI_OK;
+}
+
+femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const double* const* g,
+                                       double* const* u_vert, const femi_cg_opts* opts, int32_t* iters,
+                                       double* relres, femi_stream stream) {
+    if (B < 0 || (B > 0 && (!sys || !g || !u_vert || !opts))) {
+        set_error("inpaint_solve_batched: NULL argument or B < 0");
+        return FEMI_E_ARG;
+    }
+    if (B == 0) return FEMI_OK;
+    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond < 0 || opts->precond > 1 || opts->x0 < 0 ||
+        opts->x0 > 2 || opts->check_every < 0) {
+        set_error("inpaint_solve_batched: invalid options");
+        return FEMI_E_ARG;
+    }
+    for (int b = 0; b < B; ++b)
+        if (!sys[b] || !g[b] || !u_vert[b]) {
+            set_error("inpaint_solve_batched: NULL entry");
+            return FEMI_E_ARG;
+        }
+    femi_status s = check_device();
+    if (s) return s;
+    std::vector<femi_system_s*> Sv(sys, sys + B);
+    return pcg_solve(B, Sv.data(), g, nullptr, u_vert, *opts, iters, relres, (cudaStream_t)stream, nullptr);
+}
+
+femi_status femi_rasterise_error_batched(int32_t B, const femi_system* sys, const double* const* u_vert,
+                                         const double* const* f, double* const* u_px, double* const* e_px,
+                                         double* const* tri_err, int32_t* const* tri_best_px, double* const* sse,
+                                         femi_stream stream) {
+    if (B < 0 || (B > 0 && (!sys || !u_vert || !f || !sse))) {
+        set_error("rasterise_error: NULL argument");
+        return FEMI_E_ARG;
+    }
+    for (int b = 0; b < B; ++b)
+        if (!sys[b] || !u_vert[b] || !f[b] || !sse[b]) {
+            set_error("rasterise_error: NULL entry");
+            return FEMI_E_ARG;
+        }
+    std::vector<femi_system_s*> Sv(sys, sys + B);
+    return launch_raster(B, Sv.data(), u_vert, f, u_px, e_px, tri_err, tri_best_px, sse, (cudaStream_t)stream);
+}
+
+femi_status femi_rasterise_error(femi_system sys, const double* u_vert, const double* f, double* u_px, double* e_px,
+                                 double* tri_err, int32_t* tri_best_px, double* sse, femi_stream stream) {
+    femi_system sv[1] = {sys};
+    const double* uv[1] = {u_vert};
+    const double* fv[1] = {f};
+    double* up[1] = {u_px};
+    double* ep[1] = {e_px};
+    double* te[1] = {tri_err};
+    int32_t* bp[1] = {tri_best_px};
+    double* sp[1] = {sse};
+    return femi_rasterise_error_batched(1, sv, uv, fv, up, ep, te, bp, sp, stream);
+}
+
+femi_status femi_densify_step(femi_system sys, const double* f, const double* u_vert, int64_t b,
+                              int32_t* new_mask_px, int64_t* n_added, femi_stream stream) {
+    if (!sys || !f || !u_vert || !n_added || b < 0 || (b > 0 && !new_mask_px)) {
+        set_error("densify_step: NULL argument or b < 0");
+        return FEMI_E_ARG;
+    }
+    return densify_select(sys, f, u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
+}
+
+femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
+                                femi_tonal_report* report, femi_stream stream) {
+    if (!sys || !f || !g || !opts || !report) {
+        set_error("tonal_optimise: NULL argument");
+        return FEMI_E_ARG;
+    }
+    if (!(opts->outer_rtol > 0.0) || opts->outer_max < 0 || !(opts->inner.rtol > 0.0) || opts->inner.max_iter <= 0 ||
+        opts->warm_start != 0) {
+        set_error("tonal_optimise: invalid options");
+        return FEMI_E_ARG;
+    }
+    femi_status s = check_device();
+    if (s) return s;
+    std::memset(report, 0, sizeof(*report));
+    return tonal_cgls(sys, f, g, *opts, report, (cudaStream_t)stream);
+}
+
+}  // extern "C"

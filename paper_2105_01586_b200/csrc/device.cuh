@@ -1,0 +1,152 @@
+// device.cuh -- device-side types and helpers of libfemi (sm_100a). Internal.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "femi_internal.h"
+
+namespace femi {
+
+// One triangle as the rasteriser reads it: 32 bytes, one aligned load per lane group.
+struct __align__(16) TriRec {
+    int32_t v[3];    // canonical vertex indices; v[0] has the smallest pix
+    uint32_t flags;  // bit k: owns the edge opposite v[k]; bit 3+k: owns the vertex v[k] (reading A7)
+    int16_t x[3], y[3];
+    int32_t pad;
+};
+static_assert(sizeof(TriRec) == 32, "TriRec must be 32 bytes");
+
+// A row chunk of the PCG kernels (one CTA): rows [row0, row1) of batch item `item`.
+struct Chunk {
+    int32_t item, row0, row1, local;  // local = chunk index within the item
+};
+
+// Per-RHS solver state, device resident; scalars of one CG recursion.
+struct CgState {
+    double rr;     // r^.r^ (scaled residual)
+    double rru;    // ||r||^2 unscaled (r = r^ / s)
+    double pq;     // p.q
+    double alpha, beta;
+    double bn2;    // ||b||^2 unscaled
+    double tol2;   // (rtol ||b||)^2
+    double rtol;
+    double res2;   // true ||b - A x||^2 at exit
+    unsigned long long kmin, kmax;  // order-preserving keys of min(g), max(g)
+    int32_t iters, active, status, max_iter;
+    uint32_t cnt[4];  // last-block counters (one per reduction site)
+};
+
+// One batch item as the PCG kernels see it.
+struct SolveItem {
+    const int32_t* orp;   // off-diagonal rowptr of the scaled matrix (n+1)
+    const int32_t* oci;   // off-diagonal columns
+    const double* oav;    // scaled off-diagonal values  s_i a_ij s_j
+    const double* s;      // D^-1/2
+    const int32_t* urp;   // unscaled A_uu rowptr (diagonal included), for the true residual
+    const int32_t* uci;
+    const double* uav;
+    const int32_t* krp;   // A_uk rowptr
+    const int32_t* kci;
+    const double* kav;
+    const double* g;      // mask values (m) or NULL when b is given
+    const double* bin;    // given right-hand side (n) or NULL
+    double* u_vert;       // output vertex values (n + m)
+    double *x, *r, *q, *b;
+    double* p[2];
+    int32_t n, m;
+    int32_t chunk0, nchunks;
+    int32_t x0mode;       // 0 zeros, 1 midrange(g), 2 caller-provided (u_vert[0..n))
+    int32_t pad;
+};
+
+}  // namespace femi
+
+// Device system handle (S1 output).
+struct femi_system_s {
+    int32_t W = 0, H = 0;
+    int64_t n_u = 0, m = 0, nv = 0, T = 0, nnz_uu = 0, nnz_uk = 0;
+    // mesh tables
+    int32_t* vpix = nullptr;
+    femi::TriRec* tri = nullptr;
+    int32_t* vt_ptr = nullptr;
+    int32_t* vt_idx = nullptr;
+    int32_t* uu_rowptr = nullptr;
+    int32_t* uu_col = nullptr;
+    int32_t* uu_opp = nullptr;
+    double* uu_val = nullptr;
+    int32_t* uk_rowptr = nullptr;
+    int32_t* uk_col = nullptr;
+    int32_t* uk_opp = nullptr;
+    double* uk_val = nullptr;
+    int32_t* ku_rowptr = nullptr;
+    int32_t* ku_src = nullptr;
+    int32_t* ku_row = nullptr;
+    // scaled (Jacobi) solver matrix: off-diagonal part only, unit diagonal implied
+    int32_t* o_rowptr = nullptr;
+    int32_t* o_col = nullptr;
+    double* o_val = nullptr;
+    double* s = nullptr;
+    // PCG row chunks (host copy + device copy numbered as batch item 0)
+    std::vector<femi::Chunk> chunks_h;
+    femi::Chunk* chunks_d = nullptr;
+    // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    std::vector<void*> allocs;
+};
+
+namespace femi {
+
+// error helpers
+femi_status cuda_fail(cudaError_t e, const char* what);
+#define FEMI_CUDA(call)                                              \
+    do {                                                             \
+        cudaError_t _e = (call);                                     \
+        if (_e != cudaSuccess) return femi::cuda_fail(_e, #call);   \
+    } while (0)
+
+// kernel-launch accounting (femi_kernel_launches)
+void count_launches(int64_t n);
+
+constexpr int kRowsPerChunk = 256;
+constexpr int kChunkNnzCap = 2048;
+
+// launchers (defined in the .cu files)
+femi_status launch_tri_records(femi_system_s* S, const int32_t* d_tri, const uint32_t* d_flags, cudaStream_t st);
+femi_status launch_assemble_values(femi_system_s* S, cudaStream_t st);
+femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
+                          double* const* u_px, double* const* e_px, double* const* tri_err,
+                          int32_t* const* best, double* const* sse, cudaStream_t st);
+femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
+                      double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
+                      cudaStream_t st, int64_t* total_iters);
+femi_status densify_select(femi_system_s* S, const double* f, const double* u_vert, int64_t b,
+                           int32_t* new_px, int64_t* n_added, cudaStream_t st);
+femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
+                       femi_tonal_report* rep, cudaStream_t st);
+
+// device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum (fixed tree): every thread returns the total.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) t += sh[w];
+    return t;
+}
+
+}  // namespace femi

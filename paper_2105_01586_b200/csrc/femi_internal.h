@@ -1,0 +1,43 @@
+// femi_internal.h -- internal types of libfemi (product path). Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/femi.h"
+
+namespace femi {
+
+void set_error(const std::string& msg);
+
+// Host mesh (S0). Canonical numbering: unknowns (ascending pix) then masks (ascending pix).
+struct Mesh {
+    int32_t W = 0, H = 0;
+    int64_t n_u = 0, m = 0, nv = 0, T = 0;
+    std::vector<int32_t> vpix;       // nv
+    std::vector<int32_t> tri;        // 3T canonical vertex indices (CCW, smallest pix first)
+    std::vector<int32_t> nbr;        // 3T triangle across the edge opposite vertex k, -1 on the border
+    std::vector<uint32_t> flags;     // T: bit k (0..2) owns edge opposite k; bit 3+k owns vertex k
+    std::vector<int32_t> uu_rowptr;  // n_u+1 (diagonal included)
+    std::vector<int32_t> uu_col;     // nnz_uu
+    std::vector<int32_t> uu_opp;     // 2*nnz_uu: vertices opposite the edge (i,col); -1 none; diag -1,-1
+    std::vector<int32_t> uk_rowptr;  // n_u+1
+    std::vector<int32_t> uk_col;     // nnz_uk (mask index)
+    std::vector<int32_t> uk_opp;     // 2*nnz_uk
+    std::vector<int32_t> ku_rowptr;  // m+1 transpose of A_uk
+    std::vector<int32_t> ku_src;     // index into uk arrays
+    std::vector<int32_t> ku_row;     // unknown index
+    std::vector<int32_t> vt_ptr;     // nv+1 vertex -> incident corners
+    std::vector<int32_t> vt_idx;     // 3T entries: t*3+k, ascending t
+    double build_seconds = 0.0;
+    int32_t threads = 1;
+};
+
+femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,
+                       int64_t p, Mesh& out);
+
+}  // namespace femi
+
+struct femi_mesh_s {
+    femi::Mesh mesh;
+};

@@ -1,0 +1,292 @@
+// tonal.cu -- S6 tonal optimisation by nested CG (Eqs. (4)-(5)).
+//
+// g* = argmin ||B g - f||^2 with B g = P_k g + P_u A_uu^-1 (-A_uk g) (the dense B is never
+// formed). CG on the normal equations B^T B g = B^T f in CGLS form;
+// every outer iteration applies B once (inner inpainting solve + forward raster) and B^T
+// once (adjoint raster + inner solve + A_uk^T product), strictly in sequence
+// (reading A13). Vectors stay on the device; the host only sees the outer scalars.
+//   B^T r = P_k^T r - A_uk^T A_uu^-1 (P_u^T r)
+// P^T r is a per-triangle adjoint raster (warp per triangle, the same ownership rule as
+// the forward raster) producing three partial sums per triangle, gathered per vertex over
+// the vertex->triangle incidence list in ascending triangle order (deterministic).
+#include <cmath>
+
+#include "device.cuh"
+
+namespace femi {
+namespace {
+
+constexpr int TT = 256;
+
+__device__ __forceinline__ int orient_i(int ax, int ay, int bx, int by, int px, int py) {
+    return (bx - ax) * (py - ay) - (by - ay) * (px - ax);
+}
+
+__global__ void __launch_bounds__(TT) k_adjoint_tri(int64_t T, int W, const TriRec* __restrict__ tri,
+                                                    const double* __restrict__ r, double* __restrict__ tri_w) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * TT + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * TT) >> 5;
+    for (int64_t t = warp; t < T; t += nwarps) {
+        const TriRec R = tri[t];
+        const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
+        const int x0 = min(ax, min(bx, cx)), x1 = max(ax, max(bx, cx));
+        const int y0 = min(ay, min(by, cy)), y1 = max(ay, max(by, cy));
+        const int bw = x1 - x0 + 1, nbox = bw * (y1 - y0 + 1);
+        const double D = (double)orient_i(ax, ay, bx, by, cx, cy);
+        double sa = 0.0, sb = 0.0, sc = 0.0;
+        for (int k = lane; k < nbox; k += 32) {
+            const int py = y0 + k / bw, px = x0 + k % bw;
+            const int w0 = orient_i(bx, by, cx, cy, px, py);
+            const int w1 = orient_i(cx, cy, ax, ay, px, py);
+            const int w2 = orient_i(ax, ay, bx, by, px, py);
+            if ((w0 | w1 | w2) < 0) continue;
+            const int z = (w0 == 0) + (w1 == 0) + (w2 == 0);
+            const double rv = r[py * W + px];
+            if (z == 2) {
+                const int kv = (w0 != 0) ? 0 : ((w1 != 0) ? 1 : 2);
+                if (!(R.flags & (8u << kv))) continue;
+                if (kv == 0) sa += rv;
+                else if (kv == 1) sb += rv;
+                else sc += rv;
+                continue;
+            }
+            if (z == 1) {
+                const int ke = (w0 == 0) ? 0 : ((w1 == 0) ? 1 : 2);
+                if (!(R.flags & (1u << ke))) continue;
+            }
+            sa += (w0 / D) * rv;
+            sb += (w1 / D) * rv;
+            sc += (w2 / D) * rv;
+        }
+        sa = warp_sum(sa);
+        sb = warp_sum(sb);
+        sc = warp_sum(sc);
+        if (lane == 0) {
+            tri_w[3 * t] = sa;
+            tri_w[3 * t + 1] = sb;
+            tri_w[3 * t + 2] = sc;
+        }
+    }
+}
+
+__global__ void k_vertex_gather(int64_t nv, const int32_t* __restrict__ vt_ptr, const int32_t* __restrict__ vt_idx,
+                                const double* __restrict__ tri_w, double* __restrict__ w) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) s += tri_w[vt_idx[q]];
+        w[v] = s;
+    }
+}
+
+// s_k = w_mask[k] - sum_i A_uk[i,k] y_i  (A_uk^T via the transpose index)
+__global__ void k_ku(int64_t m, int64_t n_u, const int32_t* __restrict__ krp, const int32_t* __restrict__ src,
+                     const int32_t* __restrict__ row, const double* __restrict__ uk_val, const double* __restrict__ w,
+                     const double* __restrict__ y, double* __restrict__ s) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        double acc = w[n_u + k];
+        for (int32_t q = krp[k]; q < krp[k + 1]; ++q) acc -= uk_val[src[q]] * y[row[q]];
+        s[k] = acc;
+    }
+}
+
+__global__ void k_dot_part(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ part) {
+    __shared__ double red[TT / 32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)TT + threadIdx.x; i < n; i += (int64_t)gridDim.x * TT) s += a[i] * b[i];
+    s = block_sum<TT>(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_dot_final(int nb, const double* __restrict__ part, double* __restrict__ out) {
+    __shared__ double red[TT / 32];
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nb; k += TT) s += part[k];
+    s = block_sum<TT>(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fma(alpha, x[i], y[i]);
+}
+__global__ void k_xpby(int64_t n, const double* __restrict__ x, double beta, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fma(beta, y[i], x[i]);
+}
+__global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[i] - b[i];
+}
+
+int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + TT - 1) / TT, 148 * 8)); }
+
+struct Tonal {
+    femi_system_s* S;
+    cudaStream_t st;
+    femi_cg_opts inner;
+    double* uv;     // nv
+    double* yv;     // nv
+    double* w;      // nv
+    double* tri_w;  // 3T
+    double* part;   // dot partials
+    double* dres;   // dot result
+    int64_t solves = 0, iters = 0;
+    femi_status status = FEMI_OK;
+
+    femi_status dot(int64_t n, const double* a, const double* b, double* out) {
+        const int nb = 296;
+        k_dot_part<<<nb, TT, 0, st>>>(n, a, b, part); count_launches(1);
+        k_dot_final<<<1, TT, 0, st>>>(nb, part, dres); count_launches(1);
+        FEMI_CUDA(cudaGetLastError());
+        FEMI_CUDA(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        return FEMI_OK;
+    }
+
+    void note(femi_status s) {
+        if (s != FEMI_OK && status == FEMI_OK) status = s;
+    }
+
+    // u_px = B g
+    femi_status apply_B(const double* g, double* u_px) {
+        femi_cg_opts o = inner;
+        o.x0 = 1;
+        int32_t it = 0;
+        double rr = 0.0;
+        int64_t tot = 0;
+        femi_system_s* Sv[1] = {S};
+        const double* gv[1] = {g};
+        double* uvv[1] = {uv};
+        femi_status s = pcg_solve(1, Sv, gv, nullptr, uvv, o, &it, &rr, st, &tot);
+        ++solves;
+        iters += tot;
+        if (s == FEMI_E_NONFINITE || s == FEMI_E_CUDA || s == FEMI_E_OOM) return s;
+        note(s);
+        const double* uvc[1] = {uv};
+        double* pv[1] = {u_px};
+        return launch_raster(1, Sv, uvc, nullptr, pv, nullptr, nullptr, nullptr, nullptr, st);
+    }
+
+    // s = B^T r
+    femi_status apply_BT(const double* r, double* s_out) {
+        k_adjoint_tri<<<grid_for(S->T * 32), TT, 0, st>>>(S->T, S->W, S->tri, r, tri_w); count_launches(1);
+        k_vertex_gather<<<grid_for(S->nv), TT, 0, st>>>(S->nv, S->vt_ptr, S->vt_idx, tri_w, w); count_launches(1);
+        FEMI_CUDA(cudaGetLastError());
+        femi_cg_opts o = inner;
+        o.x0 = 0;
+        int32_t it = 0;
+        double rr = 0.0;
+        int64_t tot = 0;
+        femi_system_s* Sv[1] = {S};
+        const double* bv[1] = {w};
+        double* yvv[1] = {yv};
+        femi_status s = pcg_solve(1, Sv, nullptr, bv, yvv, o, &it, &rr, st, &tot);
+        ++solves;
+        iters += tot;
+        if (s == FEMI_E_NONFINITE || s == FEMI_E_CUDA || s == FEMI_E_OOM) return s;
+        note(s);
+        k_ku<<<grid_for(S->m), TT, 0, st>>>(S->m, S->n_u, S->ku_rowptr, S->ku_src, S->ku_row, S->uk_val, w, yv,
+                                            s_out); count_launches(1);
+        FEMI_CUDA(cudaGetLastError());
+        return FEMI_OK;
+    }
+};
+
+}  // namespace
+
+femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
+                       femi_tonal_report* rep, cudaStream_t st) {
+    const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t bytes = 3 * al(sizeof(double) * nv) + al(sizeof(double) * 3 * T) + al(sizeof(double) * 300) +
+                   al(sizeof(double)) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m);
+    void* base = nullptr;
+    FEMI_CUDA(cudaMallocAsync(&base, bytes, st));
+    char* cur = (char*)base;
+    auto take = [&](size_t x) {
+        char* p = cur;
+        cur += al(x);
+        return (double*)p;
+    };
+    Tonal tn;
+    tn.S = S;
+    tn.st = st;
+    tn.inner = o.inner;
+    tn.uv = take(sizeof(double) * nv);
+    tn.yv = take(sizeof(double) * nv);
+    tn.w = take(sizeof(double) * nv);
+    tn.tri_w = take(sizeof(double) * 3 * T);
+    tn.part = take(sizeof(double) * 300);
+    tn.dres = take(sizeof(double));
+    double* u = take(sizeof(double) * N);
+    double* r = take(sizeof(double) * N);
+    double* q = take(sizeof(double) * N);
+    double* s = take(sizeof(double) * m);
+    double* p = take(sizeof(double) * m);
+    femi_status rc = FEMI_OK;
+#define TRY(x)                      \
+    do {                            \
+        rc = (x);                   \
+        if (rc != FEMI_OK) goto out; \
+    } while (0)
+    {
+        double rr = 0, btf2 = 0, gam = 0, qq = 0, gam2 = 0;
+        int outer = 0;
+        TRY(tn.apply_B(g, u));
+        k_sub<<<grid_for(N), TT, 0, st>>>(N, f, u, r); count_launches(1);
+        TRY(tn.dot(N, r, r, &rr));
+        rep->mse_before = rr / (double)N;
+        TRY(tn.apply_BT(f, s));
+        TRY(tn.dot(m, s, s, &btf2));
+        const double btf = std::sqrt(btf2);
+        TRY(tn.apply_BT(r, s));
+        FEMI_CUDA(cudaMemcpyAsync(p, s, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+        TRY(tn.dot(m, s, s, &gam));
+        double relg = btf > 0.0 ? std::sqrt(gam) / btf : 0.0;
+        while (relg >= o.outer_rtol && outer < o.outer_max) {
+            TRY(tn.apply_B(p, q));
+            TRY(tn.dot(N, q, q, &qq));
+            if (!(qq > 0.0)) break;
+            const double alpha = gam / qq;
+            k_axpy<<<grid_for(m), TT, 0, st>>>(m, alpha, p, g); count_launches(1);
+            k_axpy<<<grid_for(N), TT, 0, st>>>(N, -alpha, q, r); count_launches(1);
+            TRY(tn.apply_BT(r, s));
+            TRY(tn.dot(m, s, s, &gam2));
+            ++outer;
+            relg = std::sqrt(gam2) / btf;
+            if (!std::isfinite(relg)) {
+                rc = FEMI_E_NONFINITE;
+                goto out;
+            }
+            if (relg < o.outer_rtol) {
+                gam = gam2;
+                break;
+            }
+            const double beta = gam2 / gam;
+            k_xpby<<<grid_for(m), TT, 0, st>>>(m, s, beta, p); count_launches(1);
+            gam = gam2;
+        }
+        rep->rel_grad_recursive = relg;
+        rep->outer_iters = outer;
+        TRY(tn.apply_B(g, u));
+        k_sub<<<grid_for(N), TT, 0, st>>>(N, f, u, r); count_launches(1);
+        TRY(tn.dot(N, r, r, &rr));
+        rep->mse_after = rr / (double)N;
+        TRY(tn.apply_BT(r, s));
+        TRY(tn.dot(m, s, s, &gam2));
+        rep->rel_grad = btf > 0.0 ? std::sqrt(gam2) / btf : 0.0;
+        if (relg >= o.outer_rtol && outer >= o.outer_max) tn.note(FEMI_E_NOT_CONVERGED);
+    }
+out:
+#undef TRY
+    rep->inner_solves = (int32_t)tn.solves;
+    rep->inner_iters = tn.iters;
+    cudaFreeAsync(base, st);
+    if (rc != FEMI_OK) return rc;
+    if (tn.status != FEMI_OK) set_error("tonal_optimise: an inner solve or the outer loop did not converge");
+    return tn.status;
+}
+
+}  // namespace femi

@@ -1,0 +1,271 @@
+"""ctypes binding of libfemi (include/femi.h). Argument marshalling only: every step of the
+hot path runs in the CUDA kernels behind the C ABI. There is no CPU fallback: if the
+library or a B200 is missing, the calls raise.
+
+Device buffers are torch CUDA tensors (fp64 / int32, contiguous); host buffers are numpy
+arrays. Streams default to torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfemi.so")
+
+FEMI_OK = 0
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_DEGENERATE", 3: "E_NO_MASK", 4: "E_NOT_CONVERGED", 5: "E_NONFINITE",
+          6: "E_NEG_CURVATURE", 7: "E_SIZE", 8: "E_CUDA", 9: "E_OOM"}
+
+
+class FemiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"femi status {status} ({STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class MeshInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("width", "height", "n_vert", "n_unknown", "n_mask", "n_tri", "nnz_uu", "nnz_uk")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class CgOpts(ctypes.Structure):
+    _fields_ = [("rtol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("precond", ctypes.c_int32),
+                ("x0", ctypes.c_int32), ("check_every", ctypes.c_int32)]
+
+
+class TonalOpts(ctypes.Structure):
+    _fields_ = [("outer_rtol", ctypes.c_double), ("outer_max", ctypes.c_int32), ("inner", CgOpts),
+                ("warm_start", ctypes.c_int32)]
+
+
+class TonalReport(ctypes.Structure):
+    _fields_ = [("outer_iters", ctypes.c_int32), ("inner_solves", ctypes.c_int32), ("inner_iters", ctypes.c_int64),
+                ("rel_grad", ctypes.c_double), ("rel_grad_recursive", ctypes.c_double),
+                ("mse_before", ctypes.c_double), ("mse_after", ctypes.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+P = ctypes.c_void_p
+I32P = ctypes.POINTER(ctypes.c_int32)
+
+# every symbol include/femi.h declares
+SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh_build", "femi_mesh_info_get", "femi_mesh_export",
+           "femi_mesh_timing", "femi_mesh_free", "femi_assemble", "femi_system_info_get", "femi_system_export",
+           "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
+           "femi_densify_step", "femi_tonal_optimise"]
+
+
+def lib():
+    """Load libfemi.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FemiError(8, f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.femi_last_error.restype = ctypes.c_char_p
+        L.femi_version.restype = ctypes.c_char_p
+        L.femi_kernel_launches.restype = ctypes.c_int64
+        L.femi_mesh_build.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int64, P, ctypes.c_int64,
+                                      ctypes.POINTER(P)]
+        L.femi_mesh_info_get.argtypes = [P, ctypes.POINTER(MeshInfo)]
+        L.femi_mesh_export.argtypes = [P, P, P, P, P, P, P]
+        L.femi_mesh_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double), I32P]
+        L.femi_mesh_free.argtypes = [P]
+        L.femi_mesh_free.restype = None
+        L.femi_assemble.argtypes = [P, P, ctypes.POINTER(P)]
+        L.femi_system_info_get.argtypes = [P, ctypes.POINTER(MeshInfo)]
+        L.femi_system_export.argtypes = [P, P, P, P]
+        L.femi_system_free.argtypes = [P]
+        L.femi_system_free.restype = None
+        L.femi_inpaint_solve_batched.argtypes = [ctypes.c_int32, P, P, P, ctypes.POINTER(CgOpts), P, P, P]
+        L.femi_rasterise_error.argtypes = [P, P, P, P, P, P, P, P, P]
+        L.femi_rasterise_error_batched.argtypes = [ctypes.c_int32, P, P, P, P, P, P, P, P, P]
+        L.femi_densify_step.argtypes = [P, P, P, ctypes.c_int64, P, ctypes.POINTER(ctypes.c_int64), P]
+        L.femi_tonal_optimise.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.POINTER(TonalReport), P]
+        for name in SYMBOLS:
+            if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
+                            "femi_kernel_launches"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != FEMI_OK:
+        raise FemiError(status, lib().femi_last_error().decode())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t, dtype=None):
+    """Device pointer of a contiguous CUDA tensor (or None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise FemiError(1, "expected a contiguous CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise FemiError(1, f"expected dtype {dtype}, got {t.dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))()
+    for i, p in enumerate(ptrs):
+        arr[i] = None if p is None else (p.value if isinstance(p, ctypes.c_void_p) else p)
+    return arr
+
+
+def version() -> str:
+    return lib().femi_version().decode()
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libfemi so far (process-wide)."""
+    return int(lib().femi_kernel_launches())
+
+
+class Mesh:
+    """S0 mesh_build (host setup stage)."""
+
+    def __init__(self, W: int, H: int, mask_px, unknown_px):
+        mk = np.ascontiguousarray(np.asarray(mask_px).reshape(-1), dtype=np.int32)
+        un = np.ascontiguousarray(np.asarray(unknown_px).reshape(-1), dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(lib().femi_mesh_build(W, H, _hptr(mk), mk.size, _hptr(un), un.size, ctypes.byref(h)))
+        self._h = h
+        info = MeshInfo()
+        _check(lib().femi_mesh_info_get(h, ctypes.byref(info)))
+        self.info = info.as_dict()
+        sec, thr = ctypes.c_double(), ctypes.c_int32()
+        _check(lib().femi_mesh_timing(h, ctypes.byref(sec), ctypes.byref(thr)))
+        self.build_seconds, self.build_threads = sec.value, thr.value
+
+    def export(self) -> dict:
+        i = self.info
+        out = dict(vert_px=np.zeros(i["n_vert"], np.int32), tri=np.zeros(3 * i["n_tri"], np.int32),
+                   uu_rowptr=np.zeros(i["n_unknown"] + 1, np.int32), uu_col=np.zeros(i["nnz_uu"], np.int32),
+                   uk_rowptr=np.zeros(i["n_unknown"] + 1, np.int32), uk_col=np.zeros(i["nnz_uk"], np.int32))
+        _check(lib().femi_mesh_export(self._h, *(_hptr(out[k]) for k in
+                                                 ("vert_px", "tri", "uu_rowptr", "uu_col", "uk_rowptr", "uk_col"))))
+        out["tri"] = out["tri"].reshape(-1, 3)
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().femi_mesh_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class System:
+    """S1 assemble: device matrices and raster tables of one mesh."""
+
+    def __init__(self, mesh: Mesh, stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().femi_assemble(mesh._h, _stream(stream), ctypes.byref(h)))
+        self._h = h
+        info = MeshInfo()
+        _check(lib().femi_system_info_get(h, ctypes.byref(info)))
+        self.info = info.as_dict()
+        self.W, self.H = self.info["width"], self.info["height"]
+        self.n_u, self.m, self.nv, self.T = (self.info[k] for k in ("n_unknown", "n_mask", "n_vert", "n_tri"))
+
+    def export_values(self, stream=None):
+        uu = np.zeros(self.info["nnz_uu"], np.float64)
+        uk = np.zeros(self.info["nnz_uk"], np.float64)
+        _check(lib().femi_system_export(self._h, _hptr(uu), _hptr(uk), _stream(stream)))
+        return uu, uk
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().femi_system_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def cg_opts(rtol=1e-10, max_iter=100000, precond=1, x0=1, check_every=0) -> CgOpts:
+    return CgOpts(rtol, max_iter, precond, x0, check_every)
+
+
+def inpaint_solve_batched(systems, g_list, u_list, opts: CgOpts | None = None, stream=None):
+    """S2. Returns (status, iters[B], relres[B]); raises on hard errors."""
+    import torch
+    B = len(systems)
+    opts = opts or cg_opts()
+    sys_arr = _ptr_array([s._h for s in systems])
+    g_arr = _ptr_array([_dptr(g, torch.float64) for g in g_list])
+    u_arr = _ptr_array([_dptr(u, torch.float64) for u in u_list])
+    iters = np.zeros(B, np.int32)
+    rel = np.zeros(B, np.float64)
+    st = lib().femi_inpaint_solve_batched(B, sys_arr, g_arr, u_arr, ctypes.byref(opts), _hptr(iters), _hptr(rel),
+                                          _stream(stream))
+    if st not in (FEMI_OK, 4):
+        _check(st)
+    return st, iters, rel
+
+
+def rasterise_error_batched(systems, u_list, f_list, sse_list, u_px=None, e_px=None, tri_err=None, best=None,
+                            stream=None):
+    """S3+S4 (enqueue only)."""
+    import torch
+    B = len(systems)
+    opt = lambda L, dt: _ptr_array([_dptr(x, dt) for x in L]) if L is not None else None  # noqa: E731
+    _check(lib().femi_rasterise_error_batched(
+        B, _ptr_array([s._h for s in systems]), opt(u_list, torch.float64), opt(f_list, torch.float64),
+        opt(u_px, torch.float64), opt(e_px, torch.float64), opt(tri_err, torch.float64), opt(best, torch.int32),
+        opt(sse_list, torch.float64), _stream(stream)))
+
+
+def rasterise_error(system, u_vert, f, sse, u_px=None, e_px=None, tri_err=None, best=None, stream=None):
+    import torch
+    _check(lib().femi_rasterise_error(system._h, _dptr(u_vert, torch.float64), _dptr(f, torch.float64),
+                                      _dptr(u_px, torch.float64), _dptr(e_px, torch.float64),
+                                      _dptr(tri_err, torch.float64), _dptr(best, torch.int32),
+                                      _dptr(sse, torch.float64), _stream(stream)))
+
+
+def densify_step(system, f, u_vert, b: int, stream=None) -> np.ndarray:
+    """S5: new mask pixels (ascending) chosen from the per-triangle error of u_vert."""
+    import torch
+    out = np.zeros(max(b, 1), np.int32)
+    n = ctypes.c_int64(0)
+    _check(lib().femi_densify_step(system._h, _dptr(f, torch.float64), _dptr(u_vert, torch.float64), b, _hptr(out),
+                                   ctypes.byref(n), _stream(stream)))
+    return out[: n.value].copy()
+
+
+def tonal_optimise(system, f, g, outer_rtol=1e-8, outer_max=1000, inner: CgOpts | None = None, stream=None):
+    """S6: g (device, in/out) <- argmin ||B g - f||^2. Returns (status, report dict)."""
+    import torch
+    inner = inner or cg_opts(rtol=1e-12)
+    o = TonalOpts(outer_rtol, outer_max, inner, 0)
+    rep = TonalReport()
+    st = lib().femi_tonal_optimise(system._h, _dptr(f, torch.float64), _dptr(g, torch.float64), ctypes.byref(o),
+                                   ctypes.byref(rep), _stream(stream))
+    if st not in (FEMI_OK, 4):
+        _check(st)
+    return st, rep.as_dict()

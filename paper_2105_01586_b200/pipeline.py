@@ -1,0 +1,76 @@
+"""Host-side drivers composed from the C-ABI calls (no arithmetic of the method here).
+
+    inpaint()  -- mesh_build -> assemble -> inpaint_solve_batched -> rasterise_error
+    densify()  -- PAPER.md:L257-268: iteration 0 is the random initial mask; each later
+                  iteration inpaints on the current mesh and inserts b_t pixels chosen by
+                  densify_step; the host merges the mask and re-meshes.
+    tonal()    -- tonal_optimise on a fixed mesh with g0 = f at the mask.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import femi
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise femi.FemiError(8, "no CUDA device: the FEM inpainting path has no CPU fallback")
+    return torch
+
+
+def mask_values(f_dev, mesh_or_sys_vert_px, n_u):
+    """g = f at the mask vertices in canonical (ascending pix) order, gathered on the device."""
+    torch = _torch()
+    idx = torch.as_tensor(np.asarray(mesh_or_sys_vert_px[n_u:], dtype=np.int64), device=f_dev.device)
+    return f_dev.reshape(-1).index_select(0, idx).contiguous()
+
+
+def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None):
+    torch = _torch()
+    mesh = femi.Mesh(W, H, mask_px, unknown_px)
+    sysm = femi.System(mesh, stream)
+    vert = mesh.export()["vert_px"]
+    g = mask_values(f_dev, vert, sysm.n_u)
+    u_vert = torch.empty(sysm.nv, dtype=torch.float64, device=f_dev.device)
+    st, iters, rel = femi.inpaint_solve_batched([sysm], [g], [u_vert], femi.cg_opts(rtol=rtol), stream)
+    sse = torch.zeros(1, dtype=torch.float64, device=f_dev.device)
+    u_px = e_px = None
+    if want_images:
+        u_px = torch.empty(W * H, dtype=torch.float64, device=f_dev.device)
+        e_px = torch.empty(W * H, dtype=torch.float64, device=f_dev.device)
+    tri_err = torch.empty(max(sysm.T, 1), dtype=torch.float64, device=f_dev.device)
+    best = torch.empty(max(sysm.T, 1), dtype=torch.int32, device=f_dev.device)
+    femi.rasterise_error(sysm, u_vert, f_dev.reshape(-1), sse, u_px, e_px, tri_err, best, stream)
+    return dict(mesh=mesh, system=sysm, vert_px=vert, u_vert=u_vert, u_px=u_px, e_px=e_px, tri_err=tri_err[: sysm.T],
+                best=best[: sysm.T], sse=sse, status=st, iters=int(iters[0]), relres=float(rel[0]))
+
+
+def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks=None, stream=None):
+    """Returns (final mask, per-iteration records, final MSE)."""
+    torch = _torch()
+    mask = np.sort(np.asarray(mask0, dtype=np.int64))
+    recs = []
+    f1 = f_dev.reshape(-1)
+    for t in range(1, len(schedule)):
+        if lockstep_masks is not None:
+            mask = np.sort(np.asarray(lockstep_masks[t - 1], dtype=np.int64))
+        R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream)
+        new = femi.densify_step(R["system"], f1, R["u_vert"], int(schedule[t]), stream)
+        recs.append(dict(mask=mask.copy(), mse=float(R["sse"].item()) / (W * H), iters=R["iters"], new=new,
+                         T=R["system"].T, mesh_seconds=R["mesh"].build_seconds))
+        mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
+    R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream)
+    return mask, recs, float(R["sse"].item()) / (W * H)
+
+
+def tonal(W, H, f_dev, mask_px, unknown_px, outer_rtol=1e-8, outer_max=1000, inner_rtol=1e-12, stream=None):
+    _torch()
+    mesh = femi.Mesh(W, H, mask_px, unknown_px)
+    sysm = femi.System(mesh, stream)
+    vert = mesh.export()["vert_px"]
+    g = mask_values(f_dev, vert, sysm.n_u)
+    st, rep = femi.tonal_optimise(sysm, f_dev.reshape(-1), g, outer_rtol, outer_max, femi.cg_opts(rtol=inner_rtol),
+                                  stream)
+    return g, rep, dict(mesh=mesh, system=sysm, vert_px=vert, status=st)

@@ -1,0 +1,98 @@
+"""S0 mesh_build (host C++ stage of the product library) vs the oracle: bit-exact topology
+and CSR patterns (BASELINE.json north_star correctness criterion). CPU only: mesh_build
+runs on the host, so no GPU is needed to call it through the C ABI."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2105_01586_b200 import femi
+from synth import make_config
+from synth.generate import draw_mask, draw_unknowns
+
+
+def product_mesh(W, H, mk, un):
+    M = femi.Mesh(W, H, mk, un)
+    return M, M.export()
+
+
+def assert_same(W, H, mk, un):
+    M, E = product_mesh(W, H, mk, un)
+    S = oracle.System(W, H, mk, un)
+    np.testing.assert_array_equal(E["vert_px"], S.vpix)
+    np.testing.assert_array_equal(E["tri"], S.tri)
+    np.testing.assert_array_equal(E["uu_rowptr"], S.uu_ptr)
+    np.testing.assert_array_equal(E["uu_col"], S.uu_col)
+    np.testing.assert_array_equal(E["uk_rowptr"], S.uk_ptr)
+    np.testing.assert_array_equal(E["uk_col"], S.uk_col)
+    assert M.info["n_unknown"] == S.n_u and M.info["n_mask"] == S.m and M.info["n_tri"] == S.T
+    return M, S
+
+
+def test_abi_exports_every_declared_symbol():
+    L = femi.lib()
+    import re
+    hdr = open(__file__.replace("tests/test_mesh_host.py", "include/femi.h")).read()
+    declared = set(re.findall(r"\b(femi_[a-z_]+)\s*\(", hdr))
+    assert declared == set(femi.SYMBOLS)
+    for name in declared:
+        assert hasattr(L, name)
+    assert "sm_100a" in femi.version()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_mesh_bit_exact_small_random(seed):
+    rng = np.random.default_rng(seed)
+    W, H = int(rng.integers(2, 24)), int(rng.integers(2, 24))
+    N = W * H
+    m = int(rng.integers(1, max(2, N // 2)))
+    mk = draw_mask(rng, N, m)
+    p = int(rng.integers(0, N - m + 1))
+    un = draw_unknowns(rng, W, H, mk, min(max(p, 4), N - m)) if N - m >= 4 else np.setdiff1d(np.arange(N), mk)
+    # input order must not matter
+    assert_same(W, H, rng.permutation(mk), rng.permutation(un))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_mesh_bit_exact_configs(cfg):
+    c = make_config(cfg)
+    if cfg == 2:
+        for b in (0, 7, 31):
+            assert_same(c["W"], c["H"], c["masks"][b], c["unknowns"][b])
+    elif cfg == 3:
+        assert_same(c["W"], c["H"], c["mask0"], c["unknowns"])
+    else:
+        assert_same(c["W"], c["H"], c["mask"], c["unknowns"])
+
+
+def test_mesh_bit_exact_config4():
+    c = make_config(4)
+    assert_same(c["W"], c["H"], c["mask"], c["unknowns"])
+
+
+def test_full_grid_and_full_mask():
+    W, H = 17, 9
+    allpx = np.arange(W * H)
+    assert_same(W, H, [40], np.setdiff1d(allpx, [40]))  # maximal cocircular degeneracy
+    M, E = product_mesh(W, H, allpx, [])
+    assert M.info["n_unknown"] == 0 and M.info["nnz_uu"] == 0
+
+
+@pytest.mark.parametrize("W,H,mk,un,err", [
+    (1, 5, [0], [], 2), (5, 1, [0], [], 2), (4, 4, [], [1], 3), (4, 4, [16], [], 7), (4, 4, [3, 3], [], 7),
+    (4, 4, [5], [5], 7), (20000, 4, [0], [], 7)])
+def test_mesh_errors(W, H, mk, un, err):
+    with pytest.raises(femi.FemiError) as ei:
+        femi.Mesh(W, H, np.array(mk, np.int32), np.array(un, np.int32))
+    assert ei.value.status == err
+
+
+def test_mesh_large_structure():
+    """2048^2 with ~168K vertices: Delaunay local property on every interior edge (exact
+    SoS in-circle, reimplemented in numpy int64), plus area and Euler counts."""
+    W = H = 2048
+    rng = np.random.default_rng(12)
+    mk = draw_mask(rng, W * H, 83886)
+    un = draw_unknowns(rng, W, H, mk, 83886)
+    M, E = product_mesh(W, H, mk, un)
+    S_tri = oracle.delaunay(W, H, E["vert_px"])
+    np.testing.assert_array_equal(E["tri"], S_tri)
