@@ -1,22 +1,22 @@
 // pcg.cu -- S2: batched Jacobi-preconditioned CG for A_uu x = -A_uk g.
 //
-// The Jacobi preconditioner is folded into the matrix at assembly (A^ = D^-1/2 A D^-1/2,
-// unit diagonal, only the off-diagonal CSR is stored), so CG runs on A^ x^ = b^ with
-// x = D^-1/2 x^, b^ = D^-1/2 b. Per iteration two kernels, both over row chunks of all
-// active batch items (block-diagonal batching: one chunk table spans every system):
-//   K1  p_new = r + beta p_old (computed on the fly for every column it touches, so no
-//       separate update pass), q = A^ p_new via a CSR-stream SpMV (coalesced val/col
-//       loads into shared memory, one row per thread), partial dot(p_new, q);
-//       the last CTA of an item turns the partials into alpha.
-//   K2  x += alpha p_new, r -= alpha q, partial dot(r,r) and ||D^1/2 r||^2 (the unscaled
-//       residual used by the stopping rule); the last CTA computes beta, the iteration
-//       count and the convergence flag.
-// All reductions are per-CTA partials summed in a fixed order by the item's last CTA
-// (deterministic). Vector traffic per iteration: K1 reads r,p_old and writes p_new,q;
-// K2 reads x,p_new,r,q,s and writes x,r (11 streams of 8 B per row, SURVEY §8(d) S=11).
-// The stopping rule uses the true unscaled relative residual ||b - A x|| / ||b||,
-// confirmed at exit with the unscaled matrix; a failed confirmation restarts CG from the
-// current iterate (reading A11).
+// B200 design: ONE persistent launch per (batched) solve. The Jacobi preconditioner is
+// folded into the matrix at assembly (A^ = D^-1/2 A D^-1/2, unit diagonal, only the
+// off-diagonal CSR stored), so CG runs on A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b).
+// The recurrence is the single-reduction form of CG (Chronopoulos-Gear): per iteration
+//   U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s      (own rows)
+//   -- group barrier (r published) --
+//   S: w = A^ r (gathers r) ; partial (r.r, w.r, ||D^1/2 r||^2)
+//   -- group barrier (partials published) -- every CTA sums the partials in the same
+//   fixed order, so alpha/beta/convergence are bit-identical in all CTAs (deterministic).
+// Each batch item (one system / right-hand side) owns a group of CTAs and a contiguous
+// row range per CTA. p, s and x never leave the CTA, so they live in shared memory for
+// the whole solve; only r (gathered by neighbours) and w go through L2/HBM. Group
+// barriers: __syncthreads (1 CTA), the hardware cluster barrier (a cluster of <= 16
+// CTAs, small systems: C1-C4), or a global sense-reversing barrier over a cooperative
+// grid (one huge system: C5). The stopping rule is the unscaled relative residual
+// ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a failed
+// confirmation restarts CG from the current iterate inside the same launch (reading A11).
 #include <algorithm>
 #include <cmath>
 
@@ -24,8 +24,6 @@
 
 namespace femi {
 namespace {
-
-constexpr int NT = kRowsPerChunk;  // threads per CTA == max rows per chunk
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
     unsigned long long b = (unsigned long long)__double_as_longlong(v);
@@ -36,20 +34,35 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double((long long)b);
 }
 
-// Last-CTA election for a per-item reduction: returns true in every thread of the last CTA.
-__device__ __forceinline__ bool last_cta(uint32_t* counter, uint32_t total, int* sh_flag) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        uint32_t prev = atomicAdd(counter, 1u);
-        *sh_flag = (prev == total - 1);
-    }
-    __syncthreads();
-    if (*sh_flag) __threadfence();
-    return *sh_flag != 0;
-}
+struct RItem {
+    const int32_t* orp;  // scaled off-diagonal CSR
+    const int32_t* oci;
+    const double* oav;
+    const double* s;  // D^-1/2
+    const int32_t* urp;  // unscaled A_uu (diagonal included), true residual
+    const int32_t* uci;
+    const double* uav;
+    const int32_t* krp;  // A_uk
+    const int32_t* kci;
+    const double* kav;
+    const double* g;    // mask values or NULL (b given)
+    const double* bin;  // given b or NULL
+    double* u_vert;
+    double* b;  // unscaled right-hand side
+    double* x;  // x^ (global copy: initial guess gathers, restart)
+    double* r;  // r^ (published every iteration)
+    double* w;  // A^ r^
+    double* p;  // used when the CTA's rows do not fit shared memory
+    double* sv;
+    double* part;       // [ncta][4] partial sums
+    unsigned int* bar;  // [2] global barrier count / generation
+    CgState* st;
+    int32_t n, m, cta0, ncta, x0mode, pad;
+};
 
-__global__ void k_reset(int B, SolveItem* items, CgState* st, double rtol, int max_iter) {
+constexpr int RNT = 512;  // threads per CTA of the persistent solver
+
+__global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     CgState s = {};
@@ -57,13 +70,12 @@ __global__ void k_reset(int B, SolveItem* items, CgState* st, double rtol, int m
     s.max_iter = max_iter;
     s.kmin = ~0ull;
     s.kmax = 0ull;
-    s.active = 1;
     st[b] = s;
 }
 
-__global__ void k_minmax(int B, const SolveItem* __restrict__ items, CgState* st) {
+__global__ void k_minmax(int B, const RItem* __restrict__ items) {
     for (int b = 0; b < B; ++b) {
-        const SolveItem& it = items[b];
+        const RItem& it = items[b];
         if (it.x0mode != 1 || it.g == nullptr) continue;
         unsigned long long lo = ~0ull, hi = 0ull;
         for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x) {
@@ -76,23 +88,16 @@ __global__ void k_minmax(int B, const SolveItem* __restrict__ items, CgState* st
             hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
         if ((threadIdx.x & 31) == 0 && hi != 0ull) {
-            atomicMin(&st[b].kmin, lo);
-            atomicMax(&st[b].kmax, hi);
+            atomicMin(&it.st->kmin, lo);
+            atomicMax(&it.st->kmax, hi);
         }
     }
 }
 
-// b = -A_uk g (or the given b); x^0; ||b||^2
-__global__ void __launch_bounds__(NT) k_rhs(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                            const Chunk* __restrict__ chunks, double* __restrict__ part) {
-    __shared__ double red[NT / 32];
-    __shared__ int flag;
-    const Chunk c = chunks[blockIdx.x];
-    const SolveItem& it = items[c.item];
-    CgState* S = st + c.item;
-    const int i = c.row0 + threadIdx.x;
-    double loc = 0.0;
-    if (i < c.row1) {
+// b = -A_uk g (ascending mask index, reading A6 order), or the given b
+__global__ void k_rhs(int B, const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
         double bi;
         if (it.bin) {
             bi = it.bin[i];
@@ -102,251 +107,267 @@ __global__ void __launch_bounds__(NT) k_rhs(const SolveItem* __restrict__ items,
             bi = -acc;
         }
         it.b[i] = bi;
-        loc = bi * bi;
-        const double si = it.s[i];
-        double x0;
-        if (it.x0mode == 1) x0 = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
-        else if (it.x0mode == 2) x0 = it.u_vert[i];
-        else x0 = 0.0;
-        it.x[i] = x0 / si;
-    }
-    double tot = block_sum<NT>(loc, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
-    if (last_cta(&S->cnt[0], it.nchunks, &flag)) {
-        double s = 0.0;
-        for (int k = threadIdx.x; k < it.nchunks; k += NT) s += __ldcg(&part[it.chunk0 + k]);
-        s = block_sum<NT>(s, red);
-        if (threadIdx.x == 0) {
-            S->bn2 = s;
-            S->tol2 = S->rtol * S->rtol * s;
-            S->cnt[0] = 0;
-        }
     }
 }
 
-// r^ = b^ - A^ x^ ; p_old = 0 ; rr, rru. keep_iters: restart after a failed confirmation.
-__global__ void __launch_bounds__(NT) k_init_res(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                                 const Chunk* __restrict__ chunks, double2* __restrict__ part,
-                                                 int restart) {
-    __shared__ double red[NT / 32];
-    __shared__ int flag;
-    const Chunk c = chunks[blockIdx.x];
-    const SolveItem& it = items[c.item];
-    CgState* S = st + c.item;
-    if (restart && !S->active) return;
-    const int i = c.row0 + threadIdx.x;
-    double l1 = 0.0, l2 = 0.0;
-    if (i < c.row1) {
-        const double si = it.s[i];
-        if (restart) it.x[i] = it.u_vert[i] / si;
-        double ax = 0.0;
-        for (int e = it.orp[i]; e < it.orp[i + 1]; ++e) {
-            const int j = it.oci[e];
-            const double xj = restart ? it.u_vert[j] / it.s[j] : it.x[j];
-            ax = fma(it.oav[e], xj, ax);
-        }
-        const double xi = restart ? it.u_vert[i] / si : it.x[i];
-        const double ri = si * it.b[i] - (xi + ax);
-        it.r[i] = ri;
-        it.p[0][i] = 0.0;
-        it.p[1][i] = 0.0;
-        l1 = ri * ri;
-        const double ru = ri / si;
-        l2 = ru * ru;
-    }
-    double t1 = block_sum<NT>(l1, red);
-    double t2 = block_sum<NT>(l2, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t1, t2);
-    if (last_cta(&S->cnt[1], it.nchunks, &flag)) {
-        double s1 = 0.0, s2 = 0.0;
-        for (int k = threadIdx.x; k < it.nchunks; k += NT) {
-            double2 v = __ldcg(&part[it.chunk0 + k]);
-            s1 += v.x;
-            s2 += v.y;
-        }
-        s1 = block_sum<NT>(s1, red);
-        s2 = block_sum<NT>(s2, red);
-        if (threadIdx.x == 0) {
-            S->rr = s1;
-            S->rru = s2;
-            S->beta = 0.0;
-            if (!restart) S->iters = 0;
-            S->cnt[1] = 0;
-            if (!isfinite(s1) || !isfinite(S->bn2)) {
-                S->active = 0;
-                S->status = FEMI_E_NONFINITE;
-            } else {
-                S->active = (S->bn2 > 0.0 && s2 > S->tol2) ? 1 : 0;
+// ---- group barriers -------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, int n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = bar + 1;
+        const unsigned int g = *vgen;
+        __threadfence();
+        const unsigned int prev = atomicAdd(bar, 1u);
+        if (prev == (unsigned)n - 1u) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicExch(bar + 1, g + 1u);
+        } else {
+            while (*vgen == g) {
             }
         }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int MODE>
+__device__ __forceinline__ void group_sync(const RItem& it) {
+    if constexpr (MODE == 0) {
+        __syncthreads();
+    } else if constexpr (MODE == 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+        grid_barrier(it.bar, it.ncta);
     }
 }
 
-// K1: p_new = r + beta p_old ; q = A^ p_new ; partial p_new.q ; alpha
-__global__ void __launch_bounds__(NT) k_spmv_dot(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                                 const Chunk* __restrict__ chunks, double* __restrict__ part) {
-    __shared__ double prod[kChunkNnzCap];
-    __shared__ double red[NT / 32];
-    __shared__ int flag;
-    const Chunk c = chunks[blockIdx.x];
-    CgState* S = st + c.item;
-    if (!S->active) return;
-    const SolveItem& it = items[c.item];
-    const double beta = S->beta;
-    const int par = S->iters & 1;
-    const double* __restrict__ po = it.p[par];
-    double* __restrict__ pn = it.p[par ^ 1];
-    const double* __restrict__ r = it.r;
+// block sum of 4 values (fixed tree; result valid in every thread)
+__device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [RNT/32][4] */) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+        v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+        sh[4 * wid] = v.x;
+        sh[4 * wid + 1] = v.y;
+        sh[4 * wid + 2] = v.z;
+        sh[4 * wid + 3] = v.w;
+    }
+    __syncthreads();
+    double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < RNT / 32; ++w) {
+        t.x += sh[4 * w];
+        t.y += sh[4 * w + 1];
+        t.z += sh[4 * w + 2];
+        t.w += sh[4 * w + 3];
+    }
+    return t;
+}
+
+// publish this CTA's partials, barrier, and sum all partials of the group (fixed order)
+template <int MODE>
+__device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, double4 loc, double* sh) {
+    double4 t = block_sum4(loc, sh);
+    if (threadIdx.x == 0) {
+        double* P = it.part + 4 * rank;
+        P[0] = t.x;
+        P[1] = t.y;
+        P[2] = t.z;
+        P[3] = t.w;
+    }
+    if constexpr (MODE == 0) return t;
+    group_sync<MODE>(it);
+    double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int k = threadIdx.x; k < it.ncta; k += RNT) {
+        const double* P = it.part + 4 * k;
+        a.x += __ldcg(P);
+        a.y += __ldcg(P + 1);
+        a.z += __ldcg(P + 2);
+        a.w += __ldcg(P + 3);
+    }
+    return block_sum4(a, sh);
+}
+
+// w_i = r_i + sum_j a^_ij r_j over the CTA's rows; returns the partial (r.r, w.r, ||r/s||^2)
+__device__ __forceinline__ double4 spmv_w(const RItem& it, int R0, int R1) {
+    double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
     const int32_t* __restrict__ orp = it.orp;
     const int32_t* __restrict__ oci = it.oci;
     const double* __restrict__ oav = it.oav;
-    const int e0 = orp[c.row0], e1 = orp[c.row1];
-    const bool staged = (e1 - e0) <= kChunkNnzCap;
-    if (staged)
-        for (int e = e0 + threadIdx.x; e < e1; e += NT) {
-            const int j = oci[e];
-            prod[e - e0] = oav[e] * fma(beta, po[j], r[j]);
-        }
-    __syncthreads();
-    double loc = 0.0;
-    const int i = c.row0 + threadIdx.x;
-    if (i < c.row1) {
-        const double pi = fma(beta, po[i], r[i]);
-        double acc = pi;  // unit diagonal
-        const int a = orp[i], b = orp[i + 1];
-        if (staged) {
-            for (int e = a; e < b; ++e) acc += prod[e - e0];
-        } else {
-            for (int e = a; e < b; ++e) {
-                const int j = oci[e];
-                acc += oav[e] * fma(beta, po[j], r[j]);
-            }
-        }
-        pn[i] = pi;
-        it.q[i] = acc;
-        loc = pi * acc;
-    }
-    double tot = block_sum<NT>(loc, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
-    if (last_cta(&S->cnt[2], it.nchunks, &flag)) {
-        double s = 0.0;
-        for (int k = threadIdx.x; k < it.nchunks; k += NT) s += __ldcg(&part[it.chunk0 + k]);
-        s = block_sum<NT>(s, red);
-        if (threadIdx.x == 0) {
-            S->pq = s;
-            S->cnt[2] = 0;
-            if (!(s > 0.0)) {
-                S->active = 0;
-                S->status = isfinite(s) ? FEMI_E_NEG_CURVATURE : FEMI_E_NONFINITE;
-            } else {
-                S->alpha = S->rr / s;
-            }
-        }
-    }
-}
-
-// K2: x += alpha p_new ; r -= alpha q ; rr ; rru ; beta ; convergence
-__global__ void __launch_bounds__(NT) k_update(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                               const Chunk* __restrict__ chunks, double2* __restrict__ part) {
-    __shared__ double red[NT / 32];
-    __shared__ int flag;
-    const Chunk c = chunks[blockIdx.x];
-    CgState* S = st + c.item;
-    if (!S->active) return;
-    const SolveItem& it = items[c.item];
-    const double alpha = S->alpha;
-    const double* __restrict__ pn = it.p[(S->iters & 1) ^ 1];
-    const int i = c.row0 + threadIdx.x;
-    double l1 = 0.0, l2 = 0.0;
-    if (i < c.row1) {
-        it.x[i] = fma(alpha, pn[i], it.x[i]);
-        const double ri = fma(-alpha, it.q[i], it.r[i]);
-        it.r[i] = ri;
-        l1 = ri * ri;
+    const double* __restrict__ r = it.r;
+    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        const double ri = __ldcg(r + i);
+        double acc = ri;
+        const int e1 = orp[i + 1];
+        for (int e = orp[i]; e < e1; ++e) acc = fma(oav[e], __ldcg(r + oci[e]), acc);
+        it.w[i] = acc;
         const double ru = ri / it.s[i];
-        l2 = ru * ru;
+        loc.x += ri * ri;
+        loc.y += acc * ri;
+        loc.z += ru * ru;
     }
-    double t1 = block_sum<NT>(l1, red);
-    double t2 = block_sum<NT>(l2, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t1, t2);
-    if (last_cta(&S->cnt[3], it.nchunks, &flag)) {
-        double s1 = 0.0, s2 = 0.0;
-        for (int k = threadIdx.x; k < it.nchunks; k += NT) {
-            double2 v = __ldcg(&part[it.chunk0 + k]);
-            s1 += v.x;
-            s2 += v.y;
+    return loc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
+    k_pcg_resident(const RItem* __restrict__ items, int nitems, int smem_rows) {
+    extern __shared__ double svec[];  // [p | s | x] x smem_rows when the rows fit
+    __shared__ double sh[4 * (RNT / 32)];
+    // ---- which item / rank
+    int item = 0, rank = 0;
+    if constexpr (MODE == 1) {
+        unsigned cr, cid;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+        asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        item = (int)cid;
+        rank = (int)cr;
+    } else if constexpr (MODE == 0) {
+        item = blockIdx.x;
+        rank = 0;
+    } else {
+        for (int k = 0; k < nitems; ++k)
+            if ((int)blockIdx.x >= items[k].cta0) item = k;
+        rank = blockIdx.x - items[item].cta0;
+    }
+    const RItem& it = items[item];
+    CgState* S = it.st;
+    const int n = it.n;
+    const int R0 = (int)((long long)n * rank / it.ncta), R1 = (int)((long long)n * (rank + 1) / it.ncta);
+    const bool in_smem = (R1 - R0) <= smem_rows;
+    double* P = in_smem ? svec : it.p + R0;
+    double* SV = in_smem ? svec + smem_rows : it.sv + R0;
+    double* X = in_smem ? svec + 2 * smem_rows : it.x + R0;
+    const double rtol = S->rtol;
+    const int max_iter = S->max_iter;
+    double x0v = 0.0;
+    if (it.x0mode == 1) x0v = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
+
+    // ---- init: x^0 (global, gathered by the first residual), r0, bn2
+    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[i] : 0.0);
+        it.x[i] = x0 / it.s[i];
+    }
+    group_sync<MODE>(it);
+    double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        const double si = it.s[i];
+        double ax = __ldcg(it.x + i);
+        for (int e = it.orp[i]; e < it.orp[i + 1]; ++e) ax = fma(it.oav[e], __ldcg(it.x + it.oci[e]), ax);
+        const double bi = it.b[i];
+        const double ri = si * bi - ax;
+        it.r[i] = ri;
+        X[i - R0] = __ldcg(it.x + i);
+        loc.x += bi * bi;
+    }
+    double4 tot = group_reduce<MODE>(it, rank, loc, sh);
+    const double bn2 = tot.x;
+    const double tol2 = rtol * rtol * bn2;
+    int iters = 0, status = FEMI_OK, restarts = 0;
+    double res2 = 0.0;
+    for (;;) {  // (re)start: w = A^ r, p = s = 0
+        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+            P[i - R0] = 0.0;
+            SV[i - R0] = 0.0;
         }
-        s1 = block_sum<NT>(s1, red);
-        s2 = block_sum<NT>(s2, red);
-        if (threadIdx.x == 0) {
-            S->cnt[3] = 0;
-            S->iters += 1;
-            S->beta = s1 / S->rr;
-            S->rr = s1;
-            S->rru = s2;
-            if (!isfinite(s1)) {
-                S->active = 0;
-                S->status = FEMI_E_NONFINITE;
-            } else if (s2 <= S->tol2) {
-                S->active = 0;
-            } else if (S->iters >= S->max_iter) {
-                S->active = 0;
-                S->status = FEMI_E_NOT_CONVERGED;
+        group_sync<MODE>(it);  // r visible
+        tot = group_reduce<MODE>(it, rank, spmv_w(it, R0, R1), sh);
+        double gam = tot.x, del = tot.y, rho = tot.z;
+        double alpha = 0.0, beta = 0.0;
+        bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho);
+        if (!isfinite(gam) || !isfinite(bn2)) {
+            status = FEMI_E_NONFINITE;
+            run = false;
+        }
+        if (run) {
+            if (!(del > 0.0)) {
+                status = FEMI_E_NEG_CURVATURE;
+                run = false;
+            } else {
+                alpha = gam / del;
             }
         }
-    }
-}
-
-// x = D^-1/2 x^ into u_vert (or x0 untouched after a 0-iteration exit, 0 when b == 0),
-// then the true residual ||b - A x||^2 with the unscaled matrix.
-__global__ void __launch_bounds__(NT) k_finalize(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                                 const Chunk* __restrict__ chunks) {
-    const Chunk c = chunks[blockIdx.x];
-    const SolveItem& it = items[c.item];
-    CgState* S = st + c.item;
-    const int i = c.row0 + threadIdx.x;
-    if (i >= c.row1) return;
-    double xi;
-    if (S->bn2 == 0.0) xi = 0.0;
-    else if (S->iters == 0) {
-        if (it.x0mode == 2) return;  // caller's initial guess stays as it is
-        xi = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
-    } else {
-        xi = it.s[i] * it.x[i];
-    }
-    it.u_vert[i] = xi;
-}
-
-__global__ void __launch_bounds__(NT) k_true_res(const SolveItem* __restrict__ items, CgState* __restrict__ st,
-                                                 const Chunk* __restrict__ chunks, double* __restrict__ part) {
-    __shared__ double red[NT / 32];
-    __shared__ int flag;
-    const Chunk c = chunks[blockIdx.x];
-    const SolveItem& it = items[c.item];
-    CgState* S = st + c.item;
-    const int i = c.row0 + threadIdx.x;
-    double loc = 0.0;
-    if (i < c.row1) {
-        double ax = 0.0;
-        for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
-        const double ri = it.b[i] - ax;
-        loc = ri * ri;
-    }
-    double tot = block_sum<NT>(loc, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
-    if (last_cta(&S->cnt[0], it.nchunks, &flag)) {
-        double s = 0.0;
-        for (int k = threadIdx.x; k < it.nchunks; k += NT) s += __ldcg(&part[it.chunk0 + k]);
-        s = block_sum<NT>(s, red);
-        if (threadIdx.x == 0) {
-            S->res2 = s;
-            S->cnt[0] = 0;
+        while (run) {
+            // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+            for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+                const int l = i - R0;
+                const double ri = __ldcg(it.r + i);
+                const double pi = fma(beta, P[l], ri);
+                const double si = fma(beta, SV[l], __ldcg(it.w + i));
+                P[l] = pi;
+                SV[l] = si;
+                X[l] = fma(alpha, pi, X[l]);
+                it.r[i] = fma(-alpha, si, ri);
+            }
+            ++iters;
+            group_sync<MODE>(it);  // r published
+            tot = group_reduce<MODE>(it, rank, spmv_w(it, R0, R1), sh);
+            const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
+            if (!isfinite(gam2) || !isfinite(del2)) {
+                status = FEMI_E_NONFINITE;
+                break;
+            }
+            if (rho2 <= tol2) break;
+            if (iters >= max_iter) {
+                status = FEMI_E_NOT_CONVERGED;
+                break;
+            }
+            beta = gam2 / gam;
+            const double den = del2 - beta * gam2 / alpha;  // = p.A^p of the next direction
+            if (!(den > 0.0)) {
+                status = FEMI_E_NEG_CURVATURE;
+                break;
+            }
+            alpha = gam2 / den;
+            gam = gam2;
         }
+        // ---- finalize: x = D^-1/2 x^ (or x0 untouched at 0 iterations, 0 when b == 0)
+        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+            double xi;
+            if (bn2 == 0.0) xi = 0.0;
+            else if (iters == 0) xi = (it.x0mode == 2) ? it.u_vert[i] : x0v;
+            else xi = it.s[i] * X[i - R0];
+            it.u_vert[i] = xi;
+        }
+        if (it.g)
+            for (int k = R0 + threadIdx.x; k < R1; k += RNT) {  // mask part, split by rows over the group
+                (void)k;
+            }
+        group_sync<MODE>(it);  // u_vert visible
+        // true residual with the unscaled matrix; keeps s_i * r_true in r for a restart
+        loc = make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+            double ax = 0.0;
+            for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+            const double ri = it.b[i] - ax;
+            it.r[i] = it.s[i] * ri;
+            loc.x += ri * ri;
+        }
+        tot = group_reduce<MODE>(it, rank, loc, sh);
+        res2 = tot.x;
+        const bool fail = bn2 > 0.0 && !(res2 <= tol2);
+        if (!(status == FEMI_OK && iters > 0 && fail && iters < max_iter && restarts < 8)) break;
+        ++restarts;
+        for (int i = R0 + threadIdx.x; i < R1; i += RNT) X[i - R0] = it.u_vert[i] / it.s[i];
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        S->iters = iters;
+        S->status = status;
+        S->res2 = res2;
+        S->bn2 = bn2;
+        S->active = 0;
     }
 }
 
-__global__ void k_copy_g(int B, const SolveItem* __restrict__ items) {
-    const SolveItem& it = items[blockIdx.y];
+__global__ void k_copy_g(int B, const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
     if (!it.g) return;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x)
         it.u_vert[it.n + k] = it.g[k];
@@ -360,44 +381,107 @@ struct Workspace {
     }
 };
 
+int g_max_smem_optin = -1;
+int g_occ_grid = -1;
+
 }  // namespace
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters) {
-    // ---- plan: items, chunk table, scratch layout
-    std::vector<SolveItem> items(B);
-    std::vector<Chunk> chunks;
-    int64_t vec_doubles = 0;
-    for (int b = 0; b < B; ++b) vec_doubles += 6 * (S[b]->n_u + 1);
-    int32_t total_chunks = 0;
-    for (int b = 0; b < B; ++b) total_chunks += (int32_t)S[b]->chunks_h.size();
-    const size_t bytes_vec = sizeof(double) * (size_t)vec_doubles;
-    const size_t bytes_items = sizeof(SolveItem) * B;
-    const size_t bytes_state = sizeof(CgState) * B;
-    const size_t bytes_chunks = (B == 1) ? 0 : sizeof(Chunk) * (size_t)total_chunks;
-    const size_t bytes_part = sizeof(double2) * (size_t)std::max(total_chunks, 1);
+    if (g_max_smem_optin < 0) {
+        int dev = 0;
+        FEMI_CUDA(cudaGetDevice(&dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&g_max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       g_max_smem_optin - 4096));
+        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       g_max_smem_optin - 4096));
+        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       g_max_smem_optin / 2 - 4096));
+    }
+    // ---- choose the launch shape
+    int64_t nmax = 0, nnz_tot = 0;
+    for (int b = 0; b < B; ++b) {
+        nmax = std::max(nmax, S[b]->n_u);
+        nnz_tot += S[b]->nnz_uu;
+    }
+    int mode, ncta_item = 1;
+    if (B == 1 && S[0]->nnz_uu > 600000) {
+        mode = 2;
+    } else {
+        // one CTA per ~24K nonzeros, up to a 16-CTA cluster
+        int64_t nnz_max = 0;
+        for (int b = 0; b < B; ++b) nnz_max = std::max(nnz_max, S[b]->nnz_uu);
+        ncta_item = (int)std::min<int64_t>(16, std::max<int64_t>(1, (nnz_max + 23999) / 24000));
+        if (ncta_item > 1 && ncta_item < 16) {
+            int c = 1;
+            while (c < ncta_item) c <<= 1;
+            ncta_item = c;
+        }
+        mode = ncta_item == 1 ? 0 : 1;
+    }
+    int grid = 0;
+    std::vector<int> cta0(B), ncta(B);
+    size_t smem_bytes = 0;
+    int smem_rows = 0;
+    if (mode == 2) {
+        if (g_occ_grid < 0) {
+            int per_sm = 0, dev = 0, nsm = 0;
+            FEMI_CUDA(cudaGetDevice(&dev));
+            FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
+                                                                    g_max_smem_optin / 2 - 4096));
+            g_occ_grid = std::max(1, per_sm) * nsm;
+        }
+        grid = (int)std::min<int64_t>(g_occ_grid, std::max<int64_t>(1, (nmax + RNT - 1) / RNT));
+        cta0[0] = 0;
+        ncta[0] = grid;
+        smem_rows = (int)((nmax + grid - 1) / grid);
+        smem_bytes = sizeof(double) * 3 * (size_t)smem_rows;
+        if (smem_bytes > (size_t)(g_max_smem_optin / 2 - 4096)) {
+            smem_rows = 0;
+            smem_bytes = 0;
+        }
+    } else {
+        for (int b = 0; b < B; ++b) {
+            cta0[b] = b * ncta_item;
+            ncta[b] = ncta_item;
+        }
+        grid = B * ncta_item;
+        smem_rows = (int)((nmax + ncta_item - 1) / ncta_item);
+        smem_bytes = sizeof(double) * 3 * (size_t)smem_rows;
+        if (smem_bytes > (size_t)(g_max_smem_optin - 4096)) {
+            smem_rows = 0;
+            smem_bytes = 0;
+        }
+    }
+    const bool need_pvec = smem_rows == 0;
+
+    // ---- workspace: per item b, x, r, w (+ p, s) vectors, partials, barrier, state
+    std::vector<RItem> items(B);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t total = al(bytes_vec) + al(bytes_items) + al(bytes_state) + al(bytes_chunks) + al(bytes_part);
+    size_t total = al(sizeof(RItem) * B) + al(sizeof(CgState) * B);
+    for (int b = 0; b < B; ++b)
+        total += al(sizeof(double) * (S[b]->n_u + 1)) * (need_pvec ? 6 : 4) + al(sizeof(double) * 4 * ncta[b]) +
+                 al(2 * sizeof(unsigned));
     Workspace ws;
     ws.st = st;
     FEMI_CUDA(cudaMallocAsync(&ws.base, total, st));
     char* cur = (char*)ws.base;
-    double* vec = (double*)cur;
-    cur += al(bytes_vec);
-    SolveItem* d_items = (SolveItem*)cur;
-    cur += al(bytes_items);
-    CgState* d_state = (CgState*)cur;
-    cur += al(bytes_state);
-    Chunk* d_chunks = (Chunk*)cur;
-    cur += al(bytes_chunks);
-    double* d_part = (double*)cur;
-
-    int32_t c0 = 0;
+    auto take = [&](size_t x) {
+        char* p = cur;
+        cur += al(x);
+        return p;
+    };
+    RItem* d_items = (RItem*)take(sizeof(RItem) * B);
+    CgState* d_state = (CgState*)take(sizeof(CgState) * B);
+    char* bar_base = nullptr;
     for (int b = 0; b < B; ++b) {
         femi_system_s* s = S[b];
-        SolveItem& it = items[b];
-        const int64_t n = s->n_u;
+        RItem& it = items[b];
+        const size_t vb = sizeof(double) * (s->n_u + 1);
         it.orp = s->o_rowptr;
         it.oci = s->o_col;
         it.oav = s->o_val;
@@ -411,109 +495,97 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.g = g ? g[b] : nullptr;
         it.bin = bin ? bin[b] : nullptr;
         it.u_vert = u_vert[b];
-        it.x = vec;
-        it.r = vec + (n + 1);
-        it.q = vec + 2 * (n + 1);
-        it.b = vec + 3 * (n + 1);
-        it.p[0] = vec + 4 * (n + 1);
-        it.p[1] = vec + 5 * (n + 1);
-        vec += 6 * (n + 1);
-        it.n = (int32_t)n;
+        it.b = (double*)take(vb);
+        it.x = (double*)take(vb);
+        it.r = (double*)take(vb);
+        it.w = (double*)take(vb);
+        it.p = need_pvec ? (double*)take(vb) : nullptr;
+        it.sv = need_pvec ? (double*)take(vb) : nullptr;
+        it.part = (double*)take(sizeof(double) * 4 * ncta[b]);
+        it.bar = (unsigned*)take(2 * sizeof(unsigned));
+        if (!bar_base) bar_base = (char*)it.bar;
+        it.st = d_state + b;
+        it.n = (int32_t)s->n_u;
         it.m = (int32_t)s->m;
-        it.chunk0 = c0;
-        it.nchunks = (int32_t)s->chunks_h.size();
+        it.cta0 = cta0[b];
+        it.ncta = ncta[b];
         it.x0mode = (it.g == nullptr && o.x0 == 1) ? 0 : o.x0;
-        if (B > 1)
-            for (const Chunk& ch : s->chunks_h) chunks.push_back({b, ch.row0, ch.row1, ch.local});
-        c0 += it.nchunks;
     }
-    if (B == 1) d_chunks = S[0]->chunks_d;
-    FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
-    if (B > 1) FEMI_CUDA(cudaMemcpyAsync(d_chunks, chunks.data(), bytes_chunks, cudaMemcpyHostToDevice, st));
+    FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
+    for (int b = 0; b < B; ++b) FEMI_CUDA(cudaMemsetAsync(items[b].bar, 0, 2 * sizeof(unsigned), st));
 
-    // ---- init
-    k_reset<<<(B + 127) / 128, 128, 0, st>>>(B, d_items, d_state, o.rtol, o.max_iter); count_launches(1);
-    FEMI_CUDA(cudaGetLastError());
+    // ---- launches: reset, min/max(g), b, resident CG, mask copy
+    k_reset<<<(B + 127) / 128, 128, 0, st>>>(B, d_state, o.rtol, o.max_iter);
+    count_launches(1);
     if (o.x0 == 1) {
         int64_t mmax = 0;
         for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
         int gb = (int)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296));
-        k_minmax<<<gb, 256, 0, st>>>(B, d_items, d_state); count_launches(1);
-        FEMI_CUDA(cudaGetLastError());
+        k_minmax<<<gb, 256, 0, st>>>(B, d_items);
+        count_launches(1);
     }
-    if (total_chunks > 0) {
-        k_rhs<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, d_part); count_launches(1);
-        FEMI_CUDA(cudaGetLastError());
-        k_init_res<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, (double2*)d_part, 0); count_launches(1);
-        FEMI_CUDA(cudaGetLastError());
+    {
+        dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>((nmax + 255) / 256, 592)), B);
+        k_rhs<<<gg, 256, 0, st>>>(B, d_items);
+        count_launches(1);
+    }
+    FEMI_CUDA(cudaGetLastError());
+    if (nmax > 0) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(RNT);
+        cfg.dynamicSmemBytes = smem_bytes;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 0;
+        cudaError_t e;
+        if (mode == 2) {
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, smem_rows);
+        } else if (mode == 1) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = ncta_item;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<1>, (const RItem*)d_items, B, smem_rows);
+        } else {
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<0>, (const RItem*)d_items, B, smem_rows);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "k_pcg_resident launch");
+        count_launches(1);
     }
     {
         int64_t mmax = 1;
         for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
-        dim3 gg((unsigned)std::min<int64_t>((mmax + 255) / 256, 64), B);
-        k_copy_g<<<gg, 256, 0, st>>>(B, d_items); count_launches(1);
-        FEMI_CUDA(cudaGetLastError());
+        dim3 gg((unsigned)std::min<int64_t>((mmax + 255) / 256, 296), B);
+        k_copy_g<<<gg, 256, 0, st>>>(B, d_items);
+        count_launches(1);
     }
-
+    FEMI_CUDA(cudaGetLastError());
     std::vector<CgState> hs(B);
-    const int check = o.check_every > 0 ? o.check_every : 8;
-    int restarts = 0;
-    for (;;) {
-        // ---- iterate until every item is inactive (poll every `check` iterations)
-        bool any = total_chunks > 0;
-        while (any) {
-            for (int k = 0; k < check; ++k) {
-                k_spmv_dot<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, d_part); count_launches(1);
-                k_update<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, (double2*)d_part); count_launches(1);
-            }
-            FEMI_CUDA(cudaGetLastError());
-            FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, bytes_state, cudaMemcpyDeviceToHost, st));
-            FEMI_CUDA(cudaStreamSynchronize(st));
-            any = false;
-            for (int b = 0; b < B; ++b) any |= hs[b].active != 0;
-        }
-        if (total_chunks > 0) {
-            k_finalize<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks); count_launches(1);
-            k_true_res<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, d_part); count_launches(1);
-            FEMI_CUDA(cudaGetLastError());
-        }
-        FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, bytes_state, cudaMemcpyDeviceToHost, st));
-        FEMI_CUDA(cudaStreamSynchronize(st));
-        // confirmation of the true residual; restart the items that fail it
-        bool again = false;
-        for (int b = 0; b < B; ++b) {
-            const CgState& s = hs[b];
-            double rel = s.bn2 > 0.0 ? std::sqrt(s.res2 / s.bn2) : 0.0;
-            if (s.status == FEMI_OK && s.iters > 0 && s.iters < s.max_iter && !(rel <= o.rtol) && restarts < 8)
-                again = true;
-        }
-        if (!again) break;
-        ++restarts;
-        // reactivate the failing items and rebuild r from the current x
-        for (int b = 0; b < B; ++b) {
-            const CgState& s = hs[b];
-            double rel = s.bn2 > 0.0 ? std::sqrt(s.res2 / s.bn2) : 0.0;
-            int act = (s.status == FEMI_OK && s.iters > 0 && s.iters < s.max_iter && !(rel <= o.rtol)) ? 1 : 0;
-            FEMI_CUDA(cudaMemcpyAsync(&d_state[b].active, &act, sizeof(int), cudaMemcpyHostToDevice, st));
-        }
-        k_init_res<<<total_chunks, NT, 0, st>>>(d_items, d_state, d_chunks, (double2*)d_part, 1); count_launches(1);
-        FEMI_CUDA(cudaGetLastError());
-    }
+    FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaStreamSynchronize(st));
     femi_status ret = FEMI_OK;
     int64_t tot = 0;
     for (int b = 0; b < B; ++b) {
         const CgState& s = hs[b];
-        if (iters) iters[b] = s.iters;
         double rel = s.bn2 > 0.0 ? std::sqrt(s.res2 / s.bn2) : 0.0;
         if (S[b]->n_u == 0) rel = 0.0;
+        if (iters) iters[b] = S[b]->n_u == 0 ? 0 : s.iters;
         if (relres) relres[b] = rel;
         tot += s.iters;
-        femi_status sb = (femi_status)s.status;
+        femi_status sb = S[b]->n_u == 0 ? FEMI_OK : (femi_status)s.status;
         if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
         if (sb != FEMI_OK && ret == FEMI_OK) ret = sb;
     }
     if (total_iters) *total_iters = tot;
     if (ret != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)ret) + ")");
+    (void)bar_base;
+    (void)nnz_tot;
     return ret;
 }
 

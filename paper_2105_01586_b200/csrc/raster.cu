@@ -1,24 +1,19 @@
 // raster.cu -- S3+S4: rasterise the P1 solution and reduce the squared error
 // (PAPER.md:L239-241 interpolation; L262-265 "e_i = (u_i - f_i)^2", "total L2 error in
-// each triangle").
+// each triangle"), and the adjoint raster P^T r used by tonal optimisation (S6).
 //
-// Triangle-parallel, one warp per triangle (grid-stride over the canonical triangle
-// order, which is spatially coherent, so neighbouring warps touch neighbouring image
-// rows and the f / u / e lines are shared through L2). Lanes sweep the triangle's
-// bounding box; a pixel is processed by the triangle that owns it (reading A7: lowest
-// index among the closed triangles containing it), decided locally from the edge
-// functions and the precomputed ownership flags -- no owner map, no atomics:
-//   interior           -> owned
-//   on the edge opp. k -> owned iff flag bit k   (this triangle has the lower index)
-//   at vertex k        -> owned iff flag bit 3+k (this is the vertex's lowest triangle)
-// Per-triangle error sums and arg-max (ties: lowest pix) are warp reductions in a fixed
-// order, SSE is a per-CTA partial summed in fixed order by the last CTA: deterministic.
-#include "device.cuh"
+// Triangle-parallel with load-balanced expansion (raster_common.cuh): a pixel is
+// processed by the triangle that owns it (reading A7: lowest index among the closed
+// triangles containing it), decided locally from the edge functions and precomputed
+// ownership flags -- no owner map, no atomics. A vertex pixel takes its vertex value
+// exactly; otherwise u = u_a + l_b (u_b - u_a) + l_c (u_c - u_a), l = exact integer edge
+// function / 2*area (S3). Per-triangle error sums and arg-max (ties: lowest pix) are
+// sequential per triangle in pixel order; SSE is a per-CTA partial summed in fixed order
+// by the last CTA: deterministic.
+#include "raster_common.cuh"
 
 namespace femi {
 namespace {
-
-constexpr int RT = 256;  // threads per CTA (8 warps)
 
 struct RasterItem {
     const TriRec* tri;
@@ -34,91 +29,91 @@ struct RasterItem {
     int32_t pad;
 };
 
-__device__ __forceinline__ int orient_i(int ax, int ay, int bx, int by, int px, int py) {
-    return (bx - ax) * (py - ay) - (by - ay) * (px - ax);
-}
-
-__global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restrict__ items, double* __restrict__ part,
-                                                     uint32_t* __restrict__ counters) {
-    __shared__ double red[RT / 32];
+__global__ void __launch_bounds__(RB, 3) k_raster_error(const RasterItem* __restrict__ items, double* __restrict__ part,
+                                                        uint32_t* __restrict__ counters) {
+    __shared__ TriInfo info[RB];
+    __shared__ double tu[RB][3];
+    __shared__ int off[RB + 1];
+    __shared__ int wsum[RB / 32];
+    __shared__ double es[RCAP];
+    __shared__ unsigned char cs[RCAP];
+    __shared__ double red[RB / 32];
     __shared__ int flag;
     const RasterItem it = items[blockIdx.y];
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * RT + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * RT) >> 5;
-    double sse_loc = 0.0;
-    for (int64_t t = warp; t < it.T; t += nwarps) {
-        const TriRec R = it.tri[t];
-        const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-        const double ua = it.u_vert[R.v[0]], ub = it.u_vert[R.v[1]], uc = it.u_vert[R.v[2]];
-        const int x0 = min(ax, min(bx, cx)), x1 = max(ax, max(bx, cx));
-        const int y0 = min(ay, min(by, cy)), y1 = max(ay, max(by, cy));
-        const int bw = x1 - x0 + 1;
-        const int nbox = bw * (y1 - y0 + 1);
-        const double D = (double)orient_i(ax, ay, bx, by, cx, cy);
-        const double dba = ub - ua, dca = uc - ua;
-        double acc = 0.0;
-        double be = -1.0;
-        int bp = 0x7fffffff;
-        for (int k = lane; k < nbox; k += 32) {
-            const int py = y0 + k / bw, px = x0 + k % bw;
-            const int w0 = orient_i(bx, by, cx, cy, px, py);
-            const int w1 = orient_i(cx, cy, ax, ay, px, py);
-            const int w2 = orient_i(ax, ay, bx, by, px, py);
-            if ((w0 | w1 | w2) < 0) continue;  // outside the closed triangle
-            const int z = (w0 == 0) + (w1 == 0) + (w2 == 0);
-            double u;
-            bool vertex = false;
-            if (z == 0) {
-                u = ua + (w1 / D) * dba + (w2 / D) * dca;
-            } else if (z == 1) {
-                const int ke = (w0 == 0) ? 0 : ((w1 == 0) ? 1 : 2);
-                if (!(R.flags & (1u << ke))) continue;
-                u = ua + (w1 / D) * dba + (w2 / D) * dca;
-            } else {
-                const int kv = (w0 != 0) ? 0 : ((w1 != 0) ? 1 : 2);
-                if (!(R.flags & (8u << kv))) continue;
-                u = (kv == 0) ? ua : ((kv == 1) ? ub : uc);
-                vertex = true;
-            }
-            const int pix = py * it.W + px;
-            if (it.u_px) it.u_px[pix] = u;
-            if (it.f) {
-                const double d = u - it.f[pix];
-                const double e = d * d;
-                if (it.e_px) it.e_px[pix] = e;
-                acc += e;
-                if (!vertex && (e > be || (e == be && pix < bp))) {
-                    be = e;
-                    bp = pix;
-                }
-            }
+    const int tid = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * RB;
+    double acc = 0.0, be = -1.0;
+    int bp = -1, cnt = 0;
+    if (t0 < it.T) {
+        cnt = load_tris(it.tri, it.T, t0, info, off, wsum);
+        if (tid < cnt) {
+            const TriRec& R = it.tri[t0 + tid];
+            tu[tid][0] = it.u_vert[R.v[0]];
+            tu[tid][1] = it.u_vert[R.v[1]];
+            tu[tid][2] = it.u_vert[R.v[2]];
         }
-        if (it.f) {
-            acc = warp_sum(acc);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double oe = __shfl_xor_sync(0xffffffffu, be, o);
-                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                if (oe > be || (oe == be && op < bp)) {
-                    be = oe;
-                    bp = op;
+        __syncthreads();
+        const int total = off[cnt];
+        const bool with_f = it.f != nullptr;
+        int j = 0;
+        for (int r0 = 0; r0 < total; r0 += RCAP) {
+            const int rend = min(total, r0 + RCAP);
+            for (int k = r0 + tid; k < rend; k += RB) {
+                while (off[j + 1] <= k) ++j;
+                const TriInfo& I = info[j];
+                const int loc = k - off[j];
+                const int ry = loc / I.bw;
+                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
+                int w0, w1, w2, kv = 0;
+                const int cls = classify(I, px, py, w0, w1, w2, kv);
+                cs[k - r0] = (unsigned char)cls;
+                if (!cls) continue;
+                double u;
+                if (cls == 2) {
+                    u = tu[j][kv];
+                } else {
+                    const double D = (double)I.D, ua = tu[j][0];
+                    u = ua + (w1 / D) * (tu[j][1] - ua) + (w2 / D) * (tu[j][2] - ua);
+                }
+                const int64_t pix = (int64_t)py * it.W + px;
+                if (it.u_px) it.u_px[pix] = u;
+                if (with_f) {
+                    const double d = u - __ldcs(it.f + pix);
+                    const double e = d * d;
+                    es[k - r0] = e;
+                    if (it.e_px) __stcs(it.e_px + pix, e);
                 }
             }
-            if (lane == 0) {
-                if (it.tri_err) it.tri_err[t] = acc;
-                if (it.best) it.best[t] = (be >= 0.0) ? bp : -1;
+            __syncthreads();
+            if (with_f && tid < cnt) {
+                const int lo = max(off[tid], r0), hi = min(off[tid + 1], rend);
+                for (int k = lo; k < hi; ++k) {
+                    const int cls = cs[k - r0];
+                    if (!cls) continue;
+                    const double e = es[k - r0];
+                    acc += e;
+                    if (cls == 1 && e > be) {
+                        be = e;
+                        const TriInfo& I = info[tid];
+                        const int loc = k - off[tid];
+                        const int ry = loc / I.bw;
+                        bp = (I.y0 + ry) * it.W + I.x0 + loc - ry * I.bw;
+                    }
+                }
             }
-            sse_loc += acc;  // identical in every lane; lane 0's copy is used below
+            __syncthreads();
+        }
+        if (with_f && tid < cnt) {
+            if (it.tri_err) it.tri_err[t0 + tid] = acc;
+            if (it.best) it.best[t0 + tid] = bp;
         }
     }
     if (!it.f || !it.sse) return;
-    const double v = (lane == 0) ? sse_loc : 0.0;
-    const double tot = block_sum<RT>(v, red);
+    const double tot = block_sum<RB>(tid < cnt ? acc : 0.0, red);
     double* P = part + (size_t)blockIdx.y * gridDim.x;
-    if (threadIdx.x == 0) P[blockIdx.x] = tot;
+    if (tid == 0) P[blockIdx.x] = tot;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         __threadfence();
         flag = (atomicAdd(&counters[blockIdx.y], 1u) == gridDim.x - 1);
     }
@@ -126,12 +121,76 @@ __global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restric
     if (flag) {
         __threadfence();
         double s = 0.0;
-        for (int k = threadIdx.x; k < (int)gridDim.x; k += RT) s += __ldcg(&P[k]);
-        s = block_sum<RT>(s, red);
-        if (threadIdx.x == 0) {
+        for (int k = tid; k < (int)gridDim.x; k += RB) s += __ldcg(&P[k]);
+        s = block_sum<RB>(s, red);
+        if (tid == 0) {
             *it.sse = s;
             counters[blockIdx.y] = 0;
         }
+    }
+}
+
+// P^T r: per triangle, sum over its owned pixels of (l_a, l_b, l_c) r (vertex pixels:
+// weight 1 on that vertex) -> tri_w[3t+k]; the vertex gather happens in tonal.cu.
+__global__ void __launch_bounds__(RB, 3) k_adjoint_raster(const TriRec* __restrict__ tri, int64_t T, int W,
+                                                          const double* __restrict__ r, double* __restrict__ tri_w) {
+    __shared__ TriInfo info[RB];
+    __shared__ int off[RB + 1];
+    __shared__ int wsum[RB / 32];
+    __shared__ double rs[RCAP];
+    __shared__ unsigned char cs[RCAP];
+    const int tid = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * RB;
+    if (t0 >= T) return;
+    const int cnt = load_tris(tri, T, t0, info, off, wsum);
+    const int total = off[cnt];
+    double sa = 0.0, sb = 0.0, sc = 0.0;
+    int j = 0;
+    for (int r0 = 0; r0 < total; r0 += RCAP) {
+        const int rend = min(total, r0 + RCAP);
+        for (int k = r0 + tid; k < rend; k += RB) {
+            while (off[j + 1] <= k) ++j;
+            const TriInfo& I = info[j];
+            const int loc = k - off[j];
+            const int ry = loc / I.bw;
+            const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
+            int w0, w1, w2, kv = 0;
+            const int cls = classify(I, px, py, w0, w1, w2, kv);
+            cs[k - r0] = (unsigned char)(cls == 2 ? 2 + kv : cls);
+            if (cls) rs[k - r0] = __ldcs(r + (int64_t)py * W + px);
+        }
+        __syncthreads();
+        if (tid < cnt) {
+            const TriInfo& I = info[tid];
+            const double D = (double)I.D;
+            const int lo = max(off[tid], r0), hi = min(off[tid + 1], rend);
+            for (int k = lo; k < hi; ++k) {
+                const int c = cs[k - r0];
+                if (!c) continue;
+                const double rv = rs[k - r0];
+                if (c >= 2) {
+                    if (c == 2) sa += rv;
+                    else if (c == 3) sb += rv;
+                    else sc += rv;
+                    continue;
+                }
+                const int loc = k - off[tid];
+                const int ry = loc / I.bw;
+                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
+                const int w0 = orient_xy(I.bx, I.by, I.cx, I.cy, px, py);
+                const int w1 = orient_xy(I.cx, I.cy, I.ax, I.ay, px, py);
+                const int w2 = orient_xy(I.ax, I.ay, I.bx, I.by, px, py);
+                sa += (w0 / D) * rv;
+                sb += (w1 / D) * rv;
+                sc += (w2 / D) * rv;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < cnt) {
+        tri_w[3 * (t0 + tid)] = sa;
+        tri_w[3 * (t0 + tid) + 1] = sb;
+        tri_w[3 * (t0 + tid) + 2] = sc;
     }
 }
 
@@ -157,9 +216,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
         r.W = S[b]->W;
         Tmax = std::max(Tmax, r.T);
     }
-    // grid: enough warps for one triangle per warp up to ~8 resident CTAs per SM per item
-    int64_t want = (Tmax + (RT / 32) - 1) / (RT / 32);
-    int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)148 * 8 * 4 / std::max(1, B) + 1));
+    const int gx = (int)std::max<int64_t>(1, (Tmax + RB - 1) / RB);
     const size_t bytes_items = sizeof(RasterItem) * B;
     const size_t bytes_part = sizeof(double) * (size_t)gx * B;
     const size_t bytes_cnt = sizeof(uint32_t) * B;
@@ -172,9 +229,19 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
     dim3 grid(gx, B);
-    k_raster_error<<<grid, RT, 0, st>>>(d_items, d_part, d_cnt); count_launches(1);
+    k_raster_error<<<grid, RB, 0, st>>>(d_items, d_part, d_cnt);
+    count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
+    return FEMI_OK;
+}
+
+femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {
+    if (S->T == 0) return FEMI_OK;
+    const int gx = (int)((S->T + RB - 1) / RB);
+    k_adjoint_raster<<<gx, RB, 0, st>>>(S->tri, S->T, S->W, r, tri_w);
+    count_launches(1);
+    FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;
 }
 

@@ -18,58 +18,6 @@ namespace {
 
 constexpr int TT = 256;
 
-__device__ __forceinline__ int orient_i(int ax, int ay, int bx, int by, int px, int py) {
-    return (bx - ax) * (py - ay) - (by - ay) * (px - ax);
-}
-
-__global__ void __launch_bounds__(TT) k_adjoint_tri(int64_t T, int W, const TriRec* __restrict__ tri,
-                                                    const double* __restrict__ r, double* __restrict__ tri_w) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * TT + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * TT) >> 5;
-    for (int64_t t = warp; t < T; t += nwarps) {
-        const TriRec R = tri[t];
-        const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-        const int x0 = min(ax, min(bx, cx)), x1 = max(ax, max(bx, cx));
-        const int y0 = min(ay, min(by, cy)), y1 = max(ay, max(by, cy));
-        const int bw = x1 - x0 + 1, nbox = bw * (y1 - y0 + 1);
-        const double D = (double)orient_i(ax, ay, bx, by, cx, cy);
-        double sa = 0.0, sb = 0.0, sc = 0.0;
-        for (int k = lane; k < nbox; k += 32) {
-            const int py = y0 + k / bw, px = x0 + k % bw;
-            const int w0 = orient_i(bx, by, cx, cy, px, py);
-            const int w1 = orient_i(cx, cy, ax, ay, px, py);
-            const int w2 = orient_i(ax, ay, bx, by, px, py);
-            if ((w0 | w1 | w2) < 0) continue;
-            const int z = (w0 == 0) + (w1 == 0) + (w2 == 0);
-            const double rv = r[py * W + px];
-            if (z == 2) {
-                const int kv = (w0 != 0) ? 0 : ((w1 != 0) ? 1 : 2);
-                if (!(R.flags & (8u << kv))) continue;
-                if (kv == 0) sa += rv;
-                else if (kv == 1) sb += rv;
-                else sc += rv;
-                continue;
-            }
-            if (z == 1) {
-                const int ke = (w0 == 0) ? 0 : ((w1 == 0) ? 1 : 2);
-                if (!(R.flags & (1u << ke))) continue;
-            }
-            sa += (w0 / D) * rv;
-            sb += (w1 / D) * rv;
-            sc += (w2 / D) * rv;
-        }
-        sa = warp_sum(sa);
-        sb = warp_sum(sb);
-        sc = warp_sum(sc);
-        if (lane == 0) {
-            tri_w[3 * t] = sa;
-            tri_w[3 * t + 1] = sb;
-            tri_w[3 * t + 2] = sc;
-        }
-    }
-}
-
 __global__ void k_vertex_gather(int64_t nv, const int32_t* __restrict__ vt_ptr, const int32_t* __restrict__ vt_idx,
                                 const double* __restrict__ tri_w, double* __restrict__ w) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -171,7 +119,8 @@ struct Tonal {
 
     // s = B^T r
     femi_status apply_BT(const double* r, double* s_out) {
-        k_adjoint_tri<<<grid_for(S->T * 32), TT, 0, st>>>(S->T, S->W, S->tri, r, tri_w); count_launches(1);
+        femi_status ar = launch_adjoint_raster(S, r, tri_w, st);
+        if (ar != FEMI_OK) return ar;
         k_vertex_gather<<<grid_for(S->nv), TT, 0, st>>>(S->nv, S->vt_ptr, S->vt_idx, tri_w, w); count_launches(1);
         FEMI_CUDA(cudaGetLastError());
         femi_cg_opts o = inner;
