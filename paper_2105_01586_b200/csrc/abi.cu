@@ -49,14 +49,18 @@ femi_status check_device() {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    cudaDeviceProp prop;
-    e = cudaGetDeviceProperties(&prop, dev);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
-    if (prop.major != 10) {
-        set_error("libfemi is built for sm_100a (B200); current device is sm_" + std::to_string(prop.major) +
-                  std::to_string(prop.minor));
+    static int checked_dev = -1;  // cudaGetDeviceProperties is slow (ms): query two attributes once
+    if (checked_dev == dev) return FEMI_OK;
+    int major = 0, minor = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (major != 10 || minor != 0) {
+        set_error("libfemi is built for sm_100a (B200); current device is sm_" + std::to_string(major) +
+                  std::to_string(minor));
         return FEMI_E_CUDA;
     }
+    checked_dev = dev;
     static bool pool_set = false;
     if (!pool_set) {  // keep stream-ordered scratch cached between calls
         cudaMemPool_t pool;
@@ -231,6 +235,32 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
     U(alloc(S, &S->s, (size_t)M.n_u));
     S->chunks_h = make_chunks(M.uu_rowptr, M.n_u);
     U(upload(S, &S->chunks_d, S->chunks_h, st));
+    {
+        // chunk row table and int16 column offsets (relative to the chunk's first row)
+        std::vector<int32_t> row0(S->chunks_h.size() + 1);
+        for (size_t c = 0; c < S->chunks_h.size(); ++c) row0[c] = S->chunks_h[c].row0;
+        row0.back() = (int32_t)M.n_u;
+        S->nchunks = (int32_t)S->chunks_h.size();
+        U(upload(S, &S->chunk_row0, row0, st));
+        std::vector<int16_t> cd(M.uu_col.size() - M.n_u);
+        bool fits = true;
+        size_t o = 0;
+        for (size_t c = 0; c < S->chunks_h.size() && fits; ++c) {
+            const int32_t r0 = S->chunks_h[c].row0;
+            for (int32_t i = r0; i < S->chunks_h[c].row1 && fits; ++i)
+                for (int32_t e = M.uu_rowptr[i]; e < M.uu_rowptr[i + 1]; ++e) {
+                    const int32_t j = M.uu_col[e];
+                    if (j == i) continue;
+                    const int32_t d = j - r0;
+                    if (d < -32768 || d > 32767) {
+                        fits = false;
+                        break;
+                    }
+                    cd[o++] = (int16_t)d;
+                }
+        }
+        if (fits && !cd.empty()) U(upload(S, &S->o_cd, cd, st));
+    }
     U(launch_tri_records(S, d_tri, d_flags, st));
     U(launch_assemble_values(S, st));
     // the int32 triangle table and flags are folded into TriRec; drop them once done

@@ -89,9 +89,15 @@ struct femi_system_s {
     int32_t* o_col = nullptr;
     double* o_val = nullptr;
     double* s = nullptr;
-    // PCG row chunks (host copy + device copy numbered as batch item 0)
+    // PCG row chunks: chunk c = rows [chunk_row0[c], chunk_row0[c+1]) (<= kRowsPerChunk rows,
+    // <= kChunkNnzCap off-diagonals unless a single row is longer)
     std::vector<femi::Chunk> chunks_h;
     femi::Chunk* chunks_d = nullptr;
+    int32_t* chunk_row0 = nullptr;
+    int32_t nchunks = 0;
+    // off-diagonal columns as int16 offsets from their chunk's first row (NULL if the
+    // matrix bandwidth does not allow it; o_col is used then)
+    int16_t* o_cd = nullptr;
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -111,7 +117,7 @@ femi_status cuda_fail(cudaError_t e, const char* what);
 // kernel-launch accounting (femi_kernel_launches)
 void count_launches(int64_t n);
 
-constexpr int kRowsPerChunk = 256;
+constexpr int kRowsPerChunk = 512;
 constexpr int kChunkNnzCap = 2048;
 
 // launchers (defined in the .cu files)

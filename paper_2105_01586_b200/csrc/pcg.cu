@@ -9,14 +9,17 @@
 //   S: w = A^ r (gathers r) ; partial (r.r, w.r, ||D^1/2 r||^2)
 //   -- group barrier (partials published) -- every CTA sums the partials in the same
 //   fixed order, so alpha/beta/convergence are bit-identical in all CTAs (deterministic).
-// Each batch item (one system / right-hand side) owns a group of CTAs and a contiguous
-// row range per CTA. p, s and x never leave the CTA, so they live in shared memory for
-// the whole solve; only r (gathered by neighbours) and w go through L2/HBM. Group
-// barriers: __syncthreads (1 CTA), the hardware cluster barrier (a cluster of <= 16
-// CTAs, small systems: C1-C4), or a global sense-reversing barrier over a cooperative
-// grid (one huge system: C5). The stopping rule is the unscaled relative residual
-// ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a failed
-// confirmation restarts CG from the current iterate inside the same launch (reading A11).
+// Each batch item (one system / right-hand side) owns a group of CTAs; each CTA owns a
+// contiguous range of row chunks (<= 512 rows, <= 2048 off-diagonals). The SpMV is
+// CSR-stream per chunk: coalesced loads of values and (int16 chunk-relative) columns,
+// independent gathers of r, products staged in shared memory, then one row per thread.
+// p and s (and x when it fits) never leave the CTA: they live in shared memory for the
+// whole solve; only r (gathered by neighbours) and w go through L2/HBM. Group barriers:
+// __syncthreads (1 CTA), the hardware cluster barrier (a cluster of <= 16 CTAs, small
+// systems: C1-C4), or a global sense-reversing barrier over a cooperative grid (one huge
+// system: C5). The stopping rule is the unscaled relative residual ||D^1/2 r^|| <= rtol
+// ||b||, confirmed at exit with the unscaled matrix; a failed confirmation restarts CG
+// from the current iterate inside the same launch (reading A11).
 #include <algorithm>
 #include <cmath>
 
@@ -37,9 +40,11 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 struct RItem {
     const int32_t* orp;  // scaled off-diagonal CSR
     const int32_t* oci;
+    const int16_t* ocd;  // int16 columns relative to the chunk's first row, or NULL
     const double* oav;
-    const double* s;  // D^-1/2
-    const int32_t* urp;  // unscaled A_uu (diagonal included), true residual
+    const int32_t* crow;  // chunk c = rows [crow[c], crow[c+1])
+    const double* s;      // D^-1/2
+    const int32_t* urp;   // unscaled A_uu (diagonal included), true residual
     const int32_t* uci;
     const double* uav;
     const int32_t* krp;  // A_uk
@@ -49,7 +54,7 @@ struct RItem {
     const double* bin;  // given b or NULL
     double* u_vert;
     double* b;  // unscaled right-hand side
-    double* x;  // x^ (global copy: initial guess gathers, restart)
+    double* x;  // x^ (initial guess gathers; the iterate when it does not fit in smem)
     double* r;  // r^ (published every iteration)
     double* w;  // A^ r^
     double* p;  // used when the CTA's rows do not fit shared memory
@@ -57,10 +62,11 @@ struct RItem {
     double* part;       // [ncta][4] partial sums
     unsigned int* bar;  // [2] global barrier count / generation
     CgState* st;
-    int32_t n, m, cta0, ncta, x0mode, pad;
+    int32_t n, m, cta0, ncta, nchunks, x0mode;
 };
 
 constexpr int RNT = 512;  // threads per CTA of the persistent solver
+constexpr int NCAP = kChunkNnzCap;
 
 __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -175,6 +181,7 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [RNT/32][
 template <int MODE>
 __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, double4 loc, double* sh) {
     double4 t = block_sum4(loc, sh);
+    if constexpr (MODE == 0) return t;
     if (threadIdx.x == 0) {
         double* P = it.part + 4 * rank;
         P[0] = t.x;
@@ -182,7 +189,6 @@ __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, doubl
         P[2] = t.z;
         P[3] = t.w;
     }
-    if constexpr (MODE == 0) return t;
     group_sync<MODE>(it);
     double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
     for (int k = threadIdx.x; k < it.ncta; k += RNT) {
@@ -195,32 +201,59 @@ __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, doubl
     return block_sum4(a, sh);
 }
 
-// w_i = r_i + sum_j a^_ij r_j over the CTA's rows; returns the partial (r.r, w.r, ||r/s||^2)
-__device__ __forceinline__ double4 spmv_w(const RItem& it, int R0, int R1) {
+// w = A^ r over the CTA's chunks (CSR-stream); returns the partial (r.r, w.r, ||r/s||^2)
+__device__ __forceinline__ double4 spmv_w(const RItem& it, int c0, int c1, double* __restrict__ prod) {
     double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
     const int32_t* __restrict__ orp = it.orp;
-    const int32_t* __restrict__ oci = it.oci;
     const double* __restrict__ oav = it.oav;
     const double* __restrict__ r = it.r;
-    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
-        const double ri = __ldcg(r + i);
+    const int tid = threadIdx.x;
+    for (int c = c0; c < c1; ++c) {
+        const int rb = it.crow[c], re = it.crow[c + 1];
+        const int e0 = orp[rb], e1 = orp[re];
+        const int i = rb + tid;
+        int a = 0, b = 0;
+        double ri = 0.0, si = 1.0;
+        if (i < re) {
+            a = orp[i];
+            b = orp[i + 1];
+            ri = __ldcg(r + i);
+            si = it.s[i];
+        }
         double acc = ri;
-        const int e1 = orp[i + 1];
-        for (int e = orp[i]; e < e1; ++e) acc = fma(oav[e], __ldcg(r + oci[e]), acc);
-        it.w[i] = acc;
-        const double ru = ri / it.s[i];
-        loc.x += ri * ri;
-        loc.y += acc * ri;
-        loc.z += ru * ru;
+        if (e1 - e0 <= NCAP) {
+            if (it.ocd) {
+                const int16_t* __restrict__ cd = it.ocd;
+#pragma unroll 4
+                for (int e = e0 + tid; e < e1; e += RNT) prod[e - e0] = oav[e] * __ldcg(r + rb + cd[e]);
+            } else {
+                const int32_t* __restrict__ ci = it.oci;
+#pragma unroll 4
+                for (int e = e0 + tid; e < e1; e += RNT) prod[e - e0] = oav[e] * __ldcg(r + ci[e]);
+            }
+            __syncthreads();
+            for (int e = a; e < b; ++e) acc += prod[e - e0];
+            __syncthreads();
+        } else {  // a row longer than the staging buffer: direct gathers
+            for (int e = a; e < b; ++e) acc = fma(oav[e], __ldcg(r + it.oci[e]), acc);
+        }
+        if (i < re) {
+            it.w[i] = acc;
+            const double ru = ri / si;
+            loc.x += ri * ri;
+            loc.y += acc * ri;
+            loc.z += ru * ru;
+        }
     }
     return loc;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
-    k_pcg_resident(const RItem* __restrict__ items, int nitems, int smem_rows) {
-    extern __shared__ double svec[];  // [p | s | x] x smem_rows when the rows fit
+    k_pcg_resident(const RItem* __restrict__ items, int nitems, int vrows, int nvec) {
+    extern __shared__ double smem[];  // prod[NCAP] | p[vrows] | s[vrows] | x[vrows]
     __shared__ double sh[4 * (RNT / 32)];
+    double* prod = smem;
     // ---- which item / rank
     int item = 0, rank = 0;
     if constexpr (MODE == 1) {
@@ -231,7 +264,6 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
         rank = (int)cr;
     } else if constexpr (MODE == 0) {
         item = blockIdx.x;
-        rank = 0;
     } else {
         for (int k = 0; k < nitems; ++k)
             if ((int)blockIdx.x >= items[k].cta0) item = k;
@@ -239,32 +271,33 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
     }
     const RItem& it = items[item];
     CgState* S = it.st;
-    const int n = it.n;
-    const int R0 = (int)((long long)n * rank / it.ncta), R1 = (int)((long long)n * (rank + 1) / it.ncta);
-    const bool in_smem = (R1 - R0) <= smem_rows;
-    double* P = in_smem ? svec : it.p + R0;
-    double* SV = in_smem ? svec + smem_rows : it.sv + R0;
-    double* X = in_smem ? svec + 2 * smem_rows : it.x + R0;
+    const int c0 = (int)((long long)it.nchunks * rank / it.ncta);
+    const int c1 = (int)((long long)it.nchunks * (rank + 1) / it.ncta);
+    const int R0 = it.crow[c0], R1 = it.crow[c1];
+    double* P = nvec >= 2 ? smem + NCAP : it.p + R0;
+    double* SV = nvec >= 2 ? smem + NCAP + vrows : it.sv + R0;
+    double* X = nvec >= 3 ? smem + NCAP + 2 * vrows : it.x + R0;
     const double rtol = S->rtol;
     const int max_iter = S->max_iter;
     double x0v = 0.0;
     if (it.x0mode == 1) x0v = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
+    const int tid = threadIdx.x;
 
-    // ---- init: x^0 (global, gathered by the first residual), r0, bn2
-    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+    // ---- init: x^0 (global, gathered by the first residual), r0, ||b||^2
+    for (int i = R0 + tid; i < R1; i += RNT) {
         double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[i] : 0.0);
         it.x[i] = x0 / it.s[i];
     }
     group_sync<MODE>(it);
     double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+    for (int i = R0 + tid; i < R1; i += RNT) {
         const double si = it.s[i];
-        double ax = __ldcg(it.x + i);
+        const double xi = __ldcg(it.x + i);
+        double ax = xi;
         for (int e = it.orp[i]; e < it.orp[i + 1]; ++e) ax = fma(it.oav[e], __ldcg(it.x + it.oci[e]), ax);
         const double bi = it.b[i];
-        const double ri = si * bi - ax;
-        it.r[i] = ri;
-        X[i - R0] = __ldcg(it.x + i);
+        it.r[i] = si * bi - ax;
+        if (nvec >= 3) X[i - R0] = xi;
         loc.x += bi * bi;
     }
     double4 tot = group_reduce<MODE>(it, rank, loc, sh);
@@ -273,12 +306,12 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
     int iters = 0, status = FEMI_OK, restarts = 0;
     double res2 = 0.0;
     for (;;) {  // (re)start: w = A^ r, p = s = 0
-        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        for (int i = R0 + tid; i < R1; i += RNT) {
             P[i - R0] = 0.0;
             SV[i - R0] = 0.0;
         }
-        group_sync<MODE>(it);  // r visible
-        tot = group_reduce<MODE>(it, rank, spmv_w(it, R0, R1), sh);
+        group_sync<MODE>(it);  // r visible, partials consumed
+        tot = group_reduce<MODE>(it, rank, spmv_w(it, c0, c1, prod), sh);
         double gam = tot.x, del = tot.y, rho = tot.z;
         double alpha = 0.0, beta = 0.0;
         bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho);
@@ -295,20 +328,34 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
             }
         }
         while (run) {
-            // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
-            for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
-                const int l = i - R0;
-                const double ri = __ldcg(it.r + i);
-                const double pi = fma(beta, P[l], ri);
-                const double si = fma(beta, SV[l], __ldcg(it.w + i));
-                P[l] = pi;
-                SV[l] = si;
-                X[l] = fma(alpha, pi, X[l]);
-                it.r[i] = fma(-alpha, si, ri);
+            // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s (4 rows/thread in flight)
+            for (int base = R0 + tid; base < R1; base += 4 * RNT) {
+                double rv[4], wv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = base + q * RNT;
+                    if (i < R1) {
+                        rv[q] = __ldcg(it.r + i);
+                        wv[q] = __ldcg(it.w + i);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = base + q * RNT;
+                    if (i < R1) {
+                        const int l = i - R0;
+                        const double pi = fma(beta, P[l], rv[q]);
+                        const double si = fma(beta, SV[l], wv[q]);
+                        P[l] = pi;
+                        SV[l] = si;
+                        X[l] = fma(alpha, pi, X[l]);
+                        it.r[i] = fma(-alpha, si, rv[q]);
+                    }
+                }
             }
             ++iters;
             group_sync<MODE>(it);  // r published
-            tot = group_reduce<MODE>(it, rank, spmv_w(it, R0, R1), sh);
+            tot = group_reduce<MODE>(it, rank, spmv_w(it, c0, c1, prod), sh);
             const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 status = FEMI_E_NONFINITE;
@@ -329,23 +376,19 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
             gam = gam2;
         }
         // ---- finalize: x = D^-1/2 x^ (or x0 untouched at 0 iterations, 0 when b == 0)
-        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        for (int i = R0 + tid; i < R1; i += RNT) {
             double xi;
             if (bn2 == 0.0) xi = 0.0;
             else if (iters == 0) xi = (it.x0mode == 2) ? it.u_vert[i] : x0v;
             else xi = it.s[i] * X[i - R0];
             it.u_vert[i] = xi;
         }
-        if (it.g)
-            for (int k = R0 + threadIdx.x; k < R1; k += RNT) {  // mask part, split by rows over the group
-                (void)k;
-            }
         group_sync<MODE>(it);  // u_vert visible
         // true residual with the unscaled matrix; keeps s_i * r_true in r for a restart
         loc = make_double4(0.0, 0.0, 0.0, 0.0);
-        for (int i = R0 + threadIdx.x; i < R1; i += RNT) {
+        for (int i = R0 + tid; i < R1; i += RNT) {
             double ax = 0.0;
-            for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+            for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], __ldcg(it.u_vert + it.uci[e]), ax);
             const double ri = it.b[i] - ax;
             it.r[i] = it.s[i] * ri;
             loc.x += ri * ri;
@@ -355,9 +398,9 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
         const bool fail = bn2 > 0.0 && !(res2 <= tol2);
         if (!(status == FEMI_OK && iters > 0 && fail && iters < max_iter && restarts < 8)) break;
         ++restarts;
-        for (int i = R0 + threadIdx.x; i < R1; i += RNT) X[i - R0] = it.u_vert[i] / it.s[i];
+        for (int i = R0 + tid; i < R1; i += RNT) X[i - R0] = it.u_vert[i] / it.s[i];
     }
-    if (rank == 0 && threadIdx.x == 0) {
+    if (rank == 0 && tid == 0) {
         S->iters = iters;
         S->status = status;
         S->res2 = res2;
@@ -381,90 +424,78 @@ struct Workspace {
     }
 };
 
-int g_max_smem_optin = -1;
+int g_smem_optin = -1;
 int g_occ_grid = -1;
+int g_nsm = 0;
+
+// rows of the largest CTA range for an item split into ncta CTAs
+int64_t max_cta_rows(const femi_system_s* s, int ncta) {
+    int64_t mx = 0;
+    const int nc = s->nchunks;
+    for (int k = 0; k < ncta; ++k) {
+        const int a = (int)((long long)nc * k / ncta), b = (int)((long long)nc * (k + 1) / ncta);
+        const int r0 = a < nc ? s->chunks_h[a].row0 : (int)s->n_u;
+        const int r1 = b < nc ? s->chunks_h[b].row0 : (int)s->n_u;
+        mx = std::max<int64_t>(mx, r1 - r0);
+    }
+    return mx;
+}
 
 }  // namespace
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters) {
-    if (g_max_smem_optin < 0) {
+    if (g_smem_optin < 0) {
         int dev = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
-        FEMI_CUDA(cudaDeviceGetAttribute(&g_max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_max_smem_optin - 4096));
+                                       g_smem_optin - 2048));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_max_smem_optin - 4096));
+                                       g_smem_optin - 2048));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_max_smem_optin / 2 - 4096));
+                                       g_smem_optin / 2 - 2048));
+        int per_sm = 0;
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
+                                                                g_smem_optin / 2 - 2048));
+        g_occ_grid = std::max(1, per_sm) * g_nsm;
     }
-    // ---- choose the launch shape
-    int64_t nmax = 0, nnz_tot = 0;
+    // ---- launch shape: one huge system -> cooperative grid; otherwise one cluster per item
+    int64_t nmax = 0, nnz_max = 0;
     for (int b = 0; b < B; ++b) {
         nmax = std::max(nmax, S[b]->n_u);
-        nnz_tot += S[b]->nnz_uu;
+        nnz_max = std::max(nnz_max, S[b]->nnz_uu);
     }
     int mode, ncta_item = 1;
     if (B == 1 && S[0]->nnz_uu > 600000) {
         mode = 2;
+        ncta_item = std::max(1, std::min(g_occ_grid, S[0]->nchunks));
     } else {
-        // one CTA per ~24K nonzeros, up to a 16-CTA cluster
-        int64_t nnz_max = 0;
-        for (int b = 0; b < B; ++b) nnz_max = std::max(nnz_max, S[b]->nnz_uu);
         ncta_item = (int)std::min<int64_t>(16, std::max<int64_t>(1, (nnz_max + 23999) / 24000));
-        if (ncta_item > 1 && ncta_item < 16) {
-            int c = 1;
-            while (c < ncta_item) c <<= 1;
-            ncta_item = c;
-        }
+        int c = 1;
+        while (c < ncta_item) c <<= 1;
+        ncta_item = std::min(c, 16);
         mode = ncta_item == 1 ? 0 : 1;
     }
-    int grid = 0;
-    std::vector<int> cta0(B), ncta(B);
-    size_t smem_bytes = 0;
-    int smem_rows = 0;
-    if (mode == 2) {
-        if (g_occ_grid < 0) {
-            int per_sm = 0, dev = 0, nsm = 0;
-            FEMI_CUDA(cudaGetDevice(&dev));
-            FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
-                                                                    g_max_smem_optin / 2 - 4096));
-            g_occ_grid = std::max(1, per_sm) * nsm;
-        }
-        grid = (int)std::min<int64_t>(g_occ_grid, std::max<int64_t>(1, (nmax + RNT - 1) / RNT));
-        cta0[0] = 0;
-        ncta[0] = grid;
-        smem_rows = (int)((nmax + grid - 1) / grid);
-        smem_bytes = sizeof(double) * 3 * (size_t)smem_rows;
-        if (smem_bytes > (size_t)(g_max_smem_optin / 2 - 4096)) {
-            smem_rows = 0;
-            smem_bytes = 0;
-        }
-    } else {
-        for (int b = 0; b < B; ++b) {
-            cta0[b] = b * ncta_item;
-            ncta[b] = ncta_item;
-        }
-        grid = B * ncta_item;
-        smem_rows = (int)((nmax + ncta_item - 1) / ncta_item);
-        smem_bytes = sizeof(double) * 3 * (size_t)smem_rows;
-        if (smem_bytes > (size_t)(g_max_smem_optin - 4096)) {
-            smem_rows = 0;
-            smem_bytes = 0;
-        }
-    }
-    const bool need_pvec = smem_rows == 0;
+    const int grid = B * ncta_item;
+    // shared-memory residency of p, s (and x): as many vectors as fit the per-CTA budget
+    int64_t vrows = 0;
+    for (int b = 0; b < B; ++b) vrows = std::max(vrows, max_cta_rows(S[b], ncta_item));
+    const size_t budget = (size_t)(mode == 2 ? g_smem_optin / 2 - 2048 : g_smem_optin - 2048);
+    int nvec = 3;
+    while (nvec >= 2 && sizeof(double) * (NCAP + nvec * (size_t)vrows) > budget) --nvec;
+    if (nvec < 2) nvec = 0;
+    const size_t smem_bytes = sizeof(double) * (NCAP + (size_t)nvec * vrows);
 
-    // ---- workspace: per item b, x, r, w (+ p, s) vectors, partials, barrier, state
+    // ---- workspace: per item b, x, r, w, b (+ p, s) vectors, partials, barrier, state
     std::vector<RItem> items(B);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t total = al(sizeof(RItem) * B) + al(sizeof(CgState) * B);
     for (int b = 0; b < B; ++b)
-        total += al(sizeof(double) * (S[b]->n_u + 1)) * (need_pvec ? 6 : 4) + al(sizeof(double) * 4 * ncta[b]) +
+        total += al(sizeof(double) * (S[b]->n_u + 1)) * (nvec == 0 ? 6 : 4) + al(sizeof(double) * 4 * ncta_item) +
                  al(2 * sizeof(unsigned));
     Workspace ws;
     ws.st = st;
@@ -477,14 +508,15 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     };
     RItem* d_items = (RItem*)take(sizeof(RItem) * B);
     CgState* d_state = (CgState*)take(sizeof(CgState) * B);
-    char* bar_base = nullptr;
     for (int b = 0; b < B; ++b) {
         femi_system_s* s = S[b];
         RItem& it = items[b];
         const size_t vb = sizeof(double) * (s->n_u + 1);
         it.orp = s->o_rowptr;
         it.oci = s->o_col;
+        it.ocd = s->o_cd;
         it.oav = s->o_val;
+        it.crow = s->chunk_row0;
         it.s = s->s;
         it.urp = s->uu_rowptr;
         it.uci = s->uu_col;
@@ -499,16 +531,16 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.x = (double*)take(vb);
         it.r = (double*)take(vb);
         it.w = (double*)take(vb);
-        it.p = need_pvec ? (double*)take(vb) : nullptr;
-        it.sv = need_pvec ? (double*)take(vb) : nullptr;
-        it.part = (double*)take(sizeof(double) * 4 * ncta[b]);
+        it.p = nvec == 0 ? (double*)take(vb) : nullptr;
+        it.sv = nvec == 0 ? (double*)take(vb) : nullptr;
+        it.part = (double*)take(sizeof(double) * 4 * ncta_item);
         it.bar = (unsigned*)take(2 * sizeof(unsigned));
-        if (!bar_base) bar_base = (char*)it.bar;
         it.st = d_state + b;
         it.n = (int32_t)s->n_u;
         it.m = (int32_t)s->m;
-        it.cta0 = cta0[b];
-        it.ncta = ncta[b];
+        it.cta0 = b * ncta_item;
+        it.ncta = ncta_item;
+        it.nchunks = s->nchunks;
         it.x0mode = (it.g == nullptr && o.x0 == 1) ? 0 : o.x0;
     }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
@@ -539,21 +571,22 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 0;
+        const int vr = (int)vrows;
         cudaError_t e;
         if (mode == 2) {
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
             cfg.numAttrs = 1;
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, smem_rows);
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
         } else if (mode == 1) {
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = ncta_item;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.numAttrs = 1;
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<1>, (const RItem*)d_items, B, smem_rows);
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<1>, (const RItem*)d_items, B, vr, nvec);
         } else {
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<0>, (const RItem*)d_items, B, smem_rows);
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<0>, (const RItem*)d_items, B, vr, nvec);
         }
         if (e != cudaSuccess) return cuda_fail(e, "k_pcg_resident launch");
         count_launches(1);
@@ -577,15 +610,13 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         if (S[b]->n_u == 0) rel = 0.0;
         if (iters) iters[b] = S[b]->n_u == 0 ? 0 : s.iters;
         if (relres) relres[b] = rel;
-        tot += s.iters;
+        tot += S[b]->n_u == 0 ? 0 : s.iters;
         femi_status sb = S[b]->n_u == 0 ? FEMI_OK : (femi_status)s.status;
         if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
         if (sb != FEMI_OK && ret == FEMI_OK) ret = sb;
     }
     if (total_iters) *total_iters = tot;
     if (ret != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)ret) + ")");
-    (void)bar_base;
-    (void)nnz_tot;
     return ret;
 }
 

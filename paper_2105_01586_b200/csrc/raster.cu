@@ -78,10 +78,10 @@ __global__ void __launch_bounds__(RB, 3) k_raster_error(const RasterItem* __rest
                 const int64_t pix = (int64_t)py * it.W + px;
                 if (it.u_px) it.u_px[pix] = u;
                 if (with_f) {
-                    const double d = u - __ldcs(it.f + pix);
+                    const double d = u - it.f[pix];
                     const double e = d * d;
                     es[k - r0] = e;
-                    if (it.e_px) __stcs(it.e_px + pix, e);
+                    if (it.e_px) it.e_px[pix] = e;
                 }
             }
             __syncthreads();
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(RB, 3) k_adjoint_raster(const TriRec* __restri
             int w0, w1, w2, kv = 0;
             const int cls = classify(I, px, py, w0, w1, w2, kv);
             cs[k - r0] = (unsigned char)(cls == 2 ? 2 + kv : cls);
-            if (cls) rs[k - r0] = __ldcs(r + (int64_t)py * W + px);
+            if (cls) rs[k - r0] = r[(int64_t)py * W + px];
         }
         __syncthreads();
         if (tid < cnt) {
