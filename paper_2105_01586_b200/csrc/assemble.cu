@@ -96,7 +96,24 @@ __global__ void k_scaled_offdiag(int64_t n_u, const int32_t* __restrict__ urp, c
     }
 }
 
+__global__ void k_sell_values(int64_t ne, const int32_t* __restrict__ src, const double* __restrict__ oval,
+                              double* __restrict__ sval) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t q = src[e];
+        sval[e] = q >= 0 ? oval[q] : 0.0;
+    }
+}
+
 }  // namespace
+
+femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st) {
+    if (S->sell_nnz == 0) return FEMI_OK;
+    int g = (int)std::min<int64_t>((S->sell_nnz + 255) / 256, 148 * 16);
+    k_sell_values<<<g, 256, 0, st>>>(S->sell_nnz, d_src, S->o_val, S->sell_val);
+    count_launches(1);
+    FEMI_CUDA(cudaGetLastError());
+    return FEMI_OK;
+}
 
 femi_status launch_tri_records(femi_system_s* S, const int32_t* d_tri, const uint32_t* d_flags, cudaStream_t st) {
     if (S->T > 0) {

@@ -98,6 +98,20 @@ struct femi_system_s {
     // off-diagonal columns as int16 offsets from their chunk's first row (NULL if the
     // matrix bandwidth does not allow it; o_col is used then)
     int16_t* o_cd = nullptr;
+    // Sliced ELL (SELL-32-sigma) copy of the scaled off-diagonal matrix for the solver:
+    // windows of kSellSigma rows, rows sorted by length inside a window, slices of 32 rows
+    // stored column-major (entry k of lane l of slice s at sell_base[s] + 32k + l).
+    int32_t nwin = 0, nslices = 0;
+    int32_t* win_slice = nullptr;  // nwin+1: first slice of each window
+    int32_t* sell_perm = nullptr;  // 32*nslices: natural row of each slice lane, -1 = padding
+    int32_t* sell_len = nullptr;   // nslices: entries per lane
+    int32_t* sell_base = nullptr;  // nslices: first entry
+    int32_t* sell_cbase = nullptr; // nslices: first row of the slice's window (int16 column base)
+    double* sell_val = nullptr;
+    int16_t* sell_c16 = nullptr;   // column - window_row0 (when the bandwidth allows)
+    int32_t* sell_c32 = nullptr;   // absolute column otherwise
+    int64_t sell_nnz = 0;
+    int32_t* sell_src_tmp = nullptr;  // assembly-time map SELL entry -> o_val index
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -118,6 +132,8 @@ femi_status cuda_fail(cudaError_t e, const char* what);
 void count_launches(int64_t n);
 
 constexpr int kRowsPerChunk = 512;
+constexpr int kSellSigma = 512;  // rows per SELL window (sorting scope)
+femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st);
 constexpr int kChunkNnzCap = 2048;
 
 // launchers (defined in the .cu files)

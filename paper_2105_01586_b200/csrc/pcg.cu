@@ -2,24 +2,25 @@
 //
 // B200 design: ONE persistent launch per (batched) solve. The Jacobi preconditioner is
 // folded into the matrix at assembly (A^ = D^-1/2 A D^-1/2, unit diagonal, only the
-// off-diagonal CSR stored), so CG runs on A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b).
+// off-diagonal part stored), so CG runs on A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b).
 // The recurrence is the single-reduction form of CG (Chronopoulos-Gear): per iteration
 //   U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s      (own rows)
 //   -- group barrier (r published) --
 //   S: w = A^ r (gathers r) ; partial (r.r, w.r, ||D^1/2 r||^2)
 //   -- group barrier (partials published) -- every CTA sums the partials in the same
 //   fixed order, so alpha/beta/convergence are bit-identical in all CTAs (deterministic).
-// Each batch item (one system / right-hand side) owns a group of CTAs; each CTA owns a
-// contiguous range of row chunks (<= 512 rows, <= 2048 off-diagonals). The SpMV is
-// CSR-stream per chunk: coalesced loads of values and (int16 chunk-relative) columns,
-// independent gathers of r, products staged in shared memory, then one row per thread.
-// p and s (and x when it fits) never leave the CTA: they live in shared memory for the
-// whole solve; only r (gathered by neighbours) and w go through L2/HBM. Group barriers:
-// __syncthreads (1 CTA), the hardware cluster barrier (a cluster of <= 16 CTAs, small
-// systems: C1-C4), or a global sense-reversing barrier over a cooperative grid (one huge
-// system: C5). The stopping rule is the unscaled relative residual ||D^1/2 r^|| <= rtol
-// ||b||, confirmed at exit with the unscaled matrix; a failed confirmation restarts CG
-// from the current iterate inside the same launch (reading A11).
+// The SpMV reads the matrix in sliced-ELL form (SELL-32-sigma, sigma = 512 rows, rows
+// sorted by length inside a window): each warp takes one 32-row slice, every warp load
+// of values / int16 window-relative columns is one coalesced 32-lane access, and all
+// entries of a row are independent loads (no shared-memory staging, no block barrier in
+// the SpMV). Each batch item (system / right-hand side) owns a group of CTAs, each CTA a
+// contiguous range of windows. p and s (and x when it fits) never leave the CTA: they
+// live in shared memory for the whole solve; only r (gathered by neighbours) and w go
+// through L2/HBM. Group barriers: __syncthreads (1 CTA), the hardware cluster barrier
+// (a cluster of <= 16 CTAs: C1-C4), or a global sense-reversing barrier over a
+// cooperative grid (one huge system: C5). The stopping rule is the unscaled relative
+// residual ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a
+// failed confirmation restarts CG from the current iterate inside the launch (A11).
 #include <algorithm>
 #include <cmath>
 
@@ -38,13 +39,16 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 }
 
 struct RItem {
-    const int32_t* orp;  // scaled off-diagonal CSR
-    const int32_t* oci;
-    const int16_t* ocd;  // int16 columns relative to the chunk's first row, or NULL
-    const double* oav;
-    const int32_t* crow;  // chunk c = rows [crow[c], crow[c+1])
-    const double* s;      // D^-1/2
-    const int32_t* urp;   // unscaled A_uu (diagonal included), true residual
+    const int32_t* win_slice;  // SELL: first slice of each window
+    const int32_t* perm;       // 32 per slice: natural row or -1
+    const int32_t* len;        // per slice
+    const int32_t* base;       // per slice
+    const int32_t* cbase;      // per slice: window row0
+    const double* val;
+    const int16_t* c16;
+    const int32_t* c32;
+    const double* s;    // D^-1/2
+    const int32_t* urp;  // unscaled A_uu (diagonal included), true residual
     const int32_t* uci;
     const double* uav;
     const int32_t* krp;  // A_uk
@@ -62,11 +66,12 @@ struct RItem {
     double* part;       // [ncta][4] partial sums
     unsigned int* bar;  // [2] global barrier count / generation
     CgState* st;
-    int32_t n, m, cta0, ncta, nchunks, x0mode;
+    int32_t n, m, cta0, ncta, nwin, x0mode;
 };
 
 constexpr int RNT = 512;  // threads per CTA of the persistent solver
-constexpr int NCAP = kChunkNnzCap;
+constexpr int NWARP = RNT / 32;
+constexpr int SIG = kSellSigma;
 
 __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -149,7 +154,7 @@ __device__ __forceinline__ void group_sync(const RItem& it) {
 }
 
 // block sum of 4 values (fixed tree; result valid in every thread)
-__device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [RNT/32][4] */) {
+__device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [NWARP][4] */) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
@@ -168,7 +173,7 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [RNT/32][
     __syncthreads();
     double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
 #pragma unroll
-    for (int w = 0; w < RNT / 32; ++w) {
+    for (int w = 0; w < NWARP; ++w) {
         t.x += sh[4 * w];
         t.y += sh[4 * w + 1];
         t.z += sh[4 * w + 2];
@@ -201,48 +206,53 @@ __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, doubl
     return block_sum4(a, sh);
 }
 
-// w = A^ r over the CTA's chunks (CSR-stream); returns the partial (r.r, w.r, ||r/s||^2)
-__device__ __forceinline__ double4 spmv_w(const RItem& it, int c0, int c1, double* __restrict__ prod) {
+// SELL SpMV over the CTA's slices [S0, S1), y = src + A^_off src for each row.
+// KIND 0: w = y, partial (r.r, w.r, ||r/s||^2) with src = r.
+// KIND 1: r = s b - y (initial residual), partial (b.b) with src = x^0.
+template <int KIND>
+__device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, const double* __restrict__ src) {
     double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
-    const int32_t* __restrict__ orp = it.orp;
-    const double* __restrict__ oav = it.oav;
-    const double* __restrict__ r = it.r;
-    const int tid = threadIdx.x;
-    for (int c = c0; c < c1; ++c) {
-        const int rb = it.crow[c], re = it.crow[c + 1];
-        const int e0 = orp[rb], e1 = orp[re];
-        const int i = rb + tid;
-        int a = 0, b = 0;
-        double ri = 0.0, si = 1.0;
-        if (i < re) {
-            a = orp[i];
-            b = orp[i + 1];
-            ri = __ldcg(r + i);
-            si = it.s[i];
-        }
-        double acc = ri;
-        if (e1 - e0 <= NCAP) {
-            if (it.ocd) {
-                const int16_t* __restrict__ cd = it.ocd;
-#pragma unroll 4
-                for (int e = e0 + tid; e < e1; e += RNT) prod[e - e0] = oav[e] * __ldcg(r + rb + cd[e]);
-            } else {
-                const int32_t* __restrict__ ci = it.oci;
-#pragma unroll 4
-                for (int e = e0 + tid; e < e1; e += RNT) prod[e - e0] = oav[e] * __ldcg(r + ci[e]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* __restrict__ val = it.val;
+    for (int s = S0 + warp; s < S1; s += NWARP) {
+        const int row = it.perm[32 * s + lane];
+        const int len = it.len[s];
+        const int base = it.base[s] + lane;
+        const int cb = it.cbase[s];
+        const int rr = row >= 0 ? row : cb;
+        const double xi = __ldcg(src + rr);
+        const double si = it.s[rr];
+        double acc = 0.0;
+        for (int k0 = 0; k0 < len; k0 += 4) {
+            double v[4];
+            int c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = base + 32 * (k0 + q);
+                if (k0 + q < len) {
+                    v[q] = val[e];
+                    c[q] = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
+                } else {
+                    v[q] = 0.0;
+                    c[q] = rr;
+                }
             }
-            __syncthreads();
-            for (int e = a; e < b; ++e) acc += prod[e - e0];
-            __syncthreads();
-        } else {  // a row longer than the staging buffer: direct gathers
-            for (int e = a; e < b; ++e) acc = fma(oav[e], __ldcg(r + it.oci[e]), acc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc = fma(v[q], __ldcg(src + c[q]), acc);
         }
-        if (i < re) {
-            it.w[i] = acc;
-            const double ru = ri / si;
-            loc.x += ri * ri;
-            loc.y += acc * ri;
-            loc.z += ru * ru;
+        if (row >= 0) {
+            const double y = xi + acc;
+            if constexpr (KIND == 0) {
+                it.w[row] = y;
+                const double ru = xi / si;
+                loc.x += xi * xi;
+                loc.y += y * xi;
+                loc.z += ru * ru;
+            } else {
+                const double bi = it.b[row];
+                it.r[row] = si * bi - y;
+                loc.x += bi * bi;
+            }
         }
     }
     return loc;
@@ -251,9 +261,8 @@ __device__ __forceinline__ double4 spmv_w(const RItem& it, int c0, int c1, doubl
 template <int MODE>
 __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
     k_pcg_resident(const RItem* __restrict__ items, int nitems, int vrows, int nvec) {
-    extern __shared__ double smem[];  // prod[NCAP] | p[vrows] | s[vrows] | x[vrows]
-    __shared__ double sh[4 * (RNT / 32)];
-    double* prod = smem;
+    extern __shared__ double smem[];  // p[vrows] | s[vrows] | x[vrows]
+    __shared__ double sh[4 * NWARP];
     // ---- which item / rank
     int item = 0, rank = 0;
     if constexpr (MODE == 1) {
@@ -271,36 +280,28 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
     }
     const RItem& it = items[item];
     CgState* S = it.st;
-    const int c0 = (int)((long long)it.nchunks * rank / it.ncta);
-    const int c1 = (int)((long long)it.nchunks * (rank + 1) / it.ncta);
-    const int R0 = it.crow[c0], R1 = it.crow[c1];
-    double* P = nvec >= 2 ? smem + NCAP : it.p + R0;
-    double* SV = nvec >= 2 ? smem + NCAP + vrows : it.sv + R0;
-    double* X = nvec >= 3 ? smem + NCAP + 2 * vrows : it.x + R0;
+    const int W0 = (int)((long long)it.nwin * rank / it.ncta);
+    const int W1 = (int)((long long)it.nwin * (rank + 1) / it.ncta);
+    const int R0 = min(it.n, W0 * SIG), R1 = min(it.n, W1 * SIG);
+    const int S0 = it.win_slice[W0], S1 = it.win_slice[W1];
+    double* P = nvec >= 2 ? smem : it.p + R0;
+    double* SV = nvec >= 2 ? smem + vrows : it.sv + R0;
+    double* X = nvec >= 3 ? smem + 2 * vrows : it.x + R0;
     const double rtol = S->rtol;
     const int max_iter = S->max_iter;
     double x0v = 0.0;
     if (it.x0mode == 1) x0v = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
     const int tid = threadIdx.x;
 
-    // ---- init: x^0 (global, gathered by the first residual), r0, ||b||^2
+    // ---- init: x^0 (global, gathered by the first residual), r0 = s b - A^ x0, ||b||^2
     for (int i = R0 + tid; i < R1; i += RNT) {
         double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[i] : 0.0);
-        it.x[i] = x0 / it.s[i];
+        const double xh = x0 / it.s[i];
+        it.x[i] = xh;
+        if (nvec >= 3) X[i - R0] = xh;
     }
     group_sync<MODE>(it);
-    double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int i = R0 + tid; i < R1; i += RNT) {
-        const double si = it.s[i];
-        const double xi = __ldcg(it.x + i);
-        double ax = xi;
-        for (int e = it.orp[i]; e < it.orp[i + 1]; ++e) ax = fma(it.oav[e], __ldcg(it.x + it.oci[e]), ax);
-        const double bi = it.b[i];
-        it.r[i] = si * bi - ax;
-        if (nvec >= 3) X[i - R0] = xi;
-        loc.x += bi * bi;
-    }
-    double4 tot = group_reduce<MODE>(it, rank, loc, sh);
+    double4 tot = group_reduce<MODE>(it, rank, spmv_sell<1>(it, S0, S1, it.x), sh);
     const double bn2 = tot.x;
     const double tol2 = rtol * rtol * bn2;
     int iters = 0, status = FEMI_OK, restarts = 0;
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
             SV[i - R0] = 0.0;
         }
         group_sync<MODE>(it);  // r visible, partials consumed
-        tot = group_reduce<MODE>(it, rank, spmv_w(it, c0, c1, prod), sh);
+        tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh);
         double gam = tot.x, del = tot.y, rho = tot.z;
         double alpha = 0.0, beta = 0.0;
         bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho);
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
             }
             ++iters;
             group_sync<MODE>(it);  // r published
-            tot = group_reduce<MODE>(it, rank, spmv_w(it, c0, c1, prod), sh);
+            tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh);
             const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 status = FEMI_E_NONFINITE;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
         }
         group_sync<MODE>(it);  // u_vert visible
         // true residual with the unscaled matrix; keeps s_i * r_true in r for a restart
-        loc = make_double4(0.0, 0.0, 0.0, 0.0);
+        double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
         for (int i = R0 + tid; i < R1; i += RNT) {
             double ax = 0.0;
             for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], __ldcg(it.u_vert + it.uci[e]), ax);
@@ -428,19 +429,6 @@ int g_smem_optin = -1;
 int g_occ_grid = -1;
 int g_nsm = 0;
 
-// rows of the largest CTA range for an item split into ncta CTAs
-int64_t max_cta_rows(const femi_system_s* s, int ncta) {
-    int64_t mx = 0;
-    const int nc = s->nchunks;
-    for (int k = 0; k < ncta; ++k) {
-        const int a = (int)((long long)nc * k / ncta), b = (int)((long long)nc * (k + 1) / ncta);
-        const int r0 = a < nc ? s->chunks_h[a].row0 : (int)s->n_u;
-        const int r1 = b < nc ? s->chunks_h[b].row0 : (int)s->n_u;
-        mx = std::max<int64_t>(mx, r1 - r0);
-    }
-    return mx;
-}
-
 }  // namespace
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
@@ -472,7 +460,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     int mode, ncta_item = 1;
     if (B == 1 && S[0]->nnz_uu > 600000) {
         mode = 2;
-        ncta_item = std::max(1, std::min(g_occ_grid, S[0]->nchunks));
+        ncta_item = std::max(1, std::min(g_occ_grid, S[0]->nwin));
     } else {
         ncta_item = (int)std::min<int64_t>(16, std::max<int64_t>(1, (nnz_max + 23999) / 24000));
         int c = 1;
@@ -483,12 +471,18 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     const int grid = B * ncta_item;
     // shared-memory residency of p, s (and x): as many vectors as fit the per-CTA budget
     int64_t vrows = 0;
-    for (int b = 0; b < B; ++b) vrows = std::max(vrows, max_cta_rows(S[b], ncta_item));
+    for (int b = 0; b < B; ++b) {
+        const int nw = S[b]->nwin;
+        for (int k = 0; k < ncta_item; ++k) {
+            const int64_t w0 = (int64_t)nw * k / ncta_item, w1 = (int64_t)nw * (k + 1) / ncta_item;
+            vrows = std::max(vrows, std::min(S[b]->n_u, w1 * SIG) - std::min(S[b]->n_u, w0 * SIG));
+        }
+    }
     const size_t budget = (size_t)(mode == 2 ? g_smem_optin / 2 - 2048 : g_smem_optin - 2048);
     int nvec = 3;
-    while (nvec >= 2 && sizeof(double) * (NCAP + nvec * (size_t)vrows) > budget) --nvec;
+    while (nvec >= 2 && sizeof(double) * (nvec * (size_t)vrows) > budget) --nvec;
     if (nvec < 2) nvec = 0;
-    const size_t smem_bytes = sizeof(double) * (NCAP + (size_t)nvec * vrows);
+    const size_t smem_bytes = sizeof(double) * ((size_t)nvec * vrows);
 
     // ---- workspace: per item b, x, r, w, b (+ p, s) vectors, partials, barrier, state
     std::vector<RItem> items(B);
@@ -512,11 +506,14 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         femi_system_s* s = S[b];
         RItem& it = items[b];
         const size_t vb = sizeof(double) * (s->n_u + 1);
-        it.orp = s->o_rowptr;
-        it.oci = s->o_col;
-        it.ocd = s->o_cd;
-        it.oav = s->o_val;
-        it.crow = s->chunk_row0;
+        it.win_slice = s->win_slice;
+        it.perm = s->sell_perm;
+        it.len = s->sell_len;
+        it.base = s->sell_base;
+        it.cbase = s->sell_cbase;
+        it.val = s->sell_val;
+        it.c16 = s->sell_c16;
+        it.c32 = s->sell_c32;
         it.s = s->s;
         it.urp = s->uu_rowptr;
         it.uci = s->uu_col;
@@ -540,7 +537,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.m = (int32_t)s->m;
         it.cta0 = b * ncta_item;
         it.ncta = ncta_item;
-        it.nchunks = s->nchunks;
+        it.nwin = s->nwin;
         it.x0mode = (it.g == nullptr && o.x0 == 1) ? 0 : o.x0;
     }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));

@@ -2,14 +2,14 @@
 // (PAPER.md:L239-241 interpolation; L262-265 "e_i = (u_i - f_i)^2", "total L2 error in
 // each triangle"), and the adjoint raster P^T r used by tonal optimisation (S6).
 //
-// Triangle-parallel with load-balanced expansion (raster_common.cuh): a pixel is
+// Triangle-parallel with warp-cooperative expansion (raster_common.cuh): a pixel is
 // processed by the triangle that owns it (reading A7: lowest index among the closed
 // triangles containing it), decided locally from the edge functions and precomputed
 // ownership flags -- no owner map, no atomics. A vertex pixel takes its vertex value
 // exactly; otherwise u = u_a + l_b (u_b - u_a) + l_c (u_c - u_a), l = exact integer edge
 // function / 2*area (S3). Per-triangle error sums and arg-max (ties: lowest pix) are
-// sequential per triangle in pixel order; SSE is a per-CTA partial summed in fixed order
-// by the last CTA: deterministic.
+// segmented warp scans in pixel order; SSE is a per-CTA partial summed in fixed order by
+// the last CTA: deterministic.
 #include "raster_common.cuh"
 
 namespace femi {
@@ -29,91 +29,112 @@ struct RasterItem {
     int32_t pad;
 };
 
-__global__ void __launch_bounds__(RB, 3) k_raster_error(const RasterItem* __restrict__ items, double* __restrict__ part,
-                                                        uint32_t* __restrict__ counters) {
-    __shared__ TriInfo info[RB];
-    __shared__ double tu[RB][3];
-    __shared__ int off[RB + 1];
-    __shared__ int wsum[RB / 32];
-    __shared__ double es[RCAP];
-    __shared__ unsigned char cs[RCAP];
-    __shared__ double red[RB / 32];
+__global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restrict__ items, double* __restrict__ part,
+                                                     uint32_t* __restrict__ counters) {
+    __shared__ WTri tris[RWARPS][32];
+    __shared__ double tuv[RWARPS][32][3];
+    __shared__ double acc_s[RWARPS][32];
+    __shared__ double be_s[RWARPS][32];
+    __shared__ int bp_s[RWARPS][32];
+    __shared__ double red[RWARPS];
     __shared__ int flag;
     const RasterItem it = items[blockIdx.y];
-    const int tid = threadIdx.x;
-    const int64_t t0 = (int64_t)blockIdx.x * RB;
-    double acc = 0.0, be = -1.0;
-    int bp = -1, cnt = 0;
-    if (t0 < it.T) {
-        cnt = load_tris(it.tri, it.T, t0, info, off, wsum);
-        if (tid < cnt) {
-            const TriRec& R = it.tri[t0 + tid];
-            tu[tid][0] = it.u_vert[R.v[0]];
-            tu[tid][1] = it.u_vert[R.v[1]];
-            tu[tid][2] = it.u_vert[R.v[2]];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ngroups = (it.T + 31) / 32;
+    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    const bool with_f = it.f != nullptr;
+    WTri* ws = tris[wid];
+    double sse_loc = 0.0;
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+        const int64_t t0 = g * 32;
+        int excl, total;
+        TriRec R;
+        const int nbox = warp_load_tris(it.tri, it.T, t0, ws, excl, total, R);
+        if (nbox) {
+            tuv[wid][lane][0] = it.u_vert[R.v[0]];
+            tuv[wid][lane][1] = it.u_vert[R.v[1]];
+            tuv[wid][lane][2] = it.u_vert[R.v[2]];
         }
-        __syncthreads();
-        const int total = off[cnt];
-        const bool with_f = it.f != nullptr;
-        int j = 0;
-        for (int r0 = 0; r0 < total; r0 += RCAP) {
-            const int rend = min(total, r0 + RCAP);
-            for (int k = r0 + tid; k < rend; k += RB) {
-                while (off[j + 1] <= k) ++j;
-                const TriInfo& I = info[j];
-                const int loc = k - off[j];
+        acc_s[wid][lane] = 0.0;
+        be_s[wid][lane] = -1.0;
+        bp_s[wid][lane] = -1;
+        __syncwarp();
+        for (int base = 0; base < total; base += 32) {
+            const int k = base + lane;
+            const int j = warp_find(excl, k, total);
+            const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
+            double val = 0.0, ce = -1.0;
+            int cp = 0x7fffffff;
+            if (j < 32) {
+                const WTri& I = ws[j];
+                const int loc = k - exj;
                 const int ry = loc / I.bw;
                 const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
                 int w0, w1, w2, kv = 0;
                 const int cls = classify(I, px, py, w0, w1, w2, kv);
-                cs[k - r0] = (unsigned char)cls;
-                if (!cls) continue;
-                double u;
-                if (cls == 2) {
-                    u = tu[j][kv];
-                } else {
-                    const double D = (double)I.D, ua = tu[j][0];
-                    u = ua + (w1 / D) * (tu[j][1] - ua) + (w2 / D) * (tu[j][2] - ua);
-                }
-                const int64_t pix = (int64_t)py * it.W + px;
-                if (it.u_px) it.u_px[pix] = u;
-                if (with_f) {
-                    const double d = u - it.f[pix];
-                    const double e = d * d;
-                    es[k - r0] = e;
-                    if (it.e_px) it.e_px[pix] = e;
-                }
-            }
-            __syncthreads();
-            if (with_f && tid < cnt) {
-                const int lo = max(off[tid], r0), hi = min(off[tid + 1], rend);
-                for (int k = lo; k < hi; ++k) {
-                    const int cls = cs[k - r0];
-                    if (!cls) continue;
-                    const double e = es[k - r0];
-                    acc += e;
-                    if (cls == 1 && e > be) {
-                        be = e;
-                        const TriInfo& I = info[tid];
-                        const int loc = k - off[tid];
-                        const int ry = loc / I.bw;
-                        bp = (I.y0 + ry) * it.W + I.x0 + loc - ry * I.bw;
+                if (cls) {
+                    double u;
+                    if (cls == 2) {
+                        u = tuv[wid][j][kv];
+                    } else {
+                        const double D = (double)I.D, ua = tuv[wid][j][0];
+                        u = ua + (w1 / D) * (tuv[wid][j][1] - ua) + (w2 / D) * (tuv[wid][j][2] - ua);
+                    }
+                    const int64_t pix = (int64_t)py * it.W + px;
+                    if (it.u_px) it.u_px[pix] = u;
+                    if (with_f) {
+                        const double d = u - it.f[pix];
+                        const double e = d * d;
+                        if (it.e_px) it.e_px[pix] = e;
+                        val = e;
+                        if (cls == 1) {
+                            ce = e;
+                            cp = (int)pix;
+                        }
                     }
                 }
             }
-            __syncthreads();
+            if (!with_f) continue;
+            // segmented inclusive scan over runs of equal j: sum and (e desc, pix asc) arg-max
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double vo = __shfl_up_sync(0xffffffffu, val, o);
+                const double eo = __shfl_up_sync(0xffffffffu, ce, o);
+                const int po = __shfl_up_sync(0xffffffffu, cp, o);
+                const int jo = __shfl_up_sync(0xffffffffu, j, o);
+                if (lane >= o && jo == j) {
+                    val += vo;
+                    if (eo > ce || (eo == ce && po < cp)) {
+                        ce = eo;
+                        cp = po;
+                    }
+                }
+            }
+            const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+            if (j < 32 && (lane == 31 || jn != j)) {
+                acc_s[wid][j] += val;
+                if (ce > be_s[wid][j]) {  // earlier windows hold lower pixels: strict > keeps ties
+                    be_s[wid][j] = ce;
+                    bp_s[wid][j] = cp;
+                }
+            }
         }
-        if (with_f && tid < cnt) {
-            if (it.tri_err) it.tri_err[t0 + tid] = acc;
-            if (it.best) it.best[t0 + tid] = bp;
+        __syncwarp();
+        if (with_f && nbox) {
+            const double a = acc_s[wid][lane];
+            if (it.tri_err) it.tri_err[t0 + lane] = a;
+            if (it.best) it.best[t0 + lane] = be_s[wid][lane] >= 0.0 ? bp_s[wid][lane] : -1;
+            sse_loc += a;
         }
+        __syncwarp();
     }
-    if (!it.f || !it.sse) return;
-    const double tot = block_sum<RB>(tid < cnt ? acc : 0.0, red);
+    if (!with_f || !it.sse) return;
+    // SSE: fixed-order sums (lanes, warps, CTAs)
+    const double tot = block_sum<RT>(sse_loc, red);
     double* P = part + (size_t)blockIdx.y * gridDim.x;
-    if (tid == 0) P[blockIdx.x] = tot;
+    if (threadIdx.x == 0) P[blockIdx.x] = tot;
     __syncthreads();
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
         __threadfence();
         flag = (atomicAdd(&counters[blockIdx.y], 1u) == gridDim.x - 1);
     }
@@ -121,9 +142,9 @@ __global__ void __launch_bounds__(RB, 3) k_raster_error(const RasterItem* __rest
     if (flag) {
         __threadfence();
         double s = 0.0;
-        for (int k = tid; k < (int)gridDim.x; k += RB) s += __ldcg(&P[k]);
-        s = block_sum<RB>(s, red);
-        if (tid == 0) {
+        for (int k = threadIdx.x; k < (int)gridDim.x; k += RT) s += __ldcg(&P[k]);
+        s = block_sum<RT>(s, red);
+        if (threadIdx.x == 0) {
             *it.sse = s;
             counters[blockIdx.y] = 0;
         }
@@ -132,66 +153,82 @@ __global__ void __launch_bounds__(RB, 3) k_raster_error(const RasterItem* __rest
 
 // P^T r: per triangle, sum over its owned pixels of (l_a, l_b, l_c) r (vertex pixels:
 // weight 1 on that vertex) -> tri_w[3t+k]; the vertex gather happens in tonal.cu.
-__global__ void __launch_bounds__(RB, 3) k_adjoint_raster(const TriRec* __restrict__ tri, int64_t T, int W,
-                                                          const double* __restrict__ r, double* __restrict__ tri_w) {
-    __shared__ TriInfo info[RB];
-    __shared__ int off[RB + 1];
-    __shared__ int wsum[RB / 32];
-    __shared__ double rs[RCAP];
-    __shared__ unsigned char cs[RCAP];
-    const int tid = threadIdx.x;
-    const int64_t t0 = (int64_t)blockIdx.x * RB;
-    if (t0 >= T) return;
-    const int cnt = load_tris(tri, T, t0, info, off, wsum);
-    const int total = off[cnt];
-    double sa = 0.0, sb = 0.0, sc = 0.0;
-    int j = 0;
-    for (int r0 = 0; r0 < total; r0 += RCAP) {
-        const int rend = min(total, r0 + RCAP);
-        for (int k = r0 + tid; k < rend; k += RB) {
-            while (off[j + 1] <= k) ++j;
-            const TriInfo& I = info[j];
-            const int loc = k - off[j];
-            const int ry = loc / I.bw;
-            const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
-            int w0, w1, w2, kv = 0;
-            const int cls = classify(I, px, py, w0, w1, w2, kv);
-            cs[k - r0] = (unsigned char)(cls == 2 ? 2 + kv : cls);
-            if (cls) rs[k - r0] = r[(int64_t)py * W + px];
-        }
-        __syncthreads();
-        if (tid < cnt) {
-            const TriInfo& I = info[tid];
-            const double D = (double)I.D;
-            const int lo = max(off[tid], r0), hi = min(off[tid + 1], rend);
-            for (int k = lo; k < hi; ++k) {
-                const int c = cs[k - r0];
-                if (!c) continue;
-                const double rv = rs[k - r0];
-                if (c >= 2) {
-                    if (c == 2) sa += rv;
-                    else if (c == 3) sb += rv;
-                    else sc += rv;
-                    continue;
-                }
-                const int loc = k - off[tid];
+__global__ void __launch_bounds__(RT) k_adjoint_raster(const TriRec* __restrict__ tri, int64_t T, int W,
+                                                       const double* __restrict__ r, double* __restrict__ tri_w) {
+    __shared__ WTri tris[RWARPS][32];
+    __shared__ double acc_s[RWARPS][32][3];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ngroups = (T + 31) / 32;
+    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    WTri* ws = tris[wid];
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+        const int64_t t0 = g * 32;
+        int excl, total;
+        TriRec R;
+        const int nbox = warp_load_tris(tri, T, t0, ws, excl, total, R);
+        acc_s[wid][lane][0] = 0.0;
+        acc_s[wid][lane][1] = 0.0;
+        acc_s[wid][lane][2] = 0.0;
+        __syncwarp();
+        for (int base = 0; base < total; base += 32) {
+            const int k = base + lane;
+            const int j = warp_find(excl, k, total);
+            const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
+            double sa = 0.0, sb = 0.0, sc = 0.0;
+            if (j < 32) {
+                const WTri& I = ws[j];
+                const int loc = k - exj;
                 const int ry = loc / I.bw;
                 const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
-                const int w0 = orient_xy(I.bx, I.by, I.cx, I.cy, px, py);
-                const int w1 = orient_xy(I.cx, I.cy, I.ax, I.ay, px, py);
-                const int w2 = orient_xy(I.ax, I.ay, I.bx, I.by, px, py);
-                sa += (w0 / D) * rv;
-                sb += (w1 / D) * rv;
-                sc += (w2 / D) * rv;
+                int w0, w1, w2, kv = 0;
+                const int cls = classify(I, px, py, w0, w1, w2, kv);
+                if (cls) {
+                    const double rv = r[(int64_t)py * W + px];
+                    if (cls == 2) {
+                        if (kv == 0) sa = rv;
+                        else if (kv == 1) sb = rv;
+                        else sc = rv;
+                    } else {
+                        const double D = (double)I.D;
+                        sa = (w0 / D) * rv;
+                        sb = (w1 / D) * rv;
+                        sc = (w2 / D) * rv;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double ao = __shfl_up_sync(0xffffffffu, sa, o);
+                const double bo = __shfl_up_sync(0xffffffffu, sb, o);
+                const double co = __shfl_up_sync(0xffffffffu, sc, o);
+                const int jo = __shfl_up_sync(0xffffffffu, j, o);
+                if (lane >= o && jo == j) {
+                    sa += ao;
+                    sb += bo;
+                    sc += co;
+                }
+            }
+            const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+            if (j < 32 && (lane == 31 || jn != j)) {
+                acc_s[wid][j][0] += sa;
+                acc_s[wid][j][1] += sb;
+                acc_s[wid][j][2] += sc;
             }
         }
-        __syncthreads();
+        __syncwarp();
+        if (nbox) {
+            tri_w[3 * (t0 + lane)] = acc_s[wid][lane][0];
+            tri_w[3 * (t0 + lane) + 1] = acc_s[wid][lane][1];
+            tri_w[3 * (t0 + lane) + 2] = acc_s[wid][lane][2];
+        }
+        __syncwarp();
     }
-    if (tid < cnt) {
-        tri_w[3 * (t0 + tid)] = sa;
-        tri_w[3 * (t0 + tid) + 1] = sb;
-        tri_w[3 * (t0 + tid) + 2] = sc;
-    }
+}
+
+int raster_grid(int64_t T, int B) {
+    const int64_t groups = (T + 31) / 32;
+    const int64_t want = (groups + RWARPS - 1) / RWARPS;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)148 * 8 / std::max(1, B) + 1));
 }
 
 }  // namespace
@@ -216,7 +253,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
         r.W = S[b]->W;
         Tmax = std::max(Tmax, r.T);
     }
-    const int gx = (int)std::max<int64_t>(1, (Tmax + RB - 1) / RB);
+    const int gx = raster_grid(Tmax, B);
     const size_t bytes_items = sizeof(RasterItem) * B;
     const size_t bytes_part = sizeof(double) * (size_t)gx * B;
     const size_t bytes_cnt = sizeof(uint32_t) * B;
@@ -229,7 +266,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
     dim3 grid(gx, B);
-    k_raster_error<<<grid, RB, 0, st>>>(d_items, d_part, d_cnt);
+    k_raster_error<<<grid, RT, 0, st>>>(d_items, d_part, d_cnt);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
@@ -238,8 +275,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
 
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {
     if (S->T == 0) return FEMI_OK;
-    const int gx = (int)((S->T + RB - 1) / RB);
-    k_adjoint_raster<<<gx, RB, 0, st>>>(S->tri, S->T, S->W, r, tri_w);
+    k_adjoint_raster<<<raster_grid(S->T, 1), RT, 0, st>>>(S->tri, S->T, S->W, r, tri_w);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;
