@@ -21,10 +21,16 @@
 // cooperative grid (one huge system: C5). The stopping rule is the unscaled relative
 // residual ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a
 // failed confirmation restarts CG from the current iterate inside the launch (A11).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace femi {
 namespace {
@@ -148,9 +154,20 @@ __device__ __forceinline__ void group_sync(const RItem& it) {
         __syncthreads();
     } else if constexpr (MODE == 1) {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else if constexpr (MODE == 3) {
+        cg::this_grid().sync();
     } else {
         grid_barrier(it.bar, it.ncta);
     }
+}
+
+// optional phase timers (FEMI_PCG_TIMERS=1): rank-0 thread-0 %globaltimer deltas, ns
+__device__ unsigned long long g_pcg_timers[8];
+__device__ int g_pcg_timers_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 // block sum of 4 values (fixed tree; result valid in every thread)
@@ -259,7 +276,7 @@ __device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, co
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
+__global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
     k_pcg_resident(const RItem* __restrict__ items, int nitems, int vrows, int nvec) {
     extern __shared__ double smem[];  // p[vrows] | s[vrows] | x[vrows]
     __shared__ double sh[4 * NWARP];
@@ -328,6 +345,15 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
                 alpha = gam / del;
             }
         }
+        const bool tmr = g_pcg_timers_on && rank == 0 && tid == 0;
+        unsigned long long tl = tmr ? gtimer() : 0ull;
+        auto mark = [&](int k) {
+            if (tmr) {
+                const unsigned long long t = gtimer();
+                g_pcg_timers[k] += t - tl;
+                tl = t;
+            }
+        };
         while (run) {
             // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s (4 rows/thread in flight)
             for (int base = R0 + tid; base < R1; base += 4 * RNT) {
@@ -355,8 +381,13 @@ __global__ void __launch_bounds__(RNT, MODE == 2 ? 2 : 1)
                 }
             }
             ++iters;
+            mark(0);
             group_sync<MODE>(it);  // r published
-            tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh);
+            mark(1);
+            const double4 lsp = spmv_sell<0>(it, S0, S1, it.r);
+            mark(2);
+            tot = group_reduce<MODE>(it, rank, lsp, sh);
+            mark(3);
             const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 status = FEMI_E_NONFINITE;
@@ -428,6 +459,8 @@ struct Workspace {
 int g_smem_optin = -1;
 int g_occ_grid = -1;
 int g_nsm = 0;
+bool g_timers = false;
+bool g_cg_barrier = false;
 
 }  // namespace
 
@@ -446,6 +479,12 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        g_smem_optin / 2 - 2048));
+        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       g_smem_optin / 2 - 2048));
+        const char* tm = std::getenv("FEMI_PCG_TIMERS");
+        g_timers = tm && tm[0] == '1';
+        const char* gb = std::getenv("FEMI_GRID_BARRIER");
+        g_cg_barrier = gb && std::string(gb) == "cg";
         int per_sm = 0;
         FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
                                                                 g_smem_optin / 2 - 2048));
@@ -570,11 +609,20 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         cfg.numAttrs = 0;
         const int vr = (int)vrows;
         cudaError_t e;
+        if (g_timers) {
+            unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int on = 1;
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        }
         if (mode == 2) {
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
             cfg.numAttrs = 1;
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
+            if (g_cg_barrier)
+                e = cudaLaunchKernelEx(&cfg, k_pcg_resident<3>, (const RItem*)d_items, B, vr, nvec);
+            else
+                e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
         } else if (mode == 1) {
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = ncta_item;
@@ -599,6 +647,16 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     std::vector<CgState> hs(B);
     FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
     FEMI_CUDA(cudaStreamSynchronize(st));
+    if (g_timers && nmax > 0) {
+        unsigned long long t[8];
+        FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
+        const double it_n = std::max(1, hs[0].iters);
+        std::fprintf(stderr,
+                     "[femi pcg timers] mode %d ctas %d nvec %d iters %d | per iter us: U %.2f sync %.2f spmv %.2f "
+                     "reduce %.2f\n",
+                     mode, grid, nvec, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3,
+                     t[3] / it_n / 1e3);
+    }
     femi_status ret = FEMI_OK;
     int64_t tot = 0;
     for (int b = 0; b < B; ++b) {
