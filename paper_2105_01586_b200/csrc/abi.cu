@@ -262,71 +262,74 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         if (fits && !cd.empty()) U(upload(S, &S->o_cd, cd, st));
     }
     {
-        // SELL-32-sigma layout of the off-diagonal pattern (values filled on the device)
+        // Solver numbering + SELL-32-sigma layout of the off-diagonal pattern (values are
+        // filled on the device after assembly). Internal order: unknowns sorted by
+        // (y / kBand, x, y) -- 32 consecutive internal rows form a compact 2-D blob, so
+        // row data is contiguous and gathered neighbours sit in few cache lines -- then
+        // rows sorted by length (descending, stable) inside windows of kSellSigma.
         const int64_t n = M.n_u;
         const int SIG = kSellSigma;
         S->nwin = (int32_t)((n + SIG - 1) / SIG);
-        std::vector<int32_t> win_slice(S->nwin + 1, 0), perm, len, base, src;
-        std::vector<int32_t> c32;
+        auto rl = [&](int32_t i) { return M.uu_rowptr[i + 1] - M.uu_rowptr[i] - 1; };
+        std::vector<int32_t> pi(n), pos(n);
+        {
+            std::vector<std::pair<uint64_t, int32_t>> key(n);
+            for (int64_t i = 0; i < n; ++i) {
+                const uint64_t x = (uint64_t)(M.vpix[i] % M.W), y = (uint64_t)(M.vpix[i] / M.W);
+                key[i] = {((y / kBand) << 40) | (x << 20) | y, (int32_t)i};
+            }
+            std::sort(key.begin(), key.end());
+            for (int64_t i = 0; i < n; ++i) pi[i] = key[i].second;
+        }
+        for (int64_t w0 = 0; w0 < n; w0 += SIG)
+            std::stable_sort(pi.begin() + w0, pi.begin() + std::min<int64_t>(n, w0 + SIG),
+                             [&](int32_t a, int32_t b) { return rl(a) > rl(b); });
+        for (int64_t i = 0; i < n; ++i) pos[pi[i]] = (int32_t)i;
+        const int32_t nsl = (int32_t)((n + 31) / 32);
+        std::vector<int32_t> len(nsl), base(nsl), src, c32;
         std::vector<int16_t> c16;
         bool fits16 = true;
-        std::vector<int32_t> order;
         int64_t ent = 0;
-        for (int32_t w = 0; w < S->nwin; ++w) {
-            const int32_t r0 = w * SIG, r1 = (int32_t)std::min<int64_t>(n, (int64_t)(w + 1) * SIG);
-            order.resize(r1 - r0);
-            for (int32_t i = r0; i < r1; ++i) order[i - r0] = i;
-            auto rl = [&](int32_t i) { return M.uu_rowptr[i + 1] - M.uu_rowptr[i] - 1; };
-            std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return rl(a) > rl(b); });
-            win_slice[w] = (int32_t)len.size();
-            for (size_t s0 = 0; s0 < order.size(); s0 += 32) {
-                int32_t L = 0;
-                for (size_t l = s0; l < std::min(order.size(), s0 + 32); ++l) L = std::max(L, rl(order[l]));
-                len.push_back(L);
-                base.push_back((int32_t)ent);
-                for (int l = 0; l < 32; ++l) perm.push_back(s0 + l < order.size() ? order[s0 + l] : -1);
-                for (int32_t k = 0; k < L; ++k)
-                    for (int l = 0; l < 32; ++l) {
-                        int32_t row = s0 + l < order.size() ? order[s0 + l] : r0;
-                        int32_t col = row, sidx = -1;
-                        if (s0 + l < order.size() && k < rl(row)) {
-                            // k-th off-diagonal entry of row (CSR order, diagonal skipped)
-                            int32_t e = M.uu_rowptr[row], q = 0;
-                            for (; e < M.uu_rowptr[row + 1]; ++e) {
-                                if (M.uu_col[e] == row) continue;
-                                if (q == k) break;
-                                ++q;
-                            }
-                            col = M.uu_col[e];
-                            sidx = (M.uu_rowptr[row] - row) + k;  // index into o_val
+        for (int32_t s = 0; s < nsl; ++s) {
+            int32_t L = 0;
+            for (int l = 0; l < 32 && 32 * s + l < n; ++l) L = std::max(L, rl(pi[32 * s + l]));
+            len[s] = L;
+            base[s] = (int32_t)ent;
+            const int32_t wbase = (32 * s / SIG) * SIG;
+            for (int32_t k = 0; k < L; ++k)
+                for (int l = 0; l < 32; ++l) {
+                    const int64_t ri = 32 * (int64_t)s + l;
+                    int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
+                    if (ri < n && k < rl(pi[ri])) {
+                        const int32_t row = pi[ri];
+                        int32_t e = M.uu_rowptr[row], q = 0;  // k-th off-diagonal entry of row
+                        for (; e < M.uu_rowptr[row + 1]; ++e) {
+                            if (M.uu_col[e] == row) continue;
+                            if (q == k) break;
+                            ++q;
                         }
-                        src.push_back(sidx);
-                        c32.push_back(col);
-                        const int32_t d = col - r0;
-                        if (d < -32768 || d > 32767) fits16 = false;
-                        ++ent;
+                        col = pos[M.uu_col[e]];
+                        sidx = (M.uu_rowptr[row] - row) + k;  // index into o_val (natural CSR)
                     }
-            }
+                    src.push_back(sidx);
+                    c32.push_back(col);
+                    const int32_t d = col - wbase;
+                    if (d < -32768 || d > 32767) fits16 = false;
+                    ++ent;
+                }
         }
-        win_slice[S->nwin] = (int32_t)len.size();
-        S->nslices = (int32_t)len.size();
-        std::vector<int32_t> cbase(len.size());
-        for (int32_t w = 0; w < S->nwin; ++w)
-            for (int32_t s = win_slice[w]; s < win_slice[w + 1]; ++s) cbase[s] = w * SIG;
-        U(upload(S, &S->sell_cbase, cbase, st));
+        S->nslices = nsl;
         S->sell_nnz = ent;
-        U(upload(S, &S->win_slice, win_slice, st));
-        U(upload(S, &S->sell_perm, perm, st));
         U(upload(S, &S->sell_len, len, st));
         U(upload(S, &S->sell_base, base, st));
-        U(alloc(S, &S->sell_val, (size_t)ent));
+        U(upload(S, &S->sell_inv, pi, st));
+        U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
+        U(alloc(S, &S->s_int, (size_t)std::max<int64_t>(n, 1)));
         if (fits16) {
             c16.resize(c32.size());
-            size_t q = 0;  // column relative to the window's first row
-            for (int32_t w = 0; w < S->nwin; ++w) {
-                const int32_t r0 = w * SIG;
-                for (int32_t s = win_slice[w]; s < win_slice[w + 1]; ++s)
-                    for (int32_t k = 0; k < len[s] * 32; ++k, ++q) c16[q] = (int16_t)(c32[q] - r0);
+            for (int32_t s = 0, q = 0; s < nsl; ++s) {
+                const int32_t wbase = (32 * s / SIG) * SIG;
+                for (int32_t k = 0; k < len[s] * 32; ++k, ++q) c16[q] = (int16_t)(c32[q] - wbase);
             }
             U(upload(S, &S->sell_c16, c16, st));
         } else {

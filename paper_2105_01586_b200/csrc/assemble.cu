@@ -104,12 +104,23 @@ __global__ void k_sell_values(int64_t ne, const int32_t* __restrict__ src, const
     }
 }
 
+__global__ void k_gather_s(int64_t n, const int32_t* __restrict__ inv, const double* __restrict__ s,
+                           double* __restrict__ s_int) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s_int[i] = s[inv[i]];
+}
+
 }  // namespace
 
 femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st) {
-    if (S->sell_nnz == 0) return FEMI_OK;
-    int g = (int)std::min<int64_t>((S->sell_nnz + 255) / 256, 148 * 16);
-    k_sell_values<<<g, 256, 0, st>>>(S->sell_nnz, d_src, S->o_val, S->sell_val);
+    if (S->n_u == 0) return FEMI_OK;
+    if (S->sell_nnz > 0) {
+        int g = (int)std::min<int64_t>((S->sell_nnz + 255) / 256, 148 * 16);
+        k_sell_values<<<g, 256, 0, st>>>(S->sell_nnz, d_src, S->o_val, S->sell_val);
+        count_launches(1);
+    }
+    int g = (int)std::min<int64_t>((S->n_u + 255) / 256, 148 * 16);
+    k_gather_s<<<g, 256, 0, st>>>(S->n_u, S->sell_inv, S->s, S->s_int);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;

@@ -112,6 +112,8 @@ struct femi_system_s {
     int32_t* sell_c32 = nullptr;   // absolute column otherwise
     int64_t sell_nnz = 0;
     int32_t* sell_src_tmp = nullptr;  // assembly-time map SELL entry -> o_val index
+    int32_t* sell_inv = nullptr;      // n_u: internal solver row -> canonical unknown index
+    double* s_int = nullptr;          // D^-1/2 in internal order
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -132,7 +134,8 @@ femi_status cuda_fail(cudaError_t e, const char* what);
 void count_launches(int64_t n);
 
 constexpr int kRowsPerChunk = 512;
-constexpr int kSellSigma = 512;  // rows per SELL window (sorting scope)
+constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)
+constexpr int kBand = 32;        // image band height (pixels) of the internal solver order
 femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st);
 constexpr int kChunkNnzCap = 2048;
 

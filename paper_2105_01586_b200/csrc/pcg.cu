@@ -44,16 +44,17 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double((long long)b);
 }
 
+// All solver vectors (b, x, r, w, p, s) live in the INTERNAL row order (see abi.cu:
+// 2-D blocked numbering, length-sorted inside kSellSigma windows); inv maps an internal
+// row to its canonical unknown index for the input/output vectors (g, u_vert).
 struct RItem {
-    const int32_t* win_slice;  // SELL: first slice of each window
-    const int32_t* perm;       // 32 per slice: natural row or -1
-    const int32_t* len;        // per slice
-    const int32_t* base;       // per slice
-    const int32_t* cbase;      // per slice: window row0
+    const int32_t* inv;   // internal row -> canonical unknown
+    const int32_t* len;   // per 32-row slice
+    const int32_t* base;  // per slice: first SELL entry
     const double* val;
-    const int16_t* c16;
+    const int16_t* c16;   // column - window base (internal numbering)
     const int32_t* c32;
-    const double* s;    // D^-1/2
+    const double* s;    // D^-1/2 (internal order)
     const int32_t* urp;  // unscaled A_uu (diagonal included), true residual
     const int32_t* uci;
     const double* uav;
@@ -111,16 +112,17 @@ __global__ void k_minmax(int B, const RItem* __restrict__ items) {
     }
 }
 
-// b = -A_uk g (ascending mask index, reading A6 order), or the given b
+// b = -A_uk g (ascending mask index, reading A6 order), or the given b; stored in internal order
 __global__ void k_rhs(int B, const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        const int nat = it.inv[i];
         double bi;
         if (it.bin) {
-            bi = it.bin[i];
+            bi = it.bin[nat];
         } else {
             double acc = 0.0;
-            for (int e = it.krp[i]; e < it.krp[i + 1]; ++e) acc = acc + it.kav[e] * it.g[it.kci[e]];
+            for (int e = it.krp[nat]; e < it.krp[nat + 1]; ++e) acc = acc + it.kav[e] * it.g[it.kci[e]];
             bi = -acc;
         }
         it.b[i] = bi;
@@ -232,12 +234,12 @@ __device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, co
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* __restrict__ val = it.val;
     for (int s = S0 + warp; s < S1; s += NWARP) {
-        const int row = it.perm[32 * s + lane];
+        const int row = 32 * s + lane < it.n ? 32 * s + lane : -1;  // internal numbering
         const int len = it.len[s];
         const int base = it.base[s] + lane;
-        const int cb = it.cbase[s];
-        const int rr = row >= 0 ? row : cb;
-        const double xi = __ldcg(src + rr);
+        const int cb = (32 * s / SIG) * SIG;
+        const int rr = row >= 0 ? row : 32 * s;
+        const double xi = __ldca(src + rr);
         const double si = it.s[rr];
         double acc = 0.0;
         for (int k0 = 0; k0 < len; k0 += 4) {
@@ -255,7 +257,7 @@ __device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, co
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc = fma(v[q], __ldcg(src + c[q]), acc);
+            for (int q = 0; q < 4; ++q) acc = fma(v[q], __ldca(src + c[q]), acc);
         }
         if (row >= 0) {
             const double y = xi + acc;
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
     const int W0 = (int)((long long)it.nwin * rank / it.ncta);
     const int W1 = (int)((long long)it.nwin * (rank + 1) / it.ncta);
     const int R0 = min(it.n, W0 * SIG), R1 = min(it.n, W1 * SIG);
-    const int S0 = it.win_slice[W0], S1 = it.win_slice[W1];
+    const int S0 = R0 / 32, S1 = (R1 + 31) / 32;
     double* P = nvec >= 2 ? smem : it.p + R0;
     double* SV = nvec >= 2 ? smem + vrows : it.sv + R0;
     double* X = nvec >= 3 ? smem + 2 * vrows : it.x + R0;
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
 
     // ---- init: x^0 (global, gathered by the first residual), r0 = s b - A^ x0, ||b||^2
     for (int i = R0 + tid; i < R1; i += RNT) {
-        double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[i] : 0.0);
+        double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[it.inv[i]] : 0.0);
         const double xh = x0 / it.s[i];
         it.x[i] = xh;
         if (nvec >= 3) X[i - R0] = xh;
@@ -362,8 +364,8 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
                 for (int q = 0; q < 4; ++q) {
                     const int i = base + q * RNT;
                     if (i < R1) {
-                        rv[q] = __ldcg(it.r + i);
-                        wv[q] = __ldcg(it.w + i);
+                        rv[q] = __ldca(it.r + i);
+                        wv[q] = __ldca(it.w + i);
                     }
                 }
 #pragma unroll
@@ -409,18 +411,22 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
         }
         // ---- finalize: x = D^-1/2 x^ (or x0 untouched at 0 iterations, 0 when b == 0)
         for (int i = R0 + tid; i < R1; i += RNT) {
+            const int nat = it.inv[i];
+            if (iters == 0 && it.x0mode == 2 && bn2 != 0.0) continue;  // caller's guess stays
             double xi;
             if (bn2 == 0.0) xi = 0.0;
-            else if (iters == 0) xi = (it.x0mode == 2) ? it.u_vert[i] : x0v;
+            else if (iters == 0) xi = x0v;
             else xi = it.s[i] * X[i - R0];
-            it.u_vert[i] = xi;
+            it.u_vert[nat] = xi;
         }
         group_sync<MODE>(it);  // u_vert visible
-        // true residual with the unscaled matrix; keeps s_i * r_true in r for a restart
+        // true residual with the unscaled matrix (canonical rows); keeps s_i * r_true in r
         double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
         for (int i = R0 + tid; i < R1; i += RNT) {
+            const int nat = it.inv[i];
             double ax = 0.0;
-            for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], __ldcg(it.u_vert + it.uci[e]), ax);
+            for (int e = it.urp[nat]; e < it.urp[nat + 1]; ++e)
+                ax = fma(it.uav[e], __ldca(it.u_vert + it.uci[e]), ax);
             const double ri = it.b[i] - ax;
             it.r[i] = it.s[i] * ri;
             loc.x += ri * ri;
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
         const bool fail = bn2 > 0.0 && !(res2 <= tol2);
         if (!(status == FEMI_OK && iters > 0 && fail && iters < max_iter && restarts < 8)) break;
         ++restarts;
-        for (int i = R0 + tid; i < R1; i += RNT) X[i - R0] = it.u_vert[i] / it.s[i];
+        for (int i = R0 + tid; i < R1; i += RNT) X[i - R0] = it.u_vert[it.inv[i]] / it.s[i];
     }
     if (rank == 0 && tid == 0) {
         S->iters = iters;
@@ -545,15 +551,13 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         femi_system_s* s = S[b];
         RItem& it = items[b];
         const size_t vb = sizeof(double) * (s->n_u + 1);
-        it.win_slice = s->win_slice;
-        it.perm = s->sell_perm;
+        it.inv = s->sell_inv;
         it.len = s->sell_len;
         it.base = s->sell_base;
-        it.cbase = s->sell_cbase;
         it.val = s->sell_val;
         it.c16 = s->sell_c16;
         it.c32 = s->sell_c32;
-        it.s = s->s;
+        it.s = s->s_int;
         it.urp = s->uu_rowptr;
         it.uci = s->uu_col;
         it.uav = s->uu_val;
