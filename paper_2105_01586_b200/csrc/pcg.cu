@@ -21,8 +21,6 @@
 // cooperative grid (one huge system: C5). The stopping rule is the unscaled relative
 // residual ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a
 // failed confirmation restarts CG from the current iterate inside the launch (A11).
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -30,7 +28,6 @@
 
 #include "device.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace femi {
 namespace {
@@ -130,36 +127,47 @@ __global__ void k_rhs(int B, const RItem* __restrict__ items) {
 }
 
 // ---- group barriers -------------------------------------------------------------
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, int n) {
+// MODE 2 (cooperative grid): flag-array barrier. Every CTA owns a 32-byte slot
+// {partial x, y, z, epoch} in it.part. Arrival = (optional partials) + gpu-scope fence +
+// epoch store into the CTA's own slot -- no serialized atomics on a shared counter.
+// Waiting = each thread polls one slot (ncta <= threads) until its epoch reaches the
+// barrier's epoch, then an acquire fence. Data published at epoch e is overwritten only at
+// epoch e+2 (reductions and plain barriers alternate), i.e. after every CTA has passed the
+// plain barrier e+1 that follows its reads.
+__device__ __forceinline__ void flag_arrive(const RItem& it, int rank, unsigned long long epoch, const double4* t) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* vgen = bar + 1;
-        const unsigned int g = *vgen;
-        __threadfence();
-        const unsigned int prev = atomicAdd(bar, 1u);
-        if (prev == (unsigned)n - 1u) {
-            bar[0] = 0u;
-            __threadfence();
-            atomicExch(bar + 1, g + 1u);
-        } else {
-            while (*vgen == g) {
-            }
+        double* P = it.part + 4 * rank;
+        if (t) {
+            P[0] = t->x;
+            P[1] = t->y;
+            P[2] = t->z;
         }
         __threadfence();
+        *(volatile unsigned long long*)(P + 3) = epoch;
     }
+}
+
+__device__ __forceinline__ void flag_wait(const RItem& it, unsigned long long epoch) {
+    for (int k = threadIdx.x; k < it.ncta; k += RNT) {
+        volatile unsigned long long* E = (volatile unsigned long long*)(it.part + 4 * k + 3);
+        while (*E < epoch) {
+        }
+    }
+    __threadfence();
     __syncthreads();
 }
 
 template <int MODE>
-__device__ __forceinline__ void group_sync(const RItem& it) {
+__device__ __forceinline__ void group_sync(const RItem& it, int rank, unsigned long long& epoch) {
     if constexpr (MODE == 0) {
         __syncthreads();
     } else if constexpr (MODE == 1) {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    } else if constexpr (MODE == 3) {
-        cg::this_grid().sync();
     } else {
-        grid_barrier(it.bar, it.ncta);
+        ++epoch;
+        flag_arrive(it, rank, epoch, nullptr);
+        flag_wait(it, epoch);
     }
 }
 
@@ -201,26 +209,32 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [NWARP][4
     return t;
 }
 
-// publish this CTA's partials, barrier, and sum all partials of the group (fixed order)
+// publish this CTA's partials (3 values), barrier, and sum all partials of the group in
+// a fixed order (identical in every CTA)
 template <int MODE>
-__device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, double4 loc, double* sh) {
+__device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, double4 loc, double* sh,
+                                                unsigned long long& epoch) {
     double4 t = block_sum4(loc, sh);
     if constexpr (MODE == 0) return t;
-    if (threadIdx.x == 0) {
-        double* P = it.part + 4 * rank;
-        P[0] = t.x;
-        P[1] = t.y;
-        P[2] = t.z;
-        P[3] = t.w;
+    if constexpr (MODE == 2) {
+        ++epoch;
+        flag_arrive(it, rank, epoch, &t);
+        flag_wait(it, epoch);
+    } else {
+        if (threadIdx.x == 0) {
+            double* P = it.part + 4 * rank;
+            P[0] = t.x;
+            P[1] = t.y;
+            P[2] = t.z;
+        }
+        group_sync<MODE>(it, rank, epoch);
     }
-    group_sync<MODE>(it);
     double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
     for (int k = threadIdx.x; k < it.ncta; k += RNT) {
         const double* P = it.part + 4 * k;
         a.x += __ldcg(P);
         a.y += __ldcg(P + 1);
         a.z += __ldcg(P + 2);
-        a.w += __ldcg(P + 3);
     }
     return block_sum4(a, sh);
 }
@@ -233,43 +247,63 @@ __device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, co
     double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* __restrict__ val = it.val;
-    for (int s = S0 + warp; s < S1; s += NWARP) {
-        const int row = 32 * s + lane < it.n ? 32 * s + lane : -1;  // internal numbering
-        const int len = it.len[s];
-        const int base = it.base[s] + lane;
-        const int cb = (32 * s / SIG) * SIG;
-        const int rr = row >= 0 ? row : 32 * s;
-        const double xi = __ldca(src + rr);
-        const double si = it.s[rr];
-        double acc = 0.0;
-        for (int k0 = 0; k0 < len; k0 += 4) {
-            double v[4];
-            int c[4];
+    const int16_t* __restrict__ c16 = it.c16;
+    const int32_t* __restrict__ c32 = it.c32;
+    // two 32-row slices per warp and step: two independent load chains in flight
+    for (int sa = S0 + 2 * warp; sa < S1; sa += 2 * NWARP) {
+        const int sb = sa + 1;
+        const bool hb = sb < S1;
+        int row[2], len[2], base[2], cb[2];
+        double xi[2], si[2], acc[2] = {0.0, 0.0};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = base + 32 * (k0 + q);
-                if (k0 + q < len) {
-                    v[q] = val[e];
-                    c[q] = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
-                } else {
-                    v[q] = 0.0;
-                    c[q] = rr;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc = fma(v[q], __ldca(src + c[q]), acc);
+        for (int h = 0; h < 2; ++h) {
+            const int s = h ? sb : sa;
+            const bool ok = h == 0 || hb;
+            row[h] = (ok && 32 * s + lane < it.n) ? 32 * s + lane : -1;  // internal numbering
+            len[h] = ok ? it.len[s] : 0;
+            base[h] = ok ? it.base[s] + lane : 0;
+            cb[h] = (32 * s / SIG) * SIG;
+            const int rr = row[h] >= 0 ? row[h] : 32 * sa;
+            xi[h] = __ldca(src + rr);
+            si[h] = it.s[rr];
         }
-        if (row >= 0) {
-            const double y = xi + acc;
+        const int L = max(len[0], len[1]);
+        for (int k0 = 0; k0 < L; k0 += 4) {
+            double v[8];
+            int c[8];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = base[h] + 32 * (k0 + q);
+                    if (k0 + q < len[h]) {
+                        v[4 * h + q] = val[e];
+                        c[4 * h + q] = c16 ? cb[h] + (int)c16[e] : c32[e];
+                    } else {
+                        v[4 * h + q] = 0.0;
+                        c[4 * h + q] = 32 * sa;
+                    }
+                }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double g = __ldca(src + c[q]);
+                if (q < 4) acc[0] = fma(v[q], g, acc[0]);
+                else acc[1] = fma(v[q], g, acc[1]);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (row[h] < 0) continue;
+            const double y = xi[h] + acc[h];
             if constexpr (KIND == 0) {
-                it.w[row] = y;
-                const double ru = xi / si;
-                loc.x += xi * xi;
-                loc.y += y * xi;
+                it.w[row[h]] = y;
+                const double ru = xi[h] / si[h];
+                loc.x += xi[h] * xi[h];
+                loc.y += y * xi[h];
                 loc.z += ru * ru;
             } else {
-                const double bi = it.b[row];
-                it.r[row] = si * bi - y;
+                const double bi = it.b[row[h]];
+                it.r[row[h]] = si[h] * bi - y;
                 loc.x += bi * bi;
             }
         }
@@ -319,8 +353,9 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
         it.x[i] = xh;
         if (nvec >= 3) X[i - R0] = xh;
     }
-    group_sync<MODE>(it);
-    double4 tot = group_reduce<MODE>(it, rank, spmv_sell<1>(it, S0, S1, it.x), sh);
+    unsigned long long epoch = 0;
+    group_sync<MODE>(it, rank, epoch);
+    double4 tot = group_reduce<MODE>(it, rank, spmv_sell<1>(it, S0, S1, it.x), sh, epoch);
     const double bn2 = tot.x;
     const double tol2 = rtol * rtol * bn2;
     int iters = 0, status = FEMI_OK, restarts = 0;
@@ -330,8 +365,8 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
             P[i - R0] = 0.0;
             SV[i - R0] = 0.0;
         }
-        group_sync<MODE>(it);  // r visible, partials consumed
-        tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh);
+        group_sync<MODE>(it, rank, epoch);  // r visible, partials consumed
+        tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh, epoch);
         double gam = tot.x, del = tot.y, rho = tot.z;
         double alpha = 0.0, beta = 0.0;
         bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho);
@@ -384,11 +419,11 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
             }
             ++iters;
             mark(0);
-            group_sync<MODE>(it);  // r published
+            group_sync<MODE>(it, rank, epoch);  // r published
             mark(1);
             const double4 lsp = spmv_sell<0>(it, S0, S1, it.r);
             mark(2);
-            tot = group_reduce<MODE>(it, rank, lsp, sh);
+            tot = group_reduce<MODE>(it, rank, lsp, sh, epoch);
             mark(3);
             const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
             if (!isfinite(gam2) || !isfinite(del2)) {
@@ -419,7 +454,7 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
             else xi = it.s[i] * X[i - R0];
             it.u_vert[nat] = xi;
         }
-        group_sync<MODE>(it);  // u_vert visible
+        group_sync<MODE>(it, rank, epoch);  // u_vert visible
         // true residual with the unscaled matrix (canonical rows); keeps s_i * r_true in r
         double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
         for (int i = R0 + tid; i < R1; i += RNT) {
@@ -431,7 +466,7 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
             it.r[i] = it.s[i] * ri;
             loc.x += ri * ri;
         }
-        tot = group_reduce<MODE>(it, rank, loc, sh);
+        tot = group_reduce<MODE>(it, rank, loc, sh, epoch);
         res2 = tot.x;
         const bool fail = bn2 > 0.0 && !(res2 <= tol2);
         if (!(status == FEMI_OK && iters > 0 && fail && iters < max_iter && restarts < 8)) break;
@@ -466,7 +501,6 @@ int g_smem_optin = -1;
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
-bool g_cg_barrier = false;
 
 }  // namespace
 
@@ -485,12 +519,8 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        g_smem_optin / 2 - 2048));
-        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_smem_optin / 2 - 2048));
         const char* tm = std::getenv("FEMI_PCG_TIMERS");
         g_timers = tm && tm[0] == '1';
-        const char* gb = std::getenv("FEMI_GRID_BARRIER");
-        g_cg_barrier = gb && std::string(gb) == "cg";
         int per_sm = 0;
         FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
                                                                 g_smem_optin / 2 - 2048));
@@ -584,7 +614,8 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.x0mode = (it.g == nullptr && o.x0 == 1) ? 0 : o.x0;
     }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
-    for (int b = 0; b < B; ++b) FEMI_CUDA(cudaMemsetAsync(items[b].bar, 0, 2 * sizeof(unsigned), st));
+    for (int b = 0; b < B; ++b)  // partial/epoch slots must start at epoch 0
+        FEMI_CUDA(cudaMemsetAsync(items[b].part, 0, sizeof(double) * 4 * ncta_item, st));
 
     // ---- launches: reset, min/max(g), b, resident CG, mask copy
     k_reset<<<(B + 127) / 128, 128, 0, st>>>(B, d_state, o.rtol, o.max_iter);
@@ -623,10 +654,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
             cfg.numAttrs = 1;
-            if (g_cg_barrier)
-                e = cudaLaunchKernelEx(&cfg, k_pcg_resident<3>, (const RItem*)d_items, B, vr, nvec);
-            else
-                e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
+            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
         } else if (mode == 1) {
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = ncta_item;
