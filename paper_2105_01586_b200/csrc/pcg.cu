@@ -501,6 +501,8 @@ int g_smem_optin = -1;
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
+int g_nvec_max = 3;
+int g_l2_persist_mb = 0;
 
 }  // namespace
 
@@ -521,6 +523,17 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                                        g_smem_optin / 2 - 2048));
         const char* tm = std::getenv("FEMI_PCG_TIMERS");
         g_timers = tm && tm[0] == '1';
+        const char* nv = std::getenv("FEMI_PCG_NVEC");  // experiments: max vectors kept in smem
+        if (nv) g_nvec_max = std::atoi(nv);
+        const char* lp = std::getenv("FEMI_L2_PERSIST");  // experiments: L2 persistence window (MB)
+        if (lp) g_l2_persist_mb = std::atoi(lp);
+        if (g_l2_persist_mb > 0) {
+            int maxp = 0;
+            FEMI_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+            const size_t want = std::min<size_t>((size_t)g_l2_persist_mb << 20, (size_t)maxp);
+            FEMI_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+            std::fprintf(stderr, "[femi] persisting L2 max %d MB, set %zu MB\n", maxp >> 20, want >> 20);
+        }
         int per_sm = 0;
         FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
                                                                 g_smem_optin / 2 - 2048));
@@ -554,7 +567,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         }
     }
     const size_t budget = (size_t)(mode == 2 ? g_smem_optin / 2 - 2048 : g_smem_optin - 2048);
-    int nvec = 3;
+    int nvec = g_nvec_max;
     while (nvec >= 2 && sizeof(double) * (nvec * (size_t)vrows) > budget) --nvec;
     if (nvec < 2) nvec = 0;
     const size_t smem_bytes = sizeof(double) * ((size_t)nvec * vrows);
@@ -635,7 +648,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     FEMI_CUDA(cudaGetLastError());
     if (nmax > 0) {
         cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(RNT);
         cfg.dynamicSmemBytes = smem_bytes;
@@ -654,6 +667,17 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             attr[0].id = cudaLaunchAttributeCooperative;
             attr[0].val.cooperative = 1;
             cfg.numAttrs = 1;
+            if (g_l2_persist_mb > 0 && S[0]->sell_nnz > 0) {  // keep the SELL values L2-resident
+                const size_t bytes = sizeof(double) * (size_t)S[0]->sell_nnz;
+                const size_t lim = (size_t)g_l2_persist_mb << 20;
+                attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+                attr[1].val.accessPolicyWindow.base_ptr = S[0]->sell_val;
+                attr[1].val.accessPolicyWindow.num_bytes = bytes;
+                attr[1].val.accessPolicyWindow.hitRatio = bytes <= lim ? 1.0f : (float)lim / (float)bytes;
+                attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cfg.numAttrs = 2;
+            }
             e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
         } else if (mode == 1) {
             attr[0].id = cudaLaunchAttributeClusterDimension;
