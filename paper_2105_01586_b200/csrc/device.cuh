@@ -112,6 +112,11 @@ struct femi_system_s {
     int32_t* sell_c32 = nullptr;   // absolute column otherwise
     int64_t sell_nnz = 0;
     int32_t* sell_src_tmp = nullptr;  // assembly-time map SELL entry -> o_val index
+    // pixel ownership (reading A7), resolved once per mesh: owner[pix] = t | cls << 30,
+    // triangle-major pixel lists tp_ptr[T+1] / tp_pix[N] (ascending pix, bit 31 = vertex pixel)
+    uint32_t* owner = nullptr;
+    int32_t* tp_ptr = nullptr;
+    uint32_t* tp_pix = nullptr;
     int32_t* sell_inv = nullptr;      // n_u: internal solver row -> canonical unknown index
     double* s_int = nullptr;          // D^-1/2 in internal order
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
@@ -146,6 +151,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
                           double* const* u_px, double* const* e_px, double* const* tri_err,
                           int32_t* const* best, double* const* sse, cudaStream_t st);
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st);
+femi_status build_owner_tables(femi_system_s* S, cudaStream_t st);
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters);

@@ -2,37 +2,216 @@
 // (PAPER.md:L239-241 interpolation; L262-265 "e_i = (u_i - f_i)^2", "total L2 error in
 // each triangle"), and the adjoint raster P^T r used by tonal optimisation (S6).
 //
-// Triangle-parallel with warp-cooperative expansion (raster_common.cuh): a pixel is
-// processed by the triangle that owns it (reading A7: lowest index among the closed
-// triangles containing it), decided locally from the edge functions and precomputed
-// ownership flags -- no owner map, no atomics. A vertex pixel takes its vertex value
-// exactly; otherwise u = u_a + l_b (u_b - u_a) + l_c (u_c - u_a), l = exact integer edge
-// function / 2*area (S3). Per-triangle error sums and arg-max (ties: lowest pix) are
-// segmented warp scans in pixel order; SSE is a per-CTA partial summed in fixed order by
-// the last CTA: deterministic.
+// Pixel ownership (reading A7: lowest index among the closed triangles containing a
+// pixel) depends only on the mesh, so it is resolved ONCE per mesh at assembly by a
+// warp-cooperative triangle expansion (raster_common.cuh) into
+//   owner[pix]  = t | cls << 30   (cls 0: interior/edge pixel, 1..3: vertex pixel of v[cls-1])
+//   tp_ptr[t]   = first entry of triangle t in tp_pix (CSR, ascending triangle)
+//   tp_pix[q]   = the triangle's pixels in ascending pix order (bit 31: vertex pixel).
+// Every solve then rasterises with two streaming kernels and no atomics:
+//   R1 pixel-major: u = vertex value (vertex pixel) or u_a + l_b (u_b - u_a) + l_c (u_c - u_a)
+//      with l = exact integer edge function / 2*area (S3); e = (u - f)^2. Coalesced f/u/e.
+//   R2 triangle-major over tp_pix (coalesced list, local e gathers): per-triangle error sum
+//      and arg-max over non-vertex pixels (ties: lowest pix) by segmented warp scans in
+//      pixel order; SSE = fixed-order sum of the triangle sums. Deterministic.
+// The adjoint P^T r is R2's traversal with barycentric weights.
 #include "raster_common.cuh"
 
 namespace femi {
 namespace {
 
+constexpr uint32_t kTriMask = 0x3fffffffu;
+
+// ---------------------------------------------------------------- setup (per mesh)
+
+// MODE 0: owner map + owned-pixel count per triangle. MODE 1: triangle-major pixel list.
+template <int MODE>
+__global__ void __launch_bounds__(RT) k_build_owner(const TriRec* __restrict__ tri, int64_t T, int W,
+                                                    uint32_t* __restrict__ owner, int32_t* __restrict__ cnt,
+                                                    const int32_t* __restrict__ tp_ptr,
+                                                    uint32_t* __restrict__ tp_pix) {
+    __shared__ WTri tris[RWARPS][32];
+    __shared__ int run_s[RWARPS][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ngroups = (T + 31) / 32;
+    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    WTri* ws = tris[wid];
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+        const int64_t t0 = g * 32;
+        int excl, total;
+        TriRec R;
+        const int nbox = warp_load_tris(tri, T, t0, ws, excl, total, R);
+        run_s[wid][lane] = 0;
+        __syncwarp();
+        for (int base = 0; base < total; base += 32) {
+            const int k = base + lane;
+            const int j = warp_find(excl, k, total);
+            const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
+            int own = 0, cls = 0;
+            int64_t pix = 0;
+            if (j < 32) {
+                const WTri& I = ws[j];
+                const int loc = k - exj;
+                const int ry = loc / I.bw;
+                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
+                int w0, w1, w2, kv = 0;
+                const int c = classify(I, px, py, w0, w1, w2, kv);
+                if (c) {
+                    own = 1;
+                    cls = c == 2 ? kv + 1 : 0;
+                    pix = (int64_t)py * W + px;
+                    if (MODE == 0) owner[pix] = (uint32_t)(t0 + j) | ((uint32_t)cls << 30);
+                }
+            }
+            // rank of this owned pixel inside its triangle (slots are in pixel order)
+            int rk = own;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ro = __shfl_up_sync(0xffffffffu, rk, o);
+                const int jo = __shfl_up_sync(0xffffffffu, j, o);
+                if (lane >= o && jo == j) rk += ro;
+            }
+            if (MODE == 1 && own) {
+                const int q = tp_ptr[t0 + j] + run_s[wid][j] + rk - 1;
+                tp_pix[q] = (uint32_t)pix | (cls ? 0x80000000u : 0u);
+            }
+            __syncwarp();
+            const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+            if (j < 32 && (lane == 31 || jn != j)) run_s[wid][j] += rk;
+            __syncwarp();
+        }
+        if (MODE == 0 && nbox) cnt[t0 + lane] = run_s[wid][lane];
+        __syncwarp();
+    }
+}
+
+// exclusive scan of cnt[0..n) into ptr[0..n] (ptr[n] = total): block sums, then offsets
+constexpr int SCB = 1024;
+__global__ void k_scan_blocks(int64_t n, const int32_t* __restrict__ cnt, int32_t* __restrict__ bsum) {
+    __shared__ int sh[SCB / 32];
+    const int64_t i = (int64_t)blockIdx.x * SCB + threadIdx.x;
+    int v = i < n ? cnt[i] : 0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int w = 0; w < SCB / 32; ++w) s += sh[w];
+        bsum[blockIdx.x] = s;
+    }
+}
+__global__ void k_scan_bsum(int nb, int32_t* __restrict__ bsum) {  // one thread; nb ~ T/1024
+    if (threadIdx.x || blockIdx.x) return;
+    int run = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int c = bsum[b];
+        bsum[b] = run;
+        run += c;
+    }
+    bsum[nb] = run;
+}
+__global__ void k_scan_apply(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ bsum,
+                             int32_t* __restrict__ ptr) {
+    __shared__ int sh[SCB / 32];
+    const int64_t i = (int64_t)blockIdx.x * SCB + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int v = i < n ? cnt[i] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < SCB / 32 ? sh[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < SCB / 32) sh[lane] = s;
+    }
+    __syncthreads();
+    const int off = bsum[blockIdx.x] + (wid ? sh[wid - 1] : 0) + incl - v;
+    if (i < n) ptr[i] = off;
+    if (i == n - 1) ptr[n] = off + v;
+}
+
+// ---------------------------------------------------------------- per solve
+
 struct RasterItem {
     const TriRec* tri;
+    const uint32_t* owner;
+    const int32_t* tp_ptr;
+    const uint32_t* tp_pix;
     const double* u_vert;
     const double* f;
     double* u_px;
-    double* e_px;
+    double* e_px;  // output or scratch (needed by R2 whenever f is given)
     double* tri_err;
     int32_t* best;
     double* sse;
-    int64_t T;
+    int64_t T, N;
     int32_t W;
     int32_t pad;
 };
 
-__global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restrict__ items, double* __restrict__ part,
-                                                     uint32_t* __restrict__ counters) {
-    __shared__ WTri tris[RWARPS][32];
-    __shared__ double tuv[RWARPS][32][3];
+// R1: pixel-major values and errors
+__global__ void __launch_bounds__(256) k_px_values(const RasterItem* __restrict__ items) {
+    const RasterItem it = items[blockIdx.y];
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < it.N; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = it.owner[p];
+        const TriRec R = it.tri[o & kTriMask];
+        const uint32_t cls = o >> 30;
+        double u;
+        if (cls) {
+            u = it.u_vert[R.v[cls - 1]];
+        } else {
+            const int W = it.W;
+            const int px = (int)(p % W), py = (int)(p / W);
+            const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
+            const int w1 = (ax - cx) * (py - cy) - (ay - cy) * (px - cx);  // orient(c,a,p)
+            const int w2 = (bx - ax) * (py - ay) - (by - ay) * (px - ax);  // orient(a,b,p)
+            const double D = (double)((bx - ax) * (cy - ay) - (by - ay) * (cx - ax));
+            const double ua = it.u_vert[R.v[0]];
+            u = ua + (w1 / D) * (it.u_vert[R.v[1]] - ua) + (w2 / D) * (it.u_vert[R.v[2]] - ua);
+        }
+        if (it.u_px) it.u_px[p] = u;
+        if (it.f) {
+            const double d = u - it.f[p];
+            it.e_px[p] = d * d;
+        }
+    }
+}
+
+// Warp-cooperative traversal of the triangle-major list: lane l of a warp owns triangle
+// t0+l; list entries ptr[t0] .. ptr[t0+32] are walked 32 at a time (coalesced), each entry
+// tagged with its triangle by a shuffle binary search over the per-triangle offsets.
+struct ListWalk {
+    int excl, total, ptr0;
+};
+__device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_ptr, int64_t T, int64_t t0, int& cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = t0 + lane;
+    const int a = t < T ? tp_ptr[t] : 0;
+    const int b = t < T ? tp_ptr[t + 1] : 0;
+    cnt = b - a;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    ListWalk lw;
+    lw.excl = incl - cnt;
+    lw.total = __shfl_sync(0xffffffffu, incl, 31);
+    lw.ptr0 = __shfl_sync(0xffffffffu, a, 0);
+    return lw;
+}
+
+// R2: per-triangle error sum and arg-max, SSE
+__global__ void __launch_bounds__(RT) k_tri_reduce(const RasterItem* __restrict__ items, double* __restrict__ part,
+                                                   uint32_t* __restrict__ counters) {
     __shared__ double acc_s[RWARPS][32];
     __shared__ double be_s[RWARPS][32];
     __shared__ int bp_s[RWARPS][32];
@@ -42,60 +221,30 @@ __global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restric
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ngroups = (it.T + 31) / 32;
     const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
-    const bool with_f = it.f != nullptr;
-    WTri* ws = tris[wid];
     double sse_loc = 0.0;
     for (int64_t g = gwarp; g < ngroups; g += nwarps) {
         const int64_t t0 = g * 32;
-        int excl, total;
-        TriRec R;
-        const int nbox = warp_load_tris(it.tri, it.T, t0, ws, excl, total, R);
-        if (nbox) {
-            tuv[wid][lane][0] = it.u_vert[R.v[0]];
-            tuv[wid][lane][1] = it.u_vert[R.v[1]];
-            tuv[wid][lane][2] = it.u_vert[R.v[2]];
-        }
+        int cnt;
+        const ListWalk lw = list_begin(it.tp_ptr, it.T, t0, cnt);
         acc_s[wid][lane] = 0.0;
         be_s[wid][lane] = -1.0;
         bp_s[wid][lane] = -1;
         __syncwarp();
-        for (int base = 0; base < total; base += 32) {
+        for (int base = 0; base < lw.total; base += 32) {
             const int k = base + lane;
-            const int j = warp_find(excl, k, total);
-            const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
+            const int j = warp_find(lw.excl, k, lw.total);
             double val = 0.0, ce = -1.0;
             int cp = 0x7fffffff;
             if (j < 32) {
-                const WTri& I = ws[j];
-                const int loc = k - exj;
-                const int ry = loc / I.bw;
-                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
-                int w0, w1, w2, kv = 0;
-                const int cls = classify(I, px, py, w0, w1, w2, kv);
-                if (cls) {
-                    double u;
-                    if (cls == 2) {
-                        u = tuv[wid][j][kv];
-                    } else {
-                        const double D = (double)I.D, ua = tuv[wid][j][0];
-                        u = ua + (w1 / D) * (tuv[wid][j][1] - ua) + (w2 / D) * (tuv[wid][j][2] - ua);
-                    }
-                    const int64_t pix = (int64_t)py * it.W + px;
-                    if (it.u_px) it.u_px[pix] = u;
-                    if (with_f) {
-                        const double d = u - it.f[pix];
-                        const double e = d * d;
-                        if (it.e_px) it.e_px[pix] = e;
-                        val = e;
-                        if (cls == 1) {
-                            ce = e;
-                            cp = (int)pix;
-                        }
-                    }
+                const uint32_t v = it.tp_pix[lw.ptr0 + k];
+                const int pix = (int)(v & 0x7fffffffu);
+                const double e = it.e_px[pix];
+                val = e;
+                if (!(v >> 31)) {
+                    ce = e;
+                    cp = pix;
                 }
             }
-            if (!with_f) continue;
-            // segmented inclusive scan over runs of equal j: sum and (e desc, pix asc) arg-max
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double vo = __shfl_up_sync(0xffffffffu, val, o);
@@ -118,9 +267,10 @@ __global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restric
                     bp_s[wid][j] = cp;
                 }
             }
+            __syncwarp();
         }
         __syncwarp();
-        if (with_f && nbox) {
+        if (t0 + lane < it.T) {
             const double a = acc_s[wid][lane];
             if (it.tri_err) it.tri_err[t0 + lane] = a;
             if (it.best) it.best[t0 + lane] = be_s[wid][lane] >= 0.0 ? bp_s[wid][lane] : -1;
@@ -128,8 +278,7 @@ __global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restric
         }
         __syncwarp();
     }
-    if (!with_f || !it.sse) return;
-    // SSE: fixed-order sums (lanes, warps, CTAs)
+    if (!it.sse) return;
     const double tot = block_sum<RT>(sse_loc, red);
     double* P = part + (size_t)blockIdx.y * gridDim.x;
     if (threadIdx.x == 0) P[blockIdx.x] = tot;
@@ -153,47 +302,56 @@ __global__ void __launch_bounds__(RT) k_raster_error(const RasterItem* __restric
 
 // P^T r: per triangle, sum over its owned pixels of (l_a, l_b, l_c) r (vertex pixels:
 // weight 1 on that vertex) -> tri_w[3t+k]; the vertex gather happens in tonal.cu.
-__global__ void __launch_bounds__(RT) k_adjoint_raster(const TriRec* __restrict__ tri, int64_t T, int W,
-                                                       const double* __restrict__ r, double* __restrict__ tri_w) {
-    __shared__ WTri tris[RWARPS][32];
+__global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ tri, const int32_t* __restrict__ tp_ptr,
+                                                    const uint32_t* __restrict__ tp_pix,
+                                                    const uint32_t* __restrict__ owner, int64_t T, int W,
+                                                    const double* __restrict__ r, double* __restrict__ tri_w) {
     __shared__ double acc_s[RWARPS][32][3];
+    __shared__ WTri tris[RWARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ngroups = (T + 31) / 32;
     const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
     WTri* ws = tris[wid];
     for (int64_t g = gwarp; g < ngroups; g += nwarps) {
         const int64_t t0 = g * 32;
-        int excl, total;
-        TriRec R;
-        const int nbox = warp_load_tris(tri, T, t0, ws, excl, total, R);
+        int cnt;
+        const ListWalk lw = list_begin(tp_ptr, T, t0, cnt);
+        if (t0 + lane < T) {
+            const TriRec R = tri[t0 + lane];
+            WTri I;
+            I.ax = R.x[0];
+            I.ay = R.y[0];
+            I.bx = R.x[1];
+            I.by = R.y[1];
+            I.cx = R.x[2];
+            I.cy = R.y[2];
+            I.D = orient_xy(I.ax, I.ay, I.bx, I.by, I.cx, I.cy);
+            ws[lane] = I;
+        }
         acc_s[wid][lane][0] = 0.0;
         acc_s[wid][lane][1] = 0.0;
         acc_s[wid][lane][2] = 0.0;
         __syncwarp();
-        for (int base = 0; base < total; base += 32) {
+        for (int base = 0; base < lw.total; base += 32) {
             const int k = base + lane;
-            const int j = warp_find(excl, k, total);
-            const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
+            const int j = warp_find(lw.excl, k, lw.total);
             double sa = 0.0, sb = 0.0, sc = 0.0;
             if (j < 32) {
-                const WTri& I = ws[j];
-                const int loc = k - exj;
-                const int ry = loc / I.bw;
-                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
-                int w0, w1, w2, kv = 0;
-                const int cls = classify(I, px, py, w0, w1, w2, kv);
-                if (cls) {
-                    const double rv = r[(int64_t)py * W + px];
-                    if (cls == 2) {
-                        if (kv == 0) sa = rv;
-                        else if (kv == 1) sb = rv;
-                        else sc = rv;
-                    } else {
-                        const double D = (double)I.D;
-                        sa = (w0 / D) * rv;
-                        sb = (w1 / D) * rv;
-                        sc = (w2 / D) * rv;
-                    }
+                const uint32_t v = tp_pix[lw.ptr0 + k];
+                const int pix = (int)(v & 0x7fffffffu);
+                const double rv = r[pix];
+                if (v >> 31) {
+                    const uint32_t cls = owner[pix] >> 30;
+                    if (cls == 1) sa = rv;
+                    else if (cls == 2) sb = rv;
+                    else sc = rv;
+                } else {
+                    const WTri& I = ws[j];
+                    const int px = pix % W, py = pix / W;
+                    const double D = (double)I.D;
+                    sa = (orient_xy(I.bx, I.by, I.cx, I.cy, px, py) / D) * rv;
+                    sb = (orient_xy(I.cx, I.cy, I.ax, I.ay, px, py) / D) * rv;
+                    sc = (orient_xy(I.ax, I.ay, I.bx, I.by, px, py) / D) * rv;
                 }
             }
 #pragma unroll
@@ -214,9 +372,10 @@ __global__ void __launch_bounds__(RT) k_adjoint_raster(const TriRec* __restrict_
                 acc_s[wid][j][1] += sb;
                 acc_s[wid][j][2] += sc;
             }
+            __syncwarp();
         }
         __syncwarp();
-        if (nbox) {
+        if (t0 + lane < T) {
             tri_w[3 * (t0 + lane)] = acc_s[wid][lane][0];
             tri_w[3 * (t0 + lane) + 1] = acc_s[wid][lane][1];
             tri_w[3 * (t0 + lane) + 2] = acc_s[wid][lane][2];
@@ -225,7 +384,7 @@ __global__ void __launch_bounds__(RT) k_adjoint_raster(const TriRec* __restrict_
     }
 }
 
-int raster_grid(int64_t T, int B) {
+int warp_grid(int64_t T, int B) {
     const int64_t groups = (T + 31) / 32;
     const int64_t want = (groups + RWARPS - 1) / RWARPS;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)148 * 8 / std::max(1, B) + 1));
@@ -233,15 +392,41 @@ int raster_grid(int64_t T, int B) {
 
 }  // namespace
 
+femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
+    const int64_t T = S->T, N = (int64_t)S->W * S->H;
+    if (T == 0) return FEMI_OK;
+    const int nb = (int)((T + SCB - 1) / SCB);
+    int32_t* cnt = nullptr;
+    int32_t* bsum = nullptr;
+    FEMI_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * T, st));
+    FEMI_CUDA(cudaMallocAsync(&bsum, sizeof(int32_t) * (nb + 1), st));
+    const int g = warp_grid(T, 1);
+    k_build_owner<0><<<g, RT, 0, st>>>(S->tri, T, S->W, S->owner, cnt, nullptr, nullptr);
+    k_scan_blocks<<<nb, SCB, 0, st>>>(T, cnt, bsum);
+    k_scan_bsum<<<1, 32, 0, st>>>(nb, bsum);
+    k_scan_apply<<<nb, SCB, 0, st>>>(T, cnt, bsum, S->tp_ptr);
+    k_build_owner<1><<<g, RT, 0, st>>>(S->tri, T, S->W, nullptr, nullptr, S->tp_ptr, S->tp_pix);
+    count_launches(5);
+    FEMI_CUDA(cudaGetLastError());
+    FEMI_CUDA(cudaFreeAsync(cnt, st));
+    FEMI_CUDA(cudaFreeAsync(bsum, st));
+    (void)N;
+    return FEMI_OK;
+}
+
 femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
                           double* const* u_px, double* const* e_px, double* const* tri_err, int32_t* const* best,
                           double* const* sse, cudaStream_t st) {
     if (B <= 0) return FEMI_OK;
     std::vector<RasterItem> items(B);
-    int64_t Tmax = 0;
+    int64_t Tmax = 0, Nmax = 0, scratch = 0;
+    bool need_r2 = false;
     for (int b = 0; b < B; ++b) {
         RasterItem& r = items[b];
         r.tri = S[b]->tri;
+        r.owner = S[b]->owner;
+        r.tp_ptr = S[b]->tp_ptr;
+        r.tp_pix = S[b]->tp_pix;
         r.u_vert = u_vert[b];
         r.f = f ? f[b] : nullptr;
         r.u_px = u_px ? u_px[b] : nullptr;
@@ -250,24 +435,39 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
         r.best = best ? best[b] : nullptr;
         r.sse = sse ? sse[b] : nullptr;
         r.T = S[b]->T;
+        r.N = (int64_t)S[b]->W * S[b]->H;
         r.W = S[b]->W;
         Tmax = std::max(Tmax, r.T);
+        Nmax = std::max(Nmax, r.N);
+        if (r.f && (r.tri_err || r.best || r.sse)) need_r2 = true;
+        if (r.f && !r.e_px) scratch += r.N;
     }
-    const int gx = raster_grid(Tmax, B);
+    const int gx = warp_grid(Tmax, B);
     const size_t bytes_items = sizeof(RasterItem) * B;
     const size_t bytes_part = sizeof(double) * (size_t)gx * B;
     const size_t bytes_cnt = sizeof(uint32_t) * B;
     void* base = nullptr;
-    FEMI_CUDA(cudaMallocAsync(&base, bytes_items + bytes_part + bytes_cnt + 64, st));
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    FEMI_CUDA(cudaMallocAsync(&base, al(bytes_items) + al(bytes_part) + al(bytes_cnt) + sizeof(double) * scratch, st));
     char* cur = (char*)base;
     RasterItem* d_items = (RasterItem*)cur;
-    double* d_part = (double*)(cur + ((bytes_items + 15) & ~(size_t)15));
-    uint32_t* d_cnt = (uint32_t*)((char*)d_part + bytes_part);
+    double* d_part = (double*)(cur + al(bytes_items));
+    uint32_t* d_cnt = (uint32_t*)((char*)d_part + al(bytes_part));
+    double* scr = (double*)((char*)d_cnt + al(bytes_cnt));
+    for (int b = 0; b < B; ++b)
+        if (items[b].f && !items[b].e_px) {
+            items[b].e_px = scr;
+            scr += items[b].N;
+        }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
-    dim3 grid(gx, B);
-    k_raster_error<<<grid, RT, 0, st>>>(d_items, d_part, d_cnt);
+    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((Nmax + 255) / 256, (int64_t)148 * 16 / B + 1));
+    k_px_values<<<dim3(g1, B), 256, 0, st>>>(d_items);
     count_launches(1);
+    if (need_r2) {
+        k_tri_reduce<<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
+        count_launches(1);
+    }
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
     return FEMI_OK;
@@ -275,7 +475,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
 
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {
     if (S->T == 0) return FEMI_OK;
-    k_adjoint_raster<<<raster_grid(S->T, 1), RT, 0, st>>>(S->tri, S->T, S->W, r, tri_w);
+    k_tri_adjoint<<<warp_grid(S->T, 1), RT, 0, st>>>(S->tri, S->tp_ptr, S->tp_pix, S->owner, S->T, S->W, r, tri_w);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;
