@@ -290,15 +290,15 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         std::vector<int16_t> c16;
         bool fits16 = true;
         int64_t ent = 0;
-        for (int32_t s = 0; s < nsl; ++s) {
+        for (int32_t sl = 0; sl < nsl; ++sl) {
             int32_t L = 0;
-            for (int l = 0; l < 32 && 32 * s + l < n; ++l) L = std::max(L, rl(pi[32 * s + l]));
-            len[s] = L;
-            base[s] = (int32_t)ent;
-            const int32_t wbase = (32 * s / SIG) * SIG;
+            for (int l = 0; l < 32 && 32 * sl + l < n; ++l) L = std::max(L, rl(pi[32 * sl + l]));
+            len[sl] = L;
+            base[sl] = (int32_t)ent;
+            const int32_t wbase = (32 * sl / SIG) * SIG;
             for (int32_t k = 0; k < L; ++k)
                 for (int l = 0; l < 32; ++l) {
-                    const int64_t ri = 32 * (int64_t)s + l;
+                    const int64_t ri = 32 * (int64_t)sl + l;
                     int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
                     if (ri < n && k < rl(pi[ri])) {
                         const int32_t row = pi[ri];
@@ -327,9 +327,9 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         U(alloc(S, &S->s_int, (size_t)std::max<int64_t>(n, 1)));
         if (fits16) {
             c16.resize(c32.size());
-            for (int32_t s = 0, q = 0; s < nsl; ++s) {
-                const int32_t wbase = (32 * s / SIG) * SIG;
-                for (int32_t k = 0; k < len[s] * 32; ++k, ++q) c16[q] = (int16_t)(c32[q] - wbase);
+            for (int32_t sl = 0, q = 0; sl < nsl; ++sl) {
+                const int32_t wbase = (32 * sl / SIG) * SIG;
+                for (int32_t k = 0; k < len[sl] * 32; ++k, ++q) c16[q] = (int16_t)(c32[q] - wbase);
             }
             U(upload(S, &S->sell_c16, c16, st));
         } else {
