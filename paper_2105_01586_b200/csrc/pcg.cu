@@ -1,33 +1,33 @@
 // pcg.cu -- S2: batched Jacobi-preconditioned CG for A_uu x = -A_uk g.
 //
-// B200 design: ONE persistent launch per (batched) solve. The Jacobi preconditioner is
-// folded into the matrix at assembly (A^ = D^-1/2 A D^-1/2, unit diagonal, only the
-// off-diagonal part stored), so CG runs on A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b).
-// The recurrence is the single-reduction form of CG (Chronopoulos-Gear): per iteration
+// B200 design. The Jacobi preconditioner is folded into the matrix at assembly
+// (A^ = D^-1/2 A D^-1/2, unit diagonal, only the off-diagonal part stored), so CG runs on
+// A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b). One solve =
+//   k_rhs          b = -A_uk g (or the given b), internal row order
+//   k_init_x/_r    x^0 and r0 = s b - A^ x^0, ||b||^2
+//   k_cg           ONE persistent launch running the whole CG loop on device
+//   k_finalize     x = D^-1/2 x^ scattered to canonical order (u_vert)
+//   k_true_res     ||b - A x|| with the unscaled matrix (reading A11); a failed check
+//                  relaunches k_cg from the current iterate
+// k_cg runs the single-reduction form of CG (Chronopoulos-Gear). Per iteration
 //   U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s      (own rows)
 //   -- group barrier (r published) --
 //   S: w = A^ r (gathers r) ; partial (r.r, w.r, ||D^1/2 r||^2)
-//   -- group barrier (partials published) -- every CTA sums the partials in the same
+//   -- group barrier fused with the reduction -- every CTA sums the partials in the same
 //   fixed order, so alpha/beta/convergence are bit-identical in all CTAs (deterministic).
-// The SpMV reads the matrix in sliced-ELL form (SELL-32-sigma, sigma = 512 rows, rows
-// sorted by length inside a window): each warp takes one 32-row slice, every warp load
-// of values / int16 window-relative columns is one coalesced 32-lane access, and all
-// entries of a row are independent loads (no shared-memory staging, no block barrier in
-// the SpMV). Each batch item (system / right-hand side) owns a group of CTAs, each CTA a
-// contiguous range of windows. p and s (and x when it fits) never leave the CTA: they
-// live in shared memory for the whole solve; only r (gathered by neighbours) and w go
-// through L2/HBM. Group barriers: __syncthreads (1 CTA), the hardware cluster barrier
-// (a cluster of <= 16 CTAs: C1-C4), or a global sense-reversing barrier over a
-// cooperative grid (one huge system: C5). The stopping rule is the unscaled relative
-// residual ||D^1/2 r^|| <= rtol ||b||, confirmed at exit with the unscaled matrix; a
-// failed confirmation restarts CG from the current iterate inside the launch (A11).
+// The SpMV reads the matrix in sliced-ELL form (SELL-32-sigma): every warp load of values
+// / int16 window-relative columns is one coalesced 32-lane access; two slices per warp
+// keep two independent load chains in flight. Each batch item owns a group of CTAs and
+// each CTA a contiguous range of rows; p and s (and x when it fits) stay in shared memory
+// for the whole solve. Group barriers: __syncthreads (1 CTA), the hardware cluster
+// barrier (a cluster of <= 16 CTAs: C1-C4), or a flag-array barrier over a cooperative
+// grid (one huge system: C5).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
 #include "device.cuh"
-
 
 namespace femi {
 namespace {
@@ -51,15 +51,15 @@ struct RItem {
     const double* val;
     const int16_t* c16;   // column - window base (internal numbering)
     const int32_t* c32;
-    const double* s;    // D^-1/2 (internal order)
-    const int32_t* urp;  // unscaled A_uu (diagonal included), true residual
+    const double* s;     // D^-1/2 (internal order)
+    const int32_t* urp;  // unscaled A_uu (diagonal included), canonical rows
     const int32_t* uci;
     const double* uav;
-    const int32_t* krp;  // A_uk
+    const int32_t* krp;  // A_uk, canonical rows
     const int32_t* kci;
     const double* kav;
     const double* g;    // mask values or NULL (b given)
-    const double* bin;  // given b or NULL
+    const double* bin;  // given b (canonical order) or NULL
     double* u_vert;
     double* b;  // unscaled right-hand side
     double* x;  // x^ (initial guess gathers; the iterate when it does not fit in smem)
@@ -67,16 +67,24 @@ struct RItem {
     double* w;  // A^ r^
     double* p;  // used when the CTA's rows do not fit shared memory
     double* sv;
-    double* part;       // [ncta][4] partial sums
-    unsigned int* bar;  // [2] global barrier count / generation
+    double* part;  // [ncta][4] partial sums / barrier slots
+    double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
     int32_t n, m, cta0, ncta, nwin, x0mode;
 };
 
-constexpr int RNT = 512;  // threads per CTA of the persistent solver
-constexpr int NWARP = RNT / 32;
+constexpr int RNT = 512;  // threads per CTA of the persistent solver (block/cluster modes)
 constexpr int SIG = kSellSigma;
+constexpr int KNT = 256;  // threads per CTA of the ordinary kernels
+constexpr int KGRID = 296;
 
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------ ordinary kernels
 __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
@@ -109,8 +117,8 @@ __global__ void k_minmax(int B, const RItem* __restrict__ items) {
     }
 }
 
-// b = -A_uk g (ascending mask index, reading A6 order), or the given b; stored in internal order
-__global__ void k_rhs(int B, const RItem* __restrict__ items) {
+// b = -A_uk g (ascending mask index, reading A6 order), or the given b; internal order
+__global__ void k_rhs(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
         const int nat = it.inv[i];
@@ -126,14 +134,127 @@ __global__ void k_rhs(int B, const RItem* __restrict__ items) {
     }
 }
 
-// ---- group barriers -------------------------------------------------------------
+// x^0 = x0 / s (x0: midrange(g), 0 or the caller's u_vert)
+__global__ void k_init_x(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    const double x0v = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        const double x0 = (it.x0mode == 2) ? it.u_vert[it.inv[i]] : x0v;
+        it.x[i] = x0 / it.s[i];
+    }
+}
+
+// Deterministic grid reduction helper: per-block partial, the last block sums in order.
+template <int NQ>
+__device__ __forceinline__ bool grid_partial(double (&v)[NQ], double* red, unsigned* cnt, double* shm) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = warp_sum_d(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) shm[NQ * wid + q] = v[q];
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NQ; ++q) {
+            double t = 0.0;
+            for (int w = 0; w < KNT / 32; ++w) t += shm[NQ * w + q];
+            red[NQ * blockIdx.x + q] = t;
+        }
+        __threadfence();
+        last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NQ; ++q) {
+            double t = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(red + NQ * b + q);
+            v[q] = t;
+        }
+        *cnt = 0;
+    }
+    return true;
+}
+
+// r0 = s b - (x^ + A^_off x^) over SELL slices (warp per slice); ||b||^2 -> state
+__global__ void __launch_bounds__(KNT) k_init_r(const RItem* __restrict__ items, unsigned* cnt) {
+    __shared__ double shm[4 * (KNT / 32)];
+    const RItem& it = items[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int nsl = (it.n + 31) / 32;
+    double v[1] = {0.0};
+    for (int s = (blockIdx.x * KNT + threadIdx.x) / 32; s < nsl; s += gridDim.x * (KNT / 32)) {
+        const int row = 32 * s + lane;
+        const int len = it.len[s], base = it.base[s] + lane, cb = (32 * s / SIG) * SIG;
+        double acc = 0.0;
+        for (int k = 0; k < len; ++k) {
+            const int e = base + 32 * k;
+            const int c = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
+            acc = fma(it.val[e], it.x[c], acc);
+        }
+        if (row < it.n) {
+            const double bi = it.b[row];
+            it.r[row] = it.s[row] * bi - (it.x[row] + acc);
+            v[0] += bi * bi;
+        }
+    }
+    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) {
+        it.st->bn2 = v[0];
+        it.st->tol2 = it.st->rtol * it.st->rtol * v[0];
+    }
+}
+
+// x = D^-1/2 x^ into u_vert (canonical), or x0 untouched after a 0-iteration exit, 0 if b == 0
+__global__ void k_finalize(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    const double x0v = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        const int nat = it.inv[i];
+        if (S->iters == 0 && it.x0mode == 2 && S->bn2 != 0.0) continue;  // caller's guess stays
+        double xi;
+        if (S->bn2 == 0.0) xi = 0.0;
+        else if (S->iters == 0) xi = x0v;
+        else xi = it.s[i] * it.x[i];
+        it.u_vert[nat] = xi;
+    }
+}
+
+// true residual with the unscaled matrix (canonical rows); keeps s_i * r_true in r
+__global__ void __launch_bounds__(KNT) k_true_res(const RItem* __restrict__ items, unsigned* cnt) {
+    __shared__ double shm[4 * (KNT / 32)];
+    const RItem& it = items[blockIdx.y];
+    double v[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        const int nat = it.inv[i];
+        double ax = 0.0;
+        for (int e = it.urp[nat]; e < it.urp[nat + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+        const double ri = it.b[i] - ax;
+        it.r[i] = it.s[i] * ri;
+        v[0] += ri * ri;
+    }
+    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) it.st->res2 = v[0];
+}
+
+__global__ void k_copy_g(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    if (!it.g) return;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x)
+        it.u_vert[it.n + k] = it.g[k];
+}
+
+// ------------------------------------------------------------------ group barriers
 // MODE 2 (cooperative grid): flag-array barrier. Every CTA owns a 32-byte slot
 // {partial x, y, z, epoch} in it.part. Arrival = (optional partials) + gpu-scope fence +
 // epoch store into the CTA's own slot -- no serialized atomics on a shared counter.
-// Waiting = each thread polls one slot (ncta <= threads) until its epoch reaches the
-// barrier's epoch, then an acquire fence. Data published at epoch e is overwritten only at
-// epoch e+2 (reductions and plain barriers alternate), i.e. after every CTA has passed the
-// plain barrier e+1 that follows its reads.
+// Waiting = each thread polls one slot until its epoch reaches the barrier's epoch, then
+// an acquire fence. Data published at epoch e is overwritten only at epoch e+2
+// (reductions and plain barriers alternate), i.e. after every CTA has passed the plain
+// barrier e+1 that follows its reads.
 __device__ __forceinline__ void flag_arrive(const RItem& it, int rank, unsigned long long epoch, const double4* t) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -149,7 +270,7 @@ __device__ __forceinline__ void flag_arrive(const RItem& it, int rank, unsigned 
 }
 
 __device__ __forceinline__ void flag_wait(const RItem& it, unsigned long long epoch) {
-    for (int k = threadIdx.x; k < it.ncta; k += RNT) {
+    for (int k = threadIdx.x; k < it.ncta; k += blockDim.x) {
         volatile unsigned long long* E = (volatile unsigned long long*)(it.part + 4 * k + 3);
         while (*E < epoch) {
         }
@@ -180,22 +301,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// block sum of 4 values (fixed tree; result valid in every thread)
-__device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [NWARP][4] */) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
-        v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
-    }
+// block sum of 3 values (fixed tree; result valid in every thread)
+template <int NWARP>
+__device__ __forceinline__ double4 block_sum3(double4 v, double* sh /* [NWARP][4] */) {
+    v.x = warp_sum_d(v.x);
+    v.y = warp_sum_d(v.y);
+    v.z = warp_sum_d(v.z);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __syncthreads();
     if (lane == 0) {
         sh[4 * wid] = v.x;
         sh[4 * wid + 1] = v.y;
         sh[4 * wid + 2] = v.z;
-        sh[4 * wid + 3] = v.w;
     }
     __syncthreads();
     double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -204,17 +321,15 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double* sh /* [NWARP][4
         t.x += sh[4 * w];
         t.y += sh[4 * w + 1];
         t.z += sh[4 * w + 2];
-        t.w += sh[4 * w + 3];
     }
     return t;
 }
 
-// publish this CTA's partials (3 values), barrier, and sum all partials of the group in
-// a fixed order (identical in every CTA)
-template <int MODE>
+// publish this CTA's partials, barrier, and sum all partials of the group in a fixed order
+template <int MODE, int NT>
 __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, double4 loc, double* sh,
                                                 unsigned long long& epoch) {
-    double4 t = block_sum4(loc, sh);
+    double4 t = block_sum3<NT / 32>(loc, sh);
     if constexpr (MODE == 0) return t;
     if constexpr (MODE == 2) {
         ++epoch;
@@ -230,41 +345,39 @@ __device__ __forceinline__ double4 group_reduce(const RItem& it, int rank, doubl
         group_sync<MODE>(it, rank, epoch);
     }
     double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int k = threadIdx.x; k < it.ncta; k += RNT) {
+    for (int k = threadIdx.x; k < it.ncta; k += NT) {
         const double* P = it.part + 4 * k;
         a.x += __ldcg(P);
         a.y += __ldcg(P + 1);
         a.z += __ldcg(P + 2);
     }
-    return block_sum4(a, sh);
+    return block_sum3<NT / 32>(a, sh);
 }
 
-// SELL SpMV over the CTA's slices [S0, S1), y = src + A^_off src for each row.
-// KIND 0: w = y, partial (r.r, w.r, ||r/s||^2) with src = r.
-// KIND 1: r = s b - y (initial residual), partial (b.b) with src = x^0.
-template <int KIND>
-__device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, const double* __restrict__ src) {
+// w = r + A^_off r over the CTA's slices; partial (r.r, w.r, ||r/s||^2). Two slices per warp.
+template <int NWARP>
+__device__ __forceinline__ double4 spmv_w(const RItem& it, int S0, int S1, const int2* __restrict__ meta) {
     double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* __restrict__ val = it.val;
     const int16_t* __restrict__ c16 = it.c16;
     const int32_t* __restrict__ c32 = it.c32;
-    // two 32-row slices per warp and step: two independent load chains in flight
+    const double* __restrict__ r = it.r;
     for (int sa = S0 + 2 * warp; sa < S1; sa += 2 * NWARP) {
-        const int sb = sa + 1;
-        const bool hb = sb < S1;
+        const bool hb = sa + 1 < S1;
         int row[2], len[2], base[2], cb[2];
         double xi[2], si[2], acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int s = h ? sb : sa;
+            const int s = sa + h;
             const bool ok = h == 0 || hb;
+            const int2 md = ok ? meta[s - S0] : make_int2(0, 0);
             row[h] = (ok && 32 * s + lane < it.n) ? 32 * s + lane : -1;  // internal numbering
-            len[h] = ok ? it.len[s] : 0;
-            base[h] = ok ? it.base[s] + lane : 0;
+            len[h] = md.x;
+            base[h] = md.y + lane;
             cb[h] = (32 * s / SIG) * SIG;
             const int rr = row[h] >= 0 ? row[h] : 32 * sa;
-            xi[h] = __ldca(src + rr);
+            xi[h] = r[rr];
             si[h] = it.s[rr];
         }
         const int L = max(len[0], len[1]);
@@ -286,37 +399,33 @@ __device__ __forceinline__ double4 spmv_sell(const RItem& it, int S0, int S1, co
                 }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const double g = __ldca(src + c[q]);
-                if (q < 4) acc[0] = fma(v[q], g, acc[0]);
-                else acc[1] = fma(v[q], g, acc[1]);
+                const double gv = r[c[q]];
+                if (q < 4) acc[0] = fma(v[q], gv, acc[0]);
+                else acc[1] = fma(v[q], gv, acc[1]);
             }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (row[h] < 0) continue;
             const double y = xi[h] + acc[h];
-            if constexpr (KIND == 0) {
-                it.w[row[h]] = y;
-                const double ru = xi[h] / si[h];
-                loc.x += xi[h] * xi[h];
-                loc.y += y * xi[h];
-                loc.z += ru * ru;
-            } else {
-                const double bi = it.b[row[h]];
-                it.r[row[h]] = si[h] * bi - y;
-                loc.x += bi * bi;
-            }
+            it.w[row[h]] = y;
+            const double ru = xi[h] / si[h];
+            loc.x += xi[h] * xi[h];
+            loc.y += y * xi[h];
+            loc.z += ru * ru;
         }
     }
     return loc;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
-    k_pcg_resident(const RItem* __restrict__ items, int nitems, int vrows, int nvec) {
-    extern __shared__ double smem[];  // p[vrows] | s[vrows] | x[vrows]
+// ------------------------------------------------------------------ the CG loop
+template <int MODE, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_cg(const RItem* __restrict__ items, int nitems, int vrows, int nvec, int mrows) {
+    extern __shared__ double smem[];  // meta[mrows/32] (int2) | p[vrows] | s[vrows] | x[vrows]
+    constexpr int NWARP = NT / 32;
+    constexpr int RNT = NT;
     __shared__ double sh[4 * NWARP];
-    // ---- which item / rank
     int item = 0, rank = 0;
     if constexpr (MODE == 1) {
         unsigned cr, cid;
@@ -331,162 +440,119 @@ __global__ void __launch_bounds__(RNT, MODE >= 2 ? 2 : 1)
             if ((int)blockIdx.x >= items[k].cta0) item = k;
         rank = blockIdx.x - items[item].cta0;
     }
-    const RItem& it = items[item];
+    // the item descriptor lives in shared memory: its ~25 pointers are re-read from there
+    // instead of pinning registers (the 64-register cap of the 2-CTA/SM grid mode)
+    __shared__ RItem its;
+    if (threadIdx.x == 0) its = items[item];
+    __syncthreads();
+    const RItem& it = its;
     CgState* S = it.st;
     const int W0 = (int)((long long)it.nwin * rank / it.ncta);
     const int W1 = (int)((long long)it.nwin * (rank + 1) / it.ncta);
     const int R0 = min(it.n, W0 * SIG), R1 = min(it.n, W1 * SIG);
     const int S0 = R0 / 32, S1 = (R1 + 31) / 32;
-    double* P = nvec >= 2 ? smem : it.p + R0;
-    double* SV = nvec >= 2 ? smem + vrows : it.sv + R0;
-    double* X = nvec >= 3 ? smem + 2 * vrows : it.x + R0;
-    const double rtol = S->rtol;
-    const int max_iter = S->max_iter;
-    double x0v = 0.0;
-    if (it.x0mode == 1) x0v = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
+    int2* meta = (int2*)smem;
+    double* vbase = smem + (mrows / 32 + 1);
+    double* P = nvec >= 2 ? vbase : it.p + R0;
+    double* SV = nvec >= 2 ? vbase + vrows : it.sv + R0;
+    double* X = nvec >= 3 ? vbase + 2 * vrows : it.x + R0;
     const int tid = threadIdx.x;
-
-    // ---- init: x^0 (global, gathered by the first residual), r0 = s b - A^ x0, ||b||^2
+    for (int s = S0 + tid; s < S1; s += RNT) meta[s - S0] = make_int2(it.len[s], it.base[s]);
     for (int i = R0 + tid; i < R1; i += RNT) {
-        double x0 = (it.x0mode == 1) ? x0v : (it.x0mode == 2 ? it.u_vert[it.inv[i]] : 0.0);
-        const double xh = x0 / it.s[i];
-        it.x[i] = xh;
-        if (nvec >= 3) X[i - R0] = xh;
+        P[i - R0] = 0.0;
+        SV[i - R0] = 0.0;
+        if (nvec >= 3) X[i - R0] = it.x[i];
     }
+    __syncthreads();
+    const double tol2 = S->tol2, bn2 = S->bn2;
+    const int max_iter = S->max_iter;
+    int iters = S->iters, status = FEMI_OK;
     unsigned long long epoch = 0;
-    group_sync<MODE>(it, rank, epoch);
-    double4 tot = group_reduce<MODE>(it, rank, spmv_sell<1>(it, S0, S1, it.x), sh, epoch);
-    const double bn2 = tot.x;
-    const double tol2 = rtol * rtol * bn2;
-    int iters = 0, status = FEMI_OK, restarts = 0;
-    double res2 = 0.0;
-    for (;;) {  // (re)start: w = A^ r, p = s = 0
-        for (int i = R0 + tid; i < R1; i += RNT) {
-            P[i - R0] = 0.0;
-            SV[i - R0] = 0.0;
-        }
-        group_sync<MODE>(it, rank, epoch);  // r visible, partials consumed
-        tot = group_reduce<MODE>(it, rank, spmv_sell<0>(it, S0, S1, it.r), sh, epoch);
-        double gam = tot.x, del = tot.y, rho = tot.z;
-        double alpha = 0.0, beta = 0.0;
-        bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho);
-        if (!isfinite(gam) || !isfinite(bn2)) {
-            status = FEMI_E_NONFINITE;
-            run = false;
-        }
-        if (run) {
-            if (!(del > 0.0)) {
-                status = FEMI_E_NEG_CURVATURE;
-                run = false;
-            } else {
-                alpha = gam / del;
-            }
-        }
-        const bool tmr = g_pcg_timers_on && rank == 0 && tid == 0;
-        unsigned long long tl = tmr ? gtimer() : 0ull;
-        auto mark = [&](int k) {
-            if (tmr) {
-                const unsigned long long t = gtimer();
-                g_pcg_timers[k] += t - tl;
-                tl = t;
-            }
-        };
-        while (run) {
-            // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s (4 rows/thread in flight)
-            for (int base = R0 + tid; base < R1; base += 4 * RNT) {
-                double rv[4], wv[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = base + q * RNT;
-                    if (i < R1) {
-                        rv[q] = __ldca(it.r + i);
-                        wv[q] = __ldca(it.w + i);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = base + q * RNT;
-                    if (i < R1) {
-                        const int l = i - R0;
-                        const double pi = fma(beta, P[l], rv[q]);
-                        const double si = fma(beta, SV[l], wv[q]);
-                        P[l] = pi;
-                        SV[l] = si;
-                        X[l] = fma(alpha, pi, X[l]);
-                        it.r[i] = fma(-alpha, si, rv[q]);
-                    }
-                }
-            }
-            ++iters;
-            mark(0);
-            group_sync<MODE>(it, rank, epoch);  // r published
-            mark(1);
-            const double4 lsp = spmv_sell<0>(it, S0, S1, it.r);
-            mark(2);
-            tot = group_reduce<MODE>(it, rank, lsp, sh, epoch);
-            mark(3);
-            const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
-            if (!isfinite(gam2) || !isfinite(del2)) {
-                status = FEMI_E_NONFINITE;
-                break;
-            }
-            if (rho2 <= tol2) break;
-            if (iters >= max_iter) {
-                status = FEMI_E_NOT_CONVERGED;
-                break;
-            }
-            beta = gam2 / gam;
-            const double den = del2 - beta * gam2 / alpha;  // = p.A^p of the next direction
-            if (!(den > 0.0)) {
-                status = FEMI_E_NEG_CURVATURE;
-                break;
-            }
-            alpha = gam2 / den;
-            gam = gam2;
-        }
-        // ---- finalize: x = D^-1/2 x^ (or x0 untouched at 0 iterations, 0 when b == 0)
-        for (int i = R0 + tid; i < R1; i += RNT) {
-            const int nat = it.inv[i];
-            if (iters == 0 && it.x0mode == 2 && bn2 != 0.0) continue;  // caller's guess stays
-            double xi;
-            if (bn2 == 0.0) xi = 0.0;
-            else if (iters == 0) xi = x0v;
-            else xi = it.s[i] * X[i - R0];
-            it.u_vert[nat] = xi;
-        }
-        group_sync<MODE>(it, rank, epoch);  // u_vert visible
-        // true residual with the unscaled matrix (canonical rows); keeps s_i * r_true in r
-        double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
-        for (int i = R0 + tid; i < R1; i += RNT) {
-            const int nat = it.inv[i];
-            double ax = 0.0;
-            for (int e = it.urp[nat]; e < it.urp[nat + 1]; ++e)
-                ax = fma(it.uav[e], __ldca(it.u_vert + it.uci[e]), ax);
-            const double ri = it.b[i] - ax;
-            it.r[i] = it.s[i] * ri;
-            loc.x += ri * ri;
-        }
-        tot = group_reduce<MODE>(it, rank, loc, sh, epoch);
-        res2 = tot.x;
-        const bool fail = bn2 > 0.0 && !(res2 <= tol2);
-        if (!(status == FEMI_OK && iters > 0 && fail && iters < max_iter && restarts < 8)) break;
-        ++restarts;
-        for (int i = R0 + tid; i < R1; i += RNT) X[i - R0] = it.u_vert[it.inv[i]] / it.s[i];
+    double4 tot = group_reduce<MODE, NT>(it, rank, spmv_w<NWARP>(it, S0, S1, meta), sh, epoch);
+    double gam = tot.x, del = tot.y, rho = tot.z;
+    double alpha = 0.0, beta = 0.0;
+    bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho) && iters < max_iter;
+    if (!isfinite(gam) || !isfinite(bn2)) {
+        status = FEMI_E_NONFINITE;
+        run = false;
     }
+    if (run) {
+        if (!(del > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            run = false;
+        } else {
+            alpha = gam / del;
+        }
+    }
+    const bool tmr = g_pcg_timers_on && rank == 0 && tid == 0;
+    unsigned long long tl = tmr ? gtimer() : 0ull;
+    auto mark = [&](int k) {
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[k] += t - tl;
+            tl = t;
+        }
+    };
+    constexpr int UB = 6;  // rows per thread with loads in flight in the update phase
+    while (run) {
+        // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+        for (int b0 = R0 + tid; b0 < R1; b0 += UB * RNT) {
+            double rv[UB], wv[UB];
+#pragma unroll
+            for (int q = 0; q < UB; ++q) {
+                const int i = b0 + q * RNT;
+                if (i < R1) {
+                    rv[q] = it.r[i];
+                    wv[q] = it.w[i];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UB; ++q) {
+                const int i = b0 + q * RNT;
+                if (i < R1) {
+                    const int l = i - R0;
+                    const double pi = fma(beta, P[l], rv[q]);
+                    const double si = fma(beta, SV[l], wv[q]);
+                    P[l] = pi;
+                    SV[l] = si;
+                    X[l] = fma(alpha, pi, X[l]);
+                    it.r[i] = fma(-alpha, si, rv[q]);
+                }
+            }
+        }
+        ++iters;
+        mark(0);
+        group_sync<MODE>(it, rank, epoch);  // r published
+        mark(1);
+        const double4 lsp = spmv_w<NWARP>(it, S0, S1, meta);
+        mark(2);
+        tot = group_reduce<MODE, NT>(it, rank, lsp, sh, epoch);
+        mark(3);
+        const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
+        if (!isfinite(gam2) || !isfinite(del2)) {
+            status = FEMI_E_NONFINITE;
+            break;
+        }
+        if (rho2 <= tol2) break;
+        if (iters >= max_iter) {
+            status = FEMI_E_NOT_CONVERGED;
+            break;
+        }
+        beta = gam2 / gam;
+        const double den = del2 - beta * gam2 / alpha;  // = p.A^p of the next direction
+        if (!(den > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            break;
+        }
+        alpha = gam2 / den;
+        gam = gam2;
+    }
+    if (nvec >= 3)
+        for (int i = R0 + tid; i < R1; i += RNT) it.x[i] = X[i - R0];
     if (rank == 0 && tid == 0) {
         S->iters = iters;
         S->status = status;
-        S->res2 = res2;
-        S->bn2 = bn2;
-        S->active = 0;
     }
-}
-
-__global__ void k_copy_g(int B, const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    if (!it.g) return;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x)
-        it.u_vert[it.n + k] = it.g[k];
 }
 
 struct Workspace {
@@ -502,41 +568,39 @@ int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
 int g_nvec_max = 3;
-int g_l2_persist_mb = 0;
+int g_shape = 0;
 
 }  // namespace
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters) {
+    // grid-mode shapes (threads per CTA, CTAs per SM); FEMI_CG_SHAPE selects one for experiments
+    static void* const grid_fn[3] = {(void*)k_cg<2, 512, 2>, (void*)k_cg<2, 768, 1>, (void*)k_cg<2, 1024, 1>};
+    static const int grid_nt[3] = {512, 768, 1024};
+    static const int grid_per_sm[3] = {2, 1, 1};
     if (g_smem_optin < 0) {
         int dev = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
-        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FEMI_CUDA(cudaFuncSetAttribute(k_cg<0, RNT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        g_smem_optin - 2048));
-        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FEMI_CUDA(cudaFuncSetAttribute(k_cg<1, RNT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        g_smem_optin - 2048));
-        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        FEMI_CUDA(cudaFuncSetAttribute(k_pcg_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_smem_optin / 2 - 2048));
+        FEMI_CUDA(cudaFuncSetAttribute(k_cg<1, RNT, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         const char* tm = std::getenv("FEMI_PCG_TIMERS");
         g_timers = tm && tm[0] == '1';
         const char* nv = std::getenv("FEMI_PCG_NVEC");  // experiments: max vectors kept in smem
         if (nv) g_nvec_max = std::atoi(nv);
-        const char* lp = std::getenv("FEMI_L2_PERSIST");  // experiments: L2 persistence window (MB)
-        if (lp) g_l2_persist_mb = std::atoi(lp);
-        if (g_l2_persist_mb > 0) {
-            int maxp = 0;
-            FEMI_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-            const size_t want = std::min<size_t>((size_t)g_l2_persist_mb << 20, (size_t)maxp);
-            FEMI_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-            std::fprintf(stderr, "[femi] persisting L2 max %d MB, set %zu MB\n", maxp >> 20, want >> 20);
-        }
+        const char* sp = std::getenv("FEMI_CG_SHAPE");
+        if (sp) g_shape = std::max(0, std::min(2, std::atoi(sp)));
+        for (int k = 0; k < 3; ++k)
+            FEMI_CUDA(cudaFuncSetAttribute(grid_fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           g_smem_optin / grid_per_sm[k] - 2048));
         int per_sm = 0;
-        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<2>, RNT,
-                                                                g_smem_optin / 2 - 2048));
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_fn[g_shape], grid_nt[g_shape],
+                                                                g_smem_optin / grid_per_sm[g_shape] - 2048));
         g_occ_grid = std::max(1, per_sm) * g_nsm;
     }
     // ---- launch shape: one huge system -> cooperative grid; otherwise one cluster per item
@@ -557,7 +621,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         mode = ncta_item == 1 ? 0 : 1;
     }
     const int grid = B * ncta_item;
-    // shared-memory residency of p, s (and x): as many vectors as fit the per-CTA budget
+    // rows of the largest CTA; shared memory: slice metadata, then as many of p, s, x as fit
     int64_t vrows = 0;
     for (int b = 0; b < B; ++b) {
         const int nw = S[b]->nwin;
@@ -566,19 +630,21 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             vrows = std::max(vrows, std::min(S[b]->n_u, w1 * SIG) - std::min(S[b]->n_u, w0 * SIG));
         }
     }
-    const size_t budget = (size_t)(mode == 2 ? g_smem_optin / 2 - 2048 : g_smem_optin - 2048);
+    const int mrows = (int)(vrows + 32);
+    const size_t meta_bytes = sizeof(double) * (mrows / 32 + 1);
+    const size_t budget = (size_t)(mode == 2 ? g_smem_optin / grid_per_sm[g_shape] - 2048 : g_smem_optin - 2048);
     int nvec = g_nvec_max;
-    while (nvec >= 2 && sizeof(double) * (nvec * (size_t)vrows) > budget) --nvec;
+    while (nvec >= 2 && meta_bytes + sizeof(double) * (nvec * (size_t)vrows) > budget) --nvec;
     if (nvec < 2) nvec = 0;
-    const size_t smem_bytes = sizeof(double) * ((size_t)nvec * vrows);
+    const size_t smem_bytes = meta_bytes + sizeof(double) * ((size_t)nvec * vrows);
 
-    // ---- workspace: per item b, x, r, w, b (+ p, s) vectors, partials, barrier, state
+    // ---- workspace
     std::vector<RItem> items(B);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    size_t total = al(sizeof(RItem) * B) + al(sizeof(CgState) * B);
+    size_t total = al(sizeof(RItem) * B) + al(sizeof(CgState) * B) + al(sizeof(unsigned) * 2 * B);
     for (int b = 0; b < B; ++b)
         total += al(sizeof(double) * (S[b]->n_u + 1)) * (nvec == 0 ? 6 : 4) + al(sizeof(double) * 4 * ncta_item) +
-                 al(2 * sizeof(unsigned));
+                 al(sizeof(double) * KGRID);
     Workspace ws;
     ws.st = st;
     FEMI_CUDA(cudaMallocAsync(&ws.base, total, st));
@@ -590,6 +656,9 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     };
     RItem* d_items = (RItem*)take(sizeof(RItem) * B);
     CgState* d_state = (CgState*)take(sizeof(CgState) * B);
+    unsigned* d_cnt = (unsigned*)take(sizeof(unsigned) * 2 * B);
+    char* part_lo = nullptr;
+    char* part_hi = nullptr;
     for (int b = 0; b < B; ++b) {
         femi_system_s* s = S[b];
         RItem& it = items[b];
@@ -617,7 +686,9 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.p = nvec == 0 ? (double*)take(vb) : nullptr;
         it.sv = nvec == 0 ? (double*)take(vb) : nullptr;
         it.part = (double*)take(sizeof(double) * 4 * ncta_item);
-        it.bar = (unsigned*)take(2 * sizeof(unsigned));
+        if (!part_lo) part_lo = (char*)it.part;
+        part_hi = (char*)it.part + sizeof(double) * 4 * ncta_item;
+        it.red = (double*)take(sizeof(double) * KGRID);
         it.st = d_state + b;
         it.n = (int32_t)s->n_u;
         it.m = (int32_t)s->m;
@@ -627,91 +698,101 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.x0mode = (it.g == nullptr && o.x0 == 1) ? 0 : o.x0;
     }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
-    for (int b = 0; b < B; ++b)  // partial/epoch slots must start at epoch 0
-        FEMI_CUDA(cudaMemsetAsync(items[b].part, 0, sizeof(double) * 4 * ncta_item, st));
+    FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * 2 * B, st));
 
-    // ---- launches: reset, min/max(g), b, resident CG, mask copy
+    // ---- setup launches
+    const unsigned gy = (unsigned)B;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nmax + KNT - 1) / KNT, KGRID / B));
     k_reset<<<(B + 127) / 128, 128, 0, st>>>(B, d_state, o.rtol, o.max_iter);
     count_launches(1);
     if (o.x0 == 1) {
         int64_t mmax = 0;
         for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
-        int gb = (int)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296));
-        k_minmax<<<gb, 256, 0, st>>>(B, d_items);
+        k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296)), 256, 0, st>>>(B, d_items);
         count_launches(1);
     }
-    {
-        dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>((nmax + 255) / 256, 592)), B);
-        k_rhs<<<gg, 256, 0, st>>>(B, d_items);
-        count_launches(1);
+    if (nmax > 0) {
+        k_rhs<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+        k_init_x<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+        k_init_r<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
+        count_launches(3);
     }
     FEMI_CUDA(cudaGetLastError());
-    if (nmax > 0) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[2];
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(RNT);
-        cfg.dynamicSmemBytes = smem_bytes;
-        cfg.stream = st;
-        cfg.attrs = attr;
-        cfg.numAttrs = 0;
-        const int vr = (int)vrows;
-        cudaError_t e;
-        if (g_timers) {
-            unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            int on = 1;
-            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
-            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-        }
-        if (mode == 2) {
-            attr[0].id = cudaLaunchAttributeCooperative;
-            attr[0].val.cooperative = 1;
-            cfg.numAttrs = 1;
-            if (g_l2_persist_mb > 0 && S[0]->sell_nnz > 0) {  // keep the SELL values L2-resident
-                const size_t bytes = sizeof(double) * (size_t)S[0]->sell_nnz;
-                const size_t lim = (size_t)g_l2_persist_mb << 20;
-                attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-                attr[1].val.accessPolicyWindow.base_ptr = S[0]->sell_val;
-                attr[1].val.accessPolicyWindow.num_bytes = bytes;
-                attr[1].val.accessPolicyWindow.hitRatio = bytes <= lim ? 1.0f : (float)lim / (float)bytes;
-                attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-                attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-                cfg.numAttrs = 2;
+    std::vector<CgState> hs(B);
+    int restarts = 0;
+    for (;;) {
+        if (nmax > 0) {
+            FEMI_CUDA(cudaMemsetAsync(part_lo, 0, part_hi - part_lo, st));  // barrier slots at epoch 0
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(mode == 2 ? grid_nt[g_shape] : RNT);
+            cfg.dynamicSmemBytes = smem_bytes;
+            cfg.stream = st;
+            cfg.attrs = attr;
+            cfg.numAttrs = 0;
+            const int vr = (int)vrows;
+            if (g_timers) {
+                unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int on = 1;
+                FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+                FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
             }
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<2>, (const RItem*)d_items, B, vr, nvec);
-        } else if (mode == 1) {
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = ncta_item;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.numAttrs = 1;
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<1>, (const RItem*)d_items, B, vr, nvec);
-        } else {
-            e = cudaLaunchKernelEx(&cfg, k_pcg_resident<0>, (const RItem*)d_items, B, vr, nvec);
+            cudaError_t e;
+            if (mode == 2) {
+                attr[0].id = cudaLaunchAttributeCooperative;
+                attr[0].val.cooperative = 1;
+                cfg.numAttrs = 1;
+                const RItem* di = d_items;
+                int bb = B;
+                void* args[5] = {(void*)&di, (void*)&bb, (void*)&vr, (void*)&nvec, (void*)&mrows};
+                e = cudaLaunchKernelExC(&cfg, grid_fn[g_shape], args);
+            } else if (mode == 1) {
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = ncta_item;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.numAttrs = 1;
+                e = cudaLaunchKernelEx(&cfg, k_cg<1, RNT, 1>, (const RItem*)d_items, B, vr, nvec, mrows);
+            } else {
+                e = cudaLaunchKernelEx(&cfg, k_cg<0, RNT, 1>, (const RItem*)d_items, B, vr, nvec, mrows);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "k_cg launch");
+            k_finalize<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+            k_true_res<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt + B);
+            count_launches(3);
+            FEMI_CUDA(cudaGetLastError());
         }
-        if (e != cudaSuccess) return cuda_fail(e, "k_pcg_resident launch");
-        count_launches(1);
+        FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        if (g_timers && nmax > 0) {
+            unsigned long long t[8];
+            FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
+            const double it_n = std::max(1, hs[0].iters);
+            std::fprintf(stderr,
+                         "[femi pcg timers] mode %d ctas %d nvec %d iters %d | per iter us: U %.2f sync %.2f spmv "
+                         "%.2f reduce %.2f\n",
+                         mode, grid, nvec, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3,
+                         t[3] / it_n / 1e3);
+        }
+        // restart the items whose true residual misses rtol (recursion drift), from the current iterate
+        bool again = false;
+        for (int b = 0; b < B; ++b) {
+            const CgState& s = hs[b];
+            const bool fail = s.bn2 > 0.0 && !(s.res2 <= s.tol2);
+            again |= S[b]->n_u > 0 && s.status == FEMI_OK && s.iters > 0 && s.iters < s.max_iter && fail;
+        }
+        if (!again || restarts >= 8) break;
+        ++restarts;
+        // k_true_res left r = s * r_true and x^ is current: the CG loop restarts from there.
+        // Items that already passed run zero iterations (rho <= tol2 at entry).
     }
     {
         int64_t mmax = 1;
         for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
-        dim3 gg((unsigned)std::min<int64_t>((mmax + 255) / 256, 296), B);
-        k_copy_g<<<gg, 256, 0, st>>>(B, d_items);
+        k_copy_g<<<dim3((unsigned)std::min<int64_t>((mmax + 255) / 256, 296), gy), 256, 0, st>>>(d_items);
         count_launches(1);
-    }
-    FEMI_CUDA(cudaGetLastError());
-    std::vector<CgState> hs(B);
-    FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
-    FEMI_CUDA(cudaStreamSynchronize(st));
-    if (g_timers && nmax > 0) {
-        unsigned long long t[8];
-        FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
-        const double it_n = std::max(1, hs[0].iters);
-        std::fprintf(stderr,
-                     "[femi pcg timers] mode %d ctas %d nvec %d iters %d | per iter us: U %.2f sync %.2f spmv %.2f "
-                     "reduce %.2f\n",
-                     mode, grid, nvec, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3,
-                     t[3] / it_n / 1e3);
+        FEMI_CUDA(cudaGetLastError());
     }
     femi_status ret = FEMI_OK;
     int64_t tot = 0;
