@@ -657,8 +657,9 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     RItem* d_items = (RItem*)take(sizeof(RItem) * B);
     CgState* d_state = (CgState*)take(sizeof(CgState) * B);
     unsigned* d_cnt = (unsigned*)take(sizeof(unsigned) * 2 * B);
-    char* part_lo = nullptr;
-    char* part_hi = nullptr;
+    // barrier/partial slots of all items in one contiguous block (zeroed before each k_cg)
+    const size_t part_bytes = sizeof(double) * 4 * (size_t)ncta_item * B;
+    char* part_lo = take(part_bytes);
     for (int b = 0; b < B; ++b) {
         femi_system_s* s = S[b];
         RItem& it = items[b];
@@ -685,9 +686,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.w = (double*)take(vb);
         it.p = nvec == 0 ? (double*)take(vb) : nullptr;
         it.sv = nvec == 0 ? (double*)take(vb) : nullptr;
-        it.part = (double*)take(sizeof(double) * 4 * ncta_item);
-        if (!part_lo) part_lo = (char*)it.part;
-        part_hi = (char*)it.part + sizeof(double) * 4 * ncta_item;
+        it.part = (double*)(part_lo + sizeof(double) * 4 * (size_t)ncta_item * b);
         it.red = (double*)take(sizeof(double) * KGRID);
         it.st = d_state + b;
         it.n = (int32_t)s->n_u;
@@ -722,7 +721,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     int restarts = 0;
     for (;;) {
         if (nmax > 0) {
-            FEMI_CUDA(cudaMemsetAsync(part_lo, 0, part_hi - part_lo, st));  // barrier slots at epoch 0
+            FEMI_CUDA(cudaMemsetAsync(part_lo, 0, part_bytes, st));  // barrier slots at epoch 0
             cudaLaunchConfig_t cfg = {};
             cudaLaunchAttribute attr[1];
             cfg.gridDim = dim3(grid);
