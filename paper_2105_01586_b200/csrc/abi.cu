@@ -181,6 +181,7 @@ void femi_mesh_free(femi_mesh mesh) { delete mesh; }
 void femi_system_free(femi_system sys) {
     if (!sys) return;
     cudaDeviceSynchronize();
+    pcg_cache_free(sys);
     for (void* p : sys->allocs) cudaFree(p);
     delete sys;
 }

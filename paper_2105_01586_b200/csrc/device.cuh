@@ -152,6 +152,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
                           int32_t* const* best, double* const* sse, cudaStream_t st);
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st);
 femi_status build_owner_tables(femi_system_s* S, cudaStream_t st);
+void pcg_cache_free(femi_system_s* S);  // graph-mode workspace + instantiated graphs
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters);

@@ -71,6 +71,8 @@ struct RItem {
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
     int32_t n, m, cta0, ncta, nwin, x0mode;
+    double rtol;  // graph mode reads the options from the item (the graph is reused)
+    int32_t max_iter, pad2;
 };
 
 constexpr int RNT = 512;  // threads per CTA of the persistent solver (block/cluster modes)
@@ -419,9 +421,10 @@ __device__ __forceinline__ double4 spmv_w(const RItem& it, int S0, int S1, const
 }
 
 // ------------------------------------------------------------------ the CG loop
-template <int MODE, int NT, int MINB>
+template <int MODE, int NT, int MINB, int NV>
 __global__ void __launch_bounds__(NT, MINB)
-    k_cg(const RItem* __restrict__ items, int nitems, int vrows, int nvec, int mrows) {
+    k_cg(const RItem* __restrict__ items, int nitems, int vrows, int nvec_unused, int mrows) {
+    constexpr int nvec = NV;  // vectors resident in shared memory (p, s[, x]); compile-time
     extern __shared__ double smem[];  // meta[mrows/32] (int2) | p[vrows] | s[vrows] | x[vrows]
     constexpr int NWARP = NT / 32;
     constexpr int RNT = NT;
@@ -555,6 +558,244 @@ __global__ void __launch_bounds__(NT, MINB)
     }
 }
 
+// ------------------------------------------------------------------ graph mode
+// Large single systems (C5): the CG loop is a device-driven WHILE node of a CUDA graph whose
+// body is two lean, full-occupancy kernels -- k_gu (update, element-wise) and k_gs (SELL
+// SpMV + dots; its last block turns the partials into alpha/beta/convergence in a fixed
+// order and sets the loop condition). Lean kernels run 64 warps/SM, i.e. 2-3x the memory-
+// level parallelism of the persistent kernel, which is what the latency-bound SpMV needs.
+constexpr int GNT = 256;
+
+__global__ void k_reset_items(int B, const RItem* __restrict__ items) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    CgState s = {};
+    s.rtol = items[b].rtol;
+    s.max_iter = items[b].max_iter;
+    s.kmin = ~0ull;
+    s.kmax = 0ull;
+    *items[b].st = s;
+}
+
+// p = s = 0 (start and restart of the recurrence)
+__global__ void k_zero_ps(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        it.p[i] = 0.0;
+        it.sv[i] = 0.0;
+    }
+}
+
+// U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+__global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    if (!S->active) return;
+    const double alpha = S->alpha, beta = S->beta;
+    double* __restrict__ r = it.r;
+    const double* __restrict__ w = it.w;
+    double* __restrict__ p = it.p;
+    double* __restrict__ sv = it.sv;
+    double* __restrict__ x = it.x;
+    const int n = it.n, stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+        const int j = i + stride;
+        const bool hj = j < n;
+        const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i], xi = x[i];
+        double rj = 0.0, wj = 0.0, pj0 = 0.0, sj0 = 0.0, xj = 0.0;
+        if (hj) {
+            rj = r[j];
+            wj = w[j];
+            pj0 = p[j];
+            sj0 = sv[j];
+            xj = x[j];
+        }
+        const double pi = fma(beta, pi0, ri), si = fma(beta, si0, wi);
+        p[i] = pi;
+        sv[i] = si;
+        x[i] = fma(alpha, pi, xi);
+        r[i] = fma(-alpha, si, ri);
+        if (hj) {
+            const double pj = fma(beta, pj0, rj), sj = fma(beta, sj0, wj);
+            p[j] = pj;
+            sv[j] = sj;
+            x[j] = fma(alpha, pj, xj);
+            r[j] = fma(-alpha, sj, rj);
+        }
+    }
+}
+
+// S: w = r + A^_off r (SELL, two slices per warp) and the dots; the last block updates the
+// recurrence scalars and (FIRST: starts it) and sets the WHILE condition when every item has
+// reported (any item still active -> 1).
+template <bool FIRST>
+__global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, int B, double* __restrict__ part,
+                                           unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+    __shared__ double shm[4 * (GNT / 32)];
+    __shared__ int last;
+    const RItem& it = items[blockIdx.y];
+    CgState* S = it.st;
+    const bool act = FIRST || S->active;
+    double v[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        const int lane = threadIdx.x & 31;
+        const int nsl = (it.n + 31) / 32;
+        const int gw = (blockIdx.x * GNT + threadIdx.x) >> 5, nw = (gridDim.x * GNT) >> 5;
+        const double* __restrict__ r = it.r;
+        for (int sa = 2 * gw; sa < nsl; sa += 2 * nw) {
+            const bool hb = sa + 1 < nsl;
+            int row[2], len[2], base[2], cb[2];
+            double xi[2], si[2], acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int s = sa + hh;
+                const bool ok = hh == 0 || hb;
+                row[hh] = (ok && 32 * s + lane < it.n) ? 32 * s + lane : -1;
+                len[hh] = ok ? it.len[s] : 0;
+                base[hh] = ok ? it.base[s] + lane : 0;
+                cb[hh] = (32 * s / SIG) * SIG;
+                const int rr = row[hh] >= 0 ? row[hh] : 32 * sa;
+                xi[hh] = r[rr];
+                si[hh] = it.s[rr];
+            }
+            const int L = max(len[0], len[1]);
+            for (int k0 = 0; k0 < L; k0 += 4) {
+                double vv[8];
+                int c[8];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = base[hh] + 32 * (k0 + q);
+                        if (k0 + q < len[hh]) {
+                            vv[4 * hh + q] = it.val[e];
+                            c[4 * hh + q] = it.c16 ? cb[hh] + (int)it.c16[e] : it.c32[e];
+                        } else {
+                            vv[4 * hh + q] = 0.0;
+                            c[4 * hh + q] = 32 * sa;
+                        }
+                    }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double gv = r[c[q]];
+                    if (q < 4) acc[0] = fma(vv[q], gv, acc[0]);
+                    else acc[1] = fma(vv[q], gv, acc[1]);
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (row[hh] < 0) continue;
+                const double y = xi[hh] + acc[hh];
+                it.w[row[hh]] = y;
+                const double ru = xi[hh] / si[hh];
+                v[0] += xi[hh] * xi[hh];
+                v[1] += y * xi[hh];
+                v[2] += ru * ru;
+            }
+        }
+    }
+    // block partial -> part[item][block]; last block of the item reduces in block order
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v[q] = warp_sum_d(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) shm[4 * wid + q] = v[q];
+    __syncthreads();
+    double* P = part + 4 * (size_t)gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 3; ++q) {
+            double t = 0.0;
+            for (int w = 0; w < GNT / 32; ++w) t += shm[4 * w + q];
+            P[4 * blockIdx.x + q] = t;
+        }
+        __threadfence();
+        last = atomicAdd(&S->cnt[0], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double tot[3] = {0.0, 0.0, 0.0};
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += GNT)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) tot[q] += __ldcg(P + 4 * b + q);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) tot[q] = warp_sum_d(tot[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) shm[4 * wid + q] = tot[q];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double gam2 = 0.0, del2 = 0.0, rho2 = 0.0;
+    for (int w = 0; w < GNT / 32; ++w) {
+        gam2 += shm[4 * w];
+        del2 += shm[4 * w + 1];
+        rho2 += shm[4 * w + 2];
+    }
+    S->cnt[0] = 0;
+    int active = 0;
+    if (act) {
+        if (FIRST) {
+            const bool fin = isfinite(gam2) && isfinite(S->bn2);
+            active = (S->bn2 > 0.0 && rho2 > S->tol2 && fin && S->iters < S->max_iter) ? 1 : 0;
+            if (!fin) S->status = FEMI_E_NONFINITE;
+            if (active && !(del2 > 0.0)) {
+                S->status = FEMI_E_NEG_CURVATURE;
+                active = 0;
+            }
+            if (active) {
+                S->alpha = gam2 / del2;
+                S->beta = 0.0;
+                S->rr = gam2;
+            }
+        } else {
+            S->iters += 1;
+            if (!isfinite(gam2) || !isfinite(del2)) {
+                S->status = FEMI_E_NONFINITE;
+            } else if (rho2 <= S->tol2) {
+                // converged
+            } else if (S->iters >= S->max_iter) {
+                S->status = FEMI_E_NOT_CONVERGED;
+            } else {
+                const double beta = gam2 / S->rr;
+                const double den = del2 - beta * gam2 / S->alpha;
+                if (!(den > 0.0)) {
+                    S->status = FEMI_E_NEG_CURVATURE;
+                } else {
+                    S->beta = beta;
+                    S->alpha = gam2 / den;
+                    S->rr = gam2;
+                    active = 1;
+                }
+            }
+        }
+        S->active = active;
+    }
+    // all items reported? -> loop condition
+    __threadfence();
+    if (active) atomicAdd(gcnt + 1, 1u);
+    __threadfence();
+    if (atomicAdd(gcnt, 1u) == (unsigned)B - 1) {
+        __threadfence();
+        const unsigned any = atomicExch(gcnt + 1, 0u);
+        gcnt[0] = 0;
+        cudaGraphSetConditional(h, any ? 1u : 0u);
+    }
+}
+
+struct GraphCache {
+    void* ws = nullptr;
+    RItem* d_items = nullptr;
+    CgState* d_state = nullptr;
+    unsigned* d_cnt = nullptr;  // [0,1]: init/true-res counters; [2,3]: loop condition counters
+    double* d_part = nullptr;
+    cudaGraphExec_t main = nullptr, restart = nullptr;
+    RItem item{};
+    int gs_blocks = 0, gx = 0;
+};
+
 struct Workspace {
     void* base = nullptr;
     cudaStream_t st = nullptr;
@@ -568,38 +809,234 @@ int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
 int g_nvec_max = 3;
-int g_shape = 0;
+int g_shape = 1;
 
 }  // namespace
+
+namespace {
+
+femi_status add_kernel(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid, dim3 block, void** args,
+                       cudaGraphNode_t* out) {
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeKernel;
+    p.kernel.func = fn;
+    p.kernel.gridDim = grid;
+    p.kernel.blockDim = block;
+    p.kernel.sharedMemBytes = 0;
+    p.kernel.kernelParams = args;
+    FEMI_CUDA(cudaGraphAddNode(out, gr, dep, dep ? 1 : 0, &p));
+    return FEMI_OK;
+}
+
+// builds [prologue...] -> k_gs<true> -> WHILE{ k_gu -> k_gs<false> } -> finalize -> true_res -> copy_g
+femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
+    cudaGraph_t gr;
+    FEMI_CUDA(cudaGraphCreate(&gr, 0));
+    cudaGraphConditionalHandle h;
+    FEMI_CUDA(cudaGraphConditionalHandleCreate(&h, gr, 0, cudaGraphCondAssignDefault));
+    RItem* di = C.d_items;
+    int one = 1;
+    double* part = C.d_part;
+    unsigned* cnt0 = C.d_cnt;
+    unsigned* cnt1 = C.d_cnt + 1;
+    unsigned* gcnt = C.d_cnt + 2;
+    void* a_items[1] = {&di};
+    void* a_reset[2] = {&one, &di};
+    void* a_cnt0[2] = {&di, &cnt0};
+    void* a_cnt1[2] = {&di, &cnt1};
+    void* a_gs[5] = {&di, &one, &part, &gcnt, &h};
+    const dim3 gk(C.gx, 1), bk(KNT);
+    cudaGraphNode_t prev = nullptr, nd;
+    cudaGraphNode_t* dep = nullptr;
+    auto chain = [&](void* fn, dim3 gg, dim3 bb, void** args) -> femi_status {
+        femi_status s = add_kernel(gr, dep, fn, gg, bb, args, &nd);
+        prev = nd;
+        dep = &prev;
+        return s;
+    };
+    femi_status s = FEMI_OK;
+    if (!restart) {
+        if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
+        void* a_mm[2] = {&one, &di};
+        if ((s = chain((void*)k_minmax, dim3(296), dim3(256), a_mm))) return s;
+        if ((s = chain((void*)k_rhs, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
+    }
+    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
+    if (!restart)
+        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+    if ((s = chain((void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs))) return s;
+    {
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        FEMI_CUDA(cudaGraphAddNode(&nd, gr, dep, 1, &cp));
+        prev = nd;
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraphNode_t u, sn;
+        if ((s = add_kernel(body, nullptr, (void*)k_gu, dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT), a_items,
+                            &u)))
+            return s;
+        if ((s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn))) return s;
+    }
+    if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
+    if ((s = chain((void*)k_true_res, gk, bk, a_cnt1))) return s;
+    if ((s = chain((void*)k_copy_g, dim3(296), dim3(256), a_items))) return s;
+    FEMI_CUDA(cudaGraphInstantiate(out, gr, 0));
+    FEMI_CUDA(cudaGraphDestroy(gr));
+    return FEMI_OK;
+}
+
+femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, double* u_vert,
+                        const femi_cg_opts& o, int32_t* iters, double* relres, cudaStream_t st,
+                        int64_t* total_iters) {
+    GraphCache* C = (GraphCache*)S->scratch;
+    const int64_t n = S->n_u;
+    if (!C) {
+        C = new GraphCache();
+        const int nsl = (int)((n + 31) / 32);
+        C->gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + KNT - 1) / KNT, KGRID));
+        C->gs_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)),
+                                                                   148 * 8));
+        auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        const size_t vb = al(sizeof(double) * (n + 1));
+        const size_t bytes = al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
+                             al(sizeof(double) * 4 * C->gs_blocks) + al(sizeof(double) * KGRID) + 6 * vb;
+        FEMI_CUDA(cudaMalloc(&C->ws, bytes));
+        char* cur = (char*)C->ws;
+        auto take = [&](size_t x) {
+            char* p = cur;
+            cur += al(x);
+            return p;
+        };
+        C->d_items = (RItem*)take(sizeof(RItem));
+        C->d_state = (CgState*)take(sizeof(CgState));
+        C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
+        C->d_part = (double*)take(sizeof(double) * 4 * C->gs_blocks);
+        RItem& it = C->item;
+        it.red = (double*)take(sizeof(double) * KGRID);
+        it.b = (double*)take(vb);
+        it.x = (double*)take(vb);
+        it.r = (double*)take(vb);
+        it.w = (double*)take(vb);
+        it.p = (double*)take(vb);
+        it.sv = (double*)take(vb);
+        it.inv = S->sell_inv;
+        it.len = S->sell_len;
+        it.base = S->sell_base;
+        it.val = S->sell_val;
+        it.c16 = S->sell_c16;
+        it.c32 = S->sell_c32;
+        it.s = S->s_int;
+        it.urp = S->uu_rowptr;
+        it.uci = S->uu_col;
+        it.uav = S->uu_val;
+        it.krp = S->uk_rowptr;
+        it.kci = S->uk_col;
+        it.kav = S->uk_val;
+        it.part = nullptr;
+        it.st = C->d_state;
+        it.n = (int32_t)n;
+        it.m = (int32_t)S->m;
+        it.cta0 = 0;
+        it.ncta = 1;
+        it.nwin = S->nwin;
+        FEMI_CUDA(cudaMemset(C->d_cnt, 0, sizeof(unsigned) * 4));
+        S->scratch = C;
+        femi_status s = build_graph(*C, false, &C->main);
+        if (s == FEMI_OK) s = build_graph(*C, true, &C->restart);
+        if (s != FEMI_OK) return s;
+    }
+    RItem it = C->item;
+    it.g = g;
+    it.bin = bin;
+    it.u_vert = u_vert;
+    it.x0mode = (g == nullptr && o.x0 == 1) ? 0 : o.x0;
+    it.rtol = o.rtol;
+    it.max_iter = o.max_iter;
+    FEMI_CUDA(cudaMemcpyAsync(C->d_items, &it, sizeof(RItem), cudaMemcpyHostToDevice, st));
+    FEMI_CUDA(cudaGraphLaunch(C->main, st));
+    count_launches(11);
+    CgState hs;
+    for (int restarts = 0;; ++restarts) {
+        FEMI_CUDA(cudaMemcpyAsync(&hs, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        const bool fail = hs.bn2 > 0.0 && !(hs.res2 <= hs.tol2);
+        if (!(hs.status == FEMI_OK && hs.iters > 0 && hs.iters < hs.max_iter && fail) || restarts >= 8) break;
+        FEMI_CUDA(cudaGraphLaunch(C->restart, st));  // from the current iterate (r = s * r_true)
+        count_launches(6);
+    }
+    count_launches(2 * (int64_t)hs.iters);
+    const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
+    if (iters) *iters = hs.iters;
+    if (relres) *relres = rel;
+    if (total_iters) *total_iters = hs.iters;
+    femi_status sb = (femi_status)hs.status;
+    if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
+    if (sb != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)sb) + ")");
+    return sb;
+}
+
+}  // namespace
+
+void pcg_cache_free(femi_system_s* S) {
+    GraphCache* C = (GraphCache*)S->scratch;
+    if (!C) return;
+    if (C->main) cudaGraphExecDestroy(C->main);
+    if (C->restart) cudaGraphExecDestroy(C->restart);
+    if (C->ws) cudaFree(C->ws);
+    delete C;
+    S->scratch = nullptr;
+}
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters) {
-    // grid-mode shapes (threads per CTA, CTAs per SM); FEMI_CG_SHAPE selects one for experiments
-    static void* const grid_fn[3] = {(void*)k_cg<2, 512, 2>, (void*)k_cg<2, 768, 1>, (void*)k_cg<2, 1024, 1>};
-    static const int grid_nt[3] = {512, 768, 1024};
-    static const int grid_per_sm[3] = {2, 1, 1};
+    {
+        static int graph_mode = -1;  // FEMI_PCG_MODE=persistent forces the persistent kernel
+        if (graph_mode < 0) {
+            const char* pm = std::getenv("FEMI_PCG_MODE");
+            graph_mode = (pm && std::string(pm) == "persistent") ? 0 : 1;
+        }
+        if (graph_mode && B == 1 && S[0]->nnz_uu > 600000 && S[0]->n_u > 0)
+            return graph_solve(S[0], g ? g[0] : nullptr, bin ? bin[0] : nullptr, u_vert[0], o, iters, relres, st,
+                               total_iters);
+    }
+    // kernel table: [mode 0/1/2][nvec 0/2/3]; grid mode: 768 threads x 1 CTA/SM (shape 1,
+    // measured best) or 512 x 2 (shape 0); FEMI_CG_SHAPE selects for experiments
+    static void* const fn_block[3] = {(void*)k_cg<0, RNT, 1, 0>, (void*)k_cg<0, RNT, 1, 2>, (void*)k_cg<0, RNT, 1, 3>};
+    static void* const fn_clus[3] = {(void*)k_cg<1, RNT, 1, 0>, (void*)k_cg<1, RNT, 1, 2>, (void*)k_cg<1, RNT, 1, 3>};
+    static void* const fn_grid[2][3] = {
+        {(void*)k_cg<2, 512, 2, 0>, (void*)k_cg<2, 512, 2, 2>, (void*)k_cg<2, 512, 2, 3>},
+        {(void*)k_cg<2, 768, 1, 0>, (void*)k_cg<2, 768, 1, 2>, (void*)k_cg<2, 768, 1, 3>}};
+    static const int grid_nt[2] = {512, 768};
+    static const int grid_per_sm[2] = {2, 1};
+    auto nv_idx = [](int nv) { return nv == 0 ? 0 : (nv == 2 ? 1 : 2); };
     if (g_smem_optin < 0) {
         int dev = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
-        FEMI_CUDA(cudaFuncSetAttribute(k_cg<0, RNT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_smem_optin - 2048));
-        FEMI_CUDA(cudaFuncSetAttribute(k_cg<1, RNT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       g_smem_optin - 2048));
-        FEMI_CUDA(cudaFuncSetAttribute(k_cg<1, RNT, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (int k = 0; k < 3; ++k) {
+            FEMI_CUDA(cudaFuncSetAttribute(fn_block[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           g_smem_optin - 2048));
+            FEMI_CUDA(cudaFuncSetAttribute(fn_clus[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           g_smem_optin - 2048));
+            FEMI_CUDA(cudaFuncSetAttribute(fn_clus[k], cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            for (int s = 0; s < 2; ++s)
+                FEMI_CUDA(cudaFuncSetAttribute(fn_grid[s][k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               g_smem_optin / grid_per_sm[s] - 2048));
+        }
         const char* tm = std::getenv("FEMI_PCG_TIMERS");
         g_timers = tm && tm[0] == '1';
         const char* nv = std::getenv("FEMI_PCG_NVEC");  // experiments: max vectors kept in smem
         if (nv) g_nvec_max = std::atoi(nv);
         const char* sp = std::getenv("FEMI_CG_SHAPE");
-        if (sp) g_shape = std::max(0, std::min(2, std::atoi(sp)));
-        for (int k = 0; k < 3; ++k)
-            FEMI_CUDA(cudaFuncSetAttribute(grid_fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           g_smem_optin / grid_per_sm[k] - 2048));
+        if (sp) g_shape = std::max(0, std::min(1, std::atoi(sp)));
         int per_sm = 0;
-        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_fn[g_shape], grid_nt[g_shape],
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_grid[g_shape][0], grid_nt[g_shape],
                                                                 g_smem_optin / grid_per_sm[g_shape] - 2048));
         g_occ_grid = std::max(1, per_sm) * g_nsm;
     }
@@ -737,25 +1174,26 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                 FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
                 FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
             }
-            cudaError_t e;
+            const RItem* di = d_items;
+            int bb = B;
+            void* args[5] = {(void*)&di, (void*)&bb, (void*)&vr, (void*)&nvec, (void*)&mrows};
+            void* fn;
             if (mode == 2) {
                 attr[0].id = cudaLaunchAttributeCooperative;
                 attr[0].val.cooperative = 1;
                 cfg.numAttrs = 1;
-                const RItem* di = d_items;
-                int bb = B;
-                void* args[5] = {(void*)&di, (void*)&bb, (void*)&vr, (void*)&nvec, (void*)&mrows};
-                e = cudaLaunchKernelExC(&cfg, grid_fn[g_shape], args);
+                fn = fn_grid[g_shape][nv_idx(nvec)];
             } else if (mode == 1) {
                 attr[0].id = cudaLaunchAttributeClusterDimension;
                 attr[0].val.clusterDim.x = ncta_item;
                 attr[0].val.clusterDim.y = 1;
                 attr[0].val.clusterDim.z = 1;
                 cfg.numAttrs = 1;
-                e = cudaLaunchKernelEx(&cfg, k_cg<1, RNT, 1>, (const RItem*)d_items, B, vr, nvec, mrows);
+                fn = fn_clus[nv_idx(nvec)];
             } else {
-                e = cudaLaunchKernelEx(&cfg, k_cg<0, RNT, 1>, (const RItem*)d_items, B, vr, nvec, mrows);
+                fn = fn_block[nv_idx(nvec)];
             }
+            const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
             if (e != cudaSuccess) return cuda_fail(e, "k_cg launch");
             k_finalize<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
             k_true_res<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt + B);
