@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
         __threadfence();
         const unsigned any = atomicExch(gcnt + 1, 0u);
         gcnt[0] = 0;
-        cudaGraphSetConditional(h, any ? 1u : 0u);
+        if (h) cudaGraphSetConditional(h, any ? 1u : 0u);  // h == 0: standalone launch (kbench)
     }
 }
 
@@ -969,6 +969,41 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         count_launches(6);
     }
     count_launches(2 * (int64_t)hs.iters);
+    if (const char* mb = std::getenv("FEMI_PCG_KBENCH")) {  // experiments: body kernels standalone
+        (void)mb;
+        cudaEvent_t e0, e1, e2;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventCreate(&e2);
+        CgState act = hs;
+        act.active = 1;
+        act.alpha = 0.0;  // keeps the iterate unchanged
+        act.beta = 0.0;
+        unsigned* gcnt = C->d_cnt + 2;
+        cudaGraphConditionalHandle hdl = 0;
+        float tu = 0, ts = 0;
+        const int reps = 20;
+        for (int k = 0; k < reps; ++k) {
+            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
+            cudaEventRecord(e0, st);
+            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
+            cudaEventRecord(e1, st);
+            k_gs<false><<<dim3(C->gs_blocks), GNT, 0, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
+            cudaEventRecord(e2, st);
+            cudaEventSynchronize(e2);
+            float a, b;
+            cudaEventElapsedTime(&a, e0, e1);
+            cudaEventElapsedTime(&b, e1, e2);
+            if (k > 1) {
+                tu += a;
+                ts += b;
+            }
+        }
+        std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grid %d / %d)\n", 1e3 * tu / (reps - 2),
+                     1e3 * ts / (reps - 2), C->gx * 2 > 1184 ? 1184 : C->gx * 2, C->gs_blocks);
+        cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+    }
     const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
     if (iters) *iters = hs.iters;
     if (relres) *relres = rel;
