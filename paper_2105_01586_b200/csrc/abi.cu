@@ -341,7 +341,6 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         S->sell_src_tmp = d_src;
     }
     U(launch_tri_records(S, d_tri, d_flags, st));
-    U(alloc(S, &S->owner, (size_t)M.W * M.H));
     U(alloc(S, &S->tp_ptr, (size_t)M.T + 1));
     U(alloc(S, &S->tp_pix, (size_t)M.W * M.H));
     U(build_owner_tables(S, st));

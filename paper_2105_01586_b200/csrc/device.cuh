@@ -37,6 +37,7 @@ struct CgState {
     unsigned long long kmin, kmax;  // order-preserving keys of min(g), max(g)
     int32_t iters, active, status, max_iter;
     uint32_t cnt[4];  // last-block counters (one per reduction site)
+    int32_t par, pad;  // graph mode: which of the double-buffered r/w/s vectors is current
 };
 
 // One batch item as the PCG kernels see it.
@@ -112,9 +113,8 @@ struct femi_system_s {
     int32_t* sell_c32 = nullptr;   // absolute column otherwise
     int64_t sell_nnz = 0;
     int32_t* sell_src_tmp = nullptr;  // assembly-time map SELL entry -> o_val index
-    // pixel ownership (reading A7), resolved once per mesh: owner[pix] = t | cls << 30,
-    // triangle-major pixel lists tp_ptr[T+1] / tp_pix[N] (ascending pix, bit 31 = vertex pixel)
-    uint32_t* owner = nullptr;
+    // pixel ownership (reading A7), resolved once per mesh: triangle-major pixel lists
+    // tp_ptr[T+1] / tp_pix[N] (ascending pix per triangle; pix | cls << 30, cls 1..3 = vertex pixel)
     int32_t* tp_ptr = nullptr;
     uint32_t* tp_pix = nullptr;
     int32_t* sell_inv = nullptr;      // n_u: internal solver row -> canonical unknown index

@@ -67,6 +67,7 @@ struct RItem {
     double* w;  // A^ r^
     double* p;  // used when the CTA's rows do not fit shared memory
     double* sv;
+    double *rec0, *rec1;  // graph mode, fused body: double-buffered {r, w, s, p} records (CgState::par)
     double* part;  // [ncta][4] partial sums / barrier slots
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
@@ -625,76 +626,15 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
     }
 }
 
-// S: w = r + A^_off r (SELL, two slices per warp) and the dots; the last block updates the
-// recurrence scalars and (FIRST: starts it) and sets the WHILE condition when every item has
-// reported (any item still active -> 1).
-template <bool FIRST>
-__global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, int B, double* __restrict__ part,
-                                           unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+// Block partials -> part[item][block]; the last block of the item sums them in block order
+// (deterministic), advances the CG recurrence scalars (FIRST: starts it) and, once every item
+// has reported, sets the WHILE condition (any item still active -> 1). FLIP: the fused body
+// swaps the double-buffered vectors.
+template <bool FIRST, bool FLIP>
+__device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, int B, double* __restrict__ part,
+                                        unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
     __shared__ double shm[4 * (GNT / 32)];
     __shared__ int last;
-    const RItem& it = items[blockIdx.y];
-    CgState* S = it.st;
-    const bool act = FIRST || S->active;
-    double v[3] = {0.0, 0.0, 0.0};
-    if (act) {
-        const int lane = threadIdx.x & 31;
-        const int nsl = (it.n + 31) / 32;
-        const int gw = (blockIdx.x * GNT + threadIdx.x) >> 5, nw = (gridDim.x * GNT) >> 5;
-        const double* __restrict__ r = it.r;
-        for (int sa = 2 * gw; sa < nsl; sa += 2 * nw) {
-            const bool hb = sa + 1 < nsl;
-            int row[2], len[2], base[2], cb[2];
-            double xi[2], si[2], acc[2] = {0.0, 0.0};
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int s = sa + hh;
-                const bool ok = hh == 0 || hb;
-                row[hh] = (ok && 32 * s + lane < it.n) ? 32 * s + lane : -1;
-                len[hh] = ok ? it.len[s] : 0;
-                base[hh] = ok ? it.base[s] + lane : 0;
-                cb[hh] = (32 * s / SIG) * SIG;
-                const int rr = row[hh] >= 0 ? row[hh] : 32 * sa;
-                xi[hh] = r[rr];
-                si[hh] = it.s[rr];
-            }
-            const int L = max(len[0], len[1]);
-            for (int k0 = 0; k0 < L; k0 += 4) {
-                double vv[8];
-                int c[8];
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int e = base[hh] + 32 * (k0 + q);
-                        if (k0 + q < len[hh]) {
-                            vv[4 * hh + q] = it.val[e];
-                            c[4 * hh + q] = it.c16 ? cb[hh] + (int)it.c16[e] : it.c32[e];
-                        } else {
-                            vv[4 * hh + q] = 0.0;
-                            c[4 * hh + q] = 32 * sa;
-                        }
-                    }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const double gv = r[c[q]];
-                    if (q < 4) acc[0] = fma(vv[q], gv, acc[0]);
-                    else acc[1] = fma(vv[q], gv, acc[1]);
-                }
-            }
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                if (row[hh] < 0) continue;
-                const double y = xi[hh] + acc[hh];
-                it.w[row[hh]] = y;
-                const double ru = xi[hh] / si[hh];
-                v[0] += xi[hh] * xi[hh];
-                v[1] += y * xi[hh];
-                v[2] += ru * ru;
-            }
-        }
-    }
-    // block partial -> part[item][block]; last block of the item reduces in block order
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < 3; ++q) v[q] = warp_sum_d(v[q]);
@@ -752,6 +692,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
             }
         } else {
             S->iters += 1;
+            if (FLIP) S->par ^= 1;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 S->status = FEMI_E_NONFINITE;
             } else if (rho2 <= S->tol2) {
@@ -785,6 +726,200 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
     }
 }
 
+// S: w = r + A^_off r (SELL, two slices per warp) and the dots; the last block updates the
+// recurrence scalars and (FIRST: starts it) and sets the WHILE condition when every item has
+// reported (any item still active -> 1).
+template <bool FIRST>
+__global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, int B, double* __restrict__ part,
+                                           unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+    const RItem& it = items[blockIdx.y];
+    CgState* S = it.st;
+    const bool act = FIRST || S->active;
+    double v[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        const int lane = threadIdx.x & 31;
+        const int nsl = (it.n + 31) / 32;
+        const int gw = (blockIdx.x * GNT + threadIdx.x) >> 5, nw = (gridDim.x * GNT) >> 5;
+        const double* __restrict__ r = it.r;
+        double* __restrict__ wout = it.w;
+        for (int sa = 2 * gw; sa < nsl; sa += 2 * nw) {
+            const bool hb = sa + 1 < nsl;
+            int row[2], len[2], base[2], cb[2];
+            double xi[2], si[2], acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int s = sa + hh;
+                const bool ok = hh == 0 || hb;
+                row[hh] = (ok && 32 * s + lane < it.n) ? 32 * s + lane : -1;
+                len[hh] = ok ? it.len[s] : 0;
+                base[hh] = ok ? it.base[s] + lane : 0;
+                cb[hh] = (32 * s / SIG) * SIG;
+                const int rr = row[hh] >= 0 ? row[hh] : 32 * sa;
+                xi[hh] = r[rr];
+                si[hh] = it.s[rr];
+            }
+            const int L = max(len[0], len[1]);
+            for (int k0 = 0; k0 < L; k0 += 4) {
+                double vv[8];
+                int c[8];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = base[hh] + 32 * (k0 + q);
+                        if (k0 + q < len[hh]) {
+                            vv[4 * hh + q] = it.val[e];
+                            c[4 * hh + q] = it.c16 ? cb[hh] + (int)it.c16[e] : it.c32[e];
+                        } else {
+                            vv[4 * hh + q] = 0.0;
+                            c[4 * hh + q] = 32 * sa;
+                        }
+                    }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double gv = r[c[q]];
+                    if (q < 4) acc[0] = fma(vv[q], gv, acc[0]);
+                    else acc[1] = fma(vv[q], gv, acc[1]);
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (row[hh] < 0) continue;
+                const double y = xi[hh] + acc[hh];
+                wout[row[hh]] = y;
+                const double ru = xi[hh] / si[hh];
+                v[0] += xi[hh] * xi[hh];
+                v[1] += y * xi[hh];
+                v[2] += ru * ru;
+            }
+        }
+    }
+    cg_tail<FIRST, false>(v, act, S, B, part, gcnt, h);
+}
+
+// Fused body (one kernel per CG iteration). The vectors a neighbour gathers travel together:
+// rec[i] = {r, w, s, p} (32 B, one sector), double-buffered (CgState::par = current copy);
+// x stays a plain vector updated in place. For its own rows a warp applies the update
+//   p' = r + beta p ; s' = w + beta s ; x += alpha p' ; r' = r - alpha s'
+// and the SpMV w' = r' + A^_off r' gathers each neighbour's record and recomputes its
+// r' = r - alpha (w + beta s) with the same fma sequence as the owner (bit-identical), so no
+// grid-wide barrier separates the update from the SpMV. Per row and iteration: rec read and
+// write (64 B), x read/write (16 B), s_jacobi read (8 B) = 11 vector streams, plus the
+// matrix, one gathered sector per nonzero and one kernel boundary.
+// FIRST: no update (p = s = 0 already); w = r + A^_off r into the current record.
+struct __align__(16) Rec {
+    double r, w, s, p;
+};
+
+template <bool FIRST>
+__global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, int B, double* __restrict__ part,
+                                           unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+    const RItem& it = items[blockIdx.y];
+    CgState* S = it.st;
+    const bool act = FIRST || S->active;
+    double v[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        const int lane = threadIdx.x & 31;
+        const int n = it.n;
+        const int nsl = (n + 31) / 32;
+        const int gw = (blockIdx.x * GNT + threadIdx.x) >> 5, nw = (gridDim.x * GNT) >> 5;
+        const int cur = S->par;
+        const double alpha = FIRST ? 0.0 : S->alpha, beta = FIRST ? 0.0 : S->beta;
+        const Rec* __restrict__ R0 = (const Rec*)(cur ? it.rec1 : it.rec0);
+        Rec* __restrict__ R1 = (Rec*)(cur ? it.rec0 : it.rec1);
+        for (int sa = 2 * gw; sa < nsl; sa += 2 * nw) {
+            const bool hb = sa + 1 < nsl;
+            int row[2], len[2], base[2];
+            double rn[2], sn[2], pn[2], acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int sl = sa + hh;
+                const bool ok = hh == 0 || hb;
+                row[hh] = (ok && 32 * sl + lane < n) ? 32 * sl + lane : -1;
+                len[hh] = ok ? it.len[sl] : 0;
+                base[hh] = ok ? it.base[sl] + lane : 0;
+                const int i = row[hh] >= 0 ? row[hh] : 32 * sa;
+                const Rec q = R0[i];
+                if (FIRST) {
+                    rn[hh] = q.r;
+                } else {
+                    pn[hh] = fma(beta, q.p, q.r);
+                    sn[hh] = fma(beta, q.s, q.w);
+                    rn[hh] = fma(-alpha, sn[hh], q.r);
+                    if (row[hh] >= 0) it.x[i] = fma(alpha, pn[hh], it.x[i]);
+                }
+            }
+            const int cb = (32 * sa / SIG) * SIG;  // sa even, SIG % 64 == 0: both slices share the window
+            const int L = max(len[0], len[1]);
+            for (int k0 = 0; k0 < L; k0 += 2) {
+                double vv[4];
+                int c[4];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int e = base[hh] + 32 * (k0 + q);
+                        if (k0 + q < len[hh]) {
+                            vv[2 * hh + q] = it.val[e];
+                            c[2 * hh + q] = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
+                        } else {
+                            vv[2 * hh + q] = 0.0;
+                            c[2 * hh + q] = 32 * sa;
+                        }
+                    }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    double gc;
+                    if (FIRST) {
+                        gc = R0[c[q]].r;
+                    } else {
+                        const Rec g = R0[c[q]];
+                        gc = fma(-alpha, fma(beta, g.s, g.w), g.r);
+                    }
+                    if (q < 2) acc[0] = fma(vv[q], gc, acc[0]);
+                    else acc[1] = fma(vv[q], gc, acc[1]);
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (row[hh] < 0) continue;
+                const int i = row[hh];
+                const double y = rn[hh] + acc[hh];
+                if (FIRST) {
+                    ((Rec*)R0)[i].w = y;
+                } else {
+                    Rec o;
+                    o.r = rn[hh];
+                    o.w = y;
+                    o.s = sn[hh];
+                    o.p = pn[hh];
+                    R1[i] = o;
+                }
+                const double ru = rn[hh] / it.s[i];
+                v[0] += rn[hh] * rn[hh];
+                v[1] += y * rn[hh];
+                v[2] += ru * ru;
+            }
+        }
+    }
+    cg_tail<FIRST, !FIRST>(v, act, S, B, part, gcnt, h);
+}
+
+// rec[cur] = {r, 0, 0, 0} from the plain residual (start and restart of the recurrence)
+__global__ void k_pack(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    Rec* __restrict__ R = (Rec*)(it.st->par ? it.rec1 : it.rec0);
+    const double* __restrict__ r = it.r;  // plain residual (k_init_r / k_true_res)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        Rec o;
+        o.r = r[i];
+        o.w = 0.0;
+        o.s = 0.0;
+        o.p = 0.0;
+        R[i] = o;
+    }
+}
+
 struct GraphCache {
     void* ws = nullptr;
     RItem* d_items = nullptr;
@@ -793,7 +928,7 @@ struct GraphCache {
     double* d_part = nullptr;
     cudaGraphExec_t main = nullptr, restart = nullptr;
     RItem item{};
-    int gs_blocks = 0, gx = 0;
+    int gs_blocks = 0, gx = 0, gp_blocks = 0;
 };
 
 struct Workspace {
@@ -805,6 +940,7 @@ struct Workspace {
 };
 
 int g_smem_optin = -1;
+int g_fused = -1;  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
@@ -828,7 +964,8 @@ femi_status add_kernel(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid
     return FEMI_OK;
 }
 
-// builds [prologue...] -> k_gs<true> -> WHILE{ k_gu -> k_gs<false> } -> finalize -> true_res -> copy_g
+// builds [prologue...] -> k_gp<true> -> WHILE{ k_gp<false> } -> finalize -> true_res -> copy_g
+// (FEMI_PCG_FUSED=0: k_gs<true> -> WHILE{ k_gu -> k_gs<false> } on plain vectors)
 femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     cudaGraph_t gr;
     FEMI_CUDA(cudaGraphCreate(&gr, 0));
@@ -862,10 +999,17 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_rhs, gk, bk, a_items))) return s;
         if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
     }
-    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
-    if (!restart)
-        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-    if ((s = chain((void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs))) return s;
+    if (g_fused) {
+        if (!restart)
+            if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+        if ((s = chain((void*)k_pack, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_gp<true>, dim3(C.gp_blocks), dim3(GNT), a_gs))) return s;
+    } else {
+        if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
+        if (!restart)
+            if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+        if ((s = chain((void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs))) return s;
+    }
     {
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
@@ -876,10 +1020,15 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         prev = nd;
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         cudaGraphNode_t u, sn;
-        if ((s = add_kernel(body, nullptr, (void*)k_gu, dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT), a_items,
-                            &u)))
-            return s;
-        if ((s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn))) return s;
+        if (g_fused) {
+            if ((s = add_kernel(body, nullptr, (void*)k_gp<false>, dim3(C.gp_blocks), dim3(GNT), a_gs, &sn)))
+                return s;
+        } else {
+            if ((s = add_kernel(body, nullptr, (void*)k_gu, dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT),
+                                a_items, &u)))
+                return s;
+            if ((s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn))) return s;
+        }
     }
     if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
     if ((s = chain((void*)k_true_res, gk, bk, a_cnt1))) return s;
@@ -894,6 +1043,10 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                         int64_t* total_iters) {
     GraphCache* C = (GraphCache*)S->scratch;
     const int64_t n = S->n_u;
+    if (g_fused < 0) {
+        const char* fz = std::getenv("FEMI_PCG_FUSED");  // measured: fused 69 us vs 17 + 43 us (C5)
+        g_fused = (fz && fz[0] == '1') ? 1 : 0;
+    }
     if (!C) {
         C = new GraphCache();
         const int nsl = (int)((n + 31) / 32);
@@ -902,8 +1055,18 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                                                                    148 * 8));
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t vb = al(sizeof(double) * (n + 1));
+        {
+            int per_sm = 0, nsm = 0, dev = 0;
+            FEMI_CUDA(cudaGetDevice(&dev));
+            FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gp<false>, GNT, 0));
+            C->gp_blocks = (int)std::max<int64_t>(
+                1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)), (int64_t)std::max(1, per_sm) * nsm));
+        }
+        const int pb = std::max(C->gs_blocks, C->gp_blocks);
+        const size_t rb = al(sizeof(Rec) * (n + 1));
         const size_t bytes = al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
-                             al(sizeof(double) * 4 * C->gs_blocks) + al(sizeof(double) * KGRID) + 6 * vb;
+                             al(sizeof(double) * 4 * pb) + al(sizeof(double) * KGRID) + 6 * vb + 2 * rb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
         char* cur = (char*)C->ws;
         auto take = [&](size_t x) {
@@ -914,7 +1077,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         C->d_items = (RItem*)take(sizeof(RItem));
         C->d_state = (CgState*)take(sizeof(CgState));
         C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
-        C->d_part = (double*)take(sizeof(double) * 4 * C->gs_blocks);
+        C->d_part = (double*)take(sizeof(double) * 4 * pb);
         RItem& it = C->item;
         it.red = (double*)take(sizeof(double) * KGRID);
         it.b = (double*)take(vb);
@@ -923,6 +1086,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.w = (double*)take(vb);
         it.p = (double*)take(vb);
         it.sv = (double*)take(vb);
+        it.rec0 = (double*)take(rb);
+        it.rec1 = (double*)take(rb);
         it.inv = S->sell_inv;
         it.len = S->sell_len;
         it.base = S->sell_base;
@@ -968,7 +1133,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         FEMI_CUDA(cudaGraphLaunch(C->restart, st));  // from the current iterate (r = s * r_true)
         count_launches(6);
     }
-    count_launches(2 * (int64_t)hs.iters);
+    count_launches((g_fused ? 1 : 2) * (int64_t)hs.iters);
     if (const char* mb = std::getenv("FEMI_PCG_KBENCH")) {  // experiments: body kernels standalone
         (void)mb;
         cudaEvent_t e0, e1, e2;
@@ -981,12 +1146,27 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         act.beta = 0.0;
         unsigned* gcnt = C->d_cnt + 2;
         cudaGraphConditionalHandle hdl = 0;
-        float tu = 0, ts = 0;
+        cudaEvent_t e3;
+        cudaEventCreate(&e3);
+        float tu = 0, ts = 0, tf = 0;
         const int reps = 20;
+        const int gu = C->gx * 2 > 1184 ? 1184 : C->gx * 2;
         for (int k = 0; k < reps; ++k) {
+            act.par = 0;
+            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
+            cudaEventRecord(e3, st);
+            k_gp<false><<<dim3(C->gp_blocks), GNT, 0, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
+            cudaEventRecord(e0, st);
+            cudaEventSynchronize(e0);
+            float c;
+            cudaEventElapsedTime(&c, e3, e0);
+            if (k > 1) tf += c;
+        }
+        for (int k = 0; k < reps; ++k) {
+            act.par = 0;
             cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
             cudaEventRecord(e0, st);
-            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
+            k_gu<<<dim3(gu), GNT, 0, st>>>(C->d_items);
             cudaEventRecord(e1, st);
             k_gs<false><<<dim3(C->gs_blocks), GNT, 0, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
             cudaEventRecord(e2, st);
@@ -999,8 +1179,10 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 ts += b;
             }
         }
-        std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grid %d / %d)\n", 1e3 * tu / (reps - 2),
-                     1e3 * ts / (reps - 2), C->gx * 2 > 1184 ? 1184 : C->gx * 2, C->gs_blocks);
+        std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grids %d / %d)  fused k_gp %.2f us (grid %d)\n",
+                     1e3 * tu / (reps - 2), 1e3 * ts / (reps - 2), gu, C->gs_blocks, 1e3 * tf / (reps - 2),
+                     C->gp_blocks);
+        cudaEventDestroy(e3);
         cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st);
         cudaStreamSynchronize(st);
     }

@@ -4,30 +4,29 @@
 //
 // Pixel ownership (reading A7: lowest index among the closed triangles containing a
 // pixel) depends only on the mesh, so it is resolved ONCE per mesh at assembly by a
-// warp-cooperative triangle expansion (raster_common.cuh) into
-//   owner[pix]  = t | cls << 30   (cls 0: interior/edge pixel, 1..3: vertex pixel of v[cls-1])
+// warp-cooperative triangle expansion (raster_common.cuh) into the triangle-major lists
 //   tp_ptr[t]   = first entry of triangle t in tp_pix (CSR, ascending triangle)
-//   tp_pix[q]   = the triangle's pixels in ascending pix order (bit 31: vertex pixel).
-// Every solve then rasterises with two streaming kernels and no atomics:
-//   R1 pixel-major: u = vertex value (vertex pixel) or u_a + l_b (u_b - u_a) + l_c (u_c - u_a)
-//      with l = exact integer edge function / 2*area (S3); e = (u - f)^2. Coalesced f/u/e.
-//   R2 triangle-major over tp_pix (coalesced list, local e gathers): per-triangle error sum
-//      and arg-max over non-vertex pixels (ties: lowest pix) by segmented warp scans in
-//      pixel order; SSE = fixed-order sum of the triangle sums. Deterministic.
-// The adjoint P^T r is R2's traversal with barycentric weights.
+//   tp_pix[q]   = cls << 30 | y << 14 | x for the triangle's owned pixels in ascending pix
+//                 order (cls 0: interior/edge pixel, 1..3: the pixel of vertex v[cls-1];
+//                 W, H <= 16384 so x and y take 14 bits each).
+// Every solve then rasterises with ONE triangle-major kernel (k_raster_tri): values, errors,
+// per-triangle error sum and arg-max over non-vertex pixels (ties: lowest pix) by segmented
+// warp scans in pixel order, SSE = fixed-order sum of the triangle sums. Deterministic.
+// The adjoint P^T r is the same traversal with barycentric weights.
+#include <cstdlib>
+
 #include "raster_common.cuh"
 
 namespace femi {
 namespace {
 
-constexpr uint32_t kTriMask = 0x3fffffffu;
 
 // ---------------------------------------------------------------- setup (per mesh)
 
-// MODE 0: owner map + owned-pixel count per triangle. MODE 1: triangle-major pixel list.
+// MODE 0: owned-pixel count per triangle. MODE 1: triangle-major pixel list.
 template <int MODE>
 __global__ void __launch_bounds__(RT) k_build_owner(const TriRec* __restrict__ tri, int64_t T, int W,
-                                                    uint32_t* __restrict__ owner, int32_t* __restrict__ cnt,
+                                                    int32_t* __restrict__ cnt,
                                                     const int32_t* __restrict__ tp_ptr,
                                                     uint32_t* __restrict__ tp_pix) {
     __shared__ WTri tris[RWARPS][32];
@@ -47,20 +46,18 @@ __global__ void __launch_bounds__(RT) k_build_owner(const TriRec* __restrict__ t
             const int k = base + lane;
             const int j = warp_find(excl, k, total);
             const int exj = __shfl_sync(0xffffffffu, excl, j & 31);
-            int own = 0, cls = 0;
-            int64_t pix = 0;
+            int own = 0, cls = 0, px = 0, py = 0;
             if (j < 32) {
                 const WTri& I = ws[j];
                 const int loc = k - exj;
                 const int ry = loc / I.bw;
-                const int py = I.y0 + ry, px = I.x0 + loc - ry * I.bw;
+                py = I.y0 + ry;
+                px = I.x0 + loc - ry * I.bw;
                 int w0, w1, w2, kv = 0;
                 const int c = classify(I, px, py, w0, w1, w2, kv);
                 if (c) {
                     own = 1;
                     cls = c == 2 ? kv + 1 : 0;
-                    pix = (int64_t)py * W + px;
-                    if (MODE == 0) owner[pix] = (uint32_t)(t0 + j) | ((uint32_t)cls << 30);
                 }
             }
             // rank of this owned pixel inside its triangle (slots are in pixel order)
@@ -73,7 +70,7 @@ __global__ void __launch_bounds__(RT) k_build_owner(const TriRec* __restrict__ t
             }
             if (MODE == 1 && own) {
                 const int q = tp_ptr[t0 + j] + run_s[wid][j] + rk - 1;
-                tp_pix[q] = (uint32_t)pix | (cls ? 0x80000000u : 0u);
+                tp_pix[q] = ((uint32_t)cls << 30) | ((uint32_t)py << 14) | (uint32_t)px;
             }
             __syncwarp();
             const int jn = __shfl_down_sync(0xffffffffu, j, 1);
@@ -141,13 +138,12 @@ __global__ void k_scan_apply(int64_t n, const int32_t* __restrict__ cnt, const i
 
 struct RasterItem {
     const TriRec* tri;
-    const uint32_t* owner;
     const int32_t* tp_ptr;
     const uint32_t* tp_pix;
     const double* u_vert;
     const double* f;
     double* u_px;
-    double* e_px;  // output or scratch (needed by R2 whenever f is given)
+    double* e_px;
     double* tri_err;
     int32_t* best;
     double* sse;
@@ -155,34 +151,6 @@ struct RasterItem {
     int32_t W;
     int32_t pad;
 };
-
-// R1: pixel-major values and errors
-__global__ void __launch_bounds__(256) k_px_values(const RasterItem* __restrict__ items) {
-    const RasterItem it = items[blockIdx.y];
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < it.N; p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t o = it.owner[p];
-        const TriRec R = it.tri[o & kTriMask];
-        const uint32_t cls = o >> 30;
-        double u;
-        if (cls) {
-            u = it.u_vert[R.v[cls - 1]];
-        } else {
-            const int W = it.W;
-            const int px = (int)(p % W), py = (int)(p / W);
-            const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-            const int w1 = (ax - cx) * (py - cy) - (ay - cy) * (px - cx);  // orient(c,a,p)
-            const int w2 = (bx - ax) * (py - ay) - (by - ay) * (px - ax);  // orient(a,b,p)
-            const double D = (double)((bx - ax) * (cy - ay) - (by - ay) * (cx - ax));
-            const double ua = it.u_vert[R.v[0]];
-            u = ua + (w1 / D) * (it.u_vert[R.v[1]] - ua) + (w2 / D) * (it.u_vert[R.v[2]] - ua);
-        }
-        if (it.u_px) it.u_px[p] = u;
-        if (it.f) {
-            const double d = u - it.f[p];
-            it.e_px[p] = d * d;
-        }
-    }
-}
 
 // Warp-cooperative traversal of the triangle-major list: lane l of a warp owns triangle
 // t0+l; list entries ptr[t0] .. ptr[t0+32] are walked 32 at a time (coalesced), each entry
@@ -209,68 +177,151 @@ __device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_pt
     return lw;
 }
 
-// R2: per-triangle error sum and arg-max, SSE
-__global__ void __launch_bounds__(RT) k_tri_reduce(const RasterItem* __restrict__ items, double* __restrict__ part,
+// One triangle as the fused raster keeps it in shared memory (one slot per lane): the two
+// exact integer edge functions as planes w = A px + B py + C (S3: w_b = orient(c,a,p),
+// w_c = orient(a,b,p)), D = orient(a,b,c), u_a and the differences u_b - u_a, u_c - u_a.
+struct RTri {
+    int A1, B1, C1, A2, B2, C2, pad0, pad1;
+    double D, db, dc, u[3];
+};
+
+__device__ __forceinline__ int tp_x(uint32_t v) { return (int)(v & 0x3fffu); }
+__device__ __forceinline__ int tp_y(uint32_t v) { return (int)((v >> 14) & 0x3fffu); }
+
+// S3+S4 in ONE triangle-major pass (no owner-map read, no second pass over e): a warp takes
+// 32 consecutive triangles, keeps them in shared memory and walks their owned pixels
+// (tp_pix, ascending pix per triangle) 2 x 32 at a time:
+//   u  = the vertex value (vertex pixel) or (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
+//   e  = (u - f)^2 ; u and e written, f read at the pixel (row segments: L2-merged sectors)
+// and reduces per triangle (sum of e, arg-max of e over non-vertex pixels, ties -> lowest
+// pix) by segmented warp scans in pixel order; SSE = fixed-order sum of the triangle sums.
+// Deterministic, no atomics on values.
+template <int MINB>
+__global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ part,
                                                    uint32_t* __restrict__ counters) {
+    __shared__ RTri tris[RWARPS][32];
     __shared__ double acc_s[RWARPS][32];
     __shared__ double be_s[RWARPS][32];
     __shared__ int bp_s[RWARPS][32];
     __shared__ double red[RWARPS];
     __shared__ int flag;
-    const RasterItem it = items[blockIdx.y];
+    const RasterItem& it = items[blockIdx.y];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t ngroups = (it.T + 31) / 32;
+    const int64_t T = it.T;
+    const int W = it.W;
+    const double* __restrict__ f = it.f;
+    double* __restrict__ u_px = it.u_px;
+    double* __restrict__ e_px = it.e_px;
+    const uint32_t* __restrict__ tp_pix = it.tp_pix;
+    const int64_t ngroups = (T + 31) / 32;
     const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    RTri* ws = tris[wid];
     double sse_loc = 0.0;
     for (int64_t g = gwarp; g < ngroups; g += nwarps) {
         const int64_t t0 = g * 32;
         int cnt;
-        const ListWalk lw = list_begin(it.tp_ptr, it.T, t0, cnt);
+        const ListWalk lw = list_begin(it.tp_ptr, T, t0, cnt);
+        if (t0 + lane < T) {
+            const TriRec R = it.tri[t0 + lane];
+            const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
+            RTri I;
+            // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx)
+            I.A1 = cy - ay;
+            I.B1 = ax - cx;
+            I.C1 = (ay - cy) * cx - (ax - cx) * cy;
+            // w_c = orient(a,b,p) = (bx-ax)(py-ay) - (by-ay)(px-ax)
+            I.A2 = ay - by;
+            I.B2 = bx - ax;
+            I.C2 = (by - ay) * ax - (bx - ax) * ay;
+            I.D = (double)orient_xy(ax, ay, bx, by, cx, cy);
+            I.u[0] = it.u_vert[R.v[0]];
+            I.u[1] = it.u_vert[R.v[1]];
+            I.u[2] = it.u_vert[R.v[2]];
+            I.db = I.u[1] - I.u[0];
+            I.dc = I.u[2] - I.u[0];
+            ws[lane] = I;
+        }
         acc_s[wid][lane] = 0.0;
         be_s[wid][lane] = -1.0;
         bp_s[wid][lane] = -1;
         __syncwarp();
-        for (int base = 0; base < lw.total; base += 32) {
-            const int k = base + lane;
-            const int j = warp_find(lw.excl, k, lw.total);
-            double val = 0.0, ce = -1.0;
-            int cp = 0x7fffffff;
-            if (j < 32) {
-                const uint32_t v = it.tp_pix[lw.ptr0 + k];
-                const int pix = (int)(v & 0x7fffffffu);
-                const double e = it.e_px[pix];
-                val = e;
-                if (!(v >> 31)) {
-                    ce = e;
-                    cp = pix;
-                }
+        for (int base = 0; base < lw.total; base += 64) {
+            uint32_t v[2];
+            int j[2], seg0[2];
+            double fv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = base + 32 * h + lane;
+                j[h] = warp_find(lw.excl, k, lw.total);
+                // first lane of this lane's triangle inside the window (segmented-scan bound)
+                const int ex = __shfl_sync(0xffffffffu, lw.excl, j[h] & 31);
+                seg0[h] = max(0, ex - (base + 32 * h));
+                v[h] = j[h] < 32 ? tp_pix[lw.ptr0 + k] : 0u;
             }
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double vo = __shfl_up_sync(0xffffffffu, val, o);
-                const double eo = __shfl_up_sync(0xffffffffu, ce, o);
-                const int po = __shfl_up_sync(0xffffffffu, cp, o);
-                const int jo = __shfl_up_sync(0xffffffffu, j, o);
-                if (lane >= o && jo == j) {
-                    val += vo;
-                    if (eo > ce || (eo == ce && po < cp)) {
-                        ce = eo;
-                        cp = po;
+            for (int h = 0; h < 2; ++h)
+                fv[h] = (f && j[h] < 32) ? f[(int64_t)tp_y(v[h]) * W + tp_x(v[h])] : 0.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (base + 32 * h >= lw.total) break;  // warp-uniform
+                double val = 0.0, ce = -1.0;
+                int cp = 0x7fffffff;
+                if (j[h] < 32) {
+                    const int px = tp_x(v[h]), py = tp_y(v[h]);
+                    const int pix = py * W + px;
+                    const uint32_t cls = v[h] >> 30;
+                    const RTri& I = ws[j[h]];
+                    double u;
+                    if (cls) {
+                        u = I.u[cls - 1];
+                    } else {
+                        // S3 as the paper's barycentric form, IEEE round-to-nearest per operation
+                        // and no contraction: l_b = w_b / D, l_c = w_c / D,
+                        // u = (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
+                        const int w1 = I.A1 * px + I.B1 * py + I.C1;
+                        const int w2 = I.A2 * px + I.B2 * py + I.C2;
+                        const double lb = __ddiv_rn((double)w1, I.D), lc = __ddiv_rn((double)w2, I.D);
+                        u = __dadd_rn(__dadd_rn(I.u[0], __dmul_rn(lb, I.db)), __dmul_rn(lc, I.dc));
+                    }
+                    if (u_px) u_px[pix] = u;
+                    if (f) {
+                        const double d = __dsub_rn(u, fv[h]);
+                        const double e = __dmul_rn(d, d);
+                        if (e_px) e_px[pix] = e;
+                        val = e;
+                        if (!cls) {
+                            ce = e;
+                            cp = pix;
+                        }
                     }
                 }
-            }
-            const int jn = __shfl_down_sync(0xffffffffu, j, 1);
-            if (j < 32 && (lane == 31 || jn != j)) {
-                acc_s[wid][j] += val;
-                if (ce > be_s[wid][j]) {  // earlier windows hold lower pixels: strict > keeps ties
-                    be_s[wid][j] = ce;
-                    bp_s[wid][j] = cp;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double vo = __shfl_up_sync(0xffffffffu, val, o);
+                    const double eo = __shfl_up_sync(0xffffffffu, ce, o);
+                    const int po = __shfl_up_sync(0xffffffffu, cp, o);
+                    if (lane - o >= seg0[h]) {
+                        val += vo;
+                        if (eo > ce || (eo == ce && po < cp)) {
+                            ce = eo;
+                            cp = po;
+                        }
+                    }
                 }
+                const int jj = j[h];
+                const int jn = __shfl_down_sync(0xffffffffu, jj, 1);
+                if (jj < 32 && (lane == 31 || jn != jj)) {
+                    acc_s[wid][jj] += val;
+                    if (ce > be_s[wid][jj]) {  // earlier windows hold lower pixels: strict > keeps ties
+                        be_s[wid][jj] = ce;
+                        bp_s[wid][jj] = cp;
+                    }
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         __syncwarp();
-        if (t0 + lane < it.T) {
+        if (t0 + lane < T && f) {
             const double a = acc_s[wid][lane];
             if (it.tri_err) it.tri_err[t0 + lane] = a;
             if (it.best) it.best[t0 + lane] = be_s[wid][lane] >= 0.0 ? bp_s[wid][lane] : -1;
@@ -278,7 +329,7 @@ __global__ void __launch_bounds__(RT) k_tri_reduce(const RasterItem* __restrict_
         }
         __syncwarp();
     }
-    if (!it.sse) return;
+    if (!it.sse || !f) return;
     const double tot = block_sum<RT>(sse_loc, red);
     double* P = part + (size_t)blockIdx.y * gridDim.x;
     if (threadIdx.x == 0) P[blockIdx.x] = tot;
@@ -303,8 +354,7 @@ __global__ void __launch_bounds__(RT) k_tri_reduce(const RasterItem* __restrict_
 // P^T r: per triangle, sum over its owned pixels of (l_a, l_b, l_c) r (vertex pixels:
 // weight 1 on that vertex) -> tri_w[3t+k]; the vertex gather happens in tonal.cu.
 __global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ tri, const int32_t* __restrict__ tp_ptr,
-                                                    const uint32_t* __restrict__ tp_pix,
-                                                    const uint32_t* __restrict__ owner, int64_t T, int W,
+                                                    const uint32_t* __restrict__ tp_pix, int64_t T, int W,
                                                     const double* __restrict__ r, double* __restrict__ tri_w) {
     __shared__ double acc_s[RWARPS][32][3];
     __shared__ WTri tris[RWARPS][32];
@@ -338,16 +388,15 @@ __global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ t
             double sa = 0.0, sb = 0.0, sc = 0.0;
             if (j < 32) {
                 const uint32_t v = tp_pix[lw.ptr0 + k];
-                const int pix = (int)(v & 0x7fffffffu);
-                const double rv = r[pix];
-                if (v >> 31) {
-                    const uint32_t cls = owner[pix] >> 30;
+                const int px = (int)(v & 0x3fffu), py = (int)((v >> 14) & 0x3fffu);
+                const double rv = r[(int64_t)py * W + px];
+                const uint32_t cls = v >> 30;
+                if (cls) {
                     if (cls == 1) sa = rv;
                     else if (cls == 2) sb = rv;
                     else sc = rv;
                 } else {
                     const WTri& I = ws[j];
-                    const int px = pix % W, py = pix / W;
                     const double D = (double)I.D;
                     sa = (orient_xy(I.bx, I.by, I.cx, I.cy, px, py) / D) * rv;
                     sb = (orient_xy(I.cx, I.cy, I.ax, I.ay, px, py) / D) * rv;
@@ -401,11 +450,11 @@ femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     FEMI_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * T, st));
     FEMI_CUDA(cudaMallocAsync(&bsum, sizeof(int32_t) * (nb + 1), st));
     const int g = warp_grid(T, 1);
-    k_build_owner<0><<<g, RT, 0, st>>>(S->tri, T, S->W, S->owner, cnt, nullptr, nullptr);
+    k_build_owner<0><<<g, RT, 0, st>>>(S->tri, T, S->W, cnt, nullptr, nullptr);
     k_scan_blocks<<<nb, SCB, 0, st>>>(T, cnt, bsum);
     k_scan_bsum<<<1, 32, 0, st>>>(nb, bsum);
     k_scan_apply<<<nb, SCB, 0, st>>>(T, cnt, bsum, S->tp_ptr);
-    k_build_owner<1><<<g, RT, 0, st>>>(S->tri, T, S->W, nullptr, nullptr, S->tp_ptr, S->tp_pix);
+    k_build_owner<1><<<g, RT, 0, st>>>(S->tri, T, S->W, nullptr, S->tp_ptr, S->tp_pix);
     count_launches(5);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(cnt, st));
@@ -419,12 +468,10 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
                           double* const* sse, cudaStream_t st) {
     if (B <= 0) return FEMI_OK;
     std::vector<RasterItem> items(B);
-    int64_t Tmax = 0, Nmax = 0, scratch = 0;
-    bool need_r2 = false;
+    int64_t Tmax = 0;
     for (int b = 0; b < B; ++b) {
         RasterItem& r = items[b];
         r.tri = S[b]->tri;
-        r.owner = S[b]->owner;
         r.tp_ptr = S[b]->tp_ptr;
         r.tp_pix = S[b]->tp_pix;
         r.u_vert = u_vert[b];
@@ -438,36 +485,39 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
         r.N = (int64_t)S[b]->W * S[b]->H;
         r.W = S[b]->W;
         Tmax = std::max(Tmax, r.T);
-        Nmax = std::max(Nmax, r.N);
-        if (r.f && (r.tri_err || r.best || r.sse)) need_r2 = true;
-        if (r.f && !r.e_px) scratch += r.N;
     }
-    const int gx = warp_grid(Tmax, B);
+    if (Tmax == 0) return FEMI_OK;
+    static int minb = -1;  // 4 CTAs/SM (<= 64 registers); FEMI_RASTER_MINB=1 -> unconstrained (experiments)
+    static int resident = 0;
+    if (minb < 0) {
+        const char* e = std::getenv("FEMI_RASTER_MINB");
+        minb = (e && e[0] == '1') ? 1 : 4;
+        int dev = 0, nsm = 0, per = 0;
+        FEMI_CUDA(cudaGetDevice(&dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per, minb == 4 ? (const void*)k_raster_tri<4> : (const void*)k_raster_tri<1>, RT, 0));
+        resident = std::max(1, per) * nsm;
+    }
+    // one wave of resident CTAs (no partial last wave), grid-stride over 32-triangle groups
+    const int64_t groups = (Tmax + 31) / 32;
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((groups + RWARPS - 1) / RWARPS,
+                                                              (int64_t)std::max(1, resident / B)));
     const size_t bytes_items = sizeof(RasterItem) * B;
     const size_t bytes_part = sizeof(double) * (size_t)gx * B;
     const size_t bytes_cnt = sizeof(uint32_t) * B;
     void* base = nullptr;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    FEMI_CUDA(cudaMallocAsync(&base, al(bytes_items) + al(bytes_part) + al(bytes_cnt) + sizeof(double) * scratch, st));
+    FEMI_CUDA(cudaMallocAsync(&base, al(bytes_items) + al(bytes_part) + al(bytes_cnt), st));
     char* cur = (char*)base;
     RasterItem* d_items = (RasterItem*)cur;
     double* d_part = (double*)(cur + al(bytes_items));
     uint32_t* d_cnt = (uint32_t*)((char*)d_part + al(bytes_part));
-    double* scr = (double*)((char*)d_cnt + al(bytes_cnt));
-    for (int b = 0; b < B; ++b)
-        if (items[b].f && !items[b].e_px) {
-            items[b].e_px = scr;
-            scr += items[b].N;
-        }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
-    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((Nmax + 255) / 256, (int64_t)148 * 16 / B + 1));
-    k_px_values<<<dim3(g1, B), 256, 0, st>>>(d_items);
+    if (minb == 4) k_raster_tri<4><<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
+    else k_raster_tri<1><<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
     count_launches(1);
-    if (need_r2) {
-        k_tri_reduce<<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
-        count_launches(1);
-    }
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
     return FEMI_OK;
@@ -475,7 +525,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
 
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {
     if (S->T == 0) return FEMI_OK;
-    k_tri_adjoint<<<warp_grid(S->T, 1), RT, 0, st>>>(S->tri, S->tp_ptr, S->tp_pix, S->owner, S->T, S->W, r, tri_w);
+    k_tri_adjoint<<<warp_grid(S->T, 1), RT, 0, st>>>(S->tri, S->tp_ptr, S->tp_pix, S->T, S->W, r, tri_w);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;
