@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -275,9 +277,11 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         std::vector<int32_t> pi(n), pos(n);
         {
             std::vector<std::pair<uint64_t, int32_t>> key(n);
+            uint64_t band = kBand;
+            if (const char* e = std::getenv("FEMI_BAND")) band = (uint64_t)std::max(1, std::atoi(e));
             for (int64_t i = 0; i < n; ++i) {
                 const uint64_t x = (uint64_t)(M.vpix[i] % M.W), y = (uint64_t)(M.vpix[i] / M.W);
-                key[i] = {((y / kBand) << 40) | (x << 20) | y, (int32_t)i};
+                key[i] = {((y / band) << 40) | (x << 20) | y, (int32_t)i};
             }
             std::sort(key.begin(), key.end());
             for (int64_t i = 0; i < n; ++i) pi[i] = key[i].second;
@@ -325,7 +329,9 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         U(upload(S, &S->sell_base, base, st));
         U(upload(S, &S->sell_inv, pi, st));
         U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
-        U(alloc(S, &S->s_int, (size_t)std::max<int64_t>(n, 1)));
+        // padded to whole JDS tiles: the TMA tiles read s_int in kJdsRows blocks
+        U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
+        U(alloc(S, &S->q_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
         if (fits16) {
             c16.resize(c32.size());
             for (int32_t sl = 0, q = 0; sl < nsl; ++sl) {
@@ -339,6 +345,100 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         int32_t* d_src = nullptr;
         U(upload(S, &d_src, src, st));
         S->sell_src_tmp = d_src;
+        if (S->nnz_uu > kGraphNnz) {
+            // tiled jagged-diagonal layout (device.cuh) of the same internal order
+            const int32_t ntile = (int32_t)((n + kJdsRows - 1) / kJdsRows);
+            std::vector<int32_t> eb(ntile + 1), cbo(ntile + 1), jsrc;
+            std::vector<uint8_t> jcolb;  // per tile: int16 columns, or int32 when a column is out of range
+            // kmax = longest row; meta per tile: lengths + [slice][kmax] uint16 diagonal offsets
+            int32_t kmax = 1;
+            for (int64_t i = 0; i < n; ++i) kmax = std::max(kmax, rl((int32_t)i));
+            const int32_t meta_bytes = (kJdsRows + 2 * (kJdsRows / 32) * kmax + 15) / 16 * 16;
+            std::vector<uint8_t> meta((size_t)ntile * meta_bytes, 0);
+            bool ok = kmax <= kJdsMaxK;
+            int32_t maxe = 0, nwide = 0;
+            auto kth = [&](int32_t row, int32_t k) {  // k-th off-diagonal of a row (natural CSR)
+                int32_t e = M.uu_rowptr[row], q = 0;
+                for (; e < M.uu_rowptr[row + 1]; ++e) {
+                    if (M.uu_col[e] == row) continue;
+                    if (q == k) break;
+                    ++q;
+                }
+                return e;
+            };
+            std::vector<int64_t> tcol;
+            for (int32_t t = 0; t < ntile && ok; ++t) {
+                eb[t] = (int32_t)jsrc.size();
+                cbo[t] = (int32_t)jcolb.size();
+                tcol.clear();
+                const int64_t r0 = (int64_t)t * kJdsRows;
+                uint8_t* mt = meta.data() + (size_t)t * meta_bytes;
+                uint16_t* doff = (uint16_t*)(mt + kJdsRows);
+                for (int w = 0; w < kJdsRows / 32; ++w) {
+                    int32_t L = 0;
+                    for (int l = 0; l < 32; ++l) {
+                        const int64_t ri = r0 + 32 * w + l;
+                        const int32_t len = ri < n ? rl(pi[ri]) : 0;
+                        if (len > 255) ok = false;
+                        if (l > 0 && len > mt[32 * w + l - 1]) ok = false;  // descending inside the slice
+                        mt[32 * w + l] = (uint8_t)len;
+                        L = std::max(L, len);
+                    }
+                    for (int32_t k = 0; k < L; ++k) {
+                        const int64_t off = (int64_t)jsrc.size() - eb[t];
+                        if (off > 65535) ok = false;
+                        doff[w * kmax + k] = (uint16_t)off;
+                        for (int l = 0; l < 32; ++l) {
+                            const int64_t ri = r0 + 32 * w + l;
+                            if (ri >= n || rl(pi[ri]) <= k) continue;
+                            const int32_t row = pi[ri];
+                            const int32_t e = kth(row, k);
+                            tcol.push_back((int64_t)pos[M.uu_col[e]] - r0);
+                            jsrc.push_back((M.uu_rowptr[row] - row) + k);
+                        }
+                    }
+                }
+                while (jsrc.size() % 8) {  // 16-byte aligned tile blocks for the bulk copies
+                    tcol.push_back(0);
+                    jsrc.push_back(-1);
+                }
+                bool wide = false;
+                for (int64_t d : tcol) wide |= d < -32768 || d > 32767;
+                nwide += wide;
+                for (int64_t d : tcol) {
+                    if (wide) {
+                        const int32_t v = (int32_t)d;
+                        const uint8_t* b = (const uint8_t*)&v;
+                        jcolb.insert(jcolb.end(), b, b + 4);
+                    } else {
+                        const int16_t v = (int16_t)d;
+                        const uint8_t* b = (const uint8_t*)&v;
+                        jcolb.insert(jcolb.end(), b, b + 2);
+                    }
+                }
+                maxe = std::max(maxe, (int32_t)jsrc.size() - eb[t]);
+            }
+            eb[ntile] = (int32_t)jsrc.size();
+            cbo[ntile] = (int32_t)jcolb.size();
+            if (std::getenv("FEMI_DEBUG"))
+                std::fprintf(stderr, "[femi] jds layout: ok %d tiles %d (int32 columns: %d) entries %zu maxe %d kmax %d\n",
+                             (int)ok, ntile, nwide, jsrc.size(), maxe, kmax);
+            if (ok) {
+                S->jds_ntile = ntile;
+                S->jds_maxe = maxe;
+                S->jds_kmax = kmax;
+                S->jds_meta_bytes = meta_bytes;
+                S->jds_nnz = (int64_t)jsrc.size();
+                U(upload(S, &S->jds_eb, eb, st));
+                U(upload(S, &S->jds_cb, cbo, st));
+                U(upload(S, &S->jds_meta, meta, st));
+                U(upload(S, &S->jds_col, jcolb, st));
+                U(alloc(S, &S->jds_val, (size_t)std::max<int64_t>(S->jds_nnz, 1)));
+                int32_t* d_js = nullptr;
+                U(upload(S, &d_js, jsrc, st));
+                S->jds_src_tmp = d_js;
+            }
+        }
     }
     U(launch_tri_records(S, d_tri, d_flags, st));
     U(alloc(S, &S->tp_ptr, (size_t)M.T + 1));
@@ -352,7 +452,8 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         goto fail;
     }
     for (auto it = S->allocs.begin(); it != S->allocs.end();) {
-        if (*it == (void*)d_tri || *it == (void*)d_flags || *it == (void*)S->sell_src_tmp) {
+        if (*it == (void*)d_tri || *it == (void*)d_flags || *it == (void*)S->sell_src_tmp ||
+            (S->jds_src_tmp && *it == (void*)S->jds_src_tmp)) {
             cudaFree(*it);
             it = S->allocs.erase(it);
         } else {

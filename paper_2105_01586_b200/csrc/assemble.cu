@@ -104,10 +104,13 @@ __global__ void k_sell_values(int64_t ne, const int32_t* __restrict__ src, const
     }
 }
 
-__global__ void k_gather_s(int64_t n, const int32_t* __restrict__ inv, const double* __restrict__ s,
-                           double* __restrict__ s_int) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        s_int[i] = s[inv[i]];
+__global__ void k_gather_s(int64_t n, int64_t npad, const int32_t* __restrict__ inv, const double* __restrict__ s,
+                           double* __restrict__ s_int, double* __restrict__ q_int) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npad; i += (int64_t)gridDim.x * blockDim.x) {
+        const double si = i < n ? s[inv[i]] : 1.0;  // padding rows: harmless finite values
+        s_int[i] = si;
+        q_int[i] = 1.0 / si;
+    }
 }
 
 }  // namespace
@@ -119,8 +122,14 @@ femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStrea
         k_sell_values<<<g, 256, 0, st>>>(S->sell_nnz, d_src, S->o_val, S->sell_val);
         count_launches(1);
     }
+    if (S->jds_nnz > 0) {
+        int gj = (int)std::min<int64_t>((S->jds_nnz + 255) / 256, 148 * 16);
+        k_sell_values<<<gj, 256, 0, st>>>(S->jds_nnz, S->jds_src_tmp, S->o_val, S->jds_val);
+        count_launches(1);
+    }
     int g = (int)std::min<int64_t>((S->n_u + 255) / 256, 148 * 16);
-    k_gather_s<<<g, 256, 0, st>>>(S->n_u, S->sell_inv, S->s, S->s_int);
+    const int64_t npad = (S->n_u + kJdsRows - 1) / kJdsRows * kJdsRows;
+    k_gather_s<<<g, 256, 0, st>>>(S->n_u, npad, S->sell_inv, S->s, S->s_int, S->q_int);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;

@@ -117,8 +117,26 @@ struct femi_system_s {
     // tp_ptr[T+1] / tp_pix[N] (ascending pix per triangle; pix | cls << 30, cls 1..3 = vertex pixel)
     int32_t* tp_ptr = nullptr;
     uint32_t* tp_pix = nullptr;
+    // Tiled jagged-diagonal copy of the scaled off-diagonal matrix for the TMA-streamed SpMV of
+    // large systems (graph mode): tiles of kJdsRows internal rows; per tile a contiguous
+    // entry block [jds_eb[t], jds_eb[t+1]) (a multiple of 8 entries), inside it slice w (32
+    // rows) stores diagonal k = the k-th off-diagonal of every lane whose row has > k of them,
+    // lanes ascending; columns as int16 offsets from the tile's first row (int32 for a tile
+    // with a neighbour farther than 32767 rows, e.g. long image-border edges). jds_meta: per tile
+    // jds_meta_bytes = uint8 row lengths[kJdsRows] | uint16 diagonal offsets[kJdsRows/32][jds_kmax]
+    // (rows of a slice are in descending length order, so diagonal k of slice w is the lanes
+    // 0 .. cnt_k-1 at doff[w][k] + lane).
+    int32_t jds_ntile = 0, jds_maxe = 0, jds_kmax = 0, jds_meta_bytes = 0;
+    int32_t* jds_eb = nullptr;
+    int32_t* jds_cb = nullptr;   // per tile: byte offset of its columns (int32 if 4 bytes per entry)
+    uint8_t* jds_meta = nullptr;
+    double* jds_val = nullptr;
+    uint8_t* jds_col = nullptr;
+    int32_t* jds_src_tmp = nullptr;
+    int64_t jds_nnz = 0;
     int32_t* sell_inv = nullptr;      // n_u: internal solver row -> canonical unknown index
     double* s_int = nullptr;          // D^-1/2 in internal order
+    double* q_int = nullptr;          // D^1/2 = 1/s_int (unscaled residual monitor: r = r^ q)
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -143,6 +161,9 @@ constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)
 constexpr int kBand = 32;        // image band height (pixels) of the internal solver order
 femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st);
 constexpr int kChunkNnzCap = 2048;
+constexpr int64_t kGraphNnz = 600000;  // nnz(A_uu) above which one system solves in graph mode
+constexpr int kJdsRows = 512;          // rows per TMA tile of the jagged-diagonal layout
+constexpr int kJdsMaxK = 24;           // longest row (off-diagonals) the JDS layout takes
 
 // launchers (defined in the .cu files)
 femi_status launch_tri_records(femi_system_s* S, const int32_t* d_tri, const uint32_t* d_flags, cudaStream_t st);

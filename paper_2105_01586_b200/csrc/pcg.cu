@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "device.cuh"
+#include "tma.cuh"
 
 namespace femi {
 namespace {
@@ -52,6 +53,7 @@ struct RItem {
     const int16_t* c16;   // column - window base (internal numbering)
     const int32_t* c32;
     const double* s;     // D^-1/2 (internal order)
+    const double* q;     // D^1/2 (internal order): unscaled residual r = r^ q (monitor)
     const int32_t* urp;  // unscaled A_uu (diagonal included), canonical rows
     const int32_t* uci;
     const double* uav;
@@ -68,6 +70,13 @@ struct RItem {
     double* p;  // used when the CTA's rows do not fit shared memory
     double* sv;
     double *rec0, *rec1;  // graph mode, fused body: double-buffered {r, w, s, p} records (CgState::par)
+    const double* jval;   // graph mode: tiled jagged-diagonal matrix (device.cuh), TMA-streamed
+    const uint8_t* jcol;
+    const uint8_t* jmeta;
+    const int32_t* jeb;
+    const int32_t* jcb;
+    int32_t ntile, jmaxe, jkmax, jmbytes;
+    int32_t jpol, jpad;  // L2 policy of the streamed matrix: 0 none, 1 evict-first, 2 evict-last
     double* part;  // [ncta][4] partial sums / barrier slots
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
@@ -381,7 +390,7 @@ __device__ __forceinline__ double4 spmv_w(const RItem& it, int S0, int S1, const
             cb[h] = (32 * s / SIG) * SIG;
             const int rr = row[h] >= 0 ? row[h] : 32 * sa;
             xi[h] = r[rr];
-            si[h] = it.s[rr];
+            si[h] = it.q[rr];
         }
         const int L = max(len[0], len[1]);
         for (int k0 = 0; k0 < L; k0 += 4) {
@@ -412,7 +421,7 @@ __device__ __forceinline__ double4 spmv_w(const RItem& it, int S0, int S1, const
             if (row[h] < 0) continue;
             const double y = xi[h] + acc[h];
             it.w[row[h]] = y;
-            const double ru = xi[h] / si[h];
+            const double ru = xi[h] * si[h];
             loc.x += xi[h] * xi[h];
             loc.y += y * xi[h];
             loc.z += ru * ru;
@@ -630,10 +639,10 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
 // (deterministic), advances the CG recurrence scalars (FIRST: starts it) and, once every item
 // has reported, sets the WHILE condition (any item still active -> 1). FLIP: the fused body
 // swaps the double-buffered vectors.
-template <bool FIRST, bool FLIP>
+template <bool FIRST, bool FLIP, int NT = GNT>
 __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, int B, double* __restrict__ part,
                                         unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
-    __shared__ double shm[4 * (GNT / 32)];
+    __shared__ double shm[4 * (NT / 32)];
     __shared__ int last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -647,7 +656,7 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     if (threadIdx.x == 0) {
         for (int q = 0; q < 3; ++q) {
             double t = 0.0;
-            for (int w = 0; w < GNT / 32; ++w) t += shm[4 * w + q];
+            for (int w = 0; w < NT / 32; ++w) t += shm[4 * w + q];
             P[4 * blockIdx.x + q] = t;
         }
         __threadfence();
@@ -657,7 +666,7 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     if (!last) return;
     __threadfence();
     double tot[3] = {0.0, 0.0, 0.0};
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += GNT)
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += NT)
 #pragma unroll
         for (int q = 0; q < 3; ++q) tot[q] += __ldcg(P + 4 * b + q);
 #pragma unroll
@@ -669,7 +678,7 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     __syncthreads();
     if (threadIdx.x != 0) return;
     double gam2 = 0.0, del2 = 0.0, rho2 = 0.0;
-    for (int w = 0; w < GNT / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         gam2 += shm[4 * w];
         del2 += shm[4 * w + 1];
         rho2 += shm[4 * w + 2];
@@ -756,7 +765,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
                 cb[hh] = (32 * s / SIG) * SIG;
                 const int rr = row[hh] >= 0 ? row[hh] : 32 * sa;
                 xi[hh] = r[rr];
-                si[hh] = it.s[rr];
+                si[hh] = it.q[rr];
             }
             const int L = max(len[0], len[1]);
             for (int k0 = 0; k0 < L; k0 += 4) {
@@ -787,7 +796,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
                 if (row[hh] < 0) continue;
                 const double y = xi[hh] + acc[hh];
                 wout[row[hh]] = y;
-                const double ru = xi[hh] / si[hh];
+                const double ru = xi[hh] * si[hh];
                 v[0] += xi[hh] * xi[hh];
                 v[1] += y * xi[hh];
                 v[2] += ru * ru;
@@ -895,7 +904,7 @@ __global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, 
                     o.p = pn[hh];
                     R1[i] = o;
                 }
-                const double ru = rn[hh] / it.s[i];
+                const double ru = rn[hh] * it.q[i];
                 v[0] += rn[hh] * rn[hh];
                 v[1] += y * rn[hh];
                 v[2] += ru * ru;
@@ -903,6 +912,191 @@ __global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, 
         }
     }
     cg_tail<FIRST, !FIRST>(v, act, S, B, part, gcnt, h);
+}
+
+// S of the graph-mode body for large systems: w = r + A^_off r and the dots, with the matrix
+// and the own-row vectors STREAMED by TMA. One CTA per SM owns a contiguous range of
+// kJdsRows-row tiles; its producer warp (one elected lane) issues per tile five bulk copies
+// (values, int16 columns, row lengths + diagonal offsets, r, q) into a JNS-stage shared-memory ring
+// guarded by full/empty mbarriers; JCW consumer warps take one 32-row slice each, read the
+// jagged diagonals of their slice from shared memory (rows in descending length: diagonal k is
+// lanes 0 .. cnt_k-1 at doff[k] + lane) and gather the neighbours' r (L1/L2).
+// Bytes per iteration: 10 B per stored nonzero (no ELL padding) + 1.06 B/row of metadata +
+// r, s read + w written; the async stream keeps ~JNS tiles of loads in flight per SM.
+constexpr int JCW = kJdsRows / 32;  // consumer warps = slices per tile
+constexpr int JNT = 32 * (JCW + 1);
+constexpr int JNS = 6;
+
+struct JStage {
+    double* val;
+    uint8_t* col;
+    uint8_t* meta;
+    double* r;
+    double* s;
+};
+
+// JP: tiles a consumer warp works on at once; GM: neighbour gathers 0 = global (L1/L2), 1 = shared
+// memory inside the tile, 2 = none (experiment: streaming only, wrong result)
+template <int JP, int GM>
+__global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
+                                            unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+    extern __shared__ __align__(128) unsigned char jsm[];
+    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
+    __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
+    const RItem& it = items[0];
+    CgState* S = it.st;
+    const bool act = S->active;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntile = it.ntile;
+    const int tb = (int)((int64_t)ntile * blockIdx.x / gridDim.x), te = (int)((int64_t)ntile * (blockIdx.x + 1) / gridDim.x);
+    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
+    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 16 * kJdsRows + 127) & ~(size_t)127;
+    auto stage = [&](int k) {
+        unsigned char* b = jsm + (size_t)k * stage_bytes;
+        JStage q;
+        q.r = (double*)b;
+        q.s = q.r + kJdsRows;
+        q.val = q.s + kJdsRows;
+        q.col = (uint8_t*)(q.val + maxe);
+        q.meta = q.col + 4 * (size_t)maxe;
+        return q;
+    };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < JNS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], JCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double v[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        if (warp == JCW) {
+            // ---- producer
+            if (lane == 0) {
+                int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
+                const int pm = it.jpol;
+                const uint64_t pol = pm == 1 ? policy_evict_first() : policy_evict_last();
+                for (int t = tb, i = 0; t < te; ++t, ++i) {
+                    const int k = i % JNS;
+                    const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];  // loaded before the wait
+                    if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);
+                    const JStage q = stage(k);
+                    const int ne = e1 - e0, nc = c1 - c0;
+                    tile_e[k] = make_int2(e0, ne);
+                    tile_c[k] = make_int2(c0, nc);
+                    const uint32_t bytes = (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 16u * kJdsRows;
+                    mbar_arrive_expect_tx(&full[k], bytes);
+                    bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
+                    if (ne) {
+                        if (pm) {
+                            bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
+                            bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
+                        } else {
+                            bulk_g2s(q.val, it.jval + e0, 8u * ne, &full[k]);
+                            bulk_g2s(q.col, it.jcol + c0, (uint32_t)nc, &full[k]);
+                        }
+                    }
+                    e0 = e1;
+                    c0 = c1;
+                }
+            }
+        } else {
+            // ---- consumers: warp = slice of the tile, lane = row (rows in descending length).
+            // JP tiles at a time: their gathers are in flight together (the latency chain
+            // smem -> gather -> fma is the critical path of a warp).
+            const double* __restrict__ rg = it.r;
+            double* __restrict__ wout = it.w;
+            const int rl = 32 * warp + lane;
+            const int cnt = te - tb;
+            for (int i0 = 0; i0 < cnt; i0 += JP) {
+                int len[JP], L[JP];
+                bool wide[JP];
+                const uint16_t* doff[JP];
+                const double* val[JP];
+                const uint8_t* col[JP];
+                const double* rt[JP];
+                const double* sr[JP];
+                double xi[JP], qi[JP], acc[JP];
+                int Lm = 0;
+#pragma unroll
+                for (int p = 0; p < JP; ++p) {
+                    const int i = i0 + p;
+                    if (i < cnt) {
+                        const int k = i % JNS;
+                        mbar_wait(&full[k], (i / JNS) & 1);
+                        const JStage q = stage(k);
+                        len[p] = q.meta[rl];
+                        doff[p] = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
+                        xi[p] = q.r[rl];
+                        qi[p] = q.s[rl];
+                        wide[p] = tile_c[k].y > 2 * tile_e[k].y;  // written before the release of this stage
+                        val[p] = q.val;
+                        col[p] = q.col;
+                        rt[p] = rg + (int64_t)(tb + i) * kJdsRows;
+                        sr[p] = q.r;
+                    } else {
+                        sr[p] = nullptr;
+                        len[p] = 0;
+                        doff[p] = nullptr;
+                        xi[p] = qi[p] = 0.0;
+                        wide[p] = false;
+                        val[p] = nullptr;
+                        col[p] = nullptr;
+                        rt[p] = rg;
+                    }
+                    L[p] = __shfl_sync(0xffffffffu, len[p], 0);  // lane 0 holds the longest row
+                    Lm = max(Lm, L[p]);
+                    acc[p] = 0.0;
+                }
+                for (int k0 = 0; k0 < Lm; k0 += 8) {
+                    double vv[JP][8], gv[JP][8];
+                    int c[JP][8];
+#pragma unroll
+                    for (int p = 0; p < JP; ++p)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const bool a = k0 + u < len[p];
+                            const int idx = (k0 + u < L[p] ? doff[p][k0 + u] : 0) + lane;
+                            vv[p][u] = a ? val[p][idx] : 0.0;
+                            c[p][u] = a ? (wide[p] ? ((const int32_t*)col[p])[idx] : (int)((const int16_t*)col[p])[idx])
+                                        : rl;
+                        }
+#pragma unroll
+                    for (int p = 0; p < JP; ++p)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (GM == 2) gv[p][u] = 1.0;
+                            else if (GM == 1 && (unsigned)c[p][u] < (unsigned)kJdsRows) gv[p][u] = sr[p][c[p][u]];
+                            else gv[p][u] = rt[p][c[p][u]];
+                        }
+#pragma unroll
+                    for (int p = 0; p < JP; ++p)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[p] = fma(vv[p][u], gv[p][u], acc[p]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int p = 0; p < JP; ++p) {
+                    const int i = i0 + p;
+                    if (i >= cnt) break;
+                    if (lane == 0) mbar_arrive(&empty[i % JNS]);
+                    const int row = (tb + i) * kJdsRows + rl;
+                    if (row < it.n) {
+                        const double y = xi[p] + acc[p];
+                        wout[row] = y;
+                        const double ru = xi[p] * qi[p];
+                        v[0] += xi[p] * xi[p];
+                        v[1] += y * xi[p];
+                        v[2] += ru * ru;
+                    }
+                }
+            }
+        }
+    }
+    cg_tail<false, false, JNT>(v, act, S, B, part, gcnt, h);
 }
 
 // rec[cur] = {r, 0, 0, 0} from the plain residual (start and restart of the recurrence)
@@ -929,6 +1123,8 @@ struct GraphCache {
     cudaGraphExec_t main = nullptr, restart = nullptr;
     RItem item{};
     int gs_blocks = 0, gx = 0, gp_blocks = 0;
+    int gt_blocks = 0;
+    unsigned gt_smem = 0;  // > 0: the body's SpMV is the TMA-streamed k_gt
 };
 
 struct Workspace {
@@ -952,13 +1148,13 @@ int g_shape = 1;
 namespace {
 
 femi_status add_kernel(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid, dim3 block, void** args,
-                       cudaGraphNode_t* out) {
+                       cudaGraphNode_t* out, unsigned smem = 0) {
     cudaGraphNodeParams p = {};
     p.type = cudaGraphNodeTypeKernel;
     p.kernel.func = fn;
     p.kernel.gridDim = grid;
     p.kernel.blockDim = block;
-    p.kernel.sharedMemBytes = 0;
+    p.kernel.sharedMemBytes = smem;
     p.kernel.kernelParams = args;
     FEMI_CUDA(cudaGraphAddNode(out, gr, dep, dep ? 1 : 0, &p));
     return FEMI_OK;
@@ -1027,7 +1223,11 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
             if ((s = add_kernel(body, nullptr, (void*)k_gu, dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT),
                                 a_items, &u)))
                 return s;
-            if ((s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn))) return s;
+            if (C.gt_smem)
+                s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem);
+            else
+                s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn);
+            if (s) return s;
         }
     }
     if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
@@ -1054,7 +1254,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         C->gs_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)),
                                                                    148 * 8));
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-        const size_t vb = al(sizeof(double) * (n + 1));
+        const size_t vb = al(sizeof(double) * std::max<int64_t>(n + 1, (int64_t)S->jds_ntile * kJdsRows));
         {
             int per_sm = 0, nsm = 0, dev = 0;
             FEMI_CUDA(cudaGetDevice(&dev));
@@ -1063,7 +1263,24 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             C->gp_blocks = (int)std::max<int64_t>(
                 1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)), (int64_t)std::max(1, per_sm) * nsm));
         }
-        const int pb = std::max(C->gs_blocks, C->gp_blocks);
+        if (S->jds_ntile > 0 && std::getenv("FEMI_PCG_NOTMA") == nullptr) {
+            const size_t stage_bytes =
+                ((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 16 * kJdsRows + 127) & ~(size_t)127;
+            int dev = 0, nsm = 0, optin = 0;
+            FEMI_CUDA(cudaGetDevice(&dev));
+            FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            FEMI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            if (std::getenv("FEMI_DEBUG"))
+                std::fprintf(stderr, "[femi] k_gt: stage %zu B x %d, optin %d\n", stage_bytes, JNS, optin);
+            if (JNS * stage_bytes + 1024 <= (size_t)optin) {
+                C->gt_smem = (unsigned)(JNS * stage_bytes);
+                C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
+                for (const void* fn : {(const void*)k_gt<1, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
+                                       (const void*)k_gt<1, 2>})
+                    FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
+            }
+        }
+        const int pb = std::max(std::max(C->gs_blocks, C->gp_blocks), C->gt_blocks);
         const size_t rb = al(sizeof(Rec) * (n + 1));
         const size_t bytes = al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
                              al(sizeof(double) * 4 * pb) + al(sizeof(double) * KGRID) + 6 * vb + 2 * rb;
@@ -1088,6 +1305,17 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.sv = (double*)take(vb);
         it.rec0 = (double*)take(rb);
         it.rec1 = (double*)take(rb);
+        it.jval = S->jds_val;
+        it.jcol = S->jds_col;
+        it.jmeta = S->jds_meta;
+        it.jeb = S->jds_eb;
+        it.jcb = S->jds_cb;
+        it.ntile = S->jds_ntile;
+        it.jmaxe = S->jds_maxe;
+        it.jkmax = S->jds_kmax;
+        it.jmbytes = S->jds_meta_bytes;
+        it.jpol = 1;
+        if (const char* pe = std::getenv("FEMI_JDS_POLICY")) it.jpol = std::atoi(pe);
         it.inv = S->sell_inv;
         it.len = S->sell_len;
         it.base = S->sell_base;
@@ -1095,6 +1323,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.c16 = S->sell_c16;
         it.c32 = S->sell_c32;
         it.s = S->s_int;
+        it.q = S->q_int;
         it.urp = S->uu_rowptr;
         it.uci = S->uu_col;
         it.uav = S->uu_val;
@@ -1179,6 +1408,28 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 ts += b;
             }
         }
+        float tt[4] = {0, 0, 0, 0};
+        void (*const gts[4])(const RItem*, int, double*, unsigned*, cudaGraphConditionalHandle) = {
+            k_gt<1, 0>, k_gt<2, 0>, k_gt<1, 1>, k_gt<1, 2>};
+        if (C->gt_smem)
+            for (int v = 0; v < 4; ++v)
+                for (int k = 0; k < reps; ++k) {
+                    act.par = 0;
+                    cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
+                    k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);  // r in L2, as in the loop
+                    cudaEventRecord(e0, st);
+                    gts[v]<<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
+                    cudaEventRecord(e1, st);
+                    cudaEventSynchronize(e1);
+                    float a;
+                    cudaEventElapsedTime(&a, e0, e1);
+                    if (k > 1) tt[v] += a;
+                }
+        std::fprintf(stderr,
+                     "[femi kbench] k_gt (TMA, grid %d, smem %u): JP1 %.2f us  JP2 %.2f us  smem-gather %.2f us  "
+                     "no-gather %.2f us\n",
+                     C->gt_blocks, C->gt_smem, 1e3 * tt[0] / (reps - 2), 1e3 * tt[1] / (reps - 2),
+                     1e3 * tt[2] / (reps - 2), 1e3 * tt[3] / (reps - 2));
         std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grids %d / %d)  fused k_gp %.2f us (grid %d)\n",
                      1e3 * tu / (reps - 2), 1e3 * ts / (reps - 2), gu, C->gs_blocks, 1e3 * tf / (reps - 2),
                      C->gp_blocks);
@@ -1325,6 +1576,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.c16 = s->sell_c16;
         it.c32 = s->sell_c32;
         it.s = s->s_int;
+        it.q = s->q_int;
         it.urp = s->uu_rowptr;
         it.uci = s->uu_col;
         it.uav = s->uu_val;

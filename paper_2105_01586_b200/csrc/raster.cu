@@ -179,32 +179,43 @@ __device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_pt
 
 // One triangle as the fused raster keeps it in shared memory (one slot per lane): the two
 // exact integer edge functions as planes w = A px + B py + C (S3: w_b = orient(c,a,p),
-// w_c = orient(a,b,p)), D = orient(a,b,c), u_a and the differences u_b - u_a, u_c - u_a.
+// w_c = orient(a,b,p)), D = orient(a,b,c) and its correctly rounded reciprocal, u_a and the
+// differences u_b - u_a, u_c - u_a.
 struct RTri {
     int A1, B1, C1, A2, B2, C2, pad0, pad1;
-    double D, db, dc, u[3];
+    double D, rD, db, dc, u[3], pad2;
 };
 
 __device__ __forceinline__ int tp_x(uint32_t v) { return (int)(v & 0x3fffu); }
 __device__ __forceinline__ int tp_y(uint32_t v) { return (int)((v >> 14) & 0x3fffu); }
 
-// S3+S4 in ONE triangle-major pass (no owner-map read, no second pass over e): a warp takes
-// 32 consecutive triangles, keeps them in shared memory and walks their owned pixels
-// (tp_pix, ascending pix per triangle) 2 x 32 at a time:
-//   u  = the vertex value (vertex pixel) or (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
-//   e  = (u - f)^2 ; u and e written, f read at the pixel (row segments: L2-merged sectors)
-// and reduces per triangle (sum of e, arg-max of e over non-vertex pixels, ties -> lowest
-// pix) by segmented warp scans in pixel order; SSE = fixed-order sum of the triangle sums.
-// Deterministic, no atomics on values.
+// Correctly rounded w / D for an exact integer w (|w| < 2^53) given rD = RN(1/D): q = RN(w rD)
+// is within 1 ulp of w/D, the remainder w - qD is exact under fma, and RN(q + r rD) is RN(w/D)
+// (Markstein's theorem) -- the IEEE quotient of __ddiv_rn at three fp64 operations.
+__device__ __forceinline__ double div_rn(double w, double D, double rD) {
+    const double q = __dmul_rn(w, rD);
+    const double r = __fma_rn(-q, D, w);
+    return __fma_rn(r, rD, q);
+}
+
+constexpr int RCH = 128;  // list entries per warp chunk (4 x 32 lanes)
+
+// S3+S4 in ONE triangle-major pass. A warp takes 32 consecutive triangles (smem, one slot per
+// lane) and walks their owned pixels (tp_pix: ascending pix per triangle) in chunks of RCH:
+//  phase 1, lane per entry (coalesced list reads, f gathered and u, e written along row
+//   segments): u = the vertex value (vertex pixel) or (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
+//   with l = w / D in IEEE fp64 (S3's barycentric form, one rounding per operation, no
+//   contraction), e = (u - f)^2; e is staged in shared memory;
+//  phase 2, lane per triangle: the lane walks its triangle's entries of the chunk in pixel
+//   order: tri_err += e, best = first strict maximum over non-vertex pixels (ties: lowest
+//   pix) -- the oracle's sequential order, so tri_err and best are bit-identical to it.
+// SSE = sum of per-group partials in group order (k_sse). Deterministic, no atomics on values.
 template <int MINB>
-__global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ part,
-                                                   uint32_t* __restrict__ counters) {
+__global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ gpart,
+                                                   uint32_t* __restrict__ next, int64_t gstride) {
     __shared__ RTri tris[RWARPS][32];
-    __shared__ double acc_s[RWARPS][32];
-    __shared__ double be_s[RWARPS][32];
-    __shared__ int bp_s[RWARPS][32];
-    __shared__ double red[RWARPS];
-    __shared__ int flag;
+    __shared__ double e_s[RWARPS][RCH];
+    __shared__ int p_s[RWARPS][RCH];  // pix, or -1 for a vertex pixel (not a candidate)
     const RasterItem& it = items[blockIdx.y];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t T = it.T;
@@ -214,10 +225,18 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
     double* __restrict__ e_px = it.e_px;
     const uint32_t* __restrict__ tp_pix = it.tp_pix;
     const int64_t ngroups = (T + 31) / 32;
-    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
     RTri* ws = tris[wid];
-    double sse_loc = 0.0;
-    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+    double* __restrict__ gp = gpart + gstride * blockIdx.y;
+    double* es = e_s[wid];
+    int* ps = p_s[wid];
+    // groups of 32 triangles are handed out in canonical order by an atomic counter: the warps
+    // in flight cover one narrow band of rows, so the f/u/e sectors they share are completed
+    // in L2 before eviction (no partial-sector write-backs)
+    for (;;) {
+        int64_t g = 0;
+        if (lane == 0) g = (int64_t)atomicAdd(next + blockIdx.y, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngroups) break;
         const int64_t t0 = g * 32;
         int cnt;
         const ListWalk lw = list_begin(it.tp_ptr, T, t0, cnt);
@@ -234,105 +253,99 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
             I.B2 = bx - ax;
             I.C2 = (by - ay) * ax - (bx - ax) * ay;
             I.D = (double)orient_xy(ax, ay, bx, by, cx, cy);
+            I.rD = __drcp_rn(I.D);
             I.u[0] = it.u_vert[R.v[0]];
             I.u[1] = it.u_vert[R.v[1]];
             I.u[2] = it.u_vert[R.v[2]];
-            I.db = I.u[1] - I.u[0];
-            I.dc = I.u[2] - I.u[0];
+            I.db = __dsub_rn(I.u[1], I.u[0]);
+            I.dc = __dsub_rn(I.u[2], I.u[0]);
             ws[lane] = I;
         }
-        acc_s[wid][lane] = 0.0;
-        be_s[wid][lane] = -1.0;
-        bp_s[wid][lane] = -1;
         __syncwarp();
-        for (int base = 0; base < lw.total; base += 64) {
-            uint32_t v[2];
-            int j[2], seg0[2];
-            double fv[2];
+        double acc = 0.0, be = -1.0;
+        int bp = -1;
+        const int my0 = lw.excl, my1 = lw.excl + cnt;
+        for (int c0 = 0; c0 < lw.total; c0 += RCH) {
+            // ---- phase 1: lane per entry
+            uint32_t v[RCH / 32];
+            int j[RCH / 32];
+            double fv[RCH / 32];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int k = base + 32 * h + lane;
+            for (int h = 0; h < RCH / 32; ++h) {
+                const int k = c0 + 32 * h + lane;
                 j[h] = warp_find(lw.excl, k, lw.total);
-                // first lane of this lane's triangle inside the window (segmented-scan bound)
-                const int ex = __shfl_sync(0xffffffffu, lw.excl, j[h] & 31);
-                seg0[h] = max(0, ex - (base + 32 * h));
                 v[h] = j[h] < 32 ? tp_pix[lw.ptr0 + k] : 0u;
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < RCH / 32; ++h)
                 fv[h] = (f && j[h] < 32) ? f[(int64_t)tp_y(v[h]) * W + tp_x(v[h])] : 0.0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (base + 32 * h >= lw.total) break;  // warp-uniform
-                double val = 0.0, ce = -1.0;
-                int cp = 0x7fffffff;
-                if (j[h] < 32) {
-                    const int px = tp_x(v[h]), py = tp_y(v[h]);
-                    const int pix = py * W + px;
-                    const uint32_t cls = v[h] >> 30;
-                    const RTri& I = ws[j[h]];
-                    double u;
-                    if (cls) {
-                        u = I.u[cls - 1];
-                    } else {
-                        // S3 as the paper's barycentric form, IEEE round-to-nearest per operation
-                        // and no contraction: l_b = w_b / D, l_c = w_c / D,
-                        // u = (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
-                        const int w1 = I.A1 * px + I.B1 * py + I.C1;
-                        const int w2 = I.A2 * px + I.B2 * py + I.C2;
-                        const double lb = __ddiv_rn((double)w1, I.D), lc = __ddiv_rn((double)w2, I.D);
-                        u = __dadd_rn(__dadd_rn(I.u[0], __dmul_rn(lb, I.db)), __dmul_rn(lc, I.dc));
-                    }
-                    if (u_px) u_px[pix] = u;
-                    if (f) {
-                        const double d = __dsub_rn(u, fv[h]);
-                        const double e = __dmul_rn(d, d);
-                        if (e_px) e_px[pix] = e;
-                        val = e;
-                        if (!cls) {
-                            ce = e;
-                            cp = pix;
-                        }
-                    }
+            for (int h = 0; h < RCH / 32; ++h) {
+                if (j[h] >= 32) continue;
+                const int px = tp_x(v[h]), py = tp_y(v[h]);
+                const int pix = py * W + px;
+                const uint32_t cls = v[h] >> 30;
+                const RTri& I = ws[j[h]];
+                double u;
+                if (cls) {
+                    u = I.u[cls - 1];
+                } else {
+                    const int w1 = I.A1 * px + I.B1 * py + I.C1;
+                    const int w2 = I.A2 * px + I.B2 * py + I.C2;
+                    const double lb = div_rn((double)w1, I.D, I.rD), lc = div_rn((double)w2, I.D, I.rD);
+                    u = __dadd_rn(__dadd_rn(I.u[0], __dmul_rn(lb, I.db)), __dmul_rn(lc, I.dc));
                 }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double vo = __shfl_up_sync(0xffffffffu, val, o);
-                    const double eo = __shfl_up_sync(0xffffffffu, ce, o);
-                    const int po = __shfl_up_sync(0xffffffffu, cp, o);
-                    if (lane - o >= seg0[h]) {
-                        val += vo;
-                        if (eo > ce || (eo == ce && po < cp)) {
-                            ce = eo;
-                            cp = po;
-                        }
-                    }
+                if (u_px) u_px[pix] = u;
+                if (f) {
+                    const double d = __dsub_rn(u, fv[h]);
+                    const double e = __dmul_rn(d, d);
+                    if (e_px) e_px[pix] = e;
+                    es[32 * h + lane] = e;
+                    ps[32 * h + lane] = cls ? -1 : pix;
                 }
-                const int jj = j[h];
-                const int jn = __shfl_down_sync(0xffffffffu, jj, 1);
-                if (jj < 32 && (lane == 31 || jn != jj)) {
-                    acc_s[wid][jj] += val;
-                    if (ce > be_s[wid][jj]) {  // earlier windows hold lower pixels: strict > keeps ties
-                        be_s[wid][jj] = ce;
-                        bp_s[wid][jj] = cp;
-                    }
-                }
-                __syncwarp();
             }
+            __syncwarp();
+            // ---- phase 2: lane per triangle, pixel order
+            if (f) {
+                const int lo = max(my0, c0), hi = min(my1, c0 + RCH);
+                for (int k = lo; k < hi; ++k) {
+                    const double e = es[k - c0];
+                    acc = __dadd_rn(acc, e);
+                    const int pk = ps[k - c0];
+                    if (pk >= 0 && e > be) {
+                        be = e;
+                        bp = pk;
+                    }
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
         if (t0 + lane < T && f) {
-            const double a = acc_s[wid][lane];
-            if (it.tri_err) it.tri_err[t0 + lane] = a;
-            if (it.best) it.best[t0 + lane] = be_s[wid][lane] >= 0.0 ? bp_s[wid][lane] : -1;
-            sse_loc += a;
+            if (it.tri_err) it.tri_err[t0 + lane] = acc;
+            if (it.best) it.best[t0 + lane] = bp;
         }
-        __syncwarp();
+        if (f) {  // group partial of the SSE (fixed tree order); summed in group order by k_sse
+            const double gs = warp_sum(t0 + lane < T ? acc : 0.0);
+            if (lane == 0) gp[g] = gs;
+        }
     }
-    if (!it.sse || !f) return;
-    const double tot = block_sum<RT>(sse_loc, red);
+}
+
+// SSE = sum of the per-group partials in group order (two fixed levels: deterministic)
+__global__ void __launch_bounds__(RT) k_sse(const RasterItem* __restrict__ items, const double* __restrict__ gpart,
+                                           int64_t gstride, double* __restrict__ part, uint32_t* __restrict__ counters) {
+    __shared__ double red[RWARPS];
+    __shared__ int flag;
+    const RasterItem& it = items[blockIdx.y];
+    if (!it.sse || !it.f) return;
+    const int64_t ng = (it.T + 31) / 32;
+    const int64_t a = ng * blockIdx.x / gridDim.x, b = ng * (blockIdx.x + 1) / gridDim.x;
+    const double* gp = gpart + gstride * blockIdx.y;
+    double s = 0.0;
+    for (int64_t k = a + threadIdx.x; k < b; k += RT) s += gp[k];
+    s = block_sum<RT>(s, red);
     double* P = part + (size_t)blockIdx.y * gridDim.x;
-    if (threadIdx.x == 0) P[blockIdx.x] = tot;
+    if (threadIdx.x == 0) P[blockIdx.x] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -341,11 +354,11 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
     __syncthreads();
     if (flag) {
         __threadfence();
-        double s = 0.0;
-        for (int k = threadIdx.x; k < (int)gridDim.x; k += RT) s += __ldcg(&P[k]);
-        s = block_sum<RT>(s, red);
+        double t = 0.0;
+        for (int k = threadIdx.x; k < (int)gridDim.x; k += RT) t += __ldcg(&P[k]);
+        t = block_sum<RT>(t, red);
         if (threadIdx.x == 0) {
-            *it.sse = s;
+            *it.sse = t;
             counters[blockIdx.y] = 0;
         }
     }
@@ -499,24 +512,29 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
             &per, minb == 4 ? (const void*)k_raster_tri<4> : (const void*)k_raster_tri<1>, RT, 0));
         resident = std::max(1, per) * nsm;
     }
-    // one wave of resident CTAs (no partial last wave), grid-stride over 32-triangle groups
+    // one wave of resident CTAs; 32-triangle groups handed out dynamically in canonical order
     const int64_t groups = (Tmax + 31) / 32;
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((groups + RWARPS - 1) / RWARPS,
                                                               (int64_t)std::max(1, resident / B)));
+    constexpr int SSEB = 148;
     const size_t bytes_items = sizeof(RasterItem) * B;
-    const size_t bytes_part = sizeof(double) * (size_t)gx * B;
-    const size_t bytes_cnt = sizeof(uint32_t) * B;
+    const size_t bytes_gpart = sizeof(double) * (size_t)groups * B;
+    const size_t bytes_part = sizeof(double) * (size_t)SSEB * B;
+    const size_t bytes_cnt = sizeof(uint32_t) * 2 * B;
     void* base = nullptr;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    FEMI_CUDA(cudaMallocAsync(&base, al(bytes_items) + al(bytes_part) + al(bytes_cnt), st));
+    FEMI_CUDA(cudaMallocAsync(&base, al(bytes_items) + al(bytes_gpart) + al(bytes_part) + al(bytes_cnt), st));
     char* cur = (char*)base;
     RasterItem* d_items = (RasterItem*)cur;
-    double* d_part = (double*)(cur + al(bytes_items));
+    double* d_gpart = (double*)(cur + al(bytes_items));
+    double* d_part = (double*)((char*)d_gpart + al(bytes_gpart));
     uint32_t* d_cnt = (uint32_t*)((char*)d_part + al(bytes_part));
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
-    if (minb == 4) k_raster_tri<4><<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
-    else k_raster_tri<1><<<dim3(gx, B), RT, 0, st>>>(d_items, d_part, d_cnt);
+    if (minb == 4) k_raster_tri<4><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    else k_raster_tri<1><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    k_sse<<<dim3(SSEB, B), RT, 0, st>>>(d_items, d_gpart, groups, d_part, d_cnt + B);
+    count_launches(1);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
