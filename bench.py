@@ -12,7 +12,7 @@ so no extra flush is needed between steps.
     value  = whole-job Mpixels/s = ranks * W*H * K / max-over-ranks device time
     e2e    = the same with f and g copied host->device (pinned) and SSE device->host
              inside every step
-    roofline: the PCG loop (k_spmv_dot + k_update), algorithmic bytes per iteration
+    roofline: the PCG iteration (k_gu update + k_gt TMA SpMV), algorithmic bytes per iteration
              12 nnz_uu + 4 (n_u+1) + 80 n_u x iterations over
              the solve's device time, against MEASURED_PEAKS.json hbm_gbs.
     cpu_baseline: the fp64 oracle (oracle/, 1 thread) on the same workload, run in a
@@ -387,7 +387,7 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, c),
-            "roofline": {"bound": "hbm", "kernel": "pcg loop (k_spmv_dot + k_update)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "PCG iteration (k_gu + k_gt in the graph WHILE loop)", "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_iter": bytes_iter, "iters": iters,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"},

@@ -77,6 +77,7 @@ struct RItem {
     const int32_t* jcb;
     int32_t ntile, jmaxe, jkmax, jmbytes;
     int32_t jpol, jpad;  // L2 policy of the streamed matrix: 0 none, 1 evict-first, 2 evict-last
+    const int32_t* jpart;  // [gt_blocks + 1] first tile of each k_gt CTA
     double* part;  // [ncta][4] partial sums / barrier slots
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
@@ -596,11 +597,30 @@ __global__ void k_zero_ps(const RItem* __restrict__ items) {
     }
 }
 
+__device__ int g_gt_prof;                     // kbench: per-CTA start/end times of k_gt
+__device__ unsigned long long g_gt_times[2 * 1024];
+// FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
+constexpr int kLoopProfMax = 4096;
+__device__ int g_loop_prof;
+__device__ unsigned long long g_loop_ts[4 * kLoopProfMax];
+__device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];  // k_gt: max start, min/max consumer end
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void loop_stamp(int kern, int iter, unsigned long long t0) {
+    if (iter < 0 || iter >= kLoopProfMax) return;
+    atomicMin(&g_loop_ts[4 * iter + 2 * kern], t0);
+    atomicMax(&g_loop_ts[4 * iter + 2 * kern + 1], gtime());
+}
+
 // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
 __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
     const CgState* S = it.st;
     if (!S->active) return;
+    const unsigned long long tprof = g_loop_prof ? gtime() : 0ull;
     const double alpha = S->alpha, beta = S->beta;
     double* __restrict__ r = it.r;
     const double* __restrict__ w = it.w;
@@ -632,6 +652,10 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
             x[j] = fma(alpha, pj, xj);
             r[j] = fma(-alpha, sj, rj);
         }
+    }
+    if (g_loop_prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) loop_stamp(0, S->iters, tprof);
     }
 }
 
@@ -926,6 +950,7 @@ __global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, 
 constexpr int JCW = kJdsRows / 32;  // consumer warps = slices per tile
 constexpr int JNT = 32 * (JCW + 1);
 constexpr int JNS = 6;
+constexpr int kUnroll = 4;  // CG iterations per WHILE body (graph mode)
 
 struct JStage {
     double* val;
@@ -935,12 +960,14 @@ struct JStage {
     double* s;
 };
 
-// JP: tiles a consumer warp works on at once; GM: neighbour gathers 0 = global (L1/L2), 1 = shared
+// JP: tiles a consumer warp works on at once (0: software-pipelined, one tile ahead); GM: neighbour gathers 0 = global (L1/L2), 1 = shared
 // memory inside the tile, 2 = none (experiment: streaming only, wrong result)
 template <int JP, int GM>
 __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
                                             unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
     extern __shared__ __align__(128) unsigned char jsm[];
+    unsigned long long t_start = 0;
+    if ((g_gt_prof || g_loop_prof) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
     __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
     const RItem& it = items[0];
@@ -948,7 +975,9 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     const bool act = S->active;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntile = it.ntile;
-    const int tb = (int)((int64_t)ntile * blockIdx.x / gridDim.x), te = (int)((int64_t)ntile * (blockIdx.x + 1) / gridDim.x);
+    // contiguous tile range per CTA, balanced by bytes at setup (it.jpart)
+    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
+    (void)ntile;
     const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
     const size_t stage_bytes = ((size_t)maxe * 12 + mb + 16 * kJdsRows + 127) & ~(size_t)127;
     auto stage = [&](int k) {
@@ -1005,12 +1034,86 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             }
         } else {
             // ---- consumers: warp = slice of the tile, lane = row (rows in descending length).
-            // JP tiles at a time: their gathers are in flight together (the latency chain
-            // smem -> gather -> fma is the critical path of a warp).
             const double* __restrict__ rg = it.r;
             double* __restrict__ wout = it.w;
             const int rl = 32 * warp + lane;
             const int cnt = te - tb;
+            if constexpr (JP == 0) {
+                // software pipeline over the tiles: the first 8 diagonals of tile i+1 are read and
+                // their neighbour gathers issued before tile i's products are summed, so a warp
+                // always has one tile's gathers in flight (rows with > 8 off-diagonals finish
+                // their remaining diagonals synchronously)
+                double vv[8], gv[8];
+                double xi = 0.0, qi = 0.0;
+                int len = 0, L = 0, kst = 0;
+                auto load = [&](int i, double (&vo)[8], double (&go)[8], double& xo, double& qo, int& lo, int& Lo,
+                                int& ko) {
+                    ko = i % JNS;
+                    mbar_wait(&full[ko], (i / JNS) & 1);
+                    const JStage q = stage(ko);
+                    lo = q.meta[rl];
+                    Lo = __shfl_sync(0xffffffffu, lo, 0);
+                    xo = q.r[rl];
+                    qo = q.s[rl];
+                    const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
+                    const bool wide = tile_c[ko].y > 2 * tile_e[ko].y;
+                    const double* rt = rg + (int64_t)(tb + i) * kJdsRows;
+                    int c[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const bool a = u < lo;
+                        const int idx = (u < Lo ? doff[u] : 0) + lane;
+                        vo[u] = a ? q.val[idx] : 0.0;
+                        c[u] = a ? (wide ? ((const int32_t*)q.col)[idx] : (int)((const int16_t*)q.col)[idx]) : rl;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) go[u] = rt[c[u]];
+                };
+                if (cnt > 0) load(0, vv, gv, xi, qi, len, L, kst);
+                for (int i = 0; i < cnt; ++i) {
+                    double vn[8], gn[8], xn = 0.0, qn = 0.0;
+                    int ln = 0, Ln = 0, kn = 0;
+                    if (i + 1 < cnt) load(i + 1, vn, gn, xn, qn, ln, Ln, kn);
+                    double acc = 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
+                    if (L > 8) {  // long rows: remaining diagonals of tile i, synchronously
+                        const JStage q = stage(kst);
+                        const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
+                        const bool wide = tile_c[kst].y > 2 * tile_e[kst].y;
+                        const double* rt = rg + (int64_t)(tb + i) * kJdsRows;
+                        for (int k = 8; k < L; ++k) {
+                            const bool a = k < len;
+                            const int idx = doff[k] + lane;
+                            if (a) {
+                                const int cc = wide ? ((const int32_t*)q.col)[idx] : (int)((const int16_t*)q.col)[idx];
+                                acc = fma(q.val[idx], rt[cc], acc);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[kst]);
+                    const int row = (tb + i) * kJdsRows + rl;
+                    if (row < it.n) {
+                        const double y = xi + acc;
+                        wout[row] = y;
+                        const double ru = xi * qi;
+                        v[0] += xi * xi;
+                        v[1] += y * xi;
+                        v[2] += ru * ru;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        vv[u] = vn[u];
+                        gv[u] = gn[u];
+                    }
+                    xi = xn;
+                    qi = qn;
+                    len = ln;
+                    L = Ln;
+                    kst = kn;
+                }
+            } else
             for (int i0 = 0; i0 < cnt; i0 += JP) {
                 int len[JP], L[JP];
                 bool wide[JP];
@@ -1096,7 +1199,320 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             }
         }
     }
+    if (g_gt_prof && threadIdx.x == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        g_gt_times[2 * blockIdx.x] = t_start;
+        g_gt_times[2 * blockIdx.x + 1] = t1;
+    }
+    const int it_prof = S->iters;
+    if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax) {
+        const unsigned long long t = gtime();
+        atomicMax(&g_loop_ts2[4 * it_prof], t_start);
+        atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
+        atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
+    }
     cg_tail<false, false, JNT>(v, act, S, B, part, gcnt, h);
+    if (g_loop_prof && act) {
+        __syncthreads();
+        if (threadIdx.x == 0) loop_stamp(1, it_prof, t_start);
+    }
+}
+
+// ------------------------------------------------------------------ persistent TMA solver
+// Large systems (C5): the WHOLE CG loop in one cooperative launch, one CTA per SM, each owning
+// the same contiguous range of kJdsRows-row tiles every iteration (rows R0..R1). The matrix part
+// of a tile (values, columns, lengths + diagonal offsets, q = D^1/2) does not change between
+// iterations, so the producer warp streams it through the JNS-stage TMA ring CONTINUOUSLY --
+// across the update phase and the grid barriers -- while the JCW consumer warps run
+//   S: w = r + A^_off r over the tiles (r of the own rows from L2, neighbours gathered), dots
+//   -- grid barrier fused with the reduction (fixed-order sum: identical scalars everywhere) --
+//   U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s   (own rows)
+//   -- grid barrier (r published) --
+// Consumers synchronise among themselves with named barrier 1 (the producer never joins).
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" ::"n"(JCW * 32) : "memory"); }
+
+// consumer-only grid barrier on the per-CTA epoch slots of it.part (optional partials)
+__device__ __forceinline__ void cgrid_sync(const RItem& it, int rank, unsigned long long epoch, const double4* t) {
+    cons_bar();
+    if (threadIdx.x == 0) {
+        double* P = it.part + 4 * rank;
+        if (t) {
+            P[0] = t->x;
+            P[1] = t->y;
+            P[2] = t->z;
+        }
+        __threadfence();
+        *(volatile unsigned long long*)(P + 3) = epoch;
+    }
+    for (int k = threadIdx.x; k < it.ncta; k += JCW * 32) {
+        volatile unsigned long long* E = (volatile unsigned long long*)(it.part + 4 * k + 3);
+        while (*E < epoch) {
+        }
+    }
+    __threadfence();
+    cons_bar();
+}
+
+__device__ __forceinline__ double4 cons_sum3(double4 v, double* sh /* [JCW][4] */) {
+    v.x = warp_sum_d(v.x);
+    v.y = warp_sum_d(v.y);
+    v.z = warp_sum_d(v.z);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    cons_bar();
+    if (lane == 0) {
+        sh[4 * wid] = v.x;
+        sh[4 * wid + 1] = v.y;
+        sh[4 * wid + 2] = v.z;
+    }
+    cons_bar();
+    double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < JCW; ++w) {
+        t.x += sh[4 * w];
+        t.y += sh[4 * w + 1];
+        t.z += sh[4 * w + 2];
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(JNT, 1) k_pcgt(const RItem* __restrict__ items) {
+    extern __shared__ __align__(128) unsigned char jsm[];
+    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
+    __shared__ int2 tile_e[JNS], tile_c[JNS];
+    __shared__ double sh[4 * JCW];
+    __shared__ volatile int done_flag, pdone;
+    __shared__ volatile int issued;
+    const RItem& it = items[0];
+    CgState* S = it.st;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = blockIdx.x;
+    const int tb = it.jpart[rank], te = it.jpart[rank + 1], nt = te - tb;
+    const int n = it.n;
+    const int R0 = min(n, tb * kJdsRows), R1 = min(n, te * kJdsRows);
+    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
+    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 8 * kJdsRows + 127) & ~(size_t)127;
+    auto stage = [&](int k) {
+        unsigned char* b = jsm + (size_t)k * stage_bytes;
+        JStage q;
+        q.s = (double*)b;  // q = D^1/2
+        q.r = nullptr;
+        q.val = q.s + kJdsRows;
+        q.col = (uint8_t*)(q.val + maxe);
+        q.meta = q.col + 4 * (size_t)maxe;
+        return q;
+    };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < JNS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], JCW);
+        }
+        mbar_fence_init();
+        done_flag = 0;
+        pdone = 0;
+        issued = 0;
+    }
+    __syncthreads();
+    if (warp == JCW) {
+        // ---- producer: the CTA's tiles, cyclically, until the consumers are done
+        if (lane == 0 && nt > 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int i = 0;; ++i) {
+                const int k = i % JNS;
+                if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);  // the drain below releases it
+                if (done_flag) break;
+                const int t = tb + i % nt;
+                const JStage q = stage(k);
+                const int e0 = it.jeb[t], ne = it.jeb[t + 1] - e0;
+                const int c0 = it.jcb[t], nc = it.jcb[t + 1] - c0;
+                tile_e[k] = make_int2(e0, ne);
+                tile_c[k] = make_int2(c0, nc);
+                mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 8u * kJdsRows);
+                bulk_g2s_hint(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k], pol);
+                bulk_g2s_hint(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k], pol);
+                if (ne) {
+                    bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
+                    bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
+                }
+                issued = i + 1;
+            }
+            __threadfence_block();
+            pdone = 1;
+        }
+        return;
+    }
+    // ---- consumers
+    const int tid = threadIdx.x;
+    double* __restrict__ r = it.r;
+    double* __restrict__ w = it.w;
+    double* __restrict__ p = it.p;
+    double* __restrict__ sv = it.sv;
+    double* __restrict__ x = it.x;
+    const double tol2 = S->tol2, bn2 = S->bn2;
+    const int max_iter = S->max_iter;
+    int iters = S->iters, status = FEMI_OK;
+    unsigned long long epoch = 0;
+    int cons = 0;  // stages consumed (ring position)
+    const int rl = 32 * warp + lane;
+    auto spmv = [&]() -> double4 {
+        double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int j = 0; j < nt; ++j, ++cons) {
+            const int k = cons % JNS;
+            mbar_wait(&full[k], (cons / JNS) & 1);
+            const JStage q = stage(k);
+            const int t = tb + j;
+            const int row = t * kJdsRows + rl;
+            const int len = q.meta[rl];
+            const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
+            const double* rt = r + (int64_t)t * kJdsRows;
+            const double xi = row < n ? rt[rl] : 0.0;
+            const double qi = q.s[rl];
+            const int L = __shfl_sync(0xffffffffu, len, 0);
+            const bool wide = tile_c[k].y > 2 * tile_e[k].y;
+            const int16_t* c16 = (const int16_t*)q.col;
+            const int32_t* c32 = (const int32_t*)q.col;
+            double acc = 0.0;
+            for (int k0 = 0; k0 < L; k0 += 8) {
+                double vv[8], gv[8];
+                int c[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const bool a = k0 + u < len;
+                    const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
+                    vv[u] = a ? q.val[idx] : 0.0;
+                    c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) gv[u] = rt[c[u]];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[k]);
+            if (row < n) {
+                const double y = xi + acc;
+                w[row] = y;
+                const double ru = xi * qi;
+                loc.x += xi * xi;
+                loc.y += y * xi;
+                loc.z += ru * ru;
+            }
+        }
+        return loc;
+    };
+    auto reduce = [&](double4 loc) -> double4 {
+        const double4 t = cons_sum3(loc, sh);
+        ++epoch;
+        cgrid_sync(it, rank, epoch, &t);
+        double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int k = tid; k < it.ncta; k += JCW * 32) {
+            const double* P = it.part + 4 * k;
+            a.x += __ldcg(P);
+            a.y += __ldcg(P + 1);
+            a.z += __ldcg(P + 2);
+        }
+        return cons_sum3(a, sh);
+    };
+    double4 tot = reduce(spmv());
+    double gam = tot.x, del = tot.y, rho = tot.z;
+    double alpha = 0.0, beta = 0.0;
+    bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho) && iters < max_iter;
+    if (!isfinite(gam) || !isfinite(bn2)) {
+        status = FEMI_E_NONFINITE;
+        run = false;
+    }
+    if (run) {
+        if (!(del > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            run = false;
+        } else {
+            alpha = gam / del;
+        }
+    }
+    const bool prof = g_loop_prof && rank == 0 && tid == 0;
+    unsigned long long tp = prof ? gtime() : 0ull;
+    auto mark = [&](int k) {
+        if (prof) {
+            const unsigned long long t = gtime();
+            g_loop_ts[k] += t - tp;
+            tp = t;
+        }
+    };
+    constexpr int UB = 4;  // rows per thread with their loads in flight together
+    while (run) {
+        // U: own rows (row i handled by the thread that wrote w[i] in S: same mapping)
+        for (int b0 = R0 + tid; b0 < R1; b0 += UB * JCW * 32) {
+            double rv[UB], wv[UB], pv[UB], sv0[UB], xv[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int i = b0 + u * JCW * 32;
+                if (i < R1) {
+                    rv[u] = r[i];
+                    wv[u] = w[i];
+                    pv[u] = p[i];
+                    sv0[u] = sv[i];
+                    xv[u] = x[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int i = b0 + u * JCW * 32;
+                if (i < R1) {
+                    const double pi = fma(beta, pv[u], rv[u]), si = fma(beta, sv0[u], wv[u]);
+                    p[i] = pi;
+                    sv[i] = si;
+                    x[i] = fma(alpha, pi, xv[u]);
+                    r[i] = fma(-alpha, si, rv[u]);
+                }
+            }
+        }
+        ++iters;
+        mark(0);
+        ++epoch;
+        cgrid_sync(it, rank, epoch, nullptr);  // r published
+        mark(1);
+        const double4 lsp = spmv();
+        mark(2);
+        tot = reduce(lsp);
+        mark(3);
+        const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
+        if (!isfinite(gam2) || !isfinite(del2)) {
+            status = FEMI_E_NONFINITE;
+            break;
+        }
+        if (rho2 <= tol2) break;
+        if (iters >= max_iter) {
+            status = FEMI_E_NOT_CONVERGED;
+            break;
+        }
+        beta = gam2 / gam;
+        const double den = del2 - beta * gam2 / alpha;
+        if (!(den > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            break;
+        }
+        alpha = gam2 / den;
+        gam = gam2;
+    }
+    if (rank == 0 && tid == 0) {
+        S->iters = iters;
+        S->status = status;
+    }
+    // drain the ring: consume every stage the producer issued, then let it stop
+    if (tid == 0) done_flag = 1;
+    cons_bar();
+    for (;;) {
+        const int iss = issued;
+        if (cons < iss) {
+            const int k = cons % JNS;
+            mbar_wait(&full[k], (cons / JNS) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[k]);
+            ++cons;
+        } else if (pdone && cons >= issued) {
+            break;
+        }
+    }
 }
 
 // rec[cur] = {r, 0, 0, 0} from the plain residual (start and restart of the recurrence)
@@ -1125,6 +1541,7 @@ struct GraphCache {
     int gs_blocks = 0, gx = 0, gp_blocks = 0;
     int gt_blocks = 0;
     unsigned gt_smem = 0;  // > 0: the body's SpMV is the TMA-streamed k_gt
+    unsigned pt_smem = 0;  // dynamic shared memory of the persistent k_pcgt
 };
 
 struct Workspace {
@@ -1136,7 +1553,8 @@ struct Workspace {
 };
 
 int g_smem_optin = -1;
-int g_fused = -1;  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
+int g_fused = -1;
+int g_persist = -1;  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
@@ -1216,7 +1634,19 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         prev = nd;
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         cudaGraphNode_t u, sn;
-        if (g_fused) {
+        if (!g_fused && C.gt_smem) {
+            // kUnroll iterations per body: the WHILE re-evaluation costs ~6 us, an iteration ~35;
+            // kernels after convergence return at once (S->active == 0)
+            cudaGraphNode_t prevb = nullptr;
+            for (int k = 0; k < kUnroll; ++k) {
+                if ((s = add_kernel(body, prevb ? &prevb : nullptr, (void*)k_gu,
+                                    dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT), a_items, &u)))
+                    return s;
+                if ((s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem)))
+                    return s;
+                prevb = sn;
+            }
+        } else if (g_fused) {
             if ((s = add_kernel(body, nullptr, (void*)k_gp<false>, dim3(C.gp_blocks), dim3(GNT), a_gs, &sn)))
                 return s;
         } else {
@@ -1238,6 +1668,83 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     return FEMI_OK;
 }
 
+// Persistent TMA path: prologue kernels, ONE cooperative k_pcgt for the whole CG loop, epilogue.
+femi_status persist_solve(femi_system_s* S, GraphCache* C, RItem it, const femi_cg_opts& o, int32_t* iters,
+                          double* relres, cudaStream_t st, int64_t* total_iters) {
+    it.part = C->d_part;  // [gt_blocks][4] barrier/partial slots
+    it.ncta = C->gt_blocks;
+    FEMI_CUDA(cudaMemcpyAsync(C->d_items, &it, sizeof(RItem), cudaMemcpyHostToDevice, st));
+    RItem* di = C->d_items;
+    const dim3 gk(C->gx, 1), bk(KNT);
+    k_reset_items<<<1, 32, 0, st>>>(1, di);
+    k_minmax<<<296, 256, 0, st>>>(1, di);
+    k_rhs<<<gk, bk, 0, st>>>(di);
+    k_init_x<<<gk, bk, 0, st>>>(di);
+    k_zero_ps<<<gk, bk, 0, st>>>(di);
+    k_init_r<<<gk, bk, 0, st>>>(di, C->d_cnt);
+    count_launches(6);
+    CgState hs;
+    for (int restarts = 0;; ++restarts) {
+        if (restarts) {
+            k_zero_ps<<<gk, bk, 0, st>>>(di);
+            count_launches(1);
+        }
+        FEMI_CUDA(cudaMemsetAsync(C->d_part, 0, sizeof(double) * 4 * C->gt_blocks, st));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(C->gt_blocks);
+        cfg.blockDim = dim3(JNT);
+        cfg.dynamicSmemBytes = C->pt_smem;
+        cfg.stream = st;
+        attr[0].id = cudaLaunchAttributeCooperative;  // spin barriers: all CTAs co-resident
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* args[1] = {(void*)&di};
+        static const bool loop_prof = std::getenv("FEMI_LOOP_PROF") != nullptr;
+        if (loop_prof) {
+            unsigned long long z[4] = {0, 0, 0, 0};
+            const int on = 1;
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        }
+        const cudaError_t e = cudaLaunchKernelExC(&cfg, (void*)k_pcgt, args);
+        if (e != cudaSuccess) return cuda_fail(e, "k_pcgt launch");
+        if (loop_prof) {
+            unsigned long long z[4];
+            const int off = 0;
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+            FEMI_CUDA(cudaMemcpyFromSymbolAsync(z, g_loop_ts, sizeof(z), 0, cudaMemcpyDeviceToHost, st));
+            CgState h2;
+            FEMI_CUDA(cudaMemcpyAsync(&h2, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+            FEMI_CUDA(cudaStreamSynchronize(st));
+            const double ni = std::max(1, h2.iters);
+            std::fprintf(stderr, "[femi persist] %d iterations, per iteration us: U %.2f  barrier %.2f  S %.2f  reduce %.2f\n",
+                         h2.iters, z[0] / ni / 1e3, z[1] / ni / 1e3, z[2] / ni / 1e3, z[3] / ni / 1e3);
+        }
+        k_finalize<<<gk, bk, 0, st>>>(di);
+        k_true_res<<<gk, bk, 0, st>>>(di, C->d_cnt + 1);
+        count_launches(3);
+        FEMI_CUDA(cudaGetLastError());
+        FEMI_CUDA(cudaMemcpyAsync(&hs, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        const bool fail = hs.bn2 > 0.0 && !(hs.res2 <= hs.tol2);
+        if (!(hs.status == FEMI_OK && hs.iters > 0 && hs.iters < hs.max_iter && fail) || restarts >= 8) break;
+        // k_true_res left r = s * r_true and x^ is current: the loop restarts from there
+    }
+    k_copy_g<<<296, 256, 0, st>>>(di);
+    count_launches(1);
+    FEMI_CUDA(cudaGetLastError());
+    const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
+    if (iters) *iters = hs.iters;
+    if (relres) *relres = rel;
+    if (total_iters) *total_iters = hs.iters;
+    femi_status sb = (femi_status)hs.status;
+    if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
+    if (sb != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)sb) + ")");
+    return sb;
+}
+
 femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, double* u_vert,
                         const femi_cg_opts& o, int32_t* iters, double* relres, cudaStream_t st,
                         int64_t* total_iters) {
@@ -1246,6 +1753,10 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     if (g_fused < 0) {
         const char* fz = std::getenv("FEMI_PCG_FUSED");  // measured: fused 69 us vs 17 + 43 us (C5)
         g_fused = (fz && fz[0] == '1') ? 1 : 0;
+        // measured at C5: graph WHILE loop (k_gu + k_gt, 4 per body) 42 us/iteration, persistent
+        // k_pcgt 49 us/iteration -> the graph is the default; FEMI_PCG_PERSIST=1 selects k_pcgt
+        const char* pg = std::getenv("FEMI_PCG_PERSIST");
+        g_persist = (pg && pg[0] == '1') ? 1 : 0;
     }
     if (!C) {
         C = new GraphCache();
@@ -1274,15 +1785,36 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 std::fprintf(stderr, "[femi] k_gt: stage %zu B x %d, optin %d\n", stage_bytes, JNS, optin);
             if (JNS * stage_bytes + 1024 <= (size_t)optin) {
                 C->gt_smem = (unsigned)(JNS * stage_bytes);
+                C->pt_smem = (unsigned)(JNS * (((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 8 * kJdsRows + 127) &
+                                               ~(size_t)127));
+                FEMI_CUDA(cudaFuncSetAttribute(k_pcgt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->pt_smem));
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
-                for (const void* fn : {(const void*)k_gt<1, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
-                                       (const void*)k_gt<1, 2>})
+                for (const void* fn : {(const void*)k_gt<0, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
+                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
             }
         }
+        // tiles -> k_gt CTAs: contiguous ranges of equal streamed + gathered bytes
+        std::vector<int32_t> jpart;
+        if (C->gt_smem) {
+            const int nt = S->jds_ntile;
+            std::vector<int32_t> eb(nt + 1);
+            FEMI_CUDA(cudaMemcpy(eb.data(), S->jds_eb, sizeof(int32_t) * (nt + 1), cudaMemcpyDeviceToHost));
+            std::vector<double> cum(nt + 1, 0.0);
+            double wa = 0.0;  // bytes-per-entry weight of the balance (0: equal tile counts)
+            if (const char* e = std::getenv("FEMI_JPART_W")) wa = std::atof(e);
+            for (int t = 0; t < nt; ++t) cum[t + 1] = cum[t] + wa * (eb[t + 1] - eb[t]) + 24.0 * kJdsRows;
+            jpart.resize(C->gt_blocks + 1);
+            for (int b = 0, t = 0; b <= C->gt_blocks; ++b) {
+                const double target = cum[nt] * b / C->gt_blocks;
+                while (t < nt && cum[t] < target) ++t;
+                jpart[b] = t;
+            }
+            jpart[C->gt_blocks] = nt;
+        }
         const int pb = std::max(std::max(C->gs_blocks, C->gp_blocks), C->gt_blocks);
         const size_t rb = al(sizeof(Rec) * (n + 1));
-        const size_t bytes = al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
+        const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
                              al(sizeof(double) * 4 * pb) + al(sizeof(double) * KGRID) + 6 * vb + 2 * rb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
         char* cur = (char*)C->ws;
@@ -1292,6 +1824,9 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             return p;
         };
         C->d_items = (RItem*)take(sizeof(RItem));
+        int32_t* d_jpart = (int32_t*)take(sizeof(int32_t) * (jpart.size() + 1));
+        if (!jpart.empty())
+            FEMI_CUDA(cudaMemcpy(d_jpart, jpart.data(), sizeof(int32_t) * jpart.size(), cudaMemcpyHostToDevice));
         C->d_state = (CgState*)take(sizeof(CgState));
         C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
         C->d_part = (double*)take(sizeof(double) * 4 * pb);
@@ -1315,6 +1850,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.jkmax = S->jds_kmax;
         it.jmbytes = S->jds_meta_bytes;
         it.jpol = 1;
+        it.jpart = d_jpart;
         if (const char* pe = std::getenv("FEMI_JDS_POLICY")) it.jpol = std::atoi(pe);
         it.inv = S->sell_inv;
         it.len = S->sell_len;
@@ -1350,8 +1886,66 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     it.x0mode = (g == nullptr && o.x0 == 1) ? 0 : o.x0;
     it.rtol = o.rtol;
     it.max_iter = o.max_iter;
+    if (C->gt_smem && g_persist)
+        return persist_solve(S, C, it, o, iters, relres, st, total_iters);
     FEMI_CUDA(cudaMemcpyAsync(C->d_items, &it, sizeof(RItem), cudaMemcpyHostToDevice, st));
+    static const bool loop_prof = std::getenv("FEMI_LOOP_PROF") != nullptr;
+    if (loop_prof) {
+        std::vector<unsigned long long> init(4 * kLoopProfMax);
+        for (int k = 0; k < kLoopProfMax; ++k) {
+            init[4 * k] = init[4 * k + 2] = ~0ull;
+            init[4 * k + 1] = init[4 * k + 3] = 0ull;
+        }
+        const int on = 1;
+        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts, init.data(), sizeof(unsigned long long) * init.size(), 0,
+                                          cudaMemcpyHostToDevice, st));
+        for (int k = 0; k < kLoopProfMax; ++k) {
+            init[4 * k] = 0ull;
+            init[4 * k + 1] = ~0ull;
+            init[4 * k + 2] = 0ull;
+        }
+        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts2, init.data(), sizeof(unsigned long long) * init.size(), 0,
+                                          cudaMemcpyHostToDevice, st));
+        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    }
     FEMI_CUDA(cudaGraphLaunch(C->main, st));
+    if (loop_prof) {
+        const int off = 0;
+        std::vector<unsigned long long> ts(4 * kLoopProfMax);
+        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        FEMI_CUDA(cudaMemcpyFromSymbolAsync(ts.data(), g_loop_ts, sizeof(unsigned long long) * ts.size(), 0,
+                                            cudaMemcpyDeviceToHost, st));
+        std::vector<unsigned long long> t2(4 * kLoopProfMax);
+        FEMI_CUDA(cudaMemcpyFromSymbolAsync(t2.data(), g_loop_ts2, sizeof(unsigned long long) * t2.size(), 0,
+                                            cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        double su = 0, sg = 0, g1 = 0, g2 = 0, st_skew = 0, end0 = 0, end1 = 0;
+        int cnt = 0;
+        for (int k = 1; k + 1 < kLoopProfMax; ++k) {
+            const unsigned long long* a = &ts[4 * k];
+            const unsigned long long* nx = &ts[4 * (k + 1)];
+            if (a[1] == 0 || a[3] == 0 || nx[1] == 0) break;
+            su += (double)(a[1] - a[0]);
+            sg += (double)(a[3] - a[2]);
+            g1 += (double)a[2] - (double)a[1];
+            g2 += (double)nx[0] - (double)a[3];
+            st_skew += (double)t2[4 * k] - (double)a[2];
+            end0 += (double)t2[4 * k + 1] - (double)a[2];
+            end1 += (double)t2[4 * k + 2] - (double)a[2];
+            ++cnt;
+        }
+        if (cnt)
+            std::fprintf(stderr,
+                         "[femi loop] %d iterations: k_gu span %.2f us, gap %.2f, k_gt span %.2f us (to tail end), gap "
+                         "%.2f -> %.2f us/iteration\n",
+                         cnt, su / cnt / 1e3, g1 / cnt / 1e3, sg / cnt / 1e3, g2 / cnt / 1e3,
+                         (su + sg + g1 + g2) / cnt / 1e3);
+        if (cnt)
+            std::fprintf(stderr,
+                         "[femi loop] k_gt from first CTA start: last CTA start +%.2f us, first consumer end +%.2f, "
+                         "last consumer end +%.2f, kernel end +%.2f\n",
+                         st_skew / cnt / 1e3, end0 / cnt / 1e3, end1 / cnt / 1e3, sg / cnt / 1e3);
+    }
     count_launches(11);
     CgState hs;
     for (int restarts = 0;; ++restarts) {
@@ -1410,7 +2004,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         }
         float tt[4] = {0, 0, 0, 0};
         void (*const gts[4])(const RItem*, int, double*, unsigned*, cudaGraphConditionalHandle) = {
-            k_gt<1, 0>, k_gt<2, 0>, k_gt<1, 1>, k_gt<1, 2>};
+            k_gt<1, 0>, k_gt<0, 0>, k_gt<1, 1>, k_gt<1, 2>};
         if (C->gt_smem)
             for (int v = 0; v < 4; ++v)
                 for (int k = 0; k < reps; ++k) {
@@ -1425,8 +2019,58 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                     cudaEventElapsedTime(&a, e0, e1);
                     if (k > 1) tt[v] += a;
                 }
+        if (C->gt_smem) {  // back-to-back k_gt launches (steady state without the first-launch cost)
+            act.par = 0;
+            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
+            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
+            cudaEventRecord(e0, st);
+            for (int k = 0; k < 8; ++k)
+                k_gt<1, 0><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
+            cudaEventRecord(e1, st);
+            for (int k = 0; k < 8; ++k) k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
+            cudaEventRecord(e2, st);
+            cudaEventSynchronize(e2);
+            float a, b;
+            cudaEventElapsedTime(&a, e0, e1);
+            cudaEventElapsedTime(&b, e1, e2);
+            std::fprintf(stderr, "[femi kbench] back-to-back: k_gt %.2f us, k_gu %.2f us per launch\n", 1e3 * a / 8,
+                         1e3 * b / 8);
+        }
+        if (C->gt_smem) {  // per-CTA busy time of one k_gt<1,0> launch
+            int on = 1;
+            cudaMemcpyToSymbolAsync(g_gt_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+            act.par = 0;
+            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
+            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
+            k_gt<1, 0><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
+            on = 0;
+            cudaMemcpyToSymbolAsync(g_gt_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+            std::vector<unsigned long long> tm(2 * C->gt_blocks);
+            cudaMemcpyFromSymbolAsync(tm.data(), g_gt_times, sizeof(unsigned long long) * tm.size(), 0,
+                                      cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            unsigned long long t0 = ~0ull, t1 = 0;
+            double mn = 1e30, mx = 0, sm = 0;
+            for (int b = 0; b < C->gt_blocks; ++b) {
+                t0 = std::min(t0, tm[2 * b]);
+                t1 = std::max(t1, tm[2 * b + 1]);
+                const double d = (double)(tm[2 * b + 1] - tm[2 * b]);
+                mn = std::min(mn, d);
+                mx = std::max(mx, d);
+                sm += d;
+            }
+            unsigned long long s0 = 0, s1 = 0;
+            for (int b = 0; b < C->gt_blocks; ++b) {
+                s0 = std::max(s0, tm[2 * b] - t0);
+                s1 = std::max(s1, t1 - tm[2 * b + 1]);
+            }
+            std::fprintf(stderr,
+                         "[femi kbench] k_gt per-CTA busy us: min %.2f mean %.2f max %.2f; span %.2f; latest start "
+                         "+%.2f; earliest end -%.2f\n",
+                         mn / 1e3, sm / C->gt_blocks / 1e3, mx / 1e3, (t1 - t0) / 1e3, s0 / 1e3, s1 / 1e3);
+        }
         std::fprintf(stderr,
-                     "[femi kbench] k_gt (TMA, grid %d, smem %u): JP1 %.2f us  JP2 %.2f us  smem-gather %.2f us  "
+                     "[femi kbench] k_gt (TMA, grid %d, smem %u): JP1 %.2f us  pipelined %.2f us  smem-gather %.2f us  "
                      "no-gather %.2f us\n",
                      C->gt_blocks, C->gt_smem, 1e3 * tt[0] / (reps - 2), 1e3 * tt[1] / (reps - 2),
                      1e3 * tt[2] / (reps - 2), 1e3 * tt[3] / (reps - 2));

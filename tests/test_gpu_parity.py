@@ -55,20 +55,16 @@ def check_inpaint(W, H, f, mk, un, rtol=1e-10):
     mse = R["sse"].item() / (W * H)
     assert abs(mse - O["mse"]) <= MSE_RTOL * max(O["mse"], 1e-300) or (O["mse"] == 0 and mse == 0)
     te = R["tri_err"].cpu().numpy()
-    # tri_err: same pixels, GPU solution within tolerance -> compare against the oracle's
-    # raster of the GPU's own vertex values (isolates the reduction from the solve)
+    # tri_err / best: compared against the oracle's raster of the GPU's own vertex values
+    # (isolates S3/S4 from the solve): both sum e in pixel order and take the first strict
+    # maximum, so they are bit-identical
     Og = S.raster(u_vert, f)
-    np.testing.assert_allclose(te, Og["tri_err"], rtol=1e-9, atol=1e-9 * max(1.0, Og["tri_err"].max()))
+    np.testing.assert_array_equal(te, Og["tri_err"])
+    np.testing.assert_array_equal(R["best"].cpu().numpy(), Og["best"])
     # the raster itself is exact: same vertex values -> bit-identical pixel values and errors
     # (S3's barycentric form in IEEE fp64, one rounding per operation on both sides)
     np.testing.assert_array_equal(u_px, Og["u_px"])
     np.testing.assert_array_equal(R["e_px"].cpu().numpy(), Og["e_px"])
-    best = R["best"].cpu().numpy()
-    mism = np.nonzero(best != Og["best"])[0]
-    for t in mism:  # only genuine near-ties may differ
-        e = Og["e_px"]
-        assert best[t] >= 0 and Og["best"][t] >= 0
-        assert abs(e[best[t]] - e[Og["best"][t]]) <= 1e-9 * max(1.0, e[Og["best"][t]])
     return R, O
 
 
