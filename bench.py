@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tonal", action="store_true", help="C5: skip the 20-iteration tonal tail")
+    ap.add_argument("--shard", action="store_true",
+                    help="C2 under torchrun: split the 32 masks across ranks (strong scaling) instead of replicas")
     return ap.parse_args()
 
 
@@ -304,10 +306,8 @@ def run_ours(args):
     total_ms = e_start.elapsed_time(e_end)
     solve_ms = [e[0].elapsed_time(e[1]) for e in evs]
     raster_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    t_max = torch.tensor([total_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    total_ms = float(t_max.item())
+    from paper_2105_01586_b200 import multi
+    total_ms = multi.max_over_ranks(total_ms, device=dev)  # device time of the job = max over ranks
     ms_per_step = total_ms / args.steps
     value = world * Npx * args.steps / (total_ms * 1e-3) / 1e6
     mse = sse.item() / Npx
@@ -343,11 +343,9 @@ def run_ours(args):
             s_e2e = step_e2e()
         b.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b)], device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = multi.max_over_ranks(a.elapsed_time(b), device=dev)
         assert abs(s_e2e / Npx - mse) <= 1e-9 * mse
-        e2e = {"value": world * Npx * args.steps / (float(t.item()) * 1e-3) / 1e6, "unit": "Mpx/s",
+        e2e = {"value": world * Npx * args.steps / (t_e2e * 1e-3) / 1e6, "unit": "Mpx/s",
                "h2d_bytes_per_step": int(8 * Npx + 8 * sysm.m), "d2h_bytes_per_step": 8}
 
     # ---- roofline of the PCG loop (SURVEY §8(d) algorithmic bytes)
@@ -450,9 +448,12 @@ def run_workload(args):
     detail, setup = {}, {}
     launches0 = None
 
+    from paper_2105_01586_b200 import multi
     if args.config == 2:
         t0 = time.time()
-        meshes = [femi.Mesh(W, H, c["masks"][b], c["unknowns"][b]) for b in range(len(c["masks"]))]
+        nb = len(c["masks"])
+        mine = multi.shard(nb, rank, world) if (args.shard and world > 1) else range(nb)
+        meshes = [femi.Mesh(W, H, c["masks"][b], c["unknowns"][b]) for b in mine]
         setup["mesh_build_s"] = time.time() - t0
         t0 = time.time()
         systems = [femi.System(M) for M in meshes]
@@ -487,8 +488,12 @@ def run_workload(args):
         units = B * Npx
         metric, unit, hib = "FEM inpainting Mpixels/s (solve+raster+error)", "Mpx/s", True
         value_one = units / (ms * 1e-3) / 1e6
+        mse_all = multi.gather_scalars(np.array([float(x.item()) / Npx for x in sse]), nb if args.shard else B,
+                                       device=dev) if (args.shard and world > 1) else \
+            np.array([float(x.item()) / Npx for x in sse])
         detail.update(solves_per_s=B / (ms * 1e-3), cg_iters_mean=float(np.mean(it)), cg_iters_max=int(np.max(it)),
-                      mse=[float(x.item()) / Npx for x in sse[:4]])
+                      mse_first4=[float(v) for v in mse_all[:4]], batch_per_rank=B,
+                      sharded=bool(args.shard and world > 1))
         n_u = sum(S.n_u for S in systems) / B
         nnz = sum(S.info["nnz_uu"] for S in systems) / B
         bytes_iter = B * (12 * nnz + 4 * (n_u + 1) + 80 * n_u)
@@ -583,11 +588,9 @@ def run_workload(args):
         work = "C4: 1024x1024 fp64 synthetic, fixed 3% random mask, tonal optimisation: CGLS on B^T B g = B^T f, " \
                "inner Jacobi-PCG to rtol 1e-12, until the relative gradient < 1e-8"
     launches = femi.kernel_launches() - launches0
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = (world * units / (ms * 1e-3) / 1e6) if hib else ms * 1e-3
+    ms = multi.max_over_ranks(ms, device=dev)  # device time of the job = max over ranks
+    sharded = args.config == 2 and args.shard and world > 1
+    value = ((1 if sharded else world) * (nb * Npx if sharded else units) / (ms * 1e-3) / 1e6) if hib else ms * 1e-3
     solve_s = ms * 1e-3
     achieved = bytes_iter * iters_roof / solve_s / 1e9
     pk = peaks()
@@ -595,9 +598,11 @@ def run_workload(args):
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": hib, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": hib,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": work, "W": W, "H": H, "parallelism": f"replicas{world}",
+            "config": {"workload": work, "W": W, "H": H,
+                       "parallelism": f"batch-shard{world}" if sharded else f"replicas{world}",
                        "l2_flush": "L2-resident working set (latency-bound config; no flush)"},
             "roofline": {"bound": "hbm", "kernel": "PCG iterations of the workload (L2-resident: latency-bound)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
