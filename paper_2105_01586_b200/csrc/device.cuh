@@ -183,6 +183,15 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
                        femi_tonal_report* rep, cudaStream_t st);
 
 // device helpers
+// release/acquire at gpu scope: the last-arriver pattern needs only these, not the
+// sequentially consistent fence (__threadfence = MEMBAR.SC.GPU, several microseconds under load)
+__device__ __forceinline__ unsigned atom_add_release_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -97,6 +97,25 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
+__device__ int g_gt_prof;                     // kbench: per-CTA start/end times of k_gt
+__device__ unsigned long long g_gt_times[2 * 1024];
+// FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
+constexpr int kLoopProfMax = 4096;
+__device__ int g_loop_prof;
+__device__ unsigned long long g_loop_ts[4 * kLoopProfMax];
+__device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];  // k_gt: max start, min/max consumer end
+__device__ unsigned long long g_tail_ts[4 * kLoopProfMax];   // cg_tail stamps (see cg_tail)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void loop_stamp(int kern, int iter, unsigned long long t0) {
+    if (iter < 0 || iter >= kLoopProfMax) return;
+    atomicMin(&g_loop_ts[4 * iter + 2 * kern], t0);
+    atomicMax(&g_loop_ts[4 * iter + 2 * kern + 1], gtime());
+}
+
 // ------------------------------------------------------------------ ordinary kernels
 __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -597,24 +616,6 @@ __global__ void k_zero_ps(const RItem* __restrict__ items) {
     }
 }
 
-__device__ int g_gt_prof;                     // kbench: per-CTA start/end times of k_gt
-__device__ unsigned long long g_gt_times[2 * 1024];
-// FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
-constexpr int kLoopProfMax = 4096;
-__device__ int g_loop_prof;
-__device__ unsigned long long g_loop_ts[4 * kLoopProfMax];
-__device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];  // k_gt: max start, min/max consumer end
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void loop_stamp(int kern, int iter, unsigned long long t0) {
-    if (iter < 0 || iter >= kLoopProfMax) return;
-    atomicMin(&g_loop_ts[4 * iter + 2 * kern], t0);
-    atomicMax(&g_loop_ts[4 * iter + 2 * kern + 1], gtime());
-}
-
 // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
 __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
@@ -665,7 +666,21 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
 // swaps the double-buffered vectors.
 template <bool FIRST, bool FLIP, int NT = GNT>
 __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, int B, double* __restrict__ part,
-                                        unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+                                        unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int prof_it = -1) {
+    const bool tp = prof_it >= 0 && prof_it < kLoopProfMax && g_loop_prof;
+    // the recurrence state the last CTA needs, loaded up front (off the tail's critical path);
+    // it only changes in the last CTA of the previous launch
+    double s_bn2 = 0.0, s_tol2 = 0.0, s_rr = 0.0, s_alpha = 0.0;
+    int s_iters = 0, s_max = 0, s_par = 0;
+    if (threadIdx.x == 0) {
+        s_bn2 = S->bn2;
+        s_tol2 = S->tol2;
+        s_rr = S->rr;
+        s_alpha = S->alpha;
+        s_iters = S->iters;
+        s_max = S->max_iter;
+        s_par = S->par;
+    }
     __shared__ double shm[4 * (NT / 32)];
     __shared__ int last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -677,18 +692,23 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         for (int q = 0; q < 3; ++q) shm[4 * wid + q] = v[q];
     __syncthreads();
     double* P = part + 4 * (size_t)gridDim.x * blockIdx.y;
-    if (threadIdx.x == 0) {
+    // the arrival is made by the first thread of the LAST warp: in k_gt that is the producer
+    // warp, which issued no global stores, so its release fence does not wait for the
+    // consumers' in-flight w stores (only P has to be visible to the last CTA; w is ordered
+    // by the kernel boundary)
+    constexpr int AT = NT - 32;
+    if (threadIdx.x == AT) {
         for (int q = 0; q < 3; ++q) {
             double t = 0.0;
             for (int w = 0; w < NT / 32; ++w) t += shm[4 * w + q];
             P[4 * blockIdx.x + q] = t;
         }
-        __threadfence();
-        last = atomicAdd(&S->cnt[0], 1u) == gridDim.x - 1;
+        last = atom_add_release_gpu(&S->cnt[0], 1u) == gridDim.x - 1;
+        if (tp) atomicMax(&g_tail_ts[4 * prof_it], gtime());  // A: CTA arrived
     }
     __syncthreads();
     if (!last) return;
-    __threadfence();
+    fence_acq_rel_gpu();
     double tot[3] = {0.0, 0.0, 0.0};
     for (unsigned b = threadIdx.x; b < gridDim.x; b += NT)
 #pragma unroll
@@ -701,6 +721,7 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         for (int q = 0; q < 3; ++q) shm[4 * wid + q] = tot[q];
     __syncthreads();
     if (threadIdx.x != 0) return;
+    if (tp) g_tail_ts[4 * prof_it + 1] = gtime();  // B: last CTA has the partials
     double gam2 = 0.0, del2 = 0.0, rho2 = 0.0;
     for (int w = 0; w < NT / 32; ++w) {
         gam2 += shm[4 * w];
@@ -711,8 +732,8 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     int active = 0;
     if (act) {
         if (FIRST) {
-            const bool fin = isfinite(gam2) && isfinite(S->bn2);
-            active = (S->bn2 > 0.0 && rho2 > S->tol2 && fin && S->iters < S->max_iter) ? 1 : 0;
+            const bool fin = isfinite(gam2) && isfinite(s_bn2);
+            active = (s_bn2 > 0.0 && rho2 > s_tol2 && fin && s_iters < s_max) ? 1 : 0;
             if (!fin) S->status = FEMI_E_NONFINITE;
             if (active && !(del2 > 0.0)) {
                 S->status = FEMI_E_NEG_CURVATURE;
@@ -724,17 +745,18 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
                 S->rr = gam2;
             }
         } else {
-            S->iters += 1;
-            if (FLIP) S->par ^= 1;
+            const int it1 = s_iters + 1;
+            S->iters = it1;
+            if (FLIP) S->par = s_par ^ 1;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 S->status = FEMI_E_NONFINITE;
-            } else if (rho2 <= S->tol2) {
+            } else if (rho2 <= s_tol2) {
                 // converged
-            } else if (S->iters >= S->max_iter) {
+            } else if (it1 >= s_max) {
                 S->status = FEMI_E_NOT_CONVERGED;
             } else {
-                const double beta = gam2 / S->rr;
-                const double den = del2 - beta * gam2 / S->alpha;
+                const double beta = gam2 / s_rr;
+                const double den = del2 - beta * gam2 / s_alpha;
                 if (!(den > 0.0)) {
                     S->status = FEMI_E_NEG_CURVATURE;
                 } else {
@@ -747,16 +769,20 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         }
         S->active = active;
     }
-    // all items reported? -> loop condition
-    __threadfence();
-    if (active) atomicAdd(gcnt + 1, 1u);
-    __threadfence();
-    if (atomicAdd(gcnt, 1u) == (unsigned)B - 1) {
-        __threadfence();
+    if (tp) g_tail_ts[4 * prof_it + 2] = gtime();  // C: scalars done
+    // all items reported? -> loop condition (one item: set it directly)
+    if (B == 1) {
+        if (h) cudaGraphSetConditional(h, active ? 1u : 0u);
+    } else {
+    if (active) atom_add_release_gpu(gcnt + 1, 1u);
+    if (atom_add_release_gpu(gcnt, 1u) == (unsigned)B - 1) {
+        fence_acq_rel_gpu();
         const unsigned any = atomicExch(gcnt + 1, 0u);
         gcnt[0] = 0;
         if (h) cudaGraphSetConditional(h, any ? 1u : 0u);  // h == 0: standalone launch (kbench)
     }
+    }
+    if (tp) g_tail_ts[4 * prof_it + 3] = gtime();  // D: condition set
 }
 
 // S: w = r + A^_off r (SELL, two slices per warp) and the dots; the last block updates the
@@ -1206,13 +1232,18 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         g_gt_times[2 * blockIdx.x + 1] = t1;
     }
     const int it_prof = S->iters;
-    if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax) {
-        const unsigned long long t = gtime();
-        atomicMax(&g_loop_ts2[4 * it_prof], t_start);
-        atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
-        atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
+    if (g_loop_prof && act && it_prof < kLoopProfMax) {
+        __syncthreads();  // profiling only: every warp of the CTA is done
+        if (threadIdx.x == 0) {
+            const unsigned long long t = gtime();
+            atomicMax(&g_loop_ts2[4 * it_prof], t_start);
+            atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
+            atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
+        }
     }
-    cg_tail<false, false, JNT>(v, act, S, B, part, gcnt, h);
+    cg_tail<false, false, JNT>(v, act, S, B, part, gcnt, h, act ? it_prof : -1);
+    if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax)
+        atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());  // this CTA left the tail
     if (g_loop_prof && act) {
         __syncthreads();
         if (threadIdx.x == 0) loop_stamp(1, it_prof, t_start);
@@ -1903,6 +1934,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             init[4 * k] = 0ull;
             init[4 * k + 1] = ~0ull;
             init[4 * k + 2] = 0ull;
+            init[4 * k + 3] = 0ull;
         }
         FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts2, init.data(), sizeof(unsigned long long) * init.size(), 0,
                                           cudaMemcpyHostToDevice, st));
@@ -1915,11 +1947,15 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
         FEMI_CUDA(cudaMemcpyFromSymbolAsync(ts.data(), g_loop_ts, sizeof(unsigned long long) * ts.size(), 0,
                                             cudaMemcpyDeviceToHost, st));
+        std::vector<unsigned long long> t3(4 * kLoopProfMax);
+        FEMI_CUDA(cudaMemcpyFromSymbolAsync(t3.data(), g_tail_ts, sizeof(unsigned long long) * t3.size(), 0,
+                                            cudaMemcpyDeviceToHost, st));
         std::vector<unsigned long long> t2(4 * kLoopProfMax);
         FEMI_CUDA(cudaMemcpyFromSymbolAsync(t2.data(), g_loop_ts2, sizeof(unsigned long long) * t2.size(), 0,
                                             cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
-        double su = 0, sg = 0, g1 = 0, g2 = 0, st_skew = 0, end0 = 0, end1 = 0;
+        double su = 0, sg = 0, g1 = 0, g2 = 0, st_skew = 0, end0 = 0, end1 = 0, end2 = 0, tA = 0, tB = 0, tC = 0,
+               tD = 0;
         int cnt = 0;
         for (int k = 1; k + 1 < kLoopProfMax; ++k) {
             const unsigned long long* a = &ts[4 * k];
@@ -1932,6 +1968,11 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             st_skew += (double)t2[4 * k] - (double)a[2];
             end0 += (double)t2[4 * k + 1] - (double)a[2];
             end1 += (double)t2[4 * k + 2] - (double)a[2];
+            end2 += (double)t2[4 * k + 3] - (double)a[2];
+            tA += (double)t3[4 * k] - (double)a[2];
+            tB += (double)t3[4 * k + 1] - (double)a[2];
+            tC += (double)t3[4 * k + 2] - (double)a[2];
+            tD += (double)t3[4 * k + 3] - (double)a[2];
             ++cnt;
         }
         if (cnt)
@@ -1942,9 +1983,14 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                          (su + sg + g1 + g2) / cnt / 1e3);
         if (cnt)
             std::fprintf(stderr,
-                         "[femi loop] k_gt from first CTA start: last CTA start +%.2f us, first consumer end +%.2f, "
-                         "last consumer end +%.2f, kernel end +%.2f\n",
-                         st_skew / cnt / 1e3, end0 / cnt / 1e3, end1 / cnt / 1e3, sg / cnt / 1e3);
+                         "[femi loop] k_gt from first CTA start: last CTA start +%.2f us, first CTA done +%.2f, "
+                         "last CTA done +%.2f, last CTA out of the tail +%.2f, kernel end +%.2f\n",
+                         st_skew / cnt / 1e3, end0 / cnt / 1e3, end1 / cnt / 1e3, end2 / cnt / 1e3, sg / cnt / 1e3);
+        if (cnt)
+            std::fprintf(stderr,
+                         "[femi loop] k_gt tail: last CTA arrival +%.2f, last CTA has partials +%.2f, scalars +%.2f, "
+                         "condition set +%.2f\n",
+                         tA / cnt / 1e3, tB / cnt / 1e3, tC / cnt / 1e3, tD / cnt / 1e3);
     }
     count_launches(11);
     CgState hs;

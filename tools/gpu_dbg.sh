@@ -1,7 +1,5 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-timeout 300 python -m pytest tests -m gpu -x -q -k "graph_mode" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
-FEMI_PCG_KBENCH=1 FEMI_PCG_GRAPH=1 timeout 200 python bench.py --no-cpu-baseline --no-e2e --steps 1 --warmup 1 > gpurun_out/kb4.json 2> gpurun_out/kbench4.err
-FEMI_PCG_GRAPH=1 FEMI_LOOP_PROF=1 timeout 200 python bench.py --no-cpu-baseline --no-e2e --steps 2 --warmup 1 > gpurun_out/kb3.json 2> gpurun_out/kbench3.err
-FEMI_PCG_GRAPH=1 timeout 200 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/kb.json 2> gpurun_out/kbench.err
+timeout 200 python bench.py --no-cpu-baseline --no-e2e --no-tonal --steps 5 --warmup 3 > gpurun_out/kb.json 2> gpurun_out/kbench.err
+timeout 300 python -m pytest tests -m gpu -x -q -k "graph_mode or config2 or config1 or constant" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
 echo done
