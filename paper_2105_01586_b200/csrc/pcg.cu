@@ -201,10 +201,22 @@ __device__ __forceinline__ bool grid_partial(double (&v)[NQ], double* red, unsig
     __syncthreads();
     if (!last) return false;
     __threadfence();
+    // all threads of the last block: strided partial sums, then the fixed block tree
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        double t = 0.0;
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += KNT) t += __ldcg(red + NQ * b + q);
+        v[q] = warp_sum_d(t);
+    }
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) shm[NQ * wid + q] = v[q];
+    __syncthreads();
     if (threadIdx.x == 0) {
         for (int q = 0; q < NQ; ++q) {
             double t = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(red + NQ * b + q);
+            for (int w = 0; w < KNT / 32; ++w) t += shm[NQ * w + q];
             v[q] = t;
         }
         *cnt = 0;
@@ -988,7 +1000,7 @@ struct JStage {
 
 // JP: tiles a consumer warp works on at once (0: software-pipelined, one tile ahead); GM: neighbour gathers 0 = global (L1/L2), 1 = shared
 // memory inside the tile, 2 = none (experiment: streaming only, wrong result)
-template <int JP, int GM>
+template <int JP, int GM, bool FIRST = false>
 __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
                                             unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
     extern __shared__ __align__(128) unsigned char jsm[];
@@ -998,7 +1010,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
     const RItem& it = items[0];
     CgState* S = it.st;
-    const bool act = S->active;
+    const bool act = FIRST || S->active;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntile = it.ntile;
     // contiguous tile range per CTA, balanced by bytes at setup (it.jpart)
@@ -1241,7 +1253,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
         }
     }
-    cg_tail<false, false, JNT>(v, act, S, B, part, gcnt, h, act ? it_prof : -1);
+    cg_tail<FIRST, false, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1);
     if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax)
         atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());  // this CTA left the tail
     if (g_loop_prof && act) {
@@ -1585,7 +1597,8 @@ struct Workspace {
 
 int g_smem_optin = -1;
 int g_fused = -1;
-int g_persist = -1;  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
+int g_persist = -1;
+int g_gt_static = 0;  // FEMI_GT_STATIC=1: static tile ranges (k_gt) instead of dynamic (k_gtd)  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
@@ -1653,7 +1666,13 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
         if (!restart)
             if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-        if ((s = chain((void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs))) return s;
+        if (C.gt_smem)
+            s = add_kernel(gr, dep, (void*)k_gt<1, 0, true>, dim3(C.gt_blocks), dim3(JNT), a_gs, &nd, C.gt_smem);
+        else
+            s = add_kernel(gr, dep, (void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs, &nd);
+        if (s) return s;
+        prev = nd;
+        dep = &prev;
     }
     {
         cudaGraphNodeParams cp = {};
@@ -1792,7 +1811,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     if (!C) {
         C = new GraphCache();
         const int nsl = (int)((n + 31) / 32);
-        C->gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + KNT - 1) / KNT, KGRID));
+        // one row per thread for the prologue/epilogue kernels (memory-level parallelism)
+        C->gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + KNT - 1) / KNT, 148 * 16));
         C->gs_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)),
                                                                    148 * 8));
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -1821,7 +1841,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 FEMI_CUDA(cudaFuncSetAttribute(k_pcgt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->pt_smem));
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
                 for (const void* fn : {(const void*)k_gt<0, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
-                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>})
+                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>, (const void*)k_gt<1, 0, true>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
             }
         }
@@ -1846,7 +1866,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         const int pb = std::max(std::max(C->gs_blocks, C->gp_blocks), C->gt_blocks);
         const size_t rb = al(sizeof(Rec) * (n + 1));
         const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
-                             al(sizeof(double) * 4 * pb) + al(sizeof(double) * KGRID) + 6 * vb + 2 * rb;
+                             al(sizeof(double) * 4 * pb) + al(sizeof(double) * C->gx) + 6 * vb + 2 * rb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
         char* cur = (char*)C->ws;
         auto take = [&](size_t x) {
@@ -1862,7 +1882,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
         C->d_part = (double*)take(sizeof(double) * 4 * pb);
         RItem& it = C->item;
-        it.red = (double*)take(sizeof(double) * KGRID);
+        it.red = (double*)take(sizeof(double) * C->gx);
         it.b = (double*)take(vb);
         it.x = (double*)take(vb);
         it.r = (double*)take(vb);
@@ -2003,6 +2023,47 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         count_launches(6);
     }
     count_launches((g_fused ? 1 : 2) * (int64_t)hs.iters);
+    if (std::getenv("FEMI_PCG_PROLOG")) {  // experiments: prologue/epilogue kernels standalone
+        cudaEvent_t ev[10];
+        for (auto& e : ev) cudaEventCreate(&e);
+        RItem* di = C->d_items;
+        const dim3 gk(C->gx, 1), bk(KNT);
+        unsigned* gcnt = C->d_cnt + 2;
+        cudaGraphConditionalHandle hdl = 0;
+        int one = 1;
+        cudaEventRecord(ev[0], st);
+        k_reset_items<<<1, 32, 0, st>>>(one, di);
+        cudaEventRecord(ev[1], st);
+        k_minmax<<<296, 256, 0, st>>>(one, di);
+        cudaEventRecord(ev[2], st);
+        k_rhs<<<gk, bk, 0, st>>>(di);
+        cudaEventRecord(ev[3], st);
+        k_init_x<<<gk, bk, 0, st>>>(di);
+        cudaEventRecord(ev[4], st);
+        k_zero_ps<<<gk, bk, 0, st>>>(di);
+        k_init_r<<<gk, bk, 0, st>>>(di, C->d_cnt);
+        cudaEventRecord(ev[5], st);
+        k_gs<true><<<dim3(C->gs_blocks), GNT, 0, st>>>(di, 1, C->d_part, gcnt, hdl);
+        cudaEventRecord(ev[6], st);
+        k_finalize<<<gk, bk, 0, st>>>(di);
+        cudaEventRecord(ev[7], st);
+        k_true_res<<<gk, bk, 0, st>>>(di, C->d_cnt + 1);
+        cudaEventRecord(ev[8], st);
+        k_copy_g<<<296, 256, 0, st>>>(di);
+        cudaEventRecord(ev[9], st);
+        cudaEventSynchronize(ev[9]);
+        float t[9];
+        for (int k = 0; k < 9; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
+        std::fprintf(stderr,
+                     "[femi prolog] us: reset %.1f minmax %.1f rhs %.1f init_x %.1f zero+init_r %.1f first-spmv %.1f "
+                     "finalize %.1f true_res %.1f copy_g %.1f\n",
+                     1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3], 1e3 * t[4], 1e3 * t[5], 1e3 * t[6], 1e3 * t[7],
+                     1e3 * t[8]);
+        for (auto& e : ev) cudaEventDestroy(e);
+        // restore the solve's state (the standalone launches above re-ran the prologue)
+        FEMI_CUDA(cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+    }
     if (const char* mb = std::getenv("FEMI_PCG_KBENCH")) {  // experiments: body kernels standalone
         (void)mb;
         cudaEvent_t e0, e1, e2;
