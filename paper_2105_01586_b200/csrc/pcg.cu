@@ -1596,9 +1596,8 @@ struct Workspace {
 };
 
 int g_smem_optin = -1;
-int g_fused = -1;
-int g_persist = -1;
-int g_gt_static = 0;  // FEMI_GT_STATIC=1: static tile ranges (k_gt) instead of dynamic (k_gtd)  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt  // graph mode body: 0 = k_gu + k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
+int g_fused = -1;    // graph mode body: 0 = k_gu + k_gt/k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
+int g_persist = -1;  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
