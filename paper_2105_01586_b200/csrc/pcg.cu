@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, 
 constexpr int JCW = kJdsRows / 32;  // consumer warps = slices per tile
 constexpr int JNT = 32 * (JCW + 1);
 constexpr int JNS = 6;
-constexpr int kUnroll = 4;  // CG iterations per WHILE body (graph mode)
+constexpr int kUnroll = 8;  // CG iterations per WHILE body (graph mode; measured: x4 2.9 us, x8 2.2 us of WHILE gap per iteration)
 
 struct JStage {
     double* val;
