@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "device.cuh"
 #include "tma.cuh"
@@ -77,6 +78,7 @@ struct RItem {
     const int32_t* jcb;
     int32_t ntile, jmaxe, jkmax, jmbytes;
     int32_t jpol, jpad;  // L2 policy of the streamed matrix: 0 none, 1 evict-first, 2 evict-last
+    double dmin;         // min_i diag(A_uu)_i: ||r||^2 >= dmin ||r^||^2 (skips the monitor far from rtol)
     const int32_t* jpart;  // [gt_blocks + 1] first tile of each k_gt CTA
     double* part;  // [ncta][4] partial sums / barrier slots
     double* red;   // [reduction blocks] partials of the ordinary kernels
@@ -678,13 +680,15 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
 // swaps the double-buffered vectors.
 template <bool FIRST, bool FLIP, int NT = GNT>
 __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, int B, double* __restrict__ part,
-                                        unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int prof_it = -1) {
+                                        unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int prof_it = -1,
+                                        double dmin = 0.0) {
     const bool tp = prof_it >= 0 && prof_it < kLoopProfMax && g_loop_prof;
     // the recurrence state the last CTA needs, loaded up front (off the tail's critical path);
     // it only changes in the last CTA of the previous launch
     double s_bn2 = 0.0, s_tol2 = 0.0, s_rr = 0.0, s_alpha = 0.0;
-    int s_iters = 0, s_max = 0, s_par = 0;
+    int s_iters = 0, s_max = 0, s_par = 0, s_need = 1;
     if (threadIdx.x == 0) {
+        s_need = FIRST ? 1 : S->need_rho;
         s_bn2 = S->bn2;
         s_tol2 = S->tol2;
         s_rr = S->rr;
@@ -762,8 +766,8 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
             if (FLIP) S->par = s_par ^ 1;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 S->status = FEMI_E_NONFINITE;
-            } else if (rho2 <= s_tol2) {
-                // converged
+            } else if (s_need && rho2 <= s_tol2) {
+                // converged (rho2 is only computed when dmin gam2 was within 100x of tol2)
             } else if (it1 >= s_max) {
                 S->status = FEMI_E_NOT_CONVERGED;
             } else {
@@ -780,6 +784,9 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
             }
         }
         S->active = active;
+        // the next SpMV needs the unscaled norm only when it can possibly be <= tol2:
+        // ||r||^2 >= dmin ||r^||^2, with two orders of magnitude of slack for one iteration
+        S->need_rho = (gam2 * dmin <= 100.0 * s_tol2) ? 1 : 0;
     }
     if (tp) g_tail_ts[4 * prof_it + 2] = gtime();  // C: scalars done
     // all items reported? -> loop condition (one item: set it directly)
@@ -1011,6 +1018,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     const RItem& it = items[0];
     CgState* S = it.st;
     const bool act = FIRST || S->active;
+    const bool nrho = FIRST || S->need_rho;  // else the q stream and the residual monitor are skipped
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntile = it.ntile;
     // contiguous tile range per CTA, balanced by bytes at setup (it.jpart)
@@ -1052,10 +1060,11 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                     const int ne = e1 - e0, nc = c1 - c0;
                     tile_e[k] = make_int2(e0, ne);
                     tile_c[k] = make_int2(c0, nc);
-                    const uint32_t bytes = (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 16u * kJdsRows;
+                    const uint32_t bytes =
+                        (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + (nrho ? 16u : 8u) * kJdsRows;
                     mbar_arrive_expect_tx(&full[k], bytes);
                     bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
-                    bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    if (nrho) bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
                     bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
                     if (ne) {
                         if (pm) {
@@ -1152,6 +1161,14 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                     kst = kn;
                 }
             } else
+            if constexpr (GM == 3) {  // experiment: pure TMA stream (wait + release only)
+                for (int i = 0; i < cnt; ++i) {
+                    const int k = i % JNS;
+                    mbar_wait(&full[k], (i / JNS) & 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[k]);
+                }
+            } else
             for (int i0 = 0; i0 < cnt; i0 += JP) {
                 int len[JP], L[JP];
                 bool wide[JP];
@@ -1172,7 +1189,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                         len[p] = q.meta[rl];
                         doff[p] = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
                         xi[p] = q.r[rl];
-                        qi[p] = q.s[rl];
+                        qi[p] = nrho ? q.s[rl] : 0.0;
                         wide[p] = tile_c[k].y > 2 * tile_e[k].y;  // written before the release of this stage
                         val[p] = q.val;
                         col[p] = q.col;
@@ -1253,12 +1270,143 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
         }
     }
-    cg_tail<FIRST, false, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1);
+    cg_tail<FIRST, false, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1, it.dmin);
     if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax)
         atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());  // this CTA left the tail
     if (g_loop_prof && act) {
         __syncthreads();
         if (threadIdx.x == 0) loop_stamp(1, it_prof, t_start);
+    }
+}
+
+// k_gt2: k_gt with 31 consumer warps per SM (1024 threads, <= 64 registers) instead of 16:
+// the consumer's smem -> gather -> fma chain is latency-bound, so twice the warps keep twice
+// the gathers in flight. Warp w (0..30) takes slices w, w+31, w+62, ... of its CTA's slice
+// sequence (tile = slice / 16); a tile's stage is released after its 16 slices are done.
+constexpr int J2CW = 31;
+constexpr int J2NT = 32 * (J2CW + 1);
+template <int U, bool FIRST>
+__global__ void __launch_bounds__(J2NT, 1) k_gt2(const RItem* __restrict__ items, int B, double* __restrict__ part,
+                                               unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+    extern __shared__ __align__(128) unsigned char jsm[];
+    unsigned long long t_start = 0;
+    if (g_loop_prof && threadIdx.x == 0) t_start = gtime();
+    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
+    __shared__ int2 tile_e[JNS], tile_c[JNS];
+    const RItem& it = items[0];
+    CgState* S = it.st;
+    const bool act = FIRST || S->active;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
+    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
+    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 16 * kJdsRows + 127) & ~(size_t)127;
+    auto stage = [&](int k) {
+        unsigned char* b = jsm + (size_t)k * stage_bytes;
+        JStage q;
+        q.r = (double*)b;
+        q.s = q.r + kJdsRows;
+        q.val = q.s + kJdsRows;
+        q.col = (uint8_t*)(q.val + maxe);
+        q.meta = q.col + 4 * (size_t)maxe;
+        return q;
+    };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < JNS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], JCW);  // the 16 slices of a tile
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double v[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        if (warp == J2CW) {
+            if (lane == 0) {
+                int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
+                const uint64_t pol = policy_evict_first();
+                for (int t = tb, i = 0; t < te; ++t, ++i) {
+                    const int k = i % JNS;
+                    const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];
+                    if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);
+                    const JStage q = stage(k);
+                    const int ne = e1 - e0, nc = c1 - c0;
+                    tile_e[k] = make_int2(e0, ne);
+                    tile_c[k] = make_int2(c0, nc);
+                    mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 16u * kJdsRows);
+                    bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
+                    if (ne) {
+                        bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
+                        bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
+                    }
+                    e0 = e1;
+                    c0 = c1;
+                }
+            }
+        } else {
+            const double* __restrict__ rg = it.r;
+            double* __restrict__ wout = it.w;
+            const int nsl = (te - tb) * JCW;  // slices of this CTA
+            for (int sl = warp; sl < nsl; sl += J2CW) {
+                const int i = sl / JCW, ws = sl - i * JCW;  // tile (local index), slice in tile
+                const int k = i % JNS;
+                mbar_wait(&full[k], (i / JNS) & 1);
+                const JStage q = stage(k);
+                const int t = tb + i;
+                const int rl = 32 * ws + lane;
+                const int row = t * kJdsRows + rl;
+                const int len = q.meta[rl];
+                const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + ws * kmax;
+                const double xi = q.r[rl], qi = q.s[rl];
+                const int L = __shfl_sync(0xffffffffu, len, 0);
+                const bool wide = tile_c[k].y > 2 * tile_e[k].y;
+                const int16_t* c16 = (const int16_t*)q.col;
+                const int32_t* c32 = (const int32_t*)q.col;
+                const double* rt = rg + (int64_t)t * kJdsRows;
+                double acc = 0.0;
+                for (int k0 = 0; k0 < L; k0 += U) {
+                    double vv[U], gv[U];
+                    int c[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const bool a = k0 + u < len;
+                        const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
+                        vv[u] = a ? q.val[idx] : 0.0;
+                        c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) gv[u] = rt[c[u]];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) acc = fma(vv[u], gv[u], acc);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[k]);
+                if (row < it.n) {
+                    const double y = xi + acc;
+                    wout[row] = y;
+                    const double ru = xi * qi;
+                    v[0] += xi * xi;
+                    v[1] += y * xi;
+                    v[2] += ru * ru;
+                }
+            }
+        }
+    }
+    const int it_prof = S->iters;
+    if (g_loop_prof && act && it_prof < kLoopProfMax) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long t = gtime();
+            atomicMax(&g_loop_ts2[4 * it_prof], t_start);
+            atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
+            atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
+        }
+    }
+    cg_tail<FIRST, false, J2NT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1);
+    if (g_loop_prof && act && !FIRST && threadIdx.x == 0) {
+        if (it_prof < kLoopProfMax) atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());
+        loop_stamp(1, it_prof, t_start);
     }
 }
 
@@ -1573,6 +1721,15 @@ __global__ void k_pack(const RItem* __restrict__ items) {
     }
 }
 
+// min over i of q_i^2 = diag(A_uu)_i (order-preserving bits of positive doubles)
+__global__ void k_qmin(int64_t n, const double* __restrict__ q, unsigned long long* __restrict__ out) {
+    unsigned long long m = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = min(m, (unsigned long long)__double_as_longlong(q[i] * q[i]));
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
 struct GraphCache {
     void* ws = nullptr;
     RItem* d_items = nullptr;
@@ -1585,6 +1742,7 @@ struct GraphCache {
     int gt_blocks = 0;
     unsigned gt_smem = 0;  // > 0: the body's SpMV is the TMA-streamed k_gt
     unsigned pt_smem = 0;  // dynamic shared memory of the persistent k_pcgt
+    int gt_ver = 1, gt_u = 8;  // SpMV kernel: 1 = k_gt (16 consumer warps), 2 = k_gt2 (31, unroll gt_u)
 };
 
 struct Workspace {
@@ -1665,7 +1823,10 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
         if (!restart)
             if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-        if (C.gt_smem)
+        if (C.gt_smem && C.gt_ver == 2)
+            s = add_kernel(gr, dep, C.gt_u == 8 ? (void*)k_gt2<8, true> : (void*)k_gt2<4, true>, dim3(C.gt_blocks),
+                           dim3(J2NT), a_gs, &nd, C.gt_smem);
+        else if (C.gt_smem)
             s = add_kernel(gr, dep, (void*)k_gt<1, 0, true>, dim3(C.gt_blocks), dim3(JNT), a_gs, &nd, C.gt_smem);
         else
             s = add_kernel(gr, dep, (void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs, &nd);
@@ -1691,8 +1852,12 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
                 if ((s = add_kernel(body, prevb ? &prevb : nullptr, (void*)k_gu,
                                     dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT), a_items, &u)))
                     return s;
-                if ((s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem)))
-                    return s;
+                if (C.gt_ver == 2)
+                    s = add_kernel(body, &u, C.gt_u == 8 ? (void*)k_gt2<8, false> : (void*)k_gt2<4, false>,
+                                   dim3(C.gt_blocks), dim3(J2NT), a_gs, &sn, C.gt_smem);
+                else
+                    s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem);
+                if (s) return s;
                 prevb = sn;
             }
         } else if (g_fused) {
@@ -1835,12 +2000,17 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 std::fprintf(stderr, "[femi] k_gt: stage %zu B x %d, optin %d\n", stage_bytes, JNS, optin);
             if (JNS * stage_bytes + 1024 <= (size_t)optin) {
                 C->gt_smem = (unsigned)(JNS * stage_bytes);
+                if (const char* gv = std::getenv("FEMI_GT")) C->gt_ver = std::atoi(gv) == 2 ? 2 : 1;
+                if (const char* gu = std::getenv("FEMI_GT_U")) C->gt_u = std::atoi(gu) == 4 ? 4 : 8;
                 C->pt_smem = (unsigned)(JNS * (((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 8 * kJdsRows + 127) &
                                                ~(size_t)127));
                 FEMI_CUDA(cudaFuncSetAttribute(k_pcgt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->pt_smem));
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
                 for (const void* fn : {(const void*)k_gt<0, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
-                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>, (const void*)k_gt<1, 0, true>})
+                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>, (const void*)k_gt<1, 0, true>,
+                                       (const void*)k_gt<1, 3>,
+                                       (const void*)k_gt2<4, true>, (const void*)k_gt2<4, false>,
+                                       (const void*)k_gt2<8, true>, (const void*)k_gt2<8, false>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
             }
         }
@@ -1901,6 +2071,19 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.jmbytes = S->jds_meta_bytes;
         it.jpol = 1;
         it.jpart = d_jpart;
+        {
+            unsigned long long* d_m = nullptr;
+            unsigned long long h_m = ~0ull;
+            FEMI_CUDA(cudaMalloc(&d_m, sizeof(unsigned long long)));
+            FEMI_CUDA(cudaMemcpy(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice));
+            k_qmin<<<296, 256>>>(n, S->q_int, d_m);
+            FEMI_CUDA(cudaMemcpy(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost));
+            FEMI_CUDA(cudaFree(d_m));
+            double dm;
+            std::memcpy(&dm, &h_m, sizeof(dm));
+            it.dmin = (n > 0 && std::isfinite(dm) && dm > 0.0) ? dm * (1.0 - 1e-12) : 0.0;
+            if (std::getenv("FEMI_NO_RHO_SKIP")) it.dmin = 0.0;  // experiments: monitor every iteration
+        }
         if (const char* pe = std::getenv("FEMI_JDS_POLICY")) it.jpol = std::atoi(pe);
         it.inv = S->sell_inv;
         it.len = S->sell_len;
@@ -2108,11 +2291,11 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 ts += b;
             }
         }
-        float tt[4] = {0, 0, 0, 0};
-        void (*const gts[4])(const RItem*, int, double*, unsigned*, cudaGraphConditionalHandle) = {
-            k_gt<1, 0>, k_gt<0, 0>, k_gt<1, 1>, k_gt<1, 2>};
+        float tt[5] = {0, 0, 0, 0, 0};
+        void (*const gts[5])(const RItem*, int, double*, unsigned*, cudaGraphConditionalHandle) = {
+            k_gt<1, 0>, k_gt<0, 0>, k_gt<1, 1>, k_gt<1, 2>, k_gt<1, 3>};
         if (C->gt_smem)
-            for (int v = 0; v < 4; ++v)
+            for (int v = 0; v < 5; ++v)
                 for (int k = 0; k < reps; ++k) {
                     act.par = 0;
                     cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
@@ -2177,9 +2360,9 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         }
         std::fprintf(stderr,
                      "[femi kbench] k_gt (TMA, grid %d, smem %u): JP1 %.2f us  pipelined %.2f us  smem-gather %.2f us  "
-                     "no-gather %.2f us\n",
+                     "no-gather %.2f us  stream-only %.2f us\n",
                      C->gt_blocks, C->gt_smem, 1e3 * tt[0] / (reps - 2), 1e3 * tt[1] / (reps - 2),
-                     1e3 * tt[2] / (reps - 2), 1e3 * tt[3] / (reps - 2));
+                     1e3 * tt[2] / (reps - 2), 1e3 * tt[3] / (reps - 2), 1e3 * tt[4] / (reps - 2));
         std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grids %d / %d)  fused k_gp %.2f us (grid %d)\n",
                      1e3 * tu / (reps - 2), 1e3 * ts / (reps - 2), gu, C->gs_blocks, 1e3 * tf / (reps - 2),
                      C->gp_blocks);
