@@ -37,8 +37,8 @@ struct CgState {
     unsigned long long kmin, kmax;  // order-preserving keys of min(g), max(g)
     int32_t iters, active, status, max_iter;
     uint32_t cnt[4];  // last-block counters (one per reduction site)
-    int32_t par;       // graph mode (fused body): which of the double-buffered r/w/s vectors is current
     int32_t need_rho;  // graph mode: the next SpMV computes the unscaled residual norm (else it is skipped)
+    int32_t pad;
 };
 
 // One batch item as the PCG kernels see it.

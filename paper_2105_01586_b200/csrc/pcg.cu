@@ -70,14 +70,12 @@ struct RItem {
     double* w;  // A^ r^
     double* p;  // used when the CTA's rows do not fit shared memory
     double* sv;
-    double *rec0, *rec1;  // graph mode, fused body: double-buffered {r, w, s, p} records (CgState::par)
     const double* jval;   // graph mode: tiled jagged-diagonal matrix (device.cuh), TMA-streamed
     const uint8_t* jcol;
     const uint8_t* jmeta;
     const int32_t* jeb;
     const int32_t* jcb;
     int32_t ntile, jmaxe, jkmax, jmbytes;
-    int32_t jpol, jpad;  // L2 policy of the streamed matrix: 0 none, 1 evict-first, 2 evict-last
     double dmin;         // min_i diag(A_uu)_i: ||r||^2 >= dmin ||r^||^2 (skips the monitor far from rtol)
     const int32_t* jpart;  // [gt_blocks + 1] first tile of each k_gt CTA
     double* part;  // [ncta][4] partial sums / barrier slots
@@ -99,8 +97,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-__device__ int g_gt_prof;                     // kbench: per-CTA start/end times of k_gt
-__device__ unsigned long long g_gt_times[2 * 1024];
 // FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
 constexpr int kLoopProfMax = 4096;
 __device__ int g_loop_prof;
@@ -676,9 +672,8 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
 
 // Block partials -> part[item][block]; the last block of the item sums them in block order
 // (deterministic), advances the CG recurrence scalars (FIRST: starts it) and, once every item
-// has reported, sets the WHILE condition (any item still active -> 1). FLIP: the fused body
-// swaps the double-buffered vectors.
-template <bool FIRST, bool FLIP, int NT = GNT>
+// has reported, sets the WHILE condition (any item still active -> 1).
+template <bool FIRST, int NT = GNT>
 __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, int B, double* __restrict__ part,
                                         unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int prof_it = -1,
                                         double dmin = 0.0) {
@@ -686,7 +681,7 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     // the recurrence state the last CTA needs, loaded up front (off the tail's critical path);
     // it only changes in the last CTA of the previous launch
     double s_bn2 = 0.0, s_tol2 = 0.0, s_rr = 0.0, s_alpha = 0.0;
-    int s_iters = 0, s_max = 0, s_par = 0, s_need = 1;
+    int s_iters = 0, s_max = 0, s_need = 1;
     if (threadIdx.x == 0) {
         s_need = FIRST ? 1 : S->need_rho;
         s_bn2 = S->bn2;
@@ -695,7 +690,6 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         s_alpha = S->alpha;
         s_iters = S->iters;
         s_max = S->max_iter;
-        s_par = S->par;
     }
     __shared__ double shm[4 * (NT / 32)];
     __shared__ int last;
@@ -763,7 +757,6 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         } else {
             const int it1 = s_iters + 1;
             S->iters = it1;
-            if (FLIP) S->par = s_par ^ 1;
             if (!isfinite(gam2) || !isfinite(del2)) {
                 S->status = FEMI_E_NONFINITE;
             } else if (s_need && rho2 <= s_tol2) {
@@ -872,115 +865,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
             }
         }
     }
-    cg_tail<FIRST, false>(v, act, S, B, part, gcnt, h);
-}
-
-// Fused body (one kernel per CG iteration). The vectors a neighbour gathers travel together:
-// rec[i] = {r, w, s, p} (32 B, one sector), double-buffered (CgState::par = current copy);
-// x stays a plain vector updated in place. For its own rows a warp applies the update
-//   p' = r + beta p ; s' = w + beta s ; x += alpha p' ; r' = r - alpha s'
-// and the SpMV w' = r' + A^_off r' gathers each neighbour's record and recomputes its
-// r' = r - alpha (w + beta s) with the same fma sequence as the owner (bit-identical), so no
-// grid-wide barrier separates the update from the SpMV. Per row and iteration: rec read and
-// write (64 B), x read/write (16 B), s_jacobi read (8 B) = 11 vector streams, plus the
-// matrix, one gathered sector per nonzero and one kernel boundary.
-// FIRST: no update (p = s = 0 already); w = r + A^_off r into the current record.
-struct __align__(16) Rec {
-    double r, w, s, p;
-};
-
-template <bool FIRST>
-__global__ void __launch_bounds__(GNT, 3) k_gp(const RItem* __restrict__ items, int B, double* __restrict__ part,
-                                           unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
-    const RItem& it = items[blockIdx.y];
-    CgState* S = it.st;
-    const bool act = FIRST || S->active;
-    double v[3] = {0.0, 0.0, 0.0};
-    if (act) {
-        const int lane = threadIdx.x & 31;
-        const int n = it.n;
-        const int nsl = (n + 31) / 32;
-        const int gw = (blockIdx.x * GNT + threadIdx.x) >> 5, nw = (gridDim.x * GNT) >> 5;
-        const int cur = S->par;
-        const double alpha = FIRST ? 0.0 : S->alpha, beta = FIRST ? 0.0 : S->beta;
-        const Rec* __restrict__ R0 = (const Rec*)(cur ? it.rec1 : it.rec0);
-        Rec* __restrict__ R1 = (Rec*)(cur ? it.rec0 : it.rec1);
-        for (int sa = 2 * gw; sa < nsl; sa += 2 * nw) {
-            const bool hb = sa + 1 < nsl;
-            int row[2], len[2], base[2];
-            double rn[2], sn[2], pn[2], acc[2] = {0.0, 0.0};
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int sl = sa + hh;
-                const bool ok = hh == 0 || hb;
-                row[hh] = (ok && 32 * sl + lane < n) ? 32 * sl + lane : -1;
-                len[hh] = ok ? it.len[sl] : 0;
-                base[hh] = ok ? it.base[sl] + lane : 0;
-                const int i = row[hh] >= 0 ? row[hh] : 32 * sa;
-                const Rec q = R0[i];
-                if (FIRST) {
-                    rn[hh] = q.r;
-                } else {
-                    pn[hh] = fma(beta, q.p, q.r);
-                    sn[hh] = fma(beta, q.s, q.w);
-                    rn[hh] = fma(-alpha, sn[hh], q.r);
-                    if (row[hh] >= 0) it.x[i] = fma(alpha, pn[hh], it.x[i]);
-                }
-            }
-            const int cb = (32 * sa / SIG) * SIG;  // sa even, SIG % 64 == 0: both slices share the window
-            const int L = max(len[0], len[1]);
-            for (int k0 = 0; k0 < L; k0 += 2) {
-                double vv[4];
-                int c[4];
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int e = base[hh] + 32 * (k0 + q);
-                        if (k0 + q < len[hh]) {
-                            vv[2 * hh + q] = it.val[e];
-                            c[2 * hh + q] = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
-                        } else {
-                            vv[2 * hh + q] = 0.0;
-                            c[2 * hh + q] = 32 * sa;
-                        }
-                    }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    double gc;
-                    if (FIRST) {
-                        gc = R0[c[q]].r;
-                    } else {
-                        const Rec g = R0[c[q]];
-                        gc = fma(-alpha, fma(beta, g.s, g.w), g.r);
-                    }
-                    if (q < 2) acc[0] = fma(vv[q], gc, acc[0]);
-                    else acc[1] = fma(vv[q], gc, acc[1]);
-                }
-            }
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                if (row[hh] < 0) continue;
-                const int i = row[hh];
-                const double y = rn[hh] + acc[hh];
-                if (FIRST) {
-                    ((Rec*)R0)[i].w = y;
-                } else {
-                    Rec o;
-                    o.r = rn[hh];
-                    o.w = y;
-                    o.s = sn[hh];
-                    o.p = pn[hh];
-                    R1[i] = o;
-                }
-                const double ru = rn[hh] * it.q[i];
-                v[0] += rn[hh] * rn[hh];
-                v[1] += y * rn[hh];
-                v[2] += ru * ru;
-            }
-        }
-    }
-    cg_tail<FIRST, !FIRST>(v, act, S, B, part, gcnt, h);
+    cg_tail<FIRST>(v, act, S, B, part, gcnt, h);
 }
 
 // S of the graph-mode body for large systems: w = r + A^_off r and the dots, with the matrix
@@ -1005,14 +890,12 @@ struct JStage {
     double* s;
 };
 
-// JP: tiles a consumer warp works on at once (0: software-pipelined, one tile ahead); GM: neighbour gathers 0 = global (L1/L2), 1 = shared
-// memory inside the tile, 2 = none (experiment: streaming only, wrong result)
-template <int JP, int GM, bool FIRST = false>
+template <bool FIRST>
 __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
                                             unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
     extern __shared__ __align__(128) unsigned char jsm[];
     unsigned long long t_start = 0;
-    if ((g_gt_prof || g_loop_prof) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (g_loop_prof && threadIdx.x == 0) t_start = gtime();
     __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
     __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
     const RItem& it = items[0];
@@ -1020,13 +903,10 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     const bool act = FIRST || S->active;
     const bool nrho = FIRST || S->need_rho;  // else the q stream and the residual monitor are skipped
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntile = it.ntile;
-    // contiguous tile range per CTA, balanced by bytes at setup (it.jpart)
-    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
-    (void)ntile;
+    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];  // this CTA's tiles
     const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
     const size_t stage_bytes = ((size_t)maxe * 12 + mb + 16 * kJdsRows + 127) & ~(size_t)127;
-    auto stage = [&](int k) {
+    auto stage = [&](int k) {  // r | q | values | columns | lengths + diagonal offsets
         unsigned char* b = jsm + (size_t)k * stage_bytes;
         JStage q;
         q.r = (double*)b;
@@ -1047,11 +927,10 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     double v[3] = {0.0, 0.0, 0.0};
     if (act) {
         if (warp == JCW) {
-            // ---- producer
+            // ---- producer: one elected lane streams the CTA's tiles into the ring
             if (lane == 0) {
                 int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
-                const int pm = it.jpol;
-                const uint64_t pol = pm == 1 ? policy_evict_first() : policy_evict_last();
+                const uint64_t pol = policy_evict_first();  // keep the CG vectors L2-resident
                 for (int t = tb, i = 0; t < te; ++t, ++i) {
                     const int k = i % JNS;
                     const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];  // loaded before the wait
@@ -1060,281 +939,10 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                     const int ne = e1 - e0, nc = c1 - c0;
                     tile_e[k] = make_int2(e0, ne);
                     tile_c[k] = make_int2(c0, nc);
-                    const uint32_t bytes =
-                        (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + (nrho ? 16u : 8u) * kJdsRows;
-                    mbar_arrive_expect_tx(&full[k], bytes);
+                    mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb +
+                                                        (nrho ? 16u : 8u) * kJdsRows);
                     bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
                     if (nrho) bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
-                    bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
-                    if (ne) {
-                        if (pm) {
-                            bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
-                            bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
-                        } else {
-                            bulk_g2s(q.val, it.jval + e0, 8u * ne, &full[k]);
-                            bulk_g2s(q.col, it.jcol + c0, (uint32_t)nc, &full[k]);
-                        }
-                    }
-                    e0 = e1;
-                    c0 = c1;
-                }
-            }
-        } else {
-            // ---- consumers: warp = slice of the tile, lane = row (rows in descending length).
-            const double* __restrict__ rg = it.r;
-            double* __restrict__ wout = it.w;
-            const int rl = 32 * warp + lane;
-            const int cnt = te - tb;
-            if constexpr (JP == 0) {
-                // software pipeline over the tiles: the first 8 diagonals of tile i+1 are read and
-                // their neighbour gathers issued before tile i's products are summed, so a warp
-                // always has one tile's gathers in flight (rows with > 8 off-diagonals finish
-                // their remaining diagonals synchronously)
-                double vv[8], gv[8];
-                double xi = 0.0, qi = 0.0;
-                int len = 0, L = 0, kst = 0;
-                auto load = [&](int i, double (&vo)[8], double (&go)[8], double& xo, double& qo, int& lo, int& Lo,
-                                int& ko) {
-                    ko = i % JNS;
-                    mbar_wait(&full[ko], (i / JNS) & 1);
-                    const JStage q = stage(ko);
-                    lo = q.meta[rl];
-                    Lo = __shfl_sync(0xffffffffu, lo, 0);
-                    xo = q.r[rl];
-                    qo = q.s[rl];
-                    const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
-                    const bool wide = tile_c[ko].y > 2 * tile_e[ko].y;
-                    const double* rt = rg + (int64_t)(tb + i) * kJdsRows;
-                    int c[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const bool a = u < lo;
-                        const int idx = (u < Lo ? doff[u] : 0) + lane;
-                        vo[u] = a ? q.val[idx] : 0.0;
-                        c[u] = a ? (wide ? ((const int32_t*)q.col)[idx] : (int)((const int16_t*)q.col)[idx]) : rl;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) go[u] = rt[c[u]];
-                };
-                if (cnt > 0) load(0, vv, gv, xi, qi, len, L, kst);
-                for (int i = 0; i < cnt; ++i) {
-                    double vn[8], gn[8], xn = 0.0, qn = 0.0;
-                    int ln = 0, Ln = 0, kn = 0;
-                    if (i + 1 < cnt) load(i + 1, vn, gn, xn, qn, ln, Ln, kn);
-                    double acc = 0.0;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
-                    if (L > 8) {  // long rows: remaining diagonals of tile i, synchronously
-                        const JStage q = stage(kst);
-                        const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
-                        const bool wide = tile_c[kst].y > 2 * tile_e[kst].y;
-                        const double* rt = rg + (int64_t)(tb + i) * kJdsRows;
-                        for (int k = 8; k < L; ++k) {
-                            const bool a = k < len;
-                            const int idx = doff[k] + lane;
-                            if (a) {
-                                const int cc = wide ? ((const int32_t*)q.col)[idx] : (int)((const int16_t*)q.col)[idx];
-                                acc = fma(q.val[idx], rt[cc], acc);
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[kst]);
-                    const int row = (tb + i) * kJdsRows + rl;
-                    if (row < it.n) {
-                        const double y = xi + acc;
-                        wout[row] = y;
-                        const double ru = xi * qi;
-                        v[0] += xi * xi;
-                        v[1] += y * xi;
-                        v[2] += ru * ru;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        vv[u] = vn[u];
-                        gv[u] = gn[u];
-                    }
-                    xi = xn;
-                    qi = qn;
-                    len = ln;
-                    L = Ln;
-                    kst = kn;
-                }
-            } else
-            if constexpr (GM == 3) {  // experiment: pure TMA stream (wait + release only)
-                for (int i = 0; i < cnt; ++i) {
-                    const int k = i % JNS;
-                    mbar_wait(&full[k], (i / JNS) & 1);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[k]);
-                }
-            } else
-            for (int i0 = 0; i0 < cnt; i0 += JP) {
-                int len[JP], L[JP];
-                bool wide[JP];
-                const uint16_t* doff[JP];
-                const double* val[JP];
-                const uint8_t* col[JP];
-                const double* rt[JP];
-                const double* sr[JP];
-                double xi[JP], qi[JP], acc[JP];
-                int Lm = 0;
-#pragma unroll
-                for (int p = 0; p < JP; ++p) {
-                    const int i = i0 + p;
-                    if (i < cnt) {
-                        const int k = i % JNS;
-                        mbar_wait(&full[k], (i / JNS) & 1);
-                        const JStage q = stage(k);
-                        len[p] = q.meta[rl];
-                        doff[p] = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
-                        xi[p] = q.r[rl];
-                        qi[p] = nrho ? q.s[rl] : 0.0;
-                        wide[p] = tile_c[k].y > 2 * tile_e[k].y;  // written before the release of this stage
-                        val[p] = q.val;
-                        col[p] = q.col;
-                        rt[p] = rg + (int64_t)(tb + i) * kJdsRows;
-                        sr[p] = q.r;
-                    } else {
-                        sr[p] = nullptr;
-                        len[p] = 0;
-                        doff[p] = nullptr;
-                        xi[p] = qi[p] = 0.0;
-                        wide[p] = false;
-                        val[p] = nullptr;
-                        col[p] = nullptr;
-                        rt[p] = rg;
-                    }
-                    L[p] = __shfl_sync(0xffffffffu, len[p], 0);  // lane 0 holds the longest row
-                    Lm = max(Lm, L[p]);
-                    acc[p] = 0.0;
-                }
-                for (int k0 = 0; k0 < Lm; k0 += 8) {
-                    double vv[JP][8], gv[JP][8];
-                    int c[JP][8];
-#pragma unroll
-                    for (int p = 0; p < JP; ++p)
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const bool a = k0 + u < len[p];
-                            const int idx = (k0 + u < L[p] ? doff[p][k0 + u] : 0) + lane;
-                            vv[p][u] = a ? val[p][idx] : 0.0;
-                            c[p][u] = a ? (wide[p] ? ((const int32_t*)col[p])[idx] : (int)((const int16_t*)col[p])[idx])
-                                        : rl;
-                        }
-#pragma unroll
-                    for (int p = 0; p < JP; ++p)
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            if (GM == 2) gv[p][u] = 1.0;
-                            else if (GM == 1 && (unsigned)c[p][u] < (unsigned)kJdsRows) gv[p][u] = sr[p][c[p][u]];
-                            else gv[p][u] = rt[p][c[p][u]];
-                        }
-#pragma unroll
-                    for (int p = 0; p < JP; ++p)
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) acc[p] = fma(vv[p][u], gv[p][u], acc[p]);
-                }
-                __syncwarp();
-#pragma unroll
-                for (int p = 0; p < JP; ++p) {
-                    const int i = i0 + p;
-                    if (i >= cnt) break;
-                    if (lane == 0) mbar_arrive(&empty[i % JNS]);
-                    const int row = (tb + i) * kJdsRows + rl;
-                    if (row < it.n) {
-                        const double y = xi[p] + acc[p];
-                        wout[row] = y;
-                        const double ru = xi[p] * qi[p];
-                        v[0] += xi[p] * xi[p];
-                        v[1] += y * xi[p];
-                        v[2] += ru * ru;
-                    }
-                }
-            }
-        }
-    }
-    if (g_gt_prof && threadIdx.x == 0) {
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        g_gt_times[2 * blockIdx.x] = t_start;
-        g_gt_times[2 * blockIdx.x + 1] = t1;
-    }
-    const int it_prof = S->iters;
-    if (g_loop_prof && act && it_prof < kLoopProfMax) {
-        __syncthreads();  // profiling only: every warp of the CTA is done
-        if (threadIdx.x == 0) {
-            const unsigned long long t = gtime();
-            atomicMax(&g_loop_ts2[4 * it_prof], t_start);
-            atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
-            atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
-        }
-    }
-    cg_tail<FIRST, false, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1, it.dmin);
-    if (g_loop_prof && act && threadIdx.x == 0 && it_prof < kLoopProfMax)
-        atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());  // this CTA left the tail
-    if (g_loop_prof && act) {
-        __syncthreads();
-        if (threadIdx.x == 0) loop_stamp(1, it_prof, t_start);
-    }
-}
-
-// k_gt2: k_gt with 31 consumer warps per SM (1024 threads, <= 64 registers) instead of 16:
-// the consumer's smem -> gather -> fma chain is latency-bound, so twice the warps keep twice
-// the gathers in flight. Warp w (0..30) takes slices w, w+31, w+62, ... of its CTA's slice
-// sequence (tile = slice / 16); a tile's stage is released after its 16 slices are done.
-constexpr int J2CW = 31;
-constexpr int J2NT = 32 * (J2CW + 1);
-template <int U, bool FIRST>
-__global__ void __launch_bounds__(J2NT, 1) k_gt2(const RItem* __restrict__ items, int B, double* __restrict__ part,
-                                               unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
-    extern __shared__ __align__(128) unsigned char jsm[];
-    unsigned long long t_start = 0;
-    if (g_loop_prof && threadIdx.x == 0) t_start = gtime();
-    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
-    __shared__ int2 tile_e[JNS], tile_c[JNS];
-    const RItem& it = items[0];
-    CgState* S = it.st;
-    const bool act = FIRST || S->active;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
-    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
-    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 16 * kJdsRows + 127) & ~(size_t)127;
-    auto stage = [&](int k) {
-        unsigned char* b = jsm + (size_t)k * stage_bytes;
-        JStage q;
-        q.r = (double*)b;
-        q.s = q.r + kJdsRows;
-        q.val = q.s + kJdsRows;
-        q.col = (uint8_t*)(q.val + maxe);
-        q.meta = q.col + 4 * (size_t)maxe;
-        return q;
-    };
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < JNS; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], JCW);  // the 16 slices of a tile
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    double v[3] = {0.0, 0.0, 0.0};
-    if (act) {
-        if (warp == J2CW) {
-            if (lane == 0) {
-                int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
-                const uint64_t pol = policy_evict_first();
-                for (int t = tb, i = 0; t < te; ++t, ++i) {
-                    const int k = i % JNS;
-                    const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];
-                    if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);
-                    const JStage q = stage(k);
-                    const int ne = e1 - e0, nc = c1 - c0;
-                    tile_e[k] = make_int2(e0, ne);
-                    tile_c[k] = make_int2(c0, nc);
-                    mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 16u * kJdsRows);
-                    bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
-                    bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
                     bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
                     if (ne) {
                         bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
@@ -1345,40 +953,38 @@ __global__ void __launch_bounds__(J2NT, 1) k_gt2(const RItem* __restrict__ items
                 }
             }
         } else {
+            // ---- consumers: warp = slice of the tile, lane = row (rows in descending length)
             const double* __restrict__ rg = it.r;
             double* __restrict__ wout = it.w;
-            const int nsl = (te - tb) * JCW;  // slices of this CTA
-            for (int sl = warp; sl < nsl; sl += J2CW) {
-                const int i = sl / JCW, ws = sl - i * JCW;  // tile (local index), slice in tile
+            const int rl = 32 * warp + lane;
+            for (int t = tb, i = 0; t < te; ++t, ++i) {
                 const int k = i % JNS;
                 mbar_wait(&full[k], (i / JNS) & 1);
                 const JStage q = stage(k);
-                const int t = tb + i;
-                const int rl = 32 * ws + lane;
                 const int row = t * kJdsRows + rl;
                 const int len = q.meta[rl];
-                const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + ws * kmax;
-                const double xi = q.r[rl], qi = q.s[rl];
-                const int L = __shfl_sync(0xffffffffu, len, 0);
-                const bool wide = tile_c[k].y > 2 * tile_e[k].y;
+                const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
+                const double xi = q.r[rl], qi = nrho ? q.s[rl] : 0.0;
+                const int L = __shfl_sync(0xffffffffu, len, 0);  // lane 0 holds the longest row
+                const bool wide = tile_c[k].y > 2 * tile_e[k].y;  // int32 columns in this tile
                 const int16_t* c16 = (const int16_t*)q.col;
                 const int32_t* c32 = (const int32_t*)q.col;
                 const double* rt = rg + (int64_t)t * kJdsRows;
                 double acc = 0.0;
-                for (int k0 = 0; k0 < L; k0 += U) {
-                    double vv[U], gv[U];
-                    int c[U];
+                for (int k0 = 0; k0 < L; k0 += 8) {
+                    double vv[8], gv[8];
+                    int c[8];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         const bool a = k0 + u < len;
                         const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
                         vv[u] = a ? q.val[idx] : 0.0;
                         c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
                     }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) gv[u] = rt[c[u]];
+                    for (int u = 0; u < 8; ++u) gv[u] = rt[c[u]];  // neighbours' r (L1/L2)
 #pragma unroll
-                    for (int u = 0; u < U; ++u) acc = fma(vv[u], gv[u], acc);
+                    for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[k]);
@@ -1395,7 +1001,7 @@ __global__ void __launch_bounds__(J2NT, 1) k_gt2(const RItem* __restrict__ items
     }
     const int it_prof = S->iters;
     if (g_loop_prof && act && it_prof < kLoopProfMax) {
-        __syncthreads();
+        __syncthreads();  // profiling only: every warp of the CTA is done
         if (threadIdx.x == 0) {
             const unsigned long long t = gtime();
             atomicMax(&g_loop_ts2[4 * it_prof], t_start);
@@ -1403,321 +1009,10 @@ __global__ void __launch_bounds__(J2NT, 1) k_gt2(const RItem* __restrict__ items
             atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
         }
     }
-    cg_tail<FIRST, false, J2NT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1);
+    cg_tail<FIRST, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1, it.dmin);
     if (g_loop_prof && act && !FIRST && threadIdx.x == 0) {
         if (it_prof < kLoopProfMax) atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());
         loop_stamp(1, it_prof, t_start);
-    }
-}
-
-// ------------------------------------------------------------------ persistent TMA solver
-// Large systems (C5): the WHOLE CG loop in one cooperative launch, one CTA per SM, each owning
-// the same contiguous range of kJdsRows-row tiles every iteration (rows R0..R1). The matrix part
-// of a tile (values, columns, lengths + diagonal offsets, q = D^1/2) does not change between
-// iterations, so the producer warp streams it through the JNS-stage TMA ring CONTINUOUSLY --
-// across the update phase and the grid barriers -- while the JCW consumer warps run
-//   S: w = r + A^_off r over the tiles (r of the own rows from L2, neighbours gathered), dots
-//   -- grid barrier fused with the reduction (fixed-order sum: identical scalars everywhere) --
-//   U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s   (own rows)
-//   -- grid barrier (r published) --
-// Consumers synchronise among themselves with named barrier 1 (the producer never joins).
-__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" ::"n"(JCW * 32) : "memory"); }
-
-// consumer-only grid barrier on the per-CTA epoch slots of it.part (optional partials)
-__device__ __forceinline__ void cgrid_sync(const RItem& it, int rank, unsigned long long epoch, const double4* t) {
-    cons_bar();
-    if (threadIdx.x == 0) {
-        double* P = it.part + 4 * rank;
-        if (t) {
-            P[0] = t->x;
-            P[1] = t->y;
-            P[2] = t->z;
-        }
-        __threadfence();
-        *(volatile unsigned long long*)(P + 3) = epoch;
-    }
-    for (int k = threadIdx.x; k < it.ncta; k += JCW * 32) {
-        volatile unsigned long long* E = (volatile unsigned long long*)(it.part + 4 * k + 3);
-        while (*E < epoch) {
-        }
-    }
-    __threadfence();
-    cons_bar();
-}
-
-__device__ __forceinline__ double4 cons_sum3(double4 v, double* sh /* [JCW][4] */) {
-    v.x = warp_sum_d(v.x);
-    v.y = warp_sum_d(v.y);
-    v.z = warp_sum_d(v.z);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    cons_bar();
-    if (lane == 0) {
-        sh[4 * wid] = v.x;
-        sh[4 * wid + 1] = v.y;
-        sh[4 * wid + 2] = v.z;
-    }
-    cons_bar();
-    double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
-#pragma unroll
-    for (int w = 0; w < JCW; ++w) {
-        t.x += sh[4 * w];
-        t.y += sh[4 * w + 1];
-        t.z += sh[4 * w + 2];
-    }
-    return t;
-}
-
-__global__ void __launch_bounds__(JNT, 1) k_pcgt(const RItem* __restrict__ items) {
-    extern __shared__ __align__(128) unsigned char jsm[];
-    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
-    __shared__ int2 tile_e[JNS], tile_c[JNS];
-    __shared__ double sh[4 * JCW];
-    __shared__ volatile int done_flag, pdone;
-    __shared__ volatile int issued;
-    const RItem& it = items[0];
-    CgState* S = it.st;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rank = blockIdx.x;
-    const int tb = it.jpart[rank], te = it.jpart[rank + 1], nt = te - tb;
-    const int n = it.n;
-    const int R0 = min(n, tb * kJdsRows), R1 = min(n, te * kJdsRows);
-    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
-    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 8 * kJdsRows + 127) & ~(size_t)127;
-    auto stage = [&](int k) {
-        unsigned char* b = jsm + (size_t)k * stage_bytes;
-        JStage q;
-        q.s = (double*)b;  // q = D^1/2
-        q.r = nullptr;
-        q.val = q.s + kJdsRows;
-        q.col = (uint8_t*)(q.val + maxe);
-        q.meta = q.col + 4 * (size_t)maxe;
-        return q;
-    };
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < JNS; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], JCW);
-        }
-        mbar_fence_init();
-        done_flag = 0;
-        pdone = 0;
-        issued = 0;
-    }
-    __syncthreads();
-    if (warp == JCW) {
-        // ---- producer: the CTA's tiles, cyclically, until the consumers are done
-        if (lane == 0 && nt > 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int i = 0;; ++i) {
-                const int k = i % JNS;
-                if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);  // the drain below releases it
-                if (done_flag) break;
-                const int t = tb + i % nt;
-                const JStage q = stage(k);
-                const int e0 = it.jeb[t], ne = it.jeb[t + 1] - e0;
-                const int c0 = it.jcb[t], nc = it.jcb[t + 1] - c0;
-                tile_e[k] = make_int2(e0, ne);
-                tile_c[k] = make_int2(c0, nc);
-                mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + 8u * kJdsRows);
-                bulk_g2s_hint(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k], pol);
-                bulk_g2s_hint(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k], pol);
-                if (ne) {
-                    bulk_g2s_hint(q.val, it.jval + e0, 8u * ne, &full[k], pol);
-                    bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
-                }
-                issued = i + 1;
-            }
-            __threadfence_block();
-            pdone = 1;
-        }
-        return;
-    }
-    // ---- consumers
-    const int tid = threadIdx.x;
-    double* __restrict__ r = it.r;
-    double* __restrict__ w = it.w;
-    double* __restrict__ p = it.p;
-    double* __restrict__ sv = it.sv;
-    double* __restrict__ x = it.x;
-    const double tol2 = S->tol2, bn2 = S->bn2;
-    const int max_iter = S->max_iter;
-    int iters = S->iters, status = FEMI_OK;
-    unsigned long long epoch = 0;
-    int cons = 0;  // stages consumed (ring position)
-    const int rl = 32 * warp + lane;
-    auto spmv = [&]() -> double4 {
-        double4 loc = make_double4(0.0, 0.0, 0.0, 0.0);
-        for (int j = 0; j < nt; ++j, ++cons) {
-            const int k = cons % JNS;
-            mbar_wait(&full[k], (cons / JNS) & 1);
-            const JStage q = stage(k);
-            const int t = tb + j;
-            const int row = t * kJdsRows + rl;
-            const int len = q.meta[rl];
-            const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
-            const double* rt = r + (int64_t)t * kJdsRows;
-            const double xi = row < n ? rt[rl] : 0.0;
-            const double qi = q.s[rl];
-            const int L = __shfl_sync(0xffffffffu, len, 0);
-            const bool wide = tile_c[k].y > 2 * tile_e[k].y;
-            const int16_t* c16 = (const int16_t*)q.col;
-            const int32_t* c32 = (const int32_t*)q.col;
-            double acc = 0.0;
-            for (int k0 = 0; k0 < L; k0 += 8) {
-                double vv[8], gv[8];
-                int c[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const bool a = k0 + u < len;
-                    const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
-                    vv[u] = a ? q.val[idx] : 0.0;
-                    c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) gv[u] = rt[c[u]];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[k]);
-            if (row < n) {
-                const double y = xi + acc;
-                w[row] = y;
-                const double ru = xi * qi;
-                loc.x += xi * xi;
-                loc.y += y * xi;
-                loc.z += ru * ru;
-            }
-        }
-        return loc;
-    };
-    auto reduce = [&](double4 loc) -> double4 {
-        const double4 t = cons_sum3(loc, sh);
-        ++epoch;
-        cgrid_sync(it, rank, epoch, &t);
-        double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
-        for (int k = tid; k < it.ncta; k += JCW * 32) {
-            const double* P = it.part + 4 * k;
-            a.x += __ldcg(P);
-            a.y += __ldcg(P + 1);
-            a.z += __ldcg(P + 2);
-        }
-        return cons_sum3(a, sh);
-    };
-    double4 tot = reduce(spmv());
-    double gam = tot.x, del = tot.y, rho = tot.z;
-    double alpha = 0.0, beta = 0.0;
-    bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho) && iters < max_iter;
-    if (!isfinite(gam) || !isfinite(bn2)) {
-        status = FEMI_E_NONFINITE;
-        run = false;
-    }
-    if (run) {
-        if (!(del > 0.0)) {
-            status = FEMI_E_NEG_CURVATURE;
-            run = false;
-        } else {
-            alpha = gam / del;
-        }
-    }
-    const bool prof = g_loop_prof && rank == 0 && tid == 0;
-    unsigned long long tp = prof ? gtime() : 0ull;
-    auto mark = [&](int k) {
-        if (prof) {
-            const unsigned long long t = gtime();
-            g_loop_ts[k] += t - tp;
-            tp = t;
-        }
-    };
-    constexpr int UB = 4;  // rows per thread with their loads in flight together
-    while (run) {
-        // U: own rows (row i handled by the thread that wrote w[i] in S: same mapping)
-        for (int b0 = R0 + tid; b0 < R1; b0 += UB * JCW * 32) {
-            double rv[UB], wv[UB], pv[UB], sv0[UB], xv[UB];
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-                const int i = b0 + u * JCW * 32;
-                if (i < R1) {
-                    rv[u] = r[i];
-                    wv[u] = w[i];
-                    pv[u] = p[i];
-                    sv0[u] = sv[i];
-                    xv[u] = x[i];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-                const int i = b0 + u * JCW * 32;
-                if (i < R1) {
-                    const double pi = fma(beta, pv[u], rv[u]), si = fma(beta, sv0[u], wv[u]);
-                    p[i] = pi;
-                    sv[i] = si;
-                    x[i] = fma(alpha, pi, xv[u]);
-                    r[i] = fma(-alpha, si, rv[u]);
-                }
-            }
-        }
-        ++iters;
-        mark(0);
-        ++epoch;
-        cgrid_sync(it, rank, epoch, nullptr);  // r published
-        mark(1);
-        const double4 lsp = spmv();
-        mark(2);
-        tot = reduce(lsp);
-        mark(3);
-        const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
-        if (!isfinite(gam2) || !isfinite(del2)) {
-            status = FEMI_E_NONFINITE;
-            break;
-        }
-        if (rho2 <= tol2) break;
-        if (iters >= max_iter) {
-            status = FEMI_E_NOT_CONVERGED;
-            break;
-        }
-        beta = gam2 / gam;
-        const double den = del2 - beta * gam2 / alpha;
-        if (!(den > 0.0)) {
-            status = FEMI_E_NEG_CURVATURE;
-            break;
-        }
-        alpha = gam2 / den;
-        gam = gam2;
-    }
-    if (rank == 0 && tid == 0) {
-        S->iters = iters;
-        S->status = status;
-    }
-    // drain the ring: consume every stage the producer issued, then let it stop
-    if (tid == 0) done_flag = 1;
-    cons_bar();
-    for (;;) {
-        const int iss = issued;
-        if (cons < iss) {
-            const int k = cons % JNS;
-            mbar_wait(&full[k], (cons / JNS) & 1);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[k]);
-            ++cons;
-        } else if (pdone && cons >= issued) {
-            break;
-        }
-    }
-}
-
-// rec[cur] = {r, 0, 0, 0} from the plain residual (start and restart of the recurrence)
-__global__ void k_pack(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    Rec* __restrict__ R = (Rec*)(it.st->par ? it.rec1 : it.rec0);
-    const double* __restrict__ r = it.r;  // plain residual (k_init_r / k_true_res)
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        Rec o;
-        o.r = r[i];
-        o.w = 0.0;
-        o.s = 0.0;
-        o.p = 0.0;
-        R[i] = o;
     }
 }
 
@@ -1738,11 +1033,8 @@ struct GraphCache {
     double* d_part = nullptr;
     cudaGraphExec_t main = nullptr, restart = nullptr;
     RItem item{};
-    int gs_blocks = 0, gx = 0, gp_blocks = 0;
-    int gt_blocks = 0;
-    unsigned gt_smem = 0;  // > 0: the body's SpMV is the TMA-streamed k_gt
-    unsigned pt_smem = 0;  // dynamic shared memory of the persistent k_pcgt
-    int gt_ver = 1, gt_u = 8;  // SpMV kernel: 1 = k_gt (16 consumer warps), 2 = k_gt2 (31, unroll gt_u)
+    int gs_blocks = 0, gx = 0, gt_blocks = 0;
+    unsigned gt_smem = 0;  // > 0: the SpMV is the TMA-streamed k_gt (JDS layout); else SELL k_gs
 };
 
 struct Workspace {
@@ -1754,8 +1046,6 @@ struct Workspace {
 };
 
 int g_smem_optin = -1;
-int g_fused = -1;    // graph mode body: 0 = k_gu + k_gt/k_gs (default), 1 = fused k_gp (FEMI_PCG_FUSED=1)
-int g_persist = -1;  // large systems: 0 = graph WHILE loop (default), 1 = persistent TMA solver k_pcgt
 int g_occ_grid = -1;
 int g_nsm = 0;
 bool g_timers = false;
@@ -1779,8 +1069,10 @@ femi_status add_kernel(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid
     return FEMI_OK;
 }
 
-// builds [prologue...] -> k_gp<true> -> WHILE{ k_gp<false> } -> finalize -> true_res -> copy_g
-// (FEMI_PCG_FUSED=0: k_gs<true> -> WHILE{ k_gu -> k_gs<false> } on plain vectors)
+// main:    reset -> minmax -> rhs -> init_x -> zero_ps -> init_r -> SpMV<FIRST> ->
+//          WHILE{ kUnroll x (k_gu -> SpMV) } -> finalize -> true_res -> copy_g
+// restart: zero_ps -> SpMV<FIRST> -> WHILE{...} -> finalize -> true_res -> copy_g
+// (SpMV = k_gt on the JDS tiles, or k_gs on the SELL slices when the JDS layout is absent)
 femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     cudaGraph_t gr;
     FEMI_CUDA(cudaGraphCreate(&gr, 0));
@@ -1800,12 +1092,17 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     const dim3 gk(C.gx, 1), bk(KNT);
     cudaGraphNode_t prev = nullptr, nd;
     cudaGraphNode_t* dep = nullptr;
-    auto chain = [&](void* fn, dim3 gg, dim3 bb, void** args) -> femi_status {
-        femi_status s = add_kernel(gr, dep, fn, gg, bb, args, &nd);
+    auto chain = [&](void* fn, dim3 gg, dim3 bb, void** args, unsigned smem = 0) -> femi_status {
+        femi_status s = add_kernel(gr, dep, fn, gg, bb, args, &nd, smem);
         prev = nd;
         dep = &prev;
         return s;
     };
+    const bool tma = C.gt_smem > 0;
+    void* spmv_first = tma ? (void*)k_gt<true> : (void*)k_gs<true>;
+    void* spmv = tma ? (void*)k_gt<false> : (void*)k_gs<false>;
+    const dim3 gsp(tma ? C.gt_blocks : C.gs_blocks), bsp(tma ? JNT : GNT);
+    const unsigned ssp = tma ? C.gt_smem : 0;
     femi_status s = FEMI_OK;
     if (!restart) {
         if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
@@ -1814,26 +1111,10 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_rhs, gk, bk, a_items))) return s;
         if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
     }
-    if (g_fused) {
-        if (!restart)
-            if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-        if ((s = chain((void*)k_pack, gk, bk, a_items))) return s;
-        if ((s = chain((void*)k_gp<true>, dim3(C.gp_blocks), dim3(GNT), a_gs))) return s;
-    } else {
-        if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
-        if (!restart)
-            if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-        if (C.gt_smem && C.gt_ver == 2)
-            s = add_kernel(gr, dep, C.gt_u == 8 ? (void*)k_gt2<8, true> : (void*)k_gt2<4, true>, dim3(C.gt_blocks),
-                           dim3(J2NT), a_gs, &nd, C.gt_smem);
-        else if (C.gt_smem)
-            s = add_kernel(gr, dep, (void*)k_gt<1, 0, true>, dim3(C.gt_blocks), dim3(JNT), a_gs, &nd, C.gt_smem);
-        else
-            s = add_kernel(gr, dep, (void*)k_gs<true>, dim3(C.gs_blocks), dim3(GNT), a_gs, &nd);
-        if (s) return s;
-        prev = nd;
-        dep = &prev;
-    }
+    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
+    if (!restart)
+        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+    if ((s = chain(spmv_first, gsp, bsp, a_gs, ssp))) return s;
     {
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
@@ -1843,35 +1124,14 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         FEMI_CUDA(cudaGraphAddNode(&nd, gr, dep, 1, &cp));
         prev = nd;
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaGraphNode_t u, sn;
-        if (!g_fused && C.gt_smem) {
-            // kUnroll iterations per body: the WHILE re-evaluation costs ~6 us, an iteration ~35;
-            // kernels after convergence return at once (S->active == 0)
-            cudaGraphNode_t prevb = nullptr;
-            for (int k = 0; k < kUnroll; ++k) {
-                if ((s = add_kernel(body, prevb ? &prevb : nullptr, (void*)k_gu,
-                                    dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT), a_items, &u)))
-                    return s;
-                if (C.gt_ver == 2)
-                    s = add_kernel(body, &u, C.gt_u == 8 ? (void*)k_gt2<8, false> : (void*)k_gt2<4, false>,
-                                   dim3(C.gt_blocks), dim3(J2NT), a_gs, &sn, C.gt_smem);
-                else
-                    s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem);
-                if (s) return s;
-                prevb = sn;
-            }
-        } else if (g_fused) {
-            if ((s = add_kernel(body, nullptr, (void*)k_gp<false>, dim3(C.gp_blocks), dim3(GNT), a_gs, &sn)))
-                return s;
-        } else {
-            if ((s = add_kernel(body, nullptr, (void*)k_gu, dim3(C.gx * 2 > 1184 ? 1184 : C.gx * 2), dim3(GNT),
-                                a_items, &u)))
-                return s;
-            if (C.gt_smem)
-                s = add_kernel(body, &u, (void*)k_gt<1, 0>, dim3(C.gt_blocks), dim3(JNT), a_gs, &sn, C.gt_smem);
-            else
-                s = add_kernel(body, &u, (void*)k_gs<false>, dim3(C.gs_blocks), dim3(GNT), a_gs, &sn);
-            if (s) return s;
+        // kUnroll iterations per body: the WHILE re-evaluation costs several us; kernels after
+        // convergence return at once (S->active == 0)
+        cudaGraphNode_t bprev = nullptr, u, sn;
+        const dim3 gu(std::min(C.gx * 2, 1184));
+        for (int k = 0; k < kUnroll; ++k) {
+            if ((s = add_kernel(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u))) return s;
+            if ((s = add_kernel(body, &u, spmv, gsp, bsp, a_gs, &sn, ssp))) return s;
+            bprev = sn;
         }
     }
     if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
@@ -1882,81 +1142,64 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     return FEMI_OK;
 }
 
-// Persistent TMA path: prologue kernels, ONE cooperative k_pcgt for the whole CG loop, epilogue.
-femi_status persist_solve(femi_system_s* S, GraphCache* C, RItem it, const femi_cg_opts& o, int32_t* iters,
-                          double* relres, cudaStream_t st, int64_t* total_iters) {
-    it.part = C->d_part;  // [gt_blocks][4] barrier/partial slots
-    it.ncta = C->gt_blocks;
-    FEMI_CUDA(cudaMemcpyAsync(C->d_items, &it, sizeof(RItem), cudaMemcpyHostToDevice, st));
-    RItem* di = C->d_items;
-    const dim3 gk(C->gx, 1), bk(KNT);
-    k_reset_items<<<1, 32, 0, st>>>(1, di);
-    k_minmax<<<296, 256, 0, st>>>(1, di);
-    k_rhs<<<gk, bk, 0, st>>>(di);
-    k_init_x<<<gk, bk, 0, st>>>(di);
-    k_zero_ps<<<gk, bk, 0, st>>>(di);
-    k_init_r<<<gk, bk, 0, st>>>(di, C->d_cnt);
-    count_launches(6);
-    CgState hs;
-    for (int restarts = 0;; ++restarts) {
-        if (restarts) {
-            k_zero_ps<<<gk, bk, 0, st>>>(di);
-            count_launches(1);
-        }
-        FEMI_CUDA(cudaMemsetAsync(C->d_part, 0, sizeof(double) * 4 * C->gt_blocks, st));
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        cfg.gridDim = dim3(C->gt_blocks);
-        cfg.blockDim = dim3(JNT);
-        cfg.dynamicSmemBytes = C->pt_smem;
-        cfg.stream = st;
-        attr[0].id = cudaLaunchAttributeCooperative;  // spin barriers: all CTAs co-resident
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        void* args[1] = {(void*)&di};
-        static const bool loop_prof = std::getenv("FEMI_LOOP_PROF") != nullptr;
-        if (loop_prof) {
-            unsigned long long z[4] = {0, 0, 0, 0};
-            const int on = 1;
-            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
-            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-        }
-        const cudaError_t e = cudaLaunchKernelExC(&cfg, (void*)k_pcgt, args);
-        if (e != cudaSuccess) return cuda_fail(e, "k_pcgt launch");
-        if (loop_prof) {
-            unsigned long long z[4];
-            const int off = 0;
-            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-            FEMI_CUDA(cudaMemcpyFromSymbolAsync(z, g_loop_ts, sizeof(z), 0, cudaMemcpyDeviceToHost, st));
-            CgState h2;
-            FEMI_CUDA(cudaMemcpyAsync(&h2, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
-            FEMI_CUDA(cudaStreamSynchronize(st));
-            const double ni = std::max(1, h2.iters);
-            std::fprintf(stderr, "[femi persist] %d iterations, per iteration us: U %.2f  barrier %.2f  S %.2f  reduce %.2f\n",
-                         h2.iters, z[0] / ni / 1e3, z[1] / ni / 1e3, z[2] / ni / 1e3, z[3] / ni / 1e3);
-        }
-        k_finalize<<<gk, bk, 0, st>>>(di);
-        k_true_res<<<gk, bk, 0, st>>>(di, C->d_cnt + 1);
-        count_launches(3);
-        FEMI_CUDA(cudaGetLastError());
-        FEMI_CUDA(cudaMemcpyAsync(&hs, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
-        FEMI_CUDA(cudaStreamSynchronize(st));
-        const bool fail = hs.bn2 > 0.0 && !(hs.res2 <= hs.tol2);
-        if (!(hs.status == FEMI_OK && hs.iters > 0 && hs.iters < hs.max_iter && fail) || restarts >= 8) break;
-        // k_true_res left r = s * r_true and x^ is current: the loop restarts from there
+// FEMI_LOOP_PROF=1: per-iteration timeline of the graph loop from %globaltimer stamps
+femi_status loop_prof_begin(cudaStream_t st) {
+    std::vector<unsigned long long> init(4 * kLoopProfMax);
+    for (int k = 0; k < kLoopProfMax; ++k) {
+        init[4 * k] = init[4 * k + 2] = ~0ull;
+        init[4 * k + 1] = init[4 * k + 3] = 0ull;
     }
-    k_copy_g<<<296, 256, 0, st>>>(di);
-    count_launches(1);
-    FEMI_CUDA(cudaGetLastError());
-    const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
-    if (iters) *iters = hs.iters;
-    if (relres) *relres = rel;
-    if (total_iters) *total_iters = hs.iters;
-    femi_status sb = (femi_status)hs.status;
-    if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
-    if (sb != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)sb) + ")");
-    return sb;
+    FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts, init.data(), sizeof(unsigned long long) * init.size(), 0,
+                                      cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < kLoopProfMax; ++k) {
+        init[4 * k] = 0ull;
+        init[4 * k + 1] = ~0ull;
+        init[4 * k + 2] = init[4 * k + 3] = 0ull;
+    }
+    FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts2, init.data(), sizeof(unsigned long long) * init.size(), 0,
+                                      cudaMemcpyHostToDevice, st));
+    const int on = 1;
+    FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    return FEMI_OK;
+}
+
+femi_status loop_prof_end(cudaStream_t st) {
+    const int off = 0;
+    std::vector<unsigned long long> ts(4 * kLoopProfMax), t2(4 * kLoopProfMax), t3(4 * kLoopProfMax);
+    FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    FEMI_CUDA(cudaMemcpyFromSymbolAsync(ts.data(), g_loop_ts, sizeof(unsigned long long) * ts.size(), 0,
+                                        cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaMemcpyFromSymbolAsync(t2.data(), g_loop_ts2, sizeof(unsigned long long) * t2.size(), 0,
+                                        cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaMemcpyFromSymbolAsync(t3.data(), g_tail_ts, sizeof(unsigned long long) * t3.size(), 0,
+                                        cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaStreamSynchronize(st));
+    double su = 0, sg = 0, g1 = 0, g2 = 0, c0 = 0, c1 = 0, c2 = 0, tA = 0, tB = 0;
+    int cnt = 0;
+    for (int k = 1; k + 1 < kLoopProfMax; ++k) {
+        const unsigned long long* a = &ts[4 * k];
+        const unsigned long long* nx = &ts[4 * (k + 1)];
+        if (a[1] == 0 || a[3] == 0 || nx[1] == 0) break;
+        su += (double)(a[1] - a[0]);
+        sg += (double)(a[3] - a[2]);
+        g1 += (double)a[2] - (double)a[1];
+        g2 += (double)nx[0] - (double)a[3];
+        c0 += (double)t2[4 * k + 1] - (double)a[2];
+        c1 += (double)t2[4 * k + 2] - (double)a[2];
+        c2 += (double)t2[4 * k + 3] - (double)a[2];
+        tA += (double)t3[4 * k] - (double)a[2];
+        tB += (double)t3[4 * k + 1] - (double)a[2];
+        ++cnt;
+    }
+    if (cnt)
+        std::fprintf(stderr,
+                     "[femi loop] %d iterations: k_gu span %.2f us, gap %.2f, SpMV span %.2f us, gap %.2f -> %.2f "
+                     "us/iteration | SpMV from first CTA start: first CTA done +%.2f, last CTA done +%.2f, last CTA "
+                     "arrival +%.2f, partials summed +%.2f, last CTA out +%.2f\n",
+                     cnt, su / cnt / 1e3, g1 / cnt / 1e3, sg / cnt / 1e3, g2 / cnt / 1e3,
+                     (su + sg + g1 + g2) / cnt / 1e3, c0 / cnt / 1e3, c1 / cnt / 1e3, tA / cnt / 1e3, tB / cnt / 1e3,
+                     c2 / cnt / 1e3);
+    return FEMI_OK;
 }
 
 femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, double* u_vert,
@@ -1964,14 +1207,6 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                         int64_t* total_iters) {
     GraphCache* C = (GraphCache*)S->scratch;
     const int64_t n = S->n_u;
-    if (g_fused < 0) {
-        const char* fz = std::getenv("FEMI_PCG_FUSED");  // measured: fused 69 us vs 17 + 43 us (C5)
-        g_fused = (fz && fz[0] == '1') ? 1 : 0;
-        // measured at C5: graph WHILE loop (k_gu + k_gt, 4 per body) 42 us/iteration, persistent
-        // k_pcgt 49 us/iteration -> the graph is the default; FEMI_PCG_PERSIST=1 selects k_pcgt
-        const char* pg = std::getenv("FEMI_PCG_PERSIST");
-        g_persist = (pg && pg[0] == '1') ? 1 : 0;
-    }
     if (!C) {
         C = new GraphCache();
         const int nsl = (int)((n + 31) / 32);
@@ -1981,14 +1216,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                                                                    148 * 8));
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t vb = al(sizeof(double) * std::max<int64_t>(n + 1, (int64_t)S->jds_ntile * kJdsRows));
-        {
-            int per_sm = 0, nsm = 0, dev = 0;
-            FEMI_CUDA(cudaGetDevice(&dev));
-            FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gp<false>, GNT, 0));
-            C->gp_blocks = (int)std::max<int64_t>(
-                1, std::min<int64_t>((nsl + 2 * (GNT / 32) - 1) / (2 * (GNT / 32)), (int64_t)std::max(1, per_sm) * nsm));
-        }
+        std::vector<int32_t> jpart;
         if (S->jds_ntile > 0 && std::getenv("FEMI_PCG_NOTMA") == nullptr) {
             const size_t stage_bytes =
                 ((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 16 * kJdsRows + 127) & ~(size_t)127;
@@ -1996,46 +1224,22 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             FEMI_CUDA(cudaGetDevice(&dev));
             FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
             FEMI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-            if (std::getenv("FEMI_DEBUG"))
-                std::fprintf(stderr, "[femi] k_gt: stage %zu B x %d, optin %d\n", stage_bytes, JNS, optin);
-            if (JNS * stage_bytes + 1024 <= (size_t)optin) {
+            if (JNS * stage_bytes + 4096 <= (size_t)optin) {
                 C->gt_smem = (unsigned)(JNS * stage_bytes);
-                if (const char* gv = std::getenv("FEMI_GT")) C->gt_ver = std::atoi(gv) == 2 ? 2 : 1;
-                if (const char* gu = std::getenv("FEMI_GT_U")) C->gt_u = std::atoi(gu) == 4 ? 4 : 8;
-                C->pt_smem = (unsigned)(JNS * (((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 8 * kJdsRows + 127) &
-                                               ~(size_t)127));
-                FEMI_CUDA(cudaFuncSetAttribute(k_pcgt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->pt_smem));
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
-                for (const void* fn : {(const void*)k_gt<0, 0>, (const void*)k_gt<2, 0>, (const void*)k_gt<1, 1>,
-                                       (const void*)k_gt<1, 2>, (const void*)k_gt<1, 0>, (const void*)k_gt<1, 0, true>,
-                                       (const void*)k_gt<1, 3>,
-                                       (const void*)k_gt2<4, true>, (const void*)k_gt2<4, false>,
-                                       (const void*)k_gt2<8, true>, (const void*)k_gt2<8, false>})
+                for (const void* fn : {(const void*)k_gt<false>, (const void*)k_gt<true>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
+                // tiles -> CTAs: equal contiguous ranges (measured better than byte-weighted ranges
+                // and than dynamic scheduling, which loses gather locality)
+                const int nt = S->jds_ntile;
+                jpart.resize(C->gt_blocks + 1);
+                for (int b = 0; b <= C->gt_blocks; ++b) jpart[b] = (int)((int64_t)nt * b / C->gt_blocks);
             }
         }
-        // tiles -> k_gt CTAs: contiguous ranges of equal streamed + gathered bytes
-        std::vector<int32_t> jpart;
-        if (C->gt_smem) {
-            const int nt = S->jds_ntile;
-            std::vector<int32_t> eb(nt + 1);
-            FEMI_CUDA(cudaMemcpy(eb.data(), S->jds_eb, sizeof(int32_t) * (nt + 1), cudaMemcpyDeviceToHost));
-            std::vector<double> cum(nt + 1, 0.0);
-            double wa = 0.0;  // bytes-per-entry weight of the balance (0: equal tile counts)
-            if (const char* e = std::getenv("FEMI_JPART_W")) wa = std::atof(e);
-            for (int t = 0; t < nt; ++t) cum[t + 1] = cum[t] + wa * (eb[t + 1] - eb[t]) + 24.0 * kJdsRows;
-            jpart.resize(C->gt_blocks + 1);
-            for (int b = 0, t = 0; b <= C->gt_blocks; ++b) {
-                const double target = cum[nt] * b / C->gt_blocks;
-                while (t < nt && cum[t] < target) ++t;
-                jpart[b] = t;
-            }
-            jpart[C->gt_blocks] = nt;
-        }
-        const int pb = std::max(std::max(C->gs_blocks, C->gp_blocks), C->gt_blocks);
-        const size_t rb = al(sizeof(Rec) * (n + 1));
-        const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) + al(sizeof(unsigned) * 4) +
-                             al(sizeof(double) * 4 * pb) + al(sizeof(double) * C->gx) + 6 * vb + 2 * rb;
+        const int pb = std::max(C->gs_blocks, C->gt_blocks);
+        const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) +
+                             al(sizeof(unsigned) * 4) + al(sizeof(double) * 4 * pb) + al(sizeof(double) * C->gx) +
+                             6 * vb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
         char* cur = (char*)C->ws;
         auto take = [&](size_t x) {
@@ -2058,8 +1262,6 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.w = (double*)take(vb);
         it.p = (double*)take(vb);
         it.sv = (double*)take(vb);
-        it.rec0 = (double*)take(rb);
-        it.rec1 = (double*)take(rb);
         it.jval = S->jds_val;
         it.jcol = S->jds_col;
         it.jmeta = S->jds_meta;
@@ -2069,9 +1271,9 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.jmaxe = S->jds_maxe;
         it.jkmax = S->jds_kmax;
         it.jmbytes = S->jds_meta_bytes;
-        it.jpol = 1;
         it.jpart = d_jpart;
-        {
+        it.dmin = 0.0;
+        if (n > 0) {  // dmin = min_i diag(A_uu)_i, for skipping the residual monitor far from rtol
             unsigned long long* d_m = nullptr;
             unsigned long long h_m = ~0ull;
             FEMI_CUDA(cudaMalloc(&d_m, sizeof(unsigned long long)));
@@ -2081,10 +1283,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             FEMI_CUDA(cudaFree(d_m));
             double dm;
             std::memcpy(&dm, &h_m, sizeof(dm));
-            it.dmin = (n > 0 && std::isfinite(dm) && dm > 0.0) ? dm * (1.0 - 1e-12) : 0.0;
-            if (std::getenv("FEMI_NO_RHO_SKIP")) it.dmin = 0.0;  // experiments: monitor every iteration
+            if (std::isfinite(dm) && dm > 0.0) it.dmin = dm * (1.0 - 1e-12);
         }
-        if (const char* pe = std::getenv("FEMI_JDS_POLICY")) it.jpol = std::atoi(pe);
         it.inv = S->sell_inv;
         it.len = S->sell_len;
         it.base = S->sell_base;
@@ -2119,82 +1319,18 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     it.x0mode = (g == nullptr && o.x0 == 1) ? 0 : o.x0;
     it.rtol = o.rtol;
     it.max_iter = o.max_iter;
-    if (C->gt_smem && g_persist)
-        return persist_solve(S, C, it, o, iters, relres, st, total_iters);
     FEMI_CUDA(cudaMemcpyAsync(C->d_items, &it, sizeof(RItem), cudaMemcpyHostToDevice, st));
     static const bool loop_prof = std::getenv("FEMI_LOOP_PROF") != nullptr;
     if (loop_prof) {
-        std::vector<unsigned long long> init(4 * kLoopProfMax);
-        for (int k = 0; k < kLoopProfMax; ++k) {
-            init[4 * k] = init[4 * k + 2] = ~0ull;
-            init[4 * k + 1] = init[4 * k + 3] = 0ull;
-        }
-        const int on = 1;
-        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts, init.data(), sizeof(unsigned long long) * init.size(), 0,
-                                          cudaMemcpyHostToDevice, st));
-        for (int k = 0; k < kLoopProfMax; ++k) {
-            init[4 * k] = 0ull;
-            init[4 * k + 1] = ~0ull;
-            init[4 * k + 2] = 0ull;
-            init[4 * k + 3] = 0ull;
-        }
-        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_ts2, init.data(), sizeof(unsigned long long) * init.size(), 0,
-                                          cudaMemcpyHostToDevice, st));
-        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        const femi_status ps = loop_prof_begin(st);
+        if (ps != FEMI_OK) return ps;
     }
     FEMI_CUDA(cudaGraphLaunch(C->main, st));
     if (loop_prof) {
-        const int off = 0;
-        std::vector<unsigned long long> ts(4 * kLoopProfMax);
-        FEMI_CUDA(cudaMemcpyToSymbolAsync(g_loop_prof, &off, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-        FEMI_CUDA(cudaMemcpyFromSymbolAsync(ts.data(), g_loop_ts, sizeof(unsigned long long) * ts.size(), 0,
-                                            cudaMemcpyDeviceToHost, st));
-        std::vector<unsigned long long> t3(4 * kLoopProfMax);
-        FEMI_CUDA(cudaMemcpyFromSymbolAsync(t3.data(), g_tail_ts, sizeof(unsigned long long) * t3.size(), 0,
-                                            cudaMemcpyDeviceToHost, st));
-        std::vector<unsigned long long> t2(4 * kLoopProfMax);
-        FEMI_CUDA(cudaMemcpyFromSymbolAsync(t2.data(), g_loop_ts2, sizeof(unsigned long long) * t2.size(), 0,
-                                            cudaMemcpyDeviceToHost, st));
-        FEMI_CUDA(cudaStreamSynchronize(st));
-        double su = 0, sg = 0, g1 = 0, g2 = 0, st_skew = 0, end0 = 0, end1 = 0, end2 = 0, tA = 0, tB = 0, tC = 0,
-               tD = 0;
-        int cnt = 0;
-        for (int k = 1; k + 1 < kLoopProfMax; ++k) {
-            const unsigned long long* a = &ts[4 * k];
-            const unsigned long long* nx = &ts[4 * (k + 1)];
-            if (a[1] == 0 || a[3] == 0 || nx[1] == 0) break;
-            su += (double)(a[1] - a[0]);
-            sg += (double)(a[3] - a[2]);
-            g1 += (double)a[2] - (double)a[1];
-            g2 += (double)nx[0] - (double)a[3];
-            st_skew += (double)t2[4 * k] - (double)a[2];
-            end0 += (double)t2[4 * k + 1] - (double)a[2];
-            end1 += (double)t2[4 * k + 2] - (double)a[2];
-            end2 += (double)t2[4 * k + 3] - (double)a[2];
-            tA += (double)t3[4 * k] - (double)a[2];
-            tB += (double)t3[4 * k + 1] - (double)a[2];
-            tC += (double)t3[4 * k + 2] - (double)a[2];
-            tD += (double)t3[4 * k + 3] - (double)a[2];
-            ++cnt;
-        }
-        if (cnt)
-            std::fprintf(stderr,
-                         "[femi loop] %d iterations: k_gu span %.2f us, gap %.2f, k_gt span %.2f us (to tail end), gap "
-                         "%.2f -> %.2f us/iteration\n",
-                         cnt, su / cnt / 1e3, g1 / cnt / 1e3, sg / cnt / 1e3, g2 / cnt / 1e3,
-                         (su + sg + g1 + g2) / cnt / 1e3);
-        if (cnt)
-            std::fprintf(stderr,
-                         "[femi loop] k_gt from first CTA start: last CTA start +%.2f us, first CTA done +%.2f, "
-                         "last CTA done +%.2f, last CTA out of the tail +%.2f, kernel end +%.2f\n",
-                         st_skew / cnt / 1e3, end0 / cnt / 1e3, end1 / cnt / 1e3, end2 / cnt / 1e3, sg / cnt / 1e3);
-        if (cnt)
-            std::fprintf(stderr,
-                         "[femi loop] k_gt tail: last CTA arrival +%.2f, last CTA has partials +%.2f, scalars +%.2f, "
-                         "condition set +%.2f\n",
-                         tA / cnt / 1e3, tB / cnt / 1e3, tC / cnt / 1e3, tD / cnt / 1e3);
+        const femi_status ps = loop_prof_end(st);
+        if (ps != FEMI_OK) return ps;
     }
-    count_launches(11);
+    count_launches(10);
     CgState hs;
     for (int restarts = 0;; ++restarts) {
         FEMI_CUDA(cudaMemcpyAsync(&hs, C->d_state, sizeof(CgState), cudaMemcpyDeviceToHost, st));
@@ -2204,172 +1340,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         FEMI_CUDA(cudaGraphLaunch(C->restart, st));  // from the current iterate (r = s * r_true)
         count_launches(6);
     }
-    count_launches((g_fused ? 1 : 2) * (int64_t)hs.iters);
-    if (std::getenv("FEMI_PCG_PROLOG")) {  // experiments: prologue/epilogue kernels standalone
-        cudaEvent_t ev[10];
-        for (auto& e : ev) cudaEventCreate(&e);
-        RItem* di = C->d_items;
-        const dim3 gk(C->gx, 1), bk(KNT);
-        unsigned* gcnt = C->d_cnt + 2;
-        cudaGraphConditionalHandle hdl = 0;
-        int one = 1;
-        cudaEventRecord(ev[0], st);
-        k_reset_items<<<1, 32, 0, st>>>(one, di);
-        cudaEventRecord(ev[1], st);
-        k_minmax<<<296, 256, 0, st>>>(one, di);
-        cudaEventRecord(ev[2], st);
-        k_rhs<<<gk, bk, 0, st>>>(di);
-        cudaEventRecord(ev[3], st);
-        k_init_x<<<gk, bk, 0, st>>>(di);
-        cudaEventRecord(ev[4], st);
-        k_zero_ps<<<gk, bk, 0, st>>>(di);
-        k_init_r<<<gk, bk, 0, st>>>(di, C->d_cnt);
-        cudaEventRecord(ev[5], st);
-        k_gs<true><<<dim3(C->gs_blocks), GNT, 0, st>>>(di, 1, C->d_part, gcnt, hdl);
-        cudaEventRecord(ev[6], st);
-        k_finalize<<<gk, bk, 0, st>>>(di);
-        cudaEventRecord(ev[7], st);
-        k_true_res<<<gk, bk, 0, st>>>(di, C->d_cnt + 1);
-        cudaEventRecord(ev[8], st);
-        k_copy_g<<<296, 256, 0, st>>>(di);
-        cudaEventRecord(ev[9], st);
-        cudaEventSynchronize(ev[9]);
-        float t[9];
-        for (int k = 0; k < 9; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
-        std::fprintf(stderr,
-                     "[femi prolog] us: reset %.1f minmax %.1f rhs %.1f init_x %.1f zero+init_r %.1f first-spmv %.1f "
-                     "finalize %.1f true_res %.1f copy_g %.1f\n",
-                     1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3], 1e3 * t[4], 1e3 * t[5], 1e3 * t[6], 1e3 * t[7],
-                     1e3 * t[8]);
-        for (auto& e : ev) cudaEventDestroy(e);
-        // restore the solve's state (the standalone launches above re-ran the prologue)
-        FEMI_CUDA(cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
-        FEMI_CUDA(cudaStreamSynchronize(st));
-    }
-    if (const char* mb = std::getenv("FEMI_PCG_KBENCH")) {  // experiments: body kernels standalone
-        (void)mb;
-        cudaEvent_t e0, e1, e2;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventCreate(&e2);
-        CgState act = hs;
-        act.active = 1;
-        act.alpha = 0.0;  // keeps the iterate unchanged
-        act.beta = 0.0;
-        unsigned* gcnt = C->d_cnt + 2;
-        cudaGraphConditionalHandle hdl = 0;
-        cudaEvent_t e3;
-        cudaEventCreate(&e3);
-        float tu = 0, ts = 0, tf = 0;
-        const int reps = 20;
-        const int gu = C->gx * 2 > 1184 ? 1184 : C->gx * 2;
-        for (int k = 0; k < reps; ++k) {
-            act.par = 0;
-            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
-            cudaEventRecord(e3, st);
-            k_gp<false><<<dim3(C->gp_blocks), GNT, 0, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
-            cudaEventRecord(e0, st);
-            cudaEventSynchronize(e0);
-            float c;
-            cudaEventElapsedTime(&c, e3, e0);
-            if (k > 1) tf += c;
-        }
-        for (int k = 0; k < reps; ++k) {
-            act.par = 0;
-            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
-            cudaEventRecord(e0, st);
-            k_gu<<<dim3(gu), GNT, 0, st>>>(C->d_items);
-            cudaEventRecord(e1, st);
-            k_gs<false><<<dim3(C->gs_blocks), GNT, 0, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
-            cudaEventRecord(e2, st);
-            cudaEventSynchronize(e2);
-            float a, b;
-            cudaEventElapsedTime(&a, e0, e1);
-            cudaEventElapsedTime(&b, e1, e2);
-            if (k > 1) {
-                tu += a;
-                ts += b;
-            }
-        }
-        float tt[5] = {0, 0, 0, 0, 0};
-        void (*const gts[5])(const RItem*, int, double*, unsigned*, cudaGraphConditionalHandle) = {
-            k_gt<1, 0>, k_gt<0, 0>, k_gt<1, 1>, k_gt<1, 2>, k_gt<1, 3>};
-        if (C->gt_smem)
-            for (int v = 0; v < 5; ++v)
-                for (int k = 0; k < reps; ++k) {
-                    act.par = 0;
-                    cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
-                    k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);  // r in L2, as in the loop
-                    cudaEventRecord(e0, st);
-                    gts[v]<<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
-                    cudaEventRecord(e1, st);
-                    cudaEventSynchronize(e1);
-                    float a;
-                    cudaEventElapsedTime(&a, e0, e1);
-                    if (k > 1) tt[v] += a;
-                }
-        if (C->gt_smem) {  // back-to-back k_gt launches (steady state without the first-launch cost)
-            act.par = 0;
-            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
-            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
-            cudaEventRecord(e0, st);
-            for (int k = 0; k < 8; ++k)
-                k_gt<1, 0><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
-            cudaEventRecord(e1, st);
-            for (int k = 0; k < 8; ++k) k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
-            cudaEventRecord(e2, st);
-            cudaEventSynchronize(e2);
-            float a, b;
-            cudaEventElapsedTime(&a, e0, e1);
-            cudaEventElapsedTime(&b, e1, e2);
-            std::fprintf(stderr, "[femi kbench] back-to-back: k_gt %.2f us, k_gu %.2f us per launch\n", 1e3 * a / 8,
-                         1e3 * b / 8);
-        }
-        if (C->gt_smem) {  // per-CTA busy time of one k_gt<1,0> launch
-            int on = 1;
-            cudaMemcpyToSymbolAsync(g_gt_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-            act.par = 0;
-            cudaMemcpyAsync(C->d_state, &act, sizeof(CgState), cudaMemcpyHostToDevice, st);
-            k_gu<<<dim3(C->gx * 2 > 1184 ? 1184 : C->gx * 2), GNT, 0, st>>>(C->d_items);
-            k_gt<1, 0><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt, hdl);
-            on = 0;
-            cudaMemcpyToSymbolAsync(g_gt_prof, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-            std::vector<unsigned long long> tm(2 * C->gt_blocks);
-            cudaMemcpyFromSymbolAsync(tm.data(), g_gt_times, sizeof(unsigned long long) * tm.size(), 0,
-                                      cudaMemcpyDeviceToHost, st);
-            cudaStreamSynchronize(st);
-            unsigned long long t0 = ~0ull, t1 = 0;
-            double mn = 1e30, mx = 0, sm = 0;
-            for (int b = 0; b < C->gt_blocks; ++b) {
-                t0 = std::min(t0, tm[2 * b]);
-                t1 = std::max(t1, tm[2 * b + 1]);
-                const double d = (double)(tm[2 * b + 1] - tm[2 * b]);
-                mn = std::min(mn, d);
-                mx = std::max(mx, d);
-                sm += d;
-            }
-            unsigned long long s0 = 0, s1 = 0;
-            for (int b = 0; b < C->gt_blocks; ++b) {
-                s0 = std::max(s0, tm[2 * b] - t0);
-                s1 = std::max(s1, t1 - tm[2 * b + 1]);
-            }
-            std::fprintf(stderr,
-                         "[femi kbench] k_gt per-CTA busy us: min %.2f mean %.2f max %.2f; span %.2f; latest start "
-                         "+%.2f; earliest end -%.2f\n",
-                         mn / 1e3, sm / C->gt_blocks / 1e3, mx / 1e3, (t1 - t0) / 1e3, s0 / 1e3, s1 / 1e3);
-        }
-        std::fprintf(stderr,
-                     "[femi kbench] k_gt (TMA, grid %d, smem %u): JP1 %.2f us  pipelined %.2f us  smem-gather %.2f us  "
-                     "no-gather %.2f us  stream-only %.2f us\n",
-                     C->gt_blocks, C->gt_smem, 1e3 * tt[0] / (reps - 2), 1e3 * tt[1] / (reps - 2),
-                     1e3 * tt[2] / (reps - 2), 1e3 * tt[3] / (reps - 2), 1e3 * tt[4] / (reps - 2));
-        std::fprintf(stderr, "[femi kbench] k_gu %.2f us  k_gs %.2f us (grids %d / %d)  fused k_gp %.2f us (grid %d)\n",
-                     1e3 * tu / (reps - 2), 1e3 * ts / (reps - 2), gu, C->gs_blocks, 1e3 * tf / (reps - 2),
-                     C->gp_blocks);
-        cudaEventDestroy(e3);
-        cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st);
-        cudaStreamSynchronize(st);
-    }
+    // the body runs whole unrolled groups: kernels after convergence exit at once but still launch
+    count_launches(2 * (int64_t)((hs.iters + kUnroll - 1) / kUnroll) * kUnroll);
     const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
     if (iters) *iters = hs.iters;
     if (relres) *relres = rel;

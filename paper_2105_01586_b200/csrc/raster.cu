@@ -210,12 +210,12 @@ constexpr int RCH = 128;  // list entries per warp chunk (4 x 32 lanes)
 //   order: tri_err += e, best = first strict maximum over non-vertex pixels (ties: lowest
 //   pix) -- the oracle's sequential order, so tri_err and best are bit-identical to it.
 // SSE = sum of per-group partials in group order (k_sse). Deterministic, no atomics on values.
-template <int MINB>
+template <int MINB, int CH>
 __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ gpart,
                                                    uint32_t* __restrict__ next, int64_t gstride) {
     __shared__ RTri tris[RWARPS][32];
-    __shared__ double e_s[RWARPS][RCH];
-    __shared__ int p_s[RWARPS][RCH];  // pix, or -1 for a vertex pixel (not a candidate)
+    __shared__ double e_s[RWARPS][CH];
+    __shared__ int p_s[RWARPS][CH];  // pix, or -1 for a vertex pixel (not a candidate)
     const RasterItem& it = items[blockIdx.y];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t T = it.T;
@@ -265,16 +265,27 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
         double acc = 0.0, be = -1.0;
         int bp = -1;
         const int my0 = lw.excl, my1 = lw.excl + cnt;
-        for (int c0 = 0; c0 < lw.total; c0 += RCH) {
-            // ---- phase 1: lane per entry
+        // list entries of the next 128-entry block are loaded one block ahead (their latency
+        // overlaps the current block's f gathers and arithmetic)
+        uint32_t vn[RCH / 32];
+#pragma unroll
+        for (int h = 0; h < RCH / 32; ++h) {
+            const int k = 32 * h + lane;
+            vn[h] = k < lw.total ? tp_pix[lw.ptr0 + k] : 0u;
+        }
+        for (int c0 = 0; c0 < lw.total; c0 += CH) {
+          // ---- phase 1: lane per entry, 128 entries at a time (loads in flight together)
+          for (int c1 = c0; c1 < min(lw.total, c0 + CH); c1 += RCH) {
             uint32_t v[RCH / 32];
             int j[RCH / 32];
             double fv[RCH / 32];
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
-                const int k = c0 + 32 * h + lane;
+                const int k = c1 + 32 * h + lane;
                 j[h] = warp_find(lw.excl, k, lw.total);
-                v[h] = j[h] < 32 ? tp_pix[lw.ptr0 + k] : 0u;
+                v[h] = vn[h];
+                const int kn = k + RCH;
+                vn[h] = kn < lw.total ? tp_pix[lw.ptr0 + kn] : 0u;
             }
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h)
@@ -300,14 +311,15 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
                     const double d = __dsub_rn(u, fv[h]);
                     const double e = __dmul_rn(d, d);
                     if (e_px) e_px[pix] = e;
-                    es[32 * h + lane] = e;
-                    ps[32 * h + lane] = cls ? -1 : pix;
+                    es[c1 - c0 + 32 * h + lane] = e;
+                    ps[c1 - c0 + 32 * h + lane] = cls ? -1 : pix;
                 }
             }
+          }
             __syncwarp();
             // ---- phase 2: lane per triangle, pixel order
             if (f) {
-                const int lo = max(my0, c0), hi = min(my1, c0 + RCH);
+                const int lo = max(my0, c0), hi = min(my1, c0 + CH);
                 for (int k = lo; k < hi; ++k) {
                     const double e = es[k - c0];
                     acc = __dadd_rn(acc, e);
@@ -509,7 +521,7 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per, minb == 4 ? (const void*)k_raster_tri<4> : (const void*)k_raster_tri<1>, RT, 0));
+            &per, minb == 4 ? (const void*)k_raster_tri<4, 128> : (const void*)k_raster_tri<1, 128>, RT, 0));
         resident = std::max(1, per) * nsm;
     }
     // one wave of resident CTAs; 32-triangle groups handed out dynamically in canonical order
@@ -531,8 +543,14 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
     uint32_t* d_cnt = (uint32_t*)((char*)d_part + al(bytes_part));
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
-    if (minb == 4) k_raster_tri<4><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
-    else k_raster_tri<1><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    static int ch = -1;  // staging chunk of the per-triangle pass (FEMI_RASTER_CH: 128, 256)
+    if (ch < 0) {
+        const char* e = std::getenv("FEMI_RASTER_CH");
+        ch = e ? std::atoi(e) : 256;
+    }
+    if (minb == 4 && ch == 256) k_raster_tri<4, 256><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    else if (minb == 4) k_raster_tri<4, 128><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    else k_raster_tri<1, 128><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
     k_sse<<<dim3(SSEB, B), RT, 0, st>>>(d_items, d_gpart, groups, d_part, d_cnt + B);
     count_launches(1);
     count_launches(1);
