@@ -327,6 +327,8 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         S->sell_nnz = ent;
         U(upload(S, &S->sell_len, len, st));
         U(upload(S, &S->sell_base, base, st));
+        S->sell_base_h = base;
+        S->sell_base_h.push_back((int32_t)ent);  // [nslices] = total entries
         U(upload(S, &S->sell_inv, pi, st));
         U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
         // padded to whole JDS tiles: the TMA tiles read s_int in kJdsRows blocks

@@ -108,6 +108,7 @@ struct femi_system_s {
     int32_t* sell_perm = nullptr;  // 32*nslices: natural row of each slice lane, -1 = padding
     int32_t* sell_len = nullptr;   // nslices: entries per lane
     int32_t* sell_base = nullptr;  // nslices: first entry
+    std::vector<int32_t> sell_base_h;  // host copy (sizes the on-chip resident solver)
     int32_t* sell_cbase = nullptr; // nslices: first row of the slice's window (int16 column base)
     double* sell_val = nullptr;
     int16_t* sell_c16 = nullptr;   // column - window_row0 (when the bandwidth allows)

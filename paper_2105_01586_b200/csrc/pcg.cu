@@ -28,6 +28,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "device.cuh"
 #include "tma.cuh"
 
@@ -596,6 +598,257 @@ __global__ void __launch_bounds__(NT, MINB)
         S->iters = iters;
         S->status = status;
     }
+}
+
+// ------------------------------------------------------------------ on-chip resident CG
+// Small and medium systems (C1-C4, C2's 32 meshes): the whole CG loop in one launch with NO
+// global-memory traffic per iteration. One cluster of C <= 16 CTAs per system (C = 1: a
+// single CTA); CTA k owns rows [R0, R1) (whole 64-row windows). At entry the CTA copies its
+// SELL slices into shared memory, with every column pre-resolved to (owner CTA, local row);
+// each warp owns fixed slices, so a lane keeps x, p, s, w (and q) of its <= RPL rows in
+// registers; only r is published, in the owner's shared memory, and neighbours read it
+// there -- locally or through distributed shared memory (DSMEM) across the cluster. Per
+// iteration: U in registers, r -> smem, cluster barrier, SpMV from smem/DSMEM, partial dots
+// written into every CTA's slot array (DSMEM), cluster barrier, fixed-order sums (identical
+// scalars in every CTA: deterministic).
+constexpr int RZT = 512;           // threads per CTA
+constexpr int RZW = RZT / 32;      // warps
+constexpr int RPL = 6;             // rows per lane (slices per warp) kept in registers
+
+template <bool CL>
+__device__ __forceinline__ void rz_sync() {
+    if constexpr (CL)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    else
+        __syncthreads();
+}
+
+template <bool CL>
+__global__ void __launch_bounds__(RZT, 1) k_cgr(const RItem* __restrict__ items) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) unsigned char rzm[];
+    __shared__ RItem its;
+    __shared__ double part_s[16][4];  // partial dots of every CTA of the cluster (DSMEM-written)
+    __shared__ double sh[4 * RZW];
+    __shared__ double bc[4];
+    int item = blockIdx.x, rank = 0;
+    if constexpr (CL) {
+        unsigned cr, cid;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+        asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        item = (int)cid;
+        rank = (int)cr;
+    }
+    if (threadIdx.x == 0) its = items[item];
+    __syncthreads();
+    const RItem& it = its;
+    CgState* S = it.st;
+    const int C = it.ncta;
+    const int n = it.n, nwin = it.nwin;
+    auto row0 = [&](int k) { return min(n, (int)((long long)nwin * k / C) * SIG); };
+    const int R0 = row0(rank), R1 = row0(rank + 1);
+    const int S0 = R0 / 32, S1 = (R1 + 31) / 32, nsl = S1 - S0;
+    const int e0 = nsl > 0 ? it.base[S0] : 0;
+    const int ne = nsl > 0 ? (S1 < (n + 31) / 32 ? it.base[S1] : it.base[S1 - 1] + 32 * it.len[S1 - 1]) - e0 : 0;
+    // shared memory: r | q (one slot per slice lane) | values | (owner << 16 | local row) codes | len | base
+    double* r_s = (double*)rzm;
+    double* q_s = r_s + 32 * nsl;
+    double* val_s = q_s + 32 * nsl;
+    int* code_s = (int*)(val_s + ne);
+    int* len_s = code_s + ne;
+    int* base_s = len_s + nsl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ---- load the CTA's matrix slices, resolving every column to (owner CTA, local row)
+    for (int sl = warp; sl < nsl; sl += RZW) {
+        const int sg = S0 + sl, L = it.len[sg], b = it.base[sg] - e0, cb = (32 * sg / SIG) * SIG;
+        if (lane == 0) {
+            len_s[sl] = L;
+            base_s[sl] = b;
+        }
+        for (int k = 0; k < L; ++k) {
+            const int e = b + 32 * k + lane;
+            const int ge = e + e0;
+            const int c = it.c16 ? cb + (int)it.c16[ge] : it.c32[ge];
+            const int w = c / SIG;
+            int o = (int)(((long long)w * C) / nwin);  // owner CTA of window w: row0(o) <= c < row0(o + 1)
+            while (o + 1 < C && row0(o + 1) <= c) ++o;
+            while (o > 0 && row0(o) > c) --o;
+            val_s[e] = it.val[ge];
+            code_s[e] = (o << 16) | (c - row0(o));
+        }
+    }
+    // ---- registers: this lane's rows (slice warp + RZW j)
+    double x[RPL], p[RPL], sv[RPL], w[RPL], r[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        const int sl = warp + RZW * j;
+        const int row = 32 * (S0 + sl) + lane;
+        const bool ok = sl < nsl && row < R1;
+        x[j] = ok ? it.x[row] : 0.0;
+        r[j] = ok ? it.r[row] : 0.0;
+        p[j] = sv[j] = w[j] = 0.0;
+        if (sl < nsl) {
+            r_s[32 * sl + lane] = r[j];
+            q_s[32 * sl + lane] = ok ? it.q[row] : 0.0;
+        }
+    }
+    rz_sync<CL>();
+    cg::cluster_group cluster = cg::this_cluster();
+    auto spmv = [&](double4& loc) {
+        loc = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+            const int sl = warp + RZW * j;
+            if (sl >= nsl) break;  // warp-uniform
+            const int L = len_s[sl], b = base_s[sl] + lane;
+            double acc = 0.0;
+            for (int k0 = 0; k0 < L; k0 += 4) {
+                double vv[4], gv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    vv[u] = 0.0;
+                    gv[u] = 0.0;
+                    if (k0 + u < L) {
+                        const int e = b + 32 * (k0 + u);
+                        vv[u] = val_s[e];
+                        const int cd = code_s[e];
+                        const int o = cd >> 16, lr = cd & 0xffff;
+                        // local row lr of CTA o sits in slot lr of its r_s (rows start on a slice)
+                        if (!CL || o == rank) gv[u] = r_s[lr];
+                        else gv[u] = cluster.map_shared_rank(r_s, o)[lr];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fma(vv[u], gv[u], acc);
+            }
+            const int row = 32 * (S0 + sl) + lane;
+            if (row < R1) {
+                w[j] = r[j] + acc;
+                const double ru = r[j] * q_s[32 * sl + lane];
+                loc.x += r[j] * r[j];
+                loc.y += w[j] * r[j];
+                loc.z += ru * ru;
+            }
+        }
+    };
+    // cluster-wide fixed-order sum of the three dots
+    auto reduce = [&](double4 loc) -> double4 {
+        loc.x = warp_sum_d(loc.x);
+        loc.y = warp_sum_d(loc.y);
+        loc.z = warp_sum_d(loc.z);
+        if (lane == 0) {
+            sh[4 * warp] = loc.x;
+            sh[4 * warp + 1] = loc.y;
+            sh[4 * warp + 2] = loc.z;
+        }
+        __syncthreads();
+        if (tid < C) {  // thread k writes this CTA's partial into CTA k's slot array
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int wv = 0; wv < RZW; ++wv) {
+                t0 += sh[4 * wv];
+                t1 += sh[4 * wv + 1];
+                t2 += sh[4 * wv + 2];
+            }
+            double* dst = CL ? cluster.map_shared_rank(&part_s[0][0], tid) : &part_s[0][0];
+            dst[4 * rank] = t0;
+            dst[4 * rank + 1] = t1;
+            dst[4 * rank + 2] = t2;
+        }
+        rz_sync<CL>();
+        if (tid == 0) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            for (int k = 0; k < C; ++k) {
+                a0 += part_s[k][0];
+                a1 += part_s[k][1];
+                a2 += part_s[k][2];
+            }
+            bc[0] = a0;
+            bc[1] = a1;
+            bc[2] = a2;
+        }
+        __syncthreads();
+        return make_double4(bc[0], bc[1], bc[2], 0.0);
+    };
+    const double tol2 = S->tol2, bn2 = S->bn2;
+    const int max_iter = S->max_iter;
+    int iters = S->iters, status = FEMI_OK;
+    double4 loc;
+    spmv(loc);
+    double4 tot = reduce(loc);
+    double gam = tot.x, del = tot.y, rho = tot.z;
+    double alpha = 0.0, beta = 0.0;
+    bool run = bn2 > 0.0 && rho > tol2 && isfinite(rho) && iters < max_iter;
+    if (!isfinite(gam) || !isfinite(bn2)) {
+        status = FEMI_E_NONFINITE;
+        run = false;
+    }
+    if (run) {
+        if (!(del > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            run = false;
+        } else {
+            alpha = gam / del;
+        }
+    }
+    const bool tmr = g_pcg_timers_on && item == 0 && rank == 0 && tid == 0;
+    unsigned long long tl = tmr ? gtimer() : 0ull;
+    auto mark = [&](int k) {
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[k] += t - tl;
+            tl = t;
+        }
+    };
+    while (run) {
+        // U (registers) and r published in shared memory
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+            const int sl = warp + RZW * j;
+            if (sl >= nsl) break;
+            p[j] = fma(beta, p[j], r[j]);
+            sv[j] = fma(beta, sv[j], w[j]);
+            x[j] = fma(alpha, p[j], x[j]);
+            r[j] = fma(-alpha, sv[j], r[j]);
+            r_s[32 * sl + lane] = r[j];
+        }
+        ++iters;
+        mark(0);
+        rz_sync<CL>();  // r published (cluster-wide)
+        mark(1);
+        spmv(loc);
+        mark(2);
+        tot = reduce(loc);  // its cluster barrier also orders the next U's r writes after all reads
+        mark(3);
+        const double gam2 = tot.x, del2 = tot.y, rho2 = tot.z;
+        if (!isfinite(gam2) || !isfinite(del2)) {
+            status = FEMI_E_NONFINITE;
+            break;
+        }
+        if (rho2 <= tol2) break;
+        if (iters >= max_iter) {
+            status = FEMI_E_NOT_CONVERGED;
+            break;
+        }
+        beta = gam2 / gam;
+        const double den = del2 - beta * gam2 / alpha;
+        if (!(den > 0.0)) {
+            status = FEMI_E_NEG_CURVATURE;
+            break;
+        }
+        alpha = gam2 / den;
+        gam = gam2;
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        const int sl = warp + RZW * j;
+        const int row = 32 * (S0 + sl) + lane;
+        if (sl < nsl && row < R1) it.x[row] = x[j];
+    }
+    if (rank == 0 && tid == 0) {
+        S->iters = iters;
+        S->status = status;
+    }
+    rz_sync<CL>();  // no CTA leaves while others may still read its shared memory
 }
 
 // ------------------------------------------------------------------ graph mode
@@ -1420,7 +1673,52 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         nnz_max = std::max(nnz_max, S[b]->nnz_uu);
     }
     int mode, ncta_item = 1;
-    if (B == 1 && S[0]->nnz_uu > 600000) {
+    // on-chip resident solver (k_cgr): the smallest cluster (1..16 CTAs) whose CTAs hold their
+    // matrix slices and r in shared memory and their rows in registers (<= RPL slices per warp)
+    size_t rz_smem = 0;
+    int rz_C = 0;
+    static const bool rz_off = std::getenv("FEMI_NO_RESIDENT") != nullptr;
+    if (!rz_off && !(B == 1 && S[0]->nnz_uu > 600000)) {
+        const size_t rz_budget = (size_t)g_smem_optin - 4096;
+        // cluster size: enough CTAs to fill the GPU (B C <= #SMs) while every warp keeps at least
+        // one slice -- the per-iteration critical path is a warp's slice sequence -- and at
+        // least the smallest size whose CTAs fit in shared memory
+        int64_t nsl_max = 0;
+        for (int b = 0; b < B; ++b) nsl_max = std::max<int64_t>(nsl_max, S[b]->nslices);
+        int c_fill = 1, c_use = 1;
+        while (c_fill * 2 <= 16 && (int64_t)B * c_fill * 2 <= g_nsm) c_fill *= 2;
+        while (c_use < 16 && (int64_t)c_use * RZW < nsl_max) c_use *= 2;
+        const int c_pref = std::min(c_fill, c_use);
+        for (int C = 1; C <= 16 && !rz_C; C <<= 1) {
+            if (C < c_pref) continue;
+            bool ok = true;
+            size_t need = 0;
+            for (int b = 0; b < B && ok; ++b) {
+                const femi_system_s* sy = S[b];
+                if (sy->n_u == 0) continue;
+                if ((int)sy->sell_base_h.size() != sy->nslices + 1) {
+                    ok = false;
+                    break;
+                }
+                for (int k = 0; k < C && ok; ++k) {
+                    const int64_t r0 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * k / C * SIG);
+                    const int64_t r1 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * (k + 1) / C * SIG);
+                    const int64_t s0 = r0 / 32, s1 = (r1 + 31) / 32, nsl = s1 - s0;
+                    if (nsl > (int64_t)RZW * RPL || r1 - r0 > 65535) ok = false;
+                    const int64_t ne = nsl > 0 ? sy->sell_base_h[s1] - sy->sell_base_h[s0] : 0;
+                    need = std::max(need, (size_t)(16 * 32 * nsl + 12 * ne + 8 * nsl + 64));
+                }
+            }
+            if (ok && need <= rz_budget) {
+                rz_C = C;
+                rz_smem = need;
+            }
+        }
+    }
+    if (rz_C > 0) {
+        mode = 3;
+        ncta_item = rz_C;
+    } else if (B == 1 && S[0]->nnz_uu > 600000) {
         mode = 2;
         ncta_item = std::max(1, std::min(g_occ_grid, S[0]->nwin));
     } else {
@@ -1552,6 +1850,34 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             int bb = B;
             void* args[5] = {(void*)&di, (void*)&bb, (void*)&vr, (void*)&nvec, (void*)&mrows};
             void* fn;
+            if (mode == 3) {
+                static bool rz_attr = false;
+                if (!rz_attr) {
+                    FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   g_smem_optin - 4096));
+                    FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   g_smem_optin - 4096));
+                    FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                    rz_attr = true;
+                }
+                cfg.blockDim = dim3(RZT);
+                cfg.dynamicSmemBytes = rz_smem;
+                void* args1[1] = {(void*)&di};
+                if (ncta_item > 1) {
+                    attr[0].id = cudaLaunchAttributeClusterDimension;
+                    attr[0].val.clusterDim.x = ncta_item;
+                    attr[0].val.clusterDim.y = 1;
+                    attr[0].val.clusterDim.z = 1;
+                    cfg.numAttrs = 1;
+                }
+                const cudaError_t e3 = cudaLaunchKernelExC(&cfg, ncta_item > 1 ? (void*)k_cgr<true> : (void*)k_cgr<false>,
+                                                           args1);
+                if (e3 != cudaSuccess) return cuda_fail(e3, "k_cgr launch");
+                k_finalize<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+                k_true_res<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt + B);
+                count_launches(3);
+                FEMI_CUDA(cudaGetLastError());
+            } else {
             if (mode == 2) {
                 attr[0].id = cudaLaunchAttributeCooperative;
                 attr[0].val.cooperative = 1;
@@ -1573,6 +1899,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             k_true_res<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt + B);
             count_launches(3);
             FEMI_CUDA(cudaGetLastError());
+            }
         }
         FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));

@@ -1,8 +1,6 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --config 2 --steps 1 --warmup 1"
 timeout 600 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
-timeout 900 ncu --graph-profiling graph --profile-from-start off --clock-control none \
-  --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors.sum \
-  --csv --log-file gpurun_out/graph_bytes.csv $CMD > gpurun_out/prof_graph.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_cgr" -s 1 -c 1 -o gpurun_out/prof_cgr $CMD > gpurun_out/prof_cgr.log 2>&1
 echo done
