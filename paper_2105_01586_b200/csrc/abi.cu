@@ -330,6 +330,40 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         S->sell_base_h = base;
         S->sell_base_h.push_back((int32_t)ent);  // [nslices] = total entries
         U(upload(S, &S->sell_inv, pi, st));
+        {
+            std::vector<int32_t> ukr(n + 1), ukc, uks, uur(n + 1), uuc, uus;
+            ukc.reserve(M.uk_col.size());
+            uks.reserve(M.uk_col.size());
+            uuc.reserve(M.uu_col.size());
+            uus.reserve(M.uu_col.size());
+            for (int64_t i = 0; i < n; ++i) {
+                const int32_t nat = pi[i];
+                ukr[i] = (int32_t)ukc.size();
+                for (int32_t e = M.uk_rowptr[nat]; e < M.uk_rowptr[nat + 1]; ++e) {
+                    ukc.push_back(M.uk_col[e]);
+                    uks.push_back(e);
+                }
+                uur[i] = (int32_t)uuc.size();
+                for (int32_t e = M.uu_rowptr[nat]; e < M.uu_rowptr[nat + 1]; ++e) {
+                    uuc.push_back(M.uu_col[e]);
+                    uus.push_back(e);
+                }
+            }
+            ukr[n] = (int32_t)ukc.size();
+            uur[n] = (int32_t)uuc.size();
+            U(upload(S, &S->ukI_rowptr, ukr, st));
+            U(upload(S, &S->uuI_rowptr, uur, st));
+            if (!ukc.empty()) {
+                U(upload(S, &S->ukI_col, ukc, st));
+                U(upload(S, &S->ukI_src_tmp, uks, st));
+                U(alloc(S, &S->ukI_val, ukc.size()));
+            }
+            if (!uuc.empty()) {
+                U(upload(S, &S->uuI_col, uuc, st));
+                U(upload(S, &S->uuI_src_tmp, uus, st));
+                U(alloc(S, &S->uuI_val, uuc.size()));
+            }
+        }
         U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
         // padded to whole JDS tiles: the TMA tiles read s_int in kJdsRows blocks
         U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
@@ -455,7 +489,8 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
     }
     for (auto it = S->allocs.begin(); it != S->allocs.end();) {
         if (*it == (void*)d_tri || *it == (void*)d_flags || *it == (void*)S->sell_src_tmp ||
-            (S->jds_src_tmp && *it == (void*)S->jds_src_tmp)) {
+            (S->jds_src_tmp && *it == (void*)S->jds_src_tmp) || (S->ukI_src_tmp && *it == (void*)S->ukI_src_tmp) ||
+            (S->uuI_src_tmp && *it == (void*)S->uuI_src_tmp)) {
             cudaFree(*it);
             it = S->allocs.erase(it);
         } else {

@@ -122,6 +122,18 @@ femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStrea
         k_sell_values<<<g, 256, 0, st>>>(S->sell_nnz, d_src, S->o_val, S->sell_val);
         count_launches(1);
     }
+    if (S->ukI_val) {
+        const int64_t ne = S->nnz_uk;
+        k_sell_values<<<(int)std::min<int64_t>((ne + 255) / 256, 148 * 16), 256, 0, st>>>(ne, S->ukI_src_tmp,
+                                                                                          S->uk_val, S->ukI_val);
+        count_launches(1);
+    }
+    if (S->uuI_val) {
+        const int64_t ne = S->nnz_uu;
+        k_sell_values<<<(int)std::min<int64_t>((ne + 255) / 256, 148 * 16), 256, 0, st>>>(ne, S->uuI_src_tmp,
+                                                                                          S->uu_val, S->uuI_val);
+        count_launches(1);
+    }
     if (S->jds_nnz > 0) {
         int gj = (int)std::min<int64_t>((S->jds_nnz + 255) / 256, 148 * 16);
         k_sell_values<<<gj, 256, 0, st>>>(S->jds_nnz, S->jds_src_tmp, S->o_val, S->jds_val);

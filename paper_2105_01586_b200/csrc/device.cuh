@@ -136,6 +136,11 @@ struct femi_system_s {
     uint8_t* jds_col = nullptr;
     int32_t* jds_src_tmp = nullptr;
     int64_t jds_nnz = 0;
+    // A_uk and A_uu (unscaled) rows in the internal solver order (coalesced row access for the
+    // right-hand side and the true residual); columns canonical; values gathered after assembly
+    int32_t *ukI_rowptr = nullptr, *ukI_col = nullptr, *uuI_rowptr = nullptr, *uuI_col = nullptr;
+    double *ukI_val = nullptr, *uuI_val = nullptr;
+    int32_t *ukI_src_tmp = nullptr, *uuI_src_tmp = nullptr;
     int32_t* sell_inv = nullptr;      // n_u: internal solver row -> canonical unknown index
     double* s_int = nullptr;          // D^-1/2 in internal order
     double* q_int = nullptr;          // D^1/2 = 1/s_int (unscaled residual monitor: r = r^ q)

@@ -57,10 +57,10 @@ struct RItem {
     const int32_t* c32;
     const double* s;     // D^-1/2 (internal order)
     const double* q;     // D^1/2 (internal order): unscaled residual r = r^ q (monitor)
-    const int32_t* urp;  // unscaled A_uu (diagonal included), canonical rows
+    const int32_t* urp;  // unscaled A_uu (diagonal included), internal rows, canonical columns
     const int32_t* uci;
     const double* uav;
-    const int32_t* krp;  // A_uk, canonical rows
+    const int32_t* krp;  // A_uk, internal rows, canonical (mask) columns
     const int32_t* kci;
     const double* kav;
     const double* g;    // mask values or NULL (b given)
@@ -150,22 +150,7 @@ __global__ void k_minmax(int B, const RItem* __restrict__ items) {
 }
 
 // b = -A_uk g (ascending mask index, reading A6 order), or the given b; internal order
-__global__ void k_rhs(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        const int nat = it.inv[i];
-        double bi;
-        if (it.bin) {
-            bi = it.bin[nat];
-        } else {
-            double acc = 0.0;
-            for (int e = it.krp[nat]; e < it.krp[nat + 1]; ++e) acc = acc + it.kav[e] * it.g[it.kci[e]];
-            bi = -acc;
-        }
-        it.b[i] = bi;
-    }
-}
-
+__global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, unsigned* cnt);
 // x^0 = x0 / s (x0: midrange(g), 0 or the caller's u_vert)
 __global__ void k_init_x(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
@@ -224,10 +209,47 @@ __device__ __forceinline__ bool grid_partial(double (&v)[NQ], double* red, unsig
     return true;
 }
 
+// b = -A_uk g (internal rows, ascending mask index: reading A6 order) or the given b, and
+// ||b||^2 -> state. Unless the caller gave x0 (x0mode 2) the initial residual comes with it,
+// without an SpMV: x0 = c 1 (c = midrange(g), or 0) and A_uu 1 = -A_uk 1 (zero row sums of the
+// full stiffness matrix) give r0 = b - A_uu x0 = -A_uk (g - c 1); stored scaled, r^0 = s r0.
+__global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, unsigned* cnt) {
+    __shared__ double shm[4 * (KNT / 32)];
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    const bool direct = it.x0mode != 2;
+    const double c = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    double v[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        double bi, r0;
+        if (it.bin) {
+            bi = it.bin[it.inv[i]];
+            r0 = bi;  // x0 = 0 (x0mode 0)
+        } else {
+            double acc = 0.0, accr = 0.0;
+            for (int e = it.krp[i]; e < it.krp[i + 1]; ++e) {
+                const double a = it.kav[e], gk = it.g[it.kci[e]];
+                acc = acc + a * gk;
+                accr = fma(a, gk - c, accr);
+            }
+            bi = -acc;
+            r0 = -accr;
+        }
+        it.b[i] = bi;
+        if (direct) it.r[i] = it.s[i] * r0;
+        v[0] += bi * bi;
+    }
+    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) {
+        it.st->bn2 = v[0];
+        it.st->tol2 = it.st->rtol * it.st->rtol * v[0];
+    }
+}
+
 // r0 = s b - (x^ + A^_off x^) over SELL slices (warp per slice); ||b||^2 -> state
 __global__ void __launch_bounds__(KNT) k_init_r(const RItem* __restrict__ items, unsigned* cnt) {
     __shared__ double shm[4 * (KNT / 32)];
     const RItem& it = items[blockIdx.y];
+    if (it.x0mode != 2) return;  // r^0 came with the right-hand side (k_rhs)
     const int lane = threadIdx.x & 31;
     const int nsl = (it.n + 31) / 32;
     double v[1] = {0.0};
@@ -274,9 +296,8 @@ __global__ void __launch_bounds__(KNT) k_true_res(const RItem* __restrict__ item
     const RItem& it = items[blockIdx.y];
     double v[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        const int nat = it.inv[i];
         double ax = 0.0;
-        for (int e = it.urp[nat]; e < it.urp[nat + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+        for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
         const double ri = it.b[i] - ax;
         it.r[i] = it.s[i] * ri;
         v[0] += ri * ri;
@@ -1361,7 +1382,7 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
         void* a_mm[2] = {&one, &di};
         if ((s = chain((void*)k_minmax, dim3(296), dim3(256), a_mm))) return s;
-        if ((s = chain((void*)k_rhs, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
         if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
     }
     if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
@@ -1546,12 +1567,12 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.c32 = S->sell_c32;
         it.s = S->s_int;
         it.q = S->q_int;
-        it.urp = S->uu_rowptr;
-        it.uci = S->uu_col;
-        it.uav = S->uu_val;
-        it.krp = S->uk_rowptr;
-        it.kci = S->uk_col;
-        it.kav = S->uk_val;
+        it.urp = S->uuI_rowptr;
+        it.uci = S->uuI_col;
+        it.uav = S->uuI_val;
+        it.krp = S->ukI_rowptr;
+        it.kci = S->ukI_col;
+        it.kav = S->ukI_val;
         it.part = nullptr;
         it.st = C->d_state;
         it.n = (int32_t)n;
@@ -1780,12 +1801,12 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.c32 = s->sell_c32;
         it.s = s->s_int;
         it.q = s->q_int;
-        it.urp = s->uu_rowptr;
-        it.uci = s->uu_col;
-        it.uav = s->uu_val;
-        it.krp = s->uk_rowptr;
-        it.kci = s->uk_col;
-        it.kav = s->uk_val;
+        it.urp = s->uuI_rowptr;
+        it.uci = s->uuI_col;
+        it.uav = s->uuI_val;
+        it.krp = s->ukI_rowptr;
+        it.kci = s->ukI_col;
+        it.kav = s->ukI_val;
         it.g = g ? g[b] : nullptr;
         it.bin = bin ? bin[b] : nullptr;
         it.u_vert = u_vert[b];
@@ -1820,7 +1841,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         count_launches(1);
     }
     if (nmax > 0) {
-        k_rhs<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+        k_rhs<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
         k_init_x<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
         k_init_r<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
         count_launches(3);

@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-for c in 2 3 4; do FEMI_PCG_TIMERS=1 timeout 300 python bench.py --config $c --steps 3 --warmup 1 > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; done
-timeout 300 python bench.py --config 1 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-timeout 600 python -m pytest tests -m gpu -x -q -k "config2 or config3 or tonal or config1 or small" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 200 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/kb.json 2> gpurun_out/kbench.err
+for c in 2 4; do timeout 300 python bench.py --config $c --steps 3 --warmup 1 > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; done
 echo done
