@@ -185,6 +185,27 @@ femi_status femi_densify_step(femi_system sys, const double* f, const double* u_
                               int32_t* new_mask_px, int64_t* n_added, femi_stream stream);
 
 /* ---------------------------------------------------------------------------------
+ * Colour (C channels on one mesh). PAPER.md:L521-524 "Extending the
+ * method to colour images is straightforward": every channel is inpainted on the same mask
+ * and mesh (femi_inpaint_solve_batched with the system repeated C times solves all channels
+ * with one shared-matrix multi-right-hand-side CG); the error map is the channel sum
+ * e = sum_c (u_c - f_c)^2 (SPEC.md:L74, L83 convention), accumulated in channel order.
+ *   C in 1..4; u_vert[C], f[C]: HOST arrays of DEVICE pointers (f may be NULL: raster only);
+ *   u_px: NULL or HOST array of C DEVICE pointers (entries nullable); e_px, tri_err,
+ *   tri_best_px, sse: as femi_rasterise_error, for the channel-summed error.
+ * rasterise_error_channels enqueues only; densify_step_channels selects from the summed
+ * error exactly as femi_densify_step and synchronises `stream`.
+ * Errors: FEMI_E_ARG, FEMI_E_CUDA, FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_rasterise_error_channels(femi_system sys, int32_t C, const double* const* u_vert,
+                                          const double* const* f, double* const* u_px, double* e_px,
+                                          double* tri_err, int32_t* tri_best_px, double* sse,
+                                          femi_stream stream);
+femi_status femi_densify_step_channels(femi_system sys, int32_t C, const double* const* f,
+                                       const double* const* u_vert, int64_t b, int32_t* new_mask_px,
+                                       int64_t* n_added, femi_stream stream);
+
+/* ---------------------------------------------------------------------------------
  * S6 tonal_optimise (DEVICE + host report). PAPER.md:L280-316, Eqs. (4)-(5):
  * g* = argmin ||B g - f||^2 solved as B^T B g = B^T f by CG on the normal equations in
  * CGLS form ("nested conjugate gradient solver"), B g = P_k g + P_u A_uu^-1 (-A_uk g)

@@ -14,6 +14,7 @@ Parity status per function:
   assemble ......................... pinned (P1, P2, P5, P6)
   solve ............................ pinned (P5 FDM, P6, P7, P8, P9, dense Cholesky)
   raster / error ................... pinned (P10, P11, P7, P8)
+  raster_channels (colour) ......... pinned (C = 1 equals raster; channel sum of per-channel maps)
   select ........................... pinned (P16, brute-force re-derivation on tiny cases)
   tonal ............................ pinned (P13 dense lstsq, P14, P15)
 """
@@ -67,6 +68,9 @@ def lib():
                                     ctypes.POINTER(ctypes.c_double)]
         L.orc_sys_raster.argtypes = [ctypes.c_void_p, f64p, f64p, f64p, f64p, f64p, i32p,
                                      ctypes.POINTER(ctypes.c_double)]
+        L.orc_sys_raster_channels.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_void_p, f64p, f64p, i32p, ctypes.POINTER(ctypes.c_double)]
+        L.orc_sys_raster_channels.restype = None
         L.orc_select.restype = ctypes.c_int64
         L.orc_select.argtypes = [ctypes.c_int64, f64p, i32p, ctypes.c_int64, f64p, u8p, ctypes.c_int64, i32p]
         L.orc_sys_apply_B.restype = ctypes.c_int
@@ -199,6 +203,22 @@ class System:
         sse = ctypes.c_double(0.0)
         lib().orc_sys_raster(self._h, u_vert, f, u_px, e_px, tri_err, best, ctypes.byref(sse))
         return dict(u_px=u_px, e_px=e_px, tri_err=tri_err[: self.T], best=best[: self.T], sse=sse.value,
+                    mse=sse.value / N)
+
+    def raster_channels(self, u_list, f_list):
+        """Colour raster: channels on this mesh, e = sum_c (u_c - f_c)^2."""
+        C = len(u_list)
+        N = self.W * self.H
+        us = [np.ascontiguousarray(u, np.float64) for u in u_list]
+        fs = [np.ascontiguousarray(f, np.float64).reshape(-1) for f in f_list]
+        ups = [np.zeros(N) for _ in range(C)]
+        arr = lambda xs: (ctypes.c_void_p * C)(*[x.ctypes.data for x in xs])  # noqa: E731
+        e_px = np.zeros(N)
+        tri_err = np.zeros(max(self.T, 1))
+        best = np.zeros(max(self.T, 1), np.int32)
+        sse = ctypes.c_double(0.0)
+        lib().orc_sys_raster_channels(self._h, C, arr(us), arr(fs), arr(ups), e_px, tri_err, best, ctypes.byref(sse))
+        return dict(u_px=ups, e_px=e_px, tri_err=tri_err[: self.T], best=best[: self.T], sse=sse.value,
                     mse=sse.value / N)
 
     def is_vertex(self) -> np.ndarray:

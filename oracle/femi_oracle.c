@@ -674,6 +674,35 @@ void orc_sys_raster(const OrcSys* S, const double* u_vert, const double* f, doub
     free(best_e);
 }
 
+/* Colour ("Extending the method to colour images is straightforward"):
+ * C channels on one mesh; the error map is the channel sum e = sum_c (u_c - f_c)^2, added in
+ * channel order (SPEC.md:L74, L83 convention); per-triangle sums, arg-max and SSE as in
+ * orc_sys_raster. u_vert, f: C pointers; u_px: NULL or C pointers (entries may be NULL). */
+void orc_sys_raster_channels(const OrcSys* S, int C, const double* const* u_vert, const double* const* f,
+                             double* const* u_px, double* e_px, double* tri_err, i32* best, double* sse) {
+    i64 N = (i64)S->W * S->H;
+    double* best_e = (double*)malloc(sizeof(double) * (size_t)(S->T + 1));
+    for (i64 t = 0; t < S->T; ++t) { tri_err[t] = 0.0; best[t] = -1; best_e[t] = -1.0; }
+    double s = 0.0;
+    for (i64 p = 0; p < N; ++p) {
+        double e = 0.0;
+        for (int c = 0; c < C; ++c) {
+            double u = pixel_value(S, (i32)p, u_vert[c]);
+            double d = u - f[c][p];
+            double dd = d * d;
+            e = (c == 0) ? dd : e + dd;
+            if (u_px && u_px[c]) u_px[c][p] = u;
+        }
+        if (e_px) e_px[p] = e;
+        s = s + e;
+        i64 t = S->owner[p];
+        tri_err[t] = tri_err[t] + e;
+        if (S->vmap[p] < 0 && e > best_e[t]) { best_e[t] = e; best[t] = (i32)p; } /* ties: lowest pix */
+    }
+    *sse = s;
+    free(best_e);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Densification selection (readings A8-A10)                 */
 /* ------------------------------------------------------------------------- */

@@ -592,7 +592,45 @@ femi_status femi_densify_step(femi_system sys, const double* f, const double* u_
         set_error("densify_step: NULL argument or b < 0");
         return FEMI_E_ARG;
     }
-    return densify_select(sys, f, u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
+    return densify_select(sys, 1, &f, &u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
+}
+
+femi_status femi_rasterise_error_channels(femi_system sys, int32_t C, const double* const* u_vert,
+                                          const double* const* f, double* const* u_px, double* e_px, double* tri_err,
+                                          int32_t* tri_best_px, double* sse, femi_stream stream) {
+    if (!sys || C < 1 || C > 4 || !u_vert) {
+        set_error("rasterise_error_channels: NULL system/u_vert or C outside 1..4");
+        return FEMI_E_ARG;
+    }
+    for (int c = 0; c < C; ++c)
+        if (!u_vert[c] || (f && !f[c])) {
+            set_error("rasterise_error_channels: NULL channel pointer");
+            return FEMI_E_ARG;
+        }
+    if (!f && (e_px || tri_err || tri_best_px || sse)) {
+        set_error("rasterise_error_channels: error outputs need f");
+        return FEMI_E_ARG;
+    }
+    femi_status s = check_device();
+    if (s) return s;
+    return launch_raster_channels(sys, C, u_vert, f, u_px, e_px, tri_err, tri_best_px, sse, (cudaStream_t)stream);
+}
+
+femi_status femi_densify_step_channels(femi_system sys, int32_t C, const double* const* f,
+                                       const double* const* u_vert, int64_t b, int32_t* new_mask_px,
+                                       int64_t* n_added, femi_stream stream) {
+    if (!sys || C < 1 || C > 4 || !f || !u_vert || !n_added || b < 0 || (b > 0 && !new_mask_px)) {
+        set_error("densify_step_channels: NULL argument, C outside 1..4 or b < 0");
+        return FEMI_E_ARG;
+    }
+    for (int c = 0; c < C; ++c)
+        if (!f[c] || !u_vert[c]) {
+            set_error("densify_step_channels: NULL channel pointer");
+            return FEMI_E_ARG;
+        }
+    femi_status s = check_device();
+    if (s) return s;
+    return densify_select(sys, C, f, u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
 }
 
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,

@@ -146,6 +146,7 @@ struct femi_system_s {
     double* q_int = nullptr;          // D^1/2 = 1/s_int (unscaled residual monitor: r = r^ q)
     // cached single-RHS scratch (x, r, q, b, p0, p1, state, items, chunks, partials)
     void* scratch = nullptr;
+    void* scratch_m[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // multi-RHS graph caches (NR = 2..4)
     size_t scratch_bytes = 0;
     std::vector<void*> allocs;
 };
@@ -178,13 +179,16 @@ femi_status launch_assemble_values(femi_system_s* S, cudaStream_t st);
 femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
                           double* const* u_px, double* const* e_px, double* const* tri_err,
                           int32_t* const* best, double* const* sse, cudaStream_t st);
+femi_status launch_raster_channels(femi_system_s* S, int nc, const double* const* u_vert, const double* const* f,
+                                   double* const* u_px, double* e_px, double* tri_err, int32_t* best, double* sse,
+                                   cudaStream_t st);  // colour: e = sum over channels
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st);
 femi_status build_owner_tables(femi_system_s* S, cudaStream_t st);
 void pcg_cache_free(femi_system_s* S);  // graph-mode workspace + instantiated graphs
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters);
-femi_status densify_select(femi_system_s* S, const double* f, const double* u_vert, int64_t b,
+femi_status densify_select(femi_system_s* S, int nc, const double* const* f, const double* const* u_vert, int64_t b,
                            int32_t* new_px, int64_t* n_added, cudaStream_t st);
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
                        femi_tonal_report* rep, cudaStream_t st);

@@ -944,6 +944,56 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
     }
 }
 
+// One CG recurrence step from the summed dots (gam2 = r^.r^, del2 = w.r^, rho2 = ||D^1/2 r^||^2):
+// FIRST starts the recurrence; otherwise counts the iteration, tests convergence on rho2 (when it
+// was computed), and advances alpha, beta. Returns whether the recurrence continues; also sets
+// need_rho for the next SpMV (||r||^2 >= dmin ||r^||^2, two orders of slack).
+template <bool FIRST>
+__device__ __forceinline__ int cg_advance(CgState* S, bool act, double gam2, double del2, double rho2, double dmin,
+                                          double s_bn2, double s_tol2, double s_rr, double s_alpha, int s_iters,
+                                          int s_max, int s_need) {
+    int active = 0;
+    if (!act) return 0;
+    if (FIRST) {
+        const bool fin = isfinite(gam2) && isfinite(s_bn2);
+        active = (s_bn2 > 0.0 && rho2 > s_tol2 && fin && s_iters < s_max) ? 1 : 0;
+        if (!fin) S->status = FEMI_E_NONFINITE;
+        if (active && !(del2 > 0.0)) {
+            S->status = FEMI_E_NEG_CURVATURE;
+            active = 0;
+        }
+        if (active) {
+            S->alpha = gam2 / del2;
+            S->beta = 0.0;
+            S->rr = gam2;
+        }
+    } else {
+        const int it1 = s_iters + 1;
+        S->iters = it1;
+        if (!isfinite(gam2) || !isfinite(del2)) {
+            S->status = FEMI_E_NONFINITE;
+        } else if (s_need && rho2 <= s_tol2) {
+            // converged (rho2 is only computed when dmin gam2 was within 100x of tol2)
+        } else if (it1 >= s_max) {
+            S->status = FEMI_E_NOT_CONVERGED;
+        } else {
+            const double beta = gam2 / s_rr;
+            const double den = del2 - beta * gam2 / s_alpha;
+            if (!(den > 0.0)) {
+                S->status = FEMI_E_NEG_CURVATURE;
+            } else {
+                S->beta = beta;
+                S->alpha = gam2 / den;
+                S->rr = gam2;
+                active = 1;
+            }
+        }
+    }
+    S->active = active;
+    S->need_rho = (gam2 * dmin <= 100.0 * s_tol2) ? 1 : 0;
+    return active;
+}
+
 // Block partials -> part[item][block]; the last block of the item sums them in block order
 // (deterministic), advances the CG recurrence scalars (FIRST: starts it) and, once every item
 // has reported, sets the WHILE condition (any item still active -> 1).
@@ -1013,48 +1063,8 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         rho2 += shm[4 * w + 2];
     }
     S->cnt[0] = 0;
-    int active = 0;
-    if (act) {
-        if (FIRST) {
-            const bool fin = isfinite(gam2) && isfinite(s_bn2);
-            active = (s_bn2 > 0.0 && rho2 > s_tol2 && fin && s_iters < s_max) ? 1 : 0;
-            if (!fin) S->status = FEMI_E_NONFINITE;
-            if (active && !(del2 > 0.0)) {
-                S->status = FEMI_E_NEG_CURVATURE;
-                active = 0;
-            }
-            if (active) {
-                S->alpha = gam2 / del2;
-                S->beta = 0.0;
-                S->rr = gam2;
-            }
-        } else {
-            const int it1 = s_iters + 1;
-            S->iters = it1;
-            if (!isfinite(gam2) || !isfinite(del2)) {
-                S->status = FEMI_E_NONFINITE;
-            } else if (s_need && rho2 <= s_tol2) {
-                // converged (rho2 is only computed when dmin gam2 was within 100x of tol2)
-            } else if (it1 >= s_max) {
-                S->status = FEMI_E_NOT_CONVERGED;
-            } else {
-                const double beta = gam2 / s_rr;
-                const double den = del2 - beta * gam2 / s_alpha;
-                if (!(den > 0.0)) {
-                    S->status = FEMI_E_NEG_CURVATURE;
-                } else {
-                    S->beta = beta;
-                    S->alpha = gam2 / den;
-                    S->rr = gam2;
-                    active = 1;
-                }
-            }
-        }
-        S->active = active;
-        // the next SpMV needs the unscaled norm only when it can possibly be <= tol2:
-        // ||r||^2 >= dmin ||r^||^2, with two orders of magnitude of slack for one iteration
-        S->need_rho = (gam2 * dmin <= 100.0 * s_tol2) ? 1 : 0;
-    }
+    const int active = cg_advance<FIRST>(S, act, gam2, del2, rho2, dmin, s_bn2, s_tol2, s_rr, s_alpha, s_iters, s_max,
+                                         s_need);
     if (tp) g_tail_ts[4 * prof_it + 2] = gtime();  // C: scalars done
     // all items reported? -> loop condition (one item: set it directly)
     if (B == 1) {
@@ -1154,6 +1164,7 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
 constexpr int JCW = kJdsRows / 32;  // consumer warps = slices per tile
 constexpr int JNT = 32 * (JCW + 1);
 constexpr int JNS = 6;
+constexpr int JNS_M = 4;  // ring stages of the multi-RHS SpMV (larger stages: NR r slices)
 constexpr int kUnroll = 8;  // CG iterations per WHILE body (graph mode; measured: x4 2.9 us, x8 2.2 us of WHILE gap per iteration)
 
 struct JStage {
@@ -1288,6 +1299,245 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         if (it_prof < kLoopProfMax) atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());
         loop_stamp(1, it_prof, t_start);
     }
+}
+
+// ------------------------------------------------------------------ shared-matrix multi-RHS
+// NR <= 4 right-hand sides on ONE large system (colour channels): one CG
+// recurrence per RHS (own scalars, own convergence), but every iteration streams the matrix
+// ONCE for all of them -- the TMA tile carries the NR r slices next to the shared values /
+// columns / q, and each consumer lane gathers the NR neighbour values per nonzero. Per
+// iteration 12 nnz + 4 (n+1) + 80 NR n algorithmic bytes instead of NR (12 nnz + ...).
+template <int NR>
+__global__ void __launch_bounds__(GNT) k_gum(const RItem* __restrict__ items) {
+    double al[NR], be[NR];
+    bool on[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+        const CgState* S = items[c].st;
+        on[c] = S->active;
+        al[c] = S->alpha;
+        be[c] = S->beta;
+    }
+    const int n = items[0].n, stride = gridDim.x * blockDim.x;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+        if (!on[c]) continue;  // converged RHS keep x and r
+        const RItem& it = items[c];
+        double* __restrict__ r = it.r;
+        const double* __restrict__ w = it.w;
+        double* __restrict__ p = it.p;
+        double* __restrict__ sv = it.sv;
+        double* __restrict__ x = it.x;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+            const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i], xi = x[i];
+            const double pi = fma(be[c], pi0, ri), si = fma(be[c], si0, wi);
+            p[i] = pi;
+            sv[i] = si;
+            x[i] = fma(al[c], pi, xi);
+            r[i] = fma(-al[c], si, ri);
+        }
+    }
+}
+
+// last-CTA reduction of NR x 3 dots (fixed order) and the NR recurrence steps
+template <bool FIRST, int NR>
+__device__ __forceinline__ void cg_tail_m(double (&v)[NR][3], const bool (&act)[NR], const RItem* __restrict__ items,
+                                          double* __restrict__ part, cudaGraphConditionalHandle h, double dmin) {
+    constexpr int NQ = 3 * NR;
+    __shared__ double shm[NQ * (JNT / 32)];
+    __shared__ int last;
+    __shared__ int anyact[NR];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    CgState* S0 = items[0].st;
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[c][q] = warp_sum_d(v[c][q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < NR; ++c)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) shm[NQ * wid + 3 * c + q] = v[c][q];
+    __syncthreads();
+    constexpr int AT = JNT - 32;
+    if (threadIdx.x == AT) {
+        for (int k = 0; k < NQ; ++k) {
+            double t = 0.0;
+            for (int w = 0; w < JNT / 32; ++w) t += shm[NQ * w + k];
+            part[NQ * blockIdx.x + k] = t;
+        }
+        last = atom_add_release_gpu(&S0->cnt[0], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    fence_acq_rel_gpu();
+    double tot[NQ];
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) tot[k] = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += JNT)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) tot[k] += __ldcg(part + NQ * b + k);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) tot[k] = warp_sum_d(tot[k]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) shm[NQ * wid + k] = tot[k];
+    __syncthreads();
+    if (threadIdx.x < NR) {  // thread c advances RHS c
+        const int c = threadIdx.x;
+        CgState* S = items[c].st;
+        double d[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < JNT / 32; ++w)
+            for (int q = 0; q < 3; ++q) d[q] += shm[NQ * w + 3 * c + q];
+        const int need = FIRST ? 1 : S->need_rho;
+        anyact[c] = cg_advance<FIRST>(S, act[c], d[0], d[1], d[2], dmin, S->bn2, S->tol2, S->rr, S->alpha, S->iters,
+                                      S->max_iter, need);
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        S0->cnt[0] = 0;
+        int any = 0;
+        for (int c = 0; c < NR; ++c) any |= anyact[c];
+        if (h) cudaGraphSetConditional(h, any ? 1u : 0u);
+    }
+}
+
+template <int NR, bool FIRST>
+__global__ void __launch_bounds__(JNT, 1) k_gtm(const RItem* __restrict__ items, double* __restrict__ part,
+                                             cudaGraphConditionalHandle h) {
+    extern __shared__ __align__(128) unsigned char jsm[];
+    __shared__ __align__(8) uint64_t full[JNS_M], empty[JNS_M];
+    __shared__ int2 tile_e[JNS_M], tile_c[JNS_M];
+    const RItem& it = items[0];  // the shared matrix and q
+    bool act[NR];
+    bool anyon = false, nrho = FIRST;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+        act[c] = FIRST || items[c].st->active;
+        anyon |= act[c];
+        nrho |= (bool)items[c].st->need_rho;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
+    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
+    const size_t stage_bytes = ((size_t)maxe * 12 + mb + 8 * (NR + 1) * kJdsRows + 127) & ~(size_t)127;
+    // stage: r_0 .. r_{NR-1} | q | values | columns | lengths + diagonal offsets
+    auto sbase = [&](int k) { return jsm + (size_t)k * stage_bytes; };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < JNS_M; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], JCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double v[NR][3];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) v[c][0] = v[c][1] = v[c][2] = 0.0;
+    if (anyon) {
+        if (warp == JCW) {
+            if (lane == 0) {
+                int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
+                const uint64_t pol = policy_evict_first();
+                for (int t = tb, i = 0; t < te; ++t, ++i) {
+                    const int k = i % JNS_M;
+                    const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];
+                    if (i >= JNS_M) mbar_wait(&empty[k], ((i / JNS_M) - 1) & 1);
+                    unsigned char* b = sbase(k);
+                    double* qs = (double*)b + NR * kJdsRows;
+                    double* vs = qs + kJdsRows;
+                    uint8_t* cs = (uint8_t*)(vs + maxe);
+                    uint8_t* ms = cs + 4 * (size_t)maxe;
+                    const int ne = e1 - e0, nc = c1 - c0;
+                    tile_e[k] = make_int2(e0, ne);
+                    tile_c[k] = make_int2(c0, nc);
+                    mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb +
+                                                        (NR + (nrho ? 1u : 0u)) * 8u * kJdsRows);
+#pragma unroll
+                    for (int c = 0; c < NR; ++c)
+                        bulk_g2s((double*)b + c * kJdsRows, items[c].r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    if (nrho) bulk_g2s(qs, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[k]);
+                    bulk_g2s(ms, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
+                    if (ne) {
+                        bulk_g2s_hint(vs, it.jval + e0, 8u * ne, &full[k], pol);
+                        bulk_g2s_hint(cs, it.jcol + c0, (uint32_t)nc, &full[k], pol);
+                    }
+                    e0 = e1;
+                    c0 = c1;
+                }
+            }
+        } else {
+            const int rl = 32 * warp + lane;
+            const double* rg[NR];
+            double* wo[NR];
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                rg[c] = items[c].r;
+                wo[c] = items[c].w;
+            }
+            for (int t = tb, i = 0; t < te; ++t, ++i) {
+                const int k = i % JNS_M;
+                mbar_wait(&full[k], (i / JNS_M) & 1);
+                unsigned char* b = sbase(k);
+                const double* rs = (const double*)b;
+                const double* qs = rs + NR * kJdsRows;
+                const double* vs = qs + kJdsRows;
+                const uint8_t* cs = (const uint8_t*)(vs + maxe);
+                const uint8_t* ms = cs + 4 * (size_t)maxe;
+                const int row = t * kJdsRows + rl;
+                const int len = ms[rl];
+                const uint16_t* doff = (const uint16_t*)(ms + kJdsRows) + warp * kmax;
+                const int L = __shfl_sync(0xffffffffu, len, 0);
+                const bool wide = tile_c[k].y > 2 * tile_e[k].y;
+                const int16_t* c16 = (const int16_t*)cs;
+                const int32_t* c32 = (const int32_t*)cs;
+                const size_t t0 = (size_t)t * kJdsRows;
+                double acc[NR];
+#pragma unroll
+                for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+                for (int k0 = 0; k0 < L; k0 += 4) {
+                    double vv[4];
+                    int cc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool a = k0 + u < len;
+                        const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
+                        vv[u] = a ? vs[idx] : 0.0;
+                        cc[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
+                    }
+                    double gv[NR][4];
+#pragma unroll
+                    for (int c = 0; c < NR; ++c)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) gv[c][u] = rg[c][t0 + cc[u]];
+#pragma unroll
+                    for (int c = 0; c < NR; ++c)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[c] = fma(vv[u], gv[c][u], acc[c]);
+                }
+                const double qi = nrho ? qs[rl] : 0.0;
+                double xi[NR];
+#pragma unroll
+                for (int c = 0; c < NR; ++c) xi[c] = rs[c * kJdsRows + rl];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[k]);
+                if (row < it.n) {
+#pragma unroll
+                    for (int c = 0; c < NR; ++c) {
+                        const double y = xi[c] + acc[c];
+                        wo[c][row] = y;
+                        const double ru = xi[c] * qi;
+                        v[c][0] += xi[c] * xi[c];
+                        v[c][1] += y * xi[c];
+                        v[c][2] += ru * ru;
+                    }
+                }
+            }
+        }
+    }
+    cg_tail_m<FIRST, NR>(v, act, items, part, h, it.dmin);
 }
 
 // min over i of q_i^2 = diag(A_uu)_i (order-preserving bits of positive doubles)
@@ -1628,7 +1878,250 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
 
 }  // namespace
 
+namespace {
+
+struct GraphCacheM {
+    void* ws = nullptr;
+    RItem* d_items = nullptr;
+    CgState* d_state = nullptr;
+    unsigned* d_cnt = nullptr;
+    double* d_part = nullptr;
+    cudaGraphExec_t main = nullptr, restart = nullptr;
+    std::vector<RItem> items;
+    int nr = 0, gx = 0, gt_blocks = 0;
+    unsigned smem = 0;
+};
+
+femi_status build_graph_m(GraphCacheM& C, bool restart, cudaGraphExec_t* out) {
+    cudaGraph_t gr;
+    FEMI_CUDA(cudaGraphCreate(&gr, 0));
+    cudaGraphConditionalHandle h;
+    FEMI_CUDA(cudaGraphConditionalHandleCreate(&h, gr, 0, cudaGraphCondAssignDefault));
+    RItem* di = C.d_items;
+    int nr = C.nr;
+    double* part = C.d_part;
+    unsigned* cnt0 = C.d_cnt;
+    unsigned* cnt1 = C.d_cnt + nr;
+    void* a_items[1] = {&di};
+    void* a_reset[2] = {&nr, &di};
+    void* a_cnt0[2] = {&di, &cnt0};
+    void* a_cnt1[2] = {&di, &cnt1};
+    void* a_t[3] = {&di, &part, &h};
+    const dim3 gk(C.gx, nr), bk(KNT);
+    cudaGraphNode_t prev = nullptr, nd;
+    cudaGraphNode_t* dep = nullptr;
+    auto chain = [&](void* fn, dim3 gg, dim3 bb, void** args, unsigned smem = 0) -> femi_status {
+        femi_status s = add_kernel(gr, dep, fn, gg, bb, args, &nd, smem);
+        prev = nd;
+        dep = &prev;
+        return s;
+    };
+    void *f_first, *f_body, *f_up;
+    switch (nr) {
+        case 2: f_first = (void*)k_gtm<2, true>; f_body = (void*)k_gtm<2, false>; f_up = (void*)k_gum<2>; break;
+        case 3: f_first = (void*)k_gtm<3, true>; f_body = (void*)k_gtm<3, false>; f_up = (void*)k_gum<3>; break;
+        default: f_first = (void*)k_gtm<4, true>; f_body = (void*)k_gtm<4, false>; f_up = (void*)k_gum<4>; break;
+    }
+    femi_status s = FEMI_OK;
+    if (!restart) {
+        if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
+        void* a_mm[2] = {&nr, &di};
+        if ((s = chain((void*)k_minmax, dim3(296), dim3(256), a_mm))) return s;
+        if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
+        if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
+    }
+    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
+    if (!restart)
+        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+    if ((s = chain(f_first, dim3(C.gt_blocks), dim3(JNT), a_t, C.smem))) return s;
+    {
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        FEMI_CUDA(cudaGraphAddNode(&nd, gr, dep, 1, &cp));
+        prev = nd;
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraphNode_t bprev = nullptr, u, sn;
+        for (int k = 0; k < kUnroll; ++k) {
+            if ((s = add_kernel(body, bprev ? &bprev : nullptr, f_up, dim3(std::min(C.gx * 2, 1184)), dim3(GNT),
+                                a_items, &u)))
+                return s;
+            if ((s = add_kernel(body, &u, f_body, dim3(C.gt_blocks), dim3(JNT), a_t, &sn, C.smem))) return s;
+            bprev = sn;
+        }
+    }
+    if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
+    if ((s = chain((void*)k_true_res, gk, bk, a_cnt1))) return s;
+    if ((s = chain((void*)k_copy_g, dim3(296, nr), dim3(256), a_items))) return s;
+    FEMI_CUDA(cudaGraphInstantiate(out, gr, 0));
+    FEMI_CUDA(cudaGraphDestroy(gr));
+    return FEMI_OK;
+}
+
+// NR right-hand sides on one large system with the JDS layout; returns FEMI_E_ARG when the
+// shared-memory ring does not fit (the caller falls back to one RHS at a time)
+femi_status graph_solve_multi(femi_system_s* S, int nr, const double* const* g, const double* const* bin,
+                              double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
+                              cudaStream_t st, int64_t* total_iters) {
+    GraphCacheM* C = (GraphCacheM*)S->scratch_m[nr];
+    const int64_t n = S->n_u;
+    if (!C) {
+        const size_t stage_bytes =
+            ((size_t)S->jds_maxe * 12 + S->jds_meta_bytes + 8 * (nr + 1) * kJdsRows + 127) & ~(size_t)127;
+        int dev = 0, nsm = 0, optin = 0;
+        FEMI_CUDA(cudaGetDevice(&dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        FEMI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (JNS_M * stage_bytes + 4096 > (size_t)optin) return FEMI_E_ARG;
+        C = new GraphCacheM();
+        C->nr = nr;
+        C->smem = (unsigned)(JNS_M * stage_bytes);
+        C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
+        C->gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + KNT - 1) / KNT, 148 * 16));
+        const void* fns[6] = {(const void*)k_gtm<2, true>, (const void*)k_gtm<2, false>, (const void*)k_gtm<3, true>,
+                              (const void*)k_gtm<3, false>, (const void*)k_gtm<4, true>, (const void*)k_gtm<4, false>};
+        for (const void* fn : fns)
+            FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->smem));
+        std::vector<int32_t> jpart(C->gt_blocks + 1);
+        for (int b = 0; b <= C->gt_blocks; ++b) jpart[b] = (int)((int64_t)S->jds_ntile * b / C->gt_blocks);
+        auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        const size_t vb = al(sizeof(double) * std::max<int64_t>(n + 1, (int64_t)S->jds_ntile * kJdsRows));
+        const size_t bytes = al(sizeof(int32_t) * jpart.size()) + al(sizeof(RItem) * nr) + al(sizeof(CgState) * nr) +
+                             al(sizeof(unsigned) * 2 * nr) + al(sizeof(double) * 3 * nr * C->gt_blocks) +
+                             nr * (al(sizeof(double) * C->gx) + 6 * vb);
+        FEMI_CUDA(cudaMalloc(&C->ws, bytes));
+        char* cur = (char*)C->ws;
+        auto take = [&](size_t x) {
+            char* p = cur;
+            cur += al(x);
+            return p;
+        };
+        C->d_items = (RItem*)take(sizeof(RItem) * nr);
+        int32_t* d_jpart = (int32_t*)take(sizeof(int32_t) * jpart.size());
+        FEMI_CUDA(cudaMemcpy(d_jpart, jpart.data(), sizeof(int32_t) * jpart.size(), cudaMemcpyHostToDevice));
+        C->d_state = (CgState*)take(sizeof(CgState) * nr);
+        C->d_cnt = (unsigned*)take(sizeof(unsigned) * 2 * nr);
+        C->d_part = (double*)take(sizeof(double) * 3 * nr * C->gt_blocks);
+        FEMI_CUDA(cudaMemset(C->d_cnt, 0, sizeof(unsigned) * 2 * nr));
+        double dmin = 0.0;
+        {
+            unsigned long long* d_m = nullptr;
+            unsigned long long h_m = ~0ull;
+            FEMI_CUDA(cudaMalloc(&d_m, sizeof(unsigned long long)));
+            FEMI_CUDA(cudaMemcpy(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice));
+            k_qmin<<<296, 256>>>(n, S->q_int, d_m);
+            FEMI_CUDA(cudaMemcpy(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost));
+            FEMI_CUDA(cudaFree(d_m));
+            double dm;
+            std::memcpy(&dm, &h_m, sizeof(dm));
+            if (std::isfinite(dm) && dm > 0.0) dmin = dm * (1.0 - 1e-12);
+        }
+        C->items.resize(nr);
+        for (int c = 0; c < nr; ++c) {
+            RItem& it = C->items[c];
+            it = RItem{};
+            it.red = (double*)take(sizeof(double) * C->gx);
+            it.b = (double*)take(vb);
+            it.x = (double*)take(vb);
+            it.r = (double*)take(vb);
+            it.w = (double*)take(vb);
+            it.p = (double*)take(vb);
+            it.sv = (double*)take(vb);
+            it.jval = S->jds_val;
+            it.jcol = S->jds_col;
+            it.jmeta = S->jds_meta;
+            it.jeb = S->jds_eb;
+            it.jcb = S->jds_cb;
+            it.ntile = S->jds_ntile;
+            it.jmaxe = S->jds_maxe;
+            it.jkmax = S->jds_kmax;
+            it.jmbytes = S->jds_meta_bytes;
+            it.jpart = d_jpart;
+            it.dmin = dmin;
+            it.inv = S->sell_inv;
+            it.len = S->sell_len;
+            it.base = S->sell_base;
+            it.val = S->sell_val;
+            it.c16 = S->sell_c16;
+            it.c32 = S->sell_c32;
+            it.s = S->s_int;
+            it.q = S->q_int;
+            it.urp = S->uuI_rowptr;
+            it.uci = S->uuI_col;
+            it.uav = S->uuI_val;
+            it.krp = S->ukI_rowptr;
+            it.kci = S->ukI_col;
+            it.kav = S->ukI_val;
+            it.st = C->d_state + c;
+            it.n = (int32_t)n;
+            it.m = (int32_t)S->m;
+            it.cta0 = 0;
+            it.ncta = 1;
+            it.nwin = S->nwin;
+        }
+        S->scratch_m[nr] = C;
+        femi_status s = build_graph_m(*C, false, &C->main);
+        if (s == FEMI_OK) s = build_graph_m(*C, true, &C->restart);
+        if (s != FEMI_OK) return s;
+    }
+    std::vector<RItem> its = C->items;
+    for (int c = 0; c < nr; ++c) {
+        its[c].g = g ? g[c] : nullptr;
+        its[c].bin = bin ? bin[c] : nullptr;
+        its[c].u_vert = u_vert[c];
+        its[c].x0mode = (its[c].g == nullptr && o.x0 == 1) ? 0 : o.x0;
+        its[c].rtol = o.rtol;
+        its[c].max_iter = o.max_iter;
+    }
+    FEMI_CUDA(cudaMemcpyAsync(C->d_items, its.data(), sizeof(RItem) * nr, cudaMemcpyHostToDevice, st));
+    FEMI_CUDA(cudaGraphLaunch(C->main, st));
+    count_launches(10);
+    std::vector<CgState> hs(nr);
+    for (int restarts = 0;; ++restarts) {
+        FEMI_CUDA(cudaMemcpyAsync(hs.data(), C->d_state, sizeof(CgState) * nr, cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        bool again = false;
+        for (int c = 0; c < nr; ++c) {
+            const CgState& h = hs[c];
+            again |= h.status == FEMI_OK && h.iters > 0 && h.iters < h.max_iter && h.bn2 > 0.0 && !(h.res2 <= h.tol2);
+        }
+        if (!again || restarts >= 8) break;
+        FEMI_CUDA(cudaGraphLaunch(C->restart, st));
+        count_launches(6);
+    }
+    femi_status ret = FEMI_OK;
+    int64_t tot = 0, itmax = 0;
+    for (int c = 0; c < nr; ++c) {
+        const CgState& h = hs[c];
+        const double rel = h.bn2 > 0.0 ? std::sqrt(h.res2 / h.bn2) : 0.0;
+        if (iters) iters[c] = h.iters;
+        if (relres) relres[c] = rel;
+        tot += h.iters;
+        itmax = std::max<int64_t>(itmax, h.iters);
+        femi_status sb = (femi_status)h.status;
+        if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
+        if (sb != FEMI_OK && ret == FEMI_OK) ret = sb;
+    }
+    count_launches(2 * ((itmax + kUnroll - 1) / kUnroll) * kUnroll);
+    if (total_iters) *total_iters = tot;
+    if (ret != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)ret) + ")");
+    return ret;
+}
+
+}  // namespace
+
 void pcg_cache_free(femi_system_s* S) {
+    for (int k = 0; k < 5; ++k) {
+        GraphCacheM* M = (GraphCacheM*)S->scratch_m[k];
+        if (!M) continue;
+        if (M->main) cudaGraphExecDestroy(M->main);
+        if (M->restart) cudaGraphExecDestroy(M->restart);
+        if (M->ws) cudaFree(M->ws);
+        delete M;
+        S->scratch_m[k] = nullptr;
+    }
     GraphCache* C = (GraphCache*)S->scratch;
     if (!C) return;
     if (C->main) cudaGraphExecDestroy(C->main);
@@ -1650,6 +2143,41 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         if (graph_mode && B == 1 && S[0]->nnz_uu > 600000 && S[0]->n_u > 0)
             return graph_solve(S[0], g ? g[0] : nullptr, bin ? bin[0] : nullptr, u_vert[0], o, iters, relres, st,
                                total_iters);
+        // a repeated large system (colour channels): shared-matrix multi-RHS, <= 4 per pass
+        bool shared = graph_mode && B > 1 && S[0]->nnz_uu > 600000 && S[0]->n_u > 0 && S[0]->jds_ntile > 0 &&
+                      std::getenv("FEMI_NO_MULTI") == nullptr;
+        for (int b = 1; b < B && shared; ++b) shared = S[b] == S[0];
+        if (shared) {
+            femi_status ret = FEMI_OK;
+            int64_t tot = 0;
+            for (int b0 = 0; b0 < B;) {
+                const int nr = std::min(4, B - b0);
+                int64_t t1 = 0;
+                femi_status sb;
+                if (nr == 1)
+                    sb = graph_solve(S[0], g ? g[b0] : nullptr, bin ? bin[b0] : nullptr, u_vert[b0], o,
+                                     iters ? iters + b0 : nullptr, relres ? relres + b0 : nullptr, st, &t1);
+                else
+                    sb = graph_solve_multi(S[0], nr, g ? g + b0 : nullptr, bin ? bin + b0 : nullptr, u_vert + b0, o,
+                                           iters ? iters + b0 : nullptr, relres ? relres + b0 : nullptr, st, &t1);
+                if (sb == FEMI_E_ARG && nr > 1) {  // ring does not fit: one RHS at a time
+                    for (int c = 0; c < nr; ++c) {
+                        int64_t t2 = 0;
+                        const femi_status s2 =
+                            graph_solve(S[0], g ? g[b0 + c] : nullptr, bin ? bin[b0 + c] : nullptr, u_vert[b0 + c], o,
+                                        iters ? iters + b0 + c : nullptr, relres ? relres + b0 + c : nullptr, st, &t2);
+                        t1 += t2;
+                        if (s2 != FEMI_OK && ret == FEMI_OK) ret = s2;
+                    }
+                } else if (sb != FEMI_OK && ret == FEMI_OK) {
+                    ret = sb;
+                }
+                tot += t1;
+                b0 += nr;
+            }
+            if (total_iters) *total_iters = tot;
+            return ret;
+        }
     }
     // kernel table: [mode 0/1/2][nvec 0/2/3]; grid mode: 768 threads x 1 CTA/SM (shape 1,
     // measured best) or 512 x 2 (shape 0); FEMI_CG_SHAPE selects for experiments

@@ -136,14 +136,16 @@ __global__ void k_scan_apply(int64_t n, const int32_t* __restrict__ cnt, const i
 
 // ---------------------------------------------------------------- per solve
 
+constexpr int kMaxCh = 4;  // colour channels of one raster item (shared mesh)
+
 struct RasterItem {
     const TriRec* tri;
     const int32_t* tp_ptr;
     const uint32_t* tp_pix;
-    const double* u_vert;
-    const double* f;
-    double* u_px;
-    double* e_px;
+    const double* u_vert[kMaxCh];  // per channel
+    const double* f[kMaxCh];       // per channel; f[0] == nullptr: no error map
+    double* u_px[kMaxCh];          // per channel, nullable
+    double* e_px;                  // e = sum over channels of (u_c - f_c)^2
     double* tri_err;
     int32_t* best;
     double* sse;
@@ -181,9 +183,11 @@ __device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_pt
 // exact integer edge functions as planes w = A px + B py + C (S3: w_b = orient(c,a,p),
 // w_c = orient(a,b,p)), D = orient(a,b,c) and its correctly rounded reciprocal, u_a and the
 // differences u_b - u_a, u_c - u_a.
+template <int NC>
 struct RTri {
     int A1, B1, C1, A2, B2, C2, pad0, pad1;
-    double D, rD, db, dc, u[3], pad2;
+    double D, rD;
+    double db[NC], dc[NC], u[NC][3];
 };
 
 __device__ __forceinline__ int tp_x(uint32_t v) { return (int)(v & 0x3fffu); }
@@ -210,22 +214,21 @@ constexpr int RCH = 128;  // list entries per warp chunk (4 x 32 lanes)
 //   order: tri_err += e, best = first strict maximum over non-vertex pixels (ties: lowest
 //   pix) -- the oracle's sequential order, so tri_err and best are bit-identical to it.
 // SSE = sum of per-group partials in group order (k_sse). Deterministic, no atomics on values.
-template <int MINB, int CH>
+template <int MINB, int CH, int NC>
 __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ gpart,
                                                    uint32_t* __restrict__ next, int64_t gstride) {
-    __shared__ RTri tris[RWARPS][32];
+    extern __shared__ __align__(16) unsigned char rsm[];  // RTri<NC> [RWARPS][32] (dynamic: colour > 48 KB)
     __shared__ double e_s[RWARPS][CH];
     __shared__ int p_s[RWARPS][CH];  // pix, or -1 for a vertex pixel (not a candidate)
     const RasterItem& it = items[blockIdx.y];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t T = it.T;
     const int W = it.W;
-    const double* __restrict__ f = it.f;
-    double* __restrict__ u_px = it.u_px;
+    const bool hasf = it.f[0] != nullptr;
     double* __restrict__ e_px = it.e_px;
     const uint32_t* __restrict__ tp_pix = it.tp_pix;
     const int64_t ngroups = (T + 31) / 32;
-    RTri* ws = tris[wid];
+    RTri<NC>* ws = (RTri<NC>*)rsm + 32 * wid;
     double* __restrict__ gp = gpart + gstride * blockIdx.y;
     double* es = e_s[wid];
     int* ps = p_s[wid];
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
         if (t0 + lane < T) {
             const TriRec R = it.tri[t0 + lane];
             const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-            RTri I;
+            RTri<NC> I;
             // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx)
             I.A1 = cy - ay;
             I.B1 = ax - cx;
@@ -254,11 +257,14 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
             I.C2 = (by - ay) * ax - (bx - ax) * ay;
             I.D = (double)orient_xy(ax, ay, bx, by, cx, cy);
             I.rD = __drcp_rn(I.D);
-            I.u[0] = it.u_vert[R.v[0]];
-            I.u[1] = it.u_vert[R.v[1]];
-            I.u[2] = it.u_vert[R.v[2]];
-            I.db = __dsub_rn(I.u[1], I.u[0]);
-            I.dc = __dsub_rn(I.u[2], I.u[0]);
+#pragma unroll
+            for (int ch = 0; ch < NC; ++ch) {
+                I.u[ch][0] = it.u_vert[ch][R.v[0]];
+                I.u[ch][1] = it.u_vert[ch][R.v[1]];
+                I.u[ch][2] = it.u_vert[ch][R.v[2]];
+                I.db[ch] = __dsub_rn(I.u[ch][1], I.u[ch][0]);
+                I.dc[ch] = __dsub_rn(I.u[ch][2], I.u[ch][0]);
+            }
             ws[lane] = I;
         }
         __syncwarp();
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
           for (int c1 = c0; c1 < min(lw.total, c0 + CH); c1 += RCH) {
             uint32_t v[RCH / 32];
             int j[RCH / 32];
-            double fv[RCH / 32];
+            double fv[RCH / 32][NC];
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
                 const int k = c1 + 32 * h + lane;
@@ -289,27 +295,39 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
             }
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h)
-                fv[h] = (f && j[h] < 32) ? f[(int64_t)tp_y(v[h]) * W + tp_x(v[h])] : 0.0;
+#pragma unroll
+                for (int ch = 0; ch < NC; ++ch)
+                    fv[h][ch] = (hasf && j[h] < 32) ? it.f[ch][(int64_t)tp_y(v[h]) * W + tp_x(v[h])] : 0.0;
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
                 if (j[h] >= 32) continue;
                 const int px = tp_x(v[h]), py = tp_y(v[h]);
                 const int pix = py * W + px;
                 const uint32_t cls = v[h] >> 30;
-                const RTri& I = ws[j[h]];
-                double u;
-                if (cls) {
-                    u = I.u[cls - 1];
-                } else {
+                const RTri<NC>& I = ws[j[h]];
+                double lb = 0.0, lc = 0.0;
+                if (!cls) {
+                    // S3 as the paper's barycentric form, IEEE round-to-nearest per operation
+                    // and no contraction: l_b = w_b / D, l_c = w_c / D (shared by the channels),
+                    // u = (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
                     const int w1 = I.A1 * px + I.B1 * py + I.C1;
                     const int w2 = I.A2 * px + I.B2 * py + I.C2;
-                    const double lb = div_rn((double)w1, I.D, I.rD), lc = div_rn((double)w2, I.D, I.rD);
-                    u = __dadd_rn(__dadd_rn(I.u[0], __dmul_rn(lb, I.db)), __dmul_rn(lc, I.dc));
+                    lb = div_rn((double)w1, I.D, I.rD);
+                    lc = div_rn((double)w2, I.D, I.rD);
                 }
-                if (u_px) u_px[pix] = u;
-                if (f) {
-                    const double d = __dsub_rn(u, fv[h]);
-                    const double e = __dmul_rn(d, d);
+                double e = 0.0;
+#pragma unroll
+                for (int ch = 0; ch < NC; ++ch) {
+                    const double u = cls ? I.u[ch][cls - 1]
+                                         : __dadd_rn(__dadd_rn(I.u[ch][0], __dmul_rn(lb, I.db[ch])),
+                                                     __dmul_rn(lc, I.dc[ch]));
+                    if (it.u_px[ch]) it.u_px[ch][pix] = u;
+                    if (hasf) {
+                        const double d = __dsub_rn(u, fv[h][ch]);
+                        e = ch == 0 ? __dmul_rn(d, d) : __dadd_rn(e, __dmul_rn(d, d));  // channel sum in order
+                    }
+                }
+                if (hasf) {
                     if (e_px) e_px[pix] = e;
                     es[c1 - c0 + 32 * h + lane] = e;
                     ps[c1 - c0 + 32 * h + lane] = cls ? -1 : pix;
@@ -318,7 +336,7 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
           }
             __syncwarp();
             // ---- phase 2: lane per triangle, pixel order
-            if (f) {
+            if (hasf) {
                 const int lo = max(my0, c0), hi = min(my1, c0 + CH);
                 for (int k = lo; k < hi; ++k) {
                     const double e = es[k - c0];
@@ -332,11 +350,11 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
             }
             __syncwarp();
         }
-        if (t0 + lane < T && f) {
+        if (t0 + lane < T && hasf) {
             if (it.tri_err) it.tri_err[t0 + lane] = acc;
             if (it.best) it.best[t0 + lane] = bp;
         }
-        if (f) {  // group partial of the SSE (fixed tree order); summed in group order by k_sse
+        if (hasf) {  // group partial of the SSE (fixed tree order); summed in group order by k_sse
             const double gs = warp_sum(t0 + lane < T ? acc : 0.0);
             if (lane == 0) gp[g] = gs;
         }
@@ -349,7 +367,7 @@ __global__ void __launch_bounds__(RT) k_sse(const RasterItem* __restrict__ items
     __shared__ double red[RWARPS];
     __shared__ int flag;
     const RasterItem& it = items[blockIdx.y];
-    if (!it.sse || !it.f) return;
+    if (!it.sse || !it.f[0]) return;
     const int64_t ng = (it.T + 31) / 32;
     const int64_t a = ng * blockIdx.x / gridDim.x, b = ng * (blockIdx.x + 1) / gridDim.x;
     const double* gp = gpart + gstride * blockIdx.y;
@@ -488,46 +506,29 @@ femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     return FEMI_OK;
 }
 
-femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
-                          double* const* u_px, double* const* e_px, double* const* tri_err, int32_t* const* best,
-                          double* const* sse, cudaStream_t st) {
-    if (B <= 0) return FEMI_OK;
-    std::vector<RasterItem> items(B);
+namespace {
+
+// items[b] all with the same channel count nc (1..kMaxCh)
+femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStream_t st) {
+    const int B = (int)items.size();
     int64_t Tmax = 0;
-    for (int b = 0; b < B; ++b) {
-        RasterItem& r = items[b];
-        r.tri = S[b]->tri;
-        r.tp_ptr = S[b]->tp_ptr;
-        r.tp_pix = S[b]->tp_pix;
-        r.u_vert = u_vert[b];
-        r.f = f ? f[b] : nullptr;
-        r.u_px = u_px ? u_px[b] : nullptr;
-        r.e_px = e_px ? e_px[b] : nullptr;
-        r.tri_err = tri_err ? tri_err[b] : nullptr;
-        r.best = best ? best[b] : nullptr;
-        r.sse = sse ? sse[b] : nullptr;
-        r.T = S[b]->T;
-        r.N = (int64_t)S[b]->W * S[b]->H;
-        r.W = S[b]->W;
-        Tmax = std::max(Tmax, r.T);
-    }
-    if (Tmax == 0) return FEMI_OK;
-    static int minb = -1;  // 4 CTAs/SM (<= 64 registers); FEMI_RASTER_MINB=1 -> unconstrained (experiments)
+    for (const RasterItem& r : items) Tmax = std::max(Tmax, r.T);
+    if (B == 0 || Tmax == 0) return FEMI_OK;
     static int resident = 0;
-    if (minb < 0) {
-        const char* e = std::getenv("FEMI_RASTER_MINB");
-        minb = (e && e[0] == '1') ? 1 : 4;
+    if (resident == 0) {
         int dev = 0, nsm = 0, per = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per, minb == 4 ? (const void*)k_raster_tri<4, 128> : (const void*)k_raster_tri<1, 128>, RT, 0));
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_raster_tri<4, 256, 1>, RT,
+                                                                RWARPS * 32 * sizeof(RTri<1>)));
         resident = std::max(1, per) * nsm;
     }
-    // one wave of resident CTAs; 32-triangle groups handed out dynamically in canonical order
+    // one wave of resident CTAs (colour: 2 CTAs/SM); 32-triangle groups handed out dynamically
+    // in canonical order
     const int64_t groups = (Tmax + 31) / 32;
+    const int res = nc == 1 ? resident : resident / 2;
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((groups + RWARPS - 1) / RWARPS,
-                                                              (int64_t)std::max(1, resident / B)));
+                                                              (int64_t)std::max(1, res / B)));
     constexpr int SSEB = 148;
     const size_t bytes_items = sizeof(RasterItem) * B;
     const size_t bytes_gpart = sizeof(double) * (size_t)groups * B;
@@ -543,20 +544,85 @@ femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u
     uint32_t* d_cnt = (uint32_t*)((char*)d_part + al(bytes_part));
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
-    static int ch = -1;  // staging chunk of the per-triangle pass (FEMI_RASTER_CH: 128, 256)
-    if (ch < 0) {
-        const char* e = std::getenv("FEMI_RASTER_CH");
-        ch = e ? std::atoi(e) : 256;
+    const dim3 gr(gx, B);
+    static bool attr = false;
+    if (!attr) {
+        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_tri<2, 128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(RWARPS * 32 * sizeof(RTri<3>))));
+        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_tri<2, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(RWARPS * 32 * sizeof(RTri<4>))));
+        attr = true;
     }
-    if (minb == 4 && ch == 256) k_raster_tri<4, 256><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
-    else if (minb == 4) k_raster_tri<4, 128><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
-    else k_raster_tri<1, 128><<<dim3(gx, B), RT, 0, st>>>(d_items, d_gpart, d_cnt, groups);
+    switch (nc) {
+        case 1:
+            k_raster_tri<4, 256, 1><<<gr, RT, RWARPS * 32 * sizeof(RTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
+            break;
+        case 2:
+            k_raster_tri<2, 128, 2><<<gr, RT, RWARPS * 32 * sizeof(RTri<2>), st>>>(d_items, d_gpart, d_cnt, groups);
+            break;
+        case 3:
+            k_raster_tri<2, 128, 3><<<gr, RT, RWARPS * 32 * sizeof(RTri<3>), st>>>(d_items, d_gpart, d_cnt, groups);
+            break;
+        default:
+            k_raster_tri<2, 128, 4><<<gr, RT, RWARPS * 32 * sizeof(RTri<4>), st>>>(d_items, d_gpart, d_cnt, groups);
+            break;
+    }
     k_sse<<<dim3(SSEB, B), RT, 0, st>>>(d_items, d_gpart, groups, d_part, d_cnt + B);
-    count_launches(1);
-    count_launches(1);
+    count_launches(2);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(base, st));
     return FEMI_OK;
+}
+
+RasterItem raster_item(const femi_system_s* S) {
+    RasterItem r = {};
+    r.tri = S->tri;
+    r.tp_ptr = S->tp_ptr;
+    r.tp_pix = S->tp_pix;
+    r.T = S->T;
+    r.N = (int64_t)S->W * S->H;
+    r.W = S->W;
+    return r;
+}
+
+}  // namespace
+
+femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
+                          double* const* u_px, double* const* e_px, double* const* tri_err, int32_t* const* best,
+                          double* const* sse, cudaStream_t st) {
+    if (B <= 0) return FEMI_OK;
+    std::vector<RasterItem> items(B);
+    for (int b = 0; b < B; ++b) {
+        RasterItem& r = items[b];
+        r = raster_item(S[b]);
+        r.u_vert[0] = u_vert[b];
+        r.f[0] = f ? f[b] : nullptr;
+        r.u_px[0] = u_px ? u_px[b] : nullptr;
+        r.e_px = e_px ? e_px[b] : nullptr;
+        r.tri_err = tri_err ? tri_err[b] : nullptr;
+        r.best = best ? best[b] : nullptr;
+        r.sse = sse ? sse[b] : nullptr;
+    }
+    return launch_raster_items(items, 1, st);
+}
+
+femi_status launch_raster_channels(femi_system_s* S, int nc, const double* const* u_vert, const double* const* f,
+                                   double* const* u_px, double* e_px, double* tri_err, int32_t* best, double* sse,
+                                   cudaStream_t st) {
+    if (nc < 1 || nc > kMaxCh) return FEMI_E_ARG;
+    std::vector<RasterItem> items(1);
+    RasterItem& r = items[0];
+    r = raster_item(S);
+    for (int c = 0; c < nc; ++c) {
+        r.u_vert[c] = u_vert[c];
+        r.f[c] = f ? f[c] : nullptr;
+        r.u_px[c] = u_px ? u_px[c] : nullptr;
+    }
+    r.e_px = e_px;
+    r.tri_err = tri_err;
+    r.best = best;
+    r.sse = sse;
+    return launch_raster_items(items, nc, st);
 }
 
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {

@@ -184,8 +184,8 @@ femi_status select_topk(int64_t n, int64_t k, unsigned long long* d_key, SelStat
 
 }  // namespace
 
-femi_status densify_select(femi_system_s* S, const double* f, const double* u_vert, int64_t b, int32_t* new_px,
-                           int64_t* n_added, cudaStream_t st) {
+femi_status densify_select(femi_system_s* S, int nc, const double* const* f, const double* const* u_vert, int64_t b,
+                           int32_t* new_px, int64_t* n_added, cudaStream_t st) {
     *n_added = 0;
     if (b <= 0) return FEMI_OK;
     const int64_t T = S->T, N = (int64_t)S->W * S->H;
@@ -219,13 +219,8 @@ femi_status densify_select(femi_system_s* S, const double* f, const double* u_ve
         return s;
     };
 
-    femi_system_s* Sv[1] = {S};
-    const double* uv[1] = {u_vert};
-    const double* fv[1] = {f};
-    double* te[1] = {tri_err};
-    int32_t* bs[1] = {best};
-    double* ssev[1] = {sse};
-    rc = launch_raster(1, Sv, uv, fv, nullptr, nullptr, te, bs, ssev, st);
+    // the error map is the channel sum of (u_c - f_c)^2 (one channel: the grey error map)
+    rc = launch_raster_channels(S, nc, u_vert, f, nullptr, nullptr, tri_err, best, sse, st);
     if (rc) return fail(rc);
 
     // ---- triangles: top-b by (tri_err desc, index asc)
@@ -256,8 +251,7 @@ femi_status densify_select(femi_system_s* S, const double* f, const double* u_ve
         if (cudaMallocAsync(&e_px, sizeof(double) * N, st) != cudaSuccess ||
             cudaMallocAsync(&taken, N, st) != cudaSuccess)
             return fail(cuda_fail(cudaGetLastError(), "densify: fill scratch"));
-        double* ev[1] = {e_px};
-        rc = launch_raster(1, Sv, uv, fv, nullptr, ev, nullptr, nullptr, nullptr, st);
+        rc = launch_raster_channels(S, nc, u_vert, f, nullptr, e_px, nullptr, nullptr, nullptr, st);
         if (rc) return fail(rc);
         cudaMemsetAsync(taken, 0, N, st);
         k_mark<<<grid_for(S->nv), ST, 0, st>>>(S->nv, S->vpix, taken); count_launches(1);

@@ -61,7 +61,8 @@ I32P = ctypes.POINTER(ctypes.c_int32)
 SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh_build", "femi_mesh_info_get", "femi_mesh_export",
            "femi_mesh_timing", "femi_mesh_free", "femi_assemble", "femi_system_info_get", "femi_system_export",
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
-           "femi_densify_step", "femi_tonal_optimise"]
+           "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
+           "femi_densify_step_channels"]
 
 
 def lib():
@@ -91,6 +92,9 @@ def lib():
         L.femi_rasterise_error_batched.argtypes = [ctypes.c_int32, P, P, P, P, P, P, P, P, P]
         L.femi_densify_step.argtypes = [P, P, P, ctypes.c_int64, P, ctypes.POINTER(ctypes.c_int64), P]
         L.femi_tonal_optimise.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.POINTER(TonalReport), P]
+        L.femi_rasterise_error_channels.argtypes = [P, ctypes.c_int32, P, P, P, P, P, P, P, P]
+        L.femi_densify_step_channels.argtypes = [P, ctypes.c_int32, P, P, ctypes.c_int64, P,
+                                                 ctypes.POINTER(ctypes.c_int64), P]
         for name in SYMBOLS:
             if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
                             "femi_kernel_launches"):
@@ -255,6 +259,31 @@ def densify_step(system, f, u_vert, b: int, stream=None) -> np.ndarray:
     n = ctypes.c_int64(0)
     _check(lib().femi_densify_step(system._h, _dptr(f, torch.float64), _dptr(u_vert, torch.float64), b, _hptr(out),
                                    ctypes.byref(n), _stream(stream)))
+    return out[: n.value].copy()
+
+
+def rasterise_error_channels(system, u_list, f_list, sse=None, u_px=None, e_px=None, tri_err=None, best=None,
+                             stream=None):
+    """Colour S3+S4 (enqueue only): channels on one mesh, e = sum_c (u_c - f_c)^2."""
+    import torch
+    C = len(u_list)
+    ua = _ptr_array([_dptr(u, torch.float64) for u in u_list])
+    fa = _ptr_array([_dptr(f, torch.float64) for f in f_list]) if f_list is not None else None
+    pa = _ptr_array([_dptr(u, torch.float64) for u in u_px]) if u_px is not None else None
+    _check(lib().femi_rasterise_error_channels(system._h, C, ua, fa, pa, _dptr(e_px, torch.float64),
+                                               _dptr(tri_err, torch.float64), _dptr(best, torch.int32),
+                                               _dptr(sse, torch.float64), _stream(stream)))
+
+
+def densify_step_channels(system, f_list, u_list, b: int, stream=None) -> np.ndarray:
+    """Colour S5: new mask pixels chosen from the channel-summed error."""
+    import torch
+    out = np.zeros(max(b, 1), np.int32)
+    n = ctypes.c_int64(0)
+    fa = _ptr_array([_dptr(f, torch.float64) for f in f_list])
+    ua = _ptr_array([_dptr(u, torch.float64) for u in u_list])
+    _check(lib().femi_densify_step_channels(system._h, len(f_list), fa, ua, b, _hptr(out), ctypes.byref(n),
+                                            _stream(stream)))
     return out[: n.value].copy()
 
 

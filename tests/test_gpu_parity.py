@@ -272,3 +272,58 @@ def test_config5_full_size():
     per-triangle errors and MSE against the oracle on the same densified mask."""
     c, mask = _c5_like(8192, None)
     check_inpaint(8192, 8192, c["f"], mask, c["unknowns"])
+
+
+def _colour_case(W, seed, density=0.02):
+    """Three seeded channels (the synthetic recipe with different draws) on one mask."""
+    fs = [make_config(5, W=W, H=W, seed=seed + k)["f"].reshape(-1) for k in range(3)]
+    rng = np.random.default_rng(seed)
+    m = int(density * W * W)
+    mk = draw_mask(rng, W * W, m)
+    un = draw_unknowns(rng, W, W, mk, m)
+    return fs, mk, un
+
+
+@pytest.mark.parametrize("W", [96, 2880])
+def test_colour_shared_mesh(W):
+    """NEXT-1 colour: three channels on one mesh. The solve (the system handle repeated:
+    shared-matrix multi-RHS CG on large systems) matches the oracle per channel and equals
+    the one-channel-at-a-time solve bit for bit; the colour raster / error map / per-triangle
+    reductions equal the oracle's raster_channels bit for bit; densify_step_channels equals
+    the oracle's selection on the channel-summed error."""
+    fs, mk, un = _colour_case(W, 71)
+    M = femi.Mesh(W, W, mk, un)
+    S = femi.System(M)
+    vert = M.export()["vert_px"]
+    fd = [dev(f) for f in fs]
+    gs = [pipeline.mask_values(f, vert, S.n_u) for f in fd]
+    us = [torch.empty(S.nv, dtype=torch.float64, device=DEV) for _ in range(3)]
+    st, it, rel = femi.inpaint_solve_batched([S] * 3, gs, us, femi.cg_opts(rtol=1e-10))
+    assert st == 0 and np.all(rel <= 1e-10)
+    for k in range(3):  # one channel at a time: identical iterates
+        u1 = torch.empty_like(us[k])
+        st1, it1, _ = femi.inpaint_solve_batched([S], [gs[k]], [u1], femi.cg_opts(rtol=1e-10))
+        assert st1 == 0 and it1[0] == it[k]
+        assert torch.equal(u1, us[k])
+    O = oracle.System(W, W, mk, un)
+    for k in range(3):
+        uo = O.solve(fs[k][O.mask_px], rtol=1e-12)[0]
+        assert np.abs(us[k].cpu().numpy() - uo).max() <= GREY_TOL
+    N = W * W
+    upx = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(3)]
+    e_px = torch.empty(N, dtype=torch.float64, device=DEV)
+    te = torch.empty(S.T, dtype=torch.float64, device=DEV)
+    bs = torch.empty(S.T, dtype=torch.int32, device=DEV)
+    sse = torch.zeros(1, dtype=torch.float64, device=DEV)
+    femi.rasterise_error_channels(S, us, fd, sse, upx, e_px, te, bs)
+    uh = [u.cpu().numpy() for u in us]
+    R = O.raster_channels(uh, fs)
+    for k in range(3):
+        np.testing.assert_array_equal(upx[k].cpu().numpy(), R["u_px"][k])
+    np.testing.assert_array_equal(e_px.cpu().numpy(), R["e_px"])
+    np.testing.assert_array_equal(te.cpu().numpy(), R["tri_err"])
+    np.testing.assert_array_equal(bs.cpu().numpy(), R["best"])
+    assert abs(sse.item() - R["sse"]) <= 1e-9 * R["sse"]  # grouped vs sequential fp64 sum of N terms
+    b = max(1, int(0.002 * N))
+    new = femi.densify_step_channels(S, fd, us, b)
+    np.testing.assert_array_equal(new, oracle.select(R["tri_err"], R["best"], R["e_px"], O.is_vertex(), b))

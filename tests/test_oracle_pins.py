@@ -482,6 +482,46 @@ def test_p11_mse_golden_and_sums():
             assert R["best"][t] == cand[np.argmax(e[cand])]
 
 
+# ---------------------------------------------------------------- colour (NEXT-1)
+
+def test_colour_raster_pins():
+    """PAPER.md:L521-524 colour = channels on one mesh; error map = channel sum.
+    Pinned against the grey raster: one channel equals it bit for bit; C channels give the
+    channel-order sum of the per-channel error maps, per-triangle sums in pixel order, the
+    first strict maximum over non-vertex pixels, and SSE as the pixel-order sum."""
+    c = make_config(1)
+    W, H = c["W"], c["H"]
+    N = W * H
+    S = oracle.System(W, H, c["mask"], c["unknowns"])
+    rng = np.random.default_rng(3)
+    fs = [c["f"].reshape(-1), rng.uniform(0, 255, N), np.full(N, 17.0)]
+    us = [S.solve(f[S.mask_px])[0] for f in fs]
+    R1 = S.raster(us[0], fs[0])
+    C1 = S.raster_channels(us[:1], fs[:1])
+    for k in ("e_px", "tri_err", "best"):
+        np.testing.assert_array_equal(C1[k], R1[k])
+    np.testing.assert_array_equal(C1["u_px"][0], R1["u_px"])
+    assert C1["sse"] == R1["sse"]
+    per = [S.raster(u, f) for u, f in zip(us, fs)]
+    C3 = S.raster_channels(us, fs)
+    e = (per[0]["e_px"] + per[1]["e_px"]) + per[2]["e_px"]
+    np.testing.assert_array_equal(C3["e_px"], e)
+    for k in range(3):
+        np.testing.assert_array_equal(C3["u_px"][k], per[k]["u_px"])
+    te = np.zeros(S.T)
+    np.add.at(te, S.owner, e)  # unbuffered, in pixel order
+    np.testing.assert_array_equal(C3["tri_err"], te)
+    isv = S.is_vertex()
+    for t in range(S.T):
+        pix = np.nonzero(S.owner == t)[0]
+        cand = pix[isv[pix] == 0]
+        assert C3["best"][t] == (cand[np.argmax(e[cand])] if cand.size else -1)
+    assert C3["sse"] == float(np.cumsum(e)[-1])
+    # three identical channels: e = fl(3 e_1) (2 e_1 is exact)
+    C33 = S.raster_channels([us[0]] * 3, [fs[0]] * 3)
+    np.testing.assert_array_equal(C33["e_px"], 3.0 * R1["e_px"])
+
+
 # ---------------------------------------------------------------- P12 conditional DMP
 
 def _m_matrix(S):
