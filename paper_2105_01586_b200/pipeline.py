@@ -5,6 +5,8 @@
                   iteration inpaints on the current mesh and inserts b_t pixels chosen by
                   densify_step; the host merges the mask and re-meshes.
     tonal()    -- tonal_optimise on a fixed mesh with g0 = f at the mask.
+    inpaint_channels() / densify_channels() -- colour: channels on one
+                  mesh, one shared-matrix multi-RHS solve, channel-summed error map.
 """
 from __future__ import annotations
 
@@ -74,3 +76,33 @@ def tonal(W, H, f_dev, mask_px, unknown_px, outer_rtol=1e-8, outer_max=1000, inn
     st, rep = femi.tonal_optimise(sysm, f_dev.reshape(-1), g, outer_rtol, outer_max, femi.cg_opts(rtol=inner_rtol),
                                   stream)
     return g, rep, dict(mesh=mesh, system=sysm, vert_px=vert, status=st)
+
+
+def inpaint_channels(W, H, f_list, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None):
+    """Colour inpainting: every channel on the same mask/mesh; the error is the channel sum."""
+    torch = _torch()
+    mesh = femi.Mesh(W, H, mask_px, unknown_px)
+    sysm = femi.System(mesh, stream)
+    vert = mesh.export()["vert_px"]
+    dev = f_list[0].device
+    gs = [mask_values(f, vert, sysm.n_u) for f in f_list]
+    us = [torch.empty(sysm.nv, dtype=torch.float64, device=dev) for _ in f_list]
+    st, iters, rel = femi.inpaint_solve_batched([sysm] * len(f_list), gs, us, femi.cg_opts(rtol=rtol), stream)
+    sse = torch.zeros(1, dtype=torch.float64, device=dev)
+    u_px = [torch.empty(W * H, dtype=torch.float64, device=dev) for _ in f_list] if want_images else None
+    e_px = torch.empty(W * H, dtype=torch.float64, device=dev) if want_images else None
+    femi.rasterise_error_channels(sysm, us, [f.reshape(-1) for f in f_list], sse, u_px, e_px, stream=stream)
+    return dict(mesh=mesh, system=sysm, vert_px=vert, u_vert=us, u_px=u_px, e_px=e_px, sse=sse, status=st,
+                iters=[int(i) for i in iters], relres=[float(r) for r in rel])
+
+
+def densify_channels(W, H, f_list, mask0, unknown_px, schedule, rtol=1e-10, stream=None):
+    """Colour densification: insertion driven by the channel-summed error map."""
+    _torch()
+    mask = np.sort(np.asarray(mask0, dtype=np.int64))
+    for t in range(1, len(schedule)):
+        R = inpaint_channels(W, H, f_list, mask, unknown_px, rtol=rtol, want_images=False, stream=stream)
+        new = femi.densify_step_channels(R["system"], [f.reshape(-1) for f in f_list], R["u_vert"], int(schedule[t]),
+                                         stream)
+        mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
+    return mask
