@@ -237,6 +237,31 @@ typedef struct {
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                 femi_tonal_report* report, femi_stream stream);
 
+/* ---------------------------------------------------------------------------------
+ * L1 tonal optimisation (DEVICE + host report). PAPER.md:L524-526:
+ * "we have ... optimised the L1 error instead of the L2 one"; the paper does not give the
+ * method. Reading R3: iteratively reweighted least squares -- `irls`
+ * reweightings, each setting w_i = 1 / max(|f_i - (B g)_i|, eps) and minimising
+ * || W^1/2 (B g - f) ||^2 by the weighted nested CGLS of femi_tonal_optimise, warm-started
+ * from the current g (opts as there: outer_rtol bounds the weighted relative gradient).
+ *   f[W*H], g[n_mask]: as femi_tonal_optimise; irls >= 0; eps > 0 (0-255 scale; 1 is the
+ *   SPEC default).
+ *   report: HOST; l1_before / l1_after = mean |f - B g| at entry / exit.
+ * Synchronises `stream`. Errors: as femi_tonal_optimise.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t irls_steps;
+    int32_t outer_iters;  /* summed over the reweightings */
+    int32_t inner_solves;
+    int32_t pad;
+    int64_t inner_iters;
+    double l1_before, l1_after;
+    double mse_before, mse_after;
+} femi_tonal_l1_report;
+
+femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
+                                   int32_t irls, double eps, femi_tonal_l1_report* report, femi_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,8 @@ Parity status per function:
   raster_channels (colour) ......... pinned (C = 1 equals raster; channel sum of per-channel maps)
   select ........................... pinned (P16, brute-force re-derivation on tiny cases)
   tonal ............................ pinned (P13 dense lstsq, P14, P15)
+  tonal_weighted / tonal_l1 (IRLS) . pinned (unit weights = tonal bit for bit; weighted dense lstsq;
+                                     uniform weights = L2 solution; L1 error <= the L2 solution's)
 """
 from __future__ import annotations
 
@@ -71,6 +73,12 @@ def lib():
         L.orc_sys_raster_channels.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_void_p, f64p, f64p, i32p, ctypes.POINTER(ctypes.c_double)]
         L.orc_sys_raster_channels.restype = None
+        L.orc_sys_tonal_w.argtypes = [ctypes.c_void_p, f64p, ctypes.c_void_p, f64p, ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_double, ctypes.c_int, f64p]
+        L.orc_sys_tonal_w.restype = ctypes.c_int
+        L.orc_sys_tonal_l1.argtypes = [ctypes.c_void_p, f64p, f64p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_int, ctypes.c_double, f64p]
+        L.orc_sys_tonal_l1.restype = ctypes.c_int
         L.orc_select.restype = ctypes.c_int64
         L.orc_select.argtypes = [ctypes.c_int64, f64p, i32p, ctypes.c_int64, f64p, u8p, ctypes.c_int64, i32p]
         L.orc_sys_apply_B.restype = ctypes.c_int
@@ -250,6 +258,29 @@ class System:
         return g, dict(outer_iters=int(rep[0]), inner_solves=int(rep[1]), inner_iters=int(rep[2]),
                        rel_grad=rep[3], mse_before=rep[4], mse_after=rep[5], status=int(st),
                        rel_grad_recursive=rep[7])
+
+
+def tonal_weighted(S, f, sw, g0=None, outer_tol: float = 1e-8, outer_max: int = 1000, inner_rtol: float = 1e-12):
+    """Weighted CGLS: min || diag(sw) (B g - f) ||^2 (one IRLS step; sw = None: plain tonal)."""
+    f = np.ascontiguousarray(f, np.float64).reshape(-1)
+    g = np.array(f[S.mask_px] if g0 is None else g0, dtype=np.float64)
+    swa = None if sw is None else np.ascontiguousarray(sw, np.float64).reshape(-1)
+    rep = np.zeros(8)
+    st = lib().orc_sys_tonal_w(S._h, f, None if swa is None else swa.ctypes.data_as(ctypes.c_void_p), g, outer_tol,
+                               outer_max, inner_rtol, 0, rep)
+    return g, dict(outer_iters=int(rep[0]), inner_solves=int(rep[1]), rel_grad=rep[3], mse_before=rep[4],
+                   mse_after=rep[5], status=int(st))
+
+
+def tonal_l1(S, f, irls: int = 3, eps: float = 1.0, g0=None, outer_tol: float = 1e-8, outer_max: int = 1000,
+             inner_rtol: float = 1e-12):
+    """L1 tonal optimisation by IRLS (reading R3)."""
+    f = np.ascontiguousarray(f, np.float64).reshape(-1)
+    g = np.array(f[S.mask_px] if g0 is None else g0, dtype=np.float64)
+    rep = np.zeros(8)
+    st = lib().orc_sys_tonal_l1(S._h, f, g, irls, eps, outer_tol, outer_max, inner_rtol, rep)
+    return g, dict(outer_iters=int(rep[0]), inner_solves=int(rep[1]), inner_iters=int(rep[2]), l1_before=rep[3],
+                   l1_after=rep[4], mse_after=rep[5], status=int(st))
 
 
 def select(tri_err, best, e_px, is_vertex, b: int) -> np.ndarray:

@@ -819,8 +819,18 @@ int orc_sys_apply_BT(OrcSys* S, const double* r, double* s, double rtol) {
  * ||B^T f|| < outer_tol on the recursive gradient; at exit the gradient and MSE are
  * recomputed with fresh solves. report[0..7] = outer_iters, inner_solves, inner_iters,
  * rel_grad, mse_before, mse_after, status, rel_grad_recursive. */
+/* Weighted CGLS (IRLS step, NEXT-2): minimise || W^1/2 (B g - f) ||^2 with per-pixel sqrt
+ * weights sw (NULL = all ones: plain tonal optimisation). B_w = diag(sw) B, f_w = sw f. */
+int orc_sys_tonal_w(OrcSys* S, const double* f, const double* sw, double* g, double outer_tol, int outer_max,
+                    double inner_rtol, int inner_method, double* report);
+
 int orc_sys_tonal(OrcSys* S, const double* f, double* g, double outer_tol, int outer_max,
                   double inner_rtol, int inner_method, double* report) {
+    return orc_sys_tonal_w(S, f, NULL, g, outer_tol, outer_max, inner_rtol, inner_method, report);
+}
+
+int orc_sys_tonal_w(OrcSys* S, const double* f, const double* sw, double* g, double outer_tol, int outer_max,
+                    double inner_rtol, int inner_method, double* report) {
     i64 N = (i64)S->W * S->H, m = S->m;
     double* u = (double*)malloc(sizeof(double) * (size_t)N);
     double* r = (double*)malloc(sizeof(double) * (size_t)N);
@@ -831,24 +841,35 @@ int orc_sys_tonal(OrcSys* S, const double* f, double* g, double outer_tol, int o
     double* w = (double*)malloc(sizeof(double) * (size_t)S->nv);
     double* y = (double*)malloc(sizeof(double) * (size_t)(S->n_u + 1));
     Inner in = {1, inner_rtol, 100000, inner_method, 0, 0, 0};
+    double* fw = (double*)malloc(sizeof(double) * (size_t)N); /* W^1/2 f */
+    for (i64 p = 0; p < N; ++p) fw[p] = sw ? sw[p] * f[p] : f[p];
     apply_B(S, g, u, uv, &in);
     for (i64 p = 0; p < N; ++p) r[p] = f[p] - u[p];
     double mse_before = dot(N, r, r) / (double)N;
-    apply_BT(S, f, s, w, y, &in); /* ||B^T f|| for the relative stopping rule */
+    if (sw) for (i64 p = 0; p < N; ++p) r[p] = sw[p] * r[p];
+    for (i64 p = 0; p < N; ++p) q[p] = sw ? sw[p] * fw[p] : fw[p]; /* B_w^T f_w = B^T (W f) */
+    apply_BT(S, q, s, w, y, &in); /* ||B_w^T f_w|| for the relative stopping rule */
     double btf = sqrt(dot(m, s, s));
-    apply_BT(S, r, s, w, y, &in);
+    for (i64 p = 0; p < N; ++p) q[p] = sw ? sw[p] * r[p] : r[p];
+    apply_BT(S, q, s, w, y, &in);
     for (i64 k = 0; k < m; ++k) pdir[k] = s[k];
     double gam = dot(m, s, s);
     int outer = 0;
     double relg = btf > 0.0 ? sqrt(gam) / btf : 0.0;
     while (relg >= outer_tol && outer < outer_max) {
         apply_B(S, pdir, q, uv, &in);
+        if (sw) for (i64 p = 0; p < N; ++p) q[p] = sw[p] * q[p];
         double qq = dot(N, q, q);
         if (!(qq > 0.0)) break;
         double alpha = gam / qq;
         for (i64 k = 0; k < m; ++k) g[k] = g[k] + alpha * pdir[k];
         for (i64 p = 0; p < N; ++p) r[p] = r[p] - alpha * q[p];
-        apply_BT(S, r, s, w, y, &in);
+        if (sw) {
+            for (i64 p = 0; p < N; ++p) q[p] = sw[p] * r[p];
+            apply_BT(S, q, s, w, y, &in);
+        } else {
+            apply_BT(S, r, s, w, y, &in);
+        }
         double gam2 = dot(m, s, s);
         ++outer;
         relg = sqrt(gam2) / btf;
@@ -861,10 +882,57 @@ int orc_sys_tonal(OrcSys* S, const double* f, double* g, double outer_tol, int o
     apply_B(S, g, u, uv, &in);
     for (i64 p = 0; p < N; ++p) r[p] = f[p] - u[p];
     double mse_after = dot(N, r, r) / (double)N;
-    apply_BT(S, r, s, w, y, &in);
+    for (i64 p = 0; p < N; ++p) q[p] = sw ? (sw[p] * sw[p]) * r[p] : r[p];
+    apply_BT(S, q, s, w, y, &in);
     report[0] = outer; report[1] = (double)in.solves; report[2] = (double)in.iters;
     report[3] = btf > 0.0 ? sqrt(dot(m, s, s)) / btf : 0.0;
     report[4] = mse_before; report[5] = mse_after; report[6] = in.status; report[7] = relg_rec;
-    free(u); free(r); free(q); free(s); free(pdir); free(uv); free(w); free(y);
+    free(u); free(r); free(q); free(s); free(pdir); free(uv); free(w); free(y); free(fw);
     return in.status;
 }
+
+/* L1 tonal optimisation by iteratively reweighted least squares ("optimised
+ * the L1 error instead of the L2 one"; the method is unstated there, IRLS with weights
+ * w_i = 1 / max(|r_i|, eps) is SPEC.md:L366-374's reading, R3): each of `irls`
+ * steps computes r = f - B g, sets sqrt weights 1/sqrt(max(|r_i|, eps)) and runs the weighted
+ * CGLS from the current g. report: [0] outer iterations (all steps), [1] inner solves,
+ * [2] inner CG iterations, [3] L1 before, [4] L1 after (mean |f - B g|), [5] MSE after. */
+int orc_sys_tonal_l1(OrcSys* S, const double* f, double* g, int irls, double eps, double outer_tol, int outer_max,
+                     double inner_rtol, double* report) {
+    i64 N = (i64)S->W * S->H;
+    double* u = (double*)malloc(sizeof(double) * (size_t)N);
+    double* sw = (double*)malloc(sizeof(double) * (size_t)N);
+    double* uv = (double*)malloc(sizeof(double) * (size_t)S->nv);
+    double rep[8];
+    int st = 0;
+    double outer = 0, solves = 0, iters = 0, l1_before = 0.0;
+    Inner in = {1, inner_rtol, 100000, 0, 0, 0, 0};
+    for (int k = 0; k <= irls; ++k) {
+        apply_B(S, g, u, uv, &in);
+        double l1 = 0.0;
+        for (i64 p = 0; p < N; ++p) l1 = l1 + fabs(f[p] - u[p]);
+        if (k == 0) l1_before = l1 / (double)N;
+        if (k == irls) {
+            double mse = 0.0;
+            for (i64 p = 0; p < N; ++p) mse = mse + (f[p] - u[p]) * (f[p] - u[p]);
+            report[4] = l1 / (double)N;
+            report[5] = mse / (double)N;
+            break;
+        }
+        for (i64 p = 0; p < N; ++p) {
+            double a = fabs(f[p] - u[p]);
+            sw[p] = 1.0 / sqrt(a > eps ? a : eps);
+        }
+        int s1 = orc_sys_tonal_w(S, f, sw, g, outer_tol, outer_max, inner_rtol, 0, rep);
+        if (s1 && !st) st = s1;
+        outer += rep[0];
+        solves += rep[1];
+        iters += rep[2];
+    }
+    report[0] = outer; report[1] = solves + (double)in.solves; report[2] = iters + (double)in.iters;
+    report[3] = l1_before;
+    if (in.status && !st) st = in.status;
+    free(u); free(sw); free(uv);
+    return st;
+}
+

@@ -633,6 +633,26 @@ femi_status femi_densify_step_channels(femi_system sys, int32_t C, const double*
     return densify_select(sys, C, f, u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
 }
 
+femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
+                                   int32_t irls, double eps, femi_tonal_l1_report* report, femi_stream stream) {
+    if (!sys || !f || !g || !opts || !report || irls < 0 || !(eps > 0.0)) {
+        set_error("tonal_optimise_l1: NULL argument, irls < 0 or eps <= 0");
+        return FEMI_E_ARG;
+    }
+    if (!(opts->outer_rtol > 0.0) || opts->outer_max < 0 || !(opts->inner.rtol > 0.0) || opts->inner.max_iter <= 0 ||
+        opts->warm_start != 0) {
+        set_error("tonal_optimise_l1: invalid options");
+        return FEMI_E_ARG;
+    }
+    femi_status s = check_device();
+    if (s) return s;
+    if (sys->n_u == 0 || sys->m == 0) {
+        *report = femi_tonal_l1_report{};
+        return FEMI_OK;
+    }
+    return tonal_irls(sys, f, g, *opts, irls, eps, report, (cudaStream_t)stream);
+}
+
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                 femi_tonal_report* report, femi_stream stream) {
     if (!sys || !f || !g || !opts || !report) {

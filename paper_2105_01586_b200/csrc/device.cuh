@@ -191,7 +191,9 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
 femi_status densify_select(femi_system_s* S, int nc, const double* const* f, const double* const* u_vert, int64_t b,
                            int32_t* new_px, int64_t* n_added, cudaStream_t st);
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
-                       femi_tonal_report* rep, cudaStream_t st);
+                       femi_tonal_report* rep, cudaStream_t st, const double* sw = nullptr);
+femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o, int irls, double eps,
+                       femi_tonal_l1_report* rep, cudaStream_t st);
 
 // device helpers
 // release/acquire at gpu scope: the last-arriver pattern needs only these, not the

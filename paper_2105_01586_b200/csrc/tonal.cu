@@ -10,6 +10,7 @@
 // the forward raster) producing three partial sums per triangle, gathered per vertex over
 // the vertex->triangle incidence list in ascending triangle order (deterministic).
 #include <cmath>
+#include <vector>
 
 #include "device.cuh"
 
@@ -66,6 +67,34 @@ __global__ void k_xpby(int64_t n, const double* __restrict__ x, double beta, dou
 __global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = a[i] - b[i];
+}
+// out = a x (the IRLS sqrt weights applied to a pixel vector; out may alias x)
+__global__ void k_mul(int64_t n, const double* __restrict__ a, const double* x, double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[i] * x[i];
+}
+// out = a (a x) (the weighted right-hand side W f, as the oracle rounds it)
+__global__ void k_mul_aax(int64_t n, const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[i] * (a[i] * x[i]);
+}
+// out = (a a) x (the weighted gradient at exit)
+__global__ void k_mul_a2x(int64_t n, const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (a[i] * a[i]) * x[i];
+}
+// IRLS: sqrt weights 1/sqrt(max(|f - u|, eps)) and the partial sums of |f - u| (L1 error)
+__global__ void k_irls_weights(int64_t n, const double* __restrict__ f, const double* __restrict__ u, double eps,
+                               double* __restrict__ sw, double* __restrict__ part) {
+    __shared__ double red[TT / 32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)TT + threadIdx.x; i < n; i += (int64_t)gridDim.x * TT) {
+        const double a = fabs(f[i] - u[i]);
+        s += a;
+        if (sw) sw[i] = 1.0 / sqrt(a > eps ? a : eps);
+    }
+    s = block_sum<TT>(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + TT - 1) / TT, 148 * 8)); }
@@ -146,7 +175,7 @@ struct Tonal {
 }  // namespace
 
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
-                       femi_tonal_report* rep, cudaStream_t st) {
+                       femi_tonal_report* rep, cudaStream_t st, const double* sw) {
     const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t bytes = 3 * al(sizeof(double) * nv) + al(sizeof(double) * 3 * T) + al(sizeof(double) * 300) +
@@ -183,25 +212,49 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     {
         double rr = 0, btf2 = 0, gam = 0, qq = 0, gam2 = 0;
         int outer = 0;
+        // sw (IRLS sqrt weights, nullable): minimise || W^1/2 (B g - f) ||: B_w = diag(sw) B
         TRY(tn.apply_B(g, u));
         k_sub<<<grid_for(N), TT, 0, st>>>(N, f, u, r); count_launches(1);
         TRY(tn.dot(N, r, r, &rr));
         rep->mse_before = rr / (double)N;
-        TRY(tn.apply_BT(f, s));
+        if (sw) {
+            k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, r, r);
+            k_mul_aax<<<grid_for(N), TT, 0, st>>>(N, sw, f, u);  // B_w^T f_w = B^T (sw (sw f))
+            count_launches(2);
+            TRY(tn.apply_BT(u, s));
+        } else {
+            TRY(tn.apply_BT(f, s));
+        }
         TRY(tn.dot(m, s, s, &btf2));
         const double btf = std::sqrt(btf2);
-        TRY(tn.apply_BT(r, s));
+        if (sw) {
+            k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, r, u);
+            count_launches(1);
+            TRY(tn.apply_BT(u, s));
+        } else {
+            TRY(tn.apply_BT(r, s));
+        }
         FEMI_CUDA(cudaMemcpyAsync(p, s, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
         TRY(tn.dot(m, s, s, &gam));
         double relg = btf > 0.0 ? std::sqrt(gam) / btf : 0.0;
         while (relg >= o.outer_rtol && outer < o.outer_max) {
             TRY(tn.apply_B(p, q));
+            if (sw) {
+                k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, q, q);
+                count_launches(1);
+            }
             TRY(tn.dot(N, q, q, &qq));
             if (!(qq > 0.0)) break;
             const double alpha = gam / qq;
             k_axpy<<<grid_for(m), TT, 0, st>>>(m, alpha, p, g); count_launches(1);
             k_axpy<<<grid_for(N), TT, 0, st>>>(N, -alpha, q, r); count_launches(1);
-            TRY(tn.apply_BT(r, s));
+            if (sw) {
+                k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, r, u);
+                count_launches(1);
+                TRY(tn.apply_BT(u, s));
+            } else {
+                TRY(tn.apply_BT(r, s));
+            }
             TRY(tn.dot(m, s, s, &gam2));
             ++outer;
             relg = std::sqrt(gam2) / btf;
@@ -223,7 +276,13 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
         k_sub<<<grid_for(N), TT, 0, st>>>(N, f, u, r); count_launches(1);
         TRY(tn.dot(N, r, r, &rr));
         rep->mse_after = rr / (double)N;
-        TRY(tn.apply_BT(r, s));
+        if (sw) {
+            k_mul_a2x<<<grid_for(N), TT, 0, st>>>(N, sw, r, u);
+            count_launches(1);
+            TRY(tn.apply_BT(u, s));
+        } else {
+            TRY(tn.apply_BT(r, s));
+        }
         TRY(tn.dot(m, s, s, &gam2));
         rep->rel_grad = btf > 0.0 ? std::sqrt(gam2) / btf : 0.0;
         if (relg >= o.outer_rtol && outer >= o.outer_max) tn.note(FEMI_E_NOT_CONVERGED);
@@ -236,6 +295,79 @@ out:
     if (rc != FEMI_OK) return rc;
     if (tn.status != FEMI_OK) set_error("tonal_optimise: an inner solve or the outer loop did not converge");
     return tn.status;
+}
+
+// L1 tonal optimisation by IRLS (reading R3): `irls`
+// reweightings, each computing r = f - B g, sqrt weights 1/sqrt(max(|r|, eps)) and a weighted
+// CGLS from the current g; the L1 error mean|f - B g| is reported before and after.
+femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o, int irls, double eps,
+                       femi_tonal_l1_report* rep, cudaStream_t st) {
+    const int64_t N = (int64_t)S->W * S->H, nv = S->nv;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    void* base = nullptr;
+    FEMI_CUDA(cudaMallocAsync(&base, 2 * al(sizeof(double) * N) + al(sizeof(double) * nv) + al(sizeof(double) * 300),
+                              st));
+    double* u = (double*)base;
+    double* sw = (double*)((char*)u + al(sizeof(double) * N));
+    double* uv = (double*)((char*)sw + al(sizeof(double) * N));
+    double* part = (double*)((char*)uv + al(sizeof(double) * nv));
+    femi_status rc = FEMI_OK, note = FEMI_OK;
+    *rep = femi_tonal_l1_report{};
+    for (int k = 0; k <= irls; ++k) {
+        // u = B g (one inner solve + raster)
+        femi_cg_opts io = o.inner;
+        io.x0 = 1;
+        int32_t it = 0;
+        double rr = 0.0;
+        int64_t tot = 0;
+        femi_system_s* Sv[1] = {S};
+        const double* gv[1] = {g};
+        double* uvv[1] = {uv};
+        femi_status s1 = pcg_solve(1, Sv, gv, nullptr, uvv, io, &it, &rr, st, &tot);
+        rep->inner_solves += 1;
+        rep->inner_iters += tot;
+        if (s1 == FEMI_E_NONFINITE || s1 == FEMI_E_CUDA || s1 == FEMI_E_OOM) {
+            rc = s1;
+            break;
+        }
+        if (s1 != FEMI_OK && note == FEMI_OK) note = s1;
+        const double* uvc[1] = {uv};
+        double* upx[1] = {u};
+        if ((rc = launch_raster(1, Sv, uvc, nullptr, upx, nullptr, nullptr, nullptr, nullptr, st))) break;
+        const int nb = 296;
+        k_irls_weights<<<nb, TT, 0, st>>>(N, f, u, eps, k < irls ? sw : nullptr, part);
+        count_launches(1);
+        std::vector<double> hp(nb);
+        if (cudaMemcpyAsync(hp.data(), part, sizeof(double) * nb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            rc = cuda_fail(cudaGetLastError(), "tonal_l1: readback");
+            break;
+        }
+        double l1 = 0.0;
+        for (double v : hp) l1 += v;
+        l1 /= (double)N;
+        if (k == 0) rep->l1_before = l1;
+        if (k == irls) {
+            rep->l1_after = l1;
+            break;
+        }
+        femi_tonal_report r2{};
+        femi_status s2 = tonal_cgls(S, f, g, o, &r2, st, sw);
+        if (k == 0) rep->mse_before = r2.mse_before;
+        rep->mse_after = r2.mse_after;
+        rep->irls_steps += 1;
+        rep->outer_iters += r2.outer_iters;
+        rep->inner_solves += r2.inner_solves;
+        rep->inner_iters += r2.inner_iters;
+        if (s2 == FEMI_E_NONFINITE || s2 == FEMI_E_CUDA || s2 == FEMI_E_OOM) {
+            rc = s2;
+            break;
+        }
+        if (s2 != FEMI_OK && note == FEMI_OK) note = s2;
+    }
+    cudaFreeAsync(base, st);
+    if (rc != FEMI_OK) return rc;
+    return note;
 }
 
 }  // namespace femi

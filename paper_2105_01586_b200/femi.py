@@ -53,6 +53,15 @@ class TonalReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class TonalL1Report(ctypes.Structure):
+    _fields_ = [("irls_steps", ctypes.c_int32), ("outer_iters", ctypes.c_int32), ("inner_solves", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("inner_iters", ctypes.c_int64), ("l1_before", ctypes.c_double),
+                ("l1_after", ctypes.c_double), ("mse_before", ctypes.c_double), ("mse_after", ctypes.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad"}
+
+
 _lib = None
 P = ctypes.c_void_p
 I32P = ctypes.POINTER(ctypes.c_int32)
@@ -62,7 +71,7 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_mesh_timing", "femi_mesh_free", "femi_assemble", "femi_system_info_get", "femi_system_export",
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
-           "femi_densify_step_channels"]
+           "femi_densify_step_channels", "femi_tonal_optimise_l1"]
 
 
 def lib():
@@ -95,6 +104,8 @@ def lib():
         L.femi_rasterise_error_channels.argtypes = [P, ctypes.c_int32, P, P, P, P, P, P, P, P]
         L.femi_densify_step_channels.argtypes = [P, ctypes.c_int32, P, P, ctypes.c_int64, P,
                                                  ctypes.POINTER(ctypes.c_int64), P]
+        L.femi_tonal_optimise_l1.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.c_int32, ctypes.c_double,
+                                             ctypes.POINTER(TonalL1Report), P]
         for name in SYMBOLS:
             if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
                             "femi_kernel_launches"):
@@ -295,6 +306,20 @@ def tonal_optimise(system, f, g, outer_rtol=1e-8, outer_max=1000, inner: CgOpts 
     rep = TonalReport()
     st = lib().femi_tonal_optimise(system._h, _dptr(f, torch.float64), _dptr(g, torch.float64), ctypes.byref(o),
                                    ctypes.byref(rep), _stream(stream))
+    if st not in (FEMI_OK, 4):
+        _check(st)
+    return st, rep.as_dict()
+
+
+def tonal_optimise_l1(system, f, g, irls=3, eps=1.0, outer_rtol=1e-8, outer_max=1000, inner: CgOpts | None = None,
+                      stream=None):
+    """NEXT-2: L1 tonal optimisation by IRLS (g device, in/out). Returns (status, report dict)."""
+    import torch
+    inner = inner or cg_opts(rtol=1e-12)
+    o = TonalOpts(outer_rtol, outer_max, inner, 0)
+    rep = TonalL1Report()
+    st = lib().femi_tonal_optimise_l1(system._h, _dptr(f, torch.float64), _dptr(g, torch.float64), ctypes.byref(o),
+                                      irls, eps, ctypes.byref(rep), _stream(stream))
     if st not in (FEMI_OK, 4):
         _check(st)
     return st, rep.as_dict()

@@ -327,3 +327,24 @@ def test_colour_shared_mesh(W):
     b = max(1, int(0.002 * N))
     new = femi.densify_step_channels(S, fd, us, b)
     np.testing.assert_array_equal(new, oracle.select(R["tri_err"], R["best"], R["e_px"], O.is_vertex(), b))
+
+
+def test_tonal_l1_irls_vs_oracle():
+    """NEXT-2: L1 tonal optimisation by IRLS (reading R3) against the oracle's IRLS, same
+    weights rule, same number of reweightings; the L1 error does not increase and ends no
+    higher than the L2 solution's."""
+    cfg = make_config(4, W=128, H=96, seed=8)
+    W, H = 128, 96
+    M = femi.Mesh(W, H, cfg["mask"], cfg["unknowns"])
+    S = femi.System(M)
+    fd = dev(cfg["f"]).reshape(-1)
+    g = pipeline.mask_values(fd, M.export()["vert_px"], S.n_u)
+    st, rep = femi.tonal_optimise_l1(S, fd, g, irls=3, eps=1.0, outer_rtol=1e-9)
+    assert st == 0 and rep["irls_steps"] == 3
+    O = oracle.System(W, H, cfg["mask"], cfg["unknowns"])
+    go, orep = oracle.tonal_l1(O, cfg["f"], irls=3, eps=1.0, outer_tol=1e-9)
+    assert np.abs(g.cpu().numpy() - go).max() <= 1e-3
+    assert abs(rep["l1_after"] - orep["l1_after"]) <= 1e-6 * orep["l1_after"]
+    assert rep["l1_after"] <= rep["l1_before"]
+    g2, _ = O.tonal(cfg["f"], outer_tol=1e-9)
+    assert rep["l1_after"] <= np.abs(cfg["f"].reshape(-1) - O.apply_B(g2)).mean() + 1e-9

@@ -32,7 +32,7 @@ def test_abi_exports_every_declared_symbol():
     L = femi.lib()
     import re
     hdr = open(__file__.replace("tests/test_mesh_host.py", "include/femi.h")).read()
-    declared = set(re.findall(r"\b(femi_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(femi_[a-z0-9_]+)\s*\(", hdr))
     assert declared == set(femi.SYMBOLS)
     for name in declared:
         assert hasattr(L, name)

@@ -482,6 +482,48 @@ def test_p11_mse_golden_and_sums():
             assert R["best"][t] == cand[np.argmax(e[cand])]
 
 
+# ---------------------------------------------------------------- L1 tonal via IRLS (NEXT-2)
+
+def test_weighted_tonal_unit_weights_is_tonal():
+    """W = I: the weighted CGLS is the plain one, bit for bit (x 1.0 is exact)."""
+    cfg = make_config(4, W=40, H=32, seed=12)
+    S = oracle.System(40, 32, cfg["mask"], cfg["unknowns"])
+    g0, r0 = S.tonal(cfg["f"], outer_tol=1e-8)
+    g1, r1 = oracle.tonal_weighted(S, cfg["f"], np.ones(40 * 32), outer_tol=1e-8)
+    np.testing.assert_array_equal(g0, g1)
+    assert r0["outer_iters"] == r1["outer_iters"]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_weighted_tonal_matches_weighted_dense_lstsq(seed):
+    """IRLS step = argmin ||W^1/2 (B g - f)|| by lstsq on the materialised dense B (<= 16x16)."""
+    cfg = make_config(4, W=16, H=16, seed=70 + seed)
+    S = oracle.System(16, 16, cfg["mask"], cfg["unknowns"])
+    B = oracle.materialise_B(S)
+    f = cfg["f"].reshape(-1)
+    sw = np.random.default_rng(seed).uniform(0.2, 3.0, f.size)
+    gstar = np.linalg.lstsq(sw[:, None] * B, sw * f, rcond=None)[0]
+    g, rep = oracle.tonal_weighted(S, f, sw, outer_tol=1e-11)
+    assert np.abs(g - gstar).max() <= 1e-4
+
+
+def test_irls_uniform_weights_is_l2_and_l1_improves():
+    """eps >= max |r| makes every IRLS weight 1/eps: the weighted minimiser is the L2 one
+    (SPEC.md:L374); with eps = 1 three IRLS steps end with an L1 error no larger than the L2
+    solution's (SPEC.md:L373)."""
+    cfg = make_config(4, W=48, H=40, seed=21)
+    S = oracle.System(48, 40, cfg["mask"], cfg["unknowns"])
+    f = cfg["f"].reshape(-1)
+    g2, _ = S.tonal(cfg["f"], outer_tol=1e-10)
+    gu, rep_u = oracle.tonal_l1(S, f, irls=1, eps=1e6, outer_tol=1e-10)
+    assert np.abs(gu - g2).max() <= 1e-6
+    g1, rep1 = oracle.tonal_l1(S, f, irls=3, eps=1.0, outer_tol=1e-10)
+    l1_of_l2 = np.abs(f - S.apply_B(g2)).mean()
+    assert rep1["l1_after"] <= l1_of_l2 + 1e-9
+    assert rep1["l1_after"] <= rep1["l1_before"]
+    assert abs(rep1["l1_after"] - np.abs(f - S.apply_B(g1)).mean()) <= 1e-9
+
+
 # ---------------------------------------------------------------- colour (NEXT-1)
 
 def test_colour_raster_pins():
