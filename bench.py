@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tonal", action="store_true", help="C5: skip the 20-iteration tonal tail")
+    ap.add_argument("--n", type=int, default=0, help="C3: densification iterations (default: the config's 10)")
+    ap.add_argument("--warm", action="store_true", help="C3: warm-start each solve from the previous solution")
     ap.add_argument("--shard", action="store_true",
                     help="C2 under torchrun: split the 32 masks across ranks (strong scaling) instead of replicas")
     return ap.parse_args()
@@ -501,18 +503,25 @@ def run_workload(args):
         work = "C2: 256x256 fp64 synthetic + noise, 32 independent 4% masks (32 meshes) solved as ONE batch " \
                "(block-diagonal), 32 rasters/error maps/MSEs; step = batched PCG (rtol 1e-10) + 32 rasters"
     elif args.config == 3:
+        if args.n:  # longer schedules: same final density, n iterations
+            c = make_config(3, W=args.size or None, H=args.size or None, n=args.n)
         sched = c["schedule"]
-        opts = femi.cg_opts(rtol=RTOL)
 
         def densify_timed():
             mask = np.sort(np.asarray(c["mask0"], dtype=np.int64))
             gpu_ms, host_s, its = 0.0, 0.0, []
+            x_prev = None
             for t in range(1, len(sched) + 1):
                 h0 = time.time()
                 M = femi.Mesh(W, H, mask, c["unknowns"])
                 S = femi.System(M)
                 g = pipeline.mask_values(f_dev, M.export()["vert_px"], S.n_u)
                 u = torch.empty(S.nv, dtype=torch.float64, device=dev)
+                x0 = 1
+                if args.warm and x_prev is not None and x_prev.numel() == S.n_u:
+                    u[: S.n_u] = x_prev  # NEXT-4 warm start: previous solution at the fixed unknowns
+                    x0 = 2
+                opts = femi.cg_opts(rtol=RTOL, x0=x0)
                 sse = torch.zeros(1, dtype=torch.float64, device=dev)
                 tri = torch.empty(max(S.T, 1), dtype=torch.float64, device=dev)
                 bst = torch.empty(max(S.T, 1), dtype=torch.int32, device=dev)
@@ -527,6 +536,7 @@ def run_workload(args):
                 torch.cuda.synchronize()
                 gpu_ms += a.elapsed_time(b)
                 its.append(int(it[0]))
+                x_prev = u[: S.n_u].clone()
                 if new is not None:
                     mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
             return gpu_ms, host_s, its, float(sse.item()) / Npx, S
@@ -542,7 +552,8 @@ def run_workload(args):
                 hs_.append(h_s)
         ms = float(np.mean(gms))
         units = 1
-        metric, unit, hib = "densification seconds (n=10, 0.5%->5%; GPU stages: solve+raster+select)", "s", False
+        metric, unit, hib = (f"densification seconds (n={len(sched)}, 0.5%->5%; GPU stages: solve+raster+select"
+                             f"{', warm starts' if args.warm else ''})"), "s", False
         value_one = ms * 1e-3
         detail.update(host_mesh_assemble_s=float(np.mean(hs_)), cg_iters=its, final_mse=mse,
                       mpx_iter_per_s=Npx * len(its) / (ms * 1e-3) / 1e6)

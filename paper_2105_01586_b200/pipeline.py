@@ -29,14 +29,20 @@ def mask_values(f_dev, mesh_or_sys_vert_px, n_u):
     return f_dev.reshape(-1).index_select(0, idx).contiguous()
 
 
-def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None):
+def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None, x0_unknown=None):
+    """x0_unknown: optional initial guess at the unknown vertices (canonical order, e.g. the
+    previous densification iteration's solution: the unknown set is fixed, reading A4)."""
     torch = _torch()
     mesh = femi.Mesh(W, H, mask_px, unknown_px)
     sysm = femi.System(mesh, stream)
     vert = mesh.export()["vert_px"]
     g = mask_values(f_dev, vert, sysm.n_u)
     u_vert = torch.empty(sysm.nv, dtype=torch.float64, device=f_dev.device)
-    st, iters, rel = femi.inpaint_solve_batched([sysm], [g], [u_vert], femi.cg_opts(rtol=rtol), stream)
+    x0 = 1
+    if x0_unknown is not None and x0_unknown.numel() == sysm.n_u:
+        u_vert[: sysm.n_u] = x0_unknown
+        x0 = 2
+    st, iters, rel = femi.inpaint_solve_batched([sysm], [g], [u_vert], femi.cg_opts(rtol=rtol, x0=x0), stream)
     sse = torch.zeros(1, dtype=torch.float64, device=f_dev.device)
     u_px = e_px = None
     if want_images:
@@ -49,21 +55,28 @@ def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stre
                 best=best[: sysm.T], sse=sse, status=st, iters=int(iters[0]), relres=float(rel[0]))
 
 
-def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks=None, stream=None):
-    """Returns (final mask, per-iteration records, final MSE)."""
-    torch = _torch()
+def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks=None, stream=None,
+            warm_start=False):
+    """Returns (final mask, per-iteration records, final MSE). warm_start: each solve starts
+    from the previous iteration's solution at the (fixed, reading A4) unknown vertices
+    (changes iterates, not the solution)."""
+    _torch()
     mask = np.sort(np.asarray(mask0, dtype=np.int64))
     recs = []
     f1 = f_dev.reshape(-1)
+    x_prev = None
     for t in range(1, len(schedule)):
         if lockstep_masks is not None:
             mask = np.sort(np.asarray(lockstep_masks[t - 1], dtype=np.int64))
-        R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream)
+        R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
+                    x0_unknown=x_prev if warm_start else None)
+        x_prev = R["u_vert"][: R["system"].n_u].clone()
         new = femi.densify_step(R["system"], f1, R["u_vert"], int(schedule[t]), stream)
         recs.append(dict(mask=mask.copy(), mse=float(R["sse"].item()) / (W * H), iters=R["iters"], new=new,
                          T=R["system"].T, mesh_seconds=R["mesh"].build_seconds))
         mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
-    R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream)
+    R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
+                x0_unknown=x_prev if warm_start else None)
     return mask, recs, float(R["sse"].item()) / (W * H)
 
 

@@ -110,10 +110,14 @@ CONFIGS = {
 }
 
 
-def make_config(k: int, *, W: int | None = None, H: int | None = None, seed: int | None = None) -> dict:
+def make_config(k: int, *, W: int | None = None, H: int | None = None, seed: int | None = None,
+                n: int | None = None) -> dict:
     """Inputs of BASELINE.json config k (1-based). W/H/seed overrides give scaled-down
-    variants of the same recipe for fast tests. Returns numpy arrays only."""
+    variants of the same recipe for fast tests; n overrides the number of densification
+    iterations (longer schedules). Returns numpy arrays only."""
     c = dict(CONFIGS[k])
+    if n is not None and c["kind"].startswith("densify"):
+        c["n"] = n
     W = W or c["W"]
     H = H or c["H"]
     seed = SEEDS[k] if seed is None else seed

@@ -348,3 +348,25 @@ def test_tonal_l1_irls_vs_oracle():
     assert rep["l1_after"] <= rep["l1_before"]
     g2, _ = O.tonal(cfg["f"], outer_tol=1e-9)
     assert rep["l1_after"] <= np.abs(cfg["f"].reshape(-1) - O.apply_B(g2)).mean() + 1e-9
+
+
+def test_densify_warm_start():
+    """NEXT-4 warm starts: each densification solve may start from the previous solution at
+    the fixed unknown vertices (reading A4). It changes iterates, not solutions: on the same
+    mask the warm and cold solves agree to the solver tolerance, and the warm run needs fewer
+    iterations over the schedule."""
+    c = make_config(3, W=256, H=256, seed=31)
+    fd = dev(c["f"])
+    mask_c, recs_c, mse_c = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"])
+    masks = [r["mask"] for r in recs_c]
+    mask_w, recs_w, mse_w = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"],
+                                             lockstep_masks=masks, warm_start=True)
+    assert sum(r["iters"] for r in recs_w[1:]) < sum(r["iters"] for r in recs_c[1:])
+    for rc, rw in zip(recs_c, recs_w):
+        assert abs(rc["mse"] - rw["mse"]) <= 1e-6 * rc["mse"]
+    # the same mask from a warm guess (the previous mask's solution) and from midrange
+    Rp = pipeline.inpaint(256, 256, fd, masks[-2], c["unknowns"])
+    R0 = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"])
+    Rw = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"], x0_unknown=Rp["u_vert"][: Rp["system"].n_u])
+    assert Rw["iters"] < R0["iters"]
+    assert torch.abs(R0["u_vert"] - Rw["u_vert"]).max().item() <= 1e-4
