@@ -31,6 +31,8 @@ struct Mesh {
     std::vector<int32_t> vt_idx;     // 3T entries: t*3+k, ascending t
     double build_seconds = 0.0;
     int32_t threads = 1;
+    int32_t strips = 1;         // horizontal strips triangulated in parallel
+    int32_t strip_retries = 0;  // strips re-run with a doubled margin
 };
 
 femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,

@@ -8,10 +8,15 @@
 // integer in-circle test with the smallest-pixel tie-break. Uniqueness means any correct
 // algorithm gives the same mesh; this one is Bowyer-Watson (cavity re-triangulation)
 // with biased randomised insertion order (BRIO rounds, Hilbert order within a round) and
-// a remembering visibility walk, followed by canonical numbering and the CSR/ownership
+// a remembering visibility walk, run on overlapping row strips in parallel with a
+// certification step (build_mesh), followed by canonical numbering and the CSR/ownership
 // tables the device kernels consume.
 #include <algorithm>
+#include <atomic>
+#include <cmath>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -44,6 +49,39 @@ inline bool incircle(const Pt& a, const Pt& b, const Pt& c, const Pt& d) {
     if (s == a.pix) return orient(b, c, d) < 0;
     if (s == b.pix) return orient(c, a, d) < 0;
     return orient(a, b, d) < 0;
+}
+
+// Rows of the closed circumdisk of CCW (a,b,c), widened by one pixel and clipped to the
+// columns [0, W): [*lo, *hi] (empty when *lo > *hi). Border triangles have huge circles
+// centred outside the image whose part inside it is a thin sliver; the column clip keeps
+// only that part. Returns false for a degenerate (non-CCW) triangle.
+struct Disk {
+    double ox, oy, r;
+};
+inline bool disk_of(const Pt& a, const Pt& b, const Pt& c, Disk& D) {
+    int64_t bx = b.x - a.x, by = b.y - a.y, cx = c.x - a.x, cy = c.y - a.y;
+    int64_t d = 2 * (bx * cy - by * cx);
+    if (d <= 0) return false;
+    int64_t b2 = bx * bx + by * by, c2 = cx * cx + cy * cy;
+    double ux = (double)(cy * b2 - by * c2) / (double)d, uy = (double)(bx * c2 - cx * b2) / (double)d;
+    D = {a.x + ux, a.y + uy, std::sqrt(ux * ux + uy * uy) + 1.0};
+    return true;
+}
+// x-interval of the (widened) disk on row y, clipped to [0, W); false when it misses the row
+inline bool disk_row(const Disk& D, double y, int32_t W, int32_t& x0, int32_t& x1) {
+    double dy = std::fabs(y - D.oy);
+    if (dy >= D.r) return false;
+    double w = std::sqrt(D.r * D.r - dy * dy);
+    x0 = (int32_t)std::max(0.0, std::floor(D.ox - w));
+    x1 = (int32_t)std::min((double)(W - 1), std::ceil(D.ox + w));
+    return x0 <= x1;
+}
+inline void disk_rows(const Disk& D, int32_t W, int32_t H, int32_t& lo, int32_t& hi) {
+    double dx = D.ox < 0.0 ? -D.ox : (D.ox > W - 1 ? D.ox - (W - 1) : 0.0);
+    dx = std::max(0.0, dx - 1.0);
+    double h = dx >= D.r ? -1.0 : std::sqrt(D.r * D.r - dx * dx);
+    lo = (int32_t)std::max(0.0, std::floor(D.oy - h));
+    hi = (int32_t)std::min((double)(H - 1), std::ceil(D.oy + h));
 }
 
 inline uint64_t hilbert_key(uint32_t x, uint32_t y) {
@@ -226,6 +264,12 @@ class BowyerWatson {
 femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,
                        int64_t p, Mesh& M) {
     auto t_start = std::chrono::steady_clock::now();
+    const bool prof = std::getenv("FEMI_MESH_PROF") != nullptr;
+    auto stamp = [&](const char* what) {
+        if (prof)
+            std::fprintf(stderr, "mesh_build %-12s %.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
+    };
     if ((m > 0 && !mask_px) || (p > 0 && !unknown_px) || m < 0 || p < 0) {
         set_error("mesh_build: NULL array or negative count");
         return FEMI_E_ARG;
@@ -263,96 +307,6 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     const int32_t corners[4] = {0, W - 1, (H - 1) * W + (W - 1), (H - 1) * W};
     for (int c = 0; c < 4; ++c)
         if (!role[corners[c]]) role[corners[c]] = 2;  // reading A2
-    // canonical vertex order: unknowns ascending, then masks ascending (role-map scan)
-    std::vector<int32_t> unk, msk;
-    unk.reserve(p + 4);
-    msk.reserve(m);
-    for (int64_t q = 0; q < N; ++q) {
-        if (role[q] == 2) unk.push_back((int32_t)q);
-        else if (role[q] == 1) msk.push_back((int32_t)q);
-    }
-    M.W = W;
-    M.H = H;
-    M.n_u = (int64_t)unk.size();
-    M.m = (int64_t)msk.size();
-    M.nv = M.n_u + M.m;
-    M.vpix.resize(M.nv);
-    std::copy(unk.begin(), unk.end(), M.vpix.begin());
-    std::copy(msk.begin(), msk.end(), M.vpix.begin() + M.n_u);
-    std::vector<int32_t>().swap(unk);
-    std::vector<int32_t>().swap(msk);
-
-    const int64_t nv = M.nv;
-    std::vector<Pt> P(nv);
-    for (int64_t v = 0; v < nv; ++v) P[v] = {M.vpix[v] % W, M.vpix[v] / W, M.vpix[v]};
-    int32_t cidx[4];
-    for (int c = 0; c < 4; ++c) {
-        cidx[c] = (int32_t)(std::lower_bound(M.vpix.begin(), M.vpix.begin() + M.n_u, corners[c]) - M.vpix.begin());
-        if (cidx[c] >= M.n_u || M.vpix[cidx[c]] != corners[c])
-            cidx[c] = (int32_t)(std::lower_bound(M.vpix.begin() + M.n_u, M.vpix.end(), corners[c]) - M.vpix.begin());
-    }
-
-    // ---- insertion order: BRIO rounds (geometric sizes), Hilbert order inside a round
-    std::vector<std::pair<uint64_t, int32_t>> order;
-    order.reserve(nv);
-    const int R = 24;
-    for (int64_t v = 0; v < nv; ++v) {
-        if (v == cidx[0] || v == cidx[1] || v == cidx[2] || v == cidx[3]) continue;
-        uint32_t h = mix32((uint32_t)M.vpix[v] * 2654435761u + 0x9e3779b9u);
-        int tz = h ? __builtin_ctz(h) : 31;
-        uint64_t round = (uint64_t)(R - std::min(tz, R));  // rare (many trailing zeros) first
-        order.push_back({(round << 40) | hilbert_key((uint32_t)P[v].x, (uint32_t)P[v].y), (int32_t)v});
-    }
-    std::sort(order.begin(), order.end());
-
-    BowyerWatson bw(P);
-    bw.init(cidx[0], cidx[1], cidx[2], cidx[3]);
-    for (auto& kv : order) bw.insert(kv.second);
-    std::vector<std::pair<uint64_t, int32_t>>().swap(order);
-
-    // ---- canonical triangles: CCW, smallest pix first, lexicographic by pix triple
-    const auto& TR = bw.tris();
-    const int64_t T = (int64_t)TR.size();
-    M.T = T;
-    struct Key {
-        int32_t a, b, c;
-        int32_t src;
-    };
-    std::vector<Key> keys(T);
-    for (int64_t t = 0; t < T; ++t) {
-        const int32_t* v = TR[t].v;
-        int k = 0;
-        if (M.vpix[v[1]] < M.vpix[v[k]]) k = 1;
-        if (M.vpix[v[2]] < M.vpix[v[k]]) k = 2;
-        keys[t] = {v[k], v[(k + 1) % 3], v[(k + 2) % 3], (int32_t)t};
-    }
-    const int32_t* vp = M.vpix.data();
-    std::sort(keys.begin(), keys.end(), [vp](const Key& x, const Key& y) {
-        if (vp[x.a] != vp[y.a]) return vp[x.a] < vp[y.a];
-        if (vp[x.b] != vp[y.b]) return vp[x.b] < vp[y.b];
-        return vp[x.c] < vp[y.c];
-    });
-    M.tri.resize(3 * T);
-    for (int64_t t = 0; t < T; ++t) {
-        M.tri[3 * t] = keys[t].a;
-        M.tri[3 * t + 1] = keys[t].b;
-        M.tri[3 * t + 2] = keys[t].c;
-    }
-    std::vector<Key>().swap(keys);
-
-    // ---- vertex -> incident corners (ascending triangle index)
-    M.vt_ptr.assign(nv + 1, 0);
-    for (int64_t q = 0; q < 3 * T; ++q) M.vt_ptr[M.tri[q] + 1]++;
-    for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
-    M.vt_idx.resize(3 * T);
-    {
-        std::vector<int32_t> fill(M.vt_ptr.begin(), M.vt_ptr.end() - 1);
-        for (int64_t q = 0; q < 3 * T; ++q) M.vt_idx[fill[M.tri[q]]++] = (int32_t)q;
-    }
-
-    // ---- neighbours across edges, ownership flags (reading A7)
-    M.nbr.assign(3 * T, -1);
-    M.flags.assign(T, 0);
     const int nthreads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     M.threads = nthreads;
     auto parallel = [nthreads](int64_t n, auto&& fn) {
@@ -364,6 +318,254 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
             });
         for (auto& x : th) x.join();
     };
+
+    // canonical vertex order: unknowns ascending, then masks ascending; plus the vertex ids
+    // in pixel (row-major) order and per-row pointers. Role-map scan in row chunks: count,
+    // prefix, fill.
+    std::vector<int64_t> cu(nthreads + 1, 0), cm(nthreads + 1, 0);
+    parallel(nthreads, [&](int64_t k) {
+        const uint8_t* r0 = role.data() + (int64_t)W * (H * k / nthreads);
+        const uint8_t* r1 = role.data() + (int64_t)W * (H * (k + 1) / nthreads);
+        int64_t u = 0, mm = 0;
+        for (const uint8_t* r = r0; r < r1; ++r) {
+            u += *r == 2;
+            mm += *r == 1;
+        }
+        cu[k + 1] = u;
+        cm[k + 1] = mm;
+    });
+    for (int k = 0; k < nthreads; ++k) {
+        cu[k + 1] += cu[k];
+        cm[k + 1] += cm[k];
+    }
+    M.W = W;
+    M.H = H;
+    M.n_u = cu[nthreads];
+    M.m = cm[nthreads];
+    M.nv = M.n_u + M.m;
+    const int64_t nv = M.nv;
+    M.vpix.resize(nv);
+    std::vector<int32_t> byrow(nv);
+    std::vector<int64_t> rowptr(H + 1, 0);
+    std::vector<Pt> P(nv);
+    parallel(nthreads, [&](int64_t k) {
+        int64_t iu = cu[k], im = cm[k];
+        for (int32_t y = (int32_t)(H * k / nthreads); y < (int32_t)(H * (k + 1) / nthreads); ++y) {
+            const uint8_t* r = role.data() + (int64_t)y * W;
+            for (int32_t x = 0; x < W; ++x) {
+                if (!r[x]) continue;
+                const int32_t q = y * W + x;
+                const int64_t v = r[x] == 2 ? iu++ : M.n_u + im++;
+                M.vpix[v] = q;
+                P[v] = {x, y, q};
+                byrow[iu + im - 1] = (int32_t)v;
+            }
+            rowptr[y + 1] = iu + im;
+        }
+    });
+    std::vector<uint8_t>().swap(role);
+    const int32_t cidx[4] = {byrow[0], byrow[rowptr[1] - 1], byrow[nv - 1], byrow[rowptr[H - 1]]};
+    stamp("order");
+
+    // ---- triangulation in horizontal strips, one Bowyer-Watson per strip, in parallel.
+    // A strip owns rows [y0, y1) and triangulates the points of rows [y0-g, y1+g) plus the
+    // points of the two border column bands (x < margin, x >= W - margin) within 8g rows of
+    // them and the four image corners, so its local hull is the image rectangle and no local
+    // triangle runs along a border past points the strip does not see. A local triangle is
+    // certified when no global point outside the strip's rows lies in its SoS circumcircle:
+    // trivially when its closed circumdisk (clipped to the image columns) stays inside those
+    // rows, else by testing the points of the few outside rows the disk reaches (border
+    // slivers). Certified local triangles are Delaunay for the global set, so they belong to
+    // the unique global mesh (reading A3). If every local triangle incident to a core vertex
+    // is certified, the local star of each core vertex is its global star, and the strip
+    // emits exactly the global triangles whose smallest-pixel vertex lies in its core;
+    // otherwise it retries with g doubled (once the rows cover the image every triangle is
+    // certified). Strips own ascending row ranges, so each strip's triangles sorted by
+    // (pix a, pix b, pix c) concatenate into the canonical order directly; the Euler count
+    // T = 2 nv - 2 - (border vertices) is checked at the end.
+    struct Key {
+        int32_t a, b, c;
+    };
+    const double spacing = std::sqrt((double)W * H / (double)nv);
+    int32_t margin = (int32_t)std::ceil(4.0 * spacing) + 4;
+    int32_t nstrips = 1;
+    if (nv >= 4000) nstrips = std::max(1, std::min((int32_t)(2 * nthreads), H / std::max(1, 4 * margin)));
+    if (const char* e = std::getenv("FEMI_MESH_STRIPS")) nstrips = std::max(1, std::min(H, std::atoi(e)));
+    if (const char* e = std::getenv("FEMI_MESH_MARGIN")) margin = std::max(1, std::atoi(e));
+    std::vector<std::vector<Key>> strip_keys(nstrips);
+    std::vector<int32_t> strip_retries(nstrips, 0);
+    const int32_t* vp = M.vpix.data();
+    // points of the two border column bands (x < margin or x >= W - margin), pixel order
+    std::vector<int32_t> border;
+    for (int32_t v : byrow)
+        if (P[v].x < margin || P[v].x >= W - margin) border.push_back(v);
+    // Is no point outside rows [ry0, ry1) inside the SoS circumcircle of (a,b,c)? The rows of
+    // the disk are scanned directly when they leave the region by at most a few margins
+    // (border slivers); a disk reaching further fails and the strip grows instead.
+    auto certified = [&](const Pt& a, const Pt& b, const Pt& c, int32_t ry0, int32_t ry1) {
+        Disk D;
+        if (!disk_of(a, b, c, D)) return false;
+        int32_t lo, hi;
+        disk_rows(D, W, H, lo, hi);
+        if (lo >= ry0 && hi <= ry1 - 1) return true;
+        if ((int64_t)std::max(0, ry0 - lo) + std::max(0, hi - (ry1 - 1)) > 8 * (int64_t)margin) return false;
+        for (int32_t y = lo; y <= hi; ++y) {
+            if (y >= ry0 && y < ry1) continue;
+            int32_t x0, x1;
+            if (!disk_row(D, (double)y, W, x0, x1)) continue;
+            const int32_t* rb = byrow.data() + rowptr[y];
+            const int32_t* re = byrow.data() + rowptr[y + 1];
+            const int32_t q0 = y * W + x0, q1 = y * W + x1;
+            const int32_t* it = std::lower_bound(rb, re, q0, [vp](int32_t v, int32_t q) { return vp[v] < q; });
+            for (; it != re && vp[*it] <= q1; ++it) {
+                const Pt& d = P[*it];
+                if (d.pix == a.pix || d.pix == b.pix || d.pix == c.pix) continue;
+                if (incircle(a, b, c, d)) return false;
+            }
+        }
+        return true;
+    };
+    auto run_strip = [&](int32_t s) {
+        const int32_t y0 = (int32_t)((int64_t)H * s / nstrips), y1 = (int32_t)((int64_t)H * (s + 1) / nstrips);
+        std::vector<Key>& out = strip_keys[s];
+        std::vector<int32_t> gid;
+        std::vector<Pt> LP;
+        std::vector<std::pair<uint64_t, int32_t>> order;
+        for (int32_t g = margin;; g *= 2) {
+            const int32_t ry0 = std::max(0, y0 - g), ry1 = (int32_t)std::min<int64_t>(H, (int64_t)y1 + g);
+            const bool whole = ry0 == 0 && ry1 == H;
+            // rows [ry0, ry1), plus every point of the two border columns outside them (the
+            // image corners among them): the local hull is then the global one, so no
+            // local triangle runs along a border past points the strip does not see
+            gid.clear();
+            const int64_t by0 = (int64_t)ry0 - 8 * (int64_t)g, by1 = (int64_t)ry1 + 8 * (int64_t)g;
+            auto keep = [&](int32_t v) {
+                return (P[v].y >= by0 && P[v].y < by1) || v == cidx[0] || v == cidx[1] || v == cidx[2] || v == cidx[3];
+            };
+            for (int32_t v : border)
+                if (P[v].y < ry0 && keep(v)) gid.push_back(v);
+            gid.insert(gid.end(), byrow.begin() + rowptr[ry0], byrow.begin() + rowptr[ry1]);
+            for (int32_t v : border)
+                if (P[v].y >= ry1 && keep(v)) gid.push_back(v);
+            int32_t lc[4] = {-1, -1, -1, -1};
+            for (int64_t k = 0; k < (int64_t)gid.size(); ++k)
+                for (int c = 0; c < 4; ++c)
+                    if (gid[k] == cidx[c]) lc[c] = (int32_t)k;
+            const int64_t nl = (int64_t)gid.size();
+            LP.resize(nl);
+            for (int64_t k = 0; k < nl; ++k) LP[k] = P[gid[k]];
+            // insertion order: BRIO rounds (geometric sizes), Hilbert order inside a round
+            order.clear();
+            const int R = 24;
+            for (int64_t k = 0; k < nl; ++k) {
+                if (k == lc[0] || k == lc[1] || k == lc[2] || k == lc[3]) continue;
+                uint32_t h = mix32((uint32_t)LP[k].pix * 2654435761u + 0x9e3779b9u);
+                int tz = h ? __builtin_ctz(h) : 31;
+                uint64_t round = (uint64_t)(R - std::min(tz, R));  // rare (many trailing zeros) first
+                order.push_back({(round << 40) | hilbert_key((uint32_t)LP[k].x, (uint32_t)LP[k].y), (int32_t)k});
+            }
+            std::sort(order.begin(), order.end());
+            BowyerWatson bw(LP);
+            bw.init(lc[0], lc[1], lc[2], lc[3]);
+            for (auto& kv : order) bw.insert(kv.second);
+            out.clear();
+            bool ok = true;
+            for (const Tri& T : bw.tris()) {
+                const Pt &A = LP[T.v[0]], &B = LP[T.v[1]], &C = LP[T.v[2]];
+                bool core = (A.y >= y0 && A.y < y1) || (B.y >= y0 && B.y < y1) || (C.y >= y0 && C.y < y1);
+                if (!core) continue;
+                if (!whole && !certified(A, B, C, ry0, ry1)) {
+                    ok = false;
+                    break;
+                }
+                int k = 0;
+                if (LP[T.v[1]].pix < LP[T.v[k]].pix) k = 1;
+                if (LP[T.v[2]].pix < LP[T.v[k]].pix) k = 2;
+                if (LP[T.v[k]].y < y0 || LP[T.v[k]].y >= y1) continue;  // owned by an earlier strip
+                out.push_back({gid[T.v[k]], gid[T.v[(k + 1) % 3]], gid[T.v[(k + 2) % 3]]});
+            }
+            if (ok) break;
+            ++strip_retries[s];
+        }
+        std::sort(out.begin(), out.end(), [vp](const Key& x, const Key& y) {
+            if (vp[x.a] != vp[y.a]) return vp[x.a] < vp[y.a];
+            if (vp[x.b] != vp[y.b]) return vp[x.b] < vp[y.b];
+            return vp[x.c] < vp[y.c];
+        });
+    };
+    {
+        std::atomic<int32_t> next{0};
+        std::vector<std::thread> th;
+        const int nt = std::min<int>(nthreads, nstrips);
+        for (int k = 0; k < nt; ++k)
+            th.emplace_back([&] {
+                for (int32_t s; (s = next.fetch_add(1)) < nstrips;) run_strip(s);
+            });
+        for (auto& x : th) x.join();
+    }
+    if (prof) {
+        int32_t tot = 0;
+        for (int32_t r : strip_retries) tot += r;
+        std::fprintf(stderr, "mesh_build strips %d margin %d retries %d\n", nstrips, margin, tot);
+    }
+    stamp("triangulate");
+    M.strips = nstrips;
+    M.strip_retries = 0;
+    for (int32_t r : strip_retries) M.strip_retries += r;
+
+    // ---- canonical triangles: CCW, smallest pix first, lexicographic by pix triple
+    std::vector<int64_t> toff(nstrips + 1, 0);
+    for (int32_t s = 0; s < nstrips; ++s) toff[s + 1] = toff[s] + (int64_t)strip_keys[s].size();
+    const int64_t T = toff[nstrips];
+    // Euler check on the rectangle hull: T = 2 nv - 2 - (vertices on the image border)
+    int64_t hull = 0;
+    for (int64_t v = 0; v < nv; ++v) {
+        int32_t x = P[v].x, y = P[v].y;
+        hull += (x == 0 || y == 0 || x == W - 1 || y == H - 1);
+    }
+    if (T != 2 * nv - 2 - hull) {
+        set_error("mesh_build: internal error, strip triangulation count mismatch");
+        return FEMI_E_ARG;
+    }
+    M.T = T;
+    M.tri.resize(3 * T);
+    {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthreads; ++k)
+            th.emplace_back([&, k] {
+                for (int32_t s = k; s < nstrips; s += nthreads) {
+                    int64_t o = toff[s];
+                    for (const Key& q : strip_keys[s]) {
+                        M.tri[3 * o] = q.a;
+                        M.tri[3 * o + 1] = q.b;
+                        M.tri[3 * o + 2] = q.c;
+                        ++o;
+                    }
+                    std::vector<Key>().swap(strip_keys[s]);
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    stamp("canonical");
+
+    // ---- vertex -> incident corners (ascending triangle index): atomic counting sort,
+    // then each vertex's short list sorted
+    M.vt_ptr.assign(nv + 1, 0);
+    M.vt_idx.resize(3 * T);
+    {
+        int32_t* cnt = M.vt_ptr.data() + 1;
+        parallel(3 * T, [&](int64_t q) { __atomic_fetch_add(&cnt[M.tri[q]], 1, __ATOMIC_RELAXED); });
+        for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
+        std::vector<int32_t> fill(M.vt_ptr.begin(), M.vt_ptr.end() - 1);
+        parallel(3 * T, [&](int64_t q) {
+            M.vt_idx[__atomic_fetch_add(&fill[M.tri[q]], 1, __ATOMIC_RELAXED)] = (int32_t)q;
+        });
+        parallel(nv, [&](int64_t v) { std::sort(M.vt_idx.begin() + M.vt_ptr[v], M.vt_idx.begin() + M.vt_ptr[v + 1]); });
+    }
+    stamp("vt");
+    // ---- neighbours across edges, ownership flags (reading A7)
+    M.nbr.assign(3 * T, -1);
+    M.flags.assign(T, 0);
     parallel(T, [&](int64_t t) {
         uint32_t fl = 0;
         for (int k = 0; k < 3; ++k) {
@@ -385,6 +587,7 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
         M.flags[t] = fl;
     });
 
+    stamp("nbr");
     // ---- CSR patterns of A_uu (with diagonal) and A_uk, with opposite-vertex tables
     const int64_t n_u = M.n_u;
     std::vector<int32_t> cnt_uu(n_u, 0), cnt_uk(n_u, 0);
@@ -466,6 +669,7 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
         }
     });
 
+    stamp("csr");
     // ---- transpose of A_uk (rows = masks), for B^T in tonal optimisation
     M.ku_rowptr.assign(M.m + 1, 0);
     for (int64_t q = 0; q < nuk; ++q) M.ku_rowptr[M.uk_col[q] + 1]++;
@@ -481,6 +685,7 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
                 M.ku_row[d] = (int32_t)i;
             }
     }
+    stamp("transpose");
     M.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     return FEMI_OK;
 }

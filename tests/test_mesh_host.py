@@ -96,3 +96,43 @@ def test_mesh_large_structure():
     M, E = product_mesh(W, H, mk, un)
     S_tri = oracle.delaunay(W, H, E["vert_px"])
     np.testing.assert_array_equal(E["tri"], S_tri)
+
+
+@pytest.mark.parametrize("strips,margin", [(2, None), (7, 1), (16, 2), (40, 3)])
+def test_mesh_strip_decomposition(monkeypatch, capfd, strips, margin):
+    """The parallel strip triangulation (mesh.cpp: local Bowyer-Watson per row strip,
+    circumdisk certification, retry with a doubled margin) gives the unique SoS mesh for any
+    strip count; tiny margins force the retry path."""
+    monkeypatch.setenv("FEMI_MESH_STRIPS", str(strips))
+    monkeypatch.setenv("FEMI_MESH_PROF", "1")
+    if margin is not None:
+        monkeypatch.setenv("FEMI_MESH_MARGIN", str(margin))
+    retries = 0
+    for seed in range(3):
+        rng = np.random.default_rng(100 + seed)
+        W, H = int(rng.integers(40, 160)), int(rng.integers(40, 160))
+        N = W * H
+        mk = draw_mask(rng, N, int(rng.integers(1, N // 8)))
+        un = draw_unknowns(rng, W, H, mk, int(rng.integers(4, N // 10)))
+        assert_same(W, H, mk, un)
+        err = capfd.readouterr().err
+        line = [x for x in err.splitlines() if x.startswith("mesh_build strips")]
+        assert line and int(line[-1].split()[2]) == min(strips, H)
+        retries += int(line[-1].split()[-1])
+    c = make_config(3)
+    assert_same(c["W"], c["H"], c["mask0"], c["unknowns"])
+    if margin is not None:
+        assert retries > 0
+
+
+def test_mesh_strips_sparse_and_clustered(monkeypatch):
+    """Strips on point sets far from uniform: a sparse mask with all vertices in one corner
+    region plus long empty bands (huge circumcircles cross many strips)."""
+    monkeypatch.setenv("FEMI_MESH_STRIPS", "12")
+    W, H = 300, 240
+    rng = np.random.default_rng(5)
+    xs, ys = rng.integers(0, 60, 400), rng.integers(0, 50, 400)
+    pts = np.unique(ys * W + xs)
+    mk = pts[: len(pts) // 2]
+    un = np.concatenate([pts[len(pts) // 2:], [120 * W + 150, 200 * W + 299, 239 * W + 10]])
+    assert_same(W, H, mk, un)
