@@ -198,6 +198,14 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
     if (s) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const Mesh& M = mesh->mesh;
+    const bool prof = std::getenv("FEMI_ASM_PROF") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto stamp = [&](const char* what) {
+        if (!prof) return;
+        cudaStreamSynchronize(st);
+        std::fprintf(stderr, "assemble %-10s %.3f ms\n", what,
+                     1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
+    };
     femi_system_s* S = new (std::nothrow) femi_system_s();
     if (!S) return FEMI_E_OOM;
     S->W = M.W;
@@ -236,6 +244,7 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
     U(alloc(S, &S->o_col, M.uu_col.size() - M.n_u));
     U(alloc(S, &S->o_val, M.uu_col.size() - M.n_u));
     U(alloc(S, &S->s, (size_t)M.n_u));
+    stamp("uploads");
     S->chunks_h = make_chunks(M.uu_rowptr, M.n_u);
     U(upload(S, &S->chunks_d, S->chunks_h, st));
     {
@@ -273,56 +282,91 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         const int64_t n = M.n_u;
         const int SIG = kSellSigma;
         S->nwin = (int32_t)((n + SIG - 1) / SIG);
-        auto rl = [&](int32_t i) { return M.uu_rowptr[i + 1] - M.uu_rowptr[i] - 1; };
+        const int32_t* rp = M.uu_rowptr.data();
+        const int32_t* uc = M.uu_col.data();
+        auto rl = [rp](int32_t i) { return rp[i + 1] - rp[i] - 1; };
+        // position of the diagonal inside each row: the k-th off-diagonal entry of a row is
+        // rp[row] + k + (k >= dpos[row])
+        std::vector<int32_t> dpos(n);
+        parallel_ranges(n, [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; ++i) {
+                int32_t e = rp[i];
+                while (uc[e] != (int32_t)i) ++e;
+                dpos[i] = e - rp[i];
+            }
+        });
+        auto kth = [&](int32_t row, int32_t k) { return rp[row] + k + (k >= dpos[row] ? 1 : 0); };
         std::vector<int32_t> pi(n), pos(n);
         {
-            std::vector<std::pair<uint64_t, int32_t>> key(n);
-            uint64_t band = kBand;
-            if (const char* e = std::getenv("FEMI_BAND")) band = (uint64_t)std::max(1, std::atoi(e));
-            for (int64_t i = 0; i < n; ++i) {
-                const uint64_t x = (uint64_t)(M.vpix[i] % M.W), y = (uint64_t)(M.vpix[i] / M.W);
-                key[i] = {((y / band) << 40) | (x << 20) | y, (int32_t)i};
-            }
-            std::sort(key.begin(), key.end());
-            for (int64_t i = 0; i < n; ++i) pi[i] = key[i].second;
+            // unknowns are numbered in ascending pix (row-major) order, so every band of
+            // image rows is a contiguous run of them; inside a band sort by (x, y)
+            int64_t band = kBand;
+            if (const char* e = std::getenv("FEMI_BAND")) band = std::max(1, std::atoi(e));
+            const int64_t nb = (M.H + band - 1) / band;
+            std::vector<int64_t> bs(nb + 1);
+            for (int64_t q = 0; q <= nb; ++q)
+                bs[q] = std::lower_bound(M.vpix.begin(), M.vpix.begin() + n, std::min<int64_t>(q * band, M.H) * M.W) -
+                        M.vpix.begin();
+            const int32_t* vp = M.vpix.data();
+            const int64_t W = M.W;
+            parallel_ranges(nb, [&](int64_t lo, int64_t hi) {
+                for (int64_t q = lo; q < hi; ++q) {
+                    for (int64_t i = bs[q]; i < bs[q + 1]; ++i) pi[i] = (int32_t)i;
+                    std::sort(pi.begin() + bs[q], pi.begin() + bs[q + 1], [vp, W](int32_t u, int32_t v) {
+                        const int64_t ux = vp[u] % W, vx = vp[v] % W;
+                        return ux != vx ? ux < vx : vp[u] < vp[v];
+                    });
+                }
+            }, 1);
         }
-        for (int64_t w0 = 0; w0 < n; w0 += SIG)
-            std::stable_sort(pi.begin() + w0, pi.begin() + std::min<int64_t>(n, w0 + SIG),
-                             [&](int32_t a, int32_t b) { return rl(a) > rl(b); });
-        for (int64_t i = 0; i < n; ++i) pos[pi[i]] = (int32_t)i;
+        stamp("order");
+        parallel_ranges(S->nwin, [&](int64_t lo, int64_t hi) {
+            for (int64_t w = lo; w < hi; ++w)
+                std::stable_sort(pi.begin() + w * SIG, pi.begin() + std::min<int64_t>(n, (w + 1) * SIG),
+                                 [&](int32_t u, int32_t v) { return rl(u) > rl(v); });
+        }, 256);
+        parallel_ranges(n, [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; ++i) pos[pi[i]] = (int32_t)i;
+        });
+        // SELL-32: slice lengths, offsets, then the entries slice by slice
         const int32_t nsl = (int32_t)((n + 31) / 32);
-        std::vector<int32_t> len(nsl), base(nsl), src, c32;
-        std::vector<int16_t> c16;
-        bool fits16 = true;
+        std::vector<int32_t> len(nsl), base(nsl);
+        parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
+            for (int64_t sl = lo; sl < hi; ++sl) {
+                int32_t L = 0;
+                for (int l = 0; l < 32 && 32 * sl + l < n; ++l) L = std::max(L, rl(pi[32 * sl + l]));
+                len[sl] = L;
+            }
+        }, 512);
         int64_t ent = 0;
         for (int32_t sl = 0; sl < nsl; ++sl) {
-            int32_t L = 0;
-            for (int l = 0; l < 32 && 32 * sl + l < n; ++l) L = std::max(L, rl(pi[32 * sl + l]));
-            len[sl] = L;
             base[sl] = (int32_t)ent;
-            const int32_t wbase = (32 * sl / SIG) * SIG;
-            for (int32_t k = 0; k < L; ++k)
-                for (int l = 0; l < 32; ++l) {
-                    const int64_t ri = 32 * (int64_t)sl + l;
-                    int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
-                    if (ri < n && k < rl(pi[ri])) {
-                        const int32_t row = pi[ri];
-                        int32_t e = M.uu_rowptr[row], q = 0;  // k-th off-diagonal entry of row
-                        for (; e < M.uu_rowptr[row + 1]; ++e) {
-                            if (M.uu_col[e] == row) continue;
-                            if (q == k) break;
-                            ++q;
-                        }
-                        col = pos[M.uu_col[e]];
-                        sidx = (M.uu_rowptr[row] - row) + k;  // index into o_val (natural CSR)
-                    }
-                    src.push_back(sidx);
-                    c32.push_back(col);
-                    const int32_t d = col - wbase;
-                    if (d < -32768 || d > 32767) fits16 = false;
-                    ++ent;
-                }
+            ent += 32 * (int64_t)len[sl];
         }
+        std::vector<int32_t> src(ent), c32(ent);
+        std::atomic<bool> fits16{true};
+        parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
+            bool f16 = true;
+            for (int64_t sl = lo; sl < hi; ++sl) {
+                const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
+                int64_t q = base[sl];
+                for (int32_t k = 0; k < len[sl]; ++k)
+                    for (int l = 0; l < 32; ++l, ++q) {
+                        const int64_t ri = 32 * sl + l;
+                        int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
+                        if (ri < n && k < rl(pi[ri])) {
+                            const int32_t row = pi[ri];
+                            col = pos[uc[kth(row, k)]];
+                            sidx = (rp[row] - row) + k;  // index into o_val (natural CSR)
+                        }
+                        src[q] = sidx;
+                        c32[q] = col;
+                        const int32_t d = col - wbase;
+                        if (d < -32768 || d > 32767) f16 = false;
+                    }
+            }
+            if (!f16) fits16 = false;
+        }, 512);
         S->nslices = nsl;
         S->sell_nnz = ent;
         U(upload(S, &S->sell_len, len, st));
@@ -331,26 +375,29 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         S->sell_base_h.push_back((int32_t)ent);  // [nslices] = total entries
         U(upload(S, &S->sell_inv, pi, st));
         {
-            std::vector<int32_t> ukr(n + 1), ukc, uks, uur(n + 1), uuc, uus;
-            ukc.reserve(M.uk_col.size());
-            uks.reserve(M.uk_col.size());
-            uuc.reserve(M.uu_col.size());
-            uus.reserve(M.uu_col.size());
+            // internal-order CSR copies of A_uk and A_uu (with their natural-CSR sources)
+            std::vector<int32_t> ukr(n + 1, 0), uur(n + 1, 0);
             for (int64_t i = 0; i < n; ++i) {
                 const int32_t nat = pi[i];
-                ukr[i] = (int32_t)ukc.size();
-                for (int32_t e = M.uk_rowptr[nat]; e < M.uk_rowptr[nat + 1]; ++e) {
-                    ukc.push_back(M.uk_col[e]);
-                    uks.push_back(e);
-                }
-                uur[i] = (int32_t)uuc.size();
-                for (int32_t e = M.uu_rowptr[nat]; e < M.uu_rowptr[nat + 1]; ++e) {
-                    uuc.push_back(M.uu_col[e]);
-                    uus.push_back(e);
-                }
+                ukr[i + 1] = ukr[i] + (M.uk_rowptr[nat + 1] - M.uk_rowptr[nat]);
+                uur[i + 1] = uur[i] + (rp[nat + 1] - rp[nat]);
             }
-            ukr[n] = (int32_t)ukc.size();
-            uur[n] = (int32_t)uuc.size();
+            std::vector<int32_t> ukc(ukr[n]), uks(ukr[n]), uuc(uur[n]), uus(uur[n]);
+            parallel_ranges(n, [&](int64_t lo, int64_t hi) {
+                for (int64_t i = lo; i < hi; ++i) {
+                    const int32_t nat = pi[i];
+                    int32_t o = ukr[i];
+                    for (int32_t e = M.uk_rowptr[nat]; e < M.uk_rowptr[nat + 1]; ++e, ++o) {
+                        ukc[o] = M.uk_col[e];
+                        uks[o] = e;
+                    }
+                    o = uur[i];
+                    for (int32_t e = rp[nat]; e < rp[nat + 1]; ++e, ++o) {
+                        uuc[o] = uc[e];
+                        uus[o] = e;
+                    }
+                }
+            });
             U(upload(S, &S->ukI_rowptr, ukr, st));
             U(upload(S, &S->uuI_rowptr, uur, st));
             if (!ukc.empty()) {
@@ -369,11 +416,14 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
         U(alloc(S, &S->q_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
         if (fits16) {
-            c16.resize(c32.size());
-            for (int32_t sl = 0, q = 0; sl < nsl; ++sl) {
-                const int32_t wbase = (32 * sl / SIG) * SIG;
-                for (int32_t k = 0; k < len[sl] * 32; ++k, ++q) c16[q] = (int16_t)(c32[q] - wbase);
-            }
+            std::vector<int16_t> c16(c32.size());
+            parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
+                for (int64_t sl = lo; sl < hi; ++sl) {
+                    const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
+                    for (int64_t q = base[sl]; q < base[sl] + 32 * (int64_t)len[sl]; ++q)
+                        c16[q] = (int16_t)(c32[q] - wbase);
+                }
+            }, 512);
             U(upload(S, &S->sell_c16, c16, st));
         } else {
             U(upload(S, &S->sell_c32, c32, st));
@@ -381,90 +431,104 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         int32_t* d_src = nullptr;
         U(upload(S, &d_src, src, st));
         S->sell_src_tmp = d_src;
+        stamp("sell");
         if (S->nnz_uu > kGraphNnz) {
-            // tiled jagged-diagonal layout (device.cuh) of the same internal order
+            // tiled jagged-diagonal layout (device.cuh) of the same internal order: per tile,
+            // a size pass (entries padded to 16 bytes, int16 or int32 columns, format checks),
+            // offsets, then a fill pass -- tiles in parallel
             const int32_t ntile = (int32_t)((n + kJdsRows - 1) / kJdsRows);
-            std::vector<int32_t> eb(ntile + 1), cbo(ntile + 1), jsrc;
-            std::vector<uint8_t> jcolb;  // per tile: int16 columns, or int32 when a column is out of range
-            // kmax = longest row; meta per tile: lengths + [slice][kmax] uint16 diagonal offsets
             int32_t kmax = 1;
             for (int64_t i = 0; i < n; ++i) kmax = std::max(kmax, rl((int32_t)i));
             const int32_t meta_bytes = (kJdsRows + 2 * (kJdsRows / 32) * kmax + 15) / 16 * 16;
-            std::vector<uint8_t> meta((size_t)ntile * meta_bytes, 0);
-            bool ok = kmax <= kJdsMaxK;
-            int32_t maxe = 0, nwide = 0;
-            auto kth = [&](int32_t row, int32_t k) {  // k-th off-diagonal of a row (natural CSR)
-                int32_t e = M.uu_rowptr[row], q = 0;
-                for (; e < M.uu_rowptr[row + 1]; ++e) {
-                    if (M.uu_col[e] == row) continue;
-                    if (q == k) break;
-                    ++q;
-                }
-                return e;
-            };
-            std::vector<int64_t> tcol;
-            for (int32_t t = 0; t < ntile && ok; ++t) {
-                eb[t] = (int32_t)jsrc.size();
-                cbo[t] = (int32_t)jcolb.size();
-                tcol.clear();
-                const int64_t r0 = (int64_t)t * kJdsRows;
-                uint8_t* mt = meta.data() + (size_t)t * meta_bytes;
-                uint16_t* doff = (uint16_t*)(mt + kJdsRows);
-                for (int w = 0; w < kJdsRows / 32; ++w) {
-                    int32_t L = 0;
-                    for (int l = 0; l < 32; ++l) {
-                        const int64_t ri = r0 + 32 * w + l;
-                        const int32_t len = ri < n ? rl(pi[ri]) : 0;
-                        if (len > 255) ok = false;
-                        if (l > 0 && len > mt[32 * w + l - 1]) ok = false;  // descending inside the slice
-                        mt[32 * w + l] = (uint8_t)len;
-                        L = std::max(L, len);
+            std::vector<int32_t> tent(ntile), eb(ntile + 1), cbo(ntile + 1);
+            std::vector<uint8_t> twide(ntile);
+            std::atomic<bool> okA{kmax <= kJdsMaxK};
+            auto row_len = [&](int64_t ri) { return ri < n ? rl(pi[ri]) : 0; };
+            if (okA) {
+                parallel_ranges(ntile, [&](int64_t lo, int64_t hi) {
+                    bool ok = true;
+                    for (int64_t t = lo; t < hi; ++t) {
+                        const int64_t r0 = t * kJdsRows;
+                        int64_t cnt = 0;
+                        bool wide = false;
+                        for (int w = 0; w < kJdsRows / 32; ++w) {
+                            int32_t L = 0;
+                            for (int l = 0; l < 32; ++l) {
+                                const int32_t rlen = row_len(r0 + 32 * w + l);
+                                if (rlen > 255 || (l > 0 && rlen > row_len(r0 + 32 * w + l - 1))) ok = false;
+                                L = std::max(L, rlen);
+                            }
+                            for (int32_t k = 0; k < L; ++k) {
+                                if (cnt > 65535) ok = false;
+                                for (int l = 0; l < 32; ++l) {
+                                    const int64_t ri = r0 + 32 * w + l;
+                                    if (row_len(ri) <= k) continue;
+                                    const int64_t d = (int64_t)pos[uc[kth(pi[ri], k)]] - r0;
+                                    wide |= d < -32768 || d > 32767;
+                                    ++cnt;
+                                }
+                            }
+                        }
+                        tent[t] = (int32_t)((cnt + 7) / 8 * 8);  // 16-byte aligned tile blocks
+                        twide[t] = wide;
                     }
-                    for (int32_t k = 0; k < L; ++k) {
-                        const int64_t off = (int64_t)jsrc.size() - eb[t];
-                        if (off > 65535) ok = false;
-                        doff[w * kmax + k] = (uint16_t)off;
-                        for (int l = 0; l < 32; ++l) {
-                            const int64_t ri = r0 + 32 * w + l;
-                            if (ri >= n || rl(pi[ri]) <= k) continue;
-                            const int32_t row = pi[ri];
-                            const int32_t e = kth(row, k);
-                            tcol.push_back((int64_t)pos[M.uu_col[e]] - r0);
-                            jsrc.push_back((M.uu_rowptr[row] - row) + k);
+                    if (!ok) okA = false;
+                }, 16);
+            }
+            bool ok = okA;
+            int32_t maxe = 0, nwide = 0;
+            for (int32_t t = 0; t < ntile && ok; ++t) {
+                eb[t + 1] = eb[t] + tent[t];
+                cbo[t + 1] = cbo[t] + tent[t] * (twide[t] ? 4 : 2);
+                maxe = std::max(maxe, tent[t]);
+                nwide += twide[t];
+            }
+            if (std::getenv("FEMI_DEBUG"))
+                std::fprintf(stderr, "[femi] jds layout: ok %d tiles %d (int32 columns: %d) entries %d maxe %d kmax %d\n",
+                             (int)ok, ntile, nwide, ok ? eb[ntile] : -1, maxe, kmax);
+            if (ok) {
+                std::vector<uint8_t> meta((size_t)ntile * meta_bytes, 0), jcolb(cbo[ntile]);
+                std::vector<int32_t> jsrc(eb[ntile], -1);
+                parallel_ranges(ntile, [&](int64_t lo, int64_t hi) {
+                    for (int64_t t = lo; t < hi; ++t) {
+                        const int64_t r0 = t * kJdsRows;
+                        uint8_t* mt = meta.data() + (size_t)t * meta_bytes;
+                        uint16_t* doff = (uint16_t*)(mt + kJdsRows);
+                        int16_t* c16 = (int16_t*)(jcolb.data() + cbo[t]);
+                        int32_t* c32w = (int32_t*)(jcolb.data() + cbo[t]);
+                        int64_t q = 0;
+                        for (int w = 0; w < kJdsRows / 32; ++w) {
+                            int32_t L = 0;
+                            for (int l = 0; l < 32; ++l) {
+                                const int32_t rlen = row_len(r0 + 32 * w + l);
+                                mt[32 * w + l] = (uint8_t)rlen;
+                                L = std::max(L, rlen);
+                            }
+                            for (int32_t k = 0; k < L; ++k) {
+                                doff[w * kmax + k] = (uint16_t)q;
+                                for (int l = 0; l < 32; ++l) {
+                                    const int64_t ri = r0 + 32 * w + l;
+                                    if (row_len(ri) <= k) continue;
+                                    const int32_t row = pi[ri];
+                                    const int64_t d = (int64_t)pos[uc[kth(row, k)]] - r0;
+                                    if (twide[t]) c32w[q] = (int32_t)d;
+                                    else c16[q] = (int16_t)d;
+                                    jsrc[eb[t] + q] = (rp[row] - row) + k;
+                                    ++q;
+                                }
+                            }
+                        }
+                        for (; q < tent[t]; ++q) {  // padding entries: column 0, no source
+                            if (twide[t]) c32w[q] = 0;
+                            else c16[q] = 0;
                         }
                     }
-                }
-                while (jsrc.size() % 8) {  // 16-byte aligned tile blocks for the bulk copies
-                    tcol.push_back(0);
-                    jsrc.push_back(-1);
-                }
-                bool wide = false;
-                for (int64_t d : tcol) wide |= d < -32768 || d > 32767;
-                nwide += wide;
-                for (int64_t d : tcol) {
-                    if (wide) {
-                        const int32_t v = (int32_t)d;
-                        const uint8_t* b = (const uint8_t*)&v;
-                        jcolb.insert(jcolb.end(), b, b + 4);
-                    } else {
-                        const int16_t v = (int16_t)d;
-                        const uint8_t* b = (const uint8_t*)&v;
-                        jcolb.insert(jcolb.end(), b, b + 2);
-                    }
-                }
-                maxe = std::max(maxe, (int32_t)jsrc.size() - eb[t]);
-            }
-            eb[ntile] = (int32_t)jsrc.size();
-            cbo[ntile] = (int32_t)jcolb.size();
-            if (std::getenv("FEMI_DEBUG"))
-                std::fprintf(stderr, "[femi] jds layout: ok %d tiles %d (int32 columns: %d) entries %zu maxe %d kmax %d\n",
-                             (int)ok, ntile, nwide, jsrc.size(), maxe, kmax);
-            if (ok) {
+                }, 16);
                 S->jds_ntile = ntile;
                 S->jds_maxe = maxe;
                 S->jds_kmax = kmax;
                 S->jds_meta_bytes = meta_bytes;
-                S->jds_nnz = (int64_t)jsrc.size();
+                S->jds_nnz = (int64_t)eb[ntile];
                 U(upload(S, &S->jds_eb, eb, st));
                 U(upload(S, &S->jds_cb, cbo, st));
                 U(upload(S, &S->jds_meta, meta, st));
@@ -476,11 +540,15 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
             }
         }
     }
+    stamp("jds");
     U(launch_tri_records(S, d_tri, d_flags, st));
+    stamp("trirec");
     U(alloc(S, &S->tp_ptr, (size_t)M.T + 1));
     U(alloc(S, &S->tp_pix, (size_t)M.W * M.H));
     U(build_owner_tables(S, st));
+    stamp("owner");
     U(launch_assemble_values(S, st));
+    stamp("values");
     U(launch_sell_values(S, S->sell_src_tmp, st));
     // the int32 triangle table and flags are folded into TriRec; drop them once done
     if (cudaStreamSynchronize(st) != cudaSuccess) {
@@ -497,6 +565,7 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
             ++it;
         }
     }
+    stamp("done");
 #undef U
     *out = S;
     return FEMI_OK;

@@ -1,7 +1,9 @@
 // femi_internal.h -- internal types of libfemi (product path). Not part of the ABI.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/femi.h"
@@ -9,6 +11,21 @@
 namespace femi {
 
 void set_error(const std::string& msg);
+
+// fn(lo, hi) over contiguous chunks of [0, n) on up to 16 host threads (one chunk when n is
+// below two grains)
+template <class F>
+void parallel_ranges(int64_t n, F&& fn, int64_t grain = 1 << 14) {
+    const int64_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, n / std::max<int64_t>(1, grain)));
+    if (nt <= 1) {
+        if (n > 0) fn((int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int k = 0; k < nt; ++k) th.emplace_back([&, k] { fn(n * k / nt, n * (k + 1) / nt); });
+    for (auto& x : th) x.join();
+}
 
 // Host mesh (S0). Canonical numbering: unknowns (ascending pix) then masks (ascending pix).
 struct Mesh {

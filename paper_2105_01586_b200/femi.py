@@ -166,7 +166,8 @@ class Mesh:
         mk = np.ascontiguousarray(np.asarray(mask_px).reshape(-1), dtype=np.int32)
         un = np.ascontiguousarray(np.asarray(unknown_px).reshape(-1), dtype=np.int32)
         h = ctypes.c_void_p()
-        _check(lib().femi_mesh_build(W, H, _hptr(mk), mk.size, _hptr(un), un.size, ctypes.byref(h)))
+        self._lib = lib()  # kept: close() may run at interpreter shutdown
+        _check(self._lib.femi_mesh_build(W, H, _hptr(mk), mk.size, _hptr(un), un.size, ctypes.byref(h)))
         self._h = h
         info = MeshInfo()
         _check(lib().femi_mesh_info_get(h, ctypes.byref(info)))
@@ -187,7 +188,7 @@ class Mesh:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().femi_mesh_free(self._h)
+            self._lib.femi_mesh_free(self._h)
             self._h = None
 
     def __del__(self):
@@ -199,7 +200,8 @@ class System:
 
     def __init__(self, mesh: Mesh, stream=None):
         h = ctypes.c_void_p()
-        _check(lib().femi_assemble(mesh._h, _stream(stream), ctypes.byref(h)))
+        self._lib = lib()
+        _check(self._lib.femi_assemble(mesh._h, _stream(stream), ctypes.byref(h)))
         self._h = h
         info = MeshInfo()
         _check(lib().femi_system_info_get(h, ctypes.byref(info)))
@@ -215,7 +217,7 @@ class System:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().femi_system_free(self._h)
+            self._lib.femi_system_free(self._h)
             self._h = None
 
     def __del__(self):
