@@ -38,7 +38,8 @@ struct CgState {
     int32_t iters, active, status, max_iter;
     uint32_t cnt[4];  // last-block counters (one per reduction site)
     int32_t need_rho;  // graph mode: the next SpMV computes the unscaled residual norm (else it is skipped)
-    int32_t pad;
+    int32_t x_pend;    // graph mode: the last k_gu deferred its x += alpha_pend p (k_finalize applies it)
+    double alpha_pend; // graph mode: alpha of the previous k_gu
 };
 
 // One batch item as the PCG kernels see it.

@@ -283,9 +283,18 @@ __global__ void k_finalize(const RItem* __restrict__ items) {
         const int nat = it.inv[i];
         if (S->iters == 0 && it.x0mode == 2 && S->bn2 != 0.0) continue;  // caller's guess stays
         double xi;
-        if (S->bn2 == 0.0) xi = 0.0;
-        else if (S->iters == 0) xi = x0v;
-        else xi = it.s[i] * it.x[i];
+        if (S->bn2 == 0.0) {
+            xi = 0.0;
+        } else if (S->iters == 0) {
+            xi = x0v;
+        } else {
+            double xh = it.x[i];
+            if (S->x_pend) {  // the deferred half of k_gu's paired x update (graph mode)
+                xh = fma(S->alpha_pend, it.p[i], xh);
+                it.x[i] = xh;
+            }
+            xi = it.s[i] * xh;
+        }
         it.u_vert[nat] = xi;
     }
 }
@@ -302,7 +311,10 @@ __global__ void __launch_bounds__(KNT) k_true_res(const RItem* __restrict__ item
         it.r[i] = it.s[i] * ri;
         v[0] += ri * ri;
     }
-    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) it.st->res2 = v[0];
+    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) {
+        it.st->res2 = v[0];
+        it.st->x_pend = 0;  // k_finalize has applied it
+    }
 }
 
 __global__ void k_copy_g(const RItem* __restrict__ items) {
@@ -901,12 +913,51 @@ __global__ void k_zero_ps(const RItem* __restrict__ items) {
 }
 
 // U: p = r + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+// x is only needed at exit, so it moves every other iteration: an even iteration defers its
+// alpha_i p_i, the odd one after it applies x += alpha_{i-1} p_{i-1} + alpha_i p_i (both p's are
+// in registers there), k_finalize applies a deferred term left at exit. Saves the x read and
+// write of every other iteration (2 of the 9 vector streams).
 __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
     const CgState* S = it.st;
     if (!S->active) return;
     const unsigned long long tprof = g_loop_prof ? gtime() : 0ull;
     const double alpha = S->alpha, beta = S->beta;
+    if ((S->iters & 1) == 0) {
+        double* __restrict__ r = it.r;
+        const double* __restrict__ w = it.w;
+        double* __restrict__ p = it.p;
+        double* __restrict__ sv = it.sv;
+        const int n = it.n, stride = gridDim.x * blockDim.x;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+            const int j = i + stride;
+            const bool hj = j < n;
+            const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i];
+            double rj = 0.0, wj = 0.0, pj0 = 0.0, sj0 = 0.0;
+            if (hj) {
+                rj = r[j];
+                wj = w[j];
+                pj0 = p[j];
+                sj0 = sv[j];
+            }
+            const double si = fma(beta, si0, wi);
+            p[i] = fma(beta, pi0, ri);
+            sv[i] = si;
+            r[i] = fma(-alpha, si, ri);
+            if (hj) {
+                const double sj = fma(beta, sj0, wj);
+                p[j] = fma(beta, pj0, rj);
+                sv[j] = sj;
+                r[j] = fma(-alpha, sj, rj);
+            }
+        }
+        if (g_loop_prof) {
+            __syncthreads();
+            if (threadIdx.x == 0) loop_stamp(0, S->iters, tprof);
+        }
+        return;
+    }
+    const double ap = S->alpha_pend;
     double* __restrict__ r = it.r;
     const double* __restrict__ w = it.w;
     double* __restrict__ p = it.p;
@@ -928,13 +979,13 @@ __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
         const double pi = fma(beta, pi0, ri), si = fma(beta, si0, wi);
         p[i] = pi;
         sv[i] = si;
-        x[i] = fma(alpha, pi, xi);
+        x[i] = fma(alpha, pi, fma(ap, pi0, xi));
         r[i] = fma(-alpha, si, ri);
         if (hj) {
             const double pj = fma(beta, pj0, rj), sj = fma(beta, sj0, wj);
             p[j] = pj;
             sv[j] = sj;
-            x[j] = fma(alpha, pj, xj);
+            x[j] = fma(alpha, pj, fma(ap, pj0, xj));
             r[j] = fma(-alpha, sj, rj);
         }
     }
@@ -1063,6 +1114,10 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
         rho2 += shm[4 * w + 2];
     }
     S->cnt[0] = 0;
+    if (!FIRST && act) {  // the k_gu before this SpMV: deferred its x term (even) or not
+        S->x_pend = (s_iters & 1) == 0 ? 1 : 0;
+        S->alpha_pend = s_alpha;
+    }
     const int active = cg_advance<FIRST>(S, act, gam2, del2, rho2, dmin, s_bn2, s_tol2, s_rr, s_alpha, s_iters, s_max,
                                          s_need);
     if (tp) g_tail_ts[4 * prof_it + 2] = gtime();  // C: scalars done
