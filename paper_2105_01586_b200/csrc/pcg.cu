@@ -102,8 +102,11 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
 constexpr int kLoopProfMax = 4096;
 __device__ int g_loop_prof;
+__device__ int g_pdl_pre = 6;  // k_gt: stages streamed before grid_dep_wait (FEMI_PDL_PRE, <= JNS)
 __device__ unsigned long long g_loop_ts[4 * kLoopProfMax];
-__device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];  // k_gt: max start, min/max consumer end
+__device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];
+constexpr int kCtaProfIt = 60;  // FEMI_LOOP_PROF: per-CTA start / consumer end of this iteration's k_gt
+__device__ unsigned long long g_cta_prof[2 * 1024];  // k_gt: max start, min/max consumer end
 __device__ unsigned long long g_tail_ts[4 * kLoopProfMax];   // cg_tail stamps (see cg_tail)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -918,6 +921,7 @@ __global__ void k_zero_ps(const RItem* __restrict__ items) {
 // in registers there), k_finalize applies a deferred term left at exit. Saves the x read and
 // write of every other iteration (2 of the 9 vector streams).
 __global__ void __launch_bounds__(GNT) k_gu(const RItem* __restrict__ items) {
+    grid_dep_wait();  // behind the previous SpMV through a programmatic edge (graph body)
     const RItem& it = items[blockIdx.y];
     const CgState* S = it.st;
     if (!S->active) return;
@@ -1240,8 +1244,6 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
     const RItem& it = items[0];
     CgState* S = it.st;
-    const bool act = FIRST || S->active;
-    const bool nrho = FIRST || S->need_rho;  // else the q stream and the residual monitor are skipped
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];  // this CTA's tiles
     const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
@@ -1264,14 +1266,51 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         mbar_fence_init();
     }
     __syncthreads();
+    // The matrix does not depend on the previous kernel: behind a programmatic edge (graph
+    // body) this CTA is resident while k_gu still runs, and the producer already streams the
+    // values, columns and metadata of its first JNS tiles (expect_tx without an arrival keeps
+    // each stage's phase open); r and q follow once the update kernel has completed.
+    const int npre = min(g_pdl_pre, te - tb);
+    const uint64_t pol = policy_evict_first();  // keep the CG vectors L2-resident
+    if (warp == JCW && lane == 0) {
+        for (int i = 0; i < npre; ++i) {
+            const int t = tb + i;
+            const int e0 = it.jeb[t], e1 = it.jeb[t + 1], c0 = it.jcb[t], c1 = it.jcb[t + 1];
+            const JStage q = stage(i);
+            tile_e[i] = make_int2(e0, e1 - e0);
+            tile_c[i] = make_int2(c0, c1 - c0);
+            mbar_expect_tx(&full[i], (uint32_t)(e1 - e0) * 8u + (uint32_t)(c1 - c0) + (uint32_t)mb);
+            bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[i]);
+            if (e1 > e0) {
+                bulk_g2s_hint(q.val, it.jval + e0, 8u * (e1 - e0), &full[i], pol);
+                bulk_g2s_hint(q.col, it.jcol + c0, (uint32_t)(c1 - c0), &full[i], pol);
+            }
+        }
+    }
+    grid_dep_wait();
+    const bool act = FIRST || S->active;
+    const bool nrho = FIRST || S->need_rho;  // else the q stream and the residual monitor are skipped
     double v[3] = {0.0, 0.0, 0.0};
+    if (!act && warp == JCW && lane == 0) {
+        // nothing to compute: close the prefetched stages and let their copies land before exit
+        for (int i = 0; i < npre; ++i) {
+            mbar_arrive(&full[i]);
+            mbar_wait(&full[i], 0);
+        }
+    }
     if (act) {
         if (warp == JCW) {
             // ---- producer: one elected lane streams the CTA's tiles into the ring
             if (lane == 0) {
-                int e0 = tb < te ? it.jeb[tb] : 0, c0 = tb < te ? it.jcb[tb] : 0;
-                const uint64_t pol = policy_evict_first();  // keep the CG vectors L2-resident
-                for (int t = tb, i = 0; t < te; ++t, ++i) {
+                for (int i = 0; i < npre; ++i) {  // the prefetched stages: r (and q) only
+                    const JStage q = stage(i);
+                    const int t = tb + i;
+                    mbar_arrive_expect_tx(&full[i], (nrho ? 16u : 8u) * kJdsRows);
+                    bulk_g2s(q.r, it.r + (size_t)t * kJdsRows, 8 * kJdsRows, &full[i]);
+                    if (nrho) bulk_g2s(q.s, it.q + (size_t)t * kJdsRows, 8 * kJdsRows, &full[i]);
+                }
+                int e0 = tb + npre < te ? it.jeb[tb + npre] : 0, c0 = tb + npre < te ? it.jcb[tb + npre] : 0;
+                for (int t = tb + npre, i = npre; t < te; ++t, ++i) {
                     const int k = i % JNS;
                     const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];  // loaded before the wait
                     if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);
@@ -1344,6 +1383,10 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         __syncthreads();  // profiling only: every warp of the CTA is done
         if (threadIdx.x == 0) {
             const unsigned long long t = gtime();
+            if (it_prof == kCtaProfIt && blockIdx.x < 1024) {
+                g_cta_prof[2 * blockIdx.x] = t_start;
+                g_cta_prof[2 * blockIdx.x + 1] = t;
+            }
             atomicMax(&g_loop_ts2[4 * it_prof], t_start);
             atomicMin(&g_loop_ts2[4 * it_prof + 1], t);
             atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
@@ -1648,6 +1691,27 @@ femi_status add_kernel(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid
     return FEMI_OK;
 }
 
+// the same behind a programmatic edge: the node may launch once every block of `dep` has
+// started (it must grid_dep_wait() before touching dep's results). FEMI_NO_PDL=1 turns the
+// edges into ordinary ones.
+femi_status add_kernel_pdl(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 grid, dim3 block, void** args,
+                           cudaGraphNode_t* out, unsigned smem = 0) {
+    static const bool off = std::getenv("FEMI_NO_PDL") != nullptr;
+    if (!dep || off) return add_kernel(gr, dep, fn, grid, block, args, out, smem);
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeKernel;
+    p.kernel.func = fn;
+    p.kernel.gridDim = grid;
+    p.kernel.blockDim = block;
+    p.kernel.sharedMemBytes = smem;
+    p.kernel.kernelParams = args;
+    cudaGraphEdgeData e = {};
+    e.from_port = cudaGraphKernelNodePortLaunchCompletion;
+    e.type = cudaGraphDependencyTypeProgrammatic;
+    FEMI_CUDA(cudaGraphAddNode_v2(out, gr, dep, &e, 1, &p));
+    return FEMI_OK;
+}
+
 // main:    reset -> minmax -> rhs -> init_x -> zero_ps -> init_r -> SpMV<FIRST> ->
 //          WHILE{ kUnroll x (k_gu -> SpMV) } -> finalize -> true_res -> copy_g
 // restart: zero_ps -> SpMV<FIRST> -> WHILE{...} -> finalize -> true_res -> copy_g
@@ -1707,9 +1771,18 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         // convergence return at once (S->active == 0)
         cudaGraphNode_t bprev = nullptr, u, sn;
         const dim3 gu(std::min(C.gx * 2, 1184));
+        // inside the body, k_gu -> k_gt -> k_gu ... are programmatic edges (k_gt streams its
+        // first matrix tiles while k_gu runs; each waits in grid_dep_wait for its inputs)
         for (int k = 0; k < kUnroll; ++k) {
-            if ((s = add_kernel(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u))) return s;
-            if ((s = add_kernel(body, &u, spmv, gsp, bsp, a_gs, &sn, ssp))) return s;
+            if (tma) {
+                if ((s = add_kernel_pdl(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u)))
+                    return s;
+                if ((s = add_kernel_pdl(body, &u, spmv, gsp, bsp, a_gs, &sn, ssp))) return s;
+            } else {
+                if ((s = add_kernel(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u)))
+                    return s;
+                if ((s = add_kernel(body, &u, spmv, gsp, bsp, a_gs, &sn, ssp))) return s;
+            }
             bprev = sn;
         }
     }
@@ -1752,7 +1825,19 @@ femi_status loop_prof_end(cudaStream_t st) {
                                         cudaMemcpyDeviceToHost, st));
     FEMI_CUDA(cudaMemcpyFromSymbolAsync(t3.data(), g_tail_ts, sizeof(unsigned long long) * t3.size(), 0,
                                         cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned long long> cp(2 * 1024);
+    FEMI_CUDA(cudaMemcpyFromSymbolAsync(cp.data(), g_cta_prof, sizeof(unsigned long long) * cp.size(), 0,
+                                        cudaMemcpyDeviceToHost, st));
     FEMI_CUDA(cudaStreamSynchronize(st));
+    if (std::getenv("FEMI_CTA_PROF")) {
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < 1024; ++b)
+            if (cp[2 * b]) t0 = std::min(t0, cp[2 * b]);
+        std::fprintf(stderr, "[femi cta] iteration %d: cta start_us end_us\n", kCtaProfIt);
+        for (int b = 0; b < 1024; ++b)
+            if (cp[2 * b])
+                std::fprintf(stderr, "[femi cta] %d %.3f %.3f\n", b, (cp[2 * b] - t0) / 1e3, (cp[2 * b + 1] - t0) / 1e3);
+    }
     double su = 0, sg = 0, g1 = 0, g2 = 0, c0 = 0, c1 = 0, c2 = 0, tA = 0, tB = 0;
     int cnt = 0;
     for (int k = 1; k + 1 < kLoopProfMax; ++k) {
@@ -1781,9 +1866,47 @@ femi_status loop_prof_end(cudaStream_t st) {
     return FEMI_OK;
 }
 
+// Tiles -> k_gt CTAs: contiguous ranges, equal tile counts by default. FEMI_JPART_A=a weights
+// them by cost(tile) = a + stored entries instead. Measured at C5 (FEMI_CTA_PROF): under the
+// equal split the CTA times (14.7 .. 18.4 us) correlate 0.8 with the entry counts, yet the
+// cost-weighted split is slower (a = 5000: +0.02 ms per solve, 3700: +0.1, 2500: +0.19) --
+// the spread follows the image region, not the entry count -- so equal ranges stay.
+femi_status tile_split(const femi_system_s* S, int nblocks, std::vector<int32_t>& jpart) {
+    const int nt = S->jds_ntile;
+    jpart.assign(nblocks + 1, 0);
+    const char* env = std::getenv("FEMI_JPART_A");
+    if (!env) {
+        for (int b = 0; b <= nblocks; ++b) jpart[b] = (int)((int64_t)nt * b / nblocks);
+        return FEMI_OK;
+    }
+    std::vector<int32_t> eb(nt + 1);
+    FEMI_CUDA(cudaMemcpy(eb.data(), S->jds_eb, sizeof(int32_t) * eb.size(), cudaMemcpyDeviceToHost));
+    const double A = std::atof(env);
+    jpart[nblocks] = nt;
+    const double total = A * nt + (double)eb[nt];
+    int t = 0;
+    for (int b = 1; b < nblocks; ++b) {
+        const double target = total * b / nblocks;
+        while (t < nt && A * (t + 1) + (double)eb[t + 1] <= target) ++t;
+        // nearer of the two boundaries around the target; every CTA keeps >= 1 tile
+        if (t < nt && target - (A * t + (double)eb[t]) > (A * (t + 1) + (double)eb[t + 1]) - target) ++t;
+        jpart[b] = std::max(jpart[b - 1] + 1, std::min(t, nt - (nblocks - b)));
+        t = jpart[b];
+    }
+    return FEMI_OK;
+}
+
 femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, double* u_vert,
                         const femi_cg_opts& o, int32_t* iters, double* relres, cudaStream_t st,
                         int64_t* total_iters) {
+    static bool pre_set = false;
+    if (!pre_set) {
+        if (const char* e = std::getenv("FEMI_PDL_PRE")) {
+            const int v = std::max(0, std::min(JNS, std::atoi(e)));
+            FEMI_CUDA(cudaMemcpyToSymbol(g_pdl_pre, &v, sizeof(int)));
+        }
+        pre_set = true;
+    }
     GraphCache* C = (GraphCache*)S->scratch;
     const int64_t n = S->n_u;
     if (!C) {
@@ -1808,11 +1931,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
                 for (const void* fn : {(const void*)k_gt<false>, (const void*)k_gt<true>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
-                // tiles -> CTAs: equal contiguous ranges (measured better than byte-weighted ranges
-                // and than dynamic scheduling, which loses gather locality)
-                const int nt = S->jds_ntile;
-                jpart.resize(C->gt_blocks + 1);
-                for (int b = 0; b <= C->gt_blocks; ++b) jpart[b] = (int)((int64_t)nt * b / C->gt_blocks);
+                femi_status ts = tile_split(S, C->gt_blocks, jpart);
+                if (ts != FEMI_OK) return ts;
             }
         }
         const int pb = std::max(C->gs_blocks, C->gt_blocks);
@@ -1908,6 +2028,14 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     if (loop_prof) {
         const femi_status ps = loop_prof_end(st);
         if (ps != FEMI_OK) return ps;
+        if (std::getenv("FEMI_CTA_PROF") && S->jds_ntile > 0) {  // entries per k_gt CTA (static split)
+            std::vector<int32_t> eb(S->jds_ntile + 1), jp;
+            FEMI_CUDA(cudaMemcpy(eb.data(), S->jds_eb, sizeof(int32_t) * eb.size(), cudaMemcpyDeviceToHost));
+            const femi_status ts = tile_split(S, C->gt_blocks, jp);
+            if (ts != FEMI_OK) return ts;
+            for (int b = 0; b < C->gt_blocks; ++b)
+                std::fprintf(stderr, "[femi ctaw] %d %d %d\n", b, jp[b + 1] - jp[b], eb[jp[b + 1]] - eb[jp[b]]);
+        }
     }
     count_launches(10);
     CgState hs;
@@ -2039,8 +2167,9 @@ femi_status graph_solve_multi(femi_system_s* S, int nr, const double* const* g, 
                               (const void*)k_gtm<3, false>, (const void*)k_gtm<4, true>, (const void*)k_gtm<4, false>};
         for (const void* fn : fns)
             FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->smem));
-        std::vector<int32_t> jpart(C->gt_blocks + 1);
-        for (int b = 0; b <= C->gt_blocks; ++b) jpart[b] = (int)((int64_t)S->jds_ntile * b / C->gt_blocks);
+        std::vector<int32_t> jpart;
+        femi_status ts = tile_split(S, C->gt_blocks, jpart);
+        if (ts != FEMI_OK) return ts;
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t vb = al(sizeof(double) * std::max<int64_t>(n + 1, (int64_t)S->jds_ntile * kJdsRows));
         const size_t bytes = al(sizeof(int32_t) * jpart.size()) + al(sizeof(RItem) * nr) + al(sizeof(CgState) * nr) +

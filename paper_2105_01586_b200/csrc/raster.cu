@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
                 }
                 if (hasf) {
                     if (e_px) e_px[pix] = e;
-                    es[c1 - c0 + 32 * h + lane] = e;
-                    ps[c1 - c0 + 32 * h + lane] = cls ? -1 : pix;
+                    // vertex pixels (not arg-max candidates) staged with the sign bit set (-e,
+                    // -0.0 for e = 0); phase 2 adds |e| -- the same value
+                    es[c1 - c0 + 32 * h + lane] = cls ? -e : e;
+                    ps[c1 - c0 + 32 * h + lane] = pix;
                 }
             }
           }
@@ -338,15 +340,17 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
             // ---- phase 2: lane per triangle, pixel order
             if (hasf) {
                 const int lo = max(my0, c0), hi = min(my1, c0 + CH);
+                int bk = -1;
                 for (int k = lo; k < hi; ++k) {
-                    const double e = es[k - c0];
+                    const double es_k = es[k - c0];
+                    const double e = fabs(es_k);
                     acc = __dadd_rn(acc, e);
-                    const int pk = ps[k - c0];
-                    if (pk >= 0 && e > be) {
+                    if (__double_as_longlong(es_k) >= 0 && e > be) {
                         be = e;
-                        bp = pk;
+                        bk = k;
                     }
                 }
+                if (bk >= 0) bp = ps[bk - c0];
             }
             __syncwarp();
         }

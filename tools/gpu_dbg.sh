@@ -1,6 +1,9 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_lx.json 2> gpurun_out/bench_lx.err
-FEMI_LOOP_PROF=1 timeout 300 python bench.py --steps 2 --warmup 1 > /dev/null 2> gpurun_out/loopprof.err
+for rep in 1 2; do
+for P in 0 2 6; do
+FEMI_PDL_PRE=$P timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_pre${P}_$rep.json 2>/dev/null
+done
+FEMI_NO_PDL=1 timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_nopdl_$rep.json 2>/dev/null
+done
 echo done
