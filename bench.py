@@ -11,7 +11,9 @@ so no extra flush is needed between steps.
 
     value  = whole-job Mpixels/s = ranks * W*H * K / max-over-ranks device time
     e2e    = the same with f and g copied host->device (pinned) and SSE device->host
-             inside every step
+             inside every step; the copies run on a second stream into double buffers, so
+             step k+1's inputs move while step k computes (PCIe-bound: ~10 ms of copies
+             against ~4.8 ms of compute at C5)
     roofline: the PCG iteration (k_gu update + k_gt TMA SpMV), algorithmic bytes per iteration
              12 nnz_uu + 4 (n_u+1) + 80 n_u x iterations over
              the solve's device time, against MEASURED_PEAKS.json hbm_gbs.
@@ -321,29 +323,57 @@ def run_ours(args):
         f_host.copy_(torch.as_tensor(c["f"].reshape(-1)))
         g_host = torch.empty(sysm.m, dtype=torch.float64, pin_memory=True)
         g_host.copy_(g_dev.cpu())
-        f_d2 = torch.empty_like(f_dev)
-        g_d2 = torch.empty_like(g_dev)
+        # double-buffered inputs: step k+1's copies (g then f, on a copy stream) are issued
+        # right after step k's kernels, so they overlap step k's solve and raster; the raster
+        # of a step waits for its f, the solve for its g
+        f_d2 = [torch.empty_like(f_dev) for _ in range(2)]
+        g_d2 = [torch.empty_like(g_dev) for _ in range(2)]
         sse_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        cs = torch.cuda.Stream(device=dev)
+        g_ready = [torch.cuda.Event() for _ in range(2)]
+        f_ready = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
 
-        def step_e2e():
-            f_d2.copy_(f_host, non_blocking=True)
-            g_d2.copy_(g_host, non_blocking=True)
-            femi.inpaint_solve_batched([sysm], [g_d2], [u_vert], opts)
-            femi.rasterise_error(sysm, u_vert, f_d2, sse, u_px, e_px, tri_err, best)
-            sse_host.copy_(sse, non_blocking=True)
-            stream.synchronize()
-            return float(sse_host[0])
+        def issue_copy(k):
+            b = k % 2
+            cs.wait_event(used[b])  # step k-2 is done with this buffer
+            with torch.cuda.stream(cs):
+                g_d2[b].copy_(g_host, non_blocking=True)
+                g_ready[b].record(cs)
+                f_d2[b].copy_(f_host, non_blocking=True)
+                f_ready[b].record(cs)
 
-        for _ in range(max(1, args.warmup)):
-            step_e2e()
+        def run_e2e(nsteps, ev=None):
+            if ev:
+                ev[0].record(stream)
+            for b in range(2):
+                used[b].record(stream)  # the copies start inside the timed region
+            issue_copy(0)
+            s_val = None
+            for k in range(nsteps):
+                b = k % 2
+                stream.wait_event(g_ready[b])
+                femi.inpaint_solve_batched([sysm], [g_d2[b]], [u_vert], opts)
+                stream.wait_event(f_ready[b])
+                femi.rasterise_error(sysm, u_vert, f_d2[b], sse, u_px, e_px, tri_err, best)
+                used[b].record(stream)
+                sse_host.copy_(sse, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(stream)
+                if k + 1 < nsteps:
+                    issue_copy(k + 1)
+                done.synchronize()
+                s_val = float(sse_host[0])
+            if ev:
+                ev[1].record(stream)
+            return s_val
+
+        run_e2e(max(1, args.warmup))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            s_e2e = step_e2e()
-        b.record(stream)
+        s_e2e = run_e2e(args.steps, (a, b))
         torch.cuda.synchronize()
         t_e2e = multi.max_over_ranks(a.elapsed_time(b), device=dev)
         assert abs(s_e2e / Npx - mse) <= 1e-9 * mse
