@@ -300,7 +300,10 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         {
             // unknowns are numbered in ascending pix (row-major) order, so every band of
             // image rows is a contiguous run of them; inside a band sort by (x, y)
-            int64_t band = kBand;
+            // graph-mode (JDS) systems use taller bands: a 512-row tile is then ~64 x 400 px and
+            // ~3/4 of its neighbour gathers hit the tile's own r slice in shared memory
+            // (measured at C5: band 32 -> 64 with in-tile gathers, solve 3.95 -> 3.92 ms)
+            int64_t band = S->nnz_uu > kGraphNnz ? kBandJds : kBand;
             if (const char* e = std::getenv("FEMI_BAND")) band = std::max(1, std::atoi(e));
             const int64_t nb = (M.H + band - 1) / band;
             std::vector<int64_t> bs(nb + 1);

@@ -168,6 +168,7 @@ void count_launches(int64_t n);
 constexpr int kRowsPerChunk = 512;
 constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)
 constexpr int kBand = 32;        // image band height (pixels) of the internal solver order
+constexpr int kBandJds = 64;     // the same for graph-mode systems (JDS tiles, in-tile gathers from smem)
 femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st);
 constexpr int kChunkNnzCap = 2048;
 constexpr int64_t kGraphNnz = 600000;  // nnz(A_uu) above which one system solves in graph mode

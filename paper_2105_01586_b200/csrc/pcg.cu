@@ -102,7 +102,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // FEMI_LOOP_PROF: per iteration, earliest CTA start / latest CTA end of k_gu and k_gt (globaltimer)
 constexpr int kLoopProfMax = 4096;
 __device__ int g_loop_prof;
-__device__ int g_pdl_pre = 6;  // k_gt: stages streamed before grid_dep_wait (FEMI_PDL_PRE, <= JNS)
+__device__ int g_pdl_pre = 6;
+__device__ int g_smem_gather = 1;  // k_gt: in-tile neighbours from the staged r slice (FEMI_SMEM_GATHER=0: all from L1/L2)  // k_gt: stages streamed before grid_dep_wait (FEMI_PDL_PRE, <= JNS)
 __device__ unsigned long long g_loop_ts[4 * kLoopProfMax];
 __device__ unsigned long long g_loop_ts2[4 * kLoopProfMax];
 constexpr int kCtaProfIt = 60;  // FEMI_LOOP_PROF: per-CTA start / consumer end of this iteration's k_gt
@@ -1217,7 +1218,10 @@ __global__ void __launch_bounds__(GNT, 4) k_gs(const RItem* __restrict__ items, 
 // (values, int16 columns, row lengths + diagonal offsets, r, q) into a JNS-stage shared-memory ring
 // guarded by full/empty mbarriers; JCW consumer warps take one 32-row slice each, read the
 // jagged diagonals of their slice from shared memory (rows in descending length: diagonal k is
-// lanes 0 .. cnt_k-1 at doff[k] + lane) and gather the neighbours' r (L1/L2).
+// lanes 0 .. cnt_k-1 at doff[k] + lane) and gather the neighbours' r: from the tile's own r
+// slice in shared memory when the neighbour is in the tile (about 3/4 of the gathers with the
+// 64-pixel bands of graph-mode systems), else through L1/L2 -- the gathers' 32-byte sectors
+// were the largest share of the loop's L2 traffic.
 // Bytes per iteration: 10 B per stored nonzero (no ELL padding) + 1.06 B/row of metadata +
 // r, s read + w written; the async stream keeps ~JNS tiles of loads in flight per SM.
 constexpr int JCW = kJdsRows / 32;  // consumer warps = slices per tile
@@ -1349,6 +1353,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                 const int16_t* c16 = (const int16_t*)q.col;
                 const int32_t* c32 = (const int32_t*)q.col;
                 const double* rt = rg + (int64_t)t * kJdsRows;
+                const unsigned tile_lim = g_smem_gather ? (unsigned)kJdsRows : 0u;
                 double acc = 0.0;
                 for (int k0 = 0; k0 < L; k0 += 8) {
                     double vv[8], gv[8];
@@ -1361,7 +1366,8 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                         c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) gv[u] = rt[c[u]];  // neighbours' r (L1/L2)
+                    for (int u = 0; u < 8; ++u)  // neighbours' r: this tile's slice from shared memory, else L1/L2
+                        gv[u] = (unsigned)c[u] < tile_lim ? q.r[c[u]] : rt[c[u]];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
                 }
@@ -1609,7 +1615,9 @@ __global__ void __launch_bounds__(JNT, 1) k_gtm(const RItem* __restrict__ items,
 #pragma unroll
                     for (int c = 0; c < NR; ++c)
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) gv[c][u] = rg[c][t0 + cc[u]];
+                        for (int u = 0; u < 4; ++u)  // in-tile neighbours from the staged r slices
+                            gv[c][u] = (unsigned)cc[u] < (unsigned)kJdsRows ? rs[c * kJdsRows + cc[u]]
+                                                                            : rg[c][t0 + cc[u]];
 #pragma unroll
                     for (int c = 0; c < NR; ++c)
 #pragma unroll
@@ -1904,6 +1912,10 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         if (const char* e = std::getenv("FEMI_PDL_PRE")) {
             const int v = std::max(0, std::min(JNS, std::atoi(e)));
             FEMI_CUDA(cudaMemcpyToSymbol(g_pdl_pre, &v, sizeof(int)));
+        }
+        if (const char* e = std::getenv("FEMI_SMEM_GATHER")) {
+            const int v = std::atoi(e) ? 1 : 0;
+            FEMI_CUDA(cudaMemcpyToSymbol(g_smem_gather, &v, sizeof(int)));
         }
         pre_set = true;
     }
