@@ -2061,6 +2061,47 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     }
     // the body runs whole unrolled groups: kernels after convergence exit at once but still launch
     count_launches(2 * (int64_t)((hs.iters + kUnroll - 1) / kUnroll) * kUnroll);
+    if (std::getenv("FEMI_PCG_KBENCH") && C->gt_smem > 0) {
+        // profiling aid: the loop body's kernels launched standalone on the converged state
+        // (alpha = beta = 0 keeps the iterate), so ncu can capture them -- kernel nodes of a
+        // graph with conditional nodes cannot be profiled one by one. Event times to stderr.
+        CgState a = hs;
+        a.active = 1;
+        a.alpha = a.beta = a.alpha_pend = 0.0;
+        a.x_pend = 0;
+        unsigned* gcnt = C->d_cnt + 2;
+        cudaEvent_t e0, e1, e2;
+        FEMI_CUDA(cudaEventCreate(&e0));
+        FEMI_CUDA(cudaEventCreate(&e1));
+        FEMI_CUDA(cudaEventCreate(&e2));
+        float tu = 0.f, tg = 0.f;
+        const int reps = 12;
+        for (int k = 0; k < reps; ++k) {
+            FEMI_CUDA(cudaMemcpyAsync(C->d_state, &a, sizeof(CgState), cudaMemcpyHostToDevice, st));
+            FEMI_CUDA(cudaEventRecord(e0, st));
+            k_gu<<<dim3(std::min(C->gx * 2, 1184)), GNT, 0, st>>>(C->d_items);
+            FEMI_CUDA(cudaEventRecord(e1, st));
+            k_gt<false><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt,
+                                                                      (cudaGraphConditionalHandle)0);
+            FEMI_CUDA(cudaEventRecord(e2, st));
+            FEMI_CUDA(cudaEventSynchronize(e2));
+            float x = 0.f, y = 0.f;
+            FEMI_CUDA(cudaEventElapsedTime(&x, e0, e1));
+            FEMI_CUDA(cudaEventElapsedTime(&y, e1, e2));
+            if (k >= 2) {
+                tu += x;
+                tg += y;
+            }
+        }
+        std::fprintf(stderr, "[femi kbench] standalone k_gu %.2f us, k_gt %.2f us\n", 1e3 * tu / (reps - 2),
+                     1e3 * tg / (reps - 2));
+        FEMI_CUDA(cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        count_launches(2 * reps);
+    }
     const double rel = hs.bn2 > 0.0 ? std::sqrt(hs.res2 / hs.bn2) : 0.0;
     if (iters) *iters = hs.iters;
     if (relres) *relres = rel;
