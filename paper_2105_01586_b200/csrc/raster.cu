@@ -183,8 +183,11 @@ __device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_pt
 // exact integer edge functions as planes w = A px + B py + C (S3: w_b = orient(c,a,p),
 // w_c = orient(a,b,p)), D = orient(a,b,c) and its correctly rounded reciprocal, u_a and the
 // differences u_b - u_a, u_c - u_a.
+// 16-byte aligned (size padded to a multiple of 16): the per-entry reads of a slot become
+// 128-bit shared loads (half the LDS instructions and wavefronts of 64-bit ones; the 96-byte
+// stride keeps consecutive slots on disjoint banks)
 template <int NC>
-struct RTri {
+struct __align__(16) RTri {
     int A1, B1, C1, A2, B2, C2, pad0, pad1;
     double D, rD;
     double db[NC], dc[NC], u[NC][3];
