@@ -500,9 +500,21 @@ def run_workload(args):
         best = [torch.empty(S.T, dtype=torch.int32, device=dev) for S in systems]
         opts = femi.cg_opts(rtol=RTOL)
 
-        def step():
-            st, it, rel = femi.inpaint_solve_batched(systems, gs, us, opts)
-            femi.rasterise_error_batched(systems, us, [f_dev] * B, sse, e_px=e_px, tri_err=tri, best=best)
+        split = []
+        # the public API's plan objects: arguments marshalled once, one C call per stage
+        solve_plan = femi.SolvePlan(systems, gs, us, opts)
+        raster_plan = femi.RasterPlan(systems, us, [f_dev] * B, sse, e_px=e_px, tri_err=tri, best=best)
+
+        def step(evs=None):
+            if evs:
+                evs[0].record(stream)
+            st, it, rel = solve_plan.run()
+            if evs:
+                evs[1].record(stream)
+            raster_plan.run()
+            if evs:
+                evs[2].record(stream)
+                split.append(evs)
             return it
 
         for _ in range(args.warmup):
@@ -523,6 +535,11 @@ def run_workload(args):
         mse_all = multi.gather_scalars(np.array([float(x.item()) / Npx for x in sse]), nb if args.shard else B,
                                        device=dev) if (args.shard and world > 1) else \
             np.array([float(x.item()) / Npx for x in sse])
+        for _ in range(3):  # solve / raster split, measured after the timed region
+            step([ev(), ev(), ev()])
+        torch.cuda.synchronize()
+        detail.update(solve_ms=float(np.median([e[0].elapsed_time(e[1]) for e in split])),
+                      raster_ms=float(np.median([e[1].elapsed_time(e[2]) for e in split])))
         detail.update(solves_per_s=B / (ms * 1e-3), cg_iters_mean=float(np.mean(it)), cg_iters_max=int(np.max(it)),
                       mse_first4=[float(v) for v in mse_all[:4]], batch_per_rank=B,
                       sharded=bool(args.shard and world > 1))

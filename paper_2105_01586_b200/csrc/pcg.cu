@@ -132,21 +132,36 @@ __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     st[b] = s;
 }
 
+// min/max of g per item (x0 = midrange): blockIdx.y = item, one atomic pair per block
 __global__ void k_minmax(int B, const RItem* __restrict__ items) {
-    for (int b = 0; b < B; ++b) {
-        const RItem& it = items[b];
-        if (it.x0mode != 1 || it.g == nullptr) continue;
-        unsigned long long lo = ~0ull, hi = 0ull;
-        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x) {
-            unsigned long long key = dkey(it.g[k]);
-            lo = min(lo, key);
-            hi = max(hi, key);
-        }
+    __shared__ unsigned long long slo[32], shi[32];
+    if ((int)blockIdx.y >= B) return;
+    const RItem& it = items[blockIdx.y];
+    if (it.x0mode != 1 || it.g == nullptr) return;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x) {
+        const unsigned long long key = dkey(it.g[k]);
+        lo = min(lo, key);
+        hi = max(hi, key);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) {
+        slo[wid] = lo;
+        shi[wid] = hi;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        lo = lane < nw ? slo[lane] : ~0ull;
+        hi = lane < nw ? shi[lane] : 0ull;
         for (int o = 16; o > 0; o >>= 1) {
             lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
             hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
-        if ((threadIdx.x & 31) == 0 && hi != 0ull) {
+        if (lane == 0 && hi != 0ull) {
             atomicMin(&it.st->kmin, lo);
             atomicMax(&it.st->kmax, hi);
         }
@@ -2162,7 +2177,7 @@ femi_status build_graph_m(GraphCacheM& C, bool restart, cudaGraphExec_t* out) {
     if (!restart) {
         if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
         void* a_mm[2] = {&nr, &di};
-        if ((s = chain((void*)k_minmax, dim3(296), dim3(256), a_mm))) return s;
+        if ((s = chain((void*)k_minmax, dim3(296, (unsigned)nr), dim3(256), a_mm))) return s;
         if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
         if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
     }
@@ -2602,7 +2617,8 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     if (o.x0 == 1) {
         int64_t mmax = 0;
         for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
-        k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296)), 256, 0, st>>>(B, d_items);
+        k_minmax<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296)), (unsigned)B), 256, 0,
+                   st>>>(B, d_items);
         count_launches(1);
     }
     if (nmax > 0) {

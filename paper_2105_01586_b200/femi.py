@@ -228,33 +228,71 @@ def cg_opts(rtol=1e-10, max_iter=100000, precond=1, x0=1, check_every=0) -> CgOp
     return CgOpts(rtol, max_iter, precond, x0, check_every)
 
 
+def _dptr_array(L, dtype):
+    """ctypes array of the device pointers of a list of contiguous CUDA tensors (None -> NULL)."""
+    if L is None:
+        return None
+    ptrs = []
+    for t in L:
+        if t is None:
+            ptrs.append(None)
+            continue
+        if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+            raise FemiError(1, f"expected contiguous CUDA tensors of dtype {dtype}")
+        ptrs.append(t.data_ptr())
+    return (ctypes.c_void_p * len(ptrs))(*ptrs)
+
+
+class SolvePlan:
+    """The arguments of one batched solve, marshalled once (pointer arrays, result buffers);
+    run() is then a single C call -- for small batched workloads whose host-side marshalling
+    would otherwise show up between the launches. The tensors must stay alive and in place."""
+
+    def __init__(self, systems, g_list, u_list, opts: CgOpts | None = None):
+        import torch
+        self.B = len(systems)
+        self.opts = opts or cg_opts()
+        self._keep = (list(systems), list(g_list), list(u_list))
+        self.sys_arr = _ptr_array([s._h for s in systems])
+        self.g_arr = _dptr_array(g_list, torch.float64)
+        self.u_arr = _dptr_array(u_list, torch.float64)
+        self.iters = np.zeros(self.B, np.int32)
+        self.rel = np.zeros(self.B, np.float64)
+        self._pi, self._pr = _hptr(self.iters), _hptr(self.rel)
+
+    def run(self, stream=None):
+        st = lib().femi_inpaint_solve_batched(self.B, self.sys_arr, self.g_arr, self.u_arr, ctypes.byref(self.opts),
+                                              self._pi, self._pr, _stream(stream))
+        if st not in (FEMI_OK, 4):
+            _check(st)
+        return st, self.iters.copy(), self.rel.copy()
+
+
 def inpaint_solve_batched(systems, g_list, u_list, opts: CgOpts | None = None, stream=None):
     """S2. Returns (status, iters[B], relres[B]); raises on hard errors."""
-    import torch
-    B = len(systems)
-    opts = opts or cg_opts()
-    sys_arr = _ptr_array([s._h for s in systems])
-    g_arr = _ptr_array([_dptr(g, torch.float64) for g in g_list])
-    u_arr = _ptr_array([_dptr(u, torch.float64) for u in u_list])
-    iters = np.zeros(B, np.int32)
-    rel = np.zeros(B, np.float64)
-    st = lib().femi_inpaint_solve_batched(B, sys_arr, g_arr, u_arr, ctypes.byref(opts), _hptr(iters), _hptr(rel),
-                                          _stream(stream))
-    if st not in (FEMI_OK, 4):
-        _check(st)
-    return st, iters, rel
+    return SolvePlan(systems, g_list, u_list, opts).run(stream)
+
+
+class RasterPlan:
+    """rasterise_error_batched with its arguments marshalled once (see SolvePlan)."""
+
+    def __init__(self, systems, u_list, f_list, sse_list, u_px=None, e_px=None, tri_err=None, best=None):
+        import torch
+        self.B = len(systems)
+        self._keep = (list(systems), u_list, f_list, sse_list, u_px, e_px, tri_err, best)
+        f64 = torch.float64
+        self.args = (_ptr_array([s._h for s in systems]), _dptr_array(u_list, f64), _dptr_array(f_list, f64),
+                     _dptr_array(u_px, f64), _dptr_array(e_px, f64), _dptr_array(tri_err, f64),
+                     _dptr_array(best, torch.int32), _dptr_array(sse_list, f64))
+
+    def run(self, stream=None):
+        _check(lib().femi_rasterise_error_batched(self.B, *self.args, _stream(stream)))
 
 
 def rasterise_error_batched(systems, u_list, f_list, sse_list, u_px=None, e_px=None, tri_err=None, best=None,
                             stream=None):
     """S3+S4 (enqueue only)."""
-    import torch
-    B = len(systems)
-    opt = lambda L, dt: _ptr_array([_dptr(x, dt) for x in L]) if L is not None else None  # noqa: E731
-    _check(lib().femi_rasterise_error_batched(
-        B, _ptr_array([s._h for s in systems]), opt(u_list, torch.float64), opt(f_list, torch.float64),
-        opt(u_px, torch.float64), opt(e_px, torch.float64), opt(tri_err, torch.float64), opt(best, torch.int32),
-        opt(sse_list, torch.float64), _stream(stream)))
+    RasterPlan(systems, u_list, f_list, sse_list, u_px, e_px, tri_err, best).run(stream)
 
 
 def rasterise_error(system, u_vert, f, sse, u_px=None, e_px=None, tri_err=None, best=None, stream=None):
