@@ -9,6 +9,9 @@
 // P^T r is a per-triangle adjoint raster (warp per triangle, the same ownership rule as
 // the forward raster) producing three partial sums per triangle, gathered per vertex over
 // the vertex->triangle incidence list in ascending triangle order (deterministic).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -111,8 +114,18 @@ struct Tonal {
     double* dres;   // dot result
     int64_t solves = 0, iters = 0;
     femi_status status = FEMI_OK;
+    double t_solve = 0.0, t_dot = 0.0;  // FEMI_TONAL_PROF: host wall time in the inner solves / dots
+    static double now() {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
 
     femi_status dot(int64_t n, const double* a, const double* b, double* out) {
+        const double t0 = now();
+        struct Acc {
+            double& t;
+            double t0;
+            ~Acc() { t += now() - t0; }
+        } acc{t_dot, t0};
         const int nb = 296;
         k_dot_part<<<nb, TT, 0, st>>>(n, a, b, part); count_launches(1);
         k_dot_final<<<1, TT, 0, st>>>(nb, part, dres); count_launches(1);
@@ -136,7 +149,9 @@ struct Tonal {
         femi_system_s* Sv[1] = {S};
         const double* gv[1] = {g};
         double* uvv[1] = {uv};
+        const double ts0 = now();
         femi_status s = pcg_solve(1, Sv, gv, nullptr, uvv, o, &it, &rr, st, &tot);
+        t_solve += now() - ts0;
         ++solves;
         iters += tot;
         if (s == FEMI_E_NONFINITE || s == FEMI_E_CUDA || s == FEMI_E_OOM) return s;
@@ -160,7 +175,9 @@ struct Tonal {
         femi_system_s* Sv[1] = {S};
         const double* bv[1] = {w};
         double* yvv[1] = {yv};
+        const double ts0 = now();
         femi_status s = pcg_solve(1, Sv, nullptr, bv, yvv, o, &it, &rr, st, &tot);
+        t_solve += now() - ts0;
         ++solves;
         iters += tot;
         if (s == FEMI_E_NONFINITE || s == FEMI_E_CUDA || s == FEMI_E_OOM) return s;
@@ -289,6 +306,9 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     }
 out:
 #undef TRY
+    if (std::getenv("FEMI_TONAL_PROF"))
+        std::fprintf(stderr, "[femi tonal] solves %lld (%lld CG iterations): %.3f ms in pcg_solve, %.3f ms in dots\n",
+                     (long long)tn.solves, (long long)tn.iters, 1e3 * tn.t_solve, 1e3 * tn.t_dot);
     rep->inner_solves = (int32_t)tn.solves;
     rep->inner_iters = tn.iters;
     cudaFreeAsync(base, st);
