@@ -141,6 +141,43 @@ def test_config2_batched_block_diagonal():
     assert torch.abs(u1 - us[3]).max().item() <= GREY_TOL
 
 
+@pytest.mark.gpu
+def test_batched_plans_reuse():
+    """SolvePlan / RasterPlan (arguments marshalled once, bench C2): repeated runs equal the
+    one-shot calls bit for bit (deterministic solves and reductions); bad tensors raise."""
+    c = make_config(2)
+    W, H = c["W"], c["H"]
+    f = dev(c["f"]).reshape(-1)
+    meshes = [femi.Mesh(W, H, c["masks"][b], c["unknowns"][b]) for b in range(4)]
+    systems = [femi.System(M) for M in meshes]
+    gs = [pipeline.mask_values(f, M.export()["vert_px"], s.n_u) for M, s in zip(meshes, systems)]
+    us = [torch.empty(s.nv, dtype=torch.float64, device=DEV) for s in systems]
+    sse = [torch.zeros(1, dtype=torch.float64, device=DEV) for _ in systems]
+    tri = [torch.empty(s.T, dtype=torch.float64, device=DEV) for s in systems]
+    sp = femi.SolvePlan(systems, gs, us, femi.cg_opts(rtol=1e-10))
+    rp = femi.RasterPlan(systems, us, [f] * 4, sse, tri_err=tri)
+    runs = []
+    for _ in range(3):
+        st, it, rel = sp.run()
+        rp.run()
+        torch.cuda.synchronize()
+        assert st == 0 and np.all(rel <= 1e-10)
+        runs.append(([u.clone() for u in us], [x.item() for x in sse], [t.clone() for t in tri]))
+    us2 = [torch.empty_like(u) for u in us]
+    sse2 = [torch.zeros(1, dtype=torch.float64, device=DEV) for _ in systems]
+    femi.inpaint_solve_batched(systems, gs, us2, femi.cg_opts(rtol=1e-10))
+    femi.rasterise_error_batched(systems, us2, [f] * 4, sse2)
+    torch.cuda.synchronize()
+    for u_r, s_r, t_r in runs:
+        for b in range(4):
+            assert torch.equal(u_r[b], us2[b]) and s_r[b] == sse2[b].item()
+            assert torch.equal(t_r[b], runs[0][2][b])
+    with pytest.raises(femi.FemiError):
+        femi.SolvePlan(systems, [g.float() for g in gs], us)
+    with pytest.raises(femi.FemiError):
+        femi.RasterPlan(systems, [u.cpu() for u in us], [f] * 4, sse)
+
+
 def _near_tie_ok(gpu_new, ora_new, S, R, u_vert, f):
     """Reading A15: sets may differ only where the oracle's own ranking has a near-tie at
     the decision (triangle cut or per-triangle arg-max) within what the solve tolerance
