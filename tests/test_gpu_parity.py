@@ -311,6 +311,23 @@ def test_config5_full_size():
     check_inpaint(8192, 8192, c["f"], mask, c["unknowns"])
 
 
+def test_max_image_size():
+    """The largest image the ABI accepts (W = H = 16384: 14-bit coordinates in the pixel
+    lists, int32 pixel indices up to 2^28): sparse mask, every check of check_inpaint
+    (bit-exact mesh, raster, error maps and per-triangle reductions against the oracle)."""
+    W = H = 16384
+    rng = np.random.default_rng(16384)
+    m = 60000
+    mk = draw_mask(rng, W * H, m)
+    un = draw_unknowns(rng, W, H, mk, m)
+    y, x = np.mgrid[0:H, 0:W].astype(np.float32)
+    f = (128.0 + 90.0 * np.sin(x / 900.0) * np.cos(y / 1300.0)).astype(np.float64)
+    del x, y
+    # 60K unknowns spread over 268M px: long edges, a badly conditioned A_uu -- at rtol 1e-10
+    # the grey values move by ~3e-4 (kappa x relres), so this case solves to 1e-12
+    check_inpaint(W, H, f, mk, un, rtol=1e-12)
+
+
 def _colour_case(W, seed, density=0.02):
     """Three seeded channels (the synthetic recipe with different draws) on one mask."""
     fs = [make_config(5, W=W, H=W, seed=seed + k)["f"].reshape(-1) for k in range(3)]
