@@ -1428,14 +1428,18 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
 // iteration 12 nnz + 4 (n+1) + 80 NR n algorithmic bytes instead of NR (12 nnz + ...).
 template <int NR>
 __global__ void __launch_bounds__(GNT) k_gum(const RItem* __restrict__ items) {
-    double al[NR], be[NR];
-    bool on[NR];
+    // per RHS the same update as k_gu, x included in every other iteration only (its own
+    // iteration count decides: even defers alpha_i p_i, odd applies both terms)
+    double al[NR], be[NR], ap[NR];
+    bool on[NR], lazy[NR];
 #pragma unroll
     for (int c = 0; c < NR; ++c) {
         const CgState* S = items[c].st;
         on[c] = S->active;
         al[c] = S->alpha;
         be[c] = S->beta;
+        ap[c] = S->alpha_pend;
+        lazy[c] = (S->iters & 1) == 0;
     }
     const int n = items[0].n, stride = gridDim.x * blockDim.x;
 #pragma unroll
@@ -1447,13 +1451,23 @@ __global__ void __launch_bounds__(GNT) k_gum(const RItem* __restrict__ items) {
         double* __restrict__ p = it.p;
         double* __restrict__ sv = it.sv;
         double* __restrict__ x = it.x;
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-            const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i], xi = x[i];
-            const double pi = fma(be[c], pi0, ri), si = fma(be[c], si0, wi);
-            p[i] = pi;
-            sv[i] = si;
-            x[i] = fma(al[c], pi, xi);
-            r[i] = fma(-al[c], si, ri);
+        if (lazy[c]) {
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+                const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i];
+                const double si = fma(be[c], si0, wi);
+                p[i] = fma(be[c], pi0, ri);
+                sv[i] = si;
+                r[i] = fma(-al[c], si, ri);
+            }
+        } else {
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+                const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i], xi = x[i];
+                const double pi = fma(be[c], pi0, ri), si = fma(be[c], si0, wi);
+                p[i] = pi;
+                sv[i] = si;
+                x[i] = fma(al[c], pi, fma(ap[c], pi0, xi));
+                r[i] = fma(-al[c], si, ri);
+            }
         }
     }
 }
@@ -1511,6 +1525,10 @@ __device__ __forceinline__ void cg_tail_m(double (&v)[NR][3], const bool (&act)[
         for (int w = 0; w < JNT / 32; ++w)
             for (int q = 0; q < 3; ++q) d[q] += shm[NQ * w + 3 * c + q];
         const int need = FIRST ? 1 : S->need_rho;
+        if (!FIRST && act[c]) {  // the k_gum before this SpMV deferred its x term (even) or not
+            S->x_pend = (S->iters & 1) == 0 ? 1 : 0;
+            S->alpha_pend = S->alpha;
+        }
         anyact[c] = cg_advance<FIRST>(S, act[c], d[0], d[1], d[2], dmin, S->bn2, S->tol2, S->rr, S->alpha, S->iters,
                                       S->max_iter, need);
     }
