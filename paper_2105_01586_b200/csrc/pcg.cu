@@ -1289,7 +1289,10 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     // body) this CTA is resident while k_gu still runs, and the producer already streams the
     // values, columns and metadata of its first JNS tiles (expect_tx without an arrival keeps
     // each stage's phase open); r and q follow once the update kernel has completed.
-    const int npre = min(g_pdl_pre, te - tb);
+    // no prefetch for the no-op tail of the unrolled body: active only goes 1 -> 0 inside one
+    // graph launch, so a 0 read before the dependency wait is final (a stale 1 only prefetches)
+    const bool live = FIRST || *(volatile const int*)&S->active;
+    const int npre = live ? min(g_pdl_pre, te - tb) : 0;
     const uint64_t pol = policy_evict_first();  // keep the CG vectors L2-resident
     if (warp == JCW && lane == 0) {
         for (int i = 0; i < npre; ++i) {
