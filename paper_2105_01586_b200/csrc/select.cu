@@ -9,6 +9,7 @@
 // the same selection over the empty pixels' e-values. Output pixels go to the host,
 // which returns them ascending.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -16,6 +17,7 @@ namespace femi {
 namespace {
 
 constexpr int ST = 256;
+constexpr int64_t kSelBlockMax = 1 << 20;  // T up to which the one-block selection is used
 
 struct SelState {
     unsigned long long prefix, mask;
@@ -160,6 +162,112 @@ __global__ void k_gather_best(int64_t n, const int32_t* __restrict__ idx, const 
         out[i] = best[idx[i]];
 }
 
+// The whole triangle selection in ONE block for small T (densification of small and medium
+// images, where the multi-kernel radix select is launch-latency bound): keys, eligible count,
+// k = min(eligible, b), the same 8-pass MSB radix select and the same emission rule (keys > K,
+// then the lowest-index ties == K), each selected triangle mapped to its best pixel. out_count
+// receives the number emitted (= k). Same result as the multi-kernel path.
+constexpr int SB = 1024;
+__global__ void __launch_bounds__(SB) k_select_tri_block(int64_t T, const double* __restrict__ tri_err,
+                                                        const int32_t* __restrict__ best, long long b,
+                                                        unsigned long long* __restrict__ key, int32_t* __restrict__ out,
+                                                        unsigned long long* __restrict__ out_count) {
+    __shared__ unsigned int hist[256];
+    __shared__ long long s_red[SB / 32];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ long long s_remaining, s_k;
+    __shared__ unsigned int s_out;
+    __shared__ int s_wsum[SB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // keys and the eligible count
+    long long cnt = 0;
+    for (int64_t t = tid; t < T; t += SB) {
+        const double e = tri_err[t];
+        const bool ok = e > 0.0 && best[t] >= 0;
+        key[t] = ok ? (unsigned long long)__double_as_longlong(e) : 0ull;
+        cnt += ok;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_red[wid] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        long long E = 0;
+        for (int w = 0; w < SB / 32; ++w) E += s_red[w];
+        s_k = E < b ? E : b;
+        s_remaining = s_k;
+        s_prefix = 0ull;
+        s_mask = 0ull;
+        s_out = 0u;
+    }
+    __syncthreads();
+    if (s_k == 0) {
+        if (tid == 0) *out_count = 0ull;
+        return;
+    }
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        if (tid < 256) hist[tid] = 0u;
+        __syncthreads();
+        const unsigned long long prefix = s_prefix, mask = s_mask;
+        for (int64_t i = tid; i < T; i += SB) {
+            const unsigned long long k = key[i];
+            if (k != 0ull && (k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (wid == 0) {  // digit D (descending) where the cumulative count reaches `remaining`
+            const long long rem = s_remaining;
+            long long c = 0;
+            for (int q = 0; q < 8; ++q) c += hist[255 - 8 * lane - q];
+            long long incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, incl >= rem);
+            const int L = __ffs(hit) - 1;  // first lane (highest digits) reaching rem
+            if (lane == L) {
+                long long cum = incl - c;
+                int D = 255 - 8 * lane;
+                for (int q = 0; q < 8; ++q) {
+                    const int d = 255 - 8 * lane - q;
+                    const long long h = hist[d];
+                    if (cum + h >= rem) {
+                        D = d;
+                        break;
+                    }
+                    cum += h;
+                }
+                s_remaining = rem - cum;
+                s_prefix = prefix | ((unsigned long long)D << shift);
+                s_mask = mask | (255ull << shift);
+            }
+        }
+        __syncthreads();
+    }
+    // emission in index order: keys > K anywhere, ties == K by ascending index
+    const unsigned long long K = s_prefix;
+    const long long need = s_remaining;
+    long long base = 0;
+    for (int64_t t0 = 0; t0 < T; t0 += SB) {
+        const int64_t i = t0 + tid;
+        const unsigned long long k = i < T ? key[i] : 0ull;
+        const bool tie = i < T && k == K;
+        if (k > K) out[atomicAdd(&s_out, 1u)] = best[i];
+        const unsigned bal = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) s_wsum[wid] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int w = 0; w < SB / 32; ++w) {
+            before += w < wid ? s_wsum[w] : 0;
+            tot += s_wsum[w];
+        }
+        if (tie && base + before + __popc(bal & ((1u << lane) - 1u)) < need) out[atomicAdd(&s_out, 1u)] = best[i];
+        base += tot;
+        __syncthreads();
+    }
+    if (tid == 0) *out_count = s_out;
+}
+
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + ST - 1) / ST, 148 * 8)); }
 
 // top-k (key desc, index asc) among keys != 0; writes up to k selected indices (mapped through
@@ -224,15 +332,41 @@ femi_status densify_select(femi_system_s* S, int nc, const double* const* f, con
     if (rc) return fail(rc);
 
     // ---- triangles: top-b by (tri_err desc, index asc)
-    if (cudaMemsetAsync(ss, 0, sizeof(SelState), st) != cudaSuccess) return fail(FEMI_E_CUDA);
+    if (T <= kSelBlockMax && std::getenv("FEMI_SEL_MULTI") == nullptr) {
+        // small T: one block does keys, count, select and emission; one round trip
+        k_select_tri_block<<<1, SB, 0, st>>>(T, tri_err, best, b, key, sel_px, cnt);
+        count_launches(1);
+        unsigned long long hk = 0;
+        if (cudaMemcpyAsync(&hk, cnt, sizeof(hk), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(cuda_fail(cudaGetLastError(), "densify: block select"));
+        const int64_t k_tri = (int64_t)hk;
+        result.resize(k_tri);
+        if (k_tri > 0 &&
+            cudaMemcpyAsync(result.data(), sel_px, sizeof(int32_t) * k_tri, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            return fail(cuda_fail(cudaGetLastError(), "densify: copy"));
+        if (k_tri == b) {
+            if (cudaStreamSynchronize(st) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "densify: sync"));
+            std::sort(result.begin(), result.end());
+            std::copy(result.begin(), result.end(), new_px);
+            *n_added = (int64_t)result.size();
+            cudaFreeAsync(base, st);
+            return FEMI_OK;
+        }
+        // shortfall: fall through to the fill below with the triangle picks already in result
+    }
+    const bool tri_done = T <= kSelBlockMax && std::getenv("FEMI_SEL_MULTI") == nullptr;
+    if (!tri_done && cudaMemsetAsync(ss, 0, sizeof(SelState), st) != cudaSuccess) return fail(FEMI_E_CUDA);
+    SelState hs;
+    int64_t k_tri = (int64_t)result.size();
+    if (!tri_done) {
     if (cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st) != cudaSuccess) return fail(FEMI_E_CUDA);
     k_tri_keys<<<grid_for(T), ST, 0, st>>>(T, tri_err, best, key, ss); count_launches(1);
-    SelState hs;
     if (cudaMemcpyAsync(&hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return fail(cuda_fail(cudaGetLastError(), "densify: eligible count"));
     const int64_t E = hs.eligible;
-    const int64_t k_tri = std::min(E, b);
+    k_tri = std::min(E, b);
     if (k_tri > 0) {
         const int nbt = (int)std::min<int64_t>(1024, (T + ST - 1) / ST);
         const int64_t per = (T + nbt - 1) / nbt;
@@ -242,6 +376,7 @@ femi_status densify_select(femi_system_s* S, int nc, const double* const* f, con
         result.resize(k_tri);
         if (cudaMemcpyAsync(result.data(), sel_px, sizeof(int32_t) * k_tri, cudaMemcpyDeviceToHost, st) != cudaSuccess)
             return fail(cuda_fail(cudaGetLastError(), "densify: copy"));
+    }
     }
     // ---- shortfall: globally largest-e empty pixels (reading A10)
     const int64_t short_b = b - k_tri;
