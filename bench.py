@@ -444,7 +444,15 @@ def run_ours(args):
                        "cg_iters": iters, "us_per_cg_iter": 1e3 * float(np.median(solve_ms)) / max(iters, 1),
                        "mse": mse, "n_unknown": n_u, "n_mask": info["n_mask"], "n_tri": info["n_tri"],
                        "nnz_uu": nnz_uu, "nnz_uk": info["nnz_uk"], "setup": setup, "version": femi.version(),
-                       "tonal20": tonal},
+                       "tonal20": tonal,
+                       # the second kernel of the step: the fused raster + error pass, 28 B/px
+                       # algorithmic (list 4 + f 8 + u 8 + e 8) + 12 B/triangle, over its event time
+                       "roofline_raster": {
+                           "kernel": "k_raster_tri + k_sse (S3+S4)", "bound": "hbm",
+                           "bytes": 28 * Npx + 12 * info["n_tri"],
+                           "achieved": (28 * Npx + 12 * info["n_tri"]) / (float(np.median(raster_ms)) * 1e-3) / 1e9,
+                           "peak": hbm, "unit": "GB/s",
+                           "frac": (28 * Npx + 12 * info["n_tri"]) / (float(np.median(raster_ms)) * 1e-3) / 1e9 / hbm}},
         }
         print(json.dumps(line))
     if world > 1:

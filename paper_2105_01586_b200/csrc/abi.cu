@@ -27,12 +27,36 @@ femi_status cuda_fail(cudaError_t e, const char* what) {
 
 namespace {
 
+// Device memory of a system: arrays up to 2 MB are carved (256-byte aligned) from 8 MB arena
+// chunks, larger ones get their own allocation -- a small system then costs one or two
+// cudaMalloc/cudaFree instead of ~30 (each cudaFree synchronises the device).
+constexpr size_t kArenaChunk = 8u << 20, kArenaMax = 2u << 20;
+femi_status dev_alloc(femi_system_s* S, void** p, size_t bytes) {
+    bytes = (std::max<size_t>(bytes, 1) + 255) & ~(size_t)255;
+    if (bytes > kArenaMax) {
+        FEMI_CUDA(cudaMalloc(p, bytes));
+        S->allocs.push_back(*p);
+        return FEMI_OK;
+    }
+    if (S->arena_left < bytes) {
+        void* c = nullptr;
+        FEMI_CUDA(cudaMalloc(&c, kArenaChunk));
+        S->arena_chunks.push_back(c);  // never in allocs: carved temporaries are not freed early
+        S->arena_cur = (char*)c;
+        S->arena_left = kArenaChunk;
+    }
+    *p = S->arena_cur;
+    S->arena_cur += bytes;
+    S->arena_left -= bytes;
+    return FEMI_OK;
+}
+
 template <class T>
 femi_status upload(femi_system_s* S, T** dst, const std::vector<T>& src, cudaStream_t st, size_t extra = 0) {
     size_t n = src.size() + extra;
     void* p = nullptr;
-    FEMI_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
-    S->allocs.push_back(p);
+    femi_status s = dev_alloc(S, &p, sizeof(T) * std::max<size_t>(n, 1));
+    if (s) return s;
     if (!src.empty()) FEMI_CUDA(cudaMemcpyAsync(p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, st));
     *dst = (T*)p;
     return FEMI_OK;
@@ -41,8 +65,8 @@ femi_status upload(femi_system_s* S, T** dst, const std::vector<T>& src, cudaStr
 template <class T>
 femi_status alloc(femi_system_s* S, T** dst, size_t n) {
     void* p = nullptr;
-    FEMI_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
-    S->allocs.push_back(p);
+    femi_status s = dev_alloc(S, &p, sizeof(T) * std::max<size_t>(n, 1));
+    if (s) return s;
     *dst = (T*)p;
     return FEMI_OK;
 }
@@ -185,6 +209,7 @@ void femi_system_free(femi_system sys) {
     cudaDeviceSynchronize();
     pcg_cache_free(sys);
     for (void* p : sys->allocs) cudaFree(p);
+    for (void* p : sys->arena_chunks) cudaFree(p);
     delete sys;
 }
 

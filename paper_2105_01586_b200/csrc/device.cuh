@@ -149,7 +149,10 @@ struct femi_system_s {
     void* scratch = nullptr;
     void* scratch_m[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // multi-RHS graph caches (NR = 2..4)
     size_t scratch_bytes = 0;
-    std::vector<void*> allocs;
+    std::vector<void*> allocs;        // cudaMalloc'd large arrays
+    std::vector<void*> arena_chunks;  // cudaMalloc'd arena chunks (small arrays carved from them)
+    char* arena_cur = nullptr;  // next free byte of the current arena chunk
+    size_t arena_left = 0;
 };
 
 namespace femi {
