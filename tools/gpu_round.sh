@@ -23,7 +23,7 @@ timeout 900 ncu --graph-profiling graph --profile-from-start off --clock-control
   --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum \
   --csv --log-file gpurun_out/launches_c5.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 NCU="ncu --set full --import-source on --clock-control none"
-timeout 900 $NCU -k regex:"k_gt" -s 1 -c 1 -o gpurun_out/prof_kgt $CMD > gpurun_out/prof_kgt.log 2>&1
+FEMI_PCG_KBENCH=1 timeout 900 $NCU -k regex:"k_gu|k_gt" -s 8 -c 2 -o gpurun_out/prof_body $CMD > gpurun_out/prof_body.log 2>&1
 timeout 900 $NCU -k regex:"k_raster_tri" -s 3 -c 1 -o gpurun_out/prof_raster $CMD > gpurun_out/prof_raster.log 2>&1
-timeout 900 $NCU -k regex:"k_cgr" -s 2 -c 1 -o gpurun_out/prof_cgr python bench.py --config 2 --steps 1 --warmup 1 > gpurun_out/prof_cgr.log 2>&1
+timeout 900 $NCU -k regex:"k_cgr" -s 1 -c 1 -o gpurun_out/prof_cgr python bench.py --config 2 --steps 1 --warmup 1 > gpurun_out/prof_cgr.log 2>&1
 echo done
