@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-tonal", action="store_true", help="C5: skip the 20-iteration tonal tail")
     ap.add_argument("--n", type=int, default=0, help="C3: densification iterations (default: the config's 10)")
     ap.add_argument("--warm", action="store_true", help="C3: warm-start each solve from the previous solution")
+    ap.add_argument("--rebuild-mesh", action="store_true",
+                    help="C3: build every densification mesh from scratch instead of inserting the new pixels")
     ap.add_argument("--shard", action="store_true",
                     help="C2 under torchrun: split the 32 masks across ranks (strong scaling) instead of replicas")
     return ap.parse_args()
@@ -566,9 +568,15 @@ def run_workload(args):
             mask = np.sort(np.asarray(c["mask0"], dtype=np.int64))
             gpu_ms, host_s, its = 0.0, 0.0, []
             x_prev = None
+            M, new = None, None
             for t in range(1, len(sched) + 1):
                 h0 = time.time()
-                M = femi.Mesh(W, H, mask, c["unknowns"])
+                # re-meshing: the previous mesh plus the new mask pixels (femi_mesh_insert,
+                # identical to a rebuild); --rebuild-mesh builds each mesh from scratch
+                if M is None or args.rebuild_mesh:
+                    M = femi.Mesh(W, H, mask, c["unknowns"])
+                else:
+                    M = M.insert(new)
                 S = femi.System(M)
                 g = pipeline.mask_values(f_dev, M.export()["vert_px"], S.n_u)
                 u = torch.empty(S.nv, dtype=torch.float64, device=dev)

@@ -79,6 +79,17 @@ typedef struct {
  * ------------------------------------------------------------------------------- */
 femi_status femi_mesh_build(int32_t W, int32_t H, const int32_t* mask_px, int64_t m,
                             const int32_t* unknown_px, int64_t p, femi_mesh* out);
+/* S0 incremental, for densification (every iteration adds b_t mask
+ * pixels): the mesh of prev's vertices plus the b new MASK pixels.
+ * The new vertices are inserted into prev's triangulation (Bowyer-Watson); the SoS
+ * triangulation of reading A3 is unique, so the result -- triangles, canonical numbering,
+ * tables -- is identical to femi_mesh_build on the union (unknowns keep their indices,
+ * masks are re-ranked). prev is not modified.
+ *   new_mask_px[b]: HOST array of distinct pixels that are not vertices of prev, any order.
+ *   out: receives a new handle (free with femi_mesh_free).
+ * Errors: FEMI_E_ARG (NULL, b < 0), FEMI_E_SIZE (out of range, duplicate, already a vertex),
+ * FEMI_E_OOM. */
+femi_status femi_mesh_insert(femi_mesh prev, const int32_t* new_mask_px, int64_t b, femi_mesh* out);
 femi_status femi_mesh_info_get(femi_mesh mesh, femi_mesh_info* info);
 /* Canonical arrays to HOST buffers (any pointer may be NULL to skip it):
  *   vert_px[n_vert], tri_vert[3*n_tri] (canonical vertex indices),

@@ -159,6 +159,32 @@ femi_status femi_mesh_build(int32_t W, int32_t H, const int32_t* mask_px, int64_
     return FEMI_OK;
 }
 
+femi_status femi_mesh_insert(femi_mesh prev, const int32_t* new_mask_px, int64_t b, femi_mesh* out) {
+    if (!prev || !out) {
+        set_error("mesh_insert: NULL argument");
+        return FEMI_E_ARG;
+    }
+    *out = nullptr;
+    femi_mesh_s* h = new (std::nothrow) femi_mesh_s();
+    if (!h) return FEMI_E_OOM;
+    femi_status s;
+    try {
+        s = insert_mesh(prev->mesh, new_mask_px, b, h->mesh);
+    } catch (const std::bad_alloc&) {
+        set_error("mesh_insert: host allocation failed");
+        s = FEMI_E_OOM;
+    } catch (...) {
+        set_error("mesh_insert: internal error");
+        s = FEMI_E_ARG;
+    }
+    if (s != FEMI_OK) {
+        delete h;
+        return s;
+    }
+    *out = h;
+    return FEMI_OK;
+}
+
 femi_status femi_mesh_info_get(femi_mesh mesh, femi_mesh_info* info) {
     if (!mesh || !info) {
         set_error("mesh_info_get: NULL argument");

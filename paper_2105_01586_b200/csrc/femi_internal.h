@@ -54,6 +54,7 @@ struct Mesh {
 
 femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,
                        int64_t p, Mesh& out);
+femi_status insert_mesh(const Mesh& prev, const int32_t* new_mask_px, int64_t b, Mesh& out);
 
 }  // namespace femi
 

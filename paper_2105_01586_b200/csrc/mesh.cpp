@@ -214,6 +214,15 @@ class BowyerWatson {
 
     const std::vector<Tri>& tris() const { return tris_; }
 
+    // continue from an existing triangulation (CCW triangles, n[k] across the edge opposite
+    // v[k]) of a subset of the points
+    void adopt(std::vector<Tri>&& t) {
+        tris_ = std::move(t);
+        tris_.reserve(tris_.size() + 2 * (P_.size() - tris_.size() / 2) + 8);
+        stamp_.assign(tris_.size(), 0);
+        last_ = 0;
+    }
+
   private:
     struct Edge {
         int32_t u, w, out, old;
@@ -260,6 +269,161 @@ class BowyerWatson {
 };
 
 }  // namespace
+
+// Everything after the triangulation (M.tri canonical; M.vpix, counts set): vertex ->
+// incident corners, neighbours and ownership flags, the CSR patterns of A_uu / A_uk with the
+// opposite-vertex tables, and the transpose of A_uk. Shared by build_mesh and insert_mesh.
+template <class Stamp>
+void mesh_tables(Mesh& M, int nthreads, Stamp&& stamp) {
+    const int64_t nv = M.nv, T = M.T;
+    auto parallel = [nthreads](int64_t n, auto&& fn) {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthreads; ++k)
+            th.emplace_back([&, k] {
+                int64_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
+                for (int64_t i = lo; i < hi; ++i) fn(i);
+            });
+        for (auto& x : th) x.join();
+    };
+    // ---- vertex -> incident corners (ascending triangle index): atomic counting sort,
+    // then each vertex's short list sorted
+    M.vt_ptr.assign(nv + 1, 0);
+    M.vt_idx.resize(3 * T);
+    {
+        int32_t* cnt = M.vt_ptr.data() + 1;
+        parallel(3 * T, [&](int64_t q) { __atomic_fetch_add(&cnt[M.tri[q]], 1, __ATOMIC_RELAXED); });
+        for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
+        std::vector<int32_t> fill(M.vt_ptr.begin(), M.vt_ptr.end() - 1);
+        parallel(3 * T, [&](int64_t q) {
+            M.vt_idx[__atomic_fetch_add(&fill[M.tri[q]], 1, __ATOMIC_RELAXED)] = (int32_t)q;
+        });
+        parallel(nv, [&](int64_t v) { std::sort(M.vt_idx.begin() + M.vt_ptr[v], M.vt_idx.begin() + M.vt_ptr[v + 1]); });
+    }
+    stamp("vt");
+    // ---- neighbours across edges, ownership flags (reading A7)
+    M.nbr.assign(3 * T, -1);
+    M.flags.assign(T, 0);
+    parallel(T, [&](int64_t t) {
+        uint32_t fl = 0;
+        for (int k = 0; k < 3; ++k) {
+            int32_t a = M.tri[3 * t + (k + 1) % 3], b = M.tri[3 * t + (k + 2) % 3];
+            int32_t nb = -1;
+            for (int32_t q = M.vt_ptr[a]; q < M.vt_ptr[a + 1]; ++q) {
+                int32_t s = M.vt_idx[q] / 3;
+                if (s == t) continue;
+                if (M.tri[3 * s] == b || M.tri[3 * s + 1] == b || M.tri[3 * s + 2] == b) {
+                    nb = s;
+                    break;
+                }
+            }
+            M.nbr[3 * t + k] = nb;
+            if (nb < 0 || t < nb) fl |= 1u << k;
+            int32_t vk = M.tri[3 * t + k];
+            if (M.vt_idx[M.vt_ptr[vk]] / 3 == t) fl |= 1u << (3 + k);  // lowest incident triangle
+        }
+        M.flags[t] = fl;
+    });
+
+    stamp("nbr");
+    // ---- CSR patterns of A_uu (with diagonal) and A_uk, with opposite-vertex tables
+    const int64_t n_u = M.n_u;
+    std::vector<int32_t> cnt_uu(n_u, 0), cnt_uk(n_u, 0);
+    auto row_entries = [&](int64_t i, std::vector<std::pair<int32_t, int32_t>>& e) {
+        e.clear();
+        for (int32_t q = M.vt_ptr[i]; q < M.vt_ptr[i + 1]; ++q) {
+            int32_t t = M.vt_idx[q] / 3, k = M.vt_idx[q] % 3;
+            int32_t j1 = M.tri[3 * t + (k + 1) % 3], j2 = M.tri[3 * t + (k + 2) % 3];
+            e.push_back({j1, j2});  // edge (i,j1) has opposite vertex j2 in t
+            e.push_back({j2, j1});
+        }
+        std::sort(e.begin(), e.end());
+    };
+    parallel(nthreads, [&](int64_t k) {
+        std::vector<std::pair<int32_t, int32_t>> e;
+        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
+        for (int64_t i = lo; i < hi; ++i) {
+            row_entries(i, e);
+            int32_t cu = 1, ck = 0;  // diagonal
+            for (size_t q = 0; q < e.size(); ++q) {
+                if (q > 0 && e[q].first == e[q - 1].first) continue;
+                if (e[q].first < n_u) ++cu;
+                else ++ck;
+            }
+            cnt_uu[i] = cu;
+            cnt_uk[i] = ck;
+        }
+    });
+    M.uu_rowptr.assign(n_u + 1, 0);
+    M.uk_rowptr.assign(n_u + 1, 0);
+    for (int64_t i = 0; i < n_u; ++i) {
+        M.uu_rowptr[i + 1] = M.uu_rowptr[i] + cnt_uu[i];
+        M.uk_rowptr[i + 1] = M.uk_rowptr[i] + cnt_uk[i];
+    }
+    const int64_t nuu = M.uu_rowptr[n_u], nuk = M.uk_rowptr[n_u];
+    M.uu_col.resize(nuu);
+    M.uu_opp.resize(2 * nuu);
+    M.uk_col.resize(nuk);
+    M.uk_opp.resize(2 * nuk);
+    parallel(nthreads, [&](int64_t k) {
+        std::vector<std::pair<int32_t, int32_t>> e;
+        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
+        for (int64_t i = lo; i < hi; ++i) {
+            row_entries(i, e);
+            int32_t pu = M.uu_rowptr[i], pk = M.uk_rowptr[i];
+            bool diag_done = false;
+            for (size_t q = 0; q < e.size();) {
+                int32_t j = e[q].first, o1 = e[q].second, o2 = -1;
+                size_t r = q + 1;
+                if (r < e.size() && e[r].first == j) {
+                    o2 = e[r].second;
+                    ++r;
+                }
+                q = r;
+                if (j < n_u) {
+                    if (!diag_done && j > i) {
+                        M.uu_col[pu] = (int32_t)i;
+                        M.uu_opp[2 * pu] = -1;
+                        M.uu_opp[2 * pu + 1] = -1;
+                        ++pu;
+                        diag_done = true;
+                    }
+                    M.uu_col[pu] = j;
+                    M.uu_opp[2 * pu] = o1;
+                    M.uu_opp[2 * pu + 1] = o2;
+                    ++pu;
+                } else {
+                    M.uk_col[pk] = (int32_t)(j - n_u);
+                    M.uk_opp[2 * pk] = o1;
+                    M.uk_opp[2 * pk + 1] = o2;
+                    ++pk;
+                }
+            }
+            if (!diag_done) {
+                M.uu_col[pu] = (int32_t)i;
+                M.uu_opp[2 * pu] = -1;
+                M.uu_opp[2 * pu + 1] = -1;
+            }
+        }
+    });
+
+    stamp("csr");
+    // ---- transpose of A_uk (rows = masks), for B^T in tonal optimisation
+    M.ku_rowptr.assign(M.m + 1, 0);
+    for (int64_t q = 0; q < nuk; ++q) M.ku_rowptr[M.uk_col[q] + 1]++;
+    for (int64_t k = 0; k < M.m; ++k) M.ku_rowptr[k + 1] += M.ku_rowptr[k];
+    M.ku_src.resize(nuk);
+    M.ku_row.resize(nuk);
+    {
+        std::vector<int32_t> fill(M.ku_rowptr.begin(), M.ku_rowptr.end() - 1);
+        for (int64_t i = 0; i < n_u; ++i)
+            for (int32_t q = M.uk_rowptr[i]; q < M.uk_rowptr[i + 1]; ++q) {
+                int32_t d = fill[M.uk_col[q]]++;
+                M.ku_src[d] = q;
+                M.ku_row[d] = (int32_t)i;
+            }
+    }
+    stamp("transpose");
+}
 
 femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, const int32_t* unknown_px,
                        int64_t p, Mesh& M) {
@@ -548,144 +712,130 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     }
     stamp("canonical");
 
-    // ---- vertex -> incident corners (ascending triangle index): atomic counting sort,
-    // then each vertex's short list sorted
-    M.vt_ptr.assign(nv + 1, 0);
-    M.vt_idx.resize(3 * T);
-    {
-        int32_t* cnt = M.vt_ptr.data() + 1;
-        parallel(3 * T, [&](int64_t q) { __atomic_fetch_add(&cnt[M.tri[q]], 1, __ATOMIC_RELAXED); });
-        for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
-        std::vector<int32_t> fill(M.vt_ptr.begin(), M.vt_ptr.end() - 1);
-        parallel(3 * T, [&](int64_t q) {
-            M.vt_idx[__atomic_fetch_add(&fill[M.tri[q]], 1, __ATOMIC_RELAXED)] = (int32_t)q;
-        });
-        parallel(nv, [&](int64_t v) { std::sort(M.vt_idx.begin() + M.vt_ptr[v], M.vt_idx.begin() + M.vt_ptr[v + 1]); });
-    }
-    stamp("vt");
-    // ---- neighbours across edges, ownership flags (reading A7)
-    M.nbr.assign(3 * T, -1);
-    M.flags.assign(T, 0);
-    parallel(T, [&](int64_t t) {
-        uint32_t fl = 0;
-        for (int k = 0; k < 3; ++k) {
-            int32_t a = M.tri[3 * t + (k + 1) % 3], b = M.tri[3 * t + (k + 2) % 3];
-            int32_t nb = -1;
-            for (int32_t q = M.vt_ptr[a]; q < M.vt_ptr[a + 1]; ++q) {
-                int32_t s = M.vt_idx[q] / 3;
-                if (s == t) continue;
-                if (M.tri[3 * s] == b || M.tri[3 * s + 1] == b || M.tri[3 * s + 2] == b) {
-                    nb = s;
-                    break;
-                }
-            }
-            M.nbr[3 * t + k] = nb;
-            if (nb < 0 || t < nb) fl |= 1u << k;
-            int32_t vk = M.tri[3 * t + k];
-            if (M.vt_idx[M.vt_ptr[vk]] / 3 == t) fl |= 1u << (3 + k);  // lowest incident triangle
-        }
-        M.flags[t] = fl;
-    });
+    mesh_tables(M, nthreads, stamp);
+    M.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return FEMI_OK;
+}
 
-    stamp("nbr");
-    // ---- CSR patterns of A_uu (with diagonal) and A_uk, with opposite-vertex tables
-    const int64_t n_u = M.n_u;
-    std::vector<int32_t> cnt_uu(n_u, 0), cnt_uk(n_u, 0);
-    auto row_entries = [&](int64_t i, std::vector<std::pair<int32_t, int32_t>>& e) {
-        e.clear();
-        for (int32_t q = M.vt_ptr[i]; q < M.vt_ptr[i + 1]; ++q) {
-            int32_t t = M.vt_idx[q] / 3, k = M.vt_idx[q] % 3;
-            int32_t j1 = M.tri[3 * t + (k + 1) % 3], j2 = M.tri[3 * t + (k + 2) % 3];
-            e.push_back({j1, j2});  // edge (i,j1) has opposite vertex j2 in t
-            e.push_back({j2, j1});
-        }
-        std::sort(e.begin(), e.end());
+// S0 incremental (densification): prev's vertices plus b new MASK
+// pixels. The new points are inserted into prev's triangulation by the same Bowyer-Watson
+// (Hilbert order); by reading A3 the result is the unique triangulation of the union, i.e.
+// exactly what build_mesh gives for the union -- only the canonical numbering (unknowns keep
+// their indices, masks are re-ranked) and the tables are rebuilt.
+femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M) {
+    auto t_start = std::chrono::steady_clock::now();
+    const bool prof = std::getenv("FEMI_MESH_PROF") != nullptr;
+    auto stamp = [&](const char* what) {
+        if (prof)
+            std::fprintf(stderr, "mesh_insert %-12s %.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
     };
-    parallel(nthreads, [&](int64_t k) {
-        std::vector<std::pair<int32_t, int32_t>> e;
-        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
-        for (int64_t i = lo; i < hi; ++i) {
-            row_entries(i, e);
-            int32_t cu = 1, ck = 0;  // diagonal
-            for (size_t q = 0; q < e.size(); ++q) {
-                if (q > 0 && e[q].first == e[q - 1].first) continue;
-                if (e[q].first < n_u) ++cu;
-                else ++ck;
-            }
-            cnt_uu[i] = cu;
-            cnt_uk[i] = ck;
-        }
-    });
-    M.uu_rowptr.assign(n_u + 1, 0);
-    M.uk_rowptr.assign(n_u + 1, 0);
-    for (int64_t i = 0; i < n_u; ++i) {
-        M.uu_rowptr[i + 1] = M.uu_rowptr[i] + cnt_uu[i];
-        M.uk_rowptr[i + 1] = M.uk_rowptr[i] + cnt_uk[i];
+    if (b < 0 || (b > 0 && !px)) {
+        set_error("mesh_insert: NULL array or negative count");
+        return FEMI_E_ARG;
     }
-    const int64_t nuu = M.uu_rowptr[n_u], nuk = M.uk_rowptr[n_u];
-    M.uu_col.resize(nuu);
-    M.uu_opp.resize(2 * nuu);
-    M.uk_col.resize(nuk);
-    M.uk_opp.resize(2 * nuk);
-    parallel(nthreads, [&](int64_t k) {
-        std::vector<std::pair<int32_t, int32_t>> e;
-        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
-        for (int64_t i = lo; i < hi; ++i) {
-            row_entries(i, e);
-            int32_t pu = M.uu_rowptr[i], pk = M.uk_rowptr[i];
-            bool diag_done = false;
-            for (size_t q = 0; q < e.size();) {
-                int32_t j = e[q].first, o1 = e[q].second, o2 = -1;
-                size_t r = q + 1;
-                if (r < e.size() && e[r].first == j) {
-                    o2 = e[r].second;
-                    ++r;
-                }
-                q = r;
-                if (j < n_u) {
-                    if (!diag_done && j > i) {
-                        M.uu_col[pu] = (int32_t)i;
-                        M.uu_opp[2 * pu] = -1;
-                        M.uu_opp[2 * pu + 1] = -1;
-                        ++pu;
-                        diag_done = true;
-                    }
-                    M.uu_col[pu] = j;
-                    M.uu_opp[2 * pu] = o1;
-                    M.uu_opp[2 * pu + 1] = o2;
-                    ++pu;
-                } else {
-                    M.uk_col[pk] = (int32_t)(j - n_u);
-                    M.uk_opp[2 * pk] = o1;
-                    M.uk_opp[2 * pk + 1] = o2;
-                    ++pk;
-                }
-            }
-            if (!diag_done) {
-                M.uu_col[pu] = (int32_t)i;
-                M.uu_opp[2 * pu] = -1;
-                M.uu_opp[2 * pu + 1] = -1;
-            }
+    const int32_t W = prev.W, H = prev.H;
+    const int64_t N = (int64_t)W * H, n_u = prev.n_u, m_old = prev.m;
+    std::vector<int32_t> add(px, px + b);
+    std::sort(add.begin(), add.end());
+    for (int64_t i = 0; i < b; ++i) {
+        const int32_t q = add[i];
+        const bool vert = std::binary_search(prev.vpix.begin(), prev.vpix.begin() + n_u, q) ||
+                          std::binary_search(prev.vpix.begin() + n_u, prev.vpix.end(), q);
+        if (q < 0 || q >= N || (i > 0 && add[i - 1] == q) || vert) {
+            set_error("mesh_insert: pixel out of range, duplicated, or already a vertex");
+            return FEMI_E_SIZE;
         }
-    });
-
-    stamp("csr");
-    // ---- transpose of A_uk (rows = masks), for B^T in tonal optimisation
-    M.ku_rowptr.assign(M.m + 1, 0);
-    for (int64_t q = 0; q < nuk; ++q) M.ku_rowptr[M.uk_col[q] + 1]++;
-    for (int64_t k = 0; k < M.m; ++k) M.ku_rowptr[k + 1] += M.ku_rowptr[k];
-    M.ku_src.resize(nuk);
-    M.ku_row.resize(nuk);
+    }
+    const int nthreads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    M.W = W;
+    M.H = H;
+    M.threads = nthreads;
+    M.n_u = n_u;
+    M.m = m_old + b;
+    M.nv = n_u + M.m;
+    const int64_t nv = M.nv;
+    // masks re-ranked: merge of prev's (ascending) and the new pixels (ascending)
+    M.vpix.resize(nv);
+    std::copy(prev.vpix.begin(), prev.vpix.begin() + n_u, M.vpix.begin());
+    std::vector<int32_t> old_to_new(m_old), ins_id(b);
     {
-        std::vector<int32_t> fill(M.ku_rowptr.begin(), M.ku_rowptr.end() - 1);
-        for (int64_t i = 0; i < n_u; ++i)
-            for (int32_t q = M.uk_rowptr[i]; q < M.uk_rowptr[i + 1]; ++q) {
-                int32_t d = fill[M.uk_col[q]]++;
-                M.ku_src[d] = q;
-                M.ku_row[d] = (int32_t)i;
+        int64_t i = 0, j = 0, o = 0;
+        while (i < m_old || j < b) {
+            if (j >= b || (i < m_old && prev.vpix[n_u + i] < add[j])) {
+                old_to_new[i] = (int32_t)(n_u + o);
+                M.vpix[n_u + o++] = prev.vpix[n_u + i++];
+            } else {
+                ins_id[j] = (int32_t)(n_u + o);
+                M.vpix[n_u + o++] = add[j++];
             }
+        }
     }
-    stamp("transpose");
+    std::vector<Pt> P(nv);
+    for (int64_t v = 0; v < nv; ++v) P[v] = {M.vpix[v] % W, M.vpix[v] / W, M.vpix[v]};
+    stamp("renumber");
+    // prev's triangles with the new vertex ids, then the new points
+    std::vector<Tri> tr(prev.T);
+    for (int64_t t = 0; t < prev.T; ++t)
+        for (int k = 0; k < 3; ++k) {
+            const int32_t v = prev.tri[3 * t + k];
+            tr[t].v[k] = v < n_u ? v : old_to_new[v - n_u];
+            tr[t].n[k] = prev.nbr[3 * t + k];
+        }
+    BowyerWatson bw(P);
+    bw.adopt(std::move(tr));
+    {
+        std::vector<std::pair<uint64_t, int32_t>> order(b);
+        for (int64_t j = 0; j < b; ++j)
+            order[j] = {hilbert_key((uint32_t)P[ins_id[j]].x, (uint32_t)P[ins_id[j]].y), ins_id[j]};
+        std::sort(order.begin(), order.end());
+        for (auto& kv : order) bw.insert(kv.second);
+    }
+    stamp("insert");
+    // canonical triangles: rotate (smallest pix first), order by (pix a, pix b, pix c) --
+    // bucketed by the row of a, each row sorted
+    const auto& TR = bw.tris();
+    const int64_t T = (int64_t)TR.size();
+    struct Key {
+        int32_t a, b, c;
+    };
+    std::vector<Key> keys(T);
+    std::vector<int64_t> rp(H + 1, 0);
+    const int32_t* vp = M.vpix.data();
+    for (int64_t t = 0; t < T; ++t) {
+        const int32_t* v = TR[t].v;
+        int k = 0;
+        if (vp[v[1]] < vp[v[k]]) k = 1;
+        if (vp[v[2]] < vp[v[k]]) k = 2;
+        keys[t] = {v[k], v[(k + 1) % 3], v[(k + 2) % 3]};
+        rp[vp[v[k]] / W + 1]++;
+    }
+    for (int32_t y = 0; y < H; ++y) rp[y + 1] += rp[y];
+    std::vector<Key> sorted(T);
+    {
+        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+        for (int64_t t = 0; t < T; ++t) sorted[fill[vp[keys[t].a] / W]++] = keys[t];
+    }
+    std::vector<Key>().swap(keys);
+    parallel_ranges(H, [&](int64_t lo, int64_t hi) {
+        for (int64_t y = lo; y < hi; ++y)
+            std::sort(sorted.begin() + rp[y], sorted.begin() + rp[y + 1], [vp](const Key& x, const Key& z) {
+                if (vp[x.a] != vp[z.a]) return vp[x.a] < vp[z.a];
+                if (vp[x.b] != vp[z.b]) return vp[x.b] < vp[z.b];
+                return vp[x.c] < vp[z.c];
+            });
+    }, 64);
+    M.T = T;
+    M.tri.resize(3 * T);
+    for (int64_t t = 0; t < T; ++t) {
+        M.tri[3 * t] = sorted[t].a;
+        M.tri[3 * t + 1] = sorted[t].b;
+        M.tri[3 * t + 2] = sorted[t].c;
+    }
+    stamp("canonical");
+    mesh_tables(M, nthreads, stamp);
+    M.strips = 0;
+    M.strip_retries = 0;
     M.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     return FEMI_OK;
 }

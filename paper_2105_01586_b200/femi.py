@@ -71,7 +71,7 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_mesh_timing", "femi_mesh_free", "femi_assemble", "femi_system_info_get", "femi_system_export",
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
-           "femi_densify_step_channels", "femi_tonal_optimise_l1"]
+           "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert"]
 
 
 def lib():
@@ -90,6 +90,7 @@ def lib():
         L.femi_mesh_export.argtypes = [P, P, P, P, P, P, P]
         L.femi_mesh_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double), I32P]
         L.femi_mesh_free.argtypes = [P]
+        L.femi_mesh_insert.argtypes = [P, P, ctypes.c_int64, ctypes.POINTER(P)]
         L.femi_mesh_free.restype = None
         L.femi_assemble.argtypes = [P, P, ctypes.POINTER(P)]
         L.femi_system_info_get.argtypes = [P, ctypes.POINTER(MeshInfo)]
@@ -175,6 +176,27 @@ class Mesh:
         sec, thr = ctypes.c_double(), ctypes.c_int32()
         _check(lib().femi_mesh_timing(h, ctypes.byref(sec), ctypes.byref(thr)))
         self.build_seconds, self.build_threads = sec.value, thr.value
+
+    def insert(self, new_mask_px) -> "Mesh":
+        """S0 incremental: a new Mesh with the given pixels added as mask vertices (identical
+        to building the union from scratch; this mesh is unchanged)."""
+        add = np.ascontiguousarray(np.asarray(new_mask_px).reshape(-1), dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(self._lib.femi_mesh_insert(self._h, _hptr(add), add.size, ctypes.byref(h)))
+        return Mesh._from_handle(h, self._lib)
+
+    @classmethod
+    def _from_handle(cls, h, L):
+        M = cls.__new__(cls)
+        M._lib = L
+        M._h = h
+        info = MeshInfo()
+        _check(L.femi_mesh_info_get(h, ctypes.byref(info)))
+        M.info = info.as_dict()
+        sec, thr = ctypes.c_double(), ctypes.c_int32()
+        _check(L.femi_mesh_timing(h, ctypes.byref(sec), ctypes.byref(thr)))
+        M.build_seconds, M.build_threads = sec.value, thr.value
+        return M
 
     def export(self) -> dict:
         i = self.info

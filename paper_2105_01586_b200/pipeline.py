@@ -29,11 +29,14 @@ def mask_values(f_dev, mesh_or_sys_vert_px, n_u):
     return f_dev.reshape(-1).index_select(0, idx).contiguous()
 
 
-def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None, x0_unknown=None):
+def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None, x0_unknown=None,
+            mesh=None):
     """x0_unknown: optional initial guess at the unknown vertices (canonical order, e.g. the
-    previous densification iteration's solution: the unknown set is fixed, reading A4)."""
+    previous densification iteration's solution: the unknown set is fixed, reading A4).
+    mesh: a prebuilt femi.Mesh of exactly these vertices (e.g. from Mesh.insert)."""
     torch = _torch()
-    mesh = femi.Mesh(W, H, mask_px, unknown_px)
+    if mesh is None:
+        mesh = femi.Mesh(W, H, mask_px, unknown_px)
     sysm = femi.System(mesh, stream)
     vert = mesh.export()["vert_px"]
     g = mask_values(f_dev, vert, sysm.n_u)
@@ -56,27 +59,37 @@ def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stre
 
 
 def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks=None, stream=None,
-            warm_start=False):
+            warm_start=False, incremental_mesh=True):
     """Returns (final mask, per-iteration records, final MSE). warm_start: each solve starts
     from the previous iteration's solution at the (fixed, reading A4) unknown vertices
-    (changes iterates, not the solution)."""
+    (changes iterates, not the solution). incremental_mesh: each mesh is
+    the previous one plus the new mask pixels (Mesh.insert, identical to a rebuild)."""
     _torch()
     mask = np.sort(np.asarray(mask0, dtype=np.int64))
     recs = []
     f1 = f_dev.reshape(-1)
     x_prev = None
+    mesh, new = None, None
     for t in range(1, len(schedule)):
         if lockstep_masks is not None:
             mask = np.sort(np.asarray(lockstep_masks[t - 1], dtype=np.int64))
+            mesh = None
+        elif incremental_mesh and mesh is not None:
+            mesh = mesh.insert(new)
         R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
-                    x0_unknown=x_prev if warm_start else None)
+                    x0_unknown=x_prev if warm_start else None, mesh=mesh)
+        mesh = R["mesh"] if incremental_mesh else None
         x_prev = R["u_vert"][: R["system"].n_u].clone()
         new = femi.densify_step(R["system"], f1, R["u_vert"], int(schedule[t]), stream)
         recs.append(dict(mask=mask.copy(), mse=float(R["sse"].item()) / (W * H), iters=R["iters"], new=new,
                          T=R["system"].T, mesh_seconds=R["mesh"].build_seconds))
         mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
+    if incremental_mesh and mesh is not None and lockstep_masks is None:
+        mesh = mesh.insert(new)
+    else:
+        mesh = None
     R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
-                x0_unknown=x_prev if warm_start else None)
+                x0_unknown=x_prev if warm_start else None, mesh=mesh)
     return mask, recs, float(R["sse"].item()) / (W * H)
 
 

@@ -136,3 +136,67 @@ def test_mesh_strips_sparse_and_clustered(monkeypatch):
     mk = pts[: len(pts) // 2]
     un = np.concatenate([pts[len(pts) // 2:], [120 * W + 150, 200 * W + 299, 239 * W + 10]])
     assert_same(W, H, mk, un)
+
+
+def _same_export(A, B):
+    EA, EB = A.export(), B.export()
+    for k in ("vert_px", "tri", "uu_rowptr", "uu_col", "uk_rowptr", "uk_col"):
+        np.testing.assert_array_equal(EA[k], EB[k], err_msg=k)
+    assert A.info == B.info
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_mesh_insert_equals_rebuild(seed):
+    """S0 incremental (femi_mesh_insert): inserting new mask pixels into a mesh gives exactly
+    the mesh built from scratch on the union (reading A3: the SoS triangulation is unique)."""
+    rng = np.random.default_rng(500 + seed)
+    W, H = int(rng.integers(8, 90)), int(rng.integers(8, 90))
+    N = W * H
+    mk = draw_mask(rng, N, int(rng.integers(1, max(2, N // 10))))
+    un = draw_unknowns(rng, W, H, mk, int(rng.integers(4, max(5, N // 8))))
+    prev = femi.Mesh(W, H, mk, un)
+    free = np.setdiff1d(np.arange(N), np.concatenate([mk, prev.export()["vert_px"]]))
+    add = rng.choice(free, size=min(free.size, int(rng.integers(1, max(2, N // 12)))), replace=False)
+    new = prev.insert(rng.permutation(add))
+    ref = femi.Mesh(W, H, np.concatenate([mk, add]), un)
+    _same_export(new, ref)
+    # prev is unchanged
+    _same_export(prev, femi.Mesh(W, H, mk, un))
+
+
+def test_mesh_insert_densification_sequence():
+    """A C3-like schedule: nine insertions of ~1% of the pixels, each equal to a rebuild."""
+    c = make_config(3)
+    W, H = c["W"], c["H"]
+    rng = np.random.default_rng(33)
+    mask = np.sort(c["mask0"])
+    M = femi.Mesh(W, H, mask, c["unknowns"])
+    verts = set(M.export()["vert_px"].tolist())
+    for t in range(9):
+        cand = np.array([q for q in rng.choice(W * H, 2000, replace=False) if q not in verts][:1300])
+        M = M.insert(cand)
+        mask = np.sort(np.concatenate([mask, cand]))
+        verts.update(cand.tolist())
+        if t in (0, 4, 8):
+            _same_export(M, femi.Mesh(W, H, mask, c["unknowns"]))
+
+
+def test_mesh_insert_cocircular_lattice():
+    """Maximal cocircular degeneracy: a lattice of unknowns, lattice points inserted as masks."""
+    W, H = 33, 29
+    lat = np.array([y * W + x for y in range(0, H, 4) for x in range(0, W, 4)])
+    mk = lat[::3]
+    un = np.setdiff1d(lat, mk)
+    prev = femi.Mesh(W, H, mk, un)
+    add = np.array([y * W + x for y in range(2, H, 4) for x in range(2, W, 4)])
+    _same_export(prev.insert(add), femi.Mesh(W, H, np.concatenate([mk, add]), un))
+
+
+def test_mesh_insert_errors():
+    W, H = 20, 20
+    M = femi.Mesh(W, H, [21, 55, 300], [5, 77])
+    for bad in ([21], [5], [0], [400], [-1], [100, 100]):
+        with pytest.raises(femi.FemiError) as ei:
+            M.insert(np.array(bad, np.int32))
+        assert ei.value.status == 7
+    _same_export(M.insert(np.array([], np.int32)), M)
