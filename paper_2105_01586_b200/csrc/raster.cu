@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ t
                                                     const double* __restrict__ r, double* __restrict__ tri_w) {
     __shared__ double acc_s[RWARPS][32][3];
     __shared__ WTri tris[RWARPS][32];
+    __shared__ double rd_s[RWARPS][32];  // RN(1/D): w / D as a correctly rounded 3-op quotient
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ngroups = (T + 31) / 32;
     const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ t
             I.cy = R.y[2];
             I.D = orient_xy(I.ax, I.ay, I.bx, I.by, I.cx, I.cy);
             ws[lane] = I;
+            rd_s[wid][lane] = __drcp_rn((double)I.D);
         }
         acc_s[wid][lane][0] = 0.0;
         acc_s[wid][lane][1] = 0.0;
@@ -447,10 +449,11 @@ __global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ t
                     else sc = rv;
                 } else {
                     const WTri& I = ws[j];
-                    const double D = (double)I.D;
-                    sa = (orient_xy(I.bx, I.by, I.cx, I.cy, px, py) / D) * rv;
-                    sb = (orient_xy(I.cx, I.cy, I.ax, I.ay, px, py) / D) * rv;
-                    sc = (orient_xy(I.ax, I.ay, I.bx, I.by, px, py) / D) * rv;
+                    const double D = (double)I.D, rD = rd_s[wid][j];
+                    // div_rn == the IEEE quotient (Markstein), so the sums are unchanged
+                    sa = div_rn((double)orient_xy(I.bx, I.by, I.cx, I.cy, px, py), D, rD) * rv;
+                    sb = div_rn((double)orient_xy(I.cx, I.cy, I.ax, I.ay, px, py), D, rD) * rv;
+                    sc = div_rn((double)orient_xy(I.ax, I.ay, I.bx, I.by, px, py), D, rD) * rv;
                 }
             }
 #pragma unroll

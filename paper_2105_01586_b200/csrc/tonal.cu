@@ -59,7 +59,13 @@ __global__ void k_dot_final(int nb, const double* __restrict__ part, double* __r
     if (threadIdx.x == 0) *out = s;
 }
 
-__global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+// y += sign (num / den) x with the quotient formed on the device (no host round trip); a
+// non-positive den leaves y unchanged (the host sees it at its next synchronisation and stops)
+__global__ void k_axpy_q(int64_t n, const double* __restrict__ num, const double* __restrict__ den, double sign,
+                         const double* __restrict__ x, double* __restrict__ y) {
+    const double d = *den;
+    if (!(d > 0.0)) return;
+    const double alpha = sign * (*num / d);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = fma(alpha, x[i], y[i]);
 }
@@ -119,7 +125,10 @@ struct Tonal {
         return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     }
 
-    femi_status dot(int64_t n, const double* a, const double* b, double* out) {
+    // a.b into the device scalar `slot` (default dres); with `out` also to the host (one
+    // synchronisation, which also brings back `also` -> `also_host` when given)
+    femi_status dot(int64_t n, const double* a, const double* b, double* out, double* slot = nullptr,
+                    const double* also = nullptr, double* also_host = nullptr) {
         const double t0 = now();
         struct Acc {
             double& t;
@@ -127,10 +136,13 @@ struct Tonal {
             ~Acc() { t += now() - t0; }
         } acc{t_dot, t0};
         const int nb = 296;
+        double* dst = slot ? slot : dres;
         k_dot_part<<<nb, TT, 0, st>>>(n, a, b, part); count_launches(1);
-        k_dot_final<<<1, TT, 0, st>>>(nb, part, dres); count_launches(1);
+        k_dot_final<<<1, TT, 0, st>>>(nb, part, dst); count_launches(1);
         FEMI_CUDA(cudaGetLastError());
-        FEMI_CUDA(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (!out) return FEMI_OK;
+        FEMI_CUDA(cudaMemcpyAsync(out, dst, sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (also) FEMI_CUDA(cudaMemcpyAsync(also_host, also, sizeof(double), cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
         return FEMI_OK;
     }
@@ -196,7 +208,7 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t bytes = 3 * al(sizeof(double) * nv) + al(sizeof(double) * 3 * T) + al(sizeof(double) * 300) +
-                   al(sizeof(double)) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m);
+                   al(sizeof(double) * 4) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m);
     void* base = nullptr;
     FEMI_CUDA(cudaMallocAsync(&base, bytes, st));
     char* cur = (char*)base;
@@ -214,7 +226,7 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     tn.w = take(sizeof(double) * nv);
     tn.tri_w = take(sizeof(double) * 3 * T);
     tn.part = take(sizeof(double) * 300);
-    tn.dres = take(sizeof(double));
+    tn.dres = take(sizeof(double) * 4);  // [0] scratch, [1] gam, [2] q.q
     double* u = take(sizeof(double) * N);
     double* r = take(sizeof(double) * N);
     double* q = take(sizeof(double) * N);
@@ -252,7 +264,9 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
             TRY(tn.apply_BT(r, s));
         }
         FEMI_CUDA(cudaMemcpyAsync(p, s, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-        TRY(tn.dot(m, s, s, &gam));
+        double* gam_d = tn.dres + 1;  // gam on the device: alpha = gam / q.q is formed there
+        double* qq_d = tn.dres + 2;
+        TRY(tn.dot(m, s, s, &gam, gam_d));
         double relg = btf > 0.0 ? std::sqrt(gam) / btf : 0.0;
         while (relg >= o.outer_rtol && outer < o.outer_max) {
             TRY(tn.apply_B(p, q));
@@ -260,11 +274,9 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
                 k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, q, q);
                 count_launches(1);
             }
-            TRY(tn.dot(N, q, q, &qq));
-            if (!(qq > 0.0)) break;
-            const double alpha = gam / qq;
-            k_axpy<<<grid_for(m), TT, 0, st>>>(m, alpha, p, g); count_launches(1);
-            k_axpy<<<grid_for(N), TT, 0, st>>>(N, -alpha, q, r); count_launches(1);
+            TRY(tn.dot(N, q, q, nullptr, qq_d));  // no host round trip: alpha stays on the device
+            k_axpy_q<<<grid_for(m), TT, 0, st>>>(m, gam_d, qq_d, 1.0, p, g); count_launches(1);
+            k_axpy_q<<<grid_for(N), TT, 0, st>>>(N, gam_d, qq_d, -1.0, q, r); count_launches(1);
             if (sw) {
                 k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, r, u);
                 count_launches(1);
@@ -272,7 +284,8 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
             } else {
                 TRY(tn.apply_BT(r, s));
             }
-            TRY(tn.dot(m, s, s, &gam2));
+            TRY(tn.dot(m, s, s, &gam2, gam_d, qq_d, &qq));  // gam_d <- s.s for the next alpha
+            if (!(qq > 0.0)) break;  // g and r were left unchanged (k_axpy_q)
             ++outer;
             relg = std::sqrt(gam2) / btf;
             if (!std::isfinite(relg)) {
