@@ -424,3 +424,18 @@ def test_densify_warm_start():
     Rw = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"], x0_unknown=Rp["u_vert"][: Rp["system"].n_u])
     assert Rw["iters"] < R0["iters"]
     assert torch.abs(R0["u_vert"] - Rw["u_vert"]).max().item() <= 1e-4
+
+
+def test_densify_incremental_mesh_identical():
+    """NEXT-3: densification with incremental re-meshing (Mesh.insert) and with a full rebuild
+    every iteration give the same masks, iteration counts and MSEs bit for bit (the meshes
+    are identical, so every later stage is too)."""
+    c = make_config(3, W=256, H=256, seed=37)
+    fd = dev(c["f"])
+    mi, ri, ei = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"], incremental_mesh=True)
+    mr, rr, er = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"], incremental_mesh=False)
+    np.testing.assert_array_equal(mi, mr)
+    assert ei == er
+    for a, b in zip(ri, rr):
+        np.testing.assert_array_equal(a["new"], b["new"])
+        assert a["iters"] == b["iters"] and a["mse"] == b["mse"] and a["T"] == b["T"]
