@@ -1814,7 +1814,11 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         // kUnroll iterations per body: the WHILE re-evaluation costs several us; kernels after
         // convergence return at once (S->active == 0)
         cudaGraphNode_t bprev = nullptr, u, sn;
-        const dim3 gu(std::min(C.gx * 2, 1184));
+        // 4 CTAs per SM: measured best at C5 (1184: 3.94 ms, 888: 3.92, 740: 3.97, 592: 3.88,
+        // 444: 4.04 per solve) -- with PDL the next k_gt CTA shares the SM with k_gu's CTAs
+        int gu_ctas = std::min(C.gx * 2, 4 * 148);
+        if (const char* e = std::getenv("FEMI_GU_CTAS")) gu_ctas = std::max(1, std::atoi(e));
+        const dim3 gu(gu_ctas);
         // inside the body, k_gu -> k_gt -> k_gu ... are programmatic edges (k_gt streams its
         // first matrix tiles while k_gu runs; each waits in grid_dep_wait for its inputs)
         for (int k = 0; k < kUnroll; ++k) {
