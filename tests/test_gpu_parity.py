@@ -277,8 +277,9 @@ def _c5_like(W, seed):
 
 
 def test_graph_mode_scaled_c5():
-    """The large-system solver (CUDA-graph WHILE loop, fused update+SpMV kernel: used when
-    nnz(A_uu) > 600K) against the oracle element by element, C5 recipe at 2880^2."""
+    """The large-system solver (CUDA-graph WHILE loop of k_gu + the TMA jagged-diagonal SpMV
+    k_gt: used when nnz(A_uu) > 600K) against the oracle element by element, C5 recipe at
+    2880^2."""
     c, mask = _c5_like(2880, 55)
     R, O = check_inpaint(2880, 2880, c["f"], mask, c["unknowns"])
     assert R["system"].info["nnz_uu"] > 600000
@@ -439,3 +440,35 @@ def test_densify_incremental_mesh_identical():
     for a, b in zip(ri, rr):
         np.testing.assert_array_equal(a["new"], b["new"])
         assert a["iters"] == b["iters"] and a["mse"] == b["mse"] and a["T"] == b["T"]
+
+
+_SWITCH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2105_01586_b200 import femi, pipeline
+from synth import make_config
+c = make_config(5, W=2560, H=2560, seed=61)
+f = torch.as_tensor(c["f"], dtype=torch.float64, device="cuda:0")
+R = pipeline.inpaint(2560, 2560, f, c["mask0"], c["unknowns"], rtol=1e-10)
+assert R["system"].info["nnz_uu"] > 600000
+np.save(sys.argv[2], R["u_vert"].cpu().numpy())
+"""
+
+
+def test_graph_mode_switches_bit_identical(tmp_path):
+    """The graph-mode performance paths change timing, not arithmetic: programmatic dependent
+    launch and the in-tile shared-memory gathers on (default) or off give bit-identical
+    solutions (deterministic fixed-order reductions). Separate processes: the switches are
+    read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k, env_add in enumerate(({}, {"FEMI_NO_PDL": "1", "FEMI_SMEM_GATHER": "0"})):
+        out = str(tmp_path / f"u{k}.npy")
+        env = dict(os.environ, **env_add)
+        subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root, out], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    np.testing.assert_array_equal(outs[0], outs[1])
+
