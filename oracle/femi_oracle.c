@@ -519,7 +519,54 @@ static int factor_dense(OrcSys* S) {
     return ORC_OK;
 }
 
-/* method: 0 auto (dense Cholesky when n_u <= 1000, else CG), 1 Cholesky, 2 CG.
+/* Preconditioned CG [Sa03, Alg. 9.1] with the Jacobi preconditioner M = diag(A_uu).
+ * r holds b - A x on entry; p, q are scratch. Stops like the plain CG below: when the
+ * recursive ||r|| <= rtol ||b||, the true residual is recomputed and the iteration restarts
+ * from it if it misses (reading A11). */
+static int pcg_jacobi(const OrcSys* S, const double* b, double* x, double* r, double* p, double* q, double bn,
+                      double rtol, int max_iter, int* iters_out) {
+    i64 n = S->n_u;
+    double* dinv = (double*)malloc(sizeof(double) * (size_t)n);
+    double* z = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!dinv || !z) { free(dinv); free(z); return ORC_E_OOM; }
+    for (i64 i = 0; i < n; ++i) {
+        double d = 0.0;
+        for (i64 e = S->uu_ptr[i]; e < S->uu_ptr[i + 1]; ++e) if (S->uu_col[e] == i) d = S->uu_val[e];
+        dinv[i] = 1.0 / d;
+    }
+    int status = ORC_OK, it = 0;
+    for (i64 i = 0; i < n; ++i) { z[i] = dinv[i] * r[i]; p[i] = z[i]; }
+    double rz = dot(n, r, z);
+    while (it < max_iter) {
+        matvec_uu(S, p, q);
+        double pq = dot(n, p, q);
+        if (!(pq > 0.0)) { status = isfinite(pq) ? ORC_E_NOT_SPD : ORC_E_NONFINITE; break; }
+        double alpha = rz / pq;
+        for (i64 i = 0; i < n; ++i) { x[i] = x[i] + alpha * p[i]; r[i] = r[i] - alpha * q[i]; }
+        ++it;
+        double rr = dot(n, r, r);
+        if (!isfinite(rr)) { status = ORC_E_NONFINITE; break; }
+        if (sqrt(rr) <= rtol * bn) {
+            matvec_uu(S, x, q);
+            for (i64 i = 0; i < n; ++i) r[i] = b[i] - q[i];
+            rr = dot(n, r, r);
+            if (sqrt(rr) <= rtol * bn) break;
+            for (i64 i = 0; i < n; ++i) { z[i] = dinv[i] * r[i]; p[i] = z[i]; }
+            rz = dot(n, r, z);
+            continue;
+        }
+        for (i64 i = 0; i < n; ++i) z[i] = dinv[i] * r[i];
+        double rz2 = dot(n, r, z);
+        double beta = rz2 / rz;
+        for (i64 i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        rz = rz2;
+    }
+    *iters_out = it;
+    free(dinv); free(z);
+    return status;
+}
+
+/* method: 0 auto (dense Cholesky when n_u <= 1000, else CG), 1 Cholesky, 2 CG, 3 Jacobi PCG.
  * Solves A_uu x = b. x holds the initial guess on entry (reading A11). The method stops
  * on the true relative residual ||b - A x|| / ||b|| <= rtol. */
 static int solve_uu(OrcSys* S, const double* b, double* x, double rtol, int max_iter, int method,
@@ -558,6 +605,14 @@ static int solve_uu(OrcSys* S, const double* b, double* x, double rtol, int max_
         matvec_uu(S, x, q);
         for (i64 i = 0; i < n; ++i) r[i] = b[i] - q[i];
         rn = sqrt(dot(n, r, r));
+        goto done;
+    }
+    if (method == 3) { /* Jacobi-preconditioned CG (reading A11: changes iterates, not the solution) */
+        status = pcg_jacobi(S, b, x, r, p, q, bn, rtol, max_iter, iters_out);
+        matvec_uu(S, x, q);
+        for (i64 i = 0; i < n; ++i) r[i] = b[i] - q[i];
+        rn = sqrt(dot(n, r, r));
+        if (status == ORC_OK && !(rn <= rtol * bn)) status = ORC_E_NOT_CONVERGED;
         goto done;
     }
     /* plain conjugate gradients [Sa03], restarted from the true residual if the

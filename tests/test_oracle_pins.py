@@ -374,6 +374,33 @@ def test_p6_cholesky_and_cg_agree():
     assert np.abs(u2[: S.n_u] - x).max() <= 1e-9
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_jacobi_pcg_reaches_the_same_solution(seed):
+    """Reading A11: Jacobi preconditioning changes the iterates, not the solution. The oracle's
+    Jacobi-PCG (method 3) meets the true relative residual and agrees with numpy's dense solve
+    (a library routine, independent of the oracle's C code) and with the dense FDM on the full
+    grid (P5); a constant image still exits at 0 iterations (A16)."""
+    rng = np.random.default_rng(seed)
+    c = make_config(4, W=48, H=40, seed=70 + seed)
+    S = oracle.System(48, 40, c["mask"], c["unknowns"])
+    g = c["f"].reshape(-1)[S.mask_px]
+    u3, st, it, rr = S.solve(g, method=3, rtol=1e-12)
+    assert st == 0 and rr <= 1e-12 and it > 0
+    x = np.linalg.solve(S.dense_uu(), -S.dense_uk() @ g)
+    assert np.abs(u3[: S.n_u] - x).max() <= 1e-8
+    u2, _, it2, _ = S.solve(g, method=2, rtol=1e-12)
+    assert it < it2  # preconditioning pays on these meshes (kappa 477 -> 24 class, SURVEY App. A)
+    W, H = 16, 12
+    f = rng.uniform(0, 255, (H, W))
+    mk = draw_mask(rng, W * H, 12)
+    Sf = oracle.System(W, H, mk, np.setdiff1d(np.arange(W * H), mk))
+    uf, *_ = Sf.solve(f.reshape(-1)[Sf.mask_px], method=3, rtol=1e-13)
+    Rf = Sf.raster(uf, f)
+    assert np.abs(Rf["u_px"] - oracle.fdm_inpaint_dense(f, mk).reshape(-1)).max() <= 1e-9
+    uc, st, itc, _ = S.solve(np.full(S.m, 42.5), method=3)
+    assert itc == 0 and np.all(uc == 42.5)
+
+
 def test_cg_2x2_golden_via_dense():
     """SPEC.md:L218 closed form; confirms the numpy dense path used in these pins."""
     g = GOLD["cg_2x2"]
