@@ -133,9 +133,11 @@ void femi_system_free(femi_system sys);
  *   u_vert[B]: HOST array of DEVICE pointers, u_vert[b] has n_vert values: on return the
  *           unknown entries hold x and the mask entries hold g exactly. With x0 == 2 the
  *           unknown entries are read as the initial guess.
- *   opts: rtol (> 0), max_iter (> 0), precond (0 none, 1 Jacobi), x0 (0 zeros, 1
- *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided),
- *         check_every (iterations between device->host convergence polls; 0 = default).
+ *   opts: rtol (> 0), max_iter (> 0), precond (must be 1: Jacobi, folded into the matrix at
+ *         assembly; plain CG (0) is not offered -- it reaches the same solution in ~6x the
+ *         iterations, reading A11 -- and is rejected with FEMI_E_ARG), x0 (0 zeros, 1
+ *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided), check_every
+ *         (reserved, must be 0: convergence is tested on the device every iteration).
  *   iters[B], relres[B]: HOST outputs (iteration count, final true relative residual).
  * Special cases: ||b|| == 0 -> x = 0, 0 iterations; n_unknown == 0 -> no-op; an initial
  * guess that already satisfies rtol exits with 0 iterations and is returned unchanged.
@@ -153,6 +155,18 @@ typedef struct {
 femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const double* const* g,
                                        double* const* u_vert, const femi_cg_opts* opts,
                                        int32_t* iters, double* relres, femi_stream stream);
+
+/* Which solver the last femi_inpaint_solve_batched (or inner solve) on `sys` ran: a
+ * diagnostic for tests and benchmarks; it does not change results beyond rounding order.
+ *   FEMI_PATH_RESIDENT     whole CG loop on chip (one thread-block cluster per system)
+ *   FEMI_PATH_PERSISTENT   one persistent kernel with global vectors
+ *   FEMI_PATH_GRAPH_SELL   CUDA-graph WHILE loop, sliced-ELL SpMV
+ *   FEMI_PATH_GRAPH_TMA    CUDA-graph WHILE loop, TMA-streamed jagged-diagonal SpMV
+ *   FEMI_PATH_GRAPH_MULTI  shared-matrix multi-right-hand-side graph loop
+ * Errors: FEMI_E_ARG (NULL). */
+enum { FEMI_PATH_NONE = 0, FEMI_PATH_RESIDENT = 1, FEMI_PATH_PERSISTENT = 2, FEMI_PATH_GRAPH_SELL = 3,
+       FEMI_PATH_GRAPH_TMA = 4, FEMI_PATH_GRAPH_MULTI = 5 };
+femi_status femi_system_solver_path(femi_system sys, int32_t* path);
 
 /* ---------------------------------------------------------------------------------
  * S3+S4 rasterise_error (DEVICE). PAPER.md:L239-241 "the solution is linearly
@@ -229,6 +243,24 @@ femi_status femi_densify_step_channels(femi_system sys, int32_t C, const double*
  * Errors: FEMI_E_ARG, FEMI_E_NOT_CONVERGED (g written), FEMI_E_NONFINITE, FEMI_E_CUDA,
  * FEMI_E_OOM.
  * ------------------------------------------------------------------------------- */
+/* ---------------------------------------------------------------------------------
+ * The operator B of the tonal problem and its adjoint (DEVICE; SPEC.md:L339-351 apply /
+ * apply_adjoint). PAPER.md:L281-311, Eq. (4): u = B g is the rasterised inpainting from the
+ * mask values g, B g = P_k g + P_u A_uu^-1 (-A_uk g); its adjoint is
+ * B^T r = P_k^T r - A_uk^T A_uu^-1 (P_u^T r), where P^T r is the adjoint of the raster
+ * (each pixel's r spread onto the vertices of its owner triangle with its barycentric
+ * weights, reading A7). Each call runs one inner solve with `opts` (x0 = midrange for B,
+ * zero for B^T).
+ *   femi_apply_B:  g[n_mask] DEVICE in, u_px[W*H] DEVICE out.
+ *   femi_apply_BT: r[W*H] DEVICE in, s[n_mask] DEVICE out.
+ * Synchronise `stream` (the inner solve reports its status). Errors: FEMI_E_ARG,
+ * FEMI_E_NOT_CONVERGED (output written), FEMI_E_NONFINITE, FEMI_E_CUDA, FEMI_E_OOM.
+ * ------------------------------------------------------------------------------- */
+femi_status femi_apply_B(femi_system sys, const double* g, double* u_px, const femi_cg_opts* opts,
+                         femi_stream stream);
+femi_status femi_apply_BT(femi_system sys, const double* r, double* s, const femi_cg_opts* opts,
+                          femi_stream stream);
+
 typedef struct {
     double outer_rtol;
     int32_t outer_max;

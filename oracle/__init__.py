@@ -158,8 +158,8 @@ class System:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().orc_sys_free(h)
+        if h and _lib is not None:
+            _lib.orc_sys_free(h)
             self._h = None
 
     @property
@@ -304,7 +304,7 @@ def inpaint(W, H, f, mask_px, unknown_px, rtol=1e-12, brute=False):
     return R
 
 
-def densify(W, H, f, mask0, unknowns, schedule, rtol=1e-12, lockstep_masks=None):
+def densify(W, H, f, mask0, unknowns, schedule, rtol=1e-12, lockstep_masks=None, method=0):
     """Error-map densification: iteration 0 = the random mask0; each
     later iteration inpaints on the current mesh and inserts b_t pixels. Returns the final
     mask and per-iteration records. With `lockstep_masks` (list of masks per iteration)
@@ -316,14 +316,14 @@ def densify(W, H, f, mask0, unknowns, schedule, rtol=1e-12, lockstep_masks=None)
         if lockstep_masks is not None:
             mask = np.sort(np.asarray(lockstep_masks[t - 1], np.int64))
         S = System(W, H, mask, unknowns)
-        u, st, it, rr = S.solve(f[S.mask_px], rtol=rtol)
+        u, st, it, rr = S.solve(f[S.mask_px], rtol=rtol, method=method)
         R = S.raster(u, f)
         new = select(R["tri_err"], R["best"], R["e_px"], S.is_vertex(), schedule[t])
         recs.append(dict(mask=mask.copy(), mse=R["mse"], iters=it, new=new, tri_err=R["tri_err"],
                          best=R["best"], T=S.T))
         mask = np.sort(np.concatenate([mask, new.astype(np.int64)]))
     S = System(W, H, mask, unknowns)
-    u, st, it, rr = S.solve(f[S.mask_px], rtol=rtol)
+    u, st, it, rr = S.solve(f[S.mask_px], rtol=rtol, method=method)
     R = S.raster(u, f)
     return mask, recs, R["mse"]
 

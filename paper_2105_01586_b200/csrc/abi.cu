@@ -663,9 +663,9 @@ femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const 
         return FEMI_E_ARG;
     }
     if (B == 0) return FEMI_OK;
-    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond < 0 || opts->precond > 1 || opts->x0 < 0 ||
-        opts->x0 > 2 || opts->check_every < 0) {
-        set_error("inpaint_solve_batched: invalid options");
+    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond != 1 || opts->x0 < 0 || opts->x0 > 2 ||
+        opts->check_every != 0) {
+        set_error("inpaint_solve_batched: invalid options (rtol > 0, max_iter > 0, precond 1, x0 0..2, check_every 0)");
         return FEMI_E_ARG;
     }
     for (int b = 0; b < B; ++b)
@@ -763,7 +763,7 @@ femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, 
         return FEMI_E_ARG;
     }
     if (!(opts->outer_rtol > 0.0) || opts->outer_max < 0 || !(opts->inner.rtol > 0.0) || opts->inner.max_iter <= 0 ||
-        opts->warm_start != 0) {
+        opts->inner.precond != 1 || opts->inner.check_every != 0 || opts->warm_start != 0) {
         set_error("tonal_optimise_l1: invalid options");
         return FEMI_E_ARG;
     }
@@ -776,6 +776,38 @@ femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, 
     return tonal_irls(sys, f, g, *opts, irls, eps, report, (cudaStream_t)stream);
 }
 
+femi_status femi_system_solver_path(femi_system sys, int32_t* path) {
+    if (!sys || !path) return FEMI_E_ARG;
+    *path = sys->last_path;
+    return FEMI_OK;
+}
+
+static femi_status apply_common(const char* what, femi_system sys, const double* in, double* out,
+                                const femi_cg_opts* opts) {
+    if (!sys || !in || !out || !opts) {
+        set_error(std::string(what) + ": NULL argument");
+        return FEMI_E_ARG;
+    }
+    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond != 1 || opts->check_every != 0) {
+        set_error(std::string(what) + ": invalid options (rtol > 0, max_iter > 0, precond 1, check_every 0)");
+        return FEMI_E_ARG;
+    }
+    return check_device();
+}
+
+femi_status femi_apply_B(femi_system sys, const double* g, double* u_px, const femi_cg_opts* opts, femi_stream stream) {
+    femi_status s = apply_common("apply_B", sys, g, u_px, opts);
+    if (s) return s;
+    return tonal_apply(sys, 0, g, u_px, *opts, (cudaStream_t)stream);
+}
+
+femi_status femi_apply_BT(femi_system sys, const double* r, double* s_out, const femi_cg_opts* opts,
+                          femi_stream stream) {
+    femi_status s = apply_common("apply_BT", sys, r, s_out, opts);
+    if (s) return s;
+    return tonal_apply(sys, 1, r, s_out, *opts, (cudaStream_t)stream);
+}
+
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                 femi_tonal_report* report, femi_stream stream) {
     if (!sys || !f || !g || !opts || !report) {
@@ -783,7 +815,7 @@ femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, con
         return FEMI_E_ARG;
     }
     if (!(opts->outer_rtol > 0.0) || opts->outer_max < 0 || !(opts->inner.rtol > 0.0) || opts->inner.max_iter <= 0 ||
-        opts->warm_start != 0) {
+        opts->inner.precond != 1 || opts->inner.check_every != 0 || opts->warm_start != 0) {
         set_error("tonal_optimise: invalid options");
         return FEMI_E_ARG;
     }

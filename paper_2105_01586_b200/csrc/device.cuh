@@ -149,6 +149,7 @@ struct femi_system_s {
     void* scratch = nullptr;
     void* scratch_m[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // multi-RHS graph caches (NR = 2..4)
     size_t scratch_bytes = 0;
+    int32_t last_path = 0;  // FEMI_PATH_* of the last solve (femi_system_solver_path)
     std::vector<void*> allocs;        // cudaMalloc'd large arrays
     std::vector<void*> arena_chunks;  // cudaMalloc'd arena chunks (small arrays carved from them)
     char* arena_cur = nullptr;  // next free byte of the current arena chunk
@@ -197,6 +198,9 @@ femi_status densify_select(femi_system_s* S, int nc, const double* const* f, con
                            int32_t* new_px, int64_t* n_added, cudaStream_t st);
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
                        femi_tonal_report* rep, cudaStream_t st, const double* sw = nullptr);
+// u_px = B g (mode 0) or s = B^T r (mode 1) with inner solves at opts (tonal.cu)
+femi_status tonal_apply(femi_system_s* S, int mode, const double* in, double* out, const femi_cg_opts& o,
+                        cudaStream_t st);
 femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o, int irls, double eps,
                        femi_tonal_l1_report* rep, cudaStream_t st);
 

@@ -2063,6 +2063,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         if (s == FEMI_OK) s = build_graph(*C, true, &C->restart);
         if (s != FEMI_OK) return s;
     }
+    S->last_path = C->gt_smem > 0 ? FEMI_PATH_GRAPH_TMA : FEMI_PATH_GRAPH_SELL;
     RItem it = C->item;
     it.g = g;
     it.bin = bin;
@@ -2425,6 +2426,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                       std::getenv("FEMI_NO_MULTI") == nullptr;
         for (int b = 1; b < B && shared; ++b) shared = S[b] == S[0];
         if (shared) {
+            bool used_multi = false;
             femi_status ret = FEMI_OK;
             int64_t tot = 0;
             for (int b0 = 0; b0 < B;) {
@@ -2437,6 +2439,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                 else
                     sb = graph_solve_multi(S[0], nr, g ? g + b0 : nullptr, bin ? bin + b0 : nullptr, u_vert + b0, o,
                                            iters ? iters + b0 : nullptr, relres ? relres + b0 : nullptr, st, &t1);
+                used_multi |= nr > 1 && sb != FEMI_E_ARG;
                 if (sb == FEMI_E_ARG && nr > 1) {  // ring does not fit: one RHS at a time
                     for (int c = 0; c < nr; ++c) {
                         int64_t t2 = 0;
@@ -2453,6 +2456,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                 b0 += nr;
             }
             if (total_iters) *total_iters = tot;
+            if (used_multi) S[0]->last_path = FEMI_PATH_GRAPH_MULTI;
             return ret;
         }
     }
@@ -2555,6 +2559,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         mode = ncta_item == 1 ? 0 : 1;
     }
     const int grid = B * ncta_item;
+    for (int b = 0; b < B; ++b) S[b]->last_path = mode == 3 ? FEMI_PATH_RESIDENT : FEMI_PATH_PERSISTENT;
     // rows of the largest CTA; shared memory: slice metadata, then as many of p, s, x as fit
     int64_t vrows = 0;
     for (int b = 0; b < B; ++b) {

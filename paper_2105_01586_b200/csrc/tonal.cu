@@ -330,6 +330,40 @@ out:
     return tn.status;
 }
 
+// The operator alone (femi_apply_B / femi_apply_BT): mode 0 out = B in (pixels), mode 1
+// out = B^T in (mask values); one inner solve each, synchronised for its status.
+femi_status tonal_apply(femi_system_s* S, int mode, const double* in, double* out, const femi_cg_opts& o,
+                        cudaStream_t st) {
+    const int64_t nv = S->nv, T = S->T;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    void* base = nullptr;
+    FEMI_CUDA(cudaMallocAsync(&base, 3 * al(sizeof(double) * nv) + al(sizeof(double) * 3 * std::max<int64_t>(T, 1)) +
+                                         al(sizeof(double) * 300) + al(sizeof(double) * 4),
+                              st));
+    char* cur = (char*)base;
+    auto take = [&](size_t x) {
+        char* p = cur;
+        cur += al(x);
+        return (double*)p;
+    };
+    Tonal tn;
+    tn.S = S;
+    tn.st = st;
+    tn.inner = o;
+    tn.uv = take(sizeof(double) * nv);
+    tn.yv = take(sizeof(double) * nv);
+    tn.w = take(sizeof(double) * nv);
+    tn.tri_w = take(sizeof(double) * 3 * std::max<int64_t>(T, 1));
+    tn.part = take(sizeof(double) * 300);
+    tn.dres = take(sizeof(double) * 4);
+    femi_status rc = mode == 0 ? tn.apply_B(in, out) : tn.apply_BT(in, out);
+    if (rc == FEMI_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "apply: sync");
+    cudaFreeAsync(base, st);
+    if (rc != FEMI_OK) return rc;
+    if (tn.status != FEMI_OK) set_error("apply: the inner solve did not converge");
+    return tn.status;
+}
+
 // L1 tonal optimisation by IRLS (reading R3): `irls`
 // reweightings, each computing r = f - B g, sqrt weights 1/sqrt(max(|r|, eps)) and a weighted
 // CGLS from the current g; the L1 error mean|f - B g| is reported before and after.

@@ -71,7 +71,11 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_mesh_timing", "femi_mesh_free", "femi_assemble", "femi_system_info_get", "femi_system_export",
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
-           "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert"]
+           "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert",
+           "femi_system_solver_path", "femi_apply_B", "femi_apply_BT"]
+
+# femi_system_solver_path values (include/femi.h)
+PATH_NAMES = {0: "none", 1: "resident", 2: "persistent", 3: "graph_sell", 4: "graph_tma", 5: "graph_multi"}
 
 
 def lib():
@@ -107,6 +111,9 @@ def lib():
                                                  ctypes.POINTER(ctypes.c_int64), P]
         L.femi_tonal_optimise_l1.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.c_int32, ctypes.c_double,
                                              ctypes.POINTER(TonalL1Report), P]
+        L.femi_system_solver_path.argtypes = [P, I32P]
+        L.femi_apply_B.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
+        L.femi_apply_BT.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
         for name in SYMBOLS:
             if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
                             "femi_kernel_launches"):
@@ -385,3 +392,26 @@ def tonal_optimise_l1(system, f, g, irls=3, eps=1.0, outer_rtol=1e-8, outer_max=
     if st not in (FEMI_OK, 4):
         _check(st)
     return st, rep.as_dict()
+
+
+def solver_path(system) -> str:
+    """Which solver the last solve on `system` ran (diagnostic; include/femi.h FEMI_PATH_*)."""
+    v = ctypes.c_int32(0)
+    _check(lib().femi_system_solver_path(system._h, ctypes.byref(v)))
+    return PATH_NAMES.get(v.value, str(v.value))
+
+
+def apply_B(system, g, u_px, inner: CgOpts | None = None, stream=None):
+    """u_px (device, W*H) <- B g (Eq. (4): inpainting from mask values g, rasterised)."""
+    import torch
+    inner = inner or cg_opts(rtol=1e-12)
+    _check(lib().femi_apply_B(system._h, _dptr(g, torch.float64), _dptr(u_px, torch.float64), ctypes.byref(inner),
+                              _stream(stream)))
+
+
+def apply_BT(system, r, s, inner: CgOpts | None = None, stream=None):
+    """s (device, n_mask) <- B^T r (the adjoint of apply_B)."""
+    import torch
+    inner = inner or cg_opts(rtol=1e-12)
+    _check(lib().femi_apply_BT(system._h, _dptr(r, torch.float64), _dptr(s, torch.float64), ctypes.byref(inner),
+                               _stream(stream)))

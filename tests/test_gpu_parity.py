@@ -56,10 +56,11 @@ def check_inpaint(W, H, f, mk, un, rtol=1e-10):
     assert abs(mse - O["mse"]) <= MSE_RTOL * max(O["mse"], 1e-300) or (O["mse"] == 0 and mse == 0)
     te = R["tri_err"].cpu().numpy()
     # tri_err / best: compared against the oracle's raster of the GPU's own vertex values
-    # (isolates S3/S4 from the solve): both sum e in pixel order and take the first strict
-    # maximum, so they are bit-identical
+    # (isolates S3/S4 from the solve). best is an arg-max of bit-identical e values (ties:
+    # lowest pix), so it is exact; tri_err sums the same e values in another order (reading
+    # A18): n_t positive terms, so within n_t 2^-53 relative -- 1e-12 covers n_t <= 9000
     Og = S.raster(u_vert, f)
-    np.testing.assert_array_equal(te, Og["tri_err"])
+    np.testing.assert_allclose(te, Og["tri_err"], rtol=1e-12, atol=0)
     np.testing.assert_array_equal(R["best"].cpu().numpy(), Og["best"])
     # the raster itself is exact: same vertex values -> bit-identical pixel values and errors
     # (S3's barycentric form in IEEE fp64, one rounding per operation on both sides)
@@ -116,6 +117,9 @@ def test_constant_image_exact(c0):
 
 
 def test_config2_batched_block_diagonal():
+    """C2: 32 distinct meshes solved as one block-diagonal batch; every item against the
+    oracle: grey values (1e-4), MSE (1e-6 relative), and the error map bit-identical to the
+    oracle's raster of the GPU's own vertex values (S3/S4 are exact given u_vert)."""
     c = make_config(2)
     W, H = c["W"], c["H"]
     f = dev(c["f"])
@@ -129,12 +133,14 @@ def test_config2_batched_block_diagonal():
     sse = [torch.zeros(1, dtype=torch.float64, device=DEV) for _ in systems]
     e_px = [torch.empty(W * H, dtype=torch.float64, device=DEV) for _ in systems]
     femi.rasterise_error_batched(systems, us, [f.reshape(-1)] * 32, sse, e_px=e_px)
-    for b in (0, 5, 17, 31):
+    for b in range(32):
         O = oracle.inpaint(W, H, c["f"], c["masks"][b], c["unknowns"][b])
-        assert np.abs(us[b].cpu().numpy() - O["u_vert"]).max() <= GREY_TOL
+        np.testing.assert_array_equal(verts[b], O["system"].vpix)
+        ub = us[b].cpu().numpy()
+        assert np.abs(ub - O["u_vert"]).max() <= GREY_TOL, b
         mse = sse[b].item() / (W * H)
-        assert abs(mse - O["mse"]) <= MSE_RTOL * O["mse"]
-        assert np.abs(e_px[b].cpu().numpy() - O["e_px"]).max() <= 0.05  # e = (u-f)^2: |de| <= 2|u-f| 1e-4
+        assert abs(mse - O["mse"]) <= MSE_RTOL * O["mse"], b
+        np.testing.assert_array_equal(e_px[b].cpu().numpy(), O["system"].raster(ub, c["f"])["e_px"])
     # batched == one-by-one
     u1 = torch.empty_like(us[3])
     femi.inpaint_solve_batched([systems[3]], [gs[3]], [u1], femi.cg_opts(rtol=1e-10))
@@ -178,33 +184,46 @@ def test_batched_plans_reuse():
         femi.RasterPlan(systems, [u.cpu() for u in us], [f] * 4, sse)
 
 
-def _near_tie_ok(gpu_new, ora_new, S, R, u_vert, f):
-    """Reading A15: sets may differ only where the oracle's own ranking has a near-tie at
-    the decision (triangle cut or per-triangle arg-max) within what the solve tolerance
-    can move: e is (u-f)^2 with |du| <= 1e-6 here, so |de| <= 2|u-f| 1e-6 + 1e-12."""
+def a15_flips(gpu_new, ora_new, S, Ro, delta):
+    """Reading A15: against the oracle's own solve, the selected sets may differ
+    only at decisions the solve tolerance can flip. The GPU and oracle vertex values differ by
+    at most delta (measured, max over vertices); the raster is a convex combination, so every
+    pixel moves by <= delta, e = (u - f)^2 by <= 2|u - f| delta + delta^2 and a triangle's sum
+    of n_t pixels by M_t = 2 delta sqrt(n_t tri_err) + n_t delta^2 (Cauchy-Schwarz). A pixel
+    may differ only if (i) its owner triangle t is within M_t + M_cut of the cut value, or (ii)
+    t's two largest empty-pixel errors are within 2 (2 |u - f|_max delta + delta^2). Returns the
+    number of differing pixels (printed by the callers)."""
     diff = np.setxor1d(gpu_new, ora_new)
     if diff.size == 0:
         return 0
-    te = R["tri_err"]
-    order = np.lexsort((np.arange(te.size), -te))
-    elig = order[(te[order] > 0) & (R["best"][order] >= 0)]
-    cut = te[elig[min(len(ora_new), elig.size) - 1]] if elig.size else 0.0
+    te, best = Ro["tri_err"], Ro["best"]
     owner = S.owner
+    ntp = np.bincount(owner, minlength=te.size)
+    M = 2 * delta * np.sqrt(ntp * te) + ntp * delta ** 2 + 1e-12 * te
+    order = np.lexsort((np.arange(te.size), -te))
+    elig = order[(te[order] > 0) & (best[order] >= 0)]
+    kcut = min(len(ora_new), elig.size) - 1
+    tcut = elig[kcut] if kcut >= 0 else None
+    cut = te[tcut] if tcut is not None else 0.0
+    mcut = M[tcut] if tcut is not None else 0.0
+    isv = S.is_vertex().astype(bool)
     for p in diff:
         t = owner[p]
-        near_cut = abs(te[t] - cut) <= 1e-6 * max(cut, 1e-300) + 1e-9
-        pix = np.nonzero(owner == t)[0]
-        e = R["e_px"][pix]
-        near_best = np.sum(e >= e.max() - (2 * np.sqrt(e.max()) * 1e-6 + 1e-12)) > 1
-        assert near_cut or near_best, f"pixel {p} (triangle {t}) differs without a near-tie"
-    return diff.size
+        near_cut = abs(te[t] - cut) <= M[t] + mcut
+        pix = np.nonzero((owner == t) & ~isv)[0]
+        e = np.sort(Ro["e_px"][pix])[::-1]
+        amax = np.sqrt(e[0]) if e.size else 0.0
+        near_best = e.size > 1 and e[0] - e[1] <= 2 * (2 * amax * delta + delta ** 2)
+        assert near_cut or near_best, f"pixel {p} (triangle {t}) differs without a near-tie (A15)"
+    return int(diff.size)
 
 
 def test_config3_densify_lockstep():
     """Reading A15: both sides start each iteration from the same mask. (a) The selection
     logic is exact: the oracle's select on the GPU's own vertex values equals the GPU's
     choice bit for bit. (b) Against the oracle's own solve the sets agree except at
-    near-ties the solver tolerance can flip (reported; expected none or very few)."""
+    near-ties the solver tolerance can flip (bound derived in a15_flips; count printed).
+    (c) The final mask of the GPU run gives the same MSE on both sides (1e-6 relative)."""
     c = make_config(3)
     W, H = c["W"], c["H"]
     f2 = c["f"]
@@ -212,20 +231,27 @@ def test_config3_densify_lockstep():
     mask, recs, mse = pipeline.densify(W, H, fd, c["mask0"], c["unknowns"], c["schedule"])
     assert mask.size == c["m"] and np.unique(mask).size == c["m"]
     masks = [r["mask"] for r in recs]
-    _, orecs, omse = oracle.densify(W, H, f2, c["mask0"], c["unknowns"], c["schedule"], lockstep_masks=masks)
-    flips = 0
+    _, orecs, _ = oracle.densify(W, H, f2, c["mask0"], c["unknowns"], c["schedule"], lockstep_masks=masks)
+    flips = []
     for t, (r, o) in enumerate(zip(recs, orecs)):
-        R = pipeline.inpaint(W, H, fd, r["mask"], c["unknowns"], want_images=False)
+        R = pipeline.inpaint(W, H, fd, r["mask"], c["unknowns"])
         S = oracle.System(W, H, r["mask"], c["unknowns"])
         u_gpu = R["u_vert"].cpu().numpy()
-        Rg = S.raster(u_gpu, f2)
-        sel = oracle.select(Rg["tri_err"], Rg["best"], Rg["e_px"], S.is_vertex(), c["schedule"][t + 1])
-        np.testing.assert_array_equal(r["new"], sel)  # (a) exact
-        Ro = S.raster(S.solve(f2.reshape(-1)[S.mask_px])[0], f2)
-        flips += _near_tie_ok(r["new"], o["new"], S, Ro, u_gpu, f2)  # (b)
+        te, bst, e_px = R["tri_err"].cpu().numpy(), R["best"].cpu().numpy(), R["e_px"].cpu().numpy()
+        sel = oracle.select(te, bst, e_px, S.is_vertex(), c["schedule"][t + 1])
+        np.testing.assert_array_equal(r["new"], sel)  # (a) exact, on the GPU's own reductions
+        Rg = S.raster(u_gpu, f2)  # which match the oracle's raster of the same vertex values
+        np.testing.assert_array_equal(e_px, Rg["e_px"])
+        np.testing.assert_array_equal(bst, Rg["best"])
+        np.testing.assert_allclose(te, Rg["tri_err"], rtol=1e-12, atol=0)
+        uo = S.solve(f2.reshape(-1)[S.mask_px])[0]
+        Ro = S.raster(uo, f2)
+        flips.append(a15_flips(r["new"], o["new"], S, Ro, float(np.abs(u_gpu - uo).max())))  # (b)
         assert abs(r["mse"] - o["mse"]) <= MSE_RTOL * o["mse"]
-    assert flips <= 4, f"{flips} near-tie flips"
-    assert abs(mse - omse) <= MSE_RTOL * omse or flips > 0
+    print(f"C3 lockstep near-tie flips per iteration (A15): {flips}")
+    assert sum(flips) <= 4, f"{flips} near-tie flips"
+    Of = oracle.inpaint(W, H, f2, mask, c["unknowns"])  # (c) on the GPU run's final mask
+    assert abs(mse - Of["mse"]) <= MSE_RTOL * Of["mse"]
 
 
 def test_densify_constant_image_fill_path():
@@ -376,12 +402,14 @@ def test_colour_shared_mesh(W):
     for k in range(3):
         np.testing.assert_array_equal(upx[k].cpu().numpy(), R["u_px"][k])
     np.testing.assert_array_equal(e_px.cpu().numpy(), R["e_px"])
-    np.testing.assert_array_equal(te.cpu().numpy(), R["tri_err"])
+    np.testing.assert_allclose(te.cpu().numpy(), R["tri_err"], rtol=1e-12, atol=0)  # order (A18)
     np.testing.assert_array_equal(bs.cpu().numpy(), R["best"])
     assert abs(sse.item() - R["sse"]) <= 1e-9 * R["sse"]  # grouped vs sequential fp64 sum of N terms
     b = max(1, int(0.002 * N))
     new = femi.densify_step_channels(S, fd, us, b)
-    np.testing.assert_array_equal(new, oracle.select(R["tri_err"], R["best"], R["e_px"], O.is_vertex(), b))
+    # the selection logic on the GPU's own reductions: exact
+    np.testing.assert_array_equal(new, oracle.select(te.cpu().numpy(), bs.cpu().numpy(), e_px.cpu().numpy(),
+                                                     O.is_vertex(), b))
 
 
 def test_tonal_l1_irls_vs_oracle():

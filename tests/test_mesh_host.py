@@ -32,7 +32,7 @@ def test_abi_exports_every_declared_symbol():
     L = femi.lib()
     import re
     hdr = open(__file__.replace("tests/test_mesh_host.py", "include/femi.h")).read()
-    declared = set(re.findall(r"\b(femi_[a-z0-9_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(femi_[A-Za-z0-9_]+)\s*\(", hdr))
     assert declared == set(femi.SYMBOLS)
     for name in declared:
         assert hasattr(L, name)
@@ -96,6 +96,63 @@ def test_mesh_large_structure():
     M, E = product_mesh(W, H, mk, un)
     S_tri = oracle.delaunay(W, H, E["vert_px"])
     np.testing.assert_array_equal(E["tri"], S_tri)
+    # the shared mesh itself, checked from scratch in numpy (not through either C code):
+    vp = E["vert_px"].astype(np.int64)
+    tri = E["tri"].astype(np.int64)
+    X, Y = vp % W, vp // W
+    nv, T = vp.size, tri.shape[0]
+
+    def orient(a, b, c):
+        return (X[b] - X[a]) * (Y[c] - Y[a]) - (Y[b] - Y[a]) * (X[c] - X[a])
+
+    a, b, c = tri[:, 0], tri[:, 1], tri[:, 2]
+    o = orient(a, b, c)
+    assert np.all(o > 0)  # every triangle CCW and non-degenerate
+    assert o.sum() == 2 * (W - 1) * (H - 1)  # areas tile the image domain (reading A1)
+    on_border = (X == 0) | (X == W - 1) | (Y == 0) | (Y == H - 1)
+    assert T == 2 * nv - 2 - int(on_border.sum())  # Euler count with h hull (border) points
+    # edges: each used by <= 2 triangles; edges used once lie on the image border
+    ev = np.concatenate([np.stack([tri[:, (k + 1) % 3], tri[:, (k + 2) % 3]], 1) for k in range(3)])
+    opp = np.concatenate([tri[:, k] for k in range(3)])
+    own = np.concatenate([np.arange(T)] * 3)
+    key = np.minimum(ev[:, 0], ev[:, 1]) * nv + np.maximum(ev[:, 0], ev[:, 1])
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    _, cnt = np.unique(ks, return_counts=True)
+    assert cnt.max() <= 2
+    single = np.ones(ks.size, bool)
+    dup = ks[1:] == ks[:-1]
+    single[1:] &= ~dup
+    single[:-1] &= ~dup
+    se = ev[order[single]]
+    bx = ((X[se[:, 0]] == 0) & (X[se[:, 1]] == 0)) | ((X[se[:, 0]] == W - 1) & (X[se[:, 1]] == W - 1))
+    by = ((Y[se[:, 0]] == 0) & (Y[se[:, 1]] == 0)) | ((Y[se[:, 0]] == H - 1) & (Y[se[:, 1]] == H - 1))
+    assert np.all(bx | by)
+    # local SoS-Delaunay property (reading A3) on every interior edge, both directions
+    i1, i2 = order[:-1][dup], order[1:][dup]
+
+    def sos_inside(t, d):
+        ta, tb, tc = tri[t, 0], tri[t, 1], tri[t, 2]
+        adx, ady = X[ta] - X[d], Y[ta] - Y[d]
+        bdx, bdy = X[tb] - X[d], Y[tb] - Y[d]
+        cdx, cdy = X[tc] - X[d], Y[tc] - Y[d]
+        det = ((adx * adx + ady * ady) * (bdx * cdy - bdy * cdx) - (bdx * bdx + bdy * bdy) * (adx * cdy - ady * cdx)
+               + (cdx * cdx + cdy * cdy) * (adx * bdy - ady * bdx))
+        res = det > 0
+        z = det == 0
+        if np.any(z):
+            P = np.stack([vp[ta], vp[tb], vp[tc], vp[d]], 1)
+            smin = P.argmin(1)
+            verts = np.stack([ta, tb, tc], 1)
+            k = np.minimum(smin, 2)
+            t1 = verts[np.arange(t.size), (k + 1) % 3]
+            t2 = verts[np.arange(t.size), (k + 2) % 3]
+            tie = np.where(smin == 3, True, orient(t1, t2, d) < 0)
+            res = np.where(z, tie, res)
+        return res
+
+    assert not np.any(sos_inside(own[i1], opp[i2]))
+    assert not np.any(sos_inside(own[i2], opp[i1]))
 
 
 @pytest.mark.parametrize("strips,margin", [(2, None), (7, 1), (16, 2), (40, 3)])
