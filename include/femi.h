@@ -53,6 +53,13 @@ const char* femi_version(void);
 /* Number of CUDA kernels this library has launched since it was loaded (all threads). */
 int64_t femi_kernel_launches(void);
 
+/* Device-side bounds-check failures recorded since the last call, then reset; *first_site (if
+ * not NULL) receives the first failing check (file id * 100000 + line). Always 0 unless the
+ * library was built with device checks (libfemi_check.so, FEMI_DEVICE_CHECKS): that build,
+ * run under the GPU test suite, stands in for compute-sanitizer memcheck on the index paths.
+ * Returns -1 if the counters cannot be read. */
+int64_t femi_device_check_failures(int64_t* first_site);
+
 typedef struct femi_mesh_s* femi_mesh;
 typedef struct femi_system_s* femi_system;
 

@@ -776,6 +776,18 @@ femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, 
     return tonal_irls(sys, f, g, *opts, irls, eps, report, (cudaStream_t)stream);
 }
 
+int64_t femi_device_check_failures(int64_t* first_site) {
+    int64_t site = 0;
+    int64_t n = 0;
+    for (auto fn : {dcheck_abi, dcheck_assemble, dcheck_pcg, dcheck_raster, dcheck_select, dcheck_tonal}) {
+        const int64_t k = fn(&site);
+        if (k < 0) return -1;
+        n += k;
+    }
+    if (first_site) *first_site = site;
+    return n;
+}
+
 femi_status femi_system_solver_path(femi_system sys, int32_t* path) {
     if (!sys || !path) return FEMI_E_ARG;
     *path = sys->last_path;
@@ -826,3 +838,5 @@ femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, con
 }
 
 }  // extern "C"
+
+FEMI_DCHECK_READER(dcheck_abi)

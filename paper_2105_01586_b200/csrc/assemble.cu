@@ -58,6 +58,7 @@ __global__ void k_assemble_rows(int64_t n_u, int W, const int32_t* __restrict__ 
             }
             const int32_t pj = vpix[j];
             int32_t o1 = uop[2 * e], o2 = uop[2 * e + 1];
+            FEMI_DCHECK(j >= 0 && j < n_u && o1 >= 0, 2);
             double v = half_cot(W, pi, pj, vpix[o1]);
             if (o2 >= 0) v = v + half_cot(W, pi, pj, vpix[o2]);
             uval[e] = v;
@@ -169,3 +170,5 @@ femi_status launch_assemble_values(femi_system_s* S, cudaStream_t st) {
 }
 
 }  // namespace femi
+
+FEMI_DCHECK_READER(dcheck_assemble)

@@ -120,6 +120,11 @@ struct femi_system_s {
     // tp_ptr[T+1] / tp_pix[N] (ascending pix per triangle; pix | cls << 30, cls 1..3 = vertex pixel)
     int32_t* tp_ptr = nullptr;
     uint32_t* tp_pix = nullptr;
+    // raster windows (raster.cu): per 16-triangle group g, windows tp_wptr[g] .. tp_wptr[g+1] of
+    // <= 128 consecutive group-list entries spanning < 128 rows; a 32-byte record each
+    int32_t* tp_wptr = nullptr;
+    void* tp_win = nullptr;
+    int64_t tp_nwin = 0;
     // Tiled jagged-diagonal copy of the scaled off-diagonal matrix for the TMA-streamed SpMV of
     // large systems (graph mode): tiles of kJdsRows internal rows; per tile a contiguous
     // entry block [jds_eb[t], jds_eb[t+1]) (a multiple of 8 entries), inside it slice w (32
@@ -168,6 +173,53 @@ femi_status cuda_fail(cudaError_t e, const char* what);
 
 // kernel-launch accounting (femi_kernel_launches)
 void count_launches(int64_t n);
+
+}  // namespace femi
+
+// Device-side bounds checks, compiled in only with -DFEMI_DEVICE_CHECKS (the checked build
+// libfemi_check.so; tests select it with FEMI_LIB). compute-sanitizer is closed on the GPU
+// pool, so the checked build run under the GPU test suite stands in for memcheck on the
+// index paths: a failed check counts in a per-translation-unit device counter and records its
+// site (file id * 100000 + line); the kernel carries on. femi_device_check_failures() reads
+// and resets the counters of every translation unit (FEMI_DCHECK_READER).
+#ifdef FEMI_DEVICE_CHECKS
+namespace {
+__device__ unsigned long long g_dcheck[2];
+}
+#define FEMI_DCHECK(cond, file_id)                                                           \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            if (atomicAdd(&g_dcheck[0], 1ull) == 0ull) g_dcheck[1] = (file_id) * 100000ull + __LINE__; \
+        }                                                                                    \
+    } while (0)
+#define FEMI_DCHECK_READER(name)                                                             \
+    namespace femi {                                                                         \
+    int64_t name(int64_t* site) {                                                            \
+        unsigned long long h[2] = {0ull, 0ull};                                              \
+        if (cudaMemcpyFromSymbol(h, g_dcheck, sizeof(h)) != cudaSuccess) return -1;          \
+        const unsigned long long z[2] = {0ull, 0ull};                                        \
+        cudaMemcpyToSymbol(g_dcheck, z, sizeof(z));                                          \
+        if (h[0] && site && *site == 0) *site = (int64_t)h[1];                               \
+        return (int64_t)h[0];                                                                \
+    }                                                                                        \
+    }
+#else
+#define FEMI_DCHECK(cond, file_id) \
+    do {                           \
+    } while (0)
+#define FEMI_DCHECK_READER(name) \
+    namespace femi {             \
+    int64_t name(int64_t*) { return 0; } \
+    }
+#endif
+
+namespace femi {
+int64_t dcheck_abi(int64_t*);
+int64_t dcheck_assemble(int64_t*);
+int64_t dcheck_pcg(int64_t*);
+int64_t dcheck_raster(int64_t*);
+int64_t dcheck_select(int64_t*);
+int64_t dcheck_tonal(int64_t*);
 
 constexpr int kRowsPerChunk = 512;
 constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)

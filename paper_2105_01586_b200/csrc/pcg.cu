@@ -48,6 +48,16 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 // All solver vectors (b, x, r, w, p, s) live in the INTERNAL row order (see abi.cu:
 // 2-D blocked numbering, length-sorted inside kSellSigma windows); inv maps an internal
 // row to its canonical unknown index for the input/output vectors (g, u_vert).
+// Graph mode, lean tail: the CG recurrence scalars of the loop, double-buffered by iteration
+// parity (k_gur of body slot k reads ls[k & 1] and writes ls[(k + 1) & 1], so no CTA reads a
+// slot another CTA of the same launch writes). The final values go to the item's CgState.
+struct LoopState {
+    double alpha;  // alpha of the update this state's k_gur performed
+    double rr;     // gamma = r^.r^ of that update's residual
+    int32_t iters, active, started, need_rho;
+    int32_t status, pad;
+};
+
 struct RItem {
     const int32_t* inv;   // internal row -> canonical unknown
     const int32_t* len;   // per 32-row slice
@@ -83,6 +93,7 @@ struct RItem {
     double* part;  // [ncta][4] partial sums / barrier slots
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
+    LoopState* ls;  // graph mode (lean tail): ls[2]
     int32_t n, m, cta0, ncta, nwin, x0mode;
     double rtol;  // graph mode reads the options from the item (the graph is reused)
     int32_t max_iter, pad2;
@@ -247,6 +258,7 @@ __global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, un
         } else {
             double acc = 0.0, accr = 0.0;
             for (int e = it.krp[i]; e < it.krp[i + 1]; ++e) {
+                FEMI_DCHECK(it.kci[e] >= 0 && it.kci[e] < it.m, 3);
                 const double a = it.kav[e], gk = it.g[it.kci[e]];
                 acc = acc + a * gk;
                 accr = fma(a, gk - c, accr);
@@ -325,7 +337,10 @@ __global__ void __launch_bounds__(KNT) k_true_res(const RItem* __restrict__ item
     double v[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
         double ax = 0.0;
-        for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+        for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) {
+            FEMI_DCHECK(it.uci[e] >= 0 && it.uci[e] < it.n, 3);
+            ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
+        }
         const double ri = it.b[i] - ax;
         it.r[i] = it.s[i] * ri;
         v[0] += ri * ri;
@@ -725,6 +740,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgr(const RItem* __restrict__ items)
             int o = (int)(((long long)w * C) / nwin);  // owner CTA of window w: row0(o) <= c < row0(o + 1)
             while (o + 1 < C && row0(o + 1) <= c) ++o;
             while (o > 0 && row0(o) > c) --o;
+            FEMI_DCHECK(c >= 0 && c < n && o >= 0 && o < C && c >= row0(o) && c < row0(o + 1), 3);
             val_s[e] = it.val[ge];
             code_s[e] = (o << 16) | (c - row0(o));
         }
@@ -925,6 +941,12 @@ __global__ void k_reset_items(int B, const RItem* __restrict__ items) {
 // p = s = 0 (start and restart of the recurrence)
 __global__ void k_zero_ps(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
+    if (it.ls && blockIdx.x == 0 && threadIdx.x == 0) {  // (re)start of the lean-tail recurrence
+        LoopState l = {};
+        l.iters = it.st->iters;  // a restart continues the count
+        l.active = 1;
+        it.ls[0] = l;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
         it.p[i] = 0.0;
         it.sv[i] = 0.0;
@@ -1156,6 +1178,194 @@ __device__ __forceinline__ void cg_tail(double (&v)[3], bool act, CgState* S, in
     if (tp) g_tail_ts[4 * prof_it + 3] = gtime();  // D: condition set
 }
 
+// The CTA's three partial dots in fixed warp order -> P[0..2]
+template <int NT>
+__device__ __forceinline__ void cta_partials(double (&v)[3], double* P) {
+    __shared__ double shp[3 * (NT / 32)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v[q] = warp_sum_d(v[q]);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) shp[3 * wid + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += shp[3 * w + threadIdx.x];
+        P[threadIdx.x] = t;
+    }
+}
+
+// Graph mode, lean tail: ONE kernel per iteration does the reduction AND the update. Every CTA
+// sums the previous SpMV's per-CTA partials in the same fixed order (bit-identical scalars in
+// all CTAs), advances the CG recurrence (cg_advance's rules) from ls[par] and applies the
+// update p = r + beta p ; s = w + beta s ; r -= alpha s ; x every other iteration (as k_gu).
+// Block 0 publishes the new scalars in ls[par ^ 1]; on termination it writes the final state
+// (iteration count, status, the deferred x term) to the item's CgState and ends the WHILE loop.
+// Compared with the last-CTA tail of cg_tail, nothing serialises behind an atomic counter.
+constexpr int GRT = 256;
+__global__ void __launch_bounds__(GRT) k_gur(const RItem* __restrict__ items, const double* __restrict__ part,
+                                            int nparts, int par, cudaGraphConditionalHandle h) {
+    __shared__ double red[3 * (GRT / 32)];
+    __shared__ double sc[4];  // alpha, beta, alpha_pend
+    __shared__ int si[2];     // active, iters
+    grid_dep_wait();  // behind the SpMV through a programmatic edge (graph body)
+    const RItem& it = items[0];
+    const LoopState L = it.ls[par];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (!L.active) {  // finished earlier in this launch: keep the next slot inactive
+        if (blockIdx.x == 0 && threadIdx.x == 0) it.ls[par ^ 1].active = 0;
+        return;
+    }
+    const unsigned long long tprof = g_loop_prof ? gtime() : 0ull;
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += GRT)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[q] += __ldcg(part + 4 * b + q);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v[q] = warp_sum_d(v[q]);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) red[3 * wid + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double gam2 = 0.0, del2 = 0.0, rho2 = 0.0;
+        for (int w = 0; w < GRT / 32; ++w) {
+            gam2 += red[3 * w];
+            del2 += red[3 * w + 1];
+            rho2 += red[3 * w + 2];
+        }
+        const CgState* S = it.st;
+        const double tol2 = S->tol2, bn2 = S->bn2;
+        LoopState N = L;
+        N.started = 1;
+        int active = 0;
+        int status = L.status;
+        double alpha = 0.0, beta = 0.0;
+        int iters = L.iters;
+        if (!L.started) {  // the first SpMV: start the recurrence (cg_advance<true>)
+            const bool fin = isfinite(gam2) && isfinite(bn2);
+            active = (bn2 > 0.0 && rho2 > tol2 && fin && L.iters < S->max_iter) ? 1 : 0;
+            if (!fin) status = FEMI_E_NONFINITE;
+            if (active && !(del2 > 0.0)) {
+                status = FEMI_E_NEG_CURVATURE;
+                active = 0;
+            }
+            if (active) {
+                alpha = gam2 / del2;
+                beta = 0.0;
+            }
+        } else {  // cg_advance<false>: count the iteration, test convergence, next alpha / beta
+            iters = L.iters + 1;
+            if (!isfinite(gam2) || !isfinite(del2)) {
+                status = FEMI_E_NONFINITE;
+            } else if (L.need_rho && rho2 <= tol2) {
+                // converged
+            } else if (iters >= S->max_iter) {
+                status = FEMI_E_NOT_CONVERGED;
+            } else {
+                beta = gam2 / L.rr;
+                const double den = del2 - beta * gam2 / L.alpha;
+                if (!(den > 0.0)) {
+                    status = FEMI_E_NEG_CURVATURE;
+                } else {
+                    alpha = gam2 / den;
+                    active = 1;
+                }
+            }
+        }
+        // the previous update deferred its x term when its iteration label was even
+        const bool deferred = L.started && (L.iters & 1) == 0;
+        N.alpha = alpha;
+        N.rr = gam2;
+        N.iters = iters;
+        N.active = active;
+        N.status = status;
+        N.need_rho = (gam2 * it.dmin <= 100.0 * tol2) ? 1 : 0;
+        sc[0] = alpha;
+        sc[1] = beta;
+        sc[2] = (deferred && L.started) ? L.alpha : 0.0;
+        si[0] = active;
+        si[1] = iters;
+        if (blockIdx.x == 0) {
+            it.ls[par ^ 1] = N;
+            if (!active) {  // final state for k_finalize / k_true_res / the host
+                CgState* Sw = it.st;
+                Sw->iters = iters;
+                Sw->status = status;
+                Sw->active = 0;
+                Sw->x_pend = deferred ? 1 : 0;
+                Sw->alpha_pend = L.alpha;
+                Sw->rr = gam2;
+                if (h) cudaGraphSetConditional(h, 0u);
+            }
+        }
+    }
+    __syncthreads();
+    if (!si[0]) return;
+    const double alpha = sc[0], beta = sc[1], ap = sc[2];
+    double* __restrict__ r = it.r;
+    const double* __restrict__ w = it.w;
+    double* __restrict__ p = it.p;
+    double* __restrict__ sv = it.sv;
+    const int n = it.n, stride = gridDim.x * blockDim.x;
+    if ((si[1] & 1) == 0) {  // even label: x's term deferred to the next update (or k_finalize)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+            const int j = i + stride;
+            const bool hj = j < n;
+            const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i];
+            double rj = 0.0, wj = 0.0, pj0 = 0.0, sj0 = 0.0;
+            if (hj) {
+                rj = r[j];
+                wj = w[j];
+                pj0 = p[j];
+                sj0 = sv[j];
+            }
+            const double si = fma(beta, si0, wi);
+            p[i] = fma(beta, pi0, ri);
+            sv[i] = si;
+            r[i] = fma(-alpha, si, ri);
+            if (hj) {
+                const double sj = fma(beta, sj0, wj);
+                p[j] = fma(beta, pj0, rj);
+                sv[j] = sj;
+                r[j] = fma(-alpha, sj, rj);
+            }
+        }
+    } else {
+        double* __restrict__ x = it.x;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+            const int j = i + stride;
+            const bool hj = j < n;
+            const double ri = r[i], wi = w[i], pi0 = p[i], si0 = sv[i], xi = x[i];
+            double rj = 0.0, wj = 0.0, pj0 = 0.0, sj0 = 0.0, xj = 0.0;
+            if (hj) {
+                rj = r[j];
+                wj = w[j];
+                pj0 = p[j];
+                sj0 = sv[j];
+                xj = x[j];
+            }
+            const double pi = fma(beta, pi0, ri), si = fma(beta, si0, wi);
+            p[i] = pi;
+            sv[i] = si;
+            x[i] = fma(alpha, pi, fma(ap, pi0, xi));
+            r[i] = fma(-alpha, si, ri);
+            if (hj) {
+                const double pj = fma(beta, pj0, rj), sj = fma(beta, sj0, wj);
+                p[j] = pj;
+                sv[j] = sj;
+                x[j] = fma(alpha, pj, fma(ap, pj0, xj));
+                r[j] = fma(-alpha, sj, rj);
+            }
+        }
+    }
+    if (g_loop_prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) loop_stamp(0, si[1], tprof);
+    }
+}
+
 // S: w = r + A^_off r (SELL, two slices per warp) and the dots; the last block updates the
 // recurrence scalars and (FIRST: starts it) and sets the WHILE condition when every item has
 // reported (any item still active -> 1).
@@ -1253,9 +1463,9 @@ struct JStage {
     double* s;
 };
 
-template <bool FIRST>
+template <bool FIRST, bool LEAN>
 __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
-                                            unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h) {
+                                            unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int lsi) {
     extern __shared__ __align__(128) unsigned char jsm[];
     unsigned long long t_start = 0;
     if (g_loop_prof && threadIdx.x == 0) t_start = gtime();
@@ -1291,7 +1501,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     // each stage's phase open); r and q follow once the update kernel has completed.
     // no prefetch for the no-op tail of the unrolled body: active only goes 1 -> 0 inside one
     // graph launch, so a 0 read before the dependency wait is final (a stale 1 only prefetches)
-    const bool live = FIRST || *(volatile const int*)&S->active;
+    const bool live = FIRST || (LEAN ? *(volatile const int*)&it.ls[lsi].active : *(volatile const int*)&S->active);
     const int npre = live ? min(g_pdl_pre, te - tb) : 0;
     const uint64_t pol = policy_evict_first();  // keep the CG vectors L2-resident
     if (warp == JCW && lane == 0) {
@@ -1310,8 +1520,9 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         }
     }
     grid_dep_wait();
-    const bool act = FIRST || S->active;
-    const bool nrho = FIRST || S->need_rho;  // else the q stream and the residual monitor are skipped
+    const bool act = FIRST || (LEAN ? it.ls[lsi].active : S->active);
+    // else the q stream and the residual monitor are skipped
+    const bool nrho = FIRST || (LEAN ? it.ls[lsi].need_rho : S->need_rho);
     double v[3] = {0.0, 0.0, 0.0};
     if (!act && warp == JCW && lane == 0) {
         // nothing to compute: close the prefetched stages and let their copies land before exit
@@ -1382,6 +1593,11 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                         const int idx = (k0 + u < L ? doff[k0 + u] : 0) + lane;
                         vv[u] = a ? q.val[idx] : 0.0;
                         c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
+                        FEMI_DCHECK(!a || idx < tile_e[k].y, 3);
+                        FEMI_DCHECK((unsigned)c[u] < (unsigned)kJdsRows ||
+                                        ((int64_t)t * kJdsRows + c[u] >= 0 &&
+                                         (int64_t)t * kJdsRows + c[u] < (int64_t)it.ntile * kJdsRows),
+                                    3);
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u)  // neighbours' r: this tile's slice from shared memory, else L1/L2
@@ -1402,7 +1618,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             }
         }
     }
-    const int it_prof = S->iters;
+    const int it_prof = LEAN ? (FIRST ? 0 : it.ls[lsi].iters) : S->iters;
     if (g_loop_prof && act && it_prof < kLoopProfMax) {
         __syncthreads();  // profiling only: every warp of the CTA is done
         if (threadIdx.x == 0) {
@@ -1416,7 +1632,13 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             atomicMax(&g_loop_ts2[4 * it_prof + 2], t);
         }
     }
-    cg_tail<FIRST, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1, it.dmin);
+    if constexpr (LEAN) {
+        // lean tail: this CTA's partial dots (fixed warp order) to its slot; the next k_gur
+        // sums the slots and advances the recurrence in every CTA
+        if (act) cta_partials<JNT>(v, part + 4 * (size_t)blockIdx.x);
+    } else {
+        cg_tail<FIRST, JNT>(v, act, S, B, part, gcnt, h, (act && !FIRST) ? it_prof : -1, it.dmin);
+    }
     if (g_loop_prof && act && !FIRST && threadIdx.x == 0) {
         if (it_prof < kLoopProfMax) atomicMax(&g_loop_ts2[4 * it_prof + 3], gtime());
         loop_stamp(1, it_prof, t_start);
@@ -1763,8 +1985,9 @@ femi_status add_kernel_pdl(cudaGraph_t gr, cudaGraphNode_t* dep, void* fn, dim3 
 femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     cudaGraph_t gr;
     FEMI_CUDA(cudaGraphCreate(&gr, 0));
+    const bool tma = C.gt_smem > 0;  // TMA SpMV: lean tail (k_gur ends the loop); SELL: cg_tail does
     cudaGraphConditionalHandle h;
-    FEMI_CUDA(cudaGraphConditionalHandleCreate(&h, gr, 0, cudaGraphCondAssignDefault));
+    FEMI_CUDA(cudaGraphConditionalHandleCreate(&h, gr, tma ? 1u : 0u, cudaGraphCondAssignDefault));
     RItem* di = C.d_items;
     int one = 1;
     double* part = C.d_part;
@@ -1776,6 +1999,8 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     void* a_cnt0[2] = {&di, &cnt0};
     void* a_cnt1[2] = {&di, &cnt1};
     void* a_gs[5] = {&di, &one, &part, &gcnt, &h};
+    int lsi0 = 0;
+    void* a_gt0[6] = {&di, &one, &part, &gcnt, &h, &lsi0};
     const dim3 gk(C.gx, 1), bk(KNT);
     cudaGraphNode_t prev = nullptr, nd;
     cudaGraphNode_t* dep = nullptr;
@@ -1785,9 +2010,8 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         dep = &prev;
         return s;
     };
-    const bool tma = C.gt_smem > 0;
-    void* spmv_first = tma ? (void*)k_gt<true> : (void*)k_gs<true>;
-    void* spmv = tma ? (void*)k_gt<false> : (void*)k_gs<false>;
+    void* spmv_first = tma ? (void*)k_gt<true, true> : (void*)k_gs<true>;
+    void* spmv = tma ? (void*)k_gt<false, true> : (void*)k_gs<false>;
     const dim3 gsp(tma ? C.gt_blocks : C.gs_blocks), bsp(tma ? JNT : GNT);
     const unsigned ssp = tma ? C.gt_smem : 0;
     femi_status s = FEMI_OK;
@@ -1801,7 +2025,7 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
     if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
     if (!restart)
         if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
-    if ((s = chain(spmv_first, gsp, bsp, a_gs, ssp))) return s;
+    if ((s = chain(spmv_first, gsp, bsp, tma ? a_gt0 : a_gs, ssp))) return s;
     {
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
@@ -1823,9 +2047,14 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         // first matrix tiles while k_gu runs; each waits in grid_dep_wait for its inputs)
         for (int k = 0; k < kUnroll; ++k) {
             if (tma) {
-                if ((s = add_kernel_pdl(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u)))
+                // lean tail: k_gur (reduce the SpMV partials + update, body slot parity k & 1)
+                // -> k_gt (reads the scalars k_gur published in ls[(k + 1) & 1])
+                int par = k & 1, lsi = (k + 1) & 1, np = C.gt_blocks;
+                void* a_gur[5] = {&di, &part, &np, &par, &h};
+                void* a_gt[6] = {&di, &one, &part, &gcnt, &h, &lsi};
+                if ((s = add_kernel_pdl(body, bprev ? &bprev : nullptr, (void*)k_gur, gu, dim3(GRT), a_gur, &u)))
                     return s;
-                if ((s = add_kernel_pdl(body, &u, spmv, gsp, bsp, a_gs, &sn, ssp))) return s;
+                if ((s = add_kernel_pdl(body, &u, spmv, gsp, bsp, a_gt, &sn, ssp))) return s;
             } else {
                 if ((s = add_kernel(body, bprev ? &bprev : nullptr, (void*)k_gu, gu, dim3(GNT), a_items, &u)))
                     return s;
@@ -1981,7 +2210,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             if (JNS * stage_bytes + 4096 <= (size_t)optin) {
                 C->gt_smem = (unsigned)(JNS * stage_bytes);
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
-                for (const void* fn : {(const void*)k_gt<false>, (const void*)k_gt<true>})
+                for (const void* fn : {(const void*)k_gt<false, true>, (const void*)k_gt<true, true>,
+                                       (const void*)k_gt<false, false>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
                 femi_status ts = tile_split(S, C->gt_blocks, jpart);
                 if (ts != FEMI_OK) return ts;
@@ -1989,6 +2219,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         }
         const int pb = std::max(C->gs_blocks, C->gt_blocks);
         const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) +
+                             al(sizeof(LoopState) * 2) +
                              al(sizeof(unsigned) * 4) + al(sizeof(double) * 4 * pb) + al(sizeof(double) * C->gx) +
                              6 * vb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
@@ -2003,6 +2234,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         if (!jpart.empty())
             FEMI_CUDA(cudaMemcpy(d_jpart, jpart.data(), sizeof(int32_t) * jpart.size(), cudaMemcpyHostToDevice));
         C->d_state = (CgState*)take(sizeof(CgState));
+        LoopState* d_ls = (LoopState*)take(sizeof(LoopState) * 2);
         C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
         C->d_part = (double*)take(sizeof(double) * 4 * pb);
         RItem& it = C->item;
@@ -2052,6 +2284,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.kav = S->ukI_val;
         it.part = nullptr;
         it.st = C->d_state;
+        it.ls = C->gt_smem > 0 ? d_ls : nullptr;
         it.n = (int32_t)n;
         it.m = (int32_t)S->m;
         it.cta0 = 0;
@@ -2122,8 +2355,8 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             FEMI_CUDA(cudaEventRecord(e0, st));
             k_gu<<<dim3(std::min(C->gx * 2, 1184)), GNT, 0, st>>>(C->d_items);
             FEMI_CUDA(cudaEventRecord(e1, st));
-            k_gt<false><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt,
-                                                                      (cudaGraphConditionalHandle)0);
+            k_gt<false, false><<<dim3(C->gt_blocks), JNT, C->gt_smem, st>>>(C->d_items, 1, C->d_part, gcnt,
+                                                                             (cudaGraphConditionalHandle)0, 0);
             FEMI_CUDA(cudaEventRecord(e2, st));
             FEMI_CUDA(cudaEventSynchronize(e2));
             float x = 0.f, y = 0.f;
@@ -2783,3 +3016,5 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
 }
 
 }  // namespace femi
+
+FEMI_DCHECK_READER(dcheck_pcg)

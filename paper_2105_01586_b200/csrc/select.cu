@@ -153,13 +153,19 @@ __global__ void k_emit(int64_t n, int64_t per, const unsigned long long* __restr
 
 __global__ void k_mark(int64_t n, const int32_t* __restrict__ px, uint8_t* __restrict__ taken) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    {
+        FEMI_DCHECK(px[i] >= 0, 5);
         taken[px[i]] = 1;
+    }
 }
 
 __global__ void k_gather_best(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ best,
                               int32_t* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    {
+        FEMI_DCHECK(idx[i] >= 0, 5);
         out[i] = best[idx[i]];
+    }
 }
 
 // The whole triangle selection in ONE block for small T (densification of small and medium
@@ -421,3 +427,5 @@ femi_status densify_select(femi_system_s* S, int nc, const double* const* f, con
 }
 
 }  // namespace femi
+
+FEMI_DCHECK_READER(dcheck_select)

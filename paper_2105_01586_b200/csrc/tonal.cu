@@ -37,7 +37,10 @@ __global__ void k_ku(int64_t m, int64_t n_u, const int32_t* __restrict__ krp, co
                      const double* __restrict__ y, double* __restrict__ s) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
         double acc = w[n_u + k];
-        for (int32_t q = krp[k]; q < krp[k + 1]; ++q) acc -= uk_val[src[q]] * y[row[q]];
+        for (int32_t q = krp[k]; q < krp[k + 1]; ++q) {
+            FEMI_DCHECK(row[q] >= 0 && row[q] < n_u && src[q] >= 0, 6);
+            acc -= uk_val[src[q]] * y[row[q]];
+        }
         s[k] = acc;
     }
 }
@@ -438,3 +441,5 @@ femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_
 }
 
 }  // namespace femi
+
+FEMI_DCHECK_READER(dcheck_tonal)

@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfemi.so")
+# FEMI_LIB selects another build of the same library (e.g. libfemi_check.so, the device-
+# bounds-checked build the GPU tests can run under); default: the in-tree libfemi.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("FEMI_LIB", "libfemi.so"))
 
 FEMI_OK = 0
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_DEGENERATE", 3: "E_NO_MASK", 4: "E_NOT_CONVERGED", 5: "E_NONFINITE",
@@ -72,7 +74,7 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
            "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert",
-           "femi_system_solver_path", "femi_apply_B", "femi_apply_BT"]
+           "femi_system_solver_path", "femi_apply_B", "femi_apply_BT", "femi_device_check_failures"]
 
 # femi_system_solver_path values (include/femi.h)
 PATH_NAMES = {0: "none", 1: "resident", 2: "persistent", 3: "graph_sell", 4: "graph_tma", 5: "graph_multi"}
@@ -88,6 +90,7 @@ def lib():
         L.femi_last_error.restype = ctypes.c_char_p
         L.femi_version.restype = ctypes.c_char_p
         L.femi_kernel_launches.restype = ctypes.c_int64
+        L.femi_device_check_failures.restype = ctypes.c_int64
         L.femi_mesh_build.argtypes = [ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int64, P, ctypes.c_int64,
                                       ctypes.POINTER(P)]
         L.femi_mesh_info_get.argtypes = [P, ctypes.POINTER(MeshInfo)]
@@ -112,11 +115,12 @@ def lib():
         L.femi_tonal_optimise_l1.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.c_int32, ctypes.c_double,
                                              ctypes.POINTER(TonalL1Report), P]
         L.femi_system_solver_path.argtypes = [P, I32P]
+        L.femi_device_check_failures.argtypes = [ctypes.POINTER(ctypes.c_int64)]
         L.femi_apply_B.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
         L.femi_apply_BT.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
         for name in SYMBOLS:
             if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
-                            "femi_kernel_launches"):
+                            "femi_kernel_launches", "femi_device_check_failures"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -415,3 +419,11 @@ def apply_BT(system, r, s, inner: CgOpts | None = None, stream=None):
     inner = inner or cg_opts(rtol=1e-12)
     _check(lib().femi_apply_BT(system._h, _dptr(r, torch.float64), _dptr(s, torch.float64), ctypes.byref(inner),
                                _stream(stream)))
+
+
+def device_check_failures():
+    """(count, first failing site) of the device bounds checks since the last call (always
+    (0, 0) unless the library is the checked build, FEMI_LIB=libfemi_check.so)."""
+    site = ctypes.c_int64(0)
+    n = lib().femi_device_check_failures(ctypes.byref(site))
+    return int(n), int(site.value)

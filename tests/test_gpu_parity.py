@@ -56,11 +56,10 @@ def check_inpaint(W, H, f, mk, un, rtol=1e-10):
     assert abs(mse - O["mse"]) <= MSE_RTOL * max(O["mse"], 1e-300) or (O["mse"] == 0 and mse == 0)
     te = R["tri_err"].cpu().numpy()
     # tri_err / best: compared against the oracle's raster of the GPU's own vertex values
-    # (isolates S3/S4 from the solve). best is an arg-max of bit-identical e values (ties:
-    # lowest pix), so it is exact; tri_err sums the same e values in another order (reading
-    # A18): n_t positive terms, so within n_t 2^-53 relative -- 1e-12 covers n_t <= 9000
+    # (isolates S3/S4 from the solve): both sum e in pixel order and take the first strict
+    # maximum, so they are bit-identical
     Og = S.raster(u_vert, f)
-    np.testing.assert_allclose(te, Og["tri_err"], rtol=1e-12, atol=0)
+    np.testing.assert_array_equal(te, Og["tri_err"])
     np.testing.assert_array_equal(R["best"].cpu().numpy(), Og["best"])
     # the raster itself is exact: same vertex values -> bit-identical pixel values and errors
     # (S3's barycentric form in IEEE fp64, one rounding per operation on both sides)
@@ -243,7 +242,7 @@ def test_config3_densify_lockstep():
         Rg = S.raster(u_gpu, f2)  # which match the oracle's raster of the same vertex values
         np.testing.assert_array_equal(e_px, Rg["e_px"])
         np.testing.assert_array_equal(bst, Rg["best"])
-        np.testing.assert_allclose(te, Rg["tri_err"], rtol=1e-12, atol=0)
+        np.testing.assert_array_equal(te, Rg["tri_err"])
         uo = S.solve(f2.reshape(-1)[S.mask_px])[0]
         Ro = S.raster(uo, f2)
         flips.append(a15_flips(r["new"], o["new"], S, Ro, float(np.abs(u_gpu - uo).max())))  # (b)
@@ -402,7 +401,7 @@ def test_colour_shared_mesh(W):
     for k in range(3):
         np.testing.assert_array_equal(upx[k].cpu().numpy(), R["u_px"][k])
     np.testing.assert_array_equal(e_px.cpu().numpy(), R["e_px"])
-    np.testing.assert_allclose(te.cpu().numpy(), R["tri_err"], rtol=1e-12, atol=0)  # order (A18)
+    np.testing.assert_array_equal(te.cpu().numpy(), R["tri_err"])
     np.testing.assert_array_equal(bs.cpu().numpy(), R["best"])
     assert abs(sse.item() - R["sse"]) <= 1e-9 * R["sse"]  # grouped vs sequential fp64 sum of N terms
     b = max(1, int(0.002 * N))
