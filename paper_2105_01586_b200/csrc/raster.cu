@@ -4,15 +4,18 @@
 //
 // Pixel ownership (reading A7: lowest index among the closed triangles containing a
 // pixel) depends only on the mesh, so it is resolved ONCE per mesh at assembly by a
-// warp-cooperative triangle expansion (raster_common.cuh) into the triangle-major lists
-//   tp_ptr[t]   = first entry of triangle t in tp_pix (CSR, ascending triangle)
-//   tp_pix[q]   = cls << 30 | y << 14 | x for the triangle's owned pixels in ascending pix
-//                 order (cls 0: interior/edge pixel, 1..3: the pixel of vertex v[cls-1];
-//                 W, H <= 16384 so x and y take 14 bits each).
-// Every solve then rasterises with ONE triangle-major kernel (k_raster_tri): values, errors,
-// per-triangle error sum and arg-max over non-vertex pixels (ties: lowest pix) by segmented
-// warp scans in pixel order, SSE = fixed-order sum of the triangle sums. Deterministic.
-// The adjoint P^T r is the same traversal with barycentric weights.
+// warp-cooperative triangle expansion (raster_common.cuh) into triangle-major lists
+// (ascending pixels per triangle), which are then merged per group of 16 consecutive
+// canonical triangles into the GROUP LIST the per-solve kernels read:
+//   tp_ptr[t]   = first entry of triangle t (CSR over triangles; groups are contiguous)
+//   tp_pix[q]   = j << 28 | (y - y0) << 14 | x, the group's owned pixels in ascending pixel
+//                 order, j = the owner's slot in the group, y0 = the group's top row
+//                 (W, H <= 16384: 14 bits each).
+// Every solve then rasterises with ONE kernel (k_raster_grp): lanes take consecutive pixels
+// of the group's rows (coalesced f / u / e traffic); per-triangle error sums and arg-max over
+// non-vertex pixels (ties: lowest pix) are segmented warp reductions over runs of one
+// triangle; SSE = fixed-order sum of the group sums. Deterministic. The adjoint P^T r is the
+// same traversal with barycentric weights.
 #include <cstdlib>
 
 #include "raster_common.cuh"
@@ -142,6 +145,8 @@ struct RasterItem {
     const TriRec* tri;
     const int32_t* tp_ptr;
     const uint32_t* tp_pix;
+    const int32_t* wptr;  // windows per group (CSR)
+    const void* win;      // WinRec[]
     const double* u_vert[kMaxCh];  // per channel
     const double* f[kMaxCh];       // per channel; f[0] == nullptr: no error map
     double* u_px[kMaxCh];          // per channel, nullable
@@ -154,48 +159,6 @@ struct RasterItem {
     int32_t pad;
 };
 
-// Warp-cooperative traversal of the triangle-major list: lane l of a warp owns triangle
-// t0+l; list entries ptr[t0] .. ptr[t0+32] are walked 32 at a time (coalesced), each entry
-// tagged with its triangle by a shuffle binary search over the per-triangle offsets.
-struct ListWalk {
-    int excl, total, ptr0;
-};
-__device__ __forceinline__ ListWalk list_begin(const int32_t* __restrict__ tp_ptr, int64_t T, int64_t t0, int& cnt) {
-    const int lane = threadIdx.x & 31;
-    const int64_t t = t0 + lane;
-    const int a = t < T ? tp_ptr[t] : 0;
-    const int b = t < T ? tp_ptr[t + 1] : 0;
-    cnt = b - a;
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    ListWalk lw;
-    lw.excl = incl - cnt;
-    lw.total = __shfl_sync(0xffffffffu, incl, 31);
-    lw.ptr0 = __shfl_sync(0xffffffffu, a, 0);
-    return lw;
-}
-
-// One triangle as the fused raster keeps it in shared memory (one slot per lane): the two
-// exact integer edge functions as planes w = A px + B py + C (S3: w_b = orient(c,a,p),
-// w_c = orient(a,b,p)), D = orient(a,b,c) and its correctly rounded reciprocal, u_a and the
-// differences u_b - u_a, u_c - u_a.
-// 16-byte aligned (size padded to a multiple of 16): the per-entry reads of a slot become
-// 128-bit shared loads (half the LDS instructions and wavefronts of 64-bit ones; the 96-byte
-// stride keeps consecutive slots on disjoint banks)
-template <int NC>
-struct __align__(16) RTri {
-    int A1, B1, C1, A2, B2, C2, pad0, pad1;
-    double D, rD;
-    double db[NC], dc[NC], u[NC][3];
-};
-
-__device__ __forceinline__ int tp_x(uint32_t v) { return (int)(v & 0x3fffu); }
-__device__ __forceinline__ int tp_y(uint32_t v) { return (int)((v >> 14) & 0x3fffu); }
-
 // Correctly rounded w / D for an exact integer w (|w| < 2^53) given rD = RN(1/D): q = RN(w rD)
 // is within 1 ulp of w/D, the remainder w - qD is exact under fma, and RN(q + r rD) is RN(w/D)
 // (Markstein's theorem) -- the IEEE quotient of __ddiv_rn at three fp64 operations.
@@ -205,125 +168,230 @@ __device__ __forceinline__ double div_rn(double w, double D, double rD) {
     return __fma_rn(r, rD, q);
 }
 
-constexpr int RCH = 128;  // list entries per warp chunk (4 x 32 lanes)
+constexpr int GT = 32;    // triangles per group (5-bit slot; lane j of a warp owns triangle j)
+constexpr int RCH = 128;  // entries per raster window (7-bit slot)
 
-// S3+S4 in ONE triangle-major pass. A warp takes 32 consecutive triangles (smem, one slot per
-// lane) and walks their owned pixels (tp_pix: ascending pix per triangle) in chunks of RCH:
-//  phase 1, lane per entry (coalesced list reads, f gathered and u, e written along row
-//   segments): u = the vertex value (vertex pixel) or (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
-//   with l = w / D in IEEE fp64 (S3's barycentric form, one rounding per operation, no
-//   contraction), e = (u - f)^2; e is staged in shared memory;
-//  phase 2, lane per triangle: the lane walks its triangle's entries of the chunk in pixel
-//   order: tri_err += e, best = first strict maximum over non-vertex pixels (ties: lowest
-//   pix) -- the oracle's sequential order, so tri_err and best are bit-identical to it.
-// SSE = sum of per-group partials in group order (k_sse). Deterministic, no atomics on values.
-template <int MINB, int CH, int NC>
-__global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __restrict__ items, double* __restrict__ gpart,
-                                                   uint32_t* __restrict__ next, int64_t gstride) {
-    extern __shared__ __align__(16) unsigned char rsm[];  // RTri<NC> [RWARPS][32] (dynamic: colour > 48 KB)
-    __shared__ double e_s[RWARPS][CH];
-    __shared__ int p_s[RWARPS][CH];  // pix, or -1 for a vertex pixel (not a candidate)
+// Group list as built by k_group_list (64-bit, setup only): (y << 14 | x) << 5 | j
+__device__ __forceinline__ int gk_j(uint64_t v) { return (int)(v & 31u); }
+__device__ __forceinline__ int gk_y(uint64_t v) { return (int)(v >> 19); }
+__device__ __forceinline__ int gl_x(uint32_t v) { return (int)(v & 0x3fffu); }
+// ... and as the raster reads it (one window of <= 128 entries spanning < 64 rows):
+// slot << 25 | j << 20 | (y - y_window) << 14 | x; slot = the entry's position in the window's
+// triangle-major order (triangle j's entries at start[j] .. start[j+1], in pixel order)
+__device__ __forceinline__ int wl_slot(uint32_t v) { return (int)(v >> 25); }
+__device__ __forceinline__ int wl_j(uint32_t v) { return (int)((v >> 20) & 31u); }
+__device__ __forceinline__ int wl_dy(uint32_t v) { return (int)((v >> 14) & 63u); }
+constexpr int kWinRows = 64;  // rows a window may span (6-bit offsets)
+
+struct __align__(16) WinRec {
+    int32_t q0;             // first entry (global index into tp_pix)
+    int16_t y0;             // the window's top row
+    uint8_t n, pad0;        // entries (1..128)
+    uint8_t start[GT + 1];  // triangle-major offsets of the group's triangles in the window
+    uint8_t pad1[7];
+};
+static_assert(sizeof(WinRec) == 48, "WinRec is 48 bytes");
+
+// Per mesh, after k_group_list: split each group's list into windows (greedy: a window ends
+// after 128 entries or before an entry 64 or more rows below its first one). FILL = 0 counts
+// the windows per group; FILL = 1 writes the records and the 32-bit entries. One lane per group
+// walks the list (setup only).
+template <int FILL>
+__global__ void __launch_bounds__(RT) k_win(const TriRec* __restrict__ tri, int64_t T,
+                                            const int32_t* __restrict__ tp_ptr, const uint64_t* __restrict__ gk,
+                                            uint32_t* __restrict__ gl, int32_t* __restrict__ wcnt,
+                                            const int32_t* __restrict__ wptr, WinRec* __restrict__ win) {
+    const int64_t ngroups = (T + GT - 1) / GT;
+    for (int64_t g = blockIdx.x * (int64_t)RT + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * RT) {
+        const int64_t t0 = g * GT;
+        const int nt = (int)min((int64_t)GT, T - t0);
+        const int q0 = tp_ptr[t0], q1 = tp_ptr[t0 + nt];
+        int nw = 0;
+        int64_t w = FILL ? wptr[g] : 0;
+        int q = q0;
+        while (q < q1) {
+            const int ys = gk_y(gk[q]);
+            int e = q + 1;
+            while (e < q1 && e - q < RCH && gk_y(gk[e]) - ys < kWinRows) ++e;
+            if (FILL) {
+                int cnt[GT];
+#pragma unroll
+                for (int k = 0; k < GT; ++k) cnt[k] = 0;
+                for (int k = q; k < e; ++k) {
+                    const int j = gk_j(gk[k]);
+#pragma unroll
+                    for (int jj = 0; jj < GT; ++jj) cnt[jj] += jj == j;
+                }
+                WinRec R = {};
+                R.q0 = q;
+                R.y0 = (int16_t)ys;
+                R.n = (uint8_t)(e - q);
+                int run = 0;
+#pragma unroll
+                for (int k = 0; k < GT; ++k) {
+                    R.start[k] = (uint8_t)run;
+                    run += cnt[k];
+                    cnt[k] = R.start[k];  // running slot per triangle
+                }
+                R.start[GT] = (uint8_t)run;
+                FEMI_DCHECK(w < wptr[g + 1] && run == e - q && run <= RCH, 4);
+                win[w] = R;
+                for (int k = q; k < e; ++k) {
+                    const uint64_t v = gk[k];
+                    const int j = gk_j(v);
+                    int slot = 0;
+#pragma unroll
+                    for (int jj = 0; jj < GT; ++jj)
+                        if (jj == j) slot = cnt[jj]++;
+                    const uint32_t dyw = (uint32_t)(gk_y(v) - ys);
+                    gl[k] = ((uint32_t)slot << 25) | ((uint32_t)j << 20) | (dyw << 14) | ((uint32_t)(v >> 5) & 0x3fffu);
+                }
+                ++w;
+            }
+            ++nw;
+            q = e;
+        }
+        if (!FILL) wcnt[g] = nw;
+    }
+}
+
+// The group's triangles as the raster reads them: structure of arrays in shared memory (lanes
+// of a warp index different triangles -- one bank-conflict-free access per field): the exact
+// integer edge-function planes w = A px + B py + C (S3: w_b = orient(c,a,p), w_c = orient(a,b,p)),
+// D = orient(a,b,c) as int and double, RN(1/D), u_a and the differences u_b - u_a, u_c - u_a,
+// and the vertex values u_b, u_c (vertex pixels take them exactly).
+template <int NC>
+struct GTri {
+    int A1[GT], B1[GT], C1[GT], A2[GT], B2[GT], C2[GT], Di[GT], pad[GT];
+    double D[GT], rD[GT];
+    double ua[NC][GT], db[NC][GT], dc[NC][GT], ub[NC][GT], uc[NC][GT];
+};
+
+// S3+S4 in ONE pass over the raster windows of each 16-triangle group (groups handed out in
+// canonical order by an atomic counter). Per window of <= 128 entries (the group's owned pixels
+// in ascending pixel order: row segments of the group's region, so consecutive lanes read f
+// and write u, e at consecutive pixels -- coalesced):
+//   lane per entry: u = the vertex value (vertex pixel: both barycentric numerators 0 or one
+//   of them == D, exact integers) or (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a) with l = w / D
+//   in IEEE fp64 (S3's form, one rounding per operation, no contraction); e = (u - f)^2, staged
+//   in shared memory at the entry's precomputed triangle-major slot;
+//   lane j < 16: walks triangle j's slots start[j] .. start[j+1] (its entries of the window in
+//   pixel order): tri_err += e, best = first strict maximum over non-vertex pixels.
+// Windows are in pixel order, so every triangle is summed in the oracle's sequential order:
+// u_px, e_px, tri_err and best are bit-identical to it. SSE = per-group sums in group order.
+template <int MINB, int NC>
+__global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __restrict__ items,
+                                                         double* __restrict__ gpart, uint32_t* __restrict__ next,
+                                                         int64_t gstride) {
+    extern __shared__ __align__(16) unsigned char rsm[];  // GTri<NC> [RWARPS]
+    __shared__ double e_s[RWARPS][RCH];                   // staged e (sign bit set: vertex pixel)
+    __shared__ int p_s[RWARPS][RCH];                      // staged pix
     const RasterItem& it = items[blockIdx.y];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t T = it.T;
     const int W = it.W;
     const bool hasf = it.f[0] != nullptr;
     double* __restrict__ e_px = it.e_px;
-    const uint32_t* __restrict__ tp_pix = it.tp_pix;
-    const int64_t ngroups = (T + 31) / 32;
-    RTri<NC>* ws = (RTri<NC>*)rsm + 32 * wid;
+    const uint32_t* __restrict__ gl = it.tp_pix;
+    const WinRec* __restrict__ win = (const WinRec*)it.win;
+    const int64_t ngroups = (T + GT - 1) / GT;
+    GTri<NC>& G = ((GTri<NC>*)rsm)[wid];
     double* __restrict__ gp = gpart + gstride * blockIdx.y;
     double* es = e_s[wid];
     int* ps = p_s[wid];
-    // groups of 32 triangles are handed out in canonical order by an atomic counter: the warps
-    // in flight cover one narrow band of rows, so the f/u/e sectors they share are completed
-    // in L2 before eviction (no partial-sector write-backs)
     for (;;) {
         int64_t g = 0;
         if (lane == 0) g = (int64_t)atomicAdd(next + blockIdx.y, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= ngroups) break;
-        const int64_t t0 = g * 32;
-        int cnt;
-        const ListWalk lw = list_begin(it.tp_ptr, T, t0, cnt);
-        if (t0 + lane < T) {
+        const int64_t t0 = g * GT;
+        const int nt = (int)min((int64_t)GT, T - t0);
+        const int w0 = it.wptr[g], w1 = it.wptr[g + 1];
+        if (lane < nt) {
             const TriRec R = it.tri[t0 + lane];
             const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-            RTri<NC> I;
-            // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx)
-            I.A1 = cy - ay;
-            I.B1 = ax - cx;
-            I.C1 = (ay - cy) * cx - (ax - cx) * cy;
-            // w_c = orient(a,b,p) = (bx-ax)(py-ay) - (by-ay)(px-ax)
-            I.A2 = ay - by;
-            I.B2 = bx - ax;
-            I.C2 = (by - ay) * ax - (bx - ax) * ay;
-            I.D = (double)orient_xy(ax, ay, bx, by, cx, cy);
-            I.rD = __drcp_rn(I.D);
+            G.A1[lane] = cy - ay;  // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx)
+            G.B1[lane] = ax - cx;
+            G.C1[lane] = (ay - cy) * cx - (ax - cx) * cy;
+            G.A2[lane] = ay - by;  // w_c = orient(a,b,p) = (bx-ax)(py-ay) - (by-ay)(px-ax)
+            G.B2[lane] = bx - ax;
+            G.C2[lane] = (by - ay) * ax - (bx - ax) * ay;
+            const int Di = orient_xy(ax, ay, bx, by, cx, cy);
+            G.Di[lane] = Di;
+            G.D[lane] = (double)Di;
+            G.rD[lane] = __drcp_rn((double)Di);
 #pragma unroll
             for (int ch = 0; ch < NC; ++ch) {
-                I.u[ch][0] = it.u_vert[ch][R.v[0]];
-                I.u[ch][1] = it.u_vert[ch][R.v[1]];
-                I.u[ch][2] = it.u_vert[ch][R.v[2]];
-                I.db[ch] = __dsub_rn(I.u[ch][1], I.u[ch][0]);
-                I.dc[ch] = __dsub_rn(I.u[ch][2], I.u[ch][0]);
+                const double u0 = it.u_vert[ch][R.v[0]], u1 = it.u_vert[ch][R.v[1]], u2 = it.u_vert[ch][R.v[2]];
+                G.ua[ch][lane] = u0;
+                G.ub[ch][lane] = u1;
+                G.uc[ch][lane] = u2;
+                G.db[ch][lane] = __dsub_rn(u1, u0);
+                G.dc[ch][lane] = __dsub_rn(u2, u0);
             }
-            ws[lane] = I;
         }
-        __syncwarp();
-        double acc = 0.0, be = -1.0;
+        double acc = 0.0, be = -1.0;  // lane j < nt: triangle j's running sum / best e
         int bp = -1;
-        const int my0 = lw.excl, my1 = lw.excl + cnt;
-        // list entries of the next 128-entry block are loaded one block ahead (their latency
-        // overlaps the current block's f gathers and arithmetic)
+        __syncwarp();
+        // window w's record and entries are loaded one window ahead
+        int nq0 = 0, ny0 = 0, nn = 0, ns0 = 0, ns1 = 0;
         uint32_t vn[RCH / 32];
-#pragma unroll
-        for (int h = 0; h < RCH / 32; ++h) {
-            const int k = 32 * h + lane;
-            vn[h] = k < lw.total ? tp_pix[lw.ptr0 + k] : 0u;
-        }
-        for (int c0 = 0; c0 < lw.total; c0 += CH) {
-          // ---- phase 1: lane per entry, 128 entries at a time (loads in flight together)
-          for (int c1 = c0; c1 < min(lw.total, c0 + CH); c1 += RCH) {
-            uint32_t v[RCH / 32];
-            int j[RCH / 32];
-            double fv[RCH / 32][NC];
+        auto load_win = [&](int w) {
+            const WinRec& R = win[w];
+            nq0 = R.q0;
+            ny0 = R.y0;
+            nn = R.n;
+            if (lane < nt) {
+                ns0 = R.start[lane];
+                ns1 = R.start[lane + 1];
+            }
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
-                const int k = c1 + 32 * h + lane;
-                j[h] = warp_find(lw.excl, k, lw.total);
-                v[h] = vn[h];
-                const int kn = k + RCH;
-                vn[h] = kn < lw.total ? tp_pix[lw.ptr0 + kn] : 0u;
+                const int k = 32 * h + lane;
+                vn[h] = k < nn ? gl[nq0 + k] : 0xffffffffu;
             }
+        };
+        if (w0 < w1) load_win(w0);
+        for (int w = w0; w < w1; ++w) {
+            uint32_t v[RCH / 32];
+            const int y0 = ny0, s0 = ns0, s1 = ns1;
+#pragma unroll
+            for (int h = 0; h < RCH / 32; ++h) v[h] = vn[h];
+            if (w + 1 < w1) load_win(w + 1);
+            double fv[RCH / 32][NC];
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h)
 #pragma unroll
                 for (int ch = 0; ch < NC; ++ch)
-                    fv[h][ch] = (hasf && j[h] < 32) ? it.f[ch][(int64_t)tp_y(v[h]) * W + tp_x(v[h])] : 0.0;
+                    fv[h][ch] = (hasf && v[h] != 0xffffffffu)
+                                    ? __ldg(it.f[ch] + (int64_t)(y0 + wl_dy(v[h])) * W + gl_x(v[h]))
+                                    : 0.0;
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
-                if (j[h] >= 32) continue;
-                const int px = tp_x(v[h]), py = tp_y(v[h]);
+                if (v[h] == 0xffffffffu) continue;
+                const int j = wl_j(v[h]);
+                const int px = gl_x(v[h]), py = y0 + wl_dy(v[h]);
                 const int pix = py * W + px;
-                const uint32_t cls = v[h] >> 30;
-                const RTri<NC>& I = ws[j[h]];
+                FEMI_DCHECK(j < nt && px < W && (int64_t)pix < it.N && wl_slot(v[h]) < RCH, 4);
+                const int w1v = G.A1[j] * px + G.B1[j] * py + G.C1[j];
+                const int w2v = G.A2[j] * px + G.B2[j] * py + G.C2[j];
+                const int Di = G.Di[j];
+                // vertex pixels: a (w_b = w_c = 0), b (w_b = D, w_c = 0), c (w_b = 0, w_c = D)
+                const int cls = (w1v == 0) ? (w2v == 0 ? 1 : (w2v == Di ? 3 : 0)) : ((w1v == Di && w2v == 0) ? 2 : 0);
                 double lb = 0.0, lc = 0.0;
                 if (!cls) {
-                    // S3 as the paper's barycentric form, IEEE round-to-nearest per operation
-                    // and no contraction: l_b = w_b / D, l_c = w_c / D (shared by the channels),
-                    // u = (u_a + l_b (u_b - u_a)) + l_c (u_c - u_a)
-                    const int w1 = I.A1 * px + I.B1 * py + I.C1;
-                    const int w2 = I.A2 * px + I.B2 * py + I.C2;
-                    lb = div_rn((double)w1, I.D, I.rD);
-                    lc = div_rn((double)w2, I.D, I.rD);
+                    const double D = G.D[j], rD = G.rD[j];
+                    lb = div_rn((double)w1v, D, rD);
+                    lc = div_rn((double)w2v, D, rD);
                 }
                 double e = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NC; ++ch) {
-                    const double u = cls ? I.u[ch][cls - 1]
-                                         : __dadd_rn(__dadd_rn(I.u[ch][0], __dmul_rn(lb, I.db[ch])),
-                                                     __dmul_rn(lc, I.dc[ch]));
+                    double u;
+                    if (cls == 0)
+                        u = __dadd_rn(__dadd_rn(G.ua[ch][j], __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
+                    else
+                        u = cls == 1 ? G.ua[ch][j] : (cls == 2 ? G.ub[ch][j] : G.uc[ch][j]);
                     if (it.u_px[ch]) it.u_px[ch][pix] = u;
                     if (hasf) {
                         const double d = __dsub_rn(u, fv[h][ch]);
@@ -332,39 +400,34 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_tri(const RasterItem* __res
                 }
                 if (hasf) {
                     if (e_px) e_px[pix] = e;
-                    // vertex pixels (not arg-max candidates) staged with the sign bit set (-e,
-                    // -0.0 for e = 0); phase 2 adds |e| -- the same value
-                    es[c1 - c0 + 32 * h + lane] = cls ? -e : e;
-                    ps[c1 - c0 + 32 * h + lane] = pix;
+                    const int sl = wl_slot(v[h]);
+                    es[sl] = cls ? -e : e;  // -0.0 for e = 0: the sign bit is the flag
+                    ps[sl] = pix;
                 }
             }
-          }
             __syncwarp();
-            // ---- phase 2: lane per triangle, pixel order
-            if (hasf) {
-                const int lo = max(my0, c0), hi = min(my1, c0 + CH);
-                int bk = -1;
-                for (int k = lo; k < hi; ++k) {
-                    const double es_k = es[k - c0];
-                    const double e = fabs(es_k);
+            if (hasf && lane < nt) {
+                for (int k = s0; k < s1; ++k) {
+                    const double x = es[k];
+                    const double e = fabs(x);
                     acc = __dadd_rn(acc, e);
-                    if (__double_as_longlong(es_k) >= 0 && e > be) {
+                    if (__double_as_longlong(x) >= 0 && e > be) {
                         be = e;
-                        bk = k;
+                        bp = ps[k];
                     }
                 }
-                if (bk >= 0) bp = ps[bk - c0];
             }
             __syncwarp();
         }
-        if (t0 + lane < T && hasf) {
-            if (it.tri_err) it.tri_err[t0 + lane] = acc;
-            if (it.best) it.best[t0 + lane] = bp;
-        }
-        if (hasf) {  // group partial of the SSE (fixed tree order); summed in group order by k_sse
-            const double gs = warp_sum(t0 + lane < T ? acc : 0.0);
+        if (hasf) {
+            if (lane < nt) {
+                if (it.tri_err) it.tri_err[t0 + lane] = acc;
+                if (it.best) it.best[t0 + lane] = bp;
+            }
+            const double gs = warp_sum(lane < nt ? acc : 0.0);  // group partial of the SSE (fixed order)
             if (lane == 0) gp[g] = gs;
         }
+        __syncwarp();
     }
 }
 
@@ -375,7 +438,7 @@ __global__ void __launch_bounds__(RT) k_sse(const RasterItem* __restrict__ items
     __shared__ int flag;
     const RasterItem& it = items[blockIdx.y];
     if (!it.sse || !it.f[0]) return;
-    const int64_t ng = (it.T + 31) / 32;
+    const int64_t ng = (it.T + GT - 1) / GT;
     const int64_t a = ng * blockIdx.x / gridDim.x, b = ng * (blockIdx.x + 1) / gridDim.x;
     const double* gp = gpart + gstride * blockIdx.y;
     double s = 0.0;
@@ -401,86 +464,115 @@ __global__ void __launch_bounds__(RT) k_sse(const RasterItem* __restrict__ items
     }
 }
 
-// P^T r: per triangle, sum over its owned pixels of (l_a, l_b, l_c) r (vertex pixels:
-// weight 1 on that vertex) -> tri_w[3t+k]; the vertex gather happens in tonal.cu.
-__global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ tri, const int32_t* __restrict__ tp_ptr,
-                                                    const uint32_t* __restrict__ tp_pix, int64_t T, int W,
-                                                    const double* __restrict__ r, double* __restrict__ tri_w) {
-    __shared__ double acc_s[RWARPS][32][3];
-    __shared__ WTri tris[RWARPS][32];
-    __shared__ double rd_s[RWARPS][32];  // RN(1/D): w / D as a correctly rounded 3-op quotient
+// P^T r over the raster windows: per triangle, the sum over its owned pixels of
+// (l_a, l_b, l_c) r (vertex pixels: weight 1 on that vertex) -> tri_w[3t+k]. Staged at the
+// entries' triangle-major slots and summed per triangle in pixel order (deterministic). The
+// vertex gather happens in tonal.cu.
+__global__ void __launch_bounds__(RT) k_tri_adjoint(const TriRec* __restrict__ tri, const int32_t* __restrict__ wptr,
+                                                    const WinRec* __restrict__ win, const uint32_t* __restrict__ gl,
+                                                    int64_t T, int W, const double* __restrict__ r,
+                                                    double* __restrict__ tri_w) {
+    __shared__ int4 tg_s[RWARPS][GT];      // (A1, B1, C1, D) of w_b
+    __shared__ int4 tc_s[RWARPS][GT];      // (A2, B2, C2, -)
+    __shared__ double rd_s[RWARPS][GT];    // RN(1/D)
+    __shared__ double st_s[RWARPS][3][RCH];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t ngroups = (T + 31) / 32;
+    const int64_t ngroups = (T + GT - 1) / GT;
     const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
-    WTri* ws = tris[wid];
     for (int64_t g = gwarp; g < ngroups; g += nwarps) {
-        const int64_t t0 = g * 32;
-        int cnt;
-        const ListWalk lw = list_begin(tp_ptr, T, t0, cnt);
-        if (t0 + lane < T) {
+        const int64_t t0 = g * GT;
+        const int nt = (int)min((int64_t)GT, T - t0);
+        if (lane < nt) {
             const TriRec R = tri[t0 + lane];
-            WTri I;
-            I.ax = R.x[0];
-            I.ay = R.y[0];
-            I.bx = R.x[1];
-            I.by = R.y[1];
-            I.cx = R.x[2];
-            I.cy = R.y[2];
-            I.D = orient_xy(I.ax, I.ay, I.bx, I.by, I.cx, I.cy);
-            ws[lane] = I;
-            rd_s[wid][lane] = __drcp_rn((double)I.D);
+            const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
+            const int D = orient_xy(ax, ay, bx, by, cx, cy);
+            tg_s[wid][lane] = make_int4(cy - ay, ax - cx, (ay - cy) * cx - (ax - cx) * cy, D);
+            tc_s[wid][lane] = make_int4(ay - by, bx - ax, (by - ay) * ax - (bx - ax) * ay, 0);
+            rd_s[wid][lane] = __drcp_rn((double)D);
         }
-        acc_s[wid][lane][0] = 0.0;
-        acc_s[wid][lane][1] = 0.0;
-        acc_s[wid][lane][2] = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
         __syncwarp();
-        for (int base = 0; base < lw.total; base += 32) {
-            const int k = base + lane;
-            const int j = warp_find(lw.excl, k, lw.total);
-            double sa = 0.0, sb = 0.0, sc = 0.0;
-            if (j < 32) {
-                const uint32_t v = tp_pix[lw.ptr0 + k];
-                const int px = (int)(v & 0x3fffu), py = (int)((v >> 14) & 0x3fffu);
+        for (int w = wptr[g]; w < wptr[g + 1]; ++w) {
+            const WinRec& R = win[w];
+            const int q0 = R.q0, y0 = R.y0, n = R.n;
+            for (int k = lane; k < n; k += 32) {
+                const uint32_t v = gl[q0 + k];
+                const int j = wl_j(v), sl = wl_slot(v);
+                const int px = gl_x(v), py = y0 + wl_dy(v);
+                FEMI_DCHECK(j < nt && sl < n && px < W && (int64_t)py * W + px < (int64_t)W * 16384, 4);
                 const double rv = r[(int64_t)py * W + px];
-                const uint32_t cls = v >> 30;
-                if (cls) {
-                    if (cls == 1) sa = rv;
-                    else if (cls == 2) sb = rv;
-                    else sc = rv;
+                const int4 P1 = tg_s[wid][j], P2 = tc_s[wid][j];
+                const int w1 = P1.x * px + P1.y * py + P1.z;  // w_b
+                const int w2 = P2.x * px + P2.y * py + P2.z;  // w_c
+                const int D = P1.w;
+                double sa = 0.0, sb = 0.0, sc = 0.0;
+                if (w1 == 0 && w2 == 0) {
+                    sa = rv;
+                } else if (w1 == D && w2 == 0) {
+                    sb = rv;
+                } else if (w2 == D && w1 == 0) {
+                    sc = rv;
                 } else {
-                    const WTri& I = ws[j];
-                    const double D = (double)I.D, rD = rd_s[wid][j];
-                    // div_rn == the IEEE quotient (Markstein), so the sums are unchanged
-                    sa = div_rn((double)orient_xy(I.bx, I.by, I.cx, I.cy, px, py), D, rD) * rv;
-                    sb = div_rn((double)orient_xy(I.cx, I.cy, I.ax, I.ay, px, py), D, rD) * rv;
-                    sc = div_rn((double)orient_xy(I.ax, I.ay, I.bx, I.by, px, py), D, rD) * rv;
+                    const double Dd = (double)D, rD = rd_s[wid][j];
+                    sa = div_rn((double)(D - w1 - w2), Dd, rD) * rv;  // w_a = D - w_b - w_c exactly
+                    sb = div_rn((double)w1, Dd, rD) * rv;
+                    sc = div_rn((double)w2, Dd, rD) * rv;
                 }
-            }
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double ao = __shfl_up_sync(0xffffffffu, sa, o);
-                const double bo = __shfl_up_sync(0xffffffffu, sb, o);
-                const double co = __shfl_up_sync(0xffffffffu, sc, o);
-                const int jo = __shfl_up_sync(0xffffffffu, j, o);
-                if (lane >= o && jo == j) {
-                    sa += ao;
-                    sb += bo;
-                    sc += co;
-                }
-            }
-            const int jn = __shfl_down_sync(0xffffffffu, j, 1);
-            if (j < 32 && (lane == 31 || jn != j)) {
-                acc_s[wid][j][0] += sa;
-                acc_s[wid][j][1] += sb;
-                acc_s[wid][j][2] += sc;
+                st_s[wid][0][sl] = sa;
+                st_s[wid][1][sl] = sb;
+                st_s[wid][2][sl] = sc;
             }
             __syncwarp();
+            if (lane < nt)
+                for (int k = R.start[lane]; k < R.start[lane + 1]; ++k) {
+                    a0 += st_s[wid][0][k];
+                    a1 += st_s[wid][1][k];
+                    a2 += st_s[wid][2][k];
+                }
+            __syncwarp();
+        }
+        if (lane < nt) {
+            tri_w[3 * (t0 + lane)] = a0;
+            tri_w[3 * (t0 + lane) + 1] = a1;
+            tri_w[3 * (t0 + lane) + 2] = a2;
         }
         __syncwarp();
-        if (t0 + lane < T) {
-            tri_w[3 * (t0 + lane)] = acc_s[wid][lane][0];
-            tri_w[3 * (t0 + lane) + 1] = acc_s[wid][lane][1];
-            tri_w[3 * (t0 + lane) + 2] = acc_s[wid][lane][2];
+    }
+}
+
+// Group list from the triangle-major lists (per mesh): the entries of GT consecutive triangles
+// merged into ascending pixel order (rank = number of the group's entries with a smaller pixel,
+// one lower_bound per triangle list), tagged with the triangle slot: (y << 14 | x) << 5 | j,
+// written to `out` at the same offsets (the group's entries are contiguous).
+__global__ void __launch_bounds__(RT) k_group_list(int64_t T, const int32_t* __restrict__ tp_ptr,
+                                                   const uint32_t* __restrict__ tp_pix, uint64_t* __restrict__ out) {
+    __shared__ int off_s[RWARPS][GT + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ngroups = (T + GT - 1) / GT;
+    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    int* off = off_s[wid];
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+        const int64_t t0 = g * GT;
+        const int nt = (int)min((int64_t)GT, T - t0);
+        if (lane < nt) off[lane] = tp_ptr[t0 + lane];  // the group's offsets
+        if (lane == 0) off[nt] = tp_ptr[t0 + nt];
+        __syncwarp();
+        const int q0 = off[0], q1 = off[nt];
+        for (int q = q0 + lane; q < q1; q += 32) {
+            const uint32_t key = tp_pix[q] & 0x0fffffffu;  // y << 14 | x: pixel order
+            int rank = 0, j = 0;
+            for (int jj = 0; jj < nt; ++jj) {
+                int a = off[jj], b = off[jj + 1];
+                if (q >= a && q < b) j = jj;
+                while (a < b) {  // lower_bound of key in triangle jj's ascending list
+                    const int mid = (a + b) >> 1;
+                    if ((tp_pix[mid] & 0x0fffffffu) < key) a = mid + 1;
+                    else b = mid;
+                }
+                rank += a - off[jj];
+            }
+            FEMI_DCHECK(q0 + rank < q1, 4);
+            out[q0 + rank] = ((uint64_t)key << 5) | (uint64_t)j;
         }
         __syncwarp();
     }
@@ -494,25 +586,52 @@ int warp_grid(int64_t T, int B) {
 
 }  // namespace
 
+// Per mesh: the triangle-major lists (owned-pixel counts, scan, ascending-pixel lists), merged
+// per group of GT triangles into ascending pixel order, cut into raster windows and encoded
+// into S->tp_pix (S->tp_ptr keeps the per-triangle offsets; its values at multiples of GT
+// delimit the groups; S->tp_wptr / tp_win index the windows).
 femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     const int64_t T = S->T, N = (int64_t)S->W * S->H;
     if (T == 0) return FEMI_OK;
     const int nb = (int)((T + SCB - 1) / SCB);
     int32_t* cnt = nullptr;
     int32_t* bsum = nullptr;
+    uint32_t* tmp = nullptr;
+    uint64_t* gk = nullptr;
     FEMI_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * T, st));
     FEMI_CUDA(cudaMallocAsync(&bsum, sizeof(int32_t) * (nb + 1), st));
+    FEMI_CUDA(cudaMallocAsync(&tmp, sizeof(uint32_t) * N, st));
+    FEMI_CUDA(cudaMallocAsync(&gk, sizeof(uint64_t) * N, st));
     const int g = warp_grid(T, 1);
     k_build_owner<0><<<g, RT, 0, st>>>(S->tri, T, S->W, cnt, nullptr, nullptr);
     k_scan_blocks<<<nb, SCB, 0, st>>>(T, cnt, bsum);
     k_scan_bsum<<<1, 32, 0, st>>>(nb, bsum);
     k_scan_apply<<<nb, SCB, 0, st>>>(T, cnt, bsum, S->tp_ptr);
-    k_build_owner<1><<<g, RT, 0, st>>>(S->tri, T, S->W, nullptr, S->tp_ptr, S->tp_pix);
-    count_launches(5);
+    k_build_owner<1><<<g, RT, 0, st>>>(S->tri, T, S->W, nullptr, S->tp_ptr, tmp);
+    k_group_list<<<warp_grid(T, 1), RT, 0, st>>>(T, S->tp_ptr, tmp, gk);
+    // raster windows: count per group, scan, allocate, fill (entries re-encoded in place)
+    const int64_t ngroups = (T + GT - 1) / GT;
+    const int nbg = (int)((ngroups + SCB - 1) / SCB);
+    FEMI_CUDA(cudaMalloc(&S->tp_wptr, sizeof(int32_t) * (ngroups + 1)));  // freed with the system
+    S->allocs.push_back(S->tp_wptr);
+    const int gw = (int)std::min<int64_t>((ngroups + RT - 1) / RT, 148 * 8);
+    k_win<0><<<gw, RT, 0, st>>>(S->tri, T, S->tp_ptr, gk, nullptr, cnt, nullptr, nullptr);
+    k_scan_blocks<<<nbg, SCB, 0, st>>>(ngroups, cnt, bsum);
+    k_scan_bsum<<<1, 32, 0, st>>>(nbg, bsum);
+    k_scan_apply<<<nbg, SCB, 0, st>>>(ngroups, cnt, bsum, S->tp_wptr);
+    int32_t nwin = 0;
+    FEMI_CUDA(cudaMemcpyAsync(&nwin, S->tp_wptr + ngroups, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FEMI_CUDA(cudaStreamSynchronize(st));
+    S->tp_nwin = nwin;
+    FEMI_CUDA(cudaMalloc(&S->tp_win, sizeof(WinRec) * std::max<int64_t>(nwin, 1)));
+    S->allocs.push_back(S->tp_win);
+    k_win<1><<<gw, RT, 0, st>>>(S->tri, T, S->tp_ptr, gk, S->tp_pix, nullptr, S->tp_wptr, (WinRec*)S->tp_win);
+    count_launches(11);
     FEMI_CUDA(cudaGetLastError());
     FEMI_CUDA(cudaFreeAsync(cnt, st));
     FEMI_CUDA(cudaFreeAsync(bsum, st));
-    (void)N;
+    FEMI_CUDA(cudaFreeAsync(tmp, st));
+    FEMI_CUDA(cudaFreeAsync(gk, st));
     return FEMI_OK;
 }
 
@@ -529,13 +648,13 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
         int dev = 0, nsm = 0, per = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_raster_tri<4, 256, 1>, RT,
-                                                                RWARPS * 32 * sizeof(RTri<1>)));
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_raster_grp<4, 1>, RT,
+                                                                RWARPS * sizeof(GTri<1>)));
         resident = std::max(1, per) * nsm;
     }
-    // one wave of resident CTAs (colour: 2 CTAs/SM); 32-triangle groups handed out dynamically
+    // one wave of resident CTAs (colour: 2 CTAs/SM); 16-triangle groups handed out dynamically
     // in canonical order
-    const int64_t groups = (Tmax + 31) / 32;
+    const int64_t groups = (Tmax + GT - 1) / GT;
     const int res = nc == 1 ? resident : resident / 2;
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((groups + RWARPS - 1) / RWARPS,
                                                               (int64_t)std::max(1, res / B)));
@@ -556,25 +675,27 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
     const dim3 gr(gx, B);
     static bool attr = false;
-    if (!attr) {
-        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_tri<2, 128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(RWARPS * 32 * sizeof(RTri<3>))));
-        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_tri<2, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(RWARPS * 32 * sizeof(RTri<4>))));
+    if (!attr) {  // colour: the per-warp triangle tables exceed the default 48 KB
+        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(RWARPS * sizeof(GTri<2>))));
+        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(RWARPS * sizeof(GTri<3>))));
+        FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(RWARPS * sizeof(GTri<4>))));
         attr = true;
     }
     switch (nc) {
         case 1:
-            k_raster_tri<4, 256, 1><<<gr, RT, RWARPS * 32 * sizeof(RTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
+            k_raster_grp<4, 1><<<gr, RT, RWARPS * sizeof(GTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
             break;
         case 2:
-            k_raster_tri<2, 128, 2><<<gr, RT, RWARPS * 32 * sizeof(RTri<2>), st>>>(d_items, d_gpart, d_cnt, groups);
+            k_raster_grp<2, 2><<<gr, RT, RWARPS * sizeof(GTri<2>), st>>>(d_items, d_gpart, d_cnt, groups);
             break;
         case 3:
-            k_raster_tri<2, 128, 3><<<gr, RT, RWARPS * 32 * sizeof(RTri<3>), st>>>(d_items, d_gpart, d_cnt, groups);
+            k_raster_grp<2, 3><<<gr, RT, RWARPS * sizeof(GTri<3>), st>>>(d_items, d_gpart, d_cnt, groups);
             break;
         default:
-            k_raster_tri<2, 128, 4><<<gr, RT, RWARPS * 32 * sizeof(RTri<4>), st>>>(d_items, d_gpart, d_cnt, groups);
+            k_raster_grp<2, 4><<<gr, RT, RWARPS * sizeof(GTri<4>), st>>>(d_items, d_gpart, d_cnt, groups);
             break;
     }
     k_sse<<<dim3(SSEB, B), RT, 0, st>>>(d_items, d_gpart, groups, d_part, d_cnt + B);
@@ -589,6 +710,8 @@ RasterItem raster_item(const femi_system_s* S) {
     r.tri = S->tri;
     r.tp_ptr = S->tp_ptr;
     r.tp_pix = S->tp_pix;
+    r.wptr = S->tp_wptr;
+    r.win = S->tp_win;
     r.T = S->T;
     r.N = (int64_t)S->W * S->H;
     r.W = S->W;
@@ -637,10 +760,13 @@ femi_status launch_raster_channels(femi_system_s* S, int nc, const double* const
 
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st) {
     if (S->T == 0) return FEMI_OK;
-    k_tri_adjoint<<<warp_grid(S->T, 1), RT, 0, st>>>(S->tri, S->tp_ptr, S->tp_pix, S->T, S->W, r, tri_w);
+    k_tri_adjoint<<<warp_grid(S->T, 1), RT, 0, st>>>(S->tri, S->tp_wptr, (const WinRec*)S->tp_win, S->tp_pix, S->T,
+                                                      S->W, r, tri_w);
     count_launches(1);
     FEMI_CUDA(cudaGetLastError());
     return FEMI_OK;
 }
 
 }  // namespace femi
+
+FEMI_DCHECK_READER(dcheck_raster)
