@@ -287,6 +287,17 @@ typedef struct {
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                 femi_tonal_report* report, femi_stream stream);
 
+/* Colour tonal optimisation ("Extending the method to
+ * colour images is straightforward", reading R4): C channels on one mesh are C independent
+ * least-squares problems (B acts on each channel; the colour error is the channel sum), each
+ * solved exactly as femi_tonal_optimise. They run in lockstep: every inner solve is one batched
+ * shared-matrix solve of the active channels, and a converged channel leaves the batch.
+ *   C in 1..4; f[C], g[C]: HOST arrays of DEVICE pointers (f_c: W*H; g_c: n_mask, in/out).
+ *   reports[C]: HOST, one report per channel. Synchronises `stream`.
+ * Errors: as femi_tonal_optimise. */
+femi_status femi_tonal_optimise_channels(femi_system sys, int32_t C, const double* const* f, double* const* g,
+                                         const femi_tonal_opts* opts, femi_tonal_report* reports, femi_stream stream);
+
 /* ---------------------------------------------------------------------------------
  * L1 tonal optimisation (DEVICE + host report). PAPER.md:L524-526:
  * "we have ... optimised the L1 error instead of the L2 one"; the paper does not give the

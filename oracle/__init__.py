@@ -17,6 +17,7 @@ Parity status per function:
   raster_channels (colour) ......... pinned (C = 1 equals raster; channel sum of per-channel maps)
   select ........................... pinned (P16, brute-force re-derivation on tiny cases)
   tonal ............................ pinned (P13 dense lstsq, P14, P15)
+  tonal_channels (colour) .......... pinned (joint block-diagonal dense lstsq equals the per-channel solutions)
   tonal_weighted / tonal_l1 (IRLS) . pinned (unit weights = tonal bit for bit; weighted dense lstsq;
                                      uniform weights = L2 solution; L1 error <= the L2 solution's)
 """
@@ -281,6 +282,14 @@ def tonal_l1(S, f, irls: int = 3, eps: float = 1.0, g0=None, outer_tol: float = 
     st = lib().orc_sys_tonal_l1(S._h, f, g, irls, eps, outer_tol, outer_max, inner_rtol, rep)
     return g, dict(outer_iters=int(rep[0]), inner_solves=int(rep[1]), inner_iters=int(rep[2]), l1_before=rep[3],
                    l1_after=rep[4], mse_after=rep[5], status=int(st))
+
+
+def tonal_channels(S, f_list, **kw):
+    """Colour tonal optimisation (reading R4): the channels share the mesh
+    and B acts on each channel alone, so the colour least-squares problem min sum_c ||B g_c -
+    f_c||^2 separates into one tonal problem per channel. Returns ([g_c], [report_c])."""
+    out = [S.tonal(f, **kw) for f in f_list]
+    return [g for g, _ in out], [r for _, r in out]
 
 
 def select(tri_err, best, e_px, is_vertex, b: int) -> np.ndarray:

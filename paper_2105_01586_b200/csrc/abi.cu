@@ -820,6 +820,29 @@ femi_status femi_apply_BT(femi_system sys, const double* r, double* s_out, const
     return tonal_apply(sys, 1, r, s_out, *opts, (cudaStream_t)stream);
 }
 
+femi_status femi_tonal_optimise_channels(femi_system sys, int32_t C, const double* const* f, double* const* g,
+                                         const femi_tonal_opts* opts, femi_tonal_report* reports, femi_stream stream) {
+    if (!sys || C < 1 || C > 4 || !f || !g || !opts || !reports) {
+        set_error("tonal_optimise_channels: NULL argument or C outside 1..4");
+        return FEMI_E_ARG;
+    }
+    for (int c = 0; c < C; ++c)
+        if (!f[c] || !g[c]) {
+            set_error("tonal_optimise_channels: NULL channel pointer");
+            return FEMI_E_ARG;
+        }
+    if (!(opts->outer_rtol > 0.0) || opts->outer_max < 0 || !(opts->inner.rtol > 0.0) || opts->inner.max_iter <= 0 ||
+        opts->inner.precond != 1 || opts->inner.check_every != 0 || opts->warm_start != 0) {
+        set_error("tonal_optimise_channels: invalid options");
+        return FEMI_E_ARG;
+    }
+    femi_status s = check_device();
+    if (s) return s;
+    std::memset(reports, 0, sizeof(femi_tonal_report) * C);
+    if (sys->n_u == 0) return FEMI_OK;
+    return tonal_cgls_channels(sys, C, f, g, *opts, reports, (cudaStream_t)stream);
+}
+
 femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                 femi_tonal_report* report, femi_stream stream) {
     if (!sys || !f || !g || !opts || !report) {

@@ -253,6 +253,8 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
 // u_px = B g (mode 0) or s = B^T r (mode 1) with inner solves at opts (tonal.cu)
 femi_status tonal_apply(femi_system_s* S, int mode, const double* in, double* out, const femi_cg_opts& o,
                         cudaStream_t st);
+femi_status tonal_cgls_channels(femi_system_s* S, int C, const double* const* f, double* const* g,
+                                const femi_tonal_opts& o, femi_tonal_report* rep, cudaStream_t st);
 femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o, int irls, double eps,
                        femi_tonal_l1_report* rep, cudaStream_t st);
 

@@ -333,6 +333,236 @@ out:
     return tn.status;
 }
 
+namespace {
+
+// y += a x with a host scalar (the colour loop forms alpha / beta on the host from the
+// synchronised per-channel dots: the same IEEE quotients as k_axpy_q / k_xpby)
+__global__ void k_axpy_h(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fma(a, x[i], y[i]);
+}
+
+}  // namespace
+
+// Colour tonal optimisation (reading R4): C channels on
+// one mesh are C independent CGLS problems (B is block-diagonal over the channels). They run in
+// lockstep: every inner solve is ONE batched solve of the active channels' right-hand sides on
+// the shared matrix (the multi-RHS graph loop streams the matrix once for all of them), the
+// forward raster of all channels is one pass, and the host sees one synchronisation per dot
+// round (all channels' scalars together). Each channel follows tonal_cgls's recurrence and
+// stopping rule; a converged channel leaves the batch.
+femi_status tonal_cgls_channels(femi_system_s* S, int C, const double* const* f, double* const* g,
+                                const femi_tonal_opts& o, femi_tonal_report* rep, cudaStream_t st) {
+    const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t per = 3 * al(sizeof(double) * nv) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m) +
+                       al(sizeof(double) * 8);
+    size_t bytes = (size_t)C * per + al(sizeof(double) * 3 * std::max<int64_t>(T, 1)) + al(sizeof(double) * 300 * C);
+    void* base = nullptr;
+    FEMI_CUDA(cudaMallocAsync(&base, bytes, st));
+    char* cur = (char*)base;
+    auto take = [&](size_t x) {
+        char* p = cur;
+        cur += al(x);
+        return (double*)p;
+    };
+    std::vector<double*> uv(C), yv(C), w(C), u(C), r(C), q(C), sv(C), p(C), dr(C);
+    for (int c = 0; c < C; ++c) {
+        uv[c] = take(sizeof(double) * nv);
+        yv[c] = take(sizeof(double) * nv);
+        w[c] = take(sizeof(double) * nv);
+        u[c] = take(sizeof(double) * N);
+        r[c] = take(sizeof(double) * N);
+        q[c] = take(sizeof(double) * N);
+        sv[c] = take(sizeof(double) * m);
+        p[c] = take(sizeof(double) * m);
+        dr[c] = take(sizeof(double) * 8);
+    }
+    double* tri_w = take(sizeof(double) * 3 * std::max<int64_t>(T, 1));
+    double* part = take(sizeof(double) * 300 * C);
+    int64_t solves = 0, inner_iters = 0;
+    femi_status note = FEMI_OK;
+    auto keep = [&](femi_status s2) {
+        if (s2 != FEMI_OK && note == FEMI_OK) note = s2;
+    };
+    // inner solves of the listed channels, one batched call
+    auto solve = [&](const std::vector<int>& ch, bool from_g, const std::vector<const double*>& in,
+                     std::vector<double*>& out, int x0) -> femi_status {
+        const int B = (int)ch.size();
+        if (B == 0) return FEMI_OK;
+        std::vector<femi_system_s*> Sv(B, S);
+        std::vector<const double*> iv(B);
+        std::vector<double*> ov(B);
+        for (int b = 0; b < B; ++b) {
+            iv[b] = in[ch[b]];
+            ov[b] = out[ch[b]];
+        }
+        femi_cg_opts io = o.inner;
+        io.x0 = x0;
+        std::vector<int32_t> it(B);
+        std::vector<double> rr(B);
+        int64_t tot = 0;
+        const femi_status s2 = pcg_solve(B, Sv.data(), from_g ? iv.data() : nullptr, from_g ? nullptr : iv.data(),
+                                         ov.data(), io, it.data(), rr.data(), st, &tot);
+        solves += B;
+        inner_iters += tot;
+        if (s2 == FEMI_E_NONFINITE || s2 == FEMI_E_CUDA || s2 == FEMI_E_OOM) return s2;
+        keep(s2);
+        return FEMI_OK;
+    };
+    // out[c] = B in[c] for the listed channels: one batched solve + one raster pass
+    auto apply_B = [&](const std::vector<int>& ch, const std::vector<const double*>& in,
+                       std::vector<double*>& out) -> femi_status {
+        femi_status s2 = solve(ch, true, in, uv, 1);
+        if (s2) return s2;
+        const int B = (int)ch.size();
+        std::vector<const double*> uvc(B);
+        std::vector<double*> po(B);
+        for (int b = 0; b < B; ++b) {
+            uvc[b] = uv[ch[b]];
+            po[b] = out[ch[b]];
+        }
+        for (int b0 = 0; b0 < B; b0 += 4) {  // raster-only pass, <= 4 channels at a time
+            const int nb = std::min(4, B - b0);
+            s2 = launch_raster_channels(S, nb, uvc.data() + b0, nullptr, po.data() + b0, nullptr, nullptr, nullptr,
+                                        nullptr, st);
+            if (s2) return s2;
+        }
+        return FEMI_OK;
+    };
+    // s[c] = B^T in[c]
+    auto apply_BT = [&](const std::vector<int>& ch, const std::vector<const double*>& in,
+                        std::vector<double*>& s_out) -> femi_status {
+        for (int c : ch) {
+            femi_status s2 = launch_adjoint_raster(S, in[c], tri_w, st);
+            if (s2) return s2;
+            k_vertex_gather<<<grid_for(nv), TT, 0, st>>>(nv, S->vt_ptr, S->vt_idx, tri_w, w[c]);
+            count_launches(1);
+        }
+        std::vector<const double*> wc(C);
+        for (int c = 0; c < C; ++c) wc[c] = w[c];
+        femi_status s2 = solve(ch, false, wc, yv, 0);
+        if (s2) return s2;
+        for (int c : ch) {
+            k_ku<<<grid_for(m), TT, 0, st>>>(m, S->n_u, S->ku_rowptr, S->ku_src, S->ku_row, S->uk_val, w[c], yv[c],
+                                            s_out[c]);
+            count_launches(1);
+        }
+        FEMI_CUDA(cudaGetLastError());
+        return FEMI_OK;
+    };
+    // host[c] = a[c] . b[c] for the listed channels, one synchronisation
+    auto dots = [&](const std::vector<int>& ch, int64_t n, const std::vector<double*>& a, const std::vector<double*>& b,
+                    std::vector<double>& host) -> femi_status {
+        const int nb = 296;
+        for (int c : ch) {
+            k_dot_part<<<nb, TT, 0, st>>>(n, a[c], b[c], part + 300 * c);
+            k_dot_final<<<1, TT, 0, st>>>(nb, part + 300 * c, dr[c]);
+            count_launches(2);
+        }
+        FEMI_CUDA(cudaGetLastError());
+        for (int c : ch) FEMI_CUDA(cudaMemcpyAsync(&host[c], dr[c], sizeof(double), cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        return FEMI_OK;
+    };
+    std::vector<int> all(C);
+    for (int c = 0; c < C; ++c) all[c] = c;
+    std::vector<const double*> gc(g, g + C), fc(f, f + C), pc(C), rc(C);
+    for (int c = 0; c < C; ++c) {
+        pc[c] = p[c];
+        rc[c] = r[c];
+    }
+    std::vector<double> rr(C), btf2(C), gam(C), gam2(C), qq(C), relg(C);
+    std::vector<int> outer(C, 0);
+    femi_status rcode = FEMI_OK;
+#define TRYC(x)                          \
+    do {                                 \
+        rcode = (x);                     \
+        if (rcode != FEMI_OK) goto done; \
+    } while (0)
+    {
+        TRYC(apply_B(all, gc, u));
+        for (int c = 0; c < C; ++c) {
+            k_sub<<<grid_for(N), TT, 0, st>>>(N, f[c], u[c], r[c]);
+            count_launches(1);
+        }
+        TRYC(dots(all, N, r, r, rr));
+        for (int c = 0; c < C; ++c) rep[c].mse_before = rr[c] / (double)N;
+        TRYC(apply_BT(all, fc, sv));
+        TRYC(dots(all, m, sv, sv, btf2));
+        TRYC(apply_BT(all, rc, sv));
+        for (int c = 0; c < C; ++c) FEMI_CUDA(cudaMemcpyAsync(p[c], sv[c], sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+        TRYC(dots(all, m, sv, sv, gam));
+        std::vector<int> act;
+        for (int c = 0; c < C; ++c) {
+            relg[c] = btf2[c] > 0.0 ? std::sqrt(gam[c]) / std::sqrt(btf2[c]) : 0.0;
+            if (relg[c] >= o.outer_rtol && o.outer_max > 0) act.push_back(c);
+        }
+        while (!act.empty()) {
+            TRYC(apply_B(act, pc, q));
+            TRYC(dots(act, N, q, q, qq));
+            std::vector<int> go;
+            for (int c : act)
+                if (qq[c] > 0.0) go.push_back(c);
+            for (int c : go) {
+                const double alpha = gam[c] / qq[c];
+                k_axpy_h<<<grid_for(m), TT, 0, st>>>(m, alpha, p[c], g[c]);
+                k_axpy_h<<<grid_for(N), TT, 0, st>>>(N, -alpha, q[c], r[c]);
+                count_launches(2);
+            }
+            TRYC(apply_BT(go, rc, sv));
+            TRYC(dots(go, m, sv, sv, gam2));
+            std::vector<int> next;
+            for (int c : go) {
+                ++outer[c];
+                relg[c] = std::sqrt(gam2[c]) / std::sqrt(btf2[c]);
+                if (!std::isfinite(relg[c])) {
+                    rcode = FEMI_E_NONFINITE;
+                    goto done;
+                }
+                if (relg[c] < o.outer_rtol) {
+                    gam[c] = gam2[c];
+                    continue;
+                }
+                if (outer[c] < o.outer_max) {
+                    k_xpby<<<grid_for(m), TT, 0, st>>>(m, sv[c], gam2[c] / gam[c], p[c]);
+                    count_launches(1);
+                    next.push_back(c);
+                }
+                gam[c] = gam2[c];
+            }
+            act = next;
+        }
+        for (int c = 0; c < C; ++c) {
+            rep[c].rel_grad_recursive = relg[c];
+            rep[c].outer_iters = outer[c];
+        }
+        TRYC(apply_B(all, gc, u));
+        for (int c = 0; c < C; ++c) {
+            k_sub<<<grid_for(N), TT, 0, st>>>(N, f[c], u[c], r[c]);
+            count_launches(1);
+        }
+        TRYC(dots(all, N, r, r, rr));
+        for (int c = 0; c < C; ++c) rep[c].mse_after = rr[c] / (double)N;
+        TRYC(apply_BT(all, rc, sv));
+        TRYC(dots(all, m, sv, sv, gam2));
+        for (int c = 0; c < C; ++c) {
+            rep[c].rel_grad = btf2[c] > 0.0 ? std::sqrt(gam2[c]) / std::sqrt(btf2[c]) : 0.0;
+            if (relg[c] >= o.outer_rtol && outer[c] >= o.outer_max) keep(FEMI_E_NOT_CONVERGED);
+        }
+    }
+done:
+#undef TRYC
+    for (int c = 0; c < C; ++c) {
+        rep[c].inner_solves = (int32_t)(solves / C);
+        rep[c].inner_iters = inner_iters / C;
+    }
+    cudaFreeAsync(base, st);
+    if (rcode != FEMI_OK) return rcode;
+    if (note != FEMI_OK) set_error("tonal_optimise_channels: an inner solve or the outer loop did not converge");
+    return note;
+}
+
 // The operator alone (femi_apply_B / femi_apply_BT): mode 0 out = B in (pixels), mode 1
 // out = B^T in (mask values); one inner solve each, synchronised for its status.
 femi_status tonal_apply(femi_system_s* S, int mode, const double* in, double* out, const femi_cg_opts& o,

@@ -74,7 +74,8 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_system_free", "femi_inpaint_solve_batched", "femi_rasterise_error", "femi_rasterise_error_batched",
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
            "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert",
-           "femi_system_solver_path", "femi_apply_B", "femi_apply_BT", "femi_device_check_failures"]
+           "femi_system_solver_path", "femi_apply_B", "femi_apply_BT", "femi_device_check_failures",
+           "femi_tonal_optimise_channels"]
 
 # femi_system_solver_path values (include/femi.h)
 PATH_NAMES = {0: "none", 1: "resident", 2: "persistent", 3: "graph_sell", 4: "graph_tma", 5: "graph_multi"}
@@ -115,6 +116,7 @@ def lib():
         L.femi_tonal_optimise_l1.argtypes = [P, P, P, ctypes.POINTER(TonalOpts), ctypes.c_int32, ctypes.c_double,
                                              ctypes.POINTER(TonalL1Report), P]
         L.femi_system_solver_path.argtypes = [P, I32P]
+        L.femi_tonal_optimise_channels.argtypes = [P, ctypes.c_int32, P, P, ctypes.POINTER(TonalOpts), P, P]
         L.femi_device_check_failures.argtypes = [ctypes.POINTER(ctypes.c_int64)]
         L.femi_apply_B.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
         L.femi_apply_BT.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
@@ -427,3 +429,20 @@ def device_check_failures():
     site = ctypes.c_int64(0)
     n = lib().femi_device_check_failures(ctypes.byref(site))
     return int(n), int(site.value)
+
+
+def tonal_optimise_channels(system, f_list, g_list, outer_rtol=1e-8, outer_max=1000, inner: CgOpts | None = None,
+                            stream=None):
+    """NEXT-1 colour tonal optimisation: C channels (device f_c, g_c in/out) on one mesh.
+    Returns (status, [report dict per channel])."""
+    import torch
+    C = len(f_list)
+    inner = inner or cg_opts(rtol=1e-12)
+    o = TonalOpts(outer_rtol, outer_max, inner, 0)
+    reps = (TonalReport * C)()
+    fa = _ptr_array([_dptr(f, torch.float64) for f in f_list])
+    ga = _ptr_array([_dptr(g, torch.float64) for g in g_list])
+    st = lib().femi_tonal_optimise_channels(system._h, C, fa, ga, ctypes.byref(o), reps, _stream(stream))
+    if st not in (FEMI_OK, 4):
+        _check(st)
+    return st, [r.as_dict() for r in reps]

@@ -499,3 +499,49 @@ def test_graph_mode_switches_bit_identical(tmp_path):
         outs.append(np.load(out))
     np.testing.assert_array_equal(outs[0], outs[1])
 
+
+
+def test_tonal_channels_vs_oracle():
+    """NEXT-1 colour tonal optimisation (reading R4): three channels on one mesh, run in lockstep
+    with batched inner solves, each against the oracle's own tonal run of that channel (the
+    joint colour problem separates per channel: pinned on CPU against a block-diagonal dense
+    lstsq); converged to 1e-8: g within 1e-4, MSE within 1e-6 relative."""
+    fs, mk, un = _colour_case(128, 91, density=0.03)
+    fs = [f[: 128 * 128] for f in fs]
+    M = femi.Mesh(128, 128, mk, un)
+    S = femi.System(M)
+    vert = M.export()["vert_px"]
+    fd = [dev(f) for f in fs]
+    gs = [pipeline.mask_values(f, vert, S.n_u) for f in fd]
+    st, reps = femi.tonal_optimise_channels(S, fd, gs, outer_rtol=1e-8)
+    assert st == 0
+    O = oracle.System(128, 128, mk, un)
+    go, oreps = oracle.tonal_channels(O, fs, outer_tol=1e-8)
+    for c in range(3):
+        assert np.abs(gs[c].cpu().numpy() - go[c]).max() <= GREY_TOL
+        assert abs(reps[c]["mse_after"] - oreps[c]["mse_after"]) <= MSE_RTOL * oreps[c]["mse_after"]
+        assert reps[c]["rel_grad"] < 1e-7 and reps[c]["mse_after"] <= reps[c]["mse_before"]
+    # C = 1 is the single-channel call
+    g1 = pipeline.mask_values(fd[1], vert, S.n_u)
+    st1, rep1 = femi.tonal_optimise(S, fd[1], g1, outer_rtol=1e-8)
+    assert rep1["outer_iters"] == reps[1]["outer_iters"]
+    assert torch.abs(g1 - gs[1]).max().item() <= 1e-6
+
+
+def test_tonal_channels_graph_mode():
+    """Colour tonal on the shared-matrix multi-RHS graph loop (2880^2 x 3): 5 lockstep CGLS
+    iterations against the oracle per channel (iterate parity, reading A13b)."""
+    fs, mk, un = _colour_case(2880, 93)
+    M = femi.Mesh(2880, 2880, mk, un)
+    S = femi.System(M)
+    vert = M.export()["vert_px"]
+    fd = [dev(f) for f in fs]
+    gs = [pipeline.mask_values(f, vert, S.n_u) for f in fd]
+    st, reps = femi.tonal_optimise_channels(S, fd, gs, outer_rtol=1e-300, outer_max=5)
+    assert femi.solver_path(S) == "graph_multi"
+    O = oracle.System(2880, 2880, mk, un)
+    go, oreps = oracle.tonal_channels(O, fs, outer_tol=1e-300, outer_max=5, inner_method=3)
+    for c in range(3):
+        assert reps[c]["outer_iters"] == 5
+        assert np.abs(gs[c].cpu().numpy() - go[c]).max() <= GREY_TOL
+        assert abs(reps[c]["mse_after"] - oreps[c]["mse_after"]) <= MSE_RTOL * oreps[c]["mse_after"]

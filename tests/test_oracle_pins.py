@@ -644,6 +644,26 @@ def test_p13_tonal_matches_dense_lstsq(seed):
     np.testing.assert_array_equal(B[S.mask_px], np.eye(S.m))
 
 
+def test_colour_tonal_is_the_joint_least_squares():
+    """NEXT-1 colour tonal (reading R4): the joint problem min sum_c ||B g_c - f_c||^2 over all
+    channels, solved densely as ONE block-diagonal least-squares system with numpy, equals the
+    oracle's per-channel solutions (and a channel permutation permutes them)."""
+    cfg = make_config(4, W=14, H=12, seed=77)
+    S = oracle.System(14, 12, cfg["mask"], cfg["unknowns"])
+    rng = np.random.default_rng(77)
+    fs = [cfg["f"].reshape(-1), rng.uniform(0, 255, 14 * 12), np.clip(cfg["f"].reshape(-1) * 0.5 + 40, 0, 255)]
+    B = oracle.materialise_B(S)
+    Z = np.zeros_like(B)
+    Bj = np.block([[B, Z, Z], [Z, B, Z], [Z, Z, B]])
+    gj = np.linalg.lstsq(Bj, np.concatenate(fs), rcond=None)[0]
+    gs, reps = oracle.tonal_channels(S, fs, outer_tol=1e-10)
+    for c in range(3):
+        assert np.abs(gs[c] - gj[c * S.m:(c + 1) * S.m]).max() <= 1e-4
+        assert reps[c]["mse_after"] <= reps[c]["mse_before"]
+    gp, _ = oracle.tonal_channels(S, [fs[2], fs[0], fs[1]], outer_tol=1e-10)
+    np.testing.assert_array_equal(gp[1], gs[0])
+
+
 def test_p14_adjoint_identity_and_partition_of_unity():
     cfg = make_config(4, W=40, H=32, seed=77)
     S = oracle.System(40, 32, cfg["mask"], cfg["unknowns"])
