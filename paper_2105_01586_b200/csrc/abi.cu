@@ -99,26 +99,6 @@ femi_status check_device() {
     return FEMI_OK;
 }
 
-// row chunks for the PCG kernels: <= kRowsPerChunk rows and <= kChunkNnzCap off-diagonals
-std::vector<Chunk> make_chunks(const std::vector<int32_t>& uu_rowptr, int64_t n_u) {
-    std::vector<Chunk> ch;
-    int64_t i = 0;
-    int32_t local = 0;
-    while (i < n_u) {
-        int64_t j = i;
-        int64_t nnz = 0;
-        while (j < n_u && j - i < kRowsPerChunk) {
-            int64_t rn = (uu_rowptr[j + 1] - uu_rowptr[j]) - 1;
-            if (j > i && nnz + rn > kChunkNnzCap) break;
-            nnz += rn;
-            ++j;
-        }
-        ch.push_back({0, (int32_t)i, (int32_t)j, local++});
-        i = j;
-    }
-    return ch;
-}
-
 }  // namespace
 }  // namespace femi
 
@@ -296,34 +276,6 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
     U(alloc(S, &S->o_val, M.uu_col.size() - M.n_u));
     U(alloc(S, &S->s, (size_t)M.n_u));
     stamp("uploads");
-    S->chunks_h = make_chunks(M.uu_rowptr, M.n_u);
-    U(upload(S, &S->chunks_d, S->chunks_h, st));
-    {
-        // chunk row table and int16 column offsets (relative to the chunk's first row)
-        std::vector<int32_t> row0(S->chunks_h.size() + 1);
-        for (size_t c = 0; c < S->chunks_h.size(); ++c) row0[c] = S->chunks_h[c].row0;
-        row0.back() = (int32_t)M.n_u;
-        S->nchunks = (int32_t)S->chunks_h.size();
-        U(upload(S, &S->chunk_row0, row0, st));
-        std::vector<int16_t> cd(M.uu_col.size() - M.n_u);
-        bool fits = true;
-        size_t o = 0;
-        for (size_t c = 0; c < S->chunks_h.size() && fits; ++c) {
-            const int32_t r0 = S->chunks_h[c].row0;
-            for (int32_t i = r0; i < S->chunks_h[c].row1 && fits; ++i)
-                for (int32_t e = M.uu_rowptr[i]; e < M.uu_rowptr[i + 1]; ++e) {
-                    const int32_t j = M.uu_col[e];
-                    if (j == i) continue;
-                    const int32_t d = j - r0;
-                    if (d < -32768 || d > 32767) {
-                        fits = false;
-                        break;
-                    }
-                    cd[o++] = (int16_t)d;
-                }
-        }
-        if (fits && !cd.empty()) U(upload(S, &S->o_cd, cd, st));
-    }
     {
         // Solver numbering + SELL-32-sigma layout of the off-diagonal pattern (values are
         // filled on the device after assembly). Internal order: unknowns sorted by

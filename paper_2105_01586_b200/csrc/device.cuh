@@ -19,11 +19,6 @@ struct __align__(16) TriRec {
 };
 static_assert(sizeof(TriRec) == 32, "TriRec must be 32 bytes");
 
-// A row chunk of the PCG kernels (one CTA): rows [row0, row1) of batch item `item`.
-struct Chunk {
-    int32_t item, row0, row1, local;  // local = chunk index within the item
-};
-
 // Per-RHS solver state, device resident; scalars of one CG recursion.
 struct CgState {
     double rr;     // r^.r^ (scaled residual)
@@ -42,28 +37,6 @@ struct CgState {
     double alpha_pend; // graph mode: alpha of the previous k_gu
 };
 
-// One batch item as the PCG kernels see it.
-struct SolveItem {
-    const int32_t* orp;   // off-diagonal rowptr of the scaled matrix (n+1)
-    const int32_t* oci;   // off-diagonal columns
-    const double* oav;    // scaled off-diagonal values  s_i a_ij s_j
-    const double* s;      // D^-1/2
-    const int32_t* urp;   // unscaled A_uu rowptr (diagonal included), for the true residual
-    const int32_t* uci;
-    const double* uav;
-    const int32_t* krp;   // A_uk rowptr
-    const int32_t* kci;
-    const double* kav;
-    const double* g;      // mask values (m) or NULL when b is given
-    const double* bin;    // given right-hand side (n) or NULL
-    double* u_vert;       // output vertex values (n + m)
-    double *x, *r, *q, *b;
-    double* p[2];
-    int32_t n, m;
-    int32_t chunk0, nchunks;
-    int32_t x0mode;       // 0 zeros, 1 midrange(g), 2 caller-provided (u_vert[0..n))
-    int32_t pad;
-};
 
 }  // namespace femi
 
@@ -92,15 +65,6 @@ struct femi_system_s {
     int32_t* o_col = nullptr;
     double* o_val = nullptr;
     double* s = nullptr;
-    // PCG row chunks: chunk c = rows [chunk_row0[c], chunk_row0[c+1]) (<= kRowsPerChunk rows,
-    // <= kChunkNnzCap off-diagonals unless a single row is longer)
-    std::vector<femi::Chunk> chunks_h;
-    femi::Chunk* chunks_d = nullptr;
-    int32_t* chunk_row0 = nullptr;
-    int32_t nchunks = 0;
-    // off-diagonal columns as int16 offsets from their chunk's first row (NULL if the
-    // matrix bandwidth does not allow it; o_col is used then)
-    int16_t* o_cd = nullptr;
     // Sliced ELL (SELL-32-sigma) copy of the scaled off-diagonal matrix for the solver:
     // windows of kSellSigma rows, rows sorted by length inside a window, slices of 32 rows
     // stored column-major (entry k of lane l of slice s at sell_base[s] + 32k + l).
@@ -221,12 +185,10 @@ int64_t dcheck_raster(int64_t*);
 int64_t dcheck_select(int64_t*);
 int64_t dcheck_tonal(int64_t*);
 
-constexpr int kRowsPerChunk = 512;
 constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)
 constexpr int kBand = 32;        // image band height (pixels) of the internal solver order
 constexpr int kBandJds = 64;     // the same for graph-mode systems (JDS tiles, in-tile gathers from smem)
 femi_status launch_sell_values(femi_system_s* S, const int32_t* d_src, cudaStream_t st);
-constexpr int kChunkNnzCap = 2048;
 constexpr int64_t kGraphNnz = 600000;  // nnz(A_uu) above which one system solves in graph mode
 constexpr int kJdsRows = 512;          // rows per TMA tile of the jagged-diagonal layout
 constexpr int kJdsMaxK = 24;           // longest row (off-diagonals) the JDS layout takes

@@ -1465,14 +1465,14 @@ struct JStage {
     double* s;
 };
 
-template <bool FIRST, bool LEAN>
+template <bool FIRST, bool LEAN, int NS = JNS>
 __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, int B, double* __restrict__ part,
                                             unsigned* __restrict__ gcnt, cudaGraphConditionalHandle h, int lsi) {
     extern __shared__ __align__(128) unsigned char jsm[];
     unsigned long long t_start = 0;
     if (g_loop_prof && threadIdx.x == 0) t_start = gtime();
-    __shared__ __align__(8) uint64_t full[JNS], empty[JNS];
-    __shared__ int2 tile_e[JNS], tile_c[JNS];  // entry / column-byte range of the tile in each stage
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
+    __shared__ int2 tile_e[NS], tile_c[NS];  // entry / column-byte range of the tile in each stage
     const RItem& it = items[0];
     CgState* S = it.st;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1490,7 +1490,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
         return q;
     };
     if (threadIdx.x == 0) {
-        for (int k = 0; k < JNS; ++k) {
+        for (int k = 0; k < NS; ++k) {
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], JCW);
         }
@@ -1499,7 +1499,7 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     __syncthreads();
     // The matrix does not depend on the previous kernel: behind a programmatic edge (graph
     // body) this CTA is resident while k_gu still runs, and the producer already streams the
-    // values, columns and metadata of its first JNS tiles (expect_tx without an arrival keeps
+    // values, columns and metadata of its first NS tiles (expect_tx without an arrival keeps
     // each stage's phase open); r and q follow once the update kernel has completed.
     // no prefetch for the no-op tail of the unrolled body: active only goes 1 -> 0 inside one
     // graph launch, so a 0 read before the dependency wait is final (a stale 1 only prefetches)
@@ -1546,9 +1546,9 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
                 }
                 int e0 = tb + npre < te ? it.jeb[tb + npre] : 0, c0 = tb + npre < te ? it.jcb[tb + npre] : 0;
                 for (int t = tb + npre, i = npre; t < te; ++t, ++i) {
-                    const int k = i % JNS;
+                    const int k = i % NS;
                     const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];  // loaded before the wait
-                    if (i >= JNS) mbar_wait(&empty[k], ((i / JNS) - 1) & 1);
+                    if (i >= NS) mbar_wait(&empty[k], ((i / NS) - 1) & 1);
                     const JStage q = stage(k);
                     const int ne = e1 - e0, nc = c1 - c0;
                     tile_e[k] = make_int2(e0, ne);
@@ -1572,8 +1572,8 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
             double* __restrict__ wout = it.w;
             const int rl = 32 * warp + lane;
             for (int t = tb, i = 0; t < te; ++t, ++i) {
-                const int k = i % JNS;
-                mbar_wait(&full[k], (i / JNS) & 1);
+                const int k = i % NS;
+                mbar_wait(&full[k], (i / NS) & 1);
                 const JStage q = stage(k);
                 const int row = t * kJdsRows + rl;
                 const int len = q.meta[rl];
@@ -2272,6 +2272,7 @@ struct GraphCache {
     int gs_blocks = 0, gx = 0, gt_blocks = 0;
     unsigned gt_smem = 0;  // > 0: the SpMV is the TMA-streamed k_gt (JDS layout); else SELL k_gs
     unsigned gf_smem = 0;  // > 0: the fused iteration kernel k_gf fits
+    int gt_ns = JNS;       // ring stages of k_gt (FEMI_JNS=8: the deeper ring when it fits)
 };
 
 struct Workspace {
@@ -2359,8 +2360,8 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         dep = &prev;
         return s;
     };
-    void* spmv_first = tma ? (void*)k_gt<true, true> : (void*)k_gs<true>;
-    void* spmv = tma ? (void*)k_gt<false, true> : (void*)k_gs<false>;
+    void* spmv_first = tma ? (C.gt_ns == 8 ? (void*)k_gt<true, true, 8> : (void*)k_gt<true, true>) : (void*)k_gs<true>;
+    void* spmv = tma ? (C.gt_ns == 8 ? (void*)k_gt<false, true, 8> : (void*)k_gt<false, true>) : (void*)k_gs<false>;
     const dim3 gsp(tma ? C.gt_blocks : C.gs_blocks), bsp(tma ? JNT : GNT);
     const unsigned ssp = tma ? C.gt_smem : 0;
     femi_status s = FEMI_OK;
@@ -2572,10 +2573,21 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             FEMI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
             if (JNS * stage_bytes + 4096 <= (size_t)optin) {
                 C->gt_smem = (unsigned)(JNS * stage_bytes);
+                if (const char* e = std::getenv("FEMI_JNS"))
+                    if (std::atoi(e) == 8 && 8 * stage_bytes + 4096 <= (size_t)optin) {
+                        C->gt_ns = 8;
+                        C->gt_smem = (unsigned)(8 * stage_bytes);
+                        for (const void* fn : {(const void*)k_gt<false, true, 8>, (const void*)k_gt<true, true, 8>})
+                            FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)C->gt_smem));
+                    }
+                if (std::getenv("FEMI_DEBUG"))
+                    std::fprintf(stderr, "[femi] k_gt stage %zu B x %d stages (optin %d)\n", stage_bytes, C->gt_ns, optin);
                 C->gt_blocks = std::max(1, std::min(nsm, S->jds_ntile));
                 for (const void* fn : {(const void*)k_gt<false, true>, (const void*)k_gt<true, true>,
                                        (const void*)k_gt<false, false>})
-                    FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C->gt_smem));
+                    FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(JNS * stage_bytes)));
                 const size_t gfb = JNSF * gf_stage_bytes(S->jds_maxe, S->jds_meta_bytes);
                 if (gfb + 4096 <= (size_t)optin) {
                     C->gf_smem = (unsigned)gfb;
