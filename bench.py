@@ -273,7 +273,7 @@ def run_ours(args):
     tri_err = torch.empty(sysm.T, dtype=torch.float64, device=dev)
     best = torch.empty(sysm.T, dtype=torch.int32, device=dev)
     sse = torch.zeros(1, dtype=torch.float64, device=dev)
-    opts = femi.cg_opts(rtol=RTOL)
+    opts = femi.cg_opts(rtol=RTOL, x0=int(os.environ.get("FEMI_BENCH_X0", "1")))
     stream = torch.cuda.current_stream()
 
     def step(ev=None):

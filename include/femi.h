@@ -143,8 +143,12 @@ void femi_system_free(femi_system sys);
  *   opts: rtol (> 0), max_iter (> 0), precond (must be 1: Jacobi, folded into the matrix at
  *         assembly; plain CG (0) is not offered -- it reaches the same solution in ~6x the
  *         iterations, reading A11 -- and is rejected with FEMI_E_ARG), x0 (0 zeros, 1
- *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided), check_every
- *         (reserved, must be 0: convergence is tested on the device every iteration).
+ *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided, 3 mask-neighbour
+ *         fill: each unknown starts at the value of its most strongly coupled mask neighbour,
+ *         unknowns without one at their first filled unknown neighbour's (two hops), the rest
+ *         at midrange(g) -- same solution, fewer iterations (reading A11b); with a given b
+ *         (tonal adjoint solves) modes 1 and 3 start from 0), check_every (reserved, must be 0:
+ *         convergence is tested on the device every iteration).
  *   iters[B], relres[B]: HOST outputs (iteration count, final true relative residual).
  * Special cases: ||b|| == 0 -> x = 0, 0 iterations; n_unknown == 0 -> no-op; an initial
  * guess that already satisfies rtol exits with 0 iterations and is returned unchanged.

@@ -537,9 +537,35 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
                 S->jds_nnz = (int64_t)eb[ntile];
                 U(upload(S, &S->jds_eb, eb, st));
                 U(upload(S, &S->jds_cb, cbo, st));
-                U(upload(S, &S->jds_meta, meta, st));
-                U(upload(S, &S->jds_col, jcolb, st));
-                U(alloc(S, &S->jds_val, (size_t)std::max<int64_t>(S->jds_nnz, 1)));
+                {
+                    // values | columns | metadata in ONE allocation: the SpMV's matrix stream is one
+                    // address range (an L2 access-policy window can cover it)
+                    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+                    const size_t bv = al(sizeof(double) * (size_t)std::max<int64_t>(S->jds_nnz, 1));
+                    const size_t bc = al(std::max<size_t>(jcolb.size(), 1));
+                    const size_t bm = al(std::max<size_t>(meta.size(), 1));
+                    void* blk = nullptr;
+                    const cudaError_t e = cudaMalloc(&blk, bv + bc + bm);
+                    if (e != cudaSuccess) {
+                        s = cuda_fail(e, "assemble: matrix stream block");
+                        goto fail;
+                    }
+                    S->allocs.push_back(blk);
+                    S->jds_val = (double*)blk;
+                    S->jds_col = (uint8_t*)blk + bv;
+                    S->jds_meta = (uint8_t*)blk + bv + bc;
+                    S->jds_block_bytes = bv + bc + bm;
+                    if (!jcolb.empty() && cudaMemcpyAsync(S->jds_col, jcolb.data(), jcolb.size(), cudaMemcpyHostToDevice,
+                                                          st) != cudaSuccess) {
+                        s = cuda_fail(cudaGetLastError(), "assemble: columns");
+                        goto fail;
+                    }
+                    if (!meta.empty() && cudaMemcpyAsync(S->jds_meta, meta.data(), meta.size(), cudaMemcpyHostToDevice,
+                                                         st) != cudaSuccess) {
+                        s = cuda_fail(cudaGetLastError(), "assemble: metadata");
+                        goto fail;
+                    }
+                }
                 int32_t* d_js = nullptr;
                 U(upload(S, &d_js, jsrc, st));
                 S->jds_src_tmp = d_js;
@@ -615,9 +641,9 @@ femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const 
         return FEMI_E_ARG;
     }
     if (B == 0) return FEMI_OK;
-    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond != 1 || opts->x0 < 0 || opts->x0 > 2 ||
+    if (!(opts->rtol > 0.0) || opts->max_iter <= 0 || opts->precond != 1 || opts->x0 < 0 || opts->x0 > 3 ||
         opts->check_every != 0) {
-        set_error("inpaint_solve_batched: invalid options (rtol > 0, max_iter > 0, precond 1, x0 0..2, check_every 0)");
+        set_error("inpaint_solve_batched: invalid options (rtol > 0, max_iter > 0, precond 1, x0 0..3, check_every 0)");
         return FEMI_E_ARG;
     }
     for (int b = 0; b < B; ++b)

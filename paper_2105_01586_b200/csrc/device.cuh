@@ -99,6 +99,7 @@ struct femi_system_s {
     // (rows of a slice are in descending length order, so diagonal k of slice w is the lanes
     // 0 .. cnt_k-1 at doff[w][k] + lane).
     int32_t jds_ntile = 0, jds_maxe = 0, jds_kmax = 0, jds_meta_bytes = 0;
+    size_t jds_block_bytes = 0;  // jds_val | jds_col | jds_meta are one allocation of this size
     int32_t* jds_eb = nullptr;
     int32_t* jds_cb = nullptr;   // per tile: byte offset of its columns (int32 if 4 bytes per entry)
     uint8_t* jds_meta = nullptr;

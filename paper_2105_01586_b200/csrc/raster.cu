@@ -392,14 +392,14 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __res
                         u = __dadd_rn(__dadd_rn(G.ua[ch][j], __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
                     else
                         u = cls == 1 ? G.ua[ch][j] : (cls == 2 ? G.ub[ch][j] : G.uc[ch][j]);
-                    if (it.u_px[ch]) it.u_px[ch][pix] = u;
+                    if (it.u_px[ch]) __stcs(it.u_px[ch] + pix, u);  // streaming store (written once)
                     if (hasf) {
                         const double d = __dsub_rn(u, fv[h][ch]);
                         e = ch == 0 ? __dmul_rn(d, d) : __dadd_rn(e, __dmul_rn(d, d));  // channel sum in order
                     }
                 }
                 if (hasf) {
-                    if (e_px) e_px[pix] = e;
+                    if (e_px) __stcs(e_px + pix, e);
                     const int sl = wl_slot(v[h]);
                     es[sl] = cls ? -e : e;  // -0.0 for e = 0: the sign bit is the flag
                     ps[sl] = pix;
@@ -643,12 +643,17 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
     int64_t Tmax = 0;
     for (const RasterItem& r : items) Tmax = std::max(Tmax, r.T);
     if (B == 0 || Tmax == 0) return FEMI_OK;
+    static const bool minb5 = [] {
+        const char* e = std::getenv("FEMI_RASTER_MINB");
+        return e && std::atoi(e) == 5;
+    }();
     static int resident = 0;
     if (resident == 0) {
         int dev = 0, nsm = 0, per = 0;
         FEMI_CUDA(cudaGetDevice(&dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_raster_grp<4, 1>, RT,
+        FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, minb5 ? (const void*)k_raster_grp<5, 1>
+                                                                      : (const void*)k_raster_grp<4, 1>, RT,
                                                                 RWARPS * sizeof(GTri<1>)));
         resident = std::max(1, per) * nsm;
     }
@@ -686,7 +691,10 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
     }
     switch (nc) {
         case 1:
-            k_raster_grp<4, 1><<<gr, RT, RWARPS * sizeof(GTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
+            if (minb5)  // FEMI_RASTER_MINB=5: 5 CTAs/SM (48 registers)
+                k_raster_grp<5, 1><<<gr, RT, RWARPS * sizeof(GTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
+            else
+                k_raster_grp<4, 1><<<gr, RT, RWARPS * sizeof(GTri<1>), st>>>(d_items, d_gpart, d_cnt, groups);
             break;
         case 2:
             k_raster_grp<2, 2><<<gr, RT, RWARPS * sizeof(GTri<2>), st>>>(d_items, d_gpart, d_cnt, groups);
