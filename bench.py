@@ -273,7 +273,8 @@ def run_ours(args):
     tri_err = torch.empty(sysm.T, dtype=torch.float64, device=dev)
     best = torch.empty(sysm.T, dtype=torch.int32, device=dev)
     sse = torch.zeros(1, dtype=torch.float64, device=dev)
-    opts = femi.cg_opts(rtol=RTOL, x0=int(os.environ.get("FEMI_BENCH_X0", "1")))
+    # x0: the mask-neighbour fill (reading A11b; FEMI_BENCH_X0=1: the midrange start of round 1)
+    opts = femi.cg_opts(rtol=RTOL, x0=int(os.environ.get("FEMI_BENCH_X0", "3")))
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
@@ -596,7 +597,7 @@ def run_workload(args):
                 S = femi.System(M)
                 g = pipeline.mask_values(f_dev, M.export()["vert_px"], S.n_u)
                 u = torch.empty(S.nv, dtype=torch.float64, device=dev)
-                x0 = 1
+                x0 = 3
                 if args.warm and x_prev is not None and x_prev.numel() == S.n_u:
                     u[: S.n_u] = x_prev  # NEXT-4 warm start: previous solution at the fixed unknowns
                     x0 = 2

@@ -146,8 +146,9 @@ void femi_system_free(femi_system sys);
  *         midrange(g) = (min g + max g)/2 (reading A11), 2 caller-provided, 3 mask-neighbour
  *         fill: each unknown starts at the value of its most strongly coupled mask neighbour,
  *         unknowns without one at their first filled unknown neighbour's (two hops), the rest
- *         at midrange(g) -- same solution, fewer iterations (reading A11b); with a given b
- *         (tonal adjoint solves) modes 1 and 3 start from 0), check_every (reserved, must be 0:
+ *         at midrange(g) -- same solution, fewer iterations (reading A11b); systems below
+ *         8192 unknowns use midrange instead (the fill's extra launches cost more there); with
+ *         a given b (tonal adjoint solves) modes 1 and 3 start from 0), check_every (reserved, must be 0:
  *         convergence is tested on the device every iteration).
  *   iters[B], relres[B]: HOST outputs (iteration count, final true relative residual).
  * Special cases: ||b|| == 0 -> x = 0, 0 iterations; n_unknown == 0 -> no-op; an initial

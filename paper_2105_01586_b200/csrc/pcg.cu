@@ -1272,6 +1272,7 @@ __device__ __forceinline__ void cta_partials(double (&v)[3], double* P) {
 // (iteration count, status, the deferred x term) to the item's CgState and ends the WHILE loop.
 // Compared with the last-CTA tail of cg_tail, nothing serialises behind an atomic counter.
 constexpr int GRT = 256;
+constexpr int64_t kFillMinRows = 8192;  // reading A11b: the fill pays from here on
 __global__ void __launch_bounds__(GRT) k_gur(const RItem* __restrict__ items, const double* __restrict__ part,
                                             int nparts, int par, cudaGraphConditionalHandle h) {
     __shared__ double red[3 * (GRT / 32)];
@@ -1355,7 +1356,7 @@ __global__ void __launch_bounds__(GRT) k_gur(const RItem* __restrict__ items, co
         sc[2] = (deferred && L.started) ? L.alpha : 0.0;
         si[0] = active;
         si[1] = iters;
-        if (blockIdx.x == 0) {
+        if (blockIdx.x == 0 && !g_kbench) {
             it.ls[par ^ 1] = N;
             if (!active) {  // final state for k_finalize / k_true_res / the host
                 CgState* Sw = it.st;
@@ -3170,8 +3171,17 @@ void pcg_cache_free(femi_system_s* S) {
 }
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
-                      double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
+                      double* const* u_vert, const femi_cg_opts& o_in, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters) {
+    // reading A11b: the mask-neighbour fill costs four extra launches and an SpMV for the initial
+    // residual; below kFillMinRows unknowns (launch-latency-bound systems, C1 / C2) those cost
+    // more than the iterations it saves (measured: C2 5.76K -> 5.18K Mpx/s), so midrange is used
+    femi_cg_opts o = o_in;
+    {
+        int64_t nfill = 0;
+        for (int b = 0; b < B; ++b) nfill = std::max(nfill, S[b]->n_u);
+        if (o.x0 == 3 && nfill < kFillMinRows) o.x0 = 1;
+    }
     {
         static int graph_mode = -1;  // FEMI_PCG_MODE=persistent forces the persistent kernel
         if (graph_mode < 0) {

@@ -157,7 +157,7 @@ struct Tonal {
     // u_px = B g
     femi_status apply_B(const double* g, double* u_px) {
         femi_cg_opts o = inner;
-        o.x0 = 1;
+        o.x0 = 3;  // mask-neighbour fill (reading A11b)
         int32_t it = 0;
         double rr = 0.0;
         int64_t tot = 0;
@@ -413,7 +413,7 @@ femi_status tonal_cgls_channels(femi_system_s* S, int C, const double* const* f,
     // out[c] = B in[c] for the listed channels: one batched solve + one raster pass
     auto apply_B = [&](const std::vector<int>& ch, const std::vector<const double*>& in,
                        std::vector<double*>& out) -> femi_status {
-        femi_status s2 = solve(ch, true, in, uv, 1);
+        femi_status s2 = solve(ch, true, in, uv, 3);
         if (s2) return s2;
         const int B = (int)ch.size();
         std::vector<const double*> uvc(B);
@@ -616,7 +616,7 @@ femi_status tonal_irls(femi_system_s* S, const double* f, double* g, const femi_
     for (int k = 0; k <= irls; ++k) {
         // u = B g (one inner solve + raster)
         femi_cg_opts io = o.inner;
-        io.x0 = 1;
+        io.x0 = 3;
         int32_t it = 0;
         double rr = 0.0;
         int64_t tot = 0;

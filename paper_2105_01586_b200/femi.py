@@ -259,7 +259,9 @@ class System:
         self.close()
 
 
-def cg_opts(rtol=1e-10, max_iter=100000, precond=1, x0=1, check_every=0) -> CgOpts:
+def cg_opts(rtol=1e-10, max_iter=100000, precond=1, x0=3, check_every=0) -> CgOpts:
+    """x0: 0 zeros, 1 midrange(g), 2 caller-provided (u_vert), 3 mask-neighbour fill (default,
+    reading A11b)."""
     return CgOpts(rtol, max_iter, precond, x0, check_every)
 
 

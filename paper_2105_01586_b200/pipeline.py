@@ -30,7 +30,7 @@ def mask_values(f_dev, mesh_or_sys_vert_px, n_u):
 
 
 def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stream=None, x0_unknown=None,
-            mesh=None):
+            mesh=None, x0=3):
     """x0_unknown: optional initial guess at the unknown vertices (canonical order, e.g. the
     previous densification iteration's solution: the unknown set is fixed, reading A4).
     mesh: a prebuilt femi.Mesh of exactly these vertices (e.g. from Mesh.insert)."""
@@ -41,7 +41,6 @@ def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stre
     vert = mesh.export()["vert_px"]
     g = mask_values(f_dev, vert, sysm.n_u)
     u_vert = torch.empty(sysm.nv, dtype=torch.float64, device=f_dev.device)
-    x0 = 1
     if x0_unknown is not None and x0_unknown.numel() == sysm.n_u:
         u_vert[: sysm.n_u] = x0_unknown
         x0 = 2
@@ -59,7 +58,7 @@ def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stre
 
 
 def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks=None, stream=None,
-            warm_start=False, incremental_mesh=True):
+            warm_start=False, incremental_mesh=True, x0=3):
     """Returns (final mask, per-iteration records, final MSE). warm_start: each solve starts
     from the previous iteration's solution at the (fixed, reading A4) unknown vertices
     (changes iterates, not the solution). incremental_mesh: each mesh is
@@ -77,7 +76,7 @@ def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks
         elif incremental_mesh and mesh is not None:
             mesh = mesh.insert(new)
         R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
-                    x0_unknown=x_prev if warm_start else None, mesh=mesh)
+                    x0_unknown=x_prev if warm_start else None, mesh=mesh, x0=x0)
         mesh = R["mesh"] if incremental_mesh else None
         x_prev = R["u_vert"][: R["system"].n_u].clone()
         new = femi.densify_step(R["system"], f1, R["u_vert"], int(schedule[t]), stream)
@@ -89,7 +88,7 @@ def densify(W, H, f_dev, mask0, unknown_px, schedule, rtol=1e-10, lockstep_masks
     else:
         mesh = None
     R = inpaint(W, H, f_dev, mask, unknown_px, rtol=rtol, want_images=False, stream=stream,
-                x0_unknown=x_prev if warm_start else None, mesh=mesh)
+                x0_unknown=x_prev if warm_start else None, mesh=mesh, x0=x0)
     return mask, recs, float(R["sse"].item()) / (W * H)
 
 

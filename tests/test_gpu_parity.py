@@ -439,7 +439,7 @@ def test_densify_warm_start():
     iterations over the schedule."""
     c = make_config(3, W=256, H=256, seed=31)
     fd = dev(c["f"])
-    mask_c, recs_c, mse_c = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"])
+    mask_c, recs_c, mse_c = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"], x0=1)
     masks = [r["mask"] for r in recs_c]
     mask_w, recs_w, mse_w = pipeline.densify(256, 256, fd, c["mask0"], c["unknowns"], c["schedule"],
                                              lockstep_masks=masks, warm_start=True)
@@ -448,7 +448,7 @@ def test_densify_warm_start():
         assert abs(rc["mse"] - rw["mse"]) <= 1e-6 * rc["mse"]
     # the same mask from a warm guess (the previous mask's solution) and from midrange
     Rp = pipeline.inpaint(256, 256, fd, masks[-2], c["unknowns"])
-    R0 = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"])
+    R0 = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"], x0=1)
     Rw = pipeline.inpaint(256, 256, fd, masks[-1], c["unknowns"], x0_unknown=Rp["u_vert"][: Rp["system"].n_u])
     assert Rw["iters"] < R0["iters"]
     assert torch.abs(R0["u_vert"] - Rw["u_vert"]).max().item() <= 1e-4
@@ -545,3 +545,76 @@ def test_tonal_channels_graph_mode():
         assert reps[c]["outer_iters"] == 5
         assert np.abs(gs[c].cpu().numpy() - go[c]).max() <= GREY_TOL
         assert abs(reps[c]["mse_after"] - oreps[c]["mse_after"]) <= MSE_RTOL * oreps[c]["mse_after"]
+
+
+def _fill_reference(S, g):
+    """Reading A11b, written out with numpy on the oracle's CSR (independent of the kernels):
+    each unknown takes the mask value of its most negative A_uk entry (first in ascending mask
+    index on ties); unknowns without one take their first filled A_uu neighbour (ascending
+    column) in two passes; the rest take midrange(g)."""
+    n = S.n_u
+    x = np.full(n, np.nan)
+    for i in range(n):
+        a, b = S.uk_ptr[i], S.uk_ptr[i + 1]
+        if b > a:
+            vals = S.uk_val[a:b]
+            k = int(np.argmin(vals))
+            if vals[k] < 0.0:
+                x[i] = g[S.uk_col[a + k]]
+    for _ in range(2):
+        y = x.copy()
+        for i in np.nonzero(np.isnan(x))[0]:
+            for c in S.uu_col[S.uu_ptr[i]:S.uu_ptr[i + 1]]:
+                if not np.isnan(x[c]):
+                    y[i] = x[c]
+                    break
+        x = y
+    x[np.isnan(x)] = 0.5 * (g.min() + g.max())
+    return x
+
+
+@pytest.mark.parametrize("W,graph", [(700, False), (2880, True)])
+def test_x0_mask_neighbour_fill(W, graph):
+    """Reading A11b: the default initial guess (x0 = 3). (a) The guess itself, returned untouched
+    by a 0-iteration exit (rtol so loose that x0 already meets it), equals the numpy fill on the
+    oracle's CSR bit for bit. (b) The solve from it reaches the midrange start's solution (both
+    to rtol 1e-10: grey values within 1e-6) in fewer iterations on the C5 recipe. (c) A constant
+    image is still reproduced exactly with 0 iterations (A16). (Systems below 8192 unknowns use
+    midrange instead -- see test_x0_fill_small_systems_use_midrange.)"""
+    c = make_config(5, W=W, H=W, seed=81)
+    fd = dev(c["f"])
+    mask = np.concatenate([c["mask0"], c["unknowns"][: 0]])
+    M = femi.Mesh(W, W, mask, c["unknowns"])
+    S = femi.System(M)
+    vert = M.export()["vert_px"]
+    g = pipeline.mask_values(fd, vert, S.n_u)
+    u = torch.empty(S.nv, dtype=torch.float64, device=DEV)
+    femi.inpaint_solve_batched([S], [g], [u], femi.cg_opts(rtol=1e300, x0=3))
+    O = oracle.System(W, W, mask, c["unknowns"])
+    ref = _fill_reference(O, c["f"].reshape(-1)[O.mask_px])
+    np.testing.assert_array_equal(u[: S.n_u].cpu().numpy(), ref)
+    u1 = torch.empty_like(u)
+    u3 = torch.empty_like(u)
+    _, it1, _ = femi.inpaint_solve_batched([S], [g], [u1], femi.cg_opts(rtol=1e-10, x0=1))
+    st, it3, rel = femi.inpaint_solve_batched([S], [g], [u3], femi.cg_opts(rtol=1e-10, x0=3))
+    assert st == 0 and rel[0] <= 1e-10
+    assert femi.solver_path(S) == ("graph_tma" if graph else "resident")
+    assert torch.abs(u1 - u3).max().item() <= 1e-6
+    assert it3[0] < it1[0], (it3, it1)
+    gc = torch.full_like(g, 42.375)
+    uc = torch.empty_like(u)
+    st, itc, _ = femi.inpaint_solve_batched([S], [gc], [uc], femi.cg_opts(rtol=1e-10, x0=3))
+    assert itc[0] == 0 and torch.all(uc == 42.375).item()
+
+
+def test_x0_fill_small_systems_use_midrange():
+    """Below 8192 unknowns (launch-latency-bound systems) x0 = 3 is the midrange start: the same
+    iterates as x0 = 1, bit for bit."""
+    c = make_config(1)
+    M = femi.Mesh(64, 64, c["mask"], c["unknowns"])
+    S = femi.System(M)
+    g = pipeline.mask_values(dev(c["f"]), M.export()["vert_px"], S.n_u)
+    u1, u3 = (torch.empty(S.nv, dtype=torch.float64, device=DEV) for _ in range(2))
+    _, i1, _ = femi.inpaint_solve_batched([S], [g], [u1], femi.cg_opts(x0=1))
+    _, i3, _ = femi.inpaint_solve_batched([S], [g], [u3], femi.cg_opts(x0=3))
+    assert i1[0] == i3[0] and torch.equal(u1, u3)
