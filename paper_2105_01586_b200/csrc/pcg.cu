@@ -260,6 +260,62 @@ __global__ void k_x0_fill_end(const RItem* __restrict__ items) {
     }
 }
 
+// Graph-mode prologue fusion: k_x0_fill_end + k_init_x + k_zero_ps in one pass (each row only
+// touches its own entries) and the lean-tail loop state reset.
+__global__ void k_init_xps(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    if (it.ls && blockIdx.x == 0 && threadIdx.x == 0) {
+        LoopState l = {};
+        l.iters = S->iters;
+        l.active = 1;
+        it.ls[0] = l;
+    }
+    const double x0v = (it.x0mode == 1 || it.x0mode == 3) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+        double x0 = x0v;
+        if (it.x0mode >= 2) {
+            const int nat = it.inv[i];
+            x0 = it.u_vert[nat];
+            if (it.x0mode == 3 && isnan(x0)) {  // not reached by the fill: midrange
+                x0 = x0v;
+                it.u_vert[nat] = x0;
+            }
+        }
+        it.x[i] = x0 / it.s[i];
+        it.p[i] = 0.0;
+        it.sv[i] = 0.0;
+    }
+}
+
+// Graph-mode epilogue fusion: k_finalize + k_copy_g (the mask entries of u_vert are g exactly)
+__global__ void k_finalize_g(const RItem* __restrict__ items) {
+    const RItem& it = items[blockIdx.y];
+    const CgState* S = it.st;
+    const double x0v = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    const int nmax = max(it.n, it.g ? it.m : 0);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nmax; i += gridDim.x * blockDim.x) {
+        if (it.g && i < it.m) it.u_vert[it.n + i] = it.g[i];
+        if (i >= it.n) continue;
+        const int nat = it.inv[i];
+        if (S->iters == 0 && it.x0mode >= 2 && S->bn2 != 0.0) continue;  // the guess in u_vert stays
+        double xi;
+        if (S->bn2 == 0.0) {
+            xi = 0.0;
+        } else if (S->iters == 0) {
+            xi = x0v;
+        } else {
+            double xh = it.x[i];
+            if (S->x_pend) {
+                xh = fma(S->alpha_pend, it.p[i], xh);
+                it.x[i] = xh;
+            }
+            xi = it.s[i] * xh;
+        }
+        it.u_vert[nat] = xi;
+    }
+}
+
 // Deterministic grid reduction helper: per-block partial, the last block sums in order.
 template <int NQ>
 __device__ __forceinline__ bool grid_partial(double (&v)[NQ], double* red, unsigned* cnt, double* shm) {
@@ -2453,13 +2509,12 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
         if ((s = chain((void*)k_x0_fill1, gk, bk, a_items))) return s;
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f1))) return s;
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f0))) return s;
-        if ((s = chain((void*)k_x0_fill_end, gk, bk, a_items))) return s;
         if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
-        if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
-    }
-    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
-    if (!restart)
+        if ((s = chain((void*)k_init_xps, gk, bk, a_items))) return s;  // fill end + x^0 + p = s = 0
         if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+    } else {
+        if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
+    }
     if ((s = chain(spmv_first, gsp, bsp, tma ? a_gt0 : a_gs, ssp))) return s;
     // FEMI_L2POL=3: the matrix stream (46 MB at C5) persists in L2 across iterations through an
     // access-policy window on the SpMV nodes; the vectors share the rest of the 126 MB
@@ -2527,9 +2582,8 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out) {
             bprev = sn;
         }
     }
-    if ((s = chain((void*)k_finalize, gk, bk, a_items))) return s;
+    if ((s = chain((void*)k_finalize_g, gk, bk, a_items))) return s;  // x -> u_vert and the mask entries
     if ((s = chain((void*)k_true_res, gk, bk, a_cnt1))) return s;
-    if ((s = chain((void*)k_copy_g, dim3(296), dim3(256), a_items))) return s;
     FEMI_CUDA(cudaGraphInstantiate(out, gr, 0));
     FEMI_CUDA(cudaGraphDestroy(gr));
     return FEMI_OK;
@@ -2640,8 +2694,10 @@ femi_status tile_split(const femi_system_s* S, int nblocks, std::vector<int32_t>
 femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, double* u_vert,
                         const femi_cg_opts& o, int32_t* iters, double* relres, cudaStream_t st,
                         int64_t* total_iters) {
-    static bool pre_set = false;
-    if (!pre_set) {
+    static int pre_set_dev = -1;  // __device__ switches live per device
+    int cur_dev = 0;
+    FEMI_CUDA(cudaGetDevice(&cur_dev));
+    if (pre_set_dev != cur_dev) {
         if (const char* e = std::getenv("FEMI_PDL_PRE")) {
             const int v = std::max(0, std::min(JNS, std::atoi(e)));
             FEMI_CUDA(cudaMemcpyToSymbol(g_pdl_pre, &v, sizeof(int)));
@@ -2655,7 +2711,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
             const int v = std::atoi(e) ? 1 : 0;
             FEMI_CUDA(cudaMemcpyToSymbol(g_smem_gather, &v, sizeof(int)));
         }
-        pre_set = true;
+        pre_set_dev = cur_dev;
     }
     GraphCache* C = (GraphCache*)S->scratch;
     const int64_t n = S->n_u;
@@ -2762,11 +2818,12 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         if (n > 0) {  // dmin = min_i diag(A_uu)_i, for skipping the residual monitor far from rtol
             unsigned long long* d_m = nullptr;
             unsigned long long h_m = ~0ull;
-            FEMI_CUDA(cudaMalloc(&d_m, sizeof(unsigned long long)));
-            FEMI_CUDA(cudaMemcpy(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice));
-            k_qmin<<<296, 256>>>(n, S->q_int, d_m);
-            FEMI_CUDA(cudaMemcpy(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost));
-            FEMI_CUDA(cudaFree(d_m));
+            FEMI_CUDA(cudaMallocAsync(&d_m, sizeof(unsigned long long), st));
+            FEMI_CUDA(cudaMemcpyAsync(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice, st));
+            k_qmin<<<296, 256, 0, st>>>(n, S->q_int, d_m);
+            FEMI_CUDA(cudaMemcpyAsync(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost, st));
+            FEMI_CUDA(cudaFreeAsync(d_m, st));
+            FEMI_CUDA(cudaStreamSynchronize(st));
             double dm;
             std::memcpy(&dm, &h_m, sizeof(dm));
             if (std::isfinite(dm) && dm > 0.0) it.dmin = dm * (1.0 - 1e-12);
@@ -2793,11 +2850,17 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.cta0 = 0;
         it.ncta = 1;
         it.nwin = S->nwin;
-        FEMI_CUDA(cudaMemset(C->d_cnt, 0, sizeof(unsigned) * 4));
-        S->scratch = C;
+        FEMI_CUDA(cudaMemsetAsync(C->d_cnt, 0, sizeof(unsigned) * 4, st));
         femi_status s = build_graph(*C, false, &C->main);
         if (s == FEMI_OK) s = build_graph(*C, true, &C->restart);
-        if (s != FEMI_OK) return s;
+        if (s != FEMI_OK) {  // publish the cache only once both graphs are instantiated
+            if (C->main) cudaGraphExecDestroy(C->main);
+            if (C->restart) cudaGraphExecDestroy(C->restart);
+            cudaFree(C->ws);
+            delete C;
+            return s;
+        }
+        S->scratch = C;
     }
     S->last_path = C->gt_smem > 0 ? FEMI_PATH_GRAPH_TMA : FEMI_PATH_GRAPH_SELL;
     RItem it = C->item;
@@ -3048,11 +3111,12 @@ femi_status graph_solve_multi(femi_system_s* S, int nr, const double* const* g, 
         {
             unsigned long long* d_m = nullptr;
             unsigned long long h_m = ~0ull;
-            FEMI_CUDA(cudaMalloc(&d_m, sizeof(unsigned long long)));
-            FEMI_CUDA(cudaMemcpy(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice));
-            k_qmin<<<296, 256>>>(n, S->q_int, d_m);
-            FEMI_CUDA(cudaMemcpy(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost));
-            FEMI_CUDA(cudaFree(d_m));
+            FEMI_CUDA(cudaMallocAsync(&d_m, sizeof(unsigned long long), st));
+            FEMI_CUDA(cudaMemcpyAsync(d_m, &h_m, sizeof(h_m), cudaMemcpyHostToDevice, st));
+            k_qmin<<<296, 256, 0, st>>>(n, S->q_int, d_m);
+            FEMI_CUDA(cudaMemcpyAsync(&h_m, d_m, sizeof(h_m), cudaMemcpyDeviceToHost, st));
+            FEMI_CUDA(cudaFreeAsync(d_m, st));
+            FEMI_CUDA(cudaStreamSynchronize(st));
             double dm;
             std::memcpy(&dm, &h_m, sizeof(dm));
             if (std::isfinite(dm) && dm > 0.0) dmin = dm * (1.0 - 1e-12);
@@ -3100,10 +3164,16 @@ femi_status graph_solve_multi(femi_system_s* S, int nr, const double* const* g, 
             it.ncta = 1;
             it.nwin = S->nwin;
         }
-        S->scratch_m[nr] = C;
         femi_status s = build_graph_m(*C, false, &C->main);
         if (s == FEMI_OK) s = build_graph_m(*C, true, &C->restart);
-        if (s != FEMI_OK) return s;
+        if (s != FEMI_OK) {  // publish the cache only once both graphs are instantiated
+            if (C->main) cudaGraphExecDestroy(C->main);
+            if (C->restart) cudaGraphExecDestroy(C->restart);
+            cudaFree(C->ws);
+            delete C;
+            return s;
+        }
+        S->scratch_m[nr] = C;
     }
     std::vector<RItem> its = C->items;
     for (int c = 0; c < nr; ++c) {
@@ -3240,9 +3310,12 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     static const int grid_nt[2] = {512, 768};
     static const int grid_per_sm[2] = {2, 1};
     auto nv_idx = [](int nv) { return nv == 0 ? 0 : (nv == 2 ? 1 : 2); };
-    if (g_smem_optin < 0) {
-        int dev = 0;
-        FEMI_CUDA(cudaGetDevice(&dev));
+    static int attr_dev = -1;  // function attributes are per device: redo them on a device change
+    int cur_dev = 0;
+    FEMI_CUDA(cudaGetDevice(&cur_dev));
+    if (attr_dev != cur_dev) {
+        attr_dev = cur_dev;
+        const int dev = cur_dev;
         FEMI_CUDA(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         FEMI_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
         for (int k = 0; k < 3; ++k) {
@@ -3460,14 +3533,14 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             void* args[5] = {(void*)&di, (void*)&bb, (void*)&vr, (void*)&nvec, (void*)&mrows};
             void* fn;
             if (mode == 3) {
-                static bool rz_attr = false;
-                if (!rz_attr) {
+                static int rz_attr_dev = -1;
+                if (rz_attr_dev != cur_dev) {
                     FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    g_smem_optin - 4096));
                     FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    g_smem_optin - 4096));
                     FEMI_CUDA(cudaFuncSetAttribute((void*)k_cgr<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-                    rz_attr = true;
+                    rz_attr_dev = cur_dev;
                 }
                 cfg.blockDim = dim3(RZT);
                 cfg.dynamicSmemBytes = rz_smem;
@@ -3540,6 +3613,8 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         k_copy_g<<<dim3((unsigned)std::min<int64_t>((mmax + 255) / 256, 296), gy), 256, 0, st>>>(d_items);
         count_launches(1);
         FEMI_CUDA(cudaGetLastError());
+        // the header promises a synchronised stream: u_vert's mask entries are written when we return
+        FEMI_CUDA(cudaStreamSynchronize(st));
     }
     femi_status ret = FEMI_OK;
     int64_t tot = 0;

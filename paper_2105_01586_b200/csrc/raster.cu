@@ -647,10 +647,12 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
         const char* e = std::getenv("FEMI_RASTER_MINB");
         return e && std::atoi(e) == 5;
     }();
-    static int resident = 0;
-    if (resident == 0) {
-        int dev = 0, nsm = 0, per = 0;
-        FEMI_CUDA(cudaGetDevice(&dev));
+    static int resident = 0, res_dev = -1;  // per device (occupancy and function attributes)
+    int cur_dev = 0;
+    FEMI_CUDA(cudaGetDevice(&cur_dev));
+    if (res_dev != cur_dev) {
+        res_dev = cur_dev;
+        int dev = cur_dev, nsm = 0, per = 0;
         FEMI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         FEMI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, minb5 ? (const void*)k_raster_grp<5, 1>
                                                                       : (const void*)k_raster_grp<4, 1>, RT,
@@ -679,15 +681,15 @@ femi_status launch_raster_items(std::vector<RasterItem>& items, int nc, cudaStre
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), bytes_items, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, bytes_cnt, st));
     const dim3 gr(gx, B);
-    static bool attr = false;
-    if (!attr) {  // colour: the per-warp triangle tables exceed the default 48 KB
+    static int attr_dev = -1;
+    if (attr_dev != cur_dev) {  // colour: the per-warp triangle tables exceed the default 48 KB
         FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(RWARPS * sizeof(GTri<2>))));
         FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(RWARPS * sizeof(GTri<3>))));
         FEMI_CUDA(cudaFuncSetAttribute((const void*)k_raster_grp<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(RWARPS * sizeof(GTri<4>))));
-        attr = true;
+        attr_dev = cur_dev;
     }
     switch (nc) {
         case 1:
