@@ -386,19 +386,31 @@ def run_ours(args):
         e2e = {"value": world * Npx * args.steps / (t_e2e * 1e-3) / 1e6, "unit": "Mpx/s",
                "h2d_bytes_per_step": int(8 * Npx + 8 * sysm.m), "d2h_bytes_per_step": 8}
 
-    # ---- roofline of the PCG loop (SURVEY §8(d) algorithmic bytes)
+    # ---- roofline of the dominant launch: the solve graph (SURVEY §8(d) algorithmic bytes). Per CG
+    # iteration 12 nnz_uu + 4 (n_u + 1) + 80 n_u; plus, once per solve, the prologue / epilogue
+    # kernels' algorithmic bytes: the right-hand side (12 nnz_uk + 4 (n_u + 1) + 8 m + 16 n_u), the
+    # mask-neighbour fill (one A_uk pass 12 nnz_uk + 4 (n_u + 1) + 8 n_u, two A_uu passes
+    # 2 (4 nnz_uu + 8 nnz_uu + 8 n_u)), x^0 + p = s = 0 (40 n_u), the initial residual and the first
+    # SpMV (2 (12 nnz_uu + 4 (n_u + 1) + 24 n_u)), finalize (32 n_u + 8 m) and the true residual
+    # (12 nnz_uu + 4 (n_u + 1) + 24 n_u)
     n_u, nnz_uu = info["n_unknown"], info["nnz_uu"]
+    nnz_uk, m_ = info["nnz_uk"], info["n_mask"]
     bytes_iter = 12 * nnz_uu + 4 * (n_u + 1) + 80 * n_u
+    fill = opts.x0 == 3 and n_u >= 8192
+    bytes_once = (12 * nnz_uk + 4 * (n_u + 1) + 8 * m_ + 16 * n_u
+                  + ((12 * nnz_uk + 4 * (n_u + 1) + 8 * n_u + 2 * (12 * nnz_uu + 8 * n_u)) if fill else 0)
+                  + 40 * n_u + (2 if fill else 1) * (12 * nnz_uu + 4 * (n_u + 1) + 24 * n_u)
+                  + 32 * n_u + 8 * m_ + 12 * nnz_uu + 4 * (n_u + 1) + 24 * n_u)
     iters = int(np.median(it_list))
     solve_s = float(np.median(solve_ms)) * 1e-3
-    achieved = bytes_iter * iters / solve_s / 1e9
+    achieved = (bytes_iter * iters + bytes_once) / solve_s / 1e9
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    traffic = None
+    traffic = None  # DRAM bytes of one solve-graph launch (ncu, stored under profiles/)
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"C{args.config}", {}).get("pcg_bytes_per_iter")
+            traffic = json.load(open(tf)).get(f"C{args.config}", {}).get("solve_graph_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -449,14 +461,17 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, c),
-            "roofline": {"bound": "hbm", "kernel": "PCG iteration (k_gu + k_gt in the graph WHILE loop)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "solve graph (prologue, PCG iterations k_gur + k_gt in the WHILE loop, epilogue)",
+                         "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                         "bytes_per_iter": bytes_iter, "iters": iters,
-                         "achieved_is": "algorithmic bytes per iteration (SURVEY 8(d): 12 nnz + 4 (n+1) + 80 n) x "
-                                        "iterations / solve event time -- an effective bandwidth: the CG vectors "
-                                        "stay in the 126 MB L2, DRAM moves `traffic` bytes per iteration",
-                         "dram_gbs": (traffic * iters / solve_s / 1e9) if traffic else None,
-                         "dram_frac": (traffic * iters / solve_s / 1e9 / hbm) if traffic else None,
+                         "bytes_per_iter": bytes_iter, "bytes_once_per_solve": bytes_once, "iters": iters,
+                         "achieved_is": "algorithmic bytes of the solve launch (SURVEY 8(d): 12 nnz + 4 (n+1) + 80 n per "
+                                        "iteration x iterations + the prologue/epilogue kernels' bytes) / its event time "
+                                        "-- an effective bandwidth: the CG vectors stay in the 126 MB L2; DRAM moves "
+                                        "`traffic` bytes per launch",
+                         "dram_gbs": (traffic / solve_s / 1e9) if traffic else None,
+                         "dram_frac": (traffic / solve_s / 1e9 / hbm) if traffic else None,
+                         "traffic_source": "profiles/traffic.json: ncu dram__bytes_read + _write of one solve-graph launch",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
             "detail": {"solve_ms": float(np.median(solve_ms)), "raster_ms": float(np.median(raster_ms)),
@@ -467,7 +482,7 @@ def run_ours(args):
                        # the second kernel of the step: the fused raster + error pass, 28 B/px
                        # algorithmic (list 4 + f 8 + u 8 + e 8) + 12 B/triangle, over its event time
                        "roofline_raster": {
-                           "kernel": "k_raster_tri + k_sse (S3+S4)", "bound": "hbm",
+                           "kernel": "k_raster_grp + k_sse (S3+S4)", "bound": "hbm",
                            "bytes": 28 * Npx + 12 * info["n_tri"],
                            "achieved": (28 * Npx + 12 * info["n_tri"]) / (float(np.median(raster_ms)) * 1e-3) / 1e9,
                            "peak": hbm, "unit": "GB/s",

@@ -206,9 +206,18 @@ femi_status launch_raster_channels(femi_system_s* S, int nc, const double* const
 femi_status launch_adjoint_raster(femi_system_s* S, const double* r, double* tri_w, cudaStream_t st);
 femi_status build_owner_tables(femi_system_s* S, cudaStream_t st);
 void pcg_cache_free(femi_system_s* S);  // graph-mode workspace + instantiated graphs
+// Device-side statistics of asynchronous solves (tonal loops): CG iterations and solves summed,
+// the first non-OK status kept (a solve whose true residual misses rtol: FEMI_E_NOT_CONVERGED)
+struct DevStats {
+    unsigned long long iters;
+    int32_t solves, status;
+};
+// ds == nullptr: the ABI behaviour (host outputs, host-side restart loop, synchronised stream).
+// ds != nullptr: asynchronous -- nothing is read back, one restart round runs on the device gated
+// by the true residual, and the outcome accumulates in *ds (stream-ordered).
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o, int32_t* iters, double* relres,
-                      cudaStream_t st, int64_t* total_iters);
+                      cudaStream_t st, int64_t* total_iters, DevStats* ds = nullptr);
 femi_status densify_select(femi_system_s* S, int nc, const double* const* f, const double* const* u_vert, int64_t b,
                            int32_t* new_px, int64_t* n_added, cudaStream_t st);
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,

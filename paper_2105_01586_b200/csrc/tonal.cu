@@ -121,6 +121,7 @@ struct Tonal {
     double* tri_w;  // 3T
     double* part;   // dot partials
     double* dres;   // dot result
+    DevStats* ds = nullptr;  // non-null: asynchronous inner solves (tonal_cgls), statistics on the device
     int64_t solves = 0, iters = 0;
     femi_status status = FEMI_OK;
     double t_solve = 0.0, t_dot = 0.0;  // FEMI_TONAL_PROF: host wall time in the inner solves / dots
@@ -165,7 +166,7 @@ struct Tonal {
         const double* gv[1] = {g};
         double* uvv[1] = {uv};
         const double ts0 = now();
-        femi_status s = pcg_solve(1, Sv, gv, nullptr, uvv, o, &it, &rr, st, &tot);
+        femi_status s = pcg_solve(1, Sv, gv, nullptr, uvv, o, &it, &rr, st, &tot, ds);
         t_solve += now() - ts0;
         ++solves;
         iters += tot;
@@ -191,7 +192,7 @@ struct Tonal {
         const double* bv[1] = {w};
         double* yvv[1] = {yv};
         const double ts0 = now();
-        femi_status s = pcg_solve(1, Sv, nullptr, bv, yvv, o, &it, &rr, st, &tot);
+        femi_status s = pcg_solve(1, Sv, nullptr, bv, yvv, o, &it, &rr, st, &tot, ds);
         t_solve += now() - ts0;
         ++solves;
         iters += tot;
@@ -211,7 +212,8 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t bytes = 3 * al(sizeof(double) * nv) + al(sizeof(double) * 3 * T) + al(sizeof(double) * 300) +
-                   al(sizeof(double) * 4) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m);
+                   al(sizeof(double) * 4) + 3 * al(sizeof(double) * N) + 2 * al(sizeof(double) * m) +
+                   al(sizeof(DevStats));
     void* base = nullptr;
     FEMI_CUDA(cudaMallocAsync(&base, bytes, st));
     char* cur = (char*)base;
@@ -235,6 +237,11 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     double* q = take(sizeof(double) * N);
     double* s = take(sizeof(double) * m);
     double* p = take(sizeof(double) * m);
+    // the inner solves run asynchronously (no host round trip per solve; restarts gated on the
+    // device); the host synchronises once per outer iteration for the CGLS scalars
+    tn.ds = (DevStats*)take(sizeof(DevStats));
+    FEMI_CUDA(cudaMemsetAsync(tn.ds, 0, sizeof(DevStats), st));
+    DevStats hds = {};
     femi_status rc = FEMI_OK;
 #define TRY(x)                      \
     do {                            \
@@ -288,6 +295,11 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
                 TRY(tn.apply_BT(r, s));
             }
             TRY(tn.dot(m, s, s, &gam2, gam_d, qq_d, &qq));  // gam_d <- s.s for the next alpha
+            FEMI_CUDA(cudaMemcpy(&hds, tn.ds, sizeof(DevStats), cudaMemcpyDeviceToHost));  // stream synchronised above
+            if (hds.status == FEMI_E_NONFINITE || hds.status == FEMI_E_NEG_CURVATURE) {
+                rc = (femi_status)hds.status;
+                goto out;
+            }
             if (!(qq > 0.0)) break;  // g and r were left unchanged (k_axpy_q)
             ++outer;
             relg = std::sqrt(gam2) / btf;
@@ -325,6 +337,12 @@ out:
     if (std::getenv("FEMI_TONAL_PROF"))
         std::fprintf(stderr, "[femi tonal] solves %lld (%lld CG iterations): %.3f ms in pcg_solve, %.3f ms in dots\n",
                      (long long)tn.solves, (long long)tn.iters, 1e3 * tn.t_solve, 1e3 * tn.t_dot);
+    if (cudaMemcpyAsync(&hds, tn.ds, sizeof(DevStats), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+        cudaStreamSynchronize(st) == cudaSuccess) {
+        tn.solves = hds.solves;
+        tn.iters = (int64_t)hds.iters;
+        tn.note((femi_status)hds.status);
+    }
     rep->inner_solves = (int32_t)tn.solves;
     rep->inner_iters = tn.iters;
     cudaFreeAsync(base, st);
