@@ -274,9 +274,16 @@ class BowyerWatson {
 // incident corners, neighbours and ownership flags, the CSR patterns of A_uu / A_uk with the
 // opposite-vertex tables, and the transpose of A_uk. Shared by build_mesh and insert_mesh.
 template <class Stamp>
-void mesh_tables(Mesh& M, int nthreads, Stamp&& stamp) {
+void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
     const int64_t nv = M.nv, T = M.T;
+    // small meshes (densification steps at C3 size) run on fewer threads: spawning 16 threads
+    // per pass costs more than the pass
+    const int nthreads = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads_max, T / 16384));
     auto parallel = [nthreads](int64_t n, auto&& fn) {
+        if (nthreads == 1) {
+            for (int64_t i = 0; i < n; ++i) fn(i);
+            return;
+        }
         std::vector<std::thread> th;
         for (int k = 0; k < nthreads; ++k)
             th.emplace_back([&, k] {
@@ -824,7 +831,7 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
                 if (vp[x.b] != vp[z.b]) return vp[x.b] < vp[z.b];
                 return vp[x.c] < vp[z.c];
             });
-    }, 64);
+    }, T < 65536 ? H : 64);
     M.T = T;
     M.tri.resize(3 * T);
     for (int64_t t = 0; t < T; ++t) {

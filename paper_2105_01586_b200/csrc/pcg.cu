@@ -3,8 +3,9 @@
 // B200 design. The Jacobi preconditioner is folded into the matrix at assembly
 // (A^ = D^-1/2 A D^-1/2, unit diagonal, only the off-diagonal part stored), so CG runs on
 // A^ x^ = b^ (x = D^-1/2 x^, b^ = D^-1/2 b). One solve =
-//   k_rhs          b = -A_uk g (or the given b), internal row order
-//   k_init_x/_r    x^0 and r0 = s b - A^ x^0, ||b||^2
+//   k_pro1         min/max of g, the fill's first hop, b = -A_uk g (or the given b), internal order
+//   k_x0_fill2 x2  the fill's second hop (x0 mode 3, reading A11b)
+//   k_pro2         x^0 and r0 = s (b - A x0) (unscaled rows)
 //   k_cg           ONE persistent launch running the whole CG loop on device
 //   k_finalize     x = D^-1/2 x^ scattered to canonical order (u_vert)
 //   k_true_res     ||b - A x|| with the unscaled matrix (reading A11); a failed check
@@ -158,78 +159,14 @@ __global__ void k_reset(int B, CgState* st, double rtol, int max_iter) {
     st[b] = s;
 }
 
-// min/max of g per item (x0 = midrange): blockIdx.y = item, one atomic pair per block
-__global__ void k_minmax(int B, const RItem* __restrict__ items) {
-    __shared__ unsigned long long slo[32], shi[32];
-    if ((int)blockIdx.y >= B) return;
-    const RItem& it = items[blockIdx.y];
-    if ((it.x0mode != 1 && it.x0mode != 3) || it.g == nullptr) return;
-    unsigned long long lo = ~0ull, hi = 0ull;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.m; k += gridDim.x * blockDim.x) {
-        const unsigned long long key = dkey(it.g[k]);
-        lo = min(lo, key);
-        hi = max(hi, key);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    if (lane == 0) {
-        slo[wid] = lo;
-        shi[wid] = hi;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        lo = lane < nw ? slo[lane] : ~0ull;
-        hi = lane < nw ? shi[lane] : 0ull;
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if (lane == 0 && hi != 0ull) {
-            atomicMin(&it.st->kmin, lo);
-            atomicMax(&it.st->kmax, hi);
-        }
-    }
-}
-
-// b = -A_uk g (ascending mask index, reading A6 order), or the given b; internal order
-__global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, unsigned* cnt);
-// x^0 = x0 / s (x0: midrange(g), 0 or the caller's u_vert)
-__global__ void k_init_x(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    const CgState* S = it.st;
-    const double x0v = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        const double x0 = (it.x0mode >= 2) ? it.u_vert[it.inv[i]] : x0v;  // caller's or the filled guess
-        it.x[i] = x0 / it.s[i];
-    }
-}
-
 // x0 mode 3, the mask-neighbour fill (reading A11b): the initial guess of an unknown is the value
 // of its most strongly coupled mask neighbour (the most negative A_uk entry of its row, ties ->
 // lowest mask index); an unknown without one takes the value of its first filled unknown
 // neighbour (ascending canonical column), over up to two hops; what is left takes midrange(g).
-// The guess is written to u_vert (canonical), then the solve proceeds as with a caller's x0
-// (mode 2): same solution (reading A11), ~15 % fewer iterations on the C5 recipe. A constant g
+// k_pro1 takes the first hop, k_x0_fill2 (u_vert -> w, w -> u_vert) the second, k_pro2 the
+// midrange leftovers. The guess is written to u_vert (canonical), then the solve proceeds as
+// with a caller's x0 (mode 2): same solution (reading A11), ~15 % fewer iterations on the C5 recipe. A constant g
 // fills every unknown with that constant exactly (A16 still holds).
-__global__ void k_x0_fill1(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    if (it.x0mode != 3) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        double v = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not filled yet
-        double best = 0.0;
-        for (int e = it.krp[i]; e < it.krp[i + 1]; ++e) {
-            const double a = it.kav[e];
-            if (a < best) {
-                best = a;
-                v = it.g[it.kci[e]];
-            }
-        }
-        it.u_vert[it.inv[i]] = v;
-    }
-}
 __global__ void k_x0_fill2(const RItem* __restrict__ items, int to_w) {
     const RItem& it = items[blockIdx.y];
     if (it.x0mode != 3) return;
@@ -249,45 +186,6 @@ __global__ void k_x0_fill2(const RItem* __restrict__ items, int to_w) {
         dst[nat] = v;
     }
 }
-__global__ void k_x0_fill_end(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    if (it.x0mode != 3) return;
-    const CgState* S = it.st;
-    const double x0v = 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax));
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        const int nat = it.inv[i];
-        if (isnan(it.u_vert[nat])) it.u_vert[nat] = x0v;
-    }
-}
-
-// Graph-mode prologue fusion: k_x0_fill_end + k_init_x + k_zero_ps in one pass (each row only
-// touches its own entries) and the lean-tail loop state reset.
-__global__ void k_init_xps(const RItem* __restrict__ items) {
-    const RItem& it = items[blockIdx.y];
-    const CgState* S = it.st;
-    if (it.ls && blockIdx.x == 0 && threadIdx.x == 0) {
-        LoopState l = {};
-        l.iters = S->iters;
-        l.active = 1;
-        it.ls[0] = l;
-    }
-    const double x0v = (it.x0mode == 1 || it.x0mode == 3) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        double x0 = x0v;
-        if (it.x0mode >= 2) {
-            const int nat = it.inv[i];
-            x0 = it.u_vert[nat];
-            if (it.x0mode == 3 && isnan(x0)) {  // not reached by the fill: midrange
-                x0 = x0v;
-                it.u_vert[nat] = x0;
-            }
-        }
-        it.x[i] = x0 / it.s[i];
-        it.p[i] = 0.0;
-        it.sv[i] = 0.0;
-    }
-}
-
 // Graph-mode epilogue fusion: k_finalize + k_copy_g (the mask entries of u_vert are g exactly)
 __global__ void k_finalize_g(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
@@ -396,35 +294,95 @@ __device__ __forceinline__ bool grid_partial(double (&v)[NQ], double* red, unsig
     return true;
 }
 
-// b = -A_uk g (internal rows, ascending mask index: reading A6 order) or the given b, and
-// ||b||^2 -> state. Unless the caller gave x0 (x0mode 2) the initial residual comes with it,
-// without an SpMV: x0 = c 1 (c = midrange(g), or 0) and A_uu 1 = -A_uk 1 (zero row sums of the
-// full stiffness matrix) give r0 = b - A_uu x0 = -A_uk (g - c 1); stored scaled, r^0 = s r0.
-__global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, unsigned* cnt) {
+// ---- fused prologue (every solve path): k_pro1 -> [k_x0_fill2 x 2] -> k_pro2 replaces
+// k_minmax -> k_x0_fill1 -> k_rhs -> [fill2 x 2] -> k_x0_fill_end -> k_init_x -> k_zero_ps ->
+// k_init_r: the A_uk rows are read once for the fill candidates and b, the A_uu rows once for
+// x^0 and r^0 = s (b - A x0), the true-residual form with the unscaled matrix (reading A11).
+
+// In-order walk of one CSR row, four entries per step: the column / value loads and the
+// gathers of a step are independent (memory-level parallelism for the latency-bound walk),
+// f(a, col, src[col]) is applied in entry order, so sums keep the sequential rounding.
+template <class F>
+__device__ __forceinline__ void row_walk4(int e0, int e1, const int* __restrict__ ci, const double* __restrict__ va,
+                                          const double* __restrict__ src, F&& f) {
+    for (int e = e0; e < e1; e += 4) {
+        int c[4];
+        double a[4], x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool ok = e + q < e1;
+            c[q] = ok ? ci[e + q] : -1;
+            a[q] = ok ? va[e + q] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = c[q] >= 0 ? src[c[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (e + q < e1) f(a[q], c[q], x[q]);
+    }
+}
+
+// pass 1: min/max of g (x0 modes 1, 3), the fill's first hop (mode 3: the value of the most
+// strongly coupled mask neighbour, the most negative A_uk entry, ties -> first), b = -A_uk g
+// (ascending mask index, reading A6 order) or the given b, r^0 for modes 0 and 1 with a
+// given b (x0 = 0: r0 = b), ||b||^2 -> state
+__global__ void __launch_bounds__(KNT) k_pro1(const RItem* __restrict__ items, unsigned* cnt) {
     __shared__ double shm[4 * (KNT / 32)];
+    __shared__ unsigned long long slo[KNT / 32], shi[KNT / 32];
     const RItem& it = items[blockIdx.y];
-    const CgState* S = it.st;
-    const bool direct = it.x0mode < 2;
-    const double c = (it.x0mode == 1) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    const int mode = it.x0mode;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if ((mode == 1 || mode == 3) && it.g != nullptr) {
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (int k = blockIdx.x * KNT + threadIdx.x; k < it.m; k += gridDim.x * KNT) {
+            const unsigned long long key = dkey(it.g[k]);
+            lo = min(lo, key);
+            hi = max(hi, key);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            slo[wid] = lo;
+            shi[wid] = hi;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            lo = lane < KNT / 32 ? slo[lane] : ~0ull;
+            hi = lane < KNT / 32 ? shi[lane] : 0ull;
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            }
+            if (lane == 0 && hi != 0ull) {
+                atomicMin(&it.st->kmin, lo);
+                atomicMax(&it.st->kmax, hi);
+            }
+        }
+    }
     double v[1] = {0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
-        double bi, r0;
+    for (int i = blockIdx.x * KNT + threadIdx.x; i < it.n; i += gridDim.x * KNT) {
+        double bi;
         if (it.bin) {
             bi = it.bin[it.inv[i]];
-            r0 = bi;  // x0 = 0 (x0mode 0)
+            if (mode < 2) it.r[i] = it.s[i] * bi;
         } else {
-            double acc = 0.0, accr = 0.0;
-            for (int e = it.krp[i]; e < it.krp[i + 1]; ++e) {
-                FEMI_DCHECK(it.kci[e] >= 0 && it.kci[e] < it.m, 3);
-                const double a = it.kav[e], gk = it.g[it.kci[e]];
-                acc = acc + a * gk;
-                accr = fma(a, gk - c, accr);
-            }
+            double acc = 0.0, best = 0.0;
+            double fv = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not filled yet
+            row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g, [&](double a, int k, double gk) {
+                FEMI_DCHECK(k >= 0 && k < it.m, 3);
+                acc = fma(a, gk, acc);
+                if (a < best) {
+                    best = a;
+                    fv = gk;
+                }
+            });
             bi = -acc;
-            r0 = -accr;
+            if (mode == 0) it.r[i] = it.s[i] * bi;
+            if (mode == 3) it.u_vert[it.inv[i]] = fv;
         }
         it.b[i] = bi;
-        if (direct) it.r[i] = it.s[i] * r0;
         v[0] += bi * bi;
     }
     if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) {
@@ -433,32 +391,50 @@ __global__ void __launch_bounds__(KNT) k_rhs(const RItem* __restrict__ items, un
     }
 }
 
-// r0 = s b - (x^ + A^_off x^) over SELL slices (warp per slice); ||b||^2 -> state
-__global__ void __launch_bounds__(KNT) k_init_r(const RItem* __restrict__ items, unsigned* cnt) {
-    __shared__ double shm[4 * (KNT / 32)];
+// pass 2 (after the fill's second hop): x^0 = x0 / s (mode 3: what the fill did not reach
+// takes midrange(g)), p = s = 0, the lean-tail loop state, and r^0 = s r0:
+//   mode 1 (x0 = c 1, no given b): r0 = -A_uk (g - c 1) (zero row sums: A_uu 1 = -A_uk 1);
+//   modes 2, 3: r0 = b - A_uu x0 over the unscaled rows (neighbours' x0 read from u_vert,
+//   with the same midrange substitution their own rows make).
+__global__ void __launch_bounds__(KNT) k_pro2(const RItem* __restrict__ items) {
     const RItem& it = items[blockIdx.y];
-    if (it.x0mode < 2) return;  // r^0 came with the right-hand side (k_rhs)
-    const int lane = threadIdx.x & 31;
-    const int nsl = (it.n + 31) / 32;
-    double v[1] = {0.0};
-    for (int s = (blockIdx.x * KNT + threadIdx.x) / 32; s < nsl; s += gridDim.x * (KNT / 32)) {
-        const int row = 32 * s + lane;
-        const int len = it.len[s], base = it.base[s] + lane, cb = (32 * s / SIG) * SIG;
-        double acc = 0.0;
-        for (int k = 0; k < len; ++k) {
-            const int e = base + 32 * k;
-            const int c = it.c16 ? cb + (int)it.c16[e] : it.c32[e];
-            acc = fma(it.val[e], it.x[c], acc);
-        }
-        if (row < it.n) {
-            const double bi = it.b[row];
-            it.r[row] = it.s[row] * bi - (it.x[row] + acc);
-            v[0] += bi * bi;
-        }
+    const CgState* S = it.st;
+    const int mode = it.x0mode;
+    if (it.ls && blockIdx.x == 0 && threadIdx.x == 0) {
+        LoopState l = {};
+        l.iters = S->iters;
+        l.active = 1;
+        it.ls[0] = l;
     }
-    if (grid_partial<1>(v, it.red, cnt + blockIdx.y, shm) && threadIdx.x == 0) {
-        it.st->bn2 = v[0];
-        it.st->tol2 = it.st->rtol * it.st->rtol * v[0];
+    const double x0v = (mode == 1 || mode == 3) ? 0.5 * (dkey_inv(S->kmin) + dkey_inv(S->kmax)) : 0.0;
+    for (int i = blockIdx.x * KNT + threadIdx.x; i < it.n; i += gridDim.x * KNT) {
+        double x0 = x0v;
+        if (mode >= 2) {
+            const int nat = it.inv[i];
+            x0 = it.u_vert[nat];
+            if (mode == 3 && isnan(x0)) {
+                x0 = x0v;
+                it.u_vert[nat] = x0;
+            }
+        }
+        const double si = it.s[i];
+        it.x[i] = x0 / si;
+        if (it.p) it.p[i] = 0.0;
+        if (it.sv) it.sv[i] = 0.0;
+        if (mode == 1 && !it.bin) {
+            double accr = 0.0;
+            row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g,
+                      [&](double a, int, double gk) { accr = fma(a, gk - x0v, accr); });
+            it.r[i] = si * -accr;
+        } else if (mode >= 2) {
+            double ax = 0.0;
+            row_walk4(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
+                FEMI_DCHECK(c >= 0 && c < it.n, 3);
+                if (mode == 3 && isnan(u)) u = x0v;
+                ax = fma(a, u, ax);
+            });
+            it.r[i] = si * (it.b[i] - ax);
+        }
     }
 }
 
@@ -497,10 +473,10 @@ __global__ void __launch_bounds__(KNT) k_true_res(const RItem* __restrict__ item
     double v[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
         double ax = 0.0;
-        for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) {
-            FEMI_DCHECK(it.uci[e] >= 0 && it.uci[e] < it.n, 3);
-            ax = fma(it.uav[e], it.u_vert[it.uci[e]], ax);
-        }
+        row_walk4(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
+            FEMI_DCHECK(c >= 0 && c < it.n, 3);
+            ax = fma(a, u, ax);
+        });
         const double ri = it.b[i] - ax;
         it.r[i] = it.s[i] * ri;
         v[0] += ri * ri;
@@ -2538,7 +2514,6 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out, bool 
     void* a_items[1] = {&di};
     void* a_reset[2] = {&one, &di};
     void* a_cnt0[2] = {&di, &cnt0};
-    void* a_cnt1[2] = {&di, &cnt1};
     void* a_gs[5] = {&di, &one, &part, &gcnt, &h};
     int lsi0 = 0;
     void* a_gt0[6] = {&di, &one, &part, &gcnt, &h, &lsi0};
@@ -2558,17 +2533,13 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out, bool 
     femi_status s = FEMI_OK;
     if (!restart) {
         if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
-        void* a_mm[2] = {&one, &di};
-        if ((s = chain((void*)k_minmax, dim3(296), dim3(256), a_mm))) return s;
         int tw1 = 1, tw0 = 0;
         void* a_f1[2] = {&di, &tw1};
         void* a_f0[2] = {&di, &tw0};
-        if ((s = chain((void*)k_x0_fill1, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_pro1, gk, bk, a_cnt0))) return s;  // minmax + fill hop 1 + b
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f1))) return s;
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f0))) return s;
-        if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
-        if ((s = chain((void*)k_init_xps, gk, bk, a_items))) return s;  // fill end + x^0 + p = s = 0
-        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
+        if ((s = chain((void*)k_pro2, gk, bk, a_items))) return s;  // fill end + x^0 + p = s = 0 + r^0
     } else {
         if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
     }
@@ -2978,6 +2949,41 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
     }
     // the body runs whole unrolled groups: kernels after convergence exit at once but still launch
     count_launches(2 * (int64_t)((hs.iters + kUnroll - 1) / kUnroll) * kUnroll);
+    if (std::getenv("FEMI_PROLOGUE_BENCH") && C->gt_smem > 0) {
+        // profiling aid: the solve graph's prologue / epilogue kernels launched one by one on the
+        // converged state (event times, median of 5) -- the graph itself cannot be split by ncu
+        cudaEvent_t e0, e1;
+        FEMI_CUDA(cudaEventCreate(&e0));
+        FEMI_CUDA(cudaEventCreate(&e1));
+        const dim3 gk(C->gx, 1), bk(KNT);
+        RItem* di = C->d_items;
+        unsigned* c0 = C->d_cnt;
+        unsigned* c1 = C->d_cnt + 1;
+        auto tm = [&](const char* name, auto launch) -> femi_status {
+            std::vector<float> v;
+            for (int k = 0; k < 7; ++k) {
+                FEMI_CUDA(cudaEventRecord(e0, st));
+                launch();
+                FEMI_CUDA(cudaEventRecord(e1, st));
+                FEMI_CUDA(cudaEventSynchronize(e1));
+                float x = 0.f;
+                FEMI_CUDA(cudaEventElapsedTime(&x, e0, e1));
+                if (k >= 2) v.push_back(x);
+            }
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, "[femi prologue] %-14s %8.2f us\n", name, 1e3 * v[v.size() / 2]);
+            return FEMI_OK;
+        };
+        tm("pro1", [&] { k_pro1<<<gk, bk, 0, st>>>(di, c0); });
+        tm("x0_fill2", [&] { k_x0_fill2<<<gk, bk, 0, st>>>(di, 1); });
+        tm("pro2", [&] { k_pro2<<<gk, bk, 0, st>>>(di); });
+        tm("finalize_g", [&] { k_finalize_g<<<gk, bk, 0, st>>>(di); });
+        tm("true_res", [&] { k_true_res<<<gk, bk, 0, st>>>(di, c1, nullptr); });
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        FEMI_CUDA(cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+    }
     if (std::getenv("FEMI_PCG_KBENCH") && C->gt_smem > 0 && C->item.ls) {
         // profiling aid: the loop body's kernels launched standalone on the converged state
         // (alpha = beta = 0 keeps the iterate), so ncu can capture them -- kernel nodes of a
@@ -3076,7 +3082,6 @@ femi_status build_graph_m(GraphCacheM& C, bool restart, cudaGraphExec_t* out) {
     void* a_items[1] = {&di};
     void* a_reset[2] = {&nr, &di};
     void* a_cnt0[2] = {&di, &cnt0};
-    void* a_cnt1[2] = {&di, &cnt1};
     void* a_t[3] = {&di, &part, &h};
     const dim3 gk(C.gx, nr), bk(KNT);
     cudaGraphNode_t prev = nullptr, nd;
@@ -3096,21 +3101,16 @@ femi_status build_graph_m(GraphCacheM& C, bool restart, cudaGraphExec_t* out) {
     femi_status s = FEMI_OK;
     if (!restart) {
         if ((s = chain((void*)k_reset_items, dim3(1), dim3(32), a_reset))) return s;
-        void* a_mm[2] = {&nr, &di};
-        if ((s = chain((void*)k_minmax, dim3(296, (unsigned)nr), dim3(256), a_mm))) return s;
         int tw1 = 1, tw0 = 0;
         void* a_f1[2] = {&di, &tw1};
         void* a_f0[2] = {&di, &tw0};
-        if ((s = chain((void*)k_x0_fill1, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_pro1, gk, bk, a_cnt0))) return s;
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f1))) return s;
         if ((s = chain((void*)k_x0_fill2, gk, bk, a_f0))) return s;
-        if ((s = chain((void*)k_x0_fill_end, gk, bk, a_items))) return s;
-        if ((s = chain((void*)k_rhs, gk, bk, a_cnt0))) return s;
-        if ((s = chain((void*)k_init_x, gk, bk, a_items))) return s;
+        if ((s = chain((void*)k_pro2, gk, bk, a_items))) return s;
+    } else {
+        if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
     }
-    if ((s = chain((void*)k_zero_ps, gk, bk, a_items))) return s;
-    if (!restart)
-        if ((s = chain((void*)k_init_r, gk, bk, a_cnt0))) return s;
     if ((s = chain(f_first, dim3(C.gt_blocks), dim3(JNT), a_t, C.smem))) return s;
     {
         cudaGraphNodeParams cp = {};
@@ -3568,25 +3568,15 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nmax + KNT - 1) / KNT, KGRID / B));
     k_reset<<<(B + 127) / 128, 128, 0, st>>>(B, d_state, o.rtol, o.max_iter);
     count_launches(1);
-    if (o.x0 == 1 || o.x0 == 3) {
-        int64_t mmax = 0;
-        for (int b = 0; b < B; ++b) mmax = std::max(mmax, S[b]->m);
-        k_minmax<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((mmax + 255) / 256, 296)), (unsigned)B), 256, 0,
-                   st>>>(B, d_items);
-        count_launches(1);
-    }
-    if (o.x0 == 3 && nmax > 0) {  // the mask-neighbour fill (reading A11b)
-        k_x0_fill1<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
-        k_x0_fill2<<<dim3(gx, gy), KNT, 0, st>>>(d_items, 1);
-        k_x0_fill2<<<dim3(gx, gy), KNT, 0, st>>>(d_items, 0);
-        k_x0_fill_end<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
-        count_launches(4);
-    }
-    if (nmax > 0) {
-        k_rhs<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
-        k_init_x<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
-        k_init_r<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
-        count_launches(3);
+    if (nmax > 0) {  // min/max of g, b, x^0 (the mask-neighbour fill of reading A11b for x0 = 3), r^0
+        k_pro1<<<dim3(gx, gy), KNT, 0, st>>>(d_items, d_cnt);
+        if (o.x0 == 3) {
+            k_x0_fill2<<<dim3(gx, gy), KNT, 0, st>>>(d_items, 1);
+            k_x0_fill2<<<dim3(gx, gy), KNT, 0, st>>>(d_items, 0);
+            count_launches(2);
+        }
+        k_pro2<<<dim3(gx, gy), KNT, 0, st>>>(d_items);
+        count_launches(2);
     }
     FEMI_CUDA(cudaGetLastError());
     std::vector<CgState> hs(B);
