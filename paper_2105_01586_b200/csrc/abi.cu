@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -28,19 +29,20 @@ femi_status cuda_fail(cudaError_t e, const char* what) {
 namespace {
 
 // Device memory of a system: arrays up to 2 MB are carved (256-byte aligned) from 8 MB arena
-// chunks, larger ones get their own allocation -- a small system then costs one or two
-// cudaMalloc/cudaFree instead of ~30 (each cudaFree synchronises the device).
+// chunks, larger ones get their own allocation; all of it from the stream-ordered pool on the
+// assembling stream (S->ast), released with cudaFreeAsync -- no device-wide synchronisation
+// per allocation or free.
 constexpr size_t kArenaChunk = 8u << 20, kArenaMax = 2u << 20;
 femi_status dev_alloc(femi_system_s* S, void** p, size_t bytes) {
     bytes = (std::max<size_t>(bytes, 1) + 255) & ~(size_t)255;
     if (bytes > kArenaMax) {
-        FEMI_CUDA(cudaMalloc(p, bytes));
+        FEMI_CUDA(cudaMallocAsync(p, bytes, S->ast));
         S->allocs.push_back(*p);
         return FEMI_OK;
     }
     if (S->arena_left < bytes) {
         void* c = nullptr;
-        FEMI_CUDA(cudaMalloc(&c, kArenaChunk));
+        FEMI_CUDA(cudaMallocAsync(&c, kArenaChunk, S->ast));
         S->arena_chunks.push_back(c);  // never in allocs: carved temporaries are not freed early
         S->arena_cur = (char*)c;
         S->arena_left = kArenaChunk;
@@ -51,13 +53,63 @@ femi_status dev_alloc(femi_system_s* S, void** p, size_t bytes) {
     return FEMI_OK;
 }
 
+// Pinned staging of the assemble uploads: a host array is copied into one pinned buffer and
+// sent with an asynchronous copy; a pageable cudaMemcpyAsync stages and waits on its own
+// (tens of us per call, ~25 calls per assemble -- a C3 densification step's tables are small).
+// One assemble at a time holds the buffer (others, and arrays that do not fit, go pageable);
+// the holder synchronises its stream before releasing it.
+struct PinnedStage {
+    std::mutex m;
+    char* buf = nullptr;
+    size_t cap = 0, used = 0;
+};
+PinnedStage g_stage;
+thread_local PinnedStage* t_stage = nullptr;
+constexpr size_t kStageBytes = 32u << 20;
+
+struct StageHold {
+    std::unique_lock<std::mutex> lk;
+    cudaStream_t st;
+    explicit StageHold(cudaStream_t s) : lk(g_stage.m, std::try_to_lock), st(s) {
+        if (!lk.owns_lock()) return;
+        if (!g_stage.buf) {
+            void* b = nullptr;
+            if (cudaHostAlloc(&b, kStageBytes, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            g_stage.buf = (char*)b;
+            g_stage.cap = kStageBytes;
+        }
+        g_stage.used = 0;
+        t_stage = &g_stage;
+    }
+    ~StageHold() {
+        if (t_stage) cudaStreamSynchronize(st);  // the copies have read the buffer
+        t_stage = nullptr;
+    }
+};
+
+femi_status h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return FEMI_OK;
+    if (t_stage && bytes <= t_stage->cap - t_stage->used) {
+        char* h = t_stage->buf + t_stage->used;
+        std::memcpy(h, src, bytes);
+        t_stage->used += (bytes + 255) & ~(size_t)255;
+        FEMI_CUDA(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st));
+        return FEMI_OK;
+    }
+    FEMI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return FEMI_OK;
+}
+
 template <class T>
 femi_status upload(femi_system_s* S, T** dst, const std::vector<T>& src, cudaStream_t st, size_t extra = 0) {
     size_t n = src.size() + extra;
     void* p = nullptr;
     femi_status s = dev_alloc(S, &p, sizeof(T) * std::max<size_t>(n, 1));
     if (s) return s;
-    if (!src.empty()) FEMI_CUDA(cudaMemcpyAsync(p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, st));
+    if ((s = h2d(p, src.data(), sizeof(T) * src.size(), st))) return s;
     *dst = (T*)p;
     return FEMI_OK;
 }
@@ -212,10 +264,10 @@ void femi_mesh_free(femi_mesh mesh) { delete mesh; }
 
 void femi_system_free(femi_system sys) {
     if (!sys) return;
-    cudaDeviceSynchronize();
+    cudaDeviceSynchronize();  // no work of any stream may still read the system
     pcg_cache_free(sys);
-    for (void* p : sys->allocs) cudaFree(p);
-    for (void* p : sys->arena_chunks) cudaFree(p);
+    for (void* p : sys->allocs) cudaFreeAsync(p, nullptr);
+    for (void* p : sys->arena_chunks) cudaFreeAsync(p, nullptr);
     delete sys;
 }
 
@@ -237,8 +289,10 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         std::fprintf(stderr, "assemble %-10s %.3f ms\n", what,
                      1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
     };
+    StageHold stage_hold(st);
     femi_system_s* S = new (std::nothrow) femi_system_s();
     if (!S) return FEMI_E_OOM;
+    S->ast = st;
     S->W = M.W;
     S->H = M.H;
     S->n_u = M.n_u;
@@ -375,6 +429,7 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         }, 512);
         S->nslices = nsl;
         S->sell_nnz = ent;
+        stamp("sell_host");
         U(upload(S, &S->sell_len, len, st));
         U(upload(S, &S->sell_base, base, st));
         S->sell_base_h = base;
@@ -545,7 +600,7 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
                     const size_t bc = al(std::max<size_t>(jcolb.size(), 1));
                     const size_t bm = al(std::max<size_t>(meta.size(), 1));
                     void* blk = nullptr;
-                    const cudaError_t e = cudaMalloc(&blk, bv + bc + bm);
+                    const cudaError_t e = cudaMallocAsync(&blk, bv + bc + bm, st);
                     if (e != cudaSuccess) {
                         s = cuda_fail(e, "assemble: matrix stream block");
                         goto fail;
@@ -555,16 +610,8 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
                     S->jds_col = (uint8_t*)blk + bv;
                     S->jds_meta = (uint8_t*)blk + bv + bc;
                     S->jds_block_bytes = bv + bc + bm;
-                    if (!jcolb.empty() && cudaMemcpyAsync(S->jds_col, jcolb.data(), jcolb.size(), cudaMemcpyHostToDevice,
-                                                          st) != cudaSuccess) {
-                        s = cuda_fail(cudaGetLastError(), "assemble: columns");
-                        goto fail;
-                    }
-                    if (!meta.empty() && cudaMemcpyAsync(S->jds_meta, meta.data(), meta.size(), cudaMemcpyHostToDevice,
-                                                         st) != cudaSuccess) {
-                        s = cuda_fail(cudaGetLastError(), "assemble: metadata");
-                        goto fail;
-                    }
+                    U(h2d(S->jds_col, jcolb.data(), jcolb.size(), st));
+                    U(h2d(S->jds_meta, meta.data(), meta.size(), st));
                 }
                 int32_t* d_js = nullptr;
                 U(upload(S, &d_js, jsrc, st));
@@ -591,7 +638,7 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         if (*it == (void*)d_tri || *it == (void*)d_flags || *it == (void*)S->sell_src_tmp ||
             (S->jds_src_tmp && *it == (void*)S->jds_src_tmp) || (S->ukI_src_tmp && *it == (void*)S->ukI_src_tmp) ||
             (S->uuI_src_tmp && *it == (void*)S->uuI_src_tmp)) {
-            cudaFree(*it);
+            cudaFreeAsync(*it, st);
             it = S->allocs.erase(it);
         } else {
             ++it;

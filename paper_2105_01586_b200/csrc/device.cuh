@@ -120,8 +120,12 @@ struct femi_system_s {
     void* scratch_m[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // multi-RHS graph caches (NR = 2..4)
     size_t scratch_bytes = 0;
     int32_t last_path = 0;  // FEMI_PATH_* of the last solve (femi_system_solver_path)
-    std::vector<void*> allocs;        // cudaMalloc'd large arrays
-    std::vector<void*> arena_chunks;  // cudaMalloc'd arena chunks (small arrays carved from them)
+    // device memory of the system comes from the stream-ordered pool (cudaMallocAsync on the
+    // assembling stream; the pool keeps freed memory, so a densification step's assemble and
+    // the previous system's release cost no cudaMalloc / cudaFree device synchronisation)
+    cudaStream_t ast = nullptr;
+    std::vector<void*> allocs;        // pooled large arrays
+    std::vector<void*> arena_chunks;  // pooled arena chunks (small arrays carved from them)
     char* arena_cur = nullptr;  // next free byte of the current arena chunk
     size_t arena_left = 0;
 };

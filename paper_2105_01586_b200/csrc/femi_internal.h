@@ -2,6 +2,7 @@
 #pragma once
 #include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -12,19 +13,25 @@ namespace femi {
 
 void set_error(const std::string& msg);
 
+// Host worker pool (up to 16 threads, created once): run_chunks(n, fn) calls fn(k) for
+// k in [0, n) on the pool and the calling thread, and returns when all have finished. A
+// densification step's tables at C3 size are ~0.1 ms passes, so spawning 16 threads per pass
+// (~0.3 ms) used to cost more than the work. A call made while another parallel region runs
+// (from a worker, or from a second host thread) runs its chunks inline.
+void run_chunks(int n, const std::function<void(int)>& fn);
+int pool_threads();
+
 // fn(lo, hi) over contiguous chunks of [0, n) on up to 16 host threads (one chunk when n is
 // below two grains)
 template <class F>
 void parallel_ranges(int64_t n, F&& fn, int64_t grain = 1 << 14) {
-    const int64_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int64_t hw = pool_threads();
     const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, n / std::max<int64_t>(1, grain)));
     if (nt <= 1) {
         if (n > 0) fn((int64_t)0, n);
         return;
     }
-    std::vector<std::thread> th;
-    for (int k = 0; k < nt; ++k) th.emplace_back([&, k] { fn(n * k / nt, n * (k + 1) / nt); });
-    for (auto& x : th) x.join();
+    run_chunks(nt, [&](int k) { fn(n * k / nt, n * (k + 1) / nt); });
 }
 
 // Host mesh (S0). Canonical numbering: unknowns (ascending pix) then masks (ascending pix).

@@ -13,6 +13,8 @@
 // tables the device kernels consume.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -24,6 +26,100 @@
 #include "femi_internal.h"
 
 namespace femi {
+
+namespace {
+struct ThreadPool {
+    std::mutex run_m;  // one parallel region at a time
+    std::mutex m;
+    std::condition_variable cv, cv_done;
+    std::vector<std::thread> th;
+    const std::function<void(int)>* job = nullptr;
+    int nchunks = 0, pending = 0, active = 0;
+    std::atomic<uint64_t> next{0};  // (region generation << 32) | next chunk index
+    uint64_t gen = 0;
+    explicit ThreadPool(int n) {
+        for (int k = 0; k < n; ++k) th.emplace_back([this] { worker(); });
+    }
+    // claims chunks of region `g` only: a worker that took its snapshot late never runs a chunk
+    // index of a later region with an earlier region's function
+    void drain(const std::function<void(int)>* j, int nc, uint64_t g) {
+        int done = 0;
+        for (;;) {
+            uint64_t v = next.load();
+            int k = -1;
+            while ((v >> 32) == (g & 0xffffffffu) && (int)(v & 0xffffffffu) < nc) {
+                if (next.compare_exchange_weak(v, v + 1)) {
+                    k = (int)(v & 0xffffffffu);
+                    break;
+                }
+            }
+            if (k < 0) break;
+            (*j)(k);
+            ++done;
+        }
+        std::lock_guard<std::mutex> l(m);
+        pending -= done;
+        if (pending == 0) cv_done.notify_all();
+    }
+    void worker() {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* j;
+            int nc;
+            {
+                std::unique_lock<std::mutex> l(m);
+                cv.wait(l, [&] { return gen != seen; });
+                seen = gen;
+                j = job;
+                nc = nchunks;
+                ++active;  // run() does not return (nor start the next region) while we hold j
+            }
+            drain(j, nc, seen);
+            std::lock_guard<std::mutex> l(m);
+            if (--active == 0) cv_done.notify_all();
+        }
+    }
+    void run(int n, const std::function<void(int)>& fn) {
+        std::unique_lock<std::mutex> r(run_m, std::try_to_lock);
+        if (!r.owns_lock()) {  // nested or concurrent region: inline
+            for (int k = 0; k < n; ++k) fn(k);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> l(m);
+            job = &fn;
+            nchunks = n;
+            pending = n;
+            ++gen;
+            next.store((gen & 0xffffffffu) << 32);
+        }
+        cv.notify_all();
+        drain(&fn, n, gen);
+        std::unique_lock<std::mutex> l(m);
+        cv_done.wait(l, [&] { return pending == 0 && active == 0; });
+        job = nullptr;
+    }
+};
+ThreadPool* g_pool() {
+    // never destroyed: workers stay blocked on the condition variable until process exit
+    static ThreadPool* p = new ThreadPool(std::max(0, pool_threads() - 1));
+    return p;
+}
+}  // namespace
+
+int pool_threads() {
+    static const int n = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    return n;
+}
+
+void run_chunks(int n, const std::function<void(int)>& fn) {
+    if (n <= 0) return;
+    if (n == 1 || pool_threads() == 1) {
+        for (int k = 0; k < n; ++k) fn(k);
+        return;
+    }
+    g_pool()->run(n, fn);
+}
 namespace {
 
 struct Pt {
@@ -276,21 +372,13 @@ class BowyerWatson {
 template <class Stamp>
 void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
     const int64_t nv = M.nv, T = M.T;
-    // small meshes (densification steps at C3 size) run on fewer threads: spawning 16 threads
-    // per pass costs more than the pass
-    const int nthreads = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads_max, T / 16384));
+    // tiny meshes run on fewer pool threads
+    const int nthreads = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads_max, T / 2048));
     auto parallel = [nthreads](int64_t n, auto&& fn) {
-        if (nthreads == 1) {
-            for (int64_t i = 0; i < n; ++i) fn(i);
-            return;
-        }
-        std::vector<std::thread> th;
-        for (int k = 0; k < nthreads; ++k)
-            th.emplace_back([&, k] {
-                int64_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
-                for (int64_t i = lo; i < hi; ++i) fn(i);
-            });
-        for (auto& x : th) x.join();
+        run_chunks(nthreads, [&](int k) {
+            const int64_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
+            for (int64_t i = lo; i < hi; ++i) fn(i);
+        });
     };
     // ---- vertex -> incident corners (ascending triangle index): atomic counting sort,
     // then each vertex's short list sorted
@@ -438,7 +526,7 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     const bool prof = std::getenv("FEMI_MESH_PROF") != nullptr;
     auto stamp = [&](const char* what) {
         if (prof)
-            std::fprintf(stderr, "mesh_build %-12s %.3f s\n", what,
+            std::fprintf(stderr, "mesh_build %-12s %.3f ms\n", what, 1e3 *
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
     };
     if ((m > 0 && !mask_px) || (p > 0 && !unknown_px) || m < 0 || p < 0) {
@@ -481,13 +569,10 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     const int nthreads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     M.threads = nthreads;
     auto parallel = [nthreads](int64_t n, auto&& fn) {
-        std::vector<std::thread> th;
-        for (int k = 0; k < nthreads; ++k)
-            th.emplace_back([&, k] {
-                int64_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
-                for (int64_t i = lo; i < hi; ++i) fn(i);
-            });
-        for (auto& x : th) x.join();
+        run_chunks(nthreads, [&](int k) {
+            const int64_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
+            for (int64_t i = lo; i < hi; ++i) fn(i);
+        });
     };
 
     // canonical vertex order: unknowns ascending, then masks ascending; plus the vertex ids
@@ -666,13 +751,9 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     };
     {
         std::atomic<int32_t> next{0};
-        std::vector<std::thread> th;
-        const int nt = std::min<int>(nthreads, nstrips);
-        for (int k = 0; k < nt; ++k)
-            th.emplace_back([&] {
-                for (int32_t s; (s = next.fetch_add(1)) < nstrips;) run_strip(s);
-            });
-        for (auto& x : th) x.join();
+        run_chunks(std::min<int>(nthreads, nstrips), [&](int) {
+            for (int32_t s; (s = next.fetch_add(1)) < nstrips;) run_strip(s);
+        });
     }
     if (prof) {
         int32_t tot = 0;
@@ -701,21 +782,18 @@ femi_status build_mesh(int32_t W, int32_t H, const int32_t* mask_px, int64_t m, 
     M.T = T;
     M.tri.resize(3 * T);
     {
-        std::vector<std::thread> th;
-        for (int k = 0; k < nthreads; ++k)
-            th.emplace_back([&, k] {
-                for (int32_t s = k; s < nstrips; s += nthreads) {
-                    int64_t o = toff[s];
-                    for (const Key& q : strip_keys[s]) {
-                        M.tri[3 * o] = q.a;
-                        M.tri[3 * o + 1] = q.b;
-                        M.tri[3 * o + 2] = q.c;
-                        ++o;
-                    }
-                    std::vector<Key>().swap(strip_keys[s]);
+        run_chunks(nthreads, [&](int k) {
+            for (int32_t s = k; s < nstrips; s += nthreads) {
+                int64_t o = toff[s];
+                for (const Key& q : strip_keys[s]) {
+                    M.tri[3 * o] = q.a;
+                    M.tri[3 * o + 1] = q.b;
+                    M.tri[3 * o + 2] = q.c;
+                    ++o;
                 }
-            });
-        for (auto& x : th) x.join();
+                std::vector<Key>().swap(strip_keys[s]);
+            }
+        });
     }
     stamp("canonical");
 
@@ -734,7 +812,7 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
     const bool prof = std::getenv("FEMI_MESH_PROF") != nullptr;
     auto stamp = [&](const char* what) {
         if (prof)
-            std::fprintf(stderr, "mesh_insert %-12s %.3f s\n", what,
+            std::fprintf(stderr, "mesh_insert %-12s %.3f ms\n", what, 1e3 *
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
     };
     if (b < 0 || (b > 0 && !px)) {
@@ -807,21 +885,25 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
         int32_t a, b, c;
     };
     std::vector<Key> keys(T);
+    std::vector<int32_t> krow(T);
     std::vector<int64_t> rp(H + 1, 0);
     const int32_t* vp = M.vpix.data();
-    for (int64_t t = 0; t < T; ++t) {
-        const int32_t* v = TR[t].v;
-        int k = 0;
-        if (vp[v[1]] < vp[v[k]]) k = 1;
-        if (vp[v[2]] < vp[v[k]]) k = 2;
-        keys[t] = {v[k], v[(k + 1) % 3], v[(k + 2) % 3]};
-        rp[vp[v[k]] / W + 1]++;
-    }
+    parallel_ranges(T, [&](int64_t lo, int64_t hi) {
+        for (int64_t t = lo; t < hi; ++t) {
+            const int32_t* v = TR[t].v;
+            int k = 0;
+            if (vp[v[1]] < vp[v[k]]) k = 1;
+            if (vp[v[2]] < vp[v[k]]) k = 2;
+            keys[t] = {v[k], v[(k + 1) % 3], v[(k + 2) % 3]};
+            krow[t] = vp[v[k]] / W;
+        }
+    }, 8192);
+    for (int64_t t = 0; t < T; ++t) rp[krow[t] + 1]++;
     for (int32_t y = 0; y < H; ++y) rp[y + 1] += rp[y];
     std::vector<Key> sorted(T);
     {
         std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
-        for (int64_t t = 0; t < T; ++t) sorted[fill[vp[keys[t].a] / W]++] = keys[t];
+        for (int64_t t = 0; t < T; ++t) sorted[fill[krow[t]]++] = keys[t];
     }
     std::vector<Key>().swap(keys);
     parallel_ranges(H, [&](int64_t lo, int64_t hi) {
@@ -831,14 +913,16 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
                 if (vp[x.b] != vp[z.b]) return vp[x.b] < vp[z.b];
                 return vp[x.c] < vp[z.c];
             });
-    }, T < 65536 ? H : 64);
+    }, 64);
     M.T = T;
     M.tri.resize(3 * T);
-    for (int64_t t = 0; t < T; ++t) {
-        M.tri[3 * t] = sorted[t].a;
-        M.tri[3 * t + 1] = sorted[t].b;
-        M.tri[3 * t + 2] = sorted[t].c;
-    }
+    parallel_ranges(T, [&](int64_t lo, int64_t hi) {
+        for (int64_t t = lo; t < hi; ++t) {
+            M.tri[3 * t] = sorted[t].a;
+            M.tri[3 * t + 1] = sorted[t].b;
+            M.tri[3 * t + 2] = sorted[t].c;
+        }
+    }, 8192);
     stamp("canonical");
     mesh_tables(M, nthreads, stamp);
     M.strips = 0;

@@ -612,7 +612,7 @@ femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     // raster windows: count per group, scan, allocate, fill (entries re-encoded in place)
     const int64_t ngroups = (T + GT - 1) / GT;
     const int nbg = (int)((ngroups + SCB - 1) / SCB);
-    FEMI_CUDA(cudaMalloc(&S->tp_wptr, sizeof(int32_t) * (ngroups + 1)));  // freed with the system
+    FEMI_CUDA(cudaMallocAsync(&S->tp_wptr, sizeof(int32_t) * (ngroups + 1), st));  // freed with the system
     S->allocs.push_back(S->tp_wptr);
     const int gw = (int)std::min<int64_t>((ngroups + RT - 1) / RT, 148 * 8);
     k_win<0><<<gw, RT, 0, st>>>(S->tri, T, S->tp_ptr, gk, nullptr, cnt, nullptr, nullptr);
@@ -623,7 +623,7 @@ femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     FEMI_CUDA(cudaMemcpyAsync(&nwin, S->tp_wptr + ngroups, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     FEMI_CUDA(cudaStreamSynchronize(st));
     S->tp_nwin = nwin;
-    FEMI_CUDA(cudaMalloc(&S->tp_win, sizeof(WinRec) * std::max<int64_t>(nwin, 1)));
+    FEMI_CUDA(cudaMallocAsync(&S->tp_win, sizeof(WinRec) * std::max<int64_t>(nwin, 1), st));
     S->allocs.push_back(S->tp_win);
     k_win<1><<<gw, RT, 0, st>>>(S->tri, T, S->tp_ptr, gk, S->tp_pix, nullptr, S->tp_wptr, (WinRec*)S->tp_win);
     count_launches(11);

@@ -221,6 +221,12 @@ class Mesh:
         out["tri"] = out["tri"].reshape(-1, 3)
         return out
 
+    def vert_px(self) -> np.ndarray:
+        """Pixel index of every vertex, canonical order (export()'s vert_px alone)."""
+        v = np.zeros(self.info["n_vert"], np.int32)
+        _check(lib().femi_mesh_export(self._h, _hptr(v), None, None, None, None, None))
+        return v
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.femi_mesh_free(self._h)

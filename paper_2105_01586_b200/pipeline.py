@@ -38,7 +38,7 @@ def inpaint(W, H, f_dev, mask_px, unknown_px, rtol=1e-10, want_images=True, stre
     if mesh is None:
         mesh = femi.Mesh(W, H, mask_px, unknown_px)
     sysm = femi.System(mesh, stream)
-    vert = mesh.export()["vert_px"]
+    vert = mesh.vert_px()
     g = mask_values(f_dev, vert, sysm.n_u)
     u_vert = torch.empty(sysm.nv, dtype=torch.float64, device=f_dev.device)
     if x0_unknown is not None and x0_unknown.numel() == sysm.n_u:
@@ -96,7 +96,7 @@ def tonal(W, H, f_dev, mask_px, unknown_px, outer_rtol=1e-8, outer_max=1000, inn
     _torch()
     mesh = femi.Mesh(W, H, mask_px, unknown_px)
     sysm = femi.System(mesh, stream)
-    vert = mesh.export()["vert_px"]
+    vert = mesh.vert_px()
     g = mask_values(f_dev, vert, sysm.n_u)
     st, rep = femi.tonal_optimise(sysm, f_dev.reshape(-1), g, outer_rtol, outer_max, femi.cg_opts(rtol=inner_rtol),
                                   stream)
@@ -108,7 +108,7 @@ def inpaint_channels(W, H, f_list, mask_px, unknown_px, rtol=1e-10, want_images=
     torch = _torch()
     mesh = femi.Mesh(W, H, mask_px, unknown_px)
     sysm = femi.System(mesh, stream)
-    vert = mesh.export()["vert_px"]
+    vert = mesh.vert_px()
     dev = f_list[0].device
     gs = [mask_values(f, vert, sysm.n_u) for f in f_list]
     us = [torch.empty(sysm.nv, dtype=torch.float64, device=dev) for _ in f_list]
