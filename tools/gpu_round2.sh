@@ -15,6 +15,9 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 timeout 300 python bench.py --config 1 --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_c1.json 2> $O/bench_c1.err
 for c in 2 3 4; do timeout 600 python bench.py --config $c --steps 3 --warmup 3 > $O/bench_c$c.json 2> $O/bench_c$c.err; done
 timeout 600 python bench.py --config 3 --steps 3 --warmup 3 --warm > $O/bench_c3w.json 2> $O/bench_c3w.err
+timeout 900 python bench.py --config 3 --n 100 --warm --steps 2 --warmup 1 > $O/bench_c3_n100w.json 2> $O/bench_c3_n100w.err
+timeout 300 python tools/diag_c3_host.py 5 > $O/c3_host_split.txt 2>&1
+FEMI_PROLOGUE_BENCH=1 timeout 300 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-tonal > /dev/null 2> $O/prologue.err
 timeout 900 python bench.py --config 6 --steps 5 --warmup 3 > $O/bench_c6.json 2> $O/bench_c6.err
 FEMI_LOOP_PROF=1 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-tonal --steps 2 --warmup 3 > $O/loop.json 2> $O/loop.err
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tonal"
