@@ -2620,6 +2620,13 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out, bool 
 }
 
 
+// profiling aid (FEMI_PCG_KBENCH): an empty kernel, to measure the fixed launch cost of the
+// k_gt configuration (148 x 544 threads, with and without its dynamic shared memory)
+__global__ void k_probe(int* p) {
+    extern __shared__ unsigned char probe_sm[];
+    if (p && threadIdx.x == 0 && blockIdx.x == 0) *p = (int)probe_sm[0];
+}
+
 // FEMI_LOOP_PROF=1: per-iteration timeline of the graph loop from %globaltimer stamps
 femi_status loop_prof_begin(cudaStream_t st) {
     std::vector<unsigned long long> init(4 * kLoopProfMax);
@@ -3036,6 +3043,23 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         if (flush_buf) FEMI_CUDA(cudaFree(flush_buf));
         std::fprintf(stderr, "[femi kbench] standalone k_gur %.2f us, k_gt %.2f us\n", 1e3 * tu / (reps - 2),
                      1e3 * tg / (reps - 2));
+        {
+            FEMI_CUDA(cudaFuncSetAttribute((const void*)k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)C->gt_smem));
+            float tp[2] = {0.f, 0.f};
+            for (int m = 0; m < 2; ++m)
+                for (int k = 0; k < reps; ++k) {
+                    FEMI_CUDA(cudaEventRecord(e1, st));
+                    k_probe<<<dim3(C->gt_blocks), JNT, m ? C->gt_smem : 0, st>>>(nullptr);
+                    FEMI_CUDA(cudaEventRecord(e2, st));
+                    FEMI_CUDA(cudaEventSynchronize(e2));
+                    float y = 0.f;
+                    FEMI_CUDA(cudaEventElapsedTime(&y, e1, e2));
+                    if (k >= 2) tp[m] += y;
+                }
+            std::fprintf(stderr, "[femi kbench] empty kernel %d x %d: %.2f us (no smem), %.2f us (%u B dynamic smem)\n",
+                         C->gt_blocks, JNT, 1e3 * tp[0] / (reps - 2), 1e3 * tp[1] / (reps - 2), C->gt_smem);
+        }
         FEMI_CUDA(cudaMemcpyAsync(C->d_state, &hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
         cudaEventDestroy(e0);

@@ -337,18 +337,19 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __res
         int nq0 = 0, ny0 = 0, nn = 0, ns0 = 0, ns1 = 0;
         uint32_t vn[RCH / 32];
         auto load_win = [&](int w) {
-            const WinRec& R = win[w];
-            nq0 = R.q0;
-            ny0 = R.y0;
-            nn = R.n;
+            // the record through the read-only path: {q0, y0, n} in one 8-byte load, two start bytes
+            const int2 h0 = __ldg(reinterpret_cast<const int2*>(win + w));
+            nq0 = h0.x;
+            ny0 = (int)(int16_t)(h0.y & 0xffff);
+            nn = (h0.y >> 16) & 0xff;
             if (lane < nt) {
-                ns0 = R.start[lane];
-                ns1 = R.start[lane + 1];
+                ns0 = __ldg(&win[w].start[lane]);
+                ns1 = __ldg(&win[w].start[lane + 1]);
             }
 #pragma unroll
             for (int h = 0; h < RCH / 32; ++h) {
                 const int k = 32 * h + lane;
-                vn[h] = k < nn ? gl[nq0 + k] : 0xffffffffu;
+                vn[h] = k < nn ? __ldg(gl + nq0 + k) : 0xffffffffu;
             }
         };
         if (w0 < w1) load_win(w0);
@@ -376,22 +377,20 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __res
                 const int w1v = G.A1[j] * px + G.B1[j] * py + G.C1[j];
                 const int w2v = G.A2[j] * px + G.B2[j] * py + G.C2[j];
                 const int Di = G.Di[j];
-                // vertex pixels: a (w_b = w_c = 0), b (w_b = D, w_c = 0), c (w_b = 0, w_c = D)
-                const int cls = (w1v == 0) ? (w2v == 0 ? 1 : (w2v == Di ? 3 : 0)) : ((w1v == Di && w2v == 0) ? 2 : 0);
-                double lb = 0.0, lc = 0.0;
-                if (!cls) {
-                    const double D = G.D[j], rD = G.rD[j];
-                    lb = div_rn((double)w1v, D, rD);
-                    lc = div_rn((double)w2v, D, rD);
-                }
+                // vertex pixels: a (w_b = w_c = 0), b (w_b = D, w_c = 0), c (w_b = 0, w_c = D);
+                // branch-free: the quotients are formed for every entry, the vertex value selected
+                const bool z1 = w1v == 0, z2 = w2v == 0;
+                const bool isa = z1 && z2, isb = w1v == Di && z2, isc = z1 && w2v == Di;
+                const bool cls = isa || isb || isc;
+                const double D = G.D[j], rD = G.rD[j];
+                const double lb = div_rn((double)w1v, D, rD);
+                const double lc = div_rn((double)w2v, D, rD);
                 double e = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NC; ++ch) {
-                    double u;
-                    if (cls == 0)
-                        u = __dadd_rn(__dadd_rn(G.ua[ch][j], __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
-                    else
-                        u = cls == 1 ? G.ua[ch][j] : (cls == 2 ? G.ub[ch][j] : G.uc[ch][j]);
+                    const double ui = __dadd_rn(__dadd_rn(G.ua[ch][j], __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
+                    const double uv = isb ? G.ub[ch][j] : (isc ? G.uc[ch][j] : G.ua[ch][j]);
+                    const double u = cls ? uv : ui;
                     if (it.u_px[ch]) __stcs(it.u_px[ch] + pix, u);  // streaming store (written once)
                     if (hasf) {
                         const double d = __dsub_rn(u, fv[h][ch]);
