@@ -262,10 +262,17 @@ __global__ void __launch_bounds__(RT) k_win(const TriRec* __restrict__ tri, int6
 // and the vertex values u_b, u_c (vertex pixels take them exactly).
 template <int NC>
 struct GTri {
-    int A1[GT], B1[GT], C1[GT], A2[GT], B2[GT], C2[GT], Di[GT], pad[GT];
-    double D[GT], rD[GT];
+    int AB1[GT], C1[GT], AB2[GT], C2[GT], Di[GT], pad[3][GT];  // AB = A & 0xffff | B << 16
+    double rD[GT];
     double ua[NC][GT], db[NC][GT], dc[NC][GT], ub[NC][GT], uc[NC][GT];
 };
+// |A|, |B| <= 16383 (coordinates < 2^14): the two plane coefficients share one word, so an
+// entry reads its triangle with 5 four-byte and 4 eight-byte shared loads (the vertex values
+// u_b, u_c only at vertex pixels, a predicated load); D is converted from the exact integer Di
+// (measured at C5: shared-load wavefronts 71 M -> 61 M, raster 0.686 -> 0.679 ms)
+__device__ __forceinline__ int ab_pack(int a, int b) { return (a & 0xffff) | (int)((unsigned)b << 16); }
+__device__ __forceinline__ int ab_lo(int v) { return (int)(v << 16) >> 16; }
+__device__ __forceinline__ int ab_hi(int v) { return v >> 16; }
 
 // S3+S4 in ONE pass over the raster windows of each 16-triangle group (groups handed out in
 // canonical order by an atomic counter). Per window of <= 128 entries (the group's owned pixels
@@ -310,15 +317,14 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __res
         if (lane < nt) {
             const TriRec R = it.tri[t0 + lane];
             const int ax = R.x[0], ay = R.y[0], bx = R.x[1], by = R.y[1], cx = R.x[2], cy = R.y[2];
-            G.A1[lane] = cy - ay;  // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx)
-            G.B1[lane] = ax - cx;
+            // w_b = orient(c,a,p) = (ax-cx)(py-cy) - (ay-cy)(px-cx) = A1 px + B1 py + C1
+            G.AB1[lane] = ab_pack(cy - ay, ax - cx);
             G.C1[lane] = (ay - cy) * cx - (ax - cx) * cy;
-            G.A2[lane] = ay - by;  // w_c = orient(a,b,p) = (bx-ax)(py-ay) - (by-ay)(px-ax)
-            G.B2[lane] = bx - ax;
+            // w_c = orient(a,b,p) = (bx-ax)(py-ay) - (by-ay)(px-ax) = A2 px + B2 py + C2
+            G.AB2[lane] = ab_pack(ay - by, bx - ax);
             G.C2[lane] = (by - ay) * ax - (bx - ax) * ay;
             const int Di = orient_xy(ax, ay, bx, by, cx, cy);
             G.Di[lane] = Di;
-            G.D[lane] = (double)Di;
             G.rD[lane] = __drcp_rn((double)Di);
 #pragma unroll
             for (int ch = 0; ch < NC; ++ch) {
@@ -374,22 +380,25 @@ __global__ void __launch_bounds__(RT, MINB) k_raster_grp(const RasterItem* __res
                 const int px = gl_x(v[h]), py = y0 + wl_dy(v[h]);
                 const int pix = py * W + px;
                 FEMI_DCHECK(j < nt && px < W && (int64_t)pix < it.N && wl_slot(v[h]) < RCH, 4);
-                const int w1v = G.A1[j] * px + G.B1[j] * py + G.C1[j];
-                const int w2v = G.A2[j] * px + G.B2[j] * py + G.C2[j];
+                const int ab1 = G.AB1[j], ab2 = G.AB2[j];
+                const int w1v = ab_lo(ab1) * px + ab_hi(ab1) * py + G.C1[j];
+                const int w2v = ab_lo(ab2) * px + ab_hi(ab2) * py + G.C2[j];
                 const int Di = G.Di[j];
                 // vertex pixels: a (w_b = w_c = 0), b (w_b = D, w_c = 0), c (w_b = 0, w_c = D);
                 // branch-free: the quotients are formed for every entry, the vertex value selected
                 const bool z1 = w1v == 0, z2 = w2v == 0;
                 const bool isa = z1 && z2, isb = w1v == Di && z2, isc = z1 && w2v == Di;
                 const bool cls = isa || isb || isc;
-                const double D = G.D[j], rD = G.rD[j];
+                const double D = (double)Di, rD = G.rD[j];
                 const double lb = div_rn((double)w1v, D, rD);
                 const double lc = div_rn((double)w2v, D, rD);
                 double e = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NC; ++ch) {
-                    const double ui = __dadd_rn(__dadd_rn(G.ua[ch][j], __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
-                    const double uv = isb ? G.ub[ch][j] : (isc ? G.uc[ch][j] : G.ua[ch][j]);
+                    const double ua = G.ua[ch][j];
+                    const double ui = __dadd_rn(__dadd_rn(ua, __dmul_rn(lb, G.db[ch][j])), __dmul_rn(lc, G.dc[ch][j]));
+                    double uv = ua;
+                    if (isb || isc) uv = *(isb ? &G.ub[ch][j] : &G.uc[ch][j]);  // predicated: vertex pixels only
                     const double u = cls ? uv : ui;
                     if (it.u_px[ch]) __stcs(it.u_px[ch] + pix, u);  // streaming store (written once)
                     if (hasf) {
