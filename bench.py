@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--warm", action="store_true", help="C3: warm-start each solve from the previous solution")
     ap.add_argument("--rebuild-mesh", action="store_true",
                     help="C3: build every densification mesh from scratch instead of inserting the new pixels")
+    ap.add_argument("--band", action="store_true",
+                    help="NEXT-4: ONE image over the torchrun ranks in row bands (solve + raster + error; strong scaling)")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="with --band at N=1: R bands of one process stepped in lockstep (single-GPU check)")
     ap.add_argument("--shard", action="store_true",
                     help="C2 under torchrun: split the 32 masks across ranks (strong scaling) instead of replicas")
     return ap.parse_args()
@@ -857,10 +861,105 @@ def run_colour(args):
     return 0
 
 
+def run_band(args):
+    """NEXT-4: one image's solve split into row bands (femi_band_*, multi.band_solve). Under
+    torchrun every rank owns one band (halo exchange + 4-double all-reduce per CG iteration over
+    NCCL); with --bands R at N = 1, R bands of one process step in lockstep (LoopbackComm). The
+    step is the band solve, the all-gather of the solution, the raster/error of each rank's triangle
+    share and the SSE all-reduce; strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    from paper_2105_01586_b200 import femi, multi, pipeline
+
+    c = workload_inputs(args.config, args.size)
+    W, H = c["W"], c["H"]
+    f_dev = torch.as_tensor(c["f"], dtype=torch.float64, device=dev).reshape(-1)
+    if c["kind"].startswith("densify"):
+        mask, _, _ = pipeline.densify(W, H, f_dev, c["mask0"], c["unknowns"], c["schedule"][:2], rtol=RTOL)
+    else:
+        mask = c["mask"]
+    mesh = femi.Mesh(W, H, mask, c["unknowns"])
+    vert = mesh.vert_px()
+    n_u = mesh.info["n_unknown"]
+    g = f_dev[torch.as_tensor(vert[n_u:], dtype=torch.int64, device=dev)].contiguous()
+    R = world if world > 1 else max(1, args.bands)
+    ranks = [rank] if world > 1 else list(range(R))
+    bands = [femi.Band(mesh, R, r) for r in ranks]
+    comm = multi.DistComm(bands[0]) if world > 1 else multi.LoopbackComm(bands)
+    # raster shares: triangle ranges over their image rows (femi_band_raster_system)
+    rsys = []
+    for r in ranks:
+        Sb, bi = femi.band_raster_system(mesh, R, r)
+        o, n = bi["y0"] * W, bi["rows"] * W
+        rsys.append((Sb, f_dev[o:o + n].contiguous(), torch.empty(n, dtype=torch.float64, device=dev),
+                     torch.empty(n, dtype=torch.float64, device=dev), torch.zeros(1, dtype=torch.float64, device=dev)))
+    u_vert = torch.empty(mesh.info["n_vert"], dtype=torch.float64, device=dev)
+    sse_t = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def step():
+        rep = multi.band_solve(comm, g, rtol=RTOL)
+        comm.gather_solution(u_vert, g)
+        sse_t.zero_()
+        for Sb, fb, ub, eb, sb in rsys:
+            femi.rasterise_error(Sb, u_vert, fb, sb, ub, eb)
+            sse_t.add_(sb)
+        comm.allreduce_scalar(sse_t)
+        return rep
+
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+    assert rep["converged"], rep
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            rep = step()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = multi.max_over_ranks(ms, device=dev)
+    if rank == 0:
+        info = [b.info for b in bands]
+        print(json.dumps({
+            "metric": "row-band FEM inpainting Mpixels/s (one image over N bands: solve+raster+error)", "value": W * H / (ms * 1e-3) / 1e6,
+            "unit": "Mpx/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C{args.config} {W}x{H}: PCG solve (rtol {RTOL}, x0 = midrange) over {R} row "
+                                   f"bands + all-gather of the solution + raster/error over {R} triangle shares + "
+                                   f"SSE all-reduce ({'NCCL ranks' if world > 1 else 'lockstep bands of one process'})",
+                       "W": W, "H": H, "bands": R, "parallelism": f"rowband{R}",
+                       "l2_flush": "inputs larger than L2 (f = 537 MB at C5)"},
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "clocks": clk.summary(),
+            "detail": {"iters": rep["iters"], "restarts": rep["restarts"], "rel_res": rep["rel_res"],
+                       "mse": float(sse_t.item()) / (W * H),
+                       "n_unknown": n_u, "halo": [i["n_halo"] for i in info], "send": [i["n_send"] for i in info],
+                       "peers": [i["n_peers"] for i in info]}}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.band:
+        return run_band(args)
     if args.config in (2, 3, 4):
         return run_workload(args)
     if args.config == 6:

@@ -328,6 +328,91 @@ typedef struct {
 femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, const femi_tonal_opts* opts,
                                    int32_t irls, double eps, femi_tonal_l1_report* report, femi_stream stream);
 
+/* ---------------------------------------------------------------------------------
+ * Row-band multi-GPU solve of ONE image ("very large
+ * images", L498-502 memory linear in the image size; the iteration is PAPER.md:L236-239's CG).
+ * Canonical unknowns are in ascending pixel order, so rank r of R owns the unknowns
+ * [row0, row1) = [n_u r / R, n_u (r+1) / R): a band of image rows, its rows of A_uu / A_uk
+ * assembled on its own device (reading A6 arithmetic). The band's rows reference HALO unknowns
+ * owned by other ranks (ascending canonical id, grouped by owner = peer); by the symmetry of
+ * A_uu, rank r's SEND list to peer q is r's rows with a column in q's band, ascending -- the same
+ * sequence as q's halo slots owned by r. Jacobi-PCG in single-reduction form on the unscaled
+ * A_uu, x^0 = midrange(g) (reading A11): per iteration ONE halo exchange and ONE all-reduce of
+ * four doubles. The caller sequences
+ *     begin -> [all-reduce dots] -> pack(0) -> [exchange] -> spmv(0) -> [all-reduce dots] ->
+ *     { update -> pack(0) -> [exchange] -> spmv(0) -> [all-reduce dots] }*  (status: done?)
+ *     -> pack(1) -> [exchange] -> spmv(1) -> [all-reduce dots] -> status (true residual)
+ * where [exchange] copies, for every peer p, send[send_off[p]..send_off[p+1]) of this rank to
+ * the peer and the peer's send segment for this rank into halo[recv_off[p]..recv_off[p+1]),
+ * and [all-reduce dots] sums the four doubles of `dots` over all ranks (NCCL, or a loopback
+ * over bands of one process). All arithmetic is in the library's kernels.
+ * ------------------------------------------------------------------------------- */
+typedef struct femi_band_s* femi_band;
+typedef struct {
+    int32_t nranks, rank;
+    int64_t n_unknown;   /* global unknowns */
+    int64_t row0, row1;  /* owned canonical unknowns [row0, row1) */
+    int64_t n_halo;      /* halo slots (unknowns of other bands the band's rows reference) */
+    int64_t n_send;      /* send slots over all peers */
+    int64_t nnz_uu, nnz_uk;  /* entries of the band's rows */
+    int32_t n_peers, pad;
+} femi_band_info;
+
+/* HOST only (no device): the band plan of `rank` of `nranks`. Errors: FEMI_E_ARG. */
+femi_status femi_band_plan(femi_mesh mesh, int32_t nranks, int32_t rank, femi_band_info* info);
+/* HOST only: the plan's arrays (each NULL-able; sizes from femi_band_plan): peer[n_peers];
+ * recv_off[n_peers+1] (halo slots per peer); send_off[n_peers+1]; halo_id[n_halo] (canonical
+ * unknown ids); send_row[n_send] (local rows, i.e. canonical id - row0); rowptr[nloc+1] and
+ * col[nnz_uu] of the band's A_uu rows in canonical entry order, columns local: c < nloc is the
+ * own row row0 + c, c >= nloc is halo slot c - nloc. */
+femi_status femi_band_plan_export(femi_mesh mesh, int32_t nranks, int32_t rank, int32_t* peer, int64_t* recv_off,
+                                  int64_t* send_off, int64_t* halo_id, int32_t* send_row, int32_t* rowptr,
+                                  int32_t* col);
+/* DEVICE: the band object on the current device (plan, band matrix assembled, vectors).
+ * Synchronises `stream`. Errors: FEMI_E_ARG, FEMI_E_CUDA, FEMI_E_OOM. */
+femi_status femi_band_create(femi_mesh mesh, int32_t nranks, int32_t rank, femi_stream stream, femi_band* out);
+femi_status femi_band_info_get(femi_band band, femi_band_info* info);
+/* Caller-owned DEVICE communication buffers (they must outlive the band's use): halo[n_halo]
+ * (written by the exchange), send[n_send] (written by pack), dots[4] (written by begin / spmv,
+ * all-reduced in place by the caller). */
+femi_status femi_band_set_buffers(femi_band band, double* halo, double* send, double* dots);
+/* DEVICE, enqueued: x^0, b = -A_uk g and r^0 of the band's rows; dots = (0, 0, 0, ||b_band||^2).
+ * g: DEVICE, all n_mask mask values (every rank holds g). rtol > 0: ||b - A x|| <= rtol ||b||. */
+femi_status femi_band_begin(femi_band band, const double* g, double rtol, femi_stream stream);
+/* DEVICE, enqueued: send = which ? x : u at the send rows. */
+femi_status femi_band_pack(femi_band band, int32_t which, femi_stream stream);
+/* DEVICE, enqueued (halo filled): which 0: w = A u, dots = (r.u, w.u, r.r, 0) of the band;
+ * which 1: r = b - A x (true residual, unscaled rows), dots = (0, 0, ||r_band||^2, 0). */
+femi_status femi_band_spmv(femi_band band, int32_t which, femi_stream stream);
+/* DEVICE, enqueued (dots all-reduced): one CG update, or none once ||r||^2 <= rtol^2 ||b||^2
+ * (the all-reduced ||b||^2 of begin is captured by the first spmv after it). */
+femi_status femi_band_update(femi_band band, femi_stream stream);
+/* After a true-residual spmv(1) that missed rtol: restart the recurrence from r = b - A x.
+ * Synchronises `stream`. */
+femi_status femi_band_restart(femi_band band, femi_stream stream);
+/* HOST outputs, synchronises `stream`: converged flag, CG iterations so far, dots4 = the first
+ * three doubles of the dots buffer and the all-reduced ||b||^2 (captured by the first spmv). */
+femi_status femi_band_status(femi_band band, femi_stream stream, int32_t* done, int32_t* iters, double* dots4);
+/* DEVICE, enqueued: the band's solution x (unknowns row0..row1-1, canonical) into u_local. */
+femi_status femi_band_result(femi_band band, double* u_local, femi_stream stream);
+void femi_band_free(femi_band band);
+
+/* DEVICE: the raster / error tables of rank `rank`'s share of the triangles -- the canonical range
+ * [t0, t1) = [T r / R, T (r+1) / R) -- over the image rows [y0, y0 + rows) its triangles touch
+ * (PAPER.md:L239-241, L262-265). Pixel ownership (reading A7) is per triangle, so the shares
+ * partition the pixels exactly as the whole mesh does. The result is a RASTER-ONLY femi_system:
+ * femi_rasterise_error(_batched / _channels) take it with a GLOBAL u_vert (n_vert, canonical; the
+ * triangles keep their global vertex ids) and band-local images f, u_px, e_px of rows x W
+ * starting at row y0 (each rank writes only the pixels its triangles own); tri_err / best are
+ * per band triangle (t - t0), best as a band-local pixel index (global = best + y0 W); sse is
+ * the band's share (all-reduce for the image's). Solve, densify and tonal calls reject it
+ * (FEMI_E_ARG). info (HOST, nullable) = {t0, t1, y0, rows}. Synchronises `stream`. */
+typedef struct {
+    int64_t t0, t1, y0, rows;
+} femi_band_raster_info;
+femi_status femi_band_raster_system(femi_mesh mesh, int32_t nranks, int32_t rank, femi_stream stream,
+                                    femi_system* out, femi_band_raster_info* info);
+
 #ifdef __cplusplus
 }
 #endif

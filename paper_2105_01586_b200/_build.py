@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfemi.so")
 OUT_CHECK = os.path.join(HERE, "libfemi_check.so")  # device bounds checks (FEMI_DEVICE_CHECKS)
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["abi.cu", "assemble.cu", "pcg.cu", "raster.cu", "select.cu", "tonal.cu", "mesh.cpp"]
+SOURCES = ["abi.cu", "assemble.cu", "pcg.cu", "raster.cu", "select.cu", "tonal.cu", "band.cu", "mesh.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-pthread", "-Xptxas", "-O3"]

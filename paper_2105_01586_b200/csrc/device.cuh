@@ -124,6 +124,7 @@ struct femi_system_s {
     // assembling stream; the pool keeps freed memory, so a densification step's assemble and
     // the previous system's release cost no cudaMalloc / cudaFree device synchronisation)
     cudaStream_t ast = nullptr;
+    bool raster_only = false;         // femi_band_raster_system: raster tables of a triangle range only
     std::vector<void*> allocs;        // pooled large arrays
     std::vector<void*> arena_chunks;  // pooled arena chunks (small arrays carved from them)
     char* arena_cur = nullptr;  // next free byte of the current arena chunk
@@ -189,6 +190,7 @@ int64_t dcheck_pcg(int64_t*);
 int64_t dcheck_raster(int64_t*);
 int64_t dcheck_select(int64_t*);
 int64_t dcheck_tonal(int64_t*);
+int64_t dcheck_band(int64_t*);
 
 constexpr int kSellSigma = 64;   // rows per SELL window (length-sorting scope)
 constexpr int kBand = 32;        // image band height (pixels) of the internal solver order

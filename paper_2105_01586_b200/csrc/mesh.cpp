@@ -108,7 +108,11 @@ ThreadPool* g_pool() {
 }  // namespace
 
 int pool_threads() {
-    static const int n = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    static const int n = [] {  // FEMI_POOL_THREADS=k caps the pool (diagnostics)
+        int k = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        if (const char* e = std::getenv("FEMI_POOL_THREADS")) k = std::max(1, std::min(k, std::atoi(e)));
+        return k;
+    }();
     return n;
 }
 

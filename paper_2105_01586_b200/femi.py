@@ -55,6 +55,16 @@ class TonalReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class BandInfo(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("n_unknown", ctypes.c_int64),
+                ("row0", ctypes.c_int64), ("row1", ctypes.c_int64), ("n_halo", ctypes.c_int64),
+                ("n_send", ctypes.c_int64), ("nnz_uu", ctypes.c_int64), ("nnz_uk", ctypes.c_int64),
+                ("n_peers", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
 class TonalL1Report(ctypes.Structure):
     _fields_ = [("irls_steps", ctypes.c_int32), ("outer_iters", ctypes.c_int32), ("inner_solves", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("inner_iters", ctypes.c_int64), ("l1_before", ctypes.c_double),
@@ -75,7 +85,10 @@ SYMBOLS = ["femi_last_error", "femi_version", "femi_kernel_launches", "femi_mesh
            "femi_densify_step", "femi_tonal_optimise", "femi_rasterise_error_channels",
            "femi_densify_step_channels", "femi_tonal_optimise_l1", "femi_mesh_insert",
            "femi_system_solver_path", "femi_apply_B", "femi_apply_BT", "femi_device_check_failures",
-           "femi_tonal_optimise_channels"]
+           "femi_tonal_optimise_channels", "femi_band_plan", "femi_band_plan_export", "femi_band_create",
+           "femi_band_info_get", "femi_band_set_buffers", "femi_band_begin", "femi_band_pack", "femi_band_spmv",
+           "femi_band_update", "femi_band_restart", "femi_band_status", "femi_band_result", "femi_band_free",
+           "femi_band_raster_system"]
 
 # femi_system_solver_path values (include/femi.h)
 PATH_NAMES = {0: "none", 1: "resident", 2: "persistent", 3: "graph_sell", 4: "graph_tma", 5: "graph_multi"}
@@ -120,8 +133,24 @@ def lib():
         L.femi_device_check_failures.argtypes = [ctypes.POINTER(ctypes.c_int64)]
         L.femi_apply_B.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
         L.femi_apply_BT.argtypes = [P, P, P, ctypes.POINTER(CgOpts), P]
+        L.femi_band_plan.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BandInfo)]
+        L.femi_band_plan_export.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
+        L.femi_band_create.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, ctypes.POINTER(P)]
+        L.femi_band_info_get.argtypes = [P, ctypes.POINTER(BandInfo)]
+        L.femi_band_set_buffers.argtypes = [P, P, P, P]
+        L.femi_band_begin.argtypes = [P, P, ctypes.c_double, P]
+        L.femi_band_pack.argtypes = [P, ctypes.c_int32, P]
+        L.femi_band_spmv.argtypes = [P, ctypes.c_int32, P]
+        L.femi_band_update.argtypes = [P, P]
+        L.femi_band_restart.argtypes = [P, P]
+        L.femi_band_status.argtypes = [P, P, I32P, I32P, P]
+        L.femi_band_result.argtypes = [P, P, P]
+        L.femi_band_free.argtypes = [P]
+        L.femi_band_free.restype = None
+        L.femi_band_raster_system.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, ctypes.POINTER(P),
+                                              ctypes.POINTER(ctypes.c_int64 * 4)]
         for name in SYMBOLS:
-            if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free",
+            if name not in ("femi_last_error", "femi_version", "femi_mesh_free", "femi_system_free", "femi_band_free",
                             "femi_kernel_launches", "femi_device_check_failures"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -454,3 +483,97 @@ def tonal_optimise_channels(system, f_list, g_list, outer_rtol=1e-8, outer_max=1
     if st not in (FEMI_OK, 4):
         _check(st)
     return st, [r.as_dict() for r in reps]
+
+
+# ------------------------------------------------------------------ row-band multi-GPU (NEXT-4)
+def band_plan(mesh: Mesh, nranks: int, rank: int) -> dict:
+    """HOST only: the band plan of `rank` (sizes and arrays; femi_band_plan / _export)."""
+    info = BandInfo()
+    _check(lib().femi_band_plan(mesh._h, nranks, rank, ctypes.byref(info)))
+    d = info.as_dict()
+    nloc = d["row1"] - d["row0"]
+    out = dict(info=d, peer=np.zeros(d["n_peers"], np.int32), recv_off=np.zeros(d["n_peers"] + 1, np.int64),
+               send_off=np.zeros(d["n_peers"] + 1, np.int64), halo_id=np.zeros(d["n_halo"], np.int64),
+               send_row=np.zeros(d["n_send"], np.int32), rowptr=np.zeros(nloc + 1, np.int32),
+               col=np.zeros(d["nnz_uu"], np.int32))
+    _check(lib().femi_band_plan_export(mesh._h, nranks, rank, *(_hptr(out[k]) for k in (
+        "peer", "recv_off", "send_off", "halo_id", "send_row", "rowptr", "col"))))
+    return out
+
+
+class Band:
+    """One rank's band of a row-band solve (femi_band_*): the communication buffers are torch
+    tensors owned here and handed to the library; the exchange / all-reduce are the caller's
+    (paper_2105_01586_b200.multi)."""
+
+    def __init__(self, mesh: Mesh, nranks: int, rank: int, stream=None):
+        import torch
+        self._lib = lib()
+        h = ctypes.c_void_p()
+        _check(self._lib.femi_band_create(mesh._h, nranks, rank, _stream(stream), ctypes.byref(h)))
+        self._h = h
+        info = BandInfo()
+        _check(self._lib.femi_band_info_get(h, ctypes.byref(info)))
+        self.info = info.as_dict()
+        plan = band_plan(mesh, nranks, rank)
+        self.peer, self.recv_off, self.send_off = plan["peer"], plan["recv_off"], plan["send_off"]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.halo = torch.zeros(max(self.info["n_halo"], 1), dtype=torch.float64, device=dev)
+        self.send = torch.zeros(max(self.info["n_send"], 1), dtype=torch.float64, device=dev)
+        self.dots = torch.zeros(4, dtype=torch.float64, device=dev)
+        _check(self._lib.femi_band_set_buffers(h, _dptr(self.halo), _dptr(self.send), _dptr(self.dots)))
+        self.row0, self.row1 = self.info["row0"], self.info["row1"]
+
+    def begin(self, g, rtol, stream=None):
+        _check(self._lib.femi_band_begin(self._h, _dptr(g, _f64()), float(rtol), _stream(stream)))
+
+    def pack(self, which, stream=None):
+        _check(self._lib.femi_band_pack(self._h, int(which), _stream(stream)))
+
+    def spmv(self, which, stream=None):
+        _check(self._lib.femi_band_spmv(self._h, int(which), _stream(stream)))
+
+    def update(self, stream=None):
+        _check(self._lib.femi_band_update(self._h, _stream(stream)))
+
+    def restart(self, stream=None):
+        _check(self._lib.femi_band_restart(self._h, _stream(stream)))
+
+    def status(self, stream=None):
+        done, iters = ctypes.c_int32(), ctypes.c_int32()
+        d = np.zeros(4, np.float64)
+        _check(self._lib.femi_band_status(self._h, _stream(stream), ctypes.byref(done), ctypes.byref(iters), _hptr(d)))
+        return bool(done.value), int(iters.value), d
+
+    def result(self, u_local, stream=None):
+        _check(self._lib.femi_band_result(self._h, _dptr(u_local, _f64()), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.femi_band_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def band_raster_system(mesh: Mesh, nranks: int, rank: int, stream=None):
+    """Raster-only System over rank `rank`'s triangle share (femi_band_raster_system); returns
+    (system, {'t0', 't1', 'y0', 'rows'})."""
+    h = ctypes.c_void_p()
+    info = (ctypes.c_int64 * 4)()
+    _check(lib().femi_band_raster_system(mesh._h, nranks, rank, _stream(stream), ctypes.byref(h), ctypes.byref(info)))
+    S = System.__new__(System)
+    S._lib = lib()
+    S._h = h
+    mi = MeshInfo()
+    _check(lib().femi_system_info_get(h, ctypes.byref(mi)))
+    S.info = mi.as_dict()
+    S.W, S.H = S.info["width"], S.info["height"]
+    S.n_u, S.m, S.nv, S.T = (S.info[k] for k in ("n_unknown", "n_mask", "n_vert", "n_tri"))
+    return S, dict(zip(("t0", "t1", "y0", "rows"), (int(v) for v in info)))
+
+
+def _f64():
+    import torch
+    return torch.float64

@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 reps = sys.argv[1] if len(sys.argv) > 1 else "3"
-env = dict(os.environ, FEMI_MESH_PROF="1", FEMI_ASM_PROF="1")
+env = dict(os.environ, FEMI_MESH_PROF="1", FEMI_ASM_PROF=os.environ.get("FEMI_ASM_PROF", "1"))
 p = subprocess.run([sys.executable, "tools/diag_c3_host.py", reps], env=env, capture_output=True, text=True)
 print(p.stdout)
 tot = collections.OrderedDict()
