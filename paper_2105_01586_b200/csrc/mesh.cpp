@@ -370,6 +370,25 @@ class BowyerWatson {
 
 }  // namespace
 
+// ascending sort of a short range (a vertex's corners, a row's edge pairs: ~6-12 entries):
+// insertion sort, longer ranges std::sort
+template <class T>
+inline void small_sort(T* a, T* b) {
+    if (b - a > 32) {
+        std::sort(a, b);
+        return;
+    }
+    for (T* p = a + 1; p < b; ++p) {
+        const T x = *p;
+        T* q = p;
+        while (q > a && x < *(q - 1)) {
+            *q = *(q - 1);
+            --q;
+        }
+        *q = x;
+    }
+}
+
 // Everything after the triangulation (M.tri canonical; M.vpix, counts set): vertex ->
 // incident corners, neighbours and ownership flags, the CSR patterns of A_uu / A_uk with the
 // opposite-vertex tables, and the transpose of A_uk. Shared by build_mesh and insert_mesh.
@@ -388,7 +407,16 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
     // then each vertex's short list sorted
     M.vt_ptr.assign(nv + 1, 0);
     M.vt_idx.resize(3 * T);
-    {
+    if (T < (1 << 21)) {
+        // sequential counting sort: the corners are visited in ascending order, so every
+        // vertex's list comes out ascending -- no atomics (a locked add costs ~20 cycles even
+        // uncontended) and no per-vertex sort
+        int32_t* cnt = M.vt_ptr.data() + 1;
+        for (int64_t q = 0; q < 3 * T; ++q) ++cnt[M.tri[q]];
+        for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
+        std::vector<int32_t> fill(M.vt_ptr.begin(), M.vt_ptr.end() - 1);
+        for (int64_t q = 0; q < 3 * T; ++q) M.vt_idx[fill[M.tri[q]]++] = (int32_t)q;
+    } else {
         int32_t* cnt = M.vt_ptr.data() + 1;
         parallel(3 * T, [&](int64_t q) { __atomic_fetch_add(&cnt[M.tri[q]], 1, __ATOMIC_RELAXED); });
         for (int64_t v = 0; v < nv; ++v) M.vt_ptr[v + 1] += M.vt_ptr[v];
@@ -396,7 +424,7 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
         parallel(3 * T, [&](int64_t q) {
             M.vt_idx[__atomic_fetch_add(&fill[M.tri[q]], 1, __ATOMIC_RELAXED)] = (int32_t)q;
         });
-        parallel(nv, [&](int64_t v) { std::sort(M.vt_idx.begin() + M.vt_ptr[v], M.vt_idx.begin() + M.vt_ptr[v + 1]); });
+        parallel(nv, [&](int64_t v) { small_sort(M.vt_idx.data() + M.vt_ptr[v], M.vt_idx.data() + M.vt_ptr[v + 1]); });
     }
     stamp("vt");
     // ---- neighbours across edges, ownership flags (reading A7)
@@ -406,11 +434,12 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
         uint32_t fl = 0;
         for (int k = 0; k < 3; ++k) {
             int32_t a = M.tri[3 * t + (k + 1) % 3], b = M.tri[3 * t + (k + 2) % 3];
+            // the neighbour holds the edge as b -> a: its corner at a (vt entry 3s + j) has the
+            // previous vertex b -- one compare per incident corner
             int32_t nb = -1;
             for (int32_t q = M.vt_ptr[a]; q < M.vt_ptr[a + 1]; ++q) {
-                int32_t s = M.vt_idx[q] / 3;
-                if (s == t) continue;
-                if (M.tri[3 * s] == b || M.tri[3 * s + 1] == b || M.tri[3 * s + 2] == b) {
+                const int32_t c = M.vt_idx[q], s = c / 3, j = c - 3 * s;
+                if (s != t && M.tri[3 * s + (j + 2) % 3] == b) {
                     nb = s;
                     break;
                 }
@@ -426,7 +455,9 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
     stamp("nbr");
     // ---- CSR patterns of A_uu (with diagonal) and A_uk, with opposite-vertex tables
     const int64_t n_u = M.n_u;
-    std::vector<int32_t> cnt_uu(n_u, 0), cnt_uk(n_u, 0);
+    // ONE pass over the rows: each chunk of rows writes its rows' entries (column, two opposite
+    // vertices; the diagonal in place, A_uu and A_uk apart) into a chunk buffer and counts them;
+    // after the row-pointer prefix the buffers are copied into place
     auto row_entries = [&](int64_t i, std::vector<std::pair<int32_t, int32_t>>& e) {
         e.clear();
         for (int32_t q = M.vt_ptr[i]; q < M.vt_ptr[i + 1]; ++q) {
@@ -435,18 +466,48 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
             e.push_back({j1, j2});  // edge (i,j1) has opposite vertex j2 in t
             e.push_back({j2, j1});
         }
-        std::sort(e.begin(), e.end());
+        small_sort(e.data(), e.data() + e.size());
     };
+    struct Ent {
+        int32_t j, o1, o2;
+    };
+    std::vector<int32_t> cnt_uu(n_u, 0), cnt_uk(n_u, 0);
+    std::vector<std::vector<Ent>> buf_uu(nthreads), buf_uk(nthreads);
     parallel(nthreads, [&](int64_t k) {
         std::vector<std::pair<int32_t, int32_t>> e;
-        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
+        std::vector<Ent>& bu = buf_uu[k];
+        std::vector<Ent>& bk = buf_uk[k];
+        const int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
+        bu.reserve(7 * (hi - lo));
+        bk.reserve(4 * (hi - lo));
         for (int64_t i = lo; i < hi; ++i) {
             row_entries(i, e);
-            int32_t cu = 1, ck = 0;  // diagonal
-            for (size_t q = 0; q < e.size(); ++q) {
-                if (q > 0 && e[q].first == e[q - 1].first) continue;
-                if (e[q].first < n_u) ++cu;
-                else ++ck;
+            int32_t cu = 0, ck = 0;
+            bool diag_done = false;
+            for (size_t q = 0; q < e.size();) {
+                int32_t j = e[q].first, o1 = e[q].second, o2 = -1;
+                size_t r = q + 1;
+                if (r < e.size() && e[r].first == j) {
+                    o2 = e[r].second;
+                    ++r;
+                }
+                q = r;
+                if (j < n_u) {
+                    if (!diag_done && j > i) {
+                        bu.push_back({(int32_t)i, -1, -1});
+                        ++cu;
+                        diag_done = true;
+                    }
+                    bu.push_back({j, o1, o2});
+                    ++cu;
+                } else {
+                    bk.push_back({(int32_t)(j - n_u), o1, o2});
+                    ++ck;
+                }
+            }
+            if (!diag_done) {
+                bu.push_back({(int32_t)i, -1, -1});
+                ++cu;
             }
             cnt_uu[i] = cu;
             cnt_uk[i] = ck;
@@ -464,45 +525,22 @@ void mesh_tables(Mesh& M, int nthreads_max, Stamp&& stamp) {
     M.uk_col.resize(nuk);
     M.uk_opp.resize(2 * nuk);
     parallel(nthreads, [&](int64_t k) {
-        std::vector<std::pair<int32_t, int32_t>> e;
-        int64_t lo = n_u * k / nthreads, hi = n_u * (k + 1) / nthreads;
-        for (int64_t i = lo; i < hi; ++i) {
-            row_entries(i, e);
-            int32_t pu = M.uu_rowptr[i], pk = M.uk_rowptr[i];
-            bool diag_done = false;
-            for (size_t q = 0; q < e.size();) {
-                int32_t j = e[q].first, o1 = e[q].second, o2 = -1;
-                size_t r = q + 1;
-                if (r < e.size() && e[r].first == j) {
-                    o2 = e[r].second;
-                    ++r;
-                }
-                q = r;
-                if (j < n_u) {
-                    if (!diag_done && j > i) {
-                        M.uu_col[pu] = (int32_t)i;
-                        M.uu_opp[2 * pu] = -1;
-                        M.uu_opp[2 * pu + 1] = -1;
-                        ++pu;
-                        diag_done = true;
-                    }
-                    M.uu_col[pu] = j;
-                    M.uu_opp[2 * pu] = o1;
-                    M.uu_opp[2 * pu + 1] = o2;
-                    ++pu;
-                } else {
-                    M.uk_col[pk] = (int32_t)(j - n_u);
-                    M.uk_opp[2 * pk] = o1;
-                    M.uk_opp[2 * pk + 1] = o2;
-                    ++pk;
-                }
-            }
-            if (!diag_done) {
-                M.uu_col[pu] = (int32_t)i;
-                M.uu_opp[2 * pu] = -1;
-                M.uu_opp[2 * pu + 1] = -1;
-            }
+        const int64_t lo = n_u * k / nthreads;
+        int64_t pu = M.uu_rowptr[lo], pk = M.uk_rowptr[lo];
+        for (const Ent& x : buf_uu[k]) {
+            M.uu_col[pu] = x.j;
+            M.uu_opp[2 * pu] = x.o1;
+            M.uu_opp[2 * pu + 1] = x.o2;
+            ++pu;
         }
+        for (const Ent& x : buf_uk[k]) {
+            M.uk_col[pk] = x.j;
+            M.uk_opp[2 * pk] = x.o1;
+            M.uk_opp[2 * pk + 1] = x.o2;
+            ++pk;
+        }
+        std::vector<Ent>().swap(buf_uu[k]);
+        std::vector<Ent>().swap(buf_uk[k]);
     });
 
     stamp("csr");
@@ -861,7 +899,17 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
         }
     }
     std::vector<Pt> P(nv);
-    for (int64_t v = 0; v < nv; ++v) P[v] = {M.vpix[v] % W, M.vpix[v] / W, M.vpix[v]};
+    // (x, y) of every vertex without a division per vertex: unknowns and masks are two
+    // ascending pixel runs, so the row advances monotonically within each
+    for (int64_t r0 : {(int64_t)0, n_u}) {
+        const int64_t r1 = r0 == 0 ? n_u : nv;
+        int32_t y = r1 > r0 ? M.vpix[r0] / W : 0;
+        for (int64_t v = r0; v < r1; ++v) {
+            const int32_t p = M.vpix[v];
+            while (p >= (y + 1) * W) ++y;
+            P[v] = {p - y * W, y, p};
+        }
+    }
     stamp("renumber");
     // prev's triangles with the new vertex ids, then the new points
     std::vector<Tri> tr(prev.T);
@@ -881,50 +929,62 @@ femi_status insert_mesh(const Mesh& prev, const int32_t* px, int64_t b, Mesh& M)
         for (auto& kv : order) bw.insert(kv.second);
     }
     stamp("insert");
-    // canonical triangles: rotate (smallest pix first), order by (pix a, pix b, pix c) --
-    // bucketed by the row of a, each row sorted
+    // canonical triangles: rotate (smallest pix first), order by (pix a, pix b, pix c) -- a
+    // counting sort by the pixel rank of a (the vertex ranks by pixel merge the two ascending
+    // runs, unknowns and masks), then the few triangles sharing one a by (pix b, pix c):
+    // O(T + nv), no comparison sort of random keys
     const auto& TR = bw.tris();
     const int64_t T = (int64_t)TR.size();
     struct Key {
-        int32_t a, b, c;
+        int32_t a, b, c, pb, pc;
     };
-    std::vector<Key> keys(T);
-    std::vector<int32_t> krow(T);
-    std::vector<int64_t> rp(H + 1, 0);
     const int32_t* vp = M.vpix.data();
+    std::vector<int32_t> prank(nv);
+    {
+        int64_t i = 0, j = n_u, o = 0;
+        while (i < n_u || j < nv) {
+            if (j >= nv || (i < n_u && vp[i] < vp[j])) prank[i++] = (int32_t)o++;
+            else prank[j++] = (int32_t)o++;
+        }
+    }
+    std::vector<Key> keys(T);
+    std::vector<int32_t> off(nv + 1, 0);
     parallel_ranges(T, [&](int64_t lo, int64_t hi) {
         for (int64_t t = lo; t < hi; ++t) {
             const int32_t* v = TR[t].v;
             int k = 0;
             if (vp[v[1]] < vp[v[k]]) k = 1;
             if (vp[v[2]] < vp[v[k]]) k = 2;
-            keys[t] = {v[k], v[(k + 1) % 3], v[(k + 2) % 3]};
-            krow[t] = vp[v[k]] / W;
+            const int32_t a = v[k], b = v[(k + 1) % 3], c = v[(k + 2) % 3];
+            keys[t] = {a, b, c, vp[b], vp[c]};
         }
-    }, 8192);
-    for (int64_t t = 0; t < T; ++t) rp[krow[t] + 1]++;
-    for (int32_t y = 0; y < H; ++y) rp[y + 1] += rp[y];
+    }, 16384);
+    for (int64_t t = 0; t < T; ++t) ++off[prank[keys[t].a] + 1];
+    for (int64_t r = 0; r < nv; ++r) off[r + 1] += off[r];
     std::vector<Key> sorted(T);
     {
-        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
-        for (int64_t t = 0; t < T; ++t) sorted[fill[krow[t]]++] = keys[t];
+        std::vector<int32_t> fill(off.begin(), off.end() - 1);
+        for (int64_t t = 0; t < T; ++t) sorted[fill[prank[keys[t].a]]++] = keys[t];
     }
     std::vector<Key>().swap(keys);
-    parallel_ranges(H, [&](int64_t lo, int64_t hi) {
-        for (int64_t y = lo; y < hi; ++y)
-            std::sort(sorted.begin() + rp[y], sorted.begin() + rp[y + 1], [vp](const Key& x, const Key& z) {
-                if (vp[x.a] != vp[z.a]) return vp[x.a] < vp[z.a];
-                if (vp[x.b] != vp[z.b]) return vp[x.b] < vp[z.b];
-                return vp[x.c] < vp[z.c];
-            });
-    }, 64);
     M.T = T;
     M.tri.resize(3 * T);
-    parallel_ranges(T, [&](int64_t lo, int64_t hi) {
-        for (int64_t t = lo; t < hi; ++t) {
-            M.tri[3 * t] = sorted[t].a;
-            M.tri[3 * t + 1] = sorted[t].b;
-            M.tri[3 * t + 2] = sorted[t].c;
+    parallel_ranges(nv, [&](int64_t lo, int64_t hi) {
+        for (int64_t r = lo; r < hi; ++r) {  // insertion sort of each (small) group of one a
+            for (int32_t q = off[r] + 1; q < off[r + 1]; ++q) {
+                const Key x = sorted[q];
+                int32_t z = q - 1;
+                while (z >= off[r] && (sorted[z].pb > x.pb || (sorted[z].pb == x.pb && sorted[z].pc > x.pc))) {
+                    sorted[z + 1] = sorted[z];
+                    --z;
+                }
+                sorted[z + 1] = x;
+            }
+            for (int32_t q = off[r]; q < off[r + 1]; ++q) {
+                M.tri[3 * q] = sorted[q].a;
+                M.tri[3 * q + 1] = sorted[q].b;
+                M.tri[3 * q + 2] = sorted[q].c;
+            }
         }
     }, 8192);
     stamp("canonical");
