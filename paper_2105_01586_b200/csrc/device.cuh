@@ -120,6 +120,7 @@ struct femi_system_s {
     void* scratch_m[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // multi-RHS graph caches (NR = 2..4)
     size_t scratch_bytes = 0;
     int32_t last_path = 0;  // FEMI_PATH_* of the last solve (femi_system_solver_path)
+    void* rz_cache = nullptr;  // whole-solve resident kernel: halo codes / lists / send lists (pcg.cu)
     // device memory of the system comes from the stream-ordered pool (cudaMallocAsync on the
     // assembling stream; the pool keeps freed memory, so a densification step's assemble and
     // the previous system's release cost no cudaMalloc / cudaFree device synchronisation)

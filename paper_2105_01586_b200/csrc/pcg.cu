@@ -97,9 +97,30 @@ struct RItem {
     CgState* st;
     LoopState* ls;  // graph mode (lean tail): ls[2]
     double *r1, *w1, *s1;  // graph mode, fused iteration (k_gf): the second buffers of r, w, s
+    // whole-solve resident kernel (k_cgs): per SELL entry the 16-bit index into the CTA's
+    // extended vector (own rows | halo), per CTA the halo (canonical-internal rows it reads from
+    // peers, ascending) and the send list (src row | peer << 12 | peer's halo slot << 16), both at
+    // the CTA's first entry offset; rzn[0..16) halo counts, rzn[16..32) send counts
+    uint16_t* rzc;
+    int32_t* rzh;
+    int32_t* rzs;
+    int32_t* rzn;
+    int32_t rzhmax, rzpad;
     int32_t n, m, cta0, ncta, nwin, x0mode;
     double rtol;  // graph mode reads the options from the item (the graph is reused)
     int32_t max_iter, pad2;
+};
+
+// per-system tables of the whole-solve resident kernel for one cluster size (k_rz_halo / k_rz_send)
+struct RzCache {
+    int C = 0;
+    void* block = nullptr;  // code | halo | send | counts
+    uint16_t* code = nullptr;
+    int32_t* halo = nullptr;
+    int32_t* snd = nullptr;
+    int32_t* cnt = nullptr;  // [32] (device)
+    int32_t cnt_h[32] = {};  // host copy: halo counts [0, 16), send counts [16, 32)
+    int32_t hmax = 0;
 };
 
 constexpr int RNT = 512;  // threads per CTA of the persistent solver (block/cluster modes)
@@ -316,6 +337,27 @@ __device__ __forceinline__ void row_walk4(int e0, int e1, const int* __restrict_
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) x[q] = c[q] >= 0 ? src[c[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (e + q < e1) f(a[q], c[q], x[q]);
+    }
+}
+
+// the same walk with the gathers through L2 (ld.global.cg): data another CTA of the launch wrote
+template <class F>
+__device__ __forceinline__ void row_walk4cg(int e0, int e1, const int* __restrict__ ci, const double* __restrict__ va,
+                                            const double* src, F&& f) {
+    for (int e = e0; e < e1; e += 4) {
+        int c[4];
+        double a[4], x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool ok = e + q < e1;
+            c[q] = ok ? ci[e + q] : -1;
+            a[q] = ok ? va[e + q] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = c[q] >= 0 ? __ldcg(src + c[q]) : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             if (e + q < e1) f(a[q], c[q], x[q]);
@@ -1052,6 +1094,564 @@ __global__ void __launch_bounds__(RZT, 1) k_cgr(const RItem* __restrict__ items,
     if (rank == 0 && tid == 0) {
         S->iters = iters;
         S->status = status;
+    }
+    rz_sync<CL>();  // no CTA leaves while others may still read its shared memory
+}
+
+// ---- halo tables of the whole-solve resident kernel (built once per system and cluster size).
+// CTA k of a C-CTA cluster owns the internal rows [R0, R1) (whole windows); the columns of its
+// entries outside that range form its HALO (ascending, deduplicated through a bitmap of all n
+// rows); an entry's code is its index into the CTA's extended vector: own row - R0, or
+// HB + halo slot with HB = 32 x the largest slice count of the cluster. Because the pattern is
+// symmetric, a row c of CTA o is in CTA k's halo iff c has a neighbour in k; CTA o's send list
+// holds (c - R0_o, k, slot) for every such pair (found by binary search in k's sorted halo), at
+// most one per remote entry of o, so it fits in o's entry range.
+__device__ __forceinline__ int rz_row0(int n, int nwin, int C, int k) { return min(n, (nwin * k / C) * SIG); }
+
+__global__ void __launch_bounds__(512) k_rz_halo(const RItem* __restrict__ items, int C) {
+    extern __shared__ unsigned int bm[];  // [nw] bitmap of halo rows | [nw] exclusive prefix popcounts
+    const RItem& it = items[blockIdx.x / C];
+    if (!it.rzc) return;  // the item's tables exist
+    const int k = blockIdx.x % C, n = it.n, nwin = it.nwin;
+    const int R0 = rz_row0(n, nwin, C, k), R1 = rz_row0(n, nwin, C, k + 1);
+    const int S0 = R0 / 32, S1 = (R1 + 31) / 32, nsl = S1 - S0;
+    const int e0 = nsl > 0 ? it.base[S0] : 0;
+    int nslm = 0;
+    for (int q = 0; q < C; ++q) nslm = max(nslm, (rz_row0(n, nwin, C, q + 1) + 31) / 32 - rz_row0(n, nwin, C, q) / 32);
+    const int HB = 32 * nslm;
+    const int nw = (n + 31) / 32;
+    unsigned int* pre = bm + nw;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int w = tid; w < nw; w += 512) bm[w] = 0u;
+    __syncthreads();
+    auto col = [&](int sg, int ge) {
+        const int cb = (32 * sg / SIG) * SIG;
+        return it.c16 ? cb + (int)it.c16[ge] : it.c32[ge];
+    };
+    for (int sl = warp; sl < nsl; sl += 16) {
+        const int sg = S0 + sl, L = it.len[sg], b = it.base[sg];
+        for (int q = 0; q < L; ++q) {
+            const int c = col(sg, b + 32 * q + lane);
+            FEMI_DCHECK(c >= 0 && c < n, 3);
+            if (c < R0 || c >= R1) atomicOr(&bm[c >> 5], 1u << (c & 31));
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the popcounts: thread t owns words [t ch, (t + 1) ch)
+    const int ch = (nw + 511) / 512;
+    int loc = 0;
+    for (int w = tid * ch; w < min(nw, (tid + 1) * ch); ++w) loc += __popc(bm[w]);
+    int inc = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    __shared__ int wsum[16];
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int wo = 0;
+    for (int q = 0; q < warp; ++q) wo += wsum[q];
+    int run = wo + inc - loc;
+    for (int w = tid * ch; w < min(nw, (tid + 1) * ch); ++w) {
+        pre[w] = run;
+        run += __popc(bm[w]);
+    }
+    __syncthreads();
+    int tot = 0;
+    for (int q = 0; q < 16; ++q) tot += wsum[q];
+    for (int sl = warp; sl < nsl; sl += 16) {
+        const int sg = S0 + sl, L = it.len[sg], b = it.base[sg];
+        for (int q = 0; q < L; ++q) {
+            const int ge = b + 32 * q + lane;
+            const int c = col(sg, ge);
+            int code;
+            if (c >= R0 && c < R1) code = c - R0;
+            else code = HB + (int)pre[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
+            FEMI_DCHECK(code >= 0 && code < 65536, 3);
+            it.rzc[ge] = (uint16_t)code;
+        }
+    }
+    for (int w = tid; w < nw; w += 512) {
+        unsigned int bits = bm[w];
+        int sidx = (int)pre[w];
+        while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            it.rzh[e0 + sidx++] = 32 * w + bit;
+        }
+    }
+    if (tid == 0) it.rzn[k] = tot;
+}
+
+__global__ void __launch_bounds__(512) k_rz_send(const RItem* __restrict__ items, int C) {
+    const RItem& it = items[blockIdx.x / C];
+    if (!it.rzc) return;
+    const int o = blockIdx.x % C, n = it.n, nwin = it.nwin;
+    const int R0 = rz_row0(n, nwin, C, o), R1 = rz_row0(n, nwin, C, o + 1);
+    const int S0 = R0 / 32, nsl = (R1 + 31) / 32 - S0;
+    const int e0 = nsl > 0 ? it.base[S0] : 0;
+    int off = 0;
+    for (int k = 0; k < C; ++k) {
+        if (k == o || nsl == 0) continue;
+        const int R0k = rz_row0(n, nwin, C, k), R1k = rz_row0(n, nwin, C, k + 1);
+        if (R1k <= R0k) continue;
+        const int* H = it.rzh + it.base[R0k / 32];
+        const int hc = it.rzn[k];
+        int lo = 0, hi = hc;  // first slot >= R0
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (H[mid] < R0) lo = mid + 1;
+            else hi = mid;
+        }
+        const int a = lo;
+        hi = hc;  // first slot >= R1
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (H[mid] < R1) lo = mid + 1;
+            else hi = mid;
+        }
+        for (int h = a + threadIdx.x; h < lo; h += 512)
+            it.rzs[e0 + off + (h - a)] = (H[h] - R0) | (k << 12) | (h << 16);
+        off += lo - a;
+    }
+    if (threadIdx.x == 0) it.rzn[16 + o] = off;
+}
+
+// Whole-solve resident kernel (k_cgs, the default for systems that fit; FEMI_CG_PIPE=0 selects
+// k_cgr + the separate prologue/epilogue kernels). ONE cluster launch per solve does what the
+// sequence k_reset, k_pro1, k_x0_fill2 x2, k_pro2, k_cgr, k_finalize, k_true_res, (restart
+// rounds), k_copy_g did -- the same arithmetic, rows walked in the same entry order -- so a
+// small or medium solve costs one launch instead of ~14 (the fixed cost dominated C1-C4).
+//   prologue: min/max of g (x0 modes 1, 3), b = -A_uk g (or the given b), the mask-neighbour
+//     fill (reading A11b: first hop from A_uk, two hops over A_uu through u_vert / w), x^0 and
+//     r^0 = s (b - A x0) with the unscaled rows (modes 2, 3), -s A_uk (g - c1) (mode 1), s b (0);
+//   CG: pipelined single-reduction recurrence (Ghysels & Vanroose; Jacobi folded into A^ as
+//     everywhere here). With w = A^ r, s = A^ p, z = A^ s, per iteration
+//       gamma = r.r, delta = w.r, rho = ||D^1/2 r^||^2 (partials of r_i, w_i)  |  n = A^ w_i
+//       beta = gamma/gamma_prev, alpha = gamma/(delta - beta gamma/alpha_prev) (first: gamma/delta)
+//       z = n + beta z ; s = w + beta s ; p = r + beta p ; x += alpha p ; r -= alpha s ; w -= alpha z
+//     In exact arithmetic these are k_cgr's iterates; ONE cluster barrier per iteration carries
+//     both w_i (shared-memory buffer of parity i & 1, read by peers through DSMEM) and each
+//     warp's three partial dots (written straight into every CTA's slot array, parity i & 1);
+//     every warp then sums the C x 16 slots in a fixed order (xor butterfly: the same bits in
+//     every lane, warp and CTA, so alpha / beta / the stopping decision agree everywhere). A
+//     buffer of parity k is rewritten two barriers later, after every CTA has passed the barrier
+//     in between, i.e. after every read of it;
+//   epilogue: x = s x^ into u_vert, the true residual ||b - A x|| with the unscaled rows (reading
+//     A11) and, when it misses rtol, up to 8 restarts of the recurrence from r = s (b - A x)
+//     inside the same launch; the mask entries of u_vert = g; the CgState for the host.
+// Global data written here and read by other CTAs of the cluster (u_vert, w as the fill's
+// temporary) is ordered by the cluster barrier (release / acquire at cluster scope) and read
+// with ld.global.cg.
+template <bool CL, int RP>
+__global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items, double rtol, int max_iter) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) unsigned char rzm[];
+    __shared__ RItem its;
+    __shared__ double part_p[2][16 * RZW][3];  // [parity][cta * RZW + warp][dot], DSMEM-written
+    __shared__ unsigned long long kmm[16 * RZW][2];  // per-warp min / max keys of g
+    int item = blockIdx.x, rank = 0;
+    if constexpr (CL) {
+        unsigned cr, cid;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+        asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        item = (int)cid;
+        rank = (int)cr;
+    }
+    // every CTA of the cluster must be running before its shared memory is addressed: arrive
+    // now, wait just before the first DSMEM store (the slice loading runs in between)
+    if constexpr (CL) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (threadIdx.x == 0) its = items[item];
+    __syncthreads();
+    const RItem& it = its;
+    CgState* S = it.st;
+    const int C = it.ncta;
+    const int n = it.n, nwin = it.nwin, m = it.m, mode = it.x0mode;
+    auto row0 = [&](int k) { return min(n, (nwin * k / C) * SIG); };
+    const int R0 = row0(rank), R1 = row0(rank + 1);
+    const int S0 = R0 / 32, S1 = (R1 + 31) / 32, nsl = S1 - S0;
+    const int e0 = nsl > 0 ? it.base[S0] : 0;
+    const int ne = nsl > 0 ? (S1 < (n + 31) / 32 ? it.base[S1] : it.base[S1 - 1] + 32 * it.len[S1 - 1]) - e0 : 0;
+    // shared memory: extended vector (own rows | halo) x2 (parity) | q | values | codes | len |
+    // base | send list. The layout of the vectors is the same in every CTA of the cluster (own
+    // part 32 x the largest slice count HB, then the largest halo), since peers write halo
+    // entries into it through DSMEM.
+    int nslm = 0;
+    for (int k = 0; k < C; ++k) nslm = max(nslm, (row0(k + 1) + 31) / 32 - row0(k) / 32);
+    const int HB = 32 * nslm, WS = HB + it.rzhmax;
+    double* wb0 = (double*)rzm;
+    double* wb1 = wb0 + WS;
+    double* q_s = wb1 + WS;
+    double* val_s = q_s + 32 * nsl;
+    uint16_t* code_s = (uint16_t*)(val_s + ne);  // index into the extended vector
+    int* len_s = (int*)(code_s + ((ne + 1) & ~1));
+    int* base_s = len_s + nsl;
+    uint32_t* snd_s = (uint32_t*)(base_s + nsl);
+    const int nsnd = it.rzn ? it.rzn[16 + rank] : 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    cg::cluster_group cluster = cg::this_cluster();
+    for (int sl = warp; sl < nsl; sl += RZW) {
+        const int sg = S0 + sl, L = it.len[sg], b = it.base[sg] - e0;
+        if (lane == 0) {
+            len_s[sl] = L;
+            base_s[sl] = b;
+        }
+        for (int k = 0; k < L; ++k) {
+            const int e = b + 32 * k + lane;
+            val_s[e] = it.val[e + e0];
+            code_s[e] = it.rzc[e + e0];
+        }
+    }
+    for (int i = tid; i < nsnd; i += RZT) snd_s[i] = (uint32_t)it.rzs[e0 + i];
+    // publish this lane's values of a vector into buffer buf (own part), then push the halo
+    // entries peers read into their copies of buf (DSMEM stores; the caller's cluster barrier
+    // makes them visible)
+    auto publish = [&](double* buf, const double (&v)[RP]) {
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            const int sl = warp + RZW * j;
+            if (sl >= nsl) break;
+            buf[32 * sl + lane] = v[j];
+        }
+        if (CL && C > 1) {
+            __syncthreads();
+            for (int i = tid; i < nsnd; i += RZT) {
+                const uint32_t e = snd_s[i];
+                double* dst = cluster.map_shared_rank(buf, (int)((e >> 12) & 15u));
+                dst[HB + (int)(e >> 16)] = buf[e & 0xfffu];
+            }
+        }
+    };
+    // this lane's rows: slot j = slice warp + RZW j
+    auto row_of = [&](int j) { return 32 * (S0 + warp + RZW * j) + lane; };
+    auto row_ok = [&](int j) { return warp + RZW * j < nsl && row_of(j) < R1; };
+    // cluster-wide fixed-order sum of three per-warp values (every warp gets the same bits)
+    int par = 0;
+    auto csum3 = [&](double l0, double l1, double l2, double& t0, double& t1, double& t2) {
+        l0 = warp_sum_d(l0);
+        l1 = warp_sum_d(l1);
+        l2 = warp_sum_d(l2);
+        if (lane < C) {
+            double* dst = CL ? cluster.map_shared_rank(&part_p[par][0][0], lane) : &part_p[par][0][0];
+            dst[3 * (rank * RZW + warp)] = l0;
+            dst[3 * (rank * RZW + warp) + 1] = l1;
+            dst[3 * (rank * RZW + warp) + 2] = l2;
+        }
+        rz_sync<CL>();
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int k = lane; k < C * RZW; k += 32) {
+            a0 += part_p[par][k][0];
+            a1 += part_p[par][k][1];
+            a2 += part_p[par][k][2];
+        }
+        t0 = warp_sum_d(a0);
+        t1 = warp_sum_d(a1);
+        t2 = warp_sum_d(a2);
+        par ^= 1;
+    };
+    if constexpr (CL) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    // ---------------- prologue
+    const bool want_mm = (mode == 1 || mode == 3) && it.g != nullptr;
+    if (want_mm) {  // min / max keys of g over a strided share, per warp -> every CTA's slots
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (int k = rank * RZT + tid; k < m; k += C * RZT) {
+            const unsigned long long key = dkey(it.g[k]);
+            lo = min(lo, key);
+            hi = max(hi, key);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane < C) {
+            unsigned long long* dst = CL ? cluster.map_shared_rank(&kmm[0][0], lane) : &kmm[0][0];
+            dst[2 * (rank * RZW + warp)] = lo;
+            dst[2 * (rank * RZW + warp) + 1] = hi;
+        }
+    }
+    // pass 1: b = -A_uk g (ascending mask index), the fill's first hop, r^0 for modes 0 / 1 with a given b
+    double l_bn = 0.0;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        if (!row_ok(j)) continue;
+        const int i = row_of(j);
+        double bi;
+        if (it.bin) {
+            bi = it.bin[it.inv[i]];
+        } else {
+            double acc = 0.0, best = 0.0;
+            double fv = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not filled yet
+            row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g, [&](double a, int k, double gk) {
+                FEMI_DCHECK(k >= 0 && k < it.m, 3);
+                acc = fma(a, gk, acc);
+                if (a < best) {
+                    best = a;
+                    fv = gk;
+                }
+            });
+            bi = -acc;
+            if (mode == 3) it.u_vert[it.inv[i]] = fv;
+        }
+        it.b[i] = bi;
+        l_bn += bi * bi;
+    }
+    double bn2, d1, d2;
+    csum3(l_bn, 0.0, 0.0, bn2, d1, d2);  // also publishes the min / max slots and the first hop
+    const double tol2 = rtol * rtol * bn2;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    if (want_mm) {
+        for (int k = lane; k < C * RZW; k += 32) {
+            kmin = min(kmin, kmm[k][0]);
+            kmax = max(kmax, kmm[k][1]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        }
+    }
+    const double x0v = want_mm && kmax != 0ull ? 0.5 * (dkey_inv(kmin) + dkey_inv(kmax)) : 0.0;
+    if (mode == 3) {  // the fill's second hop: u_vert -> w, barrier, w -> u_vert, barrier
+        for (int pass = 0; pass < 2; ++pass) {
+            const double* src = pass == 0 ? it.u_vert : it.w;
+            double* dst = pass == 0 ? it.w : it.u_vert;
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                if (!row_ok(j)) continue;
+                const int i = row_of(j);
+                const int nat = it.inv[i];
+                double v = __ldcg(src + nat);
+                if (isnan(v))
+                    for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) {
+                        const double c = __ldcg(src + it.uci[e]);
+                        if (!isnan(c)) {
+                            v = c;
+                            break;
+                        }
+                    }
+                dst[nat] = v;
+            }
+            rz_sync<CL>();
+        }
+    }
+    // pass 2: x^0 = x0 / s, r^0 = s r0
+    double x[RP], r[RP], w[RP], p[RP], sv[RP], z[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        x[j] = r[j] = w[j] = p[j] = sv[j] = z[j] = 0.0;
+        if (!row_ok(j)) continue;
+        const int i = row_of(j);
+        const double si = it.s[i];
+        double x0 = mode == 1 || mode == 3 ? x0v : 0.0;
+        if (mode >= 2) x0 = __ldcg(it.u_vert + it.inv[i]);
+        if (mode == 3 && isnan(x0)) x0 = x0v;  // (neighbours substitute it the same way)
+        x[j] = x0 / si;
+        if (mode == 0) {
+            r[j] = si * __ldcg(it.b + i);
+        } else if (mode == 1) {
+            if (it.bin) {
+                r[j] = si * __ldcg(it.b + i);
+            } else {
+                double accr = 0.0;
+                row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g,
+                          [&](double a, int, double gk) { accr = fma(a, gk - x0v, accr); });
+                r[j] = si * -accr;
+            }
+        } else {
+            double ax = 0.0;
+            row_walk4cg(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
+                FEMI_DCHECK(c >= 0 && c < it.n, 3);
+                if (mode == 3 && isnan(u)) u = x0v;
+                ax = fma(a, u, ax);
+            });
+            r[j] = si * (__ldcg(it.b + i) - ax);
+        }
+    }
+    if (mode == 3) {  // the guess of the rows the fill did not reach is midrange(g), in u_vert too
+        rz_sync<CL>();  // every row's pass-2 reads of u_vert are done
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            if (!row_ok(j)) continue;
+            const int nat = it.inv[row_of(j)];
+            if (isnan(__ldcg(it.u_vert + nat))) it.u_vert[nat] = x0v;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < RP; ++j)
+        if (warp + RZW * j < nsl) q_s[32 * (warp + RZW * j) + lane] = row_ok(j) ? it.q[row_of(j)] : 0.0;
+    // ---------------- SpMV from a published buffer: out_j = in_j + sum_k a_jk buf[col_jk]
+    int Ls[RP], bs[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        Ls[j] = 0;
+        bs[j] = 0;
+    }
+    auto spmv = [&](const double* buf, double (&out)[RP], const double (&in)[RP]) {
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            if (warp + RZW * j >= nsl) break;  // warp-uniform
+            const int L = Ls[j], b = bs[j];
+            double acc = 0.0;
+            for (int k0 = 0; k0 < L; k0 += 4) {
+                double vv[4], gv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    vv[u] = 0.0;
+                    gv[u] = 0.0;
+                    if (k0 + u < L) {
+                        const int e = b + 32 * (k0 + u);
+                        vv[u] = val_s[e];
+                        gv[u] = buf[code_s[e]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fma(vv[u], gv[u], acc);
+            }
+            out[j] = in[j] + acc;
+        }
+    };
+    int iters = 0, status = FEMI_OK, restarts = 0;
+    double res2 = 0.0;
+    const bool tmr = g_pcg_timers_on && item == 0 && rank == 0 && tid == 0;
+    unsigned long long tl = tmr ? gtimer() : 0ull;
+    auto mark = [&](int k) {
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[k] += t - tl;
+            tl = t;
+        }
+    };
+    bool first_round = true;
+    for (;;) {  // CG rounds: the first, then restarts from the true residual
+        double* wb_r = par ? wb1 : wb0;  // r^0 of the round in the buffer of the current parity
+        publish(wb_r, r);
+        rz_sync<CL>();  // r^0 published (and, in the first round, the slice metadata)
+        if (first_round) {
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                const int sl = warp + RZW * j;
+                if (sl < nsl) {
+                    Ls[j] = len_s[sl];
+                    bs[j] = base_s[sl] + lane;
+                }
+            }
+        }
+        spmv(wb_r, w, r);  // w^0 = A^ r^0
+        par ^= 1;          // the buffer of r^0 is rewritten two barriers later
+        const int iters0 = iters;
+        double alpha = 0.0, gam = 0.0;
+        for (;;) {
+            double* wbp = par ? wb1 : wb0;
+            double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+            publish(wbp, w);
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                const int sl = warp + RZW * j;
+                if (sl >= nsl) break;
+                if (row_of(j) < R1) {
+                    const double ru = r[j] * q_s[32 * sl + lane];
+                    l0 += r[j] * r[j];
+                    l1 += w[j] * r[j];
+                    l2 += ru * ru;
+                }
+            }
+            mark(0);
+            double gam2, del2, rho2;
+            const int pp = par;
+            csum3(l0, l1, l2, gam2, del2, rho2);  // w_i and the partials of (r_i, w_i), cluster-wide
+            mark(1);
+            double nv[RP];
+#pragma unroll
+            for (int j = 0; j < RP; ++j) nv[j] = 0.0;
+            spmv(pp ? wb1 : wb0, nv, w);  // n = A^ w_i
+            mark(2);
+            if (!isfinite(gam2) || !isfinite(del2) || !isfinite(bn2)) {
+                status = FEMI_E_NONFINITE;
+                break;
+            }
+            if (!(bn2 > 0.0) || rho2 <= tol2) break;
+            if (iters >= max_iter) {
+                if (iters > iters0) status = FEMI_E_NOT_CONVERGED;
+                break;
+            }
+            double beta = 0.0;
+            if (iters == iters0) {
+                if (!(del2 > 0.0)) {
+                    status = FEMI_E_NEG_CURVATURE;
+                    break;
+                }
+                alpha = gam2 / del2;
+            } else {
+                beta = gam2 / gam;
+                const double den = del2 - beta * gam2 / alpha;
+                if (!(den > 0.0)) {
+                    status = FEMI_E_NEG_CURVATURE;
+                    break;
+                }
+                alpha = gam2 / den;
+            }
+            gam = gam2;
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                if (warp + RZW * j >= nsl) break;
+                z[j] = fma(beta, z[j], nv[j]);
+                sv[j] = fma(beta, sv[j], w[j]);
+                p[j] = fma(beta, p[j], r[j]);
+                x[j] = fma(alpha, p[j], x[j]);
+                r[j] = fma(-alpha, sv[j], r[j]);
+                w[j] = fma(-alpha, z[j], w[j]);
+            }
+            ++iters;
+            mark(3);
+        }
+        first_round = false;
+        // x = s x^ into u_vert (a 0-iteration exit keeps the guess: modes 2, 3 leave u_vert, mode
+        // 1 writes the midrange exactly, b = 0 gives x = 0), then the true residual
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            if (!row_ok(j)) continue;
+            const int i = row_of(j);
+            if (iters == 0 && mode >= 2 && bn2 != 0.0) continue;
+            double xi;
+            if (bn2 == 0.0) xi = 0.0;
+            else if (iters == 0) xi = mode == 1 || mode == 3 ? x0v : 0.0;
+            else xi = it.s[i] * x[j];
+            it.u_vert[it.inv[i]] = xi;
+        }
+        rz_sync<CL>();
+        double l_res = 0.0;
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            if (!row_ok(j)) continue;
+            const int i = row_of(j);
+            double ax = 0.0;
+            row_walk4cg(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
+                FEMI_DCHECK(c >= 0 && c < it.n, 3);
+                ax = fma(a, u, ax);
+            });
+            const double ri = __ldcg(it.b + i) - ax;
+            r[j] = it.s[i] * ri;  // the restart's r^0
+            l_res += ri * ri;
+        }
+        csum3(l_res, 0.0, 0.0, res2, d1, d2);
+        const bool again = status == FEMI_OK && iters > 0 && iters < max_iter && bn2 > 0.0 && !(res2 <= tol2);
+        if (!again || restarts >= 8) break;
+        ++restarts;
+#pragma unroll
+        for (int j = 0; j < RP; ++j) p[j] = sv[j] = z[j] = 0.0;
+    }
+    if (it.g)
+        for (int k = rank * RZT + tid; k < m; k += C * RZT) it.u_vert[n + k] = it.g[k];
+    if (rank == 0 && tid == 0) {
+        S->iters = iters;
+        S->status = status;
+        S->bn2 = bn2;
+        S->tol2 = tol2;
+        S->res2 = res2;
+        S->kmin = want_mm ? kmin : ~0ull;
+        S->kmax = want_mm ? kmax : 0ull;
+        S->x_pend = 0;
+        S->rtol = rtol;
+        S->max_iter = max_iter;
     }
     rz_sync<CL>();  // no CTA leaves while others may still read its shared memory
 }
@@ -3326,6 +3926,12 @@ femi_status graph_solve_multi(femi_system_s* S, int nr, const double* const* g, 
 }  // namespace
 
 void pcg_cache_free(femi_system_s* S) {
+    if (S->rz_cache) {
+        RzCache* Z = (RzCache*)S->rz_cache;
+        if (Z->block) cudaFreeAsync(Z->block, nullptr);
+        delete Z;
+        S->rz_cache = nullptr;
+    }
     for (int k = 0; k < 5; ++k) {
         GraphCacheM* M = (GraphCacheM*)S->scratch_m[k];
         if (!M) continue;
@@ -3343,6 +3949,27 @@ void pcg_cache_free(femi_system_s* S) {
     if (C->ws) cudaFree(C->ws);
     delete C;
     S->scratch = nullptr;
+}
+
+// per-item outputs of a synchronous solve from the final CgStates
+static femi_status solve_outcome(int B, femi_system_s* const* S, const std::vector<CgState>& hs, const femi_cg_opts& o,
+                                 int32_t* iters, double* relres, int64_t* total_iters) {
+    femi_status ret = FEMI_OK;
+    int64_t tot = 0;
+    for (int b = 0; b < B; ++b) {
+        const CgState& s = hs[b];
+        double rel = s.bn2 > 0.0 ? std::sqrt(s.res2 / s.bn2) : 0.0;
+        if (S[b]->n_u == 0) rel = 0.0;
+        if (iters) iters[b] = S[b]->n_u == 0 ? 0 : s.iters;
+        if (relres) relres[b] = rel;
+        tot += S[b]->n_u == 0 ? 0 : s.iters;
+        femi_status sb = S[b]->n_u == 0 ? FEMI_OK : (femi_status)s.status;
+        if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
+        if (sb != FEMI_OK && ret == FEMI_OK) ret = sb;
+    }
+    if (total_iters) *total_iters = tot;
+    if (ret != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)ret) + ")");
+    return ret;
 }
 
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
@@ -3454,8 +4081,11 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     // on-chip resident solver (k_cgr): the smallest cluster (1..16 CTAs) whose CTAs hold their
     // matrix slices and r in shared memory and their rows in registers (<= RPL slices per warp)
     size_t rz_smem = 0;
-    int rz_C = 0;
+    int rz_C = 0, rz_rp = RPL;
     static const bool rz_off = std::getenv("FEMI_NO_RESIDENT") != nullptr;
+    // whole-solve pipelined resident kernel k_cgs (default) or k_cgr + prologue/epilogue kernels (FEMI_CG_PIPE=0)
+    static const bool rz_pipe = !(std::getenv("FEMI_CG_PIPE") && std::getenv("FEMI_CG_PIPE")[0] == '0');
+    const size_t rz_static = rz_pipe ? sizeof(double) * 2 * 16 * RZW * 3 + 16 * 16 * RZW : 0;
     if (!rz_off && !(B == 1 && S[0]->nnz_uu > 600000)) {
         const size_t rz_budget = (size_t)g_smem_optin - 4096;
         // cluster size: enough CTAs to fill the GPU (B C <= #SMs) while every warp keeps at least
@@ -3471,6 +4101,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             if (C < c_pref) continue;
             bool ok = true;
             size_t need = 0;
+            int64_t nsl_cta = 0;
             for (int b = 0; b < B && ok; ++b) {
                 const femi_system_s* sy = S[b];
                 if (sy->n_u == 0) continue;
@@ -3483,6 +4114,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
                     const int64_t r1 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * (k + 1) / C * SIG);
                     const int64_t s0 = r0 / 32, s1 = (r1 + 31) / 32, nsl = s1 - s0;
                     if (nsl > (int64_t)RZW * RPL || r1 - r0 > 65535) ok = false;
+                    nsl_cta = std::max(nsl_cta, nsl);
                     const int64_t ne = nsl > 0 ? sy->sell_base_h[s1] - sy->sell_base_h[s0] : 0;
                     need = std::max(need, (size_t)(16 * 32 * nsl + 12 * ne + 8 * nsl + 64));
                 }
@@ -3490,6 +4122,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             if (ok && need <= rz_budget) {
                 rz_C = C;
                 rz_smem = need;
+                rz_rp = (int)((nsl_cta + RZW - 1) / RZW);
             }
         }
     }
@@ -3584,8 +4217,162 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         it.nwin = s->nwin;
         it.x0mode = (it.g == nullptr && (o.x0 == 1 || o.x0 == 3)) ? 0 : o.x0;
     }
+    // whole-solve resident kernel: halo tables per system (built on first use for this cluster
+    // size), then the shared-memory size of the largest CTA; too large -> the k_cgr path
+    bool use_cgs = mode == 3 && rz_pipe;
+    if (use_cgs) {
+        const int C = ncta_item;
+        std::vector<RItem> bitems(items);
+        bool build = false;
+        for (int b = 0; b < B; ++b) {
+            femi_system_s* sy = S[b];
+            RzCache* Z = (RzCache*)sy->rz_cache;
+            bitems[b].rzc = nullptr;
+            if (sy->n_u == 0) continue;
+            if (Z && Z->C == C) continue;
+            if (!Z) {
+                Z = new RzCache();
+                sy->rz_cache = Z;
+            }
+            if (Z->block) FEMI_CUDA(cudaFreeAsync(Z->block, st));
+            const size_t ne = (size_t)std::max<int64_t>(1, sy->sell_nnz);
+            const size_t bytes = ((2 * ne + 15) & ~(size_t)15) + 8 * ne + 128;
+            FEMI_CUDA(cudaMallocAsync(&Z->block, bytes, st));  // the stream-ordered pool
+            Z->C = C;
+            Z->code = (uint16_t*)Z->block;
+            Z->halo = (int32_t*)((char*)Z->block + ((2 * ne + 15) & ~(size_t)15));
+            Z->snd = Z->halo + ne;
+            Z->cnt = Z->snd + ne;
+            bitems[b].rzc = Z->code;
+            bitems[b].rzh = Z->halo;
+            bitems[b].rzs = Z->snd;
+            bitems[b].rzn = Z->cnt;
+            build = true;
+        }
+        if (build) {
+            RItem* d_bi = nullptr;
+            FEMI_CUDA(cudaMallocAsync(&d_bi, sizeof(RItem) * B, st));
+            FEMI_CUDA(cudaMemcpyAsync(d_bi, bitems.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
+            static int halo_attr_dev = -1;
+            if (halo_attr_dev != cur_dev) {
+                FEMI_CUDA(cudaFuncSetAttribute((void*)k_rz_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               g_smem_optin - 4096));
+                halo_attr_dev = cur_dev;
+            }
+            const size_t hsm = sizeof(unsigned) * 2 * (size_t)((nmax + 31) / 32);
+            k_rz_halo<<<B * C, 512, hsm, st>>>(d_bi, C);
+            k_rz_send<<<B * C, 512, 0, st>>>(d_bi, C);
+            count_launches(2);
+            FEMI_CUDA(cudaGetLastError());
+            for (int b = 0; b < B; ++b)
+                if (bitems[b].rzc) {
+                    RzCache* Z = (RzCache*)S[b]->rz_cache;
+                    FEMI_CUDA(cudaMemcpyAsync(Z->cnt_h, Z->cnt, sizeof(Z->cnt_h), cudaMemcpyDeviceToHost, st));
+                }
+            FEMI_CUDA(cudaFreeAsync(d_bi, st));
+            FEMI_CUDA(cudaStreamSynchronize(st));
+            for (int b = 0; b < B; ++b)
+                if (bitems[b].rzc) {
+                    RzCache* Z = (RzCache*)S[b]->rz_cache;
+                    Z->hmax = 0;
+                    for (int k = 0; k < C; ++k) Z->hmax = std::max(Z->hmax, Z->cnt_h[k]);
+                }
+        }
+        const size_t budget = (size_t)g_smem_optin - 4096 - rz_static;
+        size_t need = 0;
+        for (int b = 0; b < B && use_cgs; ++b) {
+            femi_system_s* sy = S[b];
+            if (sy->n_u == 0) continue;
+            const RzCache* Z = (const RzCache*)sy->rz_cache;
+            int64_t nslm = 0;
+            for (int k = 0; k < C; ++k) {
+                const int64_t r0 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * k / C * SIG);
+                const int64_t r1 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * (k + 1) / C * SIG);
+                nslm = std::max(nslm, (r1 + 31) / 32 - r0 / 32);
+            }
+            for (int k = 0; k < C; ++k) {
+                const int64_t r0 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * k / C * SIG);
+                const int64_t r1 = std::min<int64_t>(sy->n_u, (int64_t)sy->nwin * (k + 1) / C * SIG);
+                const int64_t s0 = r0 / 32, s1 = (r1 + 31) / 32, nsl = s1 - s0;
+                const int64_t ne = nsl > 0 ? sy->sell_base_h[s1] - sy->sell_base_h[s0] : 0;
+                need = std::max(need, (size_t)(16 * (32 * nslm + Z->hmax) + 8 * 32 * nsl + 10 * ne + 8 * nsl +
+                                               4 * Z->cnt_h[16 + k] + 64));
+            }
+            items[b].rzc = Z->code;
+            items[b].rzh = Z->halo;
+            items[b].rzs = Z->snd;
+            items[b].rzn = Z->cnt;
+            items[b].rzhmax = Z->hmax;
+        }
+        if (need > budget) use_cgs = false;
+        else rz_smem = need;
+    }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * 2 * B, st));
+
+    // ---- whole-solve resident kernel: one cluster launch per item does everything
+    if (use_cgs) {
+        static int cgs_attr_dev = -1;
+        if (cgs_attr_dev != cur_dev) {
+            const int pmax = g_smem_optin - 4096 - (int)rz_static;
+            for (void* fp : {(void*)k_cgs<false, 2>, (void*)k_cgs<false, 4>, (void*)k_cgs<false, 6>,
+                             (void*)k_cgs<true, 2>, (void*)k_cgs<true, 4>, (void*)k_cgs<true, 6>})
+                FEMI_CUDA(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, pmax));
+            for (void* fp : {(void*)k_cgs<true, 2>, (void*)k_cgs<true, 4>, (void*)k_cgs<true, 6>})
+                FEMI_CUDA(cudaFuncSetAttribute(fp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cgs_attr_dev = cur_dev;
+        }
+        if (g_timers) {
+            unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int on = 1;
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+            FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        }
+        void* fp_cl[3] = {(void*)k_cgs<true, 2>, (void*)k_cgs<true, 4>, (void*)k_cgs<true, 6>};
+        void* fp_1[3] = {(void*)k_cgs<false, 2>, (void*)k_cgs<false, 4>, (void*)k_cgs<false, 6>};
+        const int rpi = rz_rp <= 2 ? 0 : (rz_rp <= 4 ? 1 : 2);  // rows per lane the CTAs need
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(RZT);
+        cfg.dynamicSmemBytes = rz_smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 0;
+        if (ncta_item > 1) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = ncta_item;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.numAttrs = 1;
+        }
+        const RItem* di = d_items;
+        double rt = o.rtol;
+        int mi = o.max_iter;
+        void* args[3] = {(void*)&di, (void*)&rt, (void*)&mi};
+        const cudaError_t e = cudaLaunchKernelExC(&cfg, ncta_item > 1 ? fp_cl[rpi] : fp_1[rpi], args);
+        if (e != cudaSuccess) return cuda_fail(e, "k_cgs launch");
+        count_launches(1);
+        if (ds) {
+            k_stats<<<1, 32, 0, st>>>(B, d_items, ds);
+            count_launches(1);
+            FEMI_CUDA(cudaGetLastError());
+            return FEMI_OK;  // the workspace is released stream-ordered (Workspace)
+        }
+        std::vector<CgState> hs(B);
+        FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
+        FEMI_CUDA(cudaStreamSynchronize(st));
+        if (g_timers) {
+            unsigned long long t[8];
+            FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
+            const double it_n = std::max(1, hs[0].iters);
+            std::fprintf(stderr,
+                         "[femi pcg timers] k_cgs ctas %d iters %d | per iter us: publish %.2f barrier+sums %.2f spmv "
+                         "%.2f update %.2f\n",
+                         grid, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3, t[3] / it_n / 1e3);
+        }
+        return solve_outcome(B, S, hs, o, iters, relres, total_iters);
+    }
 
     // ---- setup launches
     const unsigned gy = (unsigned)B;
@@ -3732,26 +4519,11 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         // the header promises a synchronised stream: u_vert's mask entries are written when we return
         FEMI_CUDA(cudaStreamSynchronize(st));
     }
-    femi_status ret = FEMI_OK;
-    int64_t tot = 0;
-    for (int b = 0; b < B; ++b) {
-        const CgState& s = hs[b];
-        double rel = s.bn2 > 0.0 ? std::sqrt(s.res2 / s.bn2) : 0.0;
-        if (S[b]->n_u == 0) rel = 0.0;
-        if (iters) iters[b] = S[b]->n_u == 0 ? 0 : s.iters;
-        if (relres) relres[b] = rel;
-        tot += S[b]->n_u == 0 ? 0 : s.iters;
-        femi_status sb = S[b]->n_u == 0 ? FEMI_OK : (femi_status)s.status;
-        if (sb == FEMI_OK && !(rel <= o.rtol)) sb = FEMI_E_NOT_CONVERGED;
-        if (sb != FEMI_OK && ret == FEMI_OK) ret = sb;
-    }
-    if (total_iters) *total_iters = tot;
     if (ds) {  // asynchronous caller on a synchronous path (persistent kernel): same statistics
         k_stats<<<1, 32, 0, st>>>(B, d_items, ds);
         count_launches(1);
     }
-    if (ret != FEMI_OK) set_error("inpaint_solve: CG did not converge (status " + std::to_string((int)ret) + ")");
-    return ret;
+    return solve_outcome(B, S, hs, o, iters, relres, total_iters);
 }
 
 }  // namespace femi
