@@ -15,7 +15,11 @@
  *    mask-pix order.
  *  - Handles (femi_mesh, femi_system) are created and freed only by the library and are
  *    immutable after creation, EXCEPT that a femi_system caches device scratch for its
- *    solves: at most one call may be in flight per femi_system at a time.
+ *    solves. A femi_system may be shared across host threads and streams: calls on one
+ *    system are serialised -- host side by a per-system lock, device side by an event, so
+ *    a call's work is ordered after the work of the previous call on the same system,
+ *    whatever stream that ran on (calls on different systems run concurrently). Freeing a
+ *    system while another thread still uses it is the caller's error.
  *  - Device pointers are caller-owned (e.g. PyTorch tensors); the library never frees
  *    them; they must stay valid until the enqueued work completes. All device work is
  *    enqueued on the caller's stream (femi_stream == cudaStream_t; NULL = legacy default

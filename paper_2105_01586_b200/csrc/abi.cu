@@ -156,6 +156,44 @@ femi_status check_device() {
 
 using namespace femi;
 
+namespace femi {
+namespace {
+// A femi_system may be shared across host threads and streams. Calls that use it are
+// serialised: host side by the system's mutex (systems locked in address order, a system
+// repeated in a batch once), device side by the system's event -- the call's stream waits for
+// the work of the previous call on the system when that ran on another stream, and the event is
+// recorded after this call's work. The cached scratch of a system (graph caches, halo tables,
+// solve workspace) is therefore never used by two calls at once.
+class SysGuard {
+  public:
+    SysGuard(femi_system_s* const* S, int B, cudaStream_t st) : st_(st) {
+        for (int b = 0; b < B; ++b)
+            if (S[b]) v_.push_back(S[b]);
+        std::sort(v_.begin(), v_.end());
+        v_.erase(std::unique(v_.begin(), v_.end()), v_.end());
+        for (femi_system_s* s : v_) s->mu.lock();
+        for (femi_system_s* s : v_)
+            if (s->ev && s->ev_stream != st_) cudaStreamWaitEvent(st_, s->ev, 0);
+    }
+    ~SysGuard() {
+        for (femi_system_s* s : v_) {
+            if (!s->ev) cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming);
+            if (s->ev) cudaEventRecord(s->ev, st_);
+            s->ev_stream = st_;
+        }
+        for (auto it = v_.rbegin(); it != v_.rend(); ++it) (*it)->mu.unlock();
+    }
+    SysGuard(const SysGuard&) = delete;
+    SysGuard& operator=(const SysGuard&) = delete;
+
+  private:
+    cudaStream_t st_;
+    std::vector<femi_system_s*> v_;
+};
+}  // namespace
+}  // namespace femi
+using femi::SysGuard;
+
 extern "C" {
 
 const char* femi_last_error(void) { return g_last_error.c_str(); }
@@ -266,6 +304,7 @@ void femi_system_free(femi_system sys) {
     if (!sys) return;
     cudaDeviceSynchronize();  // no work of any stream may still read the system
     pcg_cache_free(sys);
+    if (sys->ev) cudaEventDestroy(sys->ev);
     for (void* p : sys->allocs) cudaFreeAsync(p, nullptr);
     for (void* p : sys->arena_chunks) cudaFreeAsync(p, nullptr);
     delete sys;
@@ -730,6 +769,7 @@ femi_status femi_inpaint_solve_batched(int32_t B, const femi_system* sys, const 
     femi_status s = check_device();
     if (s) return s;
     std::vector<femi_system_s*> Sv(sys, sys + B);
+    SysGuard guard(Sv.data(), B, (cudaStream_t)stream);
     return pcg_solve(B, Sv.data(), g, nullptr, u_vert, *opts, iters, relres, (cudaStream_t)stream, nullptr);
 }
 
@@ -747,6 +787,7 @@ femi_status femi_rasterise_error_batched(int32_t B, const femi_system* sys, cons
             return FEMI_E_ARG;
         }
     std::vector<femi_system_s*> Sv(sys, sys + B);
+    SysGuard guard(Sv.data(), B, (cudaStream_t)stream);
     return launch_raster(B, Sv.data(), u_vert, f, u_px, e_px, tri_err, tri_best_px, sse, (cudaStream_t)stream);
 }
 
@@ -769,6 +810,7 @@ femi_status femi_densify_step(femi_system sys, const double* f, const double* u_
         set_error("densify_step: NULL argument, b < 0 or a raster-only (band) system");
         return FEMI_E_ARG;
     }
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return densify_select(sys, 1, &f, &u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
 }
 
@@ -790,6 +832,7 @@ femi_status femi_rasterise_error_channels(femi_system sys, int32_t C, const doub
     }
     femi_status s = check_device();
     if (s) return s;
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return launch_raster_channels(sys, C, u_vert, f, u_px, e_px, tri_err, tri_best_px, sse, (cudaStream_t)stream);
 }
 
@@ -807,6 +850,7 @@ femi_status femi_densify_step_channels(femi_system sys, int32_t C, const double*
         }
     femi_status s = check_device();
     if (s) return s;
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return densify_select(sys, C, f, u_vert, b, new_mask_px, n_added, (cudaStream_t)stream);
 }
 
@@ -827,6 +871,7 @@ femi_status femi_tonal_optimise_l1(femi_system sys, const double* f, double* g, 
         *report = femi_tonal_l1_report{};
         return FEMI_OK;
     }
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return tonal_irls(sys, f, g, *opts, irls, eps, report, (cudaStream_t)stream);
 }
 
@@ -864,6 +909,7 @@ static femi_status apply_common(const char* what, femi_system sys, const double*
 femi_status femi_apply_B(femi_system sys, const double* g, double* u_px, const femi_cg_opts* opts, femi_stream stream) {
     femi_status s = apply_common("apply_B", sys, g, u_px, opts);
     if (s) return s;
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return tonal_apply(sys, 0, g, u_px, *opts, (cudaStream_t)stream);
 }
 
@@ -871,6 +917,7 @@ femi_status femi_apply_BT(femi_system sys, const double* r, double* s_out, const
                           femi_stream stream) {
     femi_status s = apply_common("apply_BT", sys, r, s_out, opts);
     if (s) return s;
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return tonal_apply(sys, 1, r, s_out, *opts, (cudaStream_t)stream);
 }
 
@@ -894,6 +941,7 @@ femi_status femi_tonal_optimise_channels(femi_system sys, int32_t C, const doubl
     if (s) return s;
     std::memset(reports, 0, sizeof(femi_tonal_report) * C);
     if (sys->n_u == 0) return FEMI_OK;
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return tonal_cgls_channels(sys, C, f, g, *opts, reports, (cudaStream_t)stream);
 }
 
@@ -911,6 +959,7 @@ femi_status femi_tonal_optimise(femi_system sys, const double* f, double* g, con
     femi_status s = check_device();
     if (s) return s;
     std::memset(report, 0, sizeof(*report));
+    SysGuard guard(&sys, 1, (cudaStream_t)stream);
     return tonal_cgls(sys, f, g, *opts, report, (cudaStream_t)stream);
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -121,6 +122,11 @@ struct femi_system_s {
     size_t scratch_bytes = 0;
     int32_t last_path = 0;  // FEMI_PATH_* of the last solve (femi_system_solver_path)
     void* rz_cache = nullptr;  // whole-solve resident kernel: halo codes / lists / send lists (pcg.cu)
+    // calls on one system from several threads / streams are serialised (abi.cu SysGuard): the
+    // host side by this mutex, the device side by an event recorded after each call's work
+    std::mutex mu;
+    cudaEvent_t ev = nullptr;
+    cudaStream_t ev_stream = nullptr;
     // device memory of the system comes from the stream-ordered pool (cudaMallocAsync on the
     // assembling stream; the pool keeps freed memory, so a densification step's assemble and
     // the previous system's release cost no cudaMalloc / cudaFree device synchronisation)

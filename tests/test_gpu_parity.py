@@ -618,3 +618,61 @@ def test_x0_fill_small_systems_use_midrange():
     _, i1, _ = femi.inpaint_solve_batched([S], [g], [u1], femi.cg_opts(x0=1))
     _, i3, _ = femi.inpaint_solve_batched([S], [g], [u3], femi.cg_opts(x0=3))
     assert i1[0] == i3[0] and torch.equal(u1, u3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [1024, 2880])
+def test_system_shared_across_threads_and_streams(W):
+    """A femi_system shared by two host threads on two streams (include/femi.h: calls on one
+    system are serialised by its lock and event): every concurrent solve + raster equals the
+    sequential result bit for bit -- the resident whole-solve kernel (1024^2, C4 recipe) and
+    the graph-mode solver with its cached graphs (2880^2, C5 recipe)."""
+    import threading
+    if W == 1024:
+        c = make_config(4)
+        mk, un = c["mask"], c["unknowns"]
+    else:
+        c = make_config(5, W=W, H=W, seed=77)
+        rng = np.random.default_rng(7)
+        extra = draw_mask(rng, W * W, len(c["mask0"]))
+        mk = np.union1d(c["mask0"], extra)
+        un = np.setdiff1d(c["unknowns"], mk)
+    f = dev(c["f"]).reshape(-1)
+    M = femi.Mesh(W, W, mk, un)
+    S = femi.System(M)
+    g = pipeline.mask_values(f, M.export()["vert_px"], S.n_u)
+    u_ref = torch.empty(S.nv, dtype=torch.float64, device=DEV)
+    femi.inpaint_solve_batched([S], [g], [u_ref], femi.cg_opts(rtol=1e-10))
+    e_ref = torch.empty(W * W, dtype=torch.float64, device=DEV)
+    femi.rasterise_error(S, u_ref, f, torch.zeros(1, dtype=torch.float64, device=DEV), e_px=e_ref)
+    torch.cuda.synchronize()
+    if W == 2880:
+        assert femi.solver_path(S) == "graph_tma"
+    out, errs = {}, []
+
+    def worker(k):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                us = [torch.empty(S.nv, dtype=torch.float64, device=DEV) for _ in range(3)]
+                es = [torch.empty(W * W, dtype=torch.float64, device=DEV) for _ in range(3)]
+                for j in range(3):
+                    femi.inpaint_solve_batched([S], [g], [us[j]], femi.cg_opts(rtol=1e-10), stream=st)
+                    femi.rasterise_error(S, us[j], f, torch.zeros(1, dtype=torch.float64, device=DEV),
+                                         e_px=es[j], stream=st)
+                st.synchronize()
+            out[k] = (us, es)
+        except Exception as ex:  # surfaced in the main thread
+            errs.append(ex)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(2):
+        us, es = out[k]
+        for j in range(3):
+            assert torch.equal(us[j], u_ref), (k, j)
+            assert torch.equal(es[j], e_ref), (k, j)
