@@ -364,6 +364,47 @@ __device__ __forceinline__ void row_walk4cg(int e0, int e1, const int* __restric
     }
 }
 
+// In-order walks of up to RP CSR rows at once (the rows of one lane, k_cgs): per step the column
+// and value loads of every row, then their gathers, then f(j, a, col, src[col]) in entry order per
+// row -- the rows' dependent load chains overlap instead of running one after another, and each
+// row's sums keep the sequential rounding. CG: gathers through L2 (data other CTAs wrote).
+template <int RP, bool CG, class F>
+__device__ __forceinline__ void walk_rows(const bool (&ok)[RP], const int (&row)[RP], const int* __restrict__ rp,
+                                          const int* __restrict__ ci, const double* __restrict__ va,
+                                          const double* src, F&& f) {
+    constexpr int W = RP <= 2 ? 4 : 2;
+    int e[RP], e1[RP];
+    int len = 0;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        e[j] = ok[j] ? rp[row[j]] : 0;
+        e1[j] = ok[j] ? rp[row[j] + 1] : 0;
+        len = max(len, e1[j] - e[j]);
+    }
+    for (int s = 0; s < len; s += W) {
+        int c[RP][W];
+        double a[RP][W], x[RP][W];
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                const bool in = e[j] + s + q < e1[j];
+                c[j][q] = in ? ci[e[j] + s + q] : -1;
+                a[j][q] = in ? va[e[j] + s + q] : 0.0;
+            }
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+#pragma unroll
+            for (int q = 0; q < W; ++q)
+                x[j][q] = c[j][q] >= 0 ? (CG ? __ldcg(src + c[j][q]) : src[c[j][q]]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+#pragma unroll
+            for (int q = 0; q < W; ++q)
+                if (c[j][q] >= 0) f(j, a[j][q], c[j][q], x[j][q]);
+    }
+}
+
 // pass 1: min/max of g (x0 modes 1, 3), the fill's first hop (mode 3: the value of the most
 // strongly coupled mask neighbour, the most negative A_uk entry, ties -> first), b = -A_uk g
 // (ascending mask index, reading A6 order) or the given b, r^0 for modes 0 and 1 with a
@@ -582,7 +623,7 @@ __device__ __forceinline__ void group_sync(const RItem& it, int rank, unsigned l
 }
 
 // optional phase timers (FEMI_PCG_TIMERS=1): rank-0 thread-0 %globaltimer deltas, ns
-__device__ unsigned long long g_pcg_timers[8];
+__device__ unsigned long long g_pcg_timers[16];
 __device__ int g_pcg_timers_on;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -1261,6 +1302,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     // every CTA of the cluster must be running before its shared memory is addressed: arrive
     // now, wait just before the first DSMEM store (the slice loading runs in between)
     if constexpr (CL) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    const unsigned long long t_k0 = g_pcg_timers_on ? gtimer() : 0ull;
     if (threadIdx.x == 0) its = items[item];
     __syncthreads();
     const RItem& it = its;
@@ -1290,19 +1332,54 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     const int nsnd = it.rzn ? it.rzn[16 + rank] : 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     cg::cluster_group cluster = cg::this_cluster();
-    for (int sl = warp; sl < nsl; sl += RZW) {
-        const int sg = S0 + sl, L = it.len[sg], b = it.base[sg] - e0;
-        if (lane == 0) {
-            len_s[sl] = L;
-            base_s[sl] = b;
-        }
-        for (int k = 0; k < L; ++k) {
-            const int e = b + 32 * k + lane;
-            val_s[e] = it.val[e + e0];
-            code_s[e] = it.rzc[e + e0];
+    for (int sl = tid; sl < nsl; sl += RZT) {
+        len_s[sl] = it.len[S0 + sl];
+        base_s[sl] = it.base[S0 + sl] - e0;
+    }
+    {  // the CTA's entries are one contiguous range: a flat copy, four loads in flight per thread
+        const double* __restrict__ gv = it.val + e0;
+        const uint16_t* __restrict__ gc = it.rzc + e0;
+        for (int i0 = 0; i0 < ne; i0 += 4 * RZT) {
+            double v[4];
+            uint16_t c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * RZT + tid;
+                v[u] = i < ne ? gv[i] : 0.0;
+                c[u] = i < ne ? gc[i] : (uint16_t)0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * RZT + tid;
+                if (i < ne) {
+                    val_s[i] = v[u];
+                    code_s[i] = c[u];
+                }
+            }
         }
     }
     for (int i = tid; i < nsnd; i += RZT) snd_s[i] = (uint32_t)it.rzs[e0 + i];
+    __syncthreads();  // the CTA's slice metadata, entries and send list are in place
+    // FEMI_PCG_TIMERS: rank-0 thread-0 %globaltimer deltas -- per iteration [0..3], per launch
+    // [4] setup (from the kernel's start), [5] pass 1 + ||b||, [6] fill + pass 2, [7] epilogue
+    const bool tmr = g_pcg_timers_on && item == 0 && rank == 0 && tid == 0;
+    unsigned long long tl = tmr ? t_k0 : 0ull;
+    auto mark = [&](int k) {
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[k] += t - tl;
+            tl = t;
+        }
+    };
+    mark(4);
+    unsigned long long tsub = tl;  // finer split of the prologue: slots 8.. (from the previous sub-mark)
+    auto smark = [&](int k) {
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[k] += t - tsub;
+            tsub = t;
+        }
+    };
     // publish this lane's values of a vector into buffer buf (own part), then push the halo
     // entries peers read into their copies of buf (DSMEM stores; the caller's cluster barrier
     // makes them visible)
@@ -1369,35 +1446,55 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             dst[2 * (rank * RZW + warp) + 1] = hi;
         }
     }
-    // pass 1: b = -A_uk g (ascending mask index), the fill's first hop, r^0 for modes 0 / 1 with a given b
-    double l_bn = 0.0;
+    // pass 1: b = -A_uk g (ascending mask index), the fill's first hop
+    bool okr[RP];
+    int rowr[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) {
-        if (!row_ok(j)) continue;
-        const int i = row_of(j);
-        double bi;
+        okr[j] = row_ok(j);
+        rowr[j] = okr[j] ? row_of(j) : 0;
+    }
+    double l_bn = 0.0;
+    {
+        double bv[RP];
         if (it.bin) {
-            bi = it.bin[it.inv[i]];
+#pragma unroll
+            for (int j = 0; j < RP; ++j) bv[j] = okr[j] ? it.bin[it.inv[rowr[j]]] : 0.0;
         } else {
-            double acc = 0.0, best = 0.0;
-            double fv = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not filled yet
-            row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g, [&](double a, int k, double gk) {
+            double acc[RP], best[RP], fv[RP];
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                acc[j] = 0.0;
+                best[j] = 0.0;
+                fv[j] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not filled yet
+            }
+            walk_rows<RP, false>(okr, rowr, it.krp, it.kci, it.kav, it.g, [&](int j, double a, int k, double gk) {
                 FEMI_DCHECK(k >= 0 && k < it.m, 3);
-                acc = fma(a, gk, acc);
-                if (a < best) {
-                    best = a;
-                    fv = gk;
+                acc[j] = fma(a, gk, acc[j]);
+                if (a < best[j]) {
+                    best[j] = a;
+                    fv[j] = gk;
                 }
             });
-            bi = -acc;
-            if (mode == 3) it.u_vert[it.inv[i]] = fv;
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                bv[j] = -acc[j];
+                if (mode == 3 && okr[j]) it.u_vert[it.inv[rowr[j]]] = fv[j];
+            }
         }
-        it.b[i] = bi;
-        l_bn += bi * bi;
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+            if (okr[j]) {
+                it.b[rowr[j]] = bv[j];
+                l_bn += bv[j] * bv[j];
+            }
     }
+    smark(8);
     double bn2, d1, d2;
     csum3(l_bn, 0.0, 0.0, bn2, d1, d2);  // also publishes the min / max slots and the first hop
     const double tol2 = rtol * rtol * bn2;
+    smark(9);
+    mark(5);
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (want_mm) {
         for (int k = lane; k < C * RZW; k += 32) {
@@ -1414,76 +1511,34 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         for (int pass = 0; pass < 2; ++pass) {
             const double* src = pass == 0 ? it.u_vert : it.w;
             double* dst = pass == 0 ? it.w : it.u_vert;
+            double v[RP];
+            bool need[RP];
+            int nat[RP];
 #pragma unroll
             for (int j = 0; j < RP; ++j) {
-                if (!row_ok(j)) continue;
-                const int i = row_of(j);
-                const int nat = it.inv[i];
-                double v = __ldcg(src + nat);
-                if (isnan(v))
-                    for (int e = it.urp[i]; e < it.urp[i + 1]; ++e) {
-                        const double c = __ldcg(src + it.uci[e]);
-                        if (!isnan(c)) {
-                            v = c;
-                            break;
-                        }
-                    }
-                dst[nat] = v;
+                nat[j] = okr[j] ? it.inv[rowr[j]] : 0;
+                v[j] = okr[j] ? __ldcg(src + nat[j]) : 0.0;
+                need[j] = okr[j] && isnan(v[j]);
             }
-            rz_sync<CL>();
-        }
-    }
-    // pass 2: x^0 = x0 / s, r^0 = s r0
-    double x[RP], r[RP], w[RP], p[RP], sv[RP], z[RP];
-#pragma unroll
-    for (int j = 0; j < RP; ++j) {
-        x[j] = r[j] = w[j] = p[j] = sv[j] = z[j] = 0.0;
-        if (!row_ok(j)) continue;
-        const int i = row_of(j);
-        const double si = it.s[i];
-        double x0 = mode == 1 || mode == 3 ? x0v : 0.0;
-        if (mode >= 2) x0 = __ldcg(it.u_vert + it.inv[i]);
-        if (mode == 3 && isnan(x0)) x0 = x0v;  // (neighbours substitute it the same way)
-        x[j] = x0 / si;
-        if (mode == 0) {
-            r[j] = si * __ldcg(it.b + i);
-        } else if (mode == 1) {
-            if (it.bin) {
-                r[j] = si * __ldcg(it.b + i);
-            } else {
-                double accr = 0.0;
-                row_walk4(it.krp[i], it.krp[i + 1], it.kci, it.kav, it.g,
-                          [&](double a, int, double gk) { accr = fma(a, gk - x0v, accr); });
-                r[j] = si * -accr;
-            }
-        } else {
-            double ax = 0.0;
-            row_walk4cg(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
-                FEMI_DCHECK(c >= 0 && c < it.n, 3);
-                if (mode == 3 && isnan(u)) u = x0v;
-                ax = fma(a, u, ax);
+            // the first non-NaN neighbour in ascending column order (rows that need one)
+            walk_rows<RP, true>(need, rowr, it.urp, it.uci, it.uav, src, [&](int j, double, int, double c) {
+                if (isnan(v[j]) && !isnan(c)) v[j] = c;
             });
-            r[j] = si * (__ldcg(it.b + i) - ax);
+#pragma unroll
+            for (int j = 0; j < RP; ++j)
+                if (okr[j]) dst[nat[j]] = v[j];
+            smark(10 + 2 * pass);
+            rz_sync<CL>();
+            smark(11 + 2 * pass);
         }
     }
-    if (mode == 3) {  // the guess of the rows the fill did not reach is midrange(g), in u_vert too
-        rz_sync<CL>();  // every row's pass-2 reads of u_vert are done
-#pragma unroll
-        for (int j = 0; j < RP; ++j) {
-            if (!row_ok(j)) continue;
-            const int nat = it.inv[row_of(j)];
-            if (isnan(__ldcg(it.u_vert + nat))) it.u_vert[nat] = x0v;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < RP; ++j)
-        if (warp + RZW * j < nsl) q_s[32 * (warp + RZW * j) + lane] = row_ok(j) ? it.q[row_of(j)] : 0.0;
     // ---------------- SpMV from a published buffer: out_j = in_j + sum_k a_jk buf[col_jk]
     int Ls[RP], bs[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) {
-        Ls[j] = 0;
-        bs[j] = 0;
+        const int sl = warp + RZW * j;
+        Ls[j] = sl < nsl ? len_s[sl] : 0;
+        bs[j] = sl < nsl ? base_s[sl] + lane : 0;
     }
     auto spmv = [&](const double* buf, double (&out)[RP], const double (&in)[RP]) {
 #pragma unroll
@@ -1509,32 +1564,63 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             out[j] = in[j] + acc;
         }
     };
+#pragma unroll
+    for (int j = 0; j < RP; ++j)
+        if (warp + RZW * j < nsl) q_s[32 * (warp + RZW * j) + lane] = row_ok(j) ? it.q[row_of(j)] : 0.0;
+    // pass 2: x^0 = x0 / s and r^0 = s (b - A x0) = s b - A^ x^0 (A = D^1/2 A^ D^1/2, s = D^-1/2):
+    // the product with the solver's own matrix in shared memory -- x^0 published like any CG
+    // vector -- instead of a second walk over the unscaled rows in global memory (any r^0
+    // consistent with x^0 starts the recurrence; the exit check uses the unscaled rows, A11).
+    // A row the fill did not reach takes midrange(g), also in u_vert (only its owner reads it).
+    double x[RP], r[RP], w[RP], p[RP], sv[RP], z[RP];
+    {
+        double acc[RP];
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            x[j] = r[j] = w[j] = p[j] = sv[j] = z[j] = 0.0;
+            acc[j] = 0.0;
+            if (!okr[j]) continue;
+            const int i = rowr[j];
+            double x0 = mode == 1 || mode == 3 ? x0v : 0.0;
+            if (mode >= 2) {
+                const int nat = it.inv[i];
+                x0 = __ldcg(it.u_vert + nat);
+                if (mode == 3 && isnan(x0)) {
+                    x0 = x0v;
+                    it.u_vert[nat] = x0;
+                }
+            }
+            x[j] = x0 / it.s[i];
+        }
+        if (mode == 1 && !it.bin) {  // r0 = -A_uk (g - c 1) (zero row sums)
+            walk_rows<RP, false>(okr, rowr, it.krp, it.kci, it.kav, it.g,
+                                 [&](int j, double a, int, double gk) { acc[j] = fma(a, gk - x0v, acc[j]); });
+        } else if (mode >= 2) {
+            publish(par ? wb1 : wb0, x);
+            rz_sync<CL>();
+            spmv(par ? wb1 : wb0, acc, x);  // A^ x^0
+            par ^= 1;  // the buffer is rewritten two barriers later
+        }
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            if (!okr[j]) continue;
+            const int i = rowr[j];
+            const double si = it.s[i];
+            if (mode == 0 || (mode == 1 && it.bin)) r[j] = si * __ldcg(it.b + i);
+            else if (mode == 1) r[j] = si * -acc[j];
+            else r[j] = fma(si, __ldcg(it.b + i), -acc[j]);
+        }
+    }
+    smark(14);
+    smark(15);
+    mark(6);
     int iters = 0, status = FEMI_OK, restarts = 0;
     double res2 = 0.0;
-    const bool tmr = g_pcg_timers_on && item == 0 && rank == 0 && tid == 0;
-    unsigned long long tl = tmr ? gtimer() : 0ull;
-    auto mark = [&](int k) {
-        if (tmr) {
-            const unsigned long long t = gtimer();
-            g_pcg_timers[k] += t - tl;
-            tl = t;
-        }
-    };
     bool first_round = true;
     for (;;) {  // CG rounds: the first, then restarts from the true residual
         double* wb_r = par ? wb1 : wb0;  // r^0 of the round in the buffer of the current parity
         publish(wb_r, r);
-        rz_sync<CL>();  // r^0 published (and, in the first round, the slice metadata)
-        if (first_round) {
-#pragma unroll
-            for (int j = 0; j < RP; ++j) {
-                const int sl = warp + RZW * j;
-                if (sl < nsl) {
-                    Ls[j] = len_s[sl];
-                    bs[j] = base_s[sl] + lane;
-                }
-            }
-        }
+        rz_sync<CL>();  // r^0 published
         spmv(wb_r, w, r);  // w^0 = A^ r^0
         par ^= 1;          // the buffer of r^0 is rewritten two barriers later
         const int iters0 = iters;
@@ -1604,6 +1690,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             mark(3);
         }
         first_round = false;
+        const unsigned long long t_ep = tmr ? gtimer() : 0ull;
         // x = s x^ into u_vert (a 0-iteration exit keeps the guess: modes 2, 3 leave u_vert, mode
         // 1 writes the midrange exactly, b = 0 gives x = 0), then the true residual
 #pragma unroll
@@ -1619,20 +1706,29 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         }
         rz_sync<CL>();
         double l_res = 0.0;
+        {
+            double ax[RP];
 #pragma unroll
-        for (int j = 0; j < RP; ++j) {
-            if (!row_ok(j)) continue;
-            const int i = row_of(j);
-            double ax = 0.0;
-            row_walk4cg(it.urp[i], it.urp[i + 1], it.uci, it.uav, it.u_vert, [&](double a, int c, double u) {
+            for (int j = 0; j < RP; ++j) ax[j] = 0.0;
+            walk_rows<RP, true>(okr, rowr, it.urp, it.uci, it.uav, it.u_vert, [&](int j, double a, int c, double u) {
                 FEMI_DCHECK(c >= 0 && c < it.n, 3);
-                ax = fma(a, u, ax);
+                ax[j] = fma(a, u, ax[j]);
             });
-            const double ri = __ldcg(it.b + i) - ax;
-            r[j] = it.s[i] * ri;  // the restart's r^0
-            l_res += ri * ri;
+#pragma unroll
+            for (int j = 0; j < RP; ++j) {
+                if (!okr[j]) continue;
+                const int i = rowr[j];
+                const double ri = __ldcg(it.b + i) - ax[j];
+                r[j] = it.s[i] * ri;  // the restart's r^0
+                l_res += ri * ri;
+            }
         }
         csum3(l_res, 0.0, 0.0, res2, d1, d2);
+        if (tmr) {
+            const unsigned long long t = gtimer();
+            g_pcg_timers[7] += t - t_ep;
+            tl = t;
+        }
         const bool again = status == FEMI_OK && iters > 0 && iters < max_iter && bn2 > 0.0 && !(res2 <= tol2);
         if (!again || restarts >= 8) break;
         ++restarts;
@@ -1941,7 +2037,7 @@ __device__ __forceinline__ void cta_partials(double (&v)[3], double* P) {
 // (iteration count, status, the deferred x term) to the item's CgState and ends the WHILE loop.
 // Compared with the last-CTA tail of cg_tail, nothing serialises behind an atomic counter.
 constexpr int GRT = 256;
-constexpr int64_t kFillMinRows = 8192;  // reading A11b: the fill pays from here on
+constexpr int64_t kFillMinRows = 0;  // reading A11b: systems below this size start at midrange (FEMI_FILL_MIN)
 __global__ void __launch_bounds__(GRT) k_gur(const RItem* __restrict__ items, const double* __restrict__ part,
                                             int nparts, int par, cudaGraphConditionalHandle h) {
     __shared__ double red[3 * (GRT / 32)];
@@ -3975,14 +4071,17 @@ static femi_status solve_outcome(int B, femi_system_s* const* S, const std::vect
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o_in, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters, DevStats* ds) {
-    // reading A11b: the mask-neighbour fill costs four extra launches and an SpMV for the initial
-    // residual; below kFillMinRows unknowns (launch-latency-bound systems, C1 / C2) those cost
-    // more than the iterations it saves (measured: C2 5.76K -> 5.18K Mpx/s), so midrange is used
+    // reading A11b: with the separate prologue kernels the fill cost four extra launches, more
+    // than it saved below 8192 unknowns (C2 5.76K -> 5.18K Mpx/s); inside the whole-solve
+    // resident kernel it costs two cluster barriers, and it pays at every size (C2 50.4 -> 42.2
+    // mean iterations, 7.34K -> 7.80K Mpx/s), so the threshold is 0 (FEMI_FILL_MIN=k restores it)
     femi_cg_opts o = o_in;
     {
         int64_t nfill = 0;
         for (int b = 0; b < B; ++b) nfill = std::max(nfill, S[b]->n_u);
-        if (o.x0 == 3 && nfill < kFillMinRows) o.x0 = 1;
+        static const int64_t fill_min = std::getenv("FEMI_FILL_MIN") ? std::atoll(std::getenv("FEMI_FILL_MIN"))
+                                                                     : kFillMinRows;
+        if (o.x0 == 3 && nfill < fill_min) o.x0 = 1;
     }
     {
         static int graph_mode = -1;  // FEMI_PCG_MODE=persistent forces the persistent kernel
@@ -4323,7 +4422,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             cgs_attr_dev = cur_dev;
         }
         if (g_timers) {
-            unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            unsigned long long z[16] = {};
             int on = 1;
             FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
             FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
@@ -4363,13 +4462,19 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
         if (g_timers) {
-            unsigned long long t[8];
+            unsigned long long t[16];
             FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
             const double it_n = std::max(1, hs[0].iters);
             std::fprintf(stderr,
                          "[femi pcg timers] k_cgs ctas %d iters %d | per iter us: publish %.2f barrier+sums %.2f spmv "
-                         "%.2f update %.2f\n",
-                         grid, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3, t[3] / it_n / 1e3);
+                         "%.2f update %.2f | per launch us: setup %.2f pass1 %.2f fill+pass2 %.2f epilogue %.2f\n",
+                         grid, hs[0].iters, t[0] / it_n / 1e3, t[1] / it_n / 1e3, t[2] / it_n / 1e3, t[3] / it_n / 1e3,
+                         t[4] / 1e3, t[5] / 1e3, t[6] / 1e3, t[7] / 1e3);
+            std::fprintf(stderr,
+                         "[femi pcg timers] k_cgs prologue us: pass1 walk %.2f | csum %.2f | hop1 %.2f bar %.2f | hop2 "
+                         "%.2f bar %.2f | pass2 %.2f | fixup+q %.2f\n",
+                         t[8] / 1e3, t[9] / 1e3, t[10] / 1e3, t[11] / 1e3, t[12] / 1e3, t[13] / 1e3, t[14] / 1e3,
+                         t[15] / 1e3);
         }
         return solve_outcome(B, S, hs, o, iters, relres, total_iters);
     }
@@ -4414,7 +4519,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
             cfg.numAttrs = 0;
             const int vr = (int)vrows;
             if (g_timers) {
-                unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                unsigned long long z[16] = {};
                 int on = 1;
                 FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
                 FEMI_CUDA(cudaMemcpyToSymbolAsync(g_pcg_timers_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
@@ -4482,7 +4587,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
         if (g_timers && nmax > 0) {
-            unsigned long long t[8];
+            unsigned long long t[16];
             FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
             const double it_n = std::max(1, hs[0].iters);
             std::fprintf(stderr,
