@@ -1380,13 +1380,19 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             tsub = t;
         }
     };
+    // slot j of this warp = slice 16 j + warp (even j) or 16 j + 15 - warp (odd j): inside a
+    // 64-row window the rows are sorted by length, so even slices hold the longer rows; the
+    // snake order gives every warp as many long as short slices (the iteration waits for the
+    // slowest warp of the cluster). Slot j + 1's slices all follow slot j's, so the first
+    // slot past nsl ends every warp's loop.
+    auto slot = [&](int j) { return RZW * j + ((j & 1) ? RZW - 1 - warp : warp); };
     // publish this lane's values of a vector into buffer buf (own part), then push the halo
     // entries peers read into their copies of buf (DSMEM stores; the caller's cluster barrier
     // makes them visible)
     auto publish = [&](double* buf, const double (&v)[RP]) {
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
-            const int sl = warp + RZW * j;
+            const int sl = slot(j);
             if (sl >= nsl) break;
             buf[32 * sl + lane] = v[j];
         }
@@ -1399,9 +1405,9 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             }
         }
     };
-    // this lane's rows: slot j = slice warp + RZW j
-    auto row_of = [&](int j) { return 32 * (S0 + warp + RZW * j) + lane; };
-    auto row_ok = [&](int j) { return warp + RZW * j < nsl && row_of(j) < R1; };
+    // this lane's rows: one per slot
+    auto row_of = [&](int j) { return 32 * (S0 + slot(j)) + lane; };
+    auto row_ok = [&](int j) { return slot(j) < nsl && row_of(j) < R1; };
     // cluster-wide fixed-order sum of three per-warp values (every warp gets the same bits)
     int par = 0;
     auto csum3 = [&](double l0, double l1, double l2, double& t0, double& t1, double& t2) {
@@ -1536,14 +1542,14 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     int Ls[RP], bs[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) {
-        const int sl = warp + RZW * j;
+        const int sl = slot(j);
         Ls[j] = sl < nsl ? len_s[sl] : 0;
         bs[j] = sl < nsl ? base_s[sl] + lane : 0;
     }
     auto spmv = [&](const double* buf, double (&out)[RP], const double (&in)[RP]) {
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
-            if (warp + RZW * j >= nsl) break;  // warp-uniform
+            if (slot(j) >= nsl) break;  // warp-uniform
             const int L = Ls[j], b = bs[j];
             double acc = 0.0;
             for (int k0 = 0; k0 < L; k0 += 4) {
@@ -1566,7 +1572,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     };
 #pragma unroll
     for (int j = 0; j < RP; ++j)
-        if (warp + RZW * j < nsl) q_s[32 * (warp + RZW * j) + lane] = row_ok(j) ? it.q[row_of(j)] : 0.0;
+        if (slot(j) < nsl) q_s[32 * slot(j) + lane] = row_ok(j) ? it.q[row_of(j)] : 0.0;
     // pass 2: x^0 = x0 / s and r^0 = s (b - A x0) = s b - A^ x^0 (A = D^1/2 A^ D^1/2, s = D^-1/2):
     // the product with the solver's own matrix in shared memory -- x^0 published like any CG
     // vector -- instead of a second walk over the unscaled rows in global memory (any r^0
@@ -1631,7 +1637,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             publish(wbp, w);
 #pragma unroll
             for (int j = 0; j < RP; ++j) {
-                const int sl = warp + RZW * j;
+                const int sl = slot(j);
                 if (sl >= nsl) break;
                 if (row_of(j) < R1) {
                     const double ru = r[j] * q_s[32 * sl + lane];
@@ -1678,7 +1684,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             gam = gam2;
 #pragma unroll
             for (int j = 0; j < RP; ++j) {
-                if (warp + RZW * j >= nsl) break;
+                if (slot(j) >= nsl) break;
                 z[j] = fma(beta, z[j], nv[j]);
                 sv[j] = fma(beta, sv[j], w[j]);
                 p[j] = fma(beta, p[j], r[j]);
