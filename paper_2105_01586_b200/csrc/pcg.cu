@@ -1291,6 +1291,8 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     __shared__ RItem its;
     __shared__ double part_p[2][16 * RZW][3];  // [parity][cta * RZW + warp][dot], DSMEM-written
     __shared__ unsigned long long kmm[16 * RZW][2];  // per-warp min / max keys of g
+    __shared__ double wsum3[RZW][3];                 // CG loop: per-warp partial dots
+    __shared__ double cpart[2][16][3];               // CG loop: per-CTA partial dots [parity][cta], DSMEM-written
     int item = blockIdx.x, rank = 0;
     if constexpr (CL) {
         unsigned cr, cid;
@@ -1633,8 +1635,11 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         double alpha = 0.0, gam = 0.0;
         for (;;) {
             double* wbp = par ? wb1 : wb0;
+            // partial dots of (r_i, w_i): per warp into shared memory, summed per CTA (fixed warp
+            // order) by warp 0 after the block barrier inside publish, which then writes the
+            // CTA's three values into every CTA's slot array; one cluster barrier; every warp
+            // sums the C slots (xor butterfly: the same bits everywhere)
             double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-            publish(wbp, w);
 #pragma unroll
             for (int j = 0; j < RP; ++j) {
                 const int sl = slot(j);
@@ -1646,10 +1651,43 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
                     l2 += ru * ru;
                 }
             }
+            l0 = warp_sum_d(l0);
+            l1 = warp_sum_d(l1);
+            l2 = warp_sum_d(l2);
+            if (lane == 0) {
+                wsum3[warp][0] = l0;
+                wsum3[warp][1] = l1;
+                wsum3[warp][2] = l2;
+            }
+            if (!CL || C == 1) __syncthreads();  // (publish has the block barrier for clusters)
+            publish(wbp, w);
+            if (warp == 0) {
+                double c0 = lane < RZW ? wsum3[lane][0] : 0.0;
+                double c1 = lane < RZW ? wsum3[lane][1] : 0.0;
+                double c2 = lane < RZW ? wsum3[lane][2] : 0.0;
+                c0 = warp_sum_d(c0);
+                c1 = warp_sum_d(c1);
+                c2 = warp_sum_d(c2);
+                if (lane < C) {
+                    double* dst = CL ? cluster.map_shared_rank(&cpart[par][0][0], lane) : &cpart[par][0][0];
+                    dst[3 * rank] = c0;
+                    dst[3 * rank + 1] = c1;
+                    dst[3 * rank + 2] = c2;
+                }
+            }
             mark(0);
+            rz_sync<CL>();
             double gam2, del2, rho2;
+            {
+                double a0 = lane < C ? cpart[par][lane][0] : 0.0;
+                double a1 = lane < C ? cpart[par][lane][1] : 0.0;
+                double a2 = lane < C ? cpart[par][lane][2] : 0.0;
+                gam2 = warp_sum_d(a0);
+                del2 = warp_sum_d(a1);
+                rho2 = warp_sum_d(a2);
+            }
             const int pp = par;
-            csum3(l0, l1, l2, gam2, del2, rho2);  // w_i and the partials of (r_i, w_i), cluster-wide
+            par ^= 1;
             mark(1);
             double nv[RP];
 #pragma unroll
