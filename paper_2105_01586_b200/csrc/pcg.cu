@@ -1265,19 +1265,23 @@ __global__ void __launch_bounds__(512) k_rz_send(const RItem* __restrict__ items
 // small or medium solve costs one launch instead of ~14 (the fixed cost dominated C1-C4).
 //   prologue: min/max of g (x0 modes 1, 3), b = -A_uk g (or the given b), the mask-neighbour
 //     fill (reading A11b: first hop from A_uk, two hops over A_uu through u_vert / w), x^0 and
-//     r^0 = s (b - A x0) with the unscaled rows (modes 2, 3), -s A_uk (g - c1) (mode 1), s b (0);
+//     r^0 = s b - A^ x^0 (modes 2, 3; = s (b - A x0) with the solver's matrix in shared memory),
+//     -s A_uk (g - c1) (mode 1), s b (mode 0); the rows of a lane are walked together;
 //   CG: pipelined single-reduction recurrence (Ghysels & Vanroose; Jacobi folded into A^ as
 //     everywhere here). With w = A^ r, s = A^ p, z = A^ s, per iteration
 //       gamma = r.r, delta = w.r, rho = ||D^1/2 r^||^2 (partials of r_i, w_i)  |  n = A^ w_i
 //       beta = gamma/gamma_prev, alpha = gamma/(delta - beta gamma/alpha_prev) (first: gamma/delta)
 //       z = n + beta z ; s = w + beta s ; p = r + beta p ; x += alpha p ; r -= alpha s ; w -= alpha z
 //     In exact arithmetic these are k_cgr's iterates; ONE cluster barrier per iteration carries
-//     both w_i (shared-memory buffer of parity i & 1, read by peers through DSMEM) and each
-//     warp's three partial dots (written straight into every CTA's slot array, parity i & 1);
-//     every warp then sums the C x 16 slots in a fixed order (xor butterfly: the same bits in
-//     every lane, warp and CTA, so alpha / beta / the stopping decision agree everywhere). A
+//     both w_i (shared-memory buffer of parity i & 1; the own rows written by their lanes, the
+//     halo entries pushed into the peers' buffers by DSMEM stores from per-CTA send lists) and
+//     the CTA's three partial dots (per warp, then per CTA in a fixed warp order, then written
+//     into every CTA's slot array of parity i & 1); every warp then sums the C slots in a fixed
+//     order (xor butterfly: the same bits in every lane, warp and CTA, so alpha / beta / the
+//     stopping decision agree everywhere) and multiplies from its own shared memory only. A
 //     buffer of parity k is rewritten two barriers later, after every CTA has passed the barrier
-//     in between, i.e. after every read of it;
+//     in between, i.e. after every read of it. Slices are dealt to warps in snake order (rows
+//     are length-sorted inside 64-row windows);
 //   epilogue: x = s x^ into u_vert, the true residual ||b - A x|| with the unscaled rows (reading
 //     A11) and, when it misses rtol, up to 8 restarts of the recurrence from r = s (b - A x)
 //     inside the same launch; the mask entries of u_vert = g; the CgState for the host.
@@ -1289,7 +1293,6 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) unsigned char rzm[];
     __shared__ RItem its;
-    __shared__ double part_p[2][16 * RZW][3];  // [parity][cta * RZW + warp][dot], DSMEM-written
     __shared__ unsigned long long kmm[16 * RZW][2];  // per-warp min / max keys of g
     __shared__ double wsum3[RZW][3];                 // CG loop: per-warp partial dots
     __shared__ double cpart[2][16][3];               // CG loop: per-CTA partial dots [parity][cta], DSMEM-written
@@ -1416,25 +1419,32 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         l0 = warp_sum_d(l0);
         l1 = warp_sum_d(l1);
         l2 = warp_sum_d(l2);
-        if (lane < C) {
-            double* dst = CL ? cluster.map_shared_rank(&part_p[par][0][0], lane) : &part_p[par][0][0];
-            dst[3 * (rank * RZW + warp)] = l0;
-            dst[3 * (rank * RZW + warp) + 1] = l1;
-            dst[3 * (rank * RZW + warp) + 2] = l2;
+        if (lane == 0) {
+            wsum3[warp][0] = l0;
+            wsum3[warp][1] = l1;
+            wsum3[warp][2] = l2;
+        }
+        __syncthreads();
+        if (warp == 0) {  // the CTA's sums (fixed warp order) into every CTA's slot array
+            double c0 = lane < RZW ? wsum3[lane][0] : 0.0;
+            double c1 = lane < RZW ? wsum3[lane][1] : 0.0;
+            double c2 = lane < RZW ? wsum3[lane][2] : 0.0;
+            c0 = warp_sum_d(c0);
+            c1 = warp_sum_d(c1);
+            c2 = warp_sum_d(c2);
+            if (lane < C) {
+                double* dst = CL ? cluster.map_shared_rank(&cpart[par][0][0], lane) : &cpart[par][0][0];
+                dst[3 * rank] = c0;
+                dst[3 * rank + 1] = c1;
+                dst[3 * rank + 2] = c2;
+            }
         }
         rz_sync<CL>();
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        for (int k = lane; k < C * RZW; k += 32) {
-            a0 += part_p[par][k][0];
-            a1 += part_p[par][k][1];
-            a2 += part_p[par][k][2];
-        }
-        t0 = warp_sum_d(a0);
-        t1 = warp_sum_d(a1);
-        t2 = warp_sum_d(a2);
+        t0 = warp_sum_d(lane < C ? cpart[par][lane][0] : 0.0);
+        t1 = warp_sum_d(lane < C ? cpart[par][lane][1] : 0.0);
+        t2 = warp_sum_d(lane < C ? cpart[par][lane][2] : 0.0);
         par ^= 1;
     };
-    if constexpr (CL) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     // ---------------- prologue
     const bool want_mm = (mode == 1 || mode == 3) && it.g != nullptr;
     if (want_mm) {  // min / max keys of g over a strided share, per warp -> every CTA's slots
@@ -4228,7 +4238,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     static const bool rz_off = std::getenv("FEMI_NO_RESIDENT") != nullptr;
     // whole-solve pipelined resident kernel k_cgs (default) or k_cgr + prologue/epilogue kernels (FEMI_CG_PIPE=0)
     static const bool rz_pipe = !(std::getenv("FEMI_CG_PIPE") && std::getenv("FEMI_CG_PIPE")[0] == '0');
-    const size_t rz_static = rz_pipe ? sizeof(double) * 2 * 16 * RZW * 3 + 16 * 16 * RZW : 0;
+    const size_t rz_static = rz_pipe ? 16 * 16 * RZW + sizeof(double) * (3 * RZW + 2 * 16 * 3) + 1024 : 0;
     if (!rz_off && !(B == 1 && S[0]->nnz_uu > 600000)) {
         const size_t rz_budget = (size_t)g_smem_optin - 4096;
         // cluster size: enough CTAs to fill the GPU (B C <= #SMs) while every warp keeps at least
