@@ -1642,7 +1642,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         spmv(wb_r, w, r);  // w^0 = A^ r^0
         par ^= 1;          // the buffer of r^0 is rewritten two barriers later
         const int iters0 = iters;
-        double alpha = 0.0, gam = 0.0;
+        double alpha = 0.0, gam = 0.0, rgam = 0.0, ralpha = 0.0;
         for (;;) {
             double* wbp = par ? wb1 : wb0;
             // partial dots of (r_i, w_i): per warp into shared memory, summed per CTA (fixed warp
@@ -1720,9 +1720,9 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
                     break;
                 }
                 alpha = gam2 / del2;
-            } else {
-                beta = gam2 / gam;
-                const double den = del2 - beta * gam2 / alpha;
+            } else {  // 1/gamma_prev and 1/alpha_prev were formed off the critical path
+                beta = gam2 * rgam;
+                const double den = del2 - beta * gam2 * ralpha;
                 if (!(den > 0.0)) {
                     status = FEMI_E_NEG_CURVATURE;
                     break;
@@ -1740,6 +1740,8 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
                 r[j] = fma(-alpha, sv[j], r[j]);
                 w[j] = fma(-alpha, z[j], w[j]);
             }
+            rgam = 1.0 / gam;  // (their latency hides in the next publish and barrier wait)
+            ralpha = 1.0 / alpha;
             ++iters;
             mark(3);
         }
