@@ -1294,7 +1294,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
     extern __shared__ __align__(16) unsigned char rzm[];
     __shared__ RItem its;
     __shared__ unsigned long long kmm[16 * RZW][2];  // per-warp min / max keys of g
-    __shared__ double wsum3[RZW][3];                 // CG loop: per-warp partial dots
+    __shared__ double wsum3[2][RZW][3];              // per-warp partial dots [parity][warp]
     __shared__ double cpart[2][16][3];               // CG loop: per-CTA partial dots [parity][cta], DSMEM-written
     int item = blockIdx.x, rank = 0;
     if constexpr (CL) {
@@ -1420,15 +1420,15 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         l1 = warp_sum_d(l1);
         l2 = warp_sum_d(l2);
         if (lane == 0) {
-            wsum3[warp][0] = l0;
-            wsum3[warp][1] = l1;
-            wsum3[warp][2] = l2;
+            wsum3[par][warp][0] = l0;
+            wsum3[par][warp][1] = l1;
+            wsum3[par][warp][2] = l2;
         }
         __syncthreads();
         if (warp == 0) {  // the CTA's sums (fixed warp order) into every CTA's slot array
-            double c0 = lane < RZW ? wsum3[lane][0] : 0.0;
-            double c1 = lane < RZW ? wsum3[lane][1] : 0.0;
-            double c2 = lane < RZW ? wsum3[lane][2] : 0.0;
+            double c0 = lane < RZW ? wsum3[par][lane][0] : 0.0;
+            double c1 = lane < RZW ? wsum3[par][lane][1] : 0.0;
+            double c2 = lane < RZW ? wsum3[par][lane][2] : 0.0;
             c0 = warp_sum_d(c0);
             c1 = warp_sum_d(c1);
             c2 = warp_sum_d(c2);
@@ -1665,16 +1665,25 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             l1 = warp_sum_d(l1);
             l2 = warp_sum_d(l2);
             if (lane == 0) {
-                wsum3[warp][0] = l0;
-                wsum3[warp][1] = l1;
-                wsum3[warp][2] = l2;
+                wsum3[par][warp][0] = l0;
+                wsum3[par][warp][1] = l1;
+                wsum3[par][warp][2] = l2;
             }
-            if (!CL || C == 1) __syncthreads();  // (publish has the block barrier for clusters)
+            double gam2, del2, rho2;
+            const int pp = par;
+            if constexpr (!CL) {  // one CTA: ONE block barrier, every warp sums the warp slots itself
+                publish(wbp, w);
+                mark(0);
+                __syncthreads();
+                gam2 = warp_sum_d(lane < RZW ? wsum3[par][lane][0] : 0.0);
+                del2 = warp_sum_d(lane < RZW ? wsum3[par][lane][1] : 0.0);
+                rho2 = warp_sum_d(lane < RZW ? wsum3[par][lane][2] : 0.0);
+            } else {
             publish(wbp, w);
             if (warp == 0) {
-                double c0 = lane < RZW ? wsum3[lane][0] : 0.0;
-                double c1 = lane < RZW ? wsum3[lane][1] : 0.0;
-                double c2 = lane < RZW ? wsum3[lane][2] : 0.0;
+                double c0 = lane < RZW ? wsum3[par][lane][0] : 0.0;
+                double c1 = lane < RZW ? wsum3[par][lane][1] : 0.0;
+                double c2 = lane < RZW ? wsum3[par][lane][2] : 0.0;
                 c0 = warp_sum_d(c0);
                 c1 = warp_sum_d(c1);
                 c2 = warp_sum_d(c2);
@@ -1687,7 +1696,6 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
             }
             mark(0);
             rz_sync<CL>();
-            double gam2, del2, rho2;
             {
                 double a0 = lane < C ? cpart[par][lane][0] : 0.0;
                 double a1 = lane < C ? cpart[par][lane][1] : 0.0;
@@ -1696,7 +1704,7 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
                 del2 = warp_sum_d(a1);
                 rho2 = warp_sum_d(a2);
             }
-            const int pp = par;
+            }
             par ^= 1;
             mark(1);
             double nv[RP];
@@ -4240,7 +4248,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     static const bool rz_off = std::getenv("FEMI_NO_RESIDENT") != nullptr;
     // whole-solve pipelined resident kernel k_cgs (default) or k_cgr + prologue/epilogue kernels (FEMI_CG_PIPE=0)
     static const bool rz_pipe = !(std::getenv("FEMI_CG_PIPE") && std::getenv("FEMI_CG_PIPE")[0] == '0');
-    const size_t rz_static = rz_pipe ? 16 * 16 * RZW + sizeof(double) * (3 * RZW + 2 * 16 * 3) + 1024 : 0;
+    const size_t rz_static = rz_pipe ? 16 * 16 * RZW + sizeof(double) * (6 * RZW + 2 * 16 * 3) + 2048 : 0;
     if (!rz_off && !(B == 1 && S[0]->nnz_uu > 600000)) {
         const size_t rz_budget = (size_t)g_smem_optin - 4096;
         // cluster size: enough CTAs to fill the GPU (B C <= #SMs) while every warp keeps at least
