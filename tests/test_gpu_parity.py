@@ -685,3 +685,60 @@ def test_system_shared_across_threads_and_streams(W):
         for j in range(3):
             assert torch.equal(us[j], u_ref), (k, j)
             assert torch.equal(es[j], e_ref), (k, j)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [1024, 2880])
+def test_failure_statuses(W):
+    """include/femi.h error contract on both solver paths (whole-solve resident kernel at
+    1024^2, graph mode at 2880^2): max_iter reached -> FEMI_E_NOT_CONVERGED (4) with exactly
+    max_iter iterations, finite outputs and a relative residual above rtol; a NaN in g ->
+    FEMI_E_NONFINITE (5) raised; the same system then solves normally (no state left behind)."""
+    if W == 1024:
+        c = make_config(4)
+        mk, un = c["mask"], c["unknowns"]
+    else:
+        c = make_config(5, W=W, H=W, seed=77)
+        rng = np.random.default_rng(7)
+        mk = np.union1d(c["mask0"], draw_mask(rng, W * W, len(c["mask0"])))
+        un = np.setdiff1d(c["unknowns"], mk)
+    f = dev(c["f"]).reshape(-1)
+    M = femi.Mesh(W, W, mk, un)
+    S = femi.System(M)
+    g = pipeline.mask_values(f, M.export()["vert_px"], S.n_u)
+    u = torch.empty(S.nv, dtype=torch.float64, device=DEV)
+    st, it, rel = femi.inpaint_solve_batched([S], [g], [u], femi.cg_opts(rtol=1e-10, max_iter=3))
+    assert st == 4 and it[0] == 3 and rel[0] > 1e-10, (st, it, rel)
+    assert torch.isfinite(u).all().item()
+    assert femi.solver_path(S) == ("resident" if W == 1024 else "graph_tma")
+    gn = g.clone()
+    gn[len(gn) // 2] = float("nan")
+    with pytest.raises(femi.FemiError) as ei:
+        femi.inpaint_solve_batched([S], [gn], [u], femi.cg_opts(rtol=1e-10))
+    assert ei.value.status == 5, str(ei.value)
+    st, it, rel = femi.inpaint_solve_batched([S], [g], [u], femi.cg_opts(rtol=1e-10))
+    assert st == 0 and rel[0] <= 1e-10
+    O = oracle.inpaint(W, W, c["f"], mk, un) if W == 1024 else None
+    if O is not None:
+        assert np.abs(u.cpu().numpy() - O["u_vert"]).max() <= GREY_TOL
+
+
+@pytest.mark.gpu
+def test_batched_status_isolated():
+    """A NaN in one item of a C2-style batch (one cluster per item): the call reports
+    FEMI_E_NONFINITE and the other items' solutions are still the oracle's."""
+    c = make_config(2)
+    W, H = c["W"], c["H"]
+    f = dev(c["f"])
+    meshes = [femi.Mesh(W, H, c["masks"][b], c["unknowns"][b]) for b in range(4)]
+    systems = [femi.System(M) for M in meshes]
+    gs = [pipeline.mask_values(f, M.export()["vert_px"], s.n_u) for M, s in zip(meshes, systems)]
+    gs[2] = gs[2].clone()
+    gs[2][0] = float("nan")
+    us = [torch.empty(s.nv, dtype=torch.float64, device=DEV) for s in systems]
+    with pytest.raises(femi.FemiError) as ei:
+        femi.inpaint_solve_batched(systems, gs, us, femi.cg_opts(rtol=1e-10))
+    assert ei.value.status == 5, str(ei.value)
+    for b in (0, 1, 3):
+        O = oracle.inpaint(W, H, c["f"], c["masks"][b], c["unknowns"][b])
+        assert np.abs(us[b].cpu().numpy() - O["u_vert"]).max() <= GREY_TOL, b
