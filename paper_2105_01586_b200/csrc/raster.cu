@@ -194,15 +194,24 @@ static_assert(sizeof(WinRec) == 48, "WinRec is 48 bytes");
 
 // Per mesh, after k_group_list: split each group's list into windows (greedy: a window ends
 // after 128 entries or before an entry 64 or more rows below its first one). FILL = 0 counts
-// the windows per group; FILL = 1 writes the records and the 32-bit entries. One lane per group
-// walks the list (setup only).
+// the windows per group; FILL = 1 writes the records and the 32-bit entries. One WARP per group
+// (setup only): the window's end is the first entry of a 32-entry ballot round that breaks the
+// row rule; per-triangle counts and the entries' triangle-major slots come from __match_any
+// rounds in entry order (rank among the round's lanes of the same triangle + a running count
+// per triangle), so the slots are the entries' positions in the window's triangle-major order,
+// pixel order inside a triangle.
 template <int FILL>
 __global__ void __launch_bounds__(RT) k_win(const TriRec* __restrict__ tri, int64_t T,
                                             const int32_t* __restrict__ tp_ptr, const uint64_t* __restrict__ gk,
                                             uint32_t* __restrict__ gl, int32_t* __restrict__ wcnt,
                                             const int32_t* __restrict__ wptr, WinRec* __restrict__ win) {
+    __shared__ int run_s[RWARPS][GT + 1];
+    __shared__ __align__(16) int rec_s[RWARPS][12];  // the 48-byte record being written
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ngroups = (T + GT - 1) / GT;
-    for (int64_t g = blockIdx.x * (int64_t)RT + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * RT) {
+    const int64_t gwarp = (int64_t)blockIdx.x * RWARPS + wid, nwarps = (int64_t)gridDim.x * RWARPS;
+    int* run = run_s[wid];
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
         const int64_t t0 = g * GT;
         const int nt = (int)min((int64_t)GT, T - t0);
         const int q0 = tp_ptr[t0], q1 = tp_ptr[t0 + nt];
@@ -211,47 +220,83 @@ __global__ void __launch_bounds__(RT) k_win(const TriRec* __restrict__ tri, int6
         int q = q0;
         while (q < q1) {
             const int ys = gk_y(gk[q]);
-            int e = q + 1;
-            while (e < q1 && e - q < RCH && gk_y(gk[e]) - ys < kWinRows) ++e;
+            const int lim = min(q1, q + RCH);
+            int e = lim;
+            for (int base = q + 1; base < lim; base += 32) {
+                const int k = base + lane;
+                const bool brk = k < lim && gk_y(gk[k]) - ys >= kWinRows;
+                const unsigned m = __ballot_sync(0xffffffffu, brk);
+                if (m) {
+                    e = base + __ffs(m) - 1;
+                    break;
+                }
+            }
             if (FILL) {
-                int cnt[GT];
-#pragma unroll
-                for (int k = 0; k < GT; ++k) cnt[k] = 0;
-                for (int k = q; k < e; ++k) {
-                    const int j = gk_j(gk[k]);
-#pragma unroll
-                    for (int jj = 0; jj < GT; ++jj) cnt[jj] += jj == j;
+                run[lane] = 0;
+                if (lane == 0) run[GT] = 0;
+                __syncwarp();
+                for (int base = q; base < e; base += 32) {  // entries per triangle
+                    const int k = base + lane;
+                    const bool act = k < e;
+                    const unsigned mask = __ballot_sync(0xffffffffu, act);
+                    if (act) {
+                        const int j = gk_j(gk[k]);
+                        const unsigned mm = __match_any_sync(mask, j);
+                        if (lane == __ffs(mm) - 1) run[j] += __popc(mm);
+                    }
+                    __syncwarp();
                 }
-                WinRec R = {};
-                R.q0 = q;
-                R.y0 = (int16_t)ys;
-                R.n = (uint8_t)(e - q);
-                int run = 0;
-#pragma unroll
-                for (int k = 0; k < GT; ++k) {
-                    R.start[k] = (uint8_t)run;
-                    run += cnt[k];
-                    cnt[k] = R.start[k];  // running slot per triangle
+                const int c = lane < GT ? run[lane] : 0;
+                int inc = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
                 }
-                R.start[GT] = (uint8_t)run;
-                FEMI_DCHECK(w < wptr[g + 1] && run == e - q && run <= RCH, 4);
-                win[w] = R;
-                for (int k = q; k < e; ++k) {
-                    const uint64_t v = gk[k];
-                    const int j = gk_j(v);
-                    int slot = 0;
-#pragma unroll
-                    for (int jj = 0; jj < GT; ++jj)
-                        if (jj == j) slot = cnt[jj]++;
-                    const uint32_t dyw = (uint32_t)(gk_y(v) - ys);
-                    gl[k] = ((uint32_t)slot << 25) | ((uint32_t)j << 20) | (dyw << 14) | ((uint32_t)(v >> 5) & 0x3fffu);
+                const int total = __shfl_sync(0xffffffffu, inc, 31);
+                FEMI_DCHECK(total == e - q && total <= RCH && w < wptr[g + 1], 4);
+                if (lane < 12) rec_s[wid][lane] = 0;
+                __syncwarp();
+                WinRec* R = reinterpret_cast<WinRec*>(rec_s[wid]);
+                if (lane == 0) {
+                    R->q0 = q;
+                    R->y0 = (int16_t)ys;
+                    R->n = (uint8_t)(e - q);
+                    R->start[GT] = (uint8_t)total;
+                }
+                R->start[lane] = (uint8_t)(inc - c);
+                __syncwarp();
+                run[lane] = inc - c;  // running slot per triangle
+                __syncwarp();
+                if (lane < 3) reinterpret_cast<int4*>(win + w)[lane] = reinterpret_cast<const int4*>(rec_s[wid])[lane];
+                for (int base = q; base < e; base += 32) {  // slots in entry order
+                    const int k = base + lane;
+                    const bool act = k < e;
+                    const unsigned mask = __ballot_sync(0xffffffffu, act);
+                    int slot = 0, j = 0;
+                    uint64_t v = 0;
+                    unsigned mm = 0;
+                    if (act) {
+                        v = gk[k];
+                        j = gk_j(v);
+                        mm = __match_any_sync(mask, j);
+                        slot = run[j] + __popc(mm & ((1u << lane) - 1u));
+                    }
+                    __syncwarp();
+                    if (act && lane == __ffs(mm) - 1) run[j] += __popc(mm);
+                    __syncwarp();
+                    if (act) {
+                        const uint32_t dyw = (uint32_t)(gk_y(v) - ys);
+                        gl[k] = ((uint32_t)slot << 25) | ((uint32_t)j << 20) | (dyw << 14) |
+                                ((uint32_t)(v >> 5) & 0x3fffu);
+                    }
                 }
                 ++w;
             }
             ++nw;
             q = e;
         }
-        if (!FILL) wcnt[g] = nw;
+        if (!FILL && lane == 0) wcnt[g] = nw;
+        __syncwarp();
     }
 }
 
@@ -622,7 +667,7 @@ femi_status build_owner_tables(femi_system_s* S, cudaStream_t st) {
     const int nbg = (int)((ngroups + SCB - 1) / SCB);
     FEMI_CUDA(cudaMallocAsync(&S->tp_wptr, sizeof(int32_t) * (ngroups + 1), st));  // freed with the system
     S->allocs.push_back(S->tp_wptr);
-    const int gw = (int)std::min<int64_t>((ngroups + RT - 1) / RT, 148 * 8);
+    const int gw = warp_grid(T, 1);
     k_win<0><<<gw, RT, 0, st>>>(S->tri, T, S->tp_ptr, gk, nullptr, cnt, nullptr, nullptr);
     k_scan_blocks<<<nbg, SCB, 0, st>>>(ngroups, cnt, bsum);
     k_scan_bsum<<<1, 32, 0, st>>>(nbg, bsum);
