@@ -456,110 +456,130 @@ femi_status femi_assemble(femi_mesh mesh, femi_stream stream, femi_system* out) 
         parallel_ranges(n, [&](int64_t lo, int64_t hi) {
             for (int64_t i = lo; i < hi; ++i) pos[pi[i]] = (int32_t)i;
         });
-        // SELL-32: slice lengths, offsets, then the entries slice by slice
-        const int32_t nsl = (int32_t)((n + 31) / 32);
-        std::vector<int32_t> len(nsl), base(nsl);
-        parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
-            for (int64_t sl = lo; sl < hi; ++sl) {
-                int32_t L = 0;
-                for (int l = 0; l < 32 && 32 * sl + l < n; ++l) L = std::max(L, rl(pi[32 * sl + l]));
-                len[sl] = L;
-            }
-        }, 512);
-        int64_t ent = 0;
-        for (int32_t sl = 0; sl < nsl; ++sl) {
-            base[sl] = (int32_t)ent;
-            ent += 32 * (int64_t)len[sl];
-        }
-        std::vector<int32_t> src(ent), c32(ent);
-        std::atomic<bool> fits16{true};
-        parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
-            bool f16 = true;
-            for (int64_t sl = lo; sl < hi; ++sl) {
-                const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
-                int64_t q = base[sl];
-                for (int32_t k = 0; k < len[sl]; ++k)
-                    for (int l = 0; l < 32; ++l, ++q) {
-                        const int64_t ri = 32 * sl + l;
-                        int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
-                        if (ri < n && k < rl(pi[ri])) {
-                            const int32_t row = pi[ri];
-                            col = pos[uc[kth(row, k)]];
-                            sidx = (rp[row] - row) + k;  // index into o_val (natural CSR)
-                        }
-                        src[q] = sidx;
-                        c32[q] = col;
-                        const int32_t d = col - wbase;
-                        if (d < -32768 || d > 32767) f16 = false;
-                    }
-            }
-            if (!f16) fits16 = false;
-        }, 512);
-        S->nslices = nsl;
-        S->sell_nnz = ent;
-        stamp("sell_host");
-        U(upload(S, &S->sell_len, len, st));
-        U(upload(S, &S->sell_base, base, st));
-        S->sell_base_h = base;
-        S->sell_base_h.push_back((int32_t)ent);  // [nslices] = total entries
-        U(upload(S, &S->sell_inv, pi, st));
-        {
-            // internal-order CSR copies of A_uk and A_uu (with their natural-CSR sources)
-            std::vector<int32_t> ukr(n + 1, 0), uur(n + 1, 0);
-            for (int64_t i = 0; i < n; ++i) {
-                const int32_t nat = pi[i];
-                ukr[i + 1] = ukr[i] + (M.uk_rowptr[nat + 1] - M.uk_rowptr[nat]);
-                uur[i + 1] = uur[i] + (rp[nat + 1] - rp[nat]);
-            }
-            std::vector<int32_t> ukc(ukr[n]), uks(ukr[n]), uuc(uur[n]), uus(uur[n]);
-            parallel_ranges(n, [&](int64_t lo, int64_t hi) {
-                for (int64_t i = lo; i < hi; ++i) {
-                    const int32_t nat = pi[i];
-                    int32_t o = ukr[i];
-                    for (int32_t e = M.uk_rowptr[nat]; e < M.uk_rowptr[nat + 1]; ++e, ++o) {
-                        ukc[o] = M.uk_col[e];
-                        uks[o] = e;
-                    }
-                    o = uur[i];
-                    for (int32_t e = rp[nat]; e < rp[nat + 1]; ++e, ++o) {
-                        uuc[o] = uc[e];
-                        uus[o] = e;
-                    }
-                }
-            });
-            U(upload(S, &S->ukI_rowptr, ukr, st));
-            U(upload(S, &S->uuI_rowptr, uur, st));
-            if (!ukc.empty()) {
-                U(upload(S, &S->ukI_col, ukc, st));
-                U(upload(S, &S->ukI_src_tmp, uks, st));
-                U(alloc(S, &S->ukI_val, ukc.size()));
-            }
-            if (!uuc.empty()) {
-                U(upload(S, &S->uuI_col, uuc, st));
-                U(upload(S, &S->uuI_src_tmp, uus, st));
-                U(alloc(S, &S->uuI_val, uuc.size()));
-            }
-        }
-        U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
-        // padded to whole JDS tiles: the TMA tiles read s_int in kJdsRows blocks
-        U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
-        U(alloc(S, &S->q_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
-        if (fits16) {
-            std::vector<int16_t> c16(c32.size());
+        // The layouts below are built on the device for systems under graph-mode size (the
+        // per-densification-step path; FEMI_SELL_HOST=1 keeps the host construction): same arrays,
+        // entry for entry (assemble.cu sell_layout_device).
+        static const bool sell_host = std::getenv("FEMI_SELL_HOST") != nullptr;
+        if (!sell_host && S->nnz_uu <= kGraphNnz && n > 0) {
+            U(upload(S, &S->sell_inv, pi, st));
+            int32_t nsl_d = 0;
+            int64_t ent_d = 0;
+            bool f16_d = true;
+            U(sell_layout_device(S, n, S->sell_inv, st,
+                                 [&](void** p, size_t bytes) { return dev_alloc(S, p, bytes); }, &nsl_d, &ent_d,
+                                 &f16_d));
+            S->nslices = nsl_d;
+            S->sell_nnz = ent_d;
+            stamp("sell_host");
+            U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent_d, 1)));
+            U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
+            U(alloc(S, &S->q_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
+        } else {
+            // SELL-32: slice lengths, offsets, then the entries slice by slice
+            const int32_t nsl = (int32_t)((n + 31) / 32);
+            std::vector<int32_t> len(nsl), base(nsl);
             parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
                 for (int64_t sl = lo; sl < hi; ++sl) {
-                    const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
-                    for (int64_t q = base[sl]; q < base[sl] + 32 * (int64_t)len[sl]; ++q)
-                        c16[q] = (int16_t)(c32[q] - wbase);
+                    int32_t L = 0;
+                    for (int l = 0; l < 32 && 32 * sl + l < n; ++l) L = std::max(L, rl(pi[32 * sl + l]));
+                    len[sl] = L;
                 }
             }, 512);
-            U(upload(S, &S->sell_c16, c16, st));
-        } else {
-            U(upload(S, &S->sell_c32, c32, st));
+            int64_t ent = 0;
+            for (int32_t sl = 0; sl < nsl; ++sl) {
+                base[sl] = (int32_t)ent;
+                ent += 32 * (int64_t)len[sl];
+            }
+            std::vector<int32_t> src(ent), c32(ent);
+            std::atomic<bool> fits16{true};
+            parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
+                bool f16 = true;
+                for (int64_t sl = lo; sl < hi; ++sl) {
+                    const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
+                    int64_t q = base[sl];
+                    for (int32_t k = 0; k < len[sl]; ++k)
+                        for (int l = 0; l < 32; ++l, ++q) {
+                            const int64_t ri = 32 * sl + l;
+                            int32_t col = (int32_t)std::min<int64_t>(ri, n - 1), sidx = -1;
+                            if (ri < n && k < rl(pi[ri])) {
+                                const int32_t row = pi[ri];
+                                col = pos[uc[kth(row, k)]];
+                                sidx = (rp[row] - row) + k;  // index into o_val (natural CSR)
+                            }
+                            src[q] = sidx;
+                            c32[q] = col;
+                            const int32_t d = col - wbase;
+                            if (d < -32768 || d > 32767) f16 = false;
+                        }
+                }
+                if (!f16) fits16 = false;
+            }, 512);
+            S->nslices = nsl;
+            S->sell_nnz = ent;
+            stamp("sell_host");
+            U(upload(S, &S->sell_len, len, st));
+            U(upload(S, &S->sell_base, base, st));
+            S->sell_base_h = base;
+            S->sell_base_h.push_back((int32_t)ent);  // [nslices] = total entries
+            U(upload(S, &S->sell_inv, pi, st));
+            {
+                // internal-order CSR copies of A_uk and A_uu (with their natural-CSR sources)
+                std::vector<int32_t> ukr(n + 1, 0), uur(n + 1, 0);
+                for (int64_t i = 0; i < n; ++i) {
+                    const int32_t nat = pi[i];
+                    ukr[i + 1] = ukr[i] + (M.uk_rowptr[nat + 1] - M.uk_rowptr[nat]);
+                    uur[i + 1] = uur[i] + (rp[nat + 1] - rp[nat]);
+                }
+                std::vector<int32_t> ukc(ukr[n]), uks(ukr[n]), uuc(uur[n]), uus(uur[n]);
+                parallel_ranges(n, [&](int64_t lo, int64_t hi) {
+                    for (int64_t i = lo; i < hi; ++i) {
+                        const int32_t nat = pi[i];
+                        int32_t o = ukr[i];
+                        for (int32_t e = M.uk_rowptr[nat]; e < M.uk_rowptr[nat + 1]; ++e, ++o) {
+                            ukc[o] = M.uk_col[e];
+                            uks[o] = e;
+                        }
+                        o = uur[i];
+                        for (int32_t e = rp[nat]; e < rp[nat + 1]; ++e, ++o) {
+                            uuc[o] = uc[e];
+                            uus[o] = e;
+                        }
+                    }
+                });
+                U(upload(S, &S->ukI_rowptr, ukr, st));
+                U(upload(S, &S->uuI_rowptr, uur, st));
+                if (!ukc.empty()) {
+                    U(upload(S, &S->ukI_col, ukc, st));
+                    U(upload(S, &S->ukI_src_tmp, uks, st));
+                    U(alloc(S, &S->ukI_val, ukc.size()));
+                }
+                if (!uuc.empty()) {
+                    U(upload(S, &S->uuI_col, uuc, st));
+                    U(upload(S, &S->uuI_src_tmp, uus, st));
+                    U(alloc(S, &S->uuI_val, uuc.size()));
+                }
+            }
+            U(alloc(S, &S->sell_val, (size_t)std::max<int64_t>(ent, 1)));
+            // padded to whole JDS tiles: the TMA tiles read s_int in kJdsRows blocks
+            U(alloc(S, &S->s_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
+            U(alloc(S, &S->q_int, (size_t)std::max<int64_t>((n + kJdsRows - 1) / kJdsRows * kJdsRows, 1)));
+            if (fits16) {
+                std::vector<int16_t> c16(c32.size());
+                parallel_ranges(nsl, [&](int64_t lo, int64_t hi) {
+                    for (int64_t sl = lo; sl < hi; ++sl) {
+                        const int32_t wbase = (int32_t)((32 * sl / SIG) * SIG);
+                        for (int64_t q = base[sl]; q < base[sl] + 32 * (int64_t)len[sl]; ++q)
+                            c16[q] = (int16_t)(c32[q] - wbase);
+                    }
+                }, 512);
+                U(upload(S, &S->sell_c16, c16, st));
+            } else {
+                U(upload(S, &S->sell_c32, c32, st));
+            }
+            int32_t* d_src = nullptr;
+            U(upload(S, &d_src, src, st));
+            S->sell_src_tmp = d_src;
         }
-        int32_t* d_src = nullptr;
-        U(upload(S, &d_src, src, st));
-        S->sell_src_tmp = d_src;
         stamp("sell");
         if (S->nnz_uu > kGraphNnz) {
             // tiled jagged-diagonal layout (device.cuh) of the same internal order: per tile,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -210,6 +211,11 @@ constexpr int kJdsMaxK = 24;           // longest row (off-diagonals) the JDS la
 // launchers (defined in the .cu files)
 femi_status launch_tri_records(femi_system_s* S, const int32_t* d_tri, const uint32_t* d_flags, cudaStream_t st);
 femi_status launch_assemble_values(femi_system_s* S, cudaStream_t st);
+// S1 solver layouts on the device (assemble.cu): SELL slices + internal-order A_uu / A_uk rows
+// from the internal order d_pi; sets S->sell_*, S->sell_base_h, S->ukI_*, S->uuI_*
+femi_status sell_layout_device(femi_system_s* S, int64_t n, const int32_t* d_pi, cudaStream_t st,
+                               const std::function<femi_status(void**, size_t)>& alloc_dev, int32_t* n_slices,
+                               int64_t* n_entries, bool* fits16);
 femi_status launch_raster(int B, femi_system_s* const* S, const double* const* u_vert, const double* const* f,
                           double* const* u_px, double* const* e_px, double* const* tri_err,
                           int32_t* const* best, double* const* sse, cudaStream_t st);

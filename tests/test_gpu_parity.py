@@ -742,3 +742,30 @@ def test_batched_status_isolated():
     for b in (0, 1, 3):
         O = oracle.inpaint(W, H, c["f"], c["masks"][b], c["unknowns"][b])
         assert np.abs(us[b].cpu().numpy() - O["u_vert"]).max() <= GREY_TOL, b
+
+
+@pytest.mark.gpu
+def test_device_layouts_match_host(tmp_path):
+    """The solver layouts built on the device (SELL slices, internal-order A_uu / A_uk rows) are
+    the host construction's arrays entry for entry: solves and rasters through them (C1, four C2
+    items, the C3 start mesh, C4) give bit-identical vertex values, iteration counts and SSE in a
+    process with FEMI_SELL_HOST=1."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for host in (False, True):
+        env = dict(os.environ)
+        env.pop("FEMI_SELL_HOST", None)
+        if host:
+            env["FEMI_SELL_HOST"] = "1"
+        p = tmp_path / f"lay_{int(host)}.npz"
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "sell_probe.py"), str(p)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(p))
+    a, b = outs
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
