@@ -769,3 +769,50 @@ def test_device_layouts_match_host(tmp_path):
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,m,p,path", [(1024, 84000, 45000, "resident"), (1536, 70800, 70800, "persistent")])
+def test_solver_size_classes(W, m, p, path):
+    """The upper size classes of the small/medium solvers against the oracle (check_inpaint:
+    mesh, grey values, MSE, error maps): 45K unknowns among 84K mask pixels (short A_uu rows, ~88
+    slices per CTA of a 16-CTA cluster: the resident kernel's largest register variant), and
+    71K unknowns -- too many slices for one cluster, below graph-mode size -- the persistent
+    cooperative kernel."""
+    rng = np.random.default_rng(W)
+    c = make_config(4, W=W, H=W, seed=W)
+    mk = draw_mask(rng, W * W, m)
+    un = draw_unknowns(rng, W, W, mk, p)
+    check_inpaint(W, W, c["f"], mk, un)
+    M = femi.Mesh(W, W, mk, un)
+    S = femi.System(M)
+    g = pipeline.mask_values(dev(c["f"]).reshape(-1), M.export()["vert_px"], S.n_u)
+    u = torch.empty(S.nv, dtype=torch.float64, device=DEV)
+    femi.inpaint_solve_batched([S], [g], [u], femi.cg_opts(rtol=1e-10))
+    assert femi.solver_path(S) == path, (femi.solver_path(S), S.n_u)
+
+
+@pytest.mark.gpu
+def test_resident_batch_with_empty_ctas():
+    """A batch of tiny systems on 4-CTA clusters (C2-style launch): most CTAs own no rows at all
+    (one 64-row window per system), which the whole-solve kernel must handle in its barriers and
+    reductions; every item against the oracle."""
+    rng = np.random.default_rng(5)
+    W = H = 24
+    items = []
+    for b in range(40):
+        mk = draw_mask(rng, W * H, 12)
+        un = draw_unknowns(rng, W, H, mk, 40)
+        items.append((mk, un))
+    f = rng.uniform(0, 255, (H, W))
+    fd = dev(f).reshape(-1)
+    meshes = [femi.Mesh(W, H, mk, un) for mk, un in items]
+    systems = [femi.System(M) for M in meshes]
+    gs = [pipeline.mask_values(fd, M.export()["vert_px"], s.n_u) for M, s in zip(meshes, systems)]
+    us = [torch.empty(s.nv, dtype=torch.float64, device=DEV) for s in systems]
+    st, it, rel = femi.inpaint_solve_batched(systems, gs, us, femi.cg_opts(rtol=1e-10))
+    assert st == 0 and np.all(rel <= 1e-10)
+    assert femi.solver_path(systems[0]) == "resident"
+    for b, (mk, un) in enumerate(items):
+        O = oracle.inpaint(W, H, f, mk, un)
+        assert np.abs(us[b].cpu().numpy() - O["u_vert"]).max() <= GREY_TOL, b
