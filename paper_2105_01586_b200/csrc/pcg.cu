@@ -24,6 +24,7 @@
 // barrier (a cluster of <= 16 CTAs: C1-C4), or a flag-array barrier over a cooperative
 // grid (one huge system: C5).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -4135,6 +4136,14 @@ static femi_status solve_outcome(int B, femi_system_s* const* S, const std::vect
 femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, const double* const* bin,
                       double* const* u_vert, const femi_cg_opts& o_in, int32_t* iters, double* relres,
                       cudaStream_t st, int64_t* total_iters, DevStats* ds) {
+    // FEMI_SOLVE_HOSTPROF=1: host-side time stamps of the whole-solve path (diagnostic)
+    static const bool hprof = std::getenv("FEMI_SOLVE_HOSTPROF") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
+    auto hstamp = [&](const char* what) {
+        if (hprof)
+            std::fprintf(stderr, "[femi solve host] %-12s %7.2f us\n", what,
+                         1e6 * std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count());
+    };
     // reading A11b: with the separate prologue kernels the fill cost four extra launches, more
     // than it saved below 8192 unknowns (C2 5.76K -> 5.18K Mpx/s); inside the whole-solve
     // resident kernel it costs two cluster barriers, and it pays at every size (C2 50.4 -> 42.2
@@ -4321,6 +4330,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
     if (nvec < 2) nvec = 0;
     const size_t smem_bytes = meta_bytes + sizeof(double) * ((size_t)nvec * vrows);
 
+    hstamp("shape");
     // ---- workspace
     std::vector<RItem> items(B);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -4471,6 +4481,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         else rz_smem = need;
     }
     FEMI_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(RItem) * B, cudaMemcpyHostToDevice, st));
+    hstamp("items_up");
     FEMI_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * 2 * B, st));
 
     // ---- whole-solve resident kernel: one cluster launch per item does everything
@@ -4513,8 +4524,10 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         double rt = o.rtol;
         int mi = o.max_iter;
         void* args[3] = {(void*)&di, (void*)&rt, (void*)&mi};
+        hstamp("pre_launch");
         const cudaError_t e = cudaLaunchKernelExC(&cfg, ncta_item > 1 ? fp_cl[rpi] : fp_1[rpi], args);
         if (e != cudaSuccess) return cuda_fail(e, "k_cgs launch");
+        hstamp("launched");
         count_launches(1);
         if (ds) {
             k_stats<<<1, 32, 0, st>>>(B, d_items, ds);
@@ -4525,6 +4538,7 @@ femi_status pcg_solve(int B, femi_system_s* const* S, const double* const* g, co
         std::vector<CgState> hs(B);
         FEMI_CUDA(cudaMemcpyAsync(hs.data(), d_state, sizeof(CgState) * B, cudaMemcpyDeviceToHost, st));
         FEMI_CUDA(cudaStreamSynchronize(st));
+        hstamp("synced");
         if (g_timers) {
             unsigned long long t[16];
             FEMI_CUDA(cudaMemcpyFromSymbol(t, g_pcg_timers, sizeof(t)));
