@@ -1342,20 +1342,21 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         len_s[sl] = it.len[S0 + sl];
         base_s[sl] = it.base[S0 + sl] - e0;
     }
-    {  // the CTA's entries are one contiguous range: a flat copy, four loads in flight per thread
+    {  // the CTA's entries are one contiguous range: a flat copy, sixteen loads in flight per thread
         const double* __restrict__ gv = it.val + e0;
         const uint16_t* __restrict__ gc = it.rzc + e0;
-        for (int i0 = 0; i0 < ne; i0 += 4 * RZT) {
-            double v[4];
-            uint16_t c[4];
+        constexpr int CU = 16;  // loads in flight per thread (registers are free before the prologue)
+        for (int i0 = 0; i0 < ne; i0 += CU * RZT) {
+            double v[CU];
+            uint16_t c[CU];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < CU; ++u) {
                 const int i = i0 + u * RZT + tid;
                 v[u] = i < ne ? gv[i] : 0.0;
                 c[u] = i < ne ? gc[i] : (uint16_t)0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < CU; ++u) {
                 const int i = i0 + u * RZT + tid;
                 if (i < ne) {
                     val_s[i] = v[u];
@@ -1404,7 +1405,9 @@ __global__ void __launch_bounds__(RZT, 1) k_cgs(const RItem* __restrict__ items,
         }
         if (CL && C > 1) {
             __syncthreads();
-            for (int i = tid; i < nsnd; i += RZT) {
+            // warps 1.. push the halo entries; warp 0 goes on to the CTA's partial sums
+            if (warp > 0)
+            for (int i = tid - 32; i < nsnd; i += RZT - 32) {
                 const uint32_t e = snd_s[i];
                 double* dst = cluster.map_shared_rank(buf, (int)((e >> 12) & 15u));
                 dst[HB + (int)(e >> 16)] = buf[e & 0xfffu];
