@@ -72,6 +72,15 @@ __global__ void k_axpy_q(int64_t n, const double* __restrict__ num, const double
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = fma(alpha, x[i], y[i]);
 }
+// y = x + (num / den) y with the quotient formed on the device (the same IEEE quotient the host
+// formed before): enqueued before the host has seen the new dot, so no host round trip sits
+// between an outer iteration's adjoint solve and the next forward solve
+__global__ void k_xpby_q(int64_t n, const double* __restrict__ x, const double* __restrict__ num,
+                         const double* __restrict__ den, double* __restrict__ y) {
+    const double beta = *num / *den;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fma(beta, y[i], x[i]);
+}
 __global__ void k_xpby(int64_t n, const double* __restrict__ x, double beta, double* __restrict__ y) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = fma(beta, y[i], x[i]);
@@ -207,6 +216,27 @@ struct Tonal {
 
 }  // namespace
 
+struct TonalReadback {
+    double gam2, qq;
+    DevStats ds;
+};
+// one pinned readback block per host thread, allocated on first use and kept (cudaMallocHost /
+// cudaFreeHost per call cost more than the host round trips they save)
+TonalReadback* tonal_readback() {
+    struct Holder {
+        TonalReadback* p = nullptr;
+        ~Holder() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Holder h;
+    if (!h.p && cudaMallocHost(&h.p, sizeof(TonalReadback)) != cudaSuccess) {
+        cudaGetLastError();
+        h.p = nullptr;
+    }
+    return h.p;
+}
+
 femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_tonal_opts& o,
                        femi_tonal_report* rep, cudaStream_t st, const double* sw) {
     const int64_t N = (int64_t)S->W * S->H, m = S->m, nv = S->nv, T = S->T;
@@ -242,6 +272,7 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
     tn.ds = (DevStats*)take(sizeof(DevStats));
     FEMI_CUDA(cudaMemsetAsync(tn.ds, 0, sizeof(DevStats), st));
     DevStats hds = {};
+    TonalReadback* rb = nullptr;
     femi_status rc = FEMI_OK;
 #define TRY(x)                      \
     do {                            \
@@ -274,11 +305,18 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
             TRY(tn.apply_BT(r, s));
         }
         FEMI_CUDA(cudaMemcpyAsync(p, s, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-        double* gam_d = tn.dres + 1;  // gam on the device: alpha = gam / q.q is formed there
+        // gam on the device in two slots by outer-iteration parity (alpha = gam / q.q and
+        // beta = gam_new / gam are formed there)
+        double* gslot[2] = {tn.dres + 1, tn.dres + 3};
         double* qq_d = tn.dres + 2;
-        TRY(tn.dot(m, s, s, &gam, gam_d));
+        TRY(tn.dot(m, s, s, &gam, gslot[0]));
         double relg = btf > 0.0 ? std::sqrt(gam) / btf : 0.0;
+        // pinned readback of (gam_new, q.q, the inner-solve statistics): one copy batch and one
+        // synchronisation per outer iteration
+        rb = tonal_readback();
         while (relg >= o.outer_rtol && outer < o.outer_max) {
+            double* gam_d = gslot[outer & 1];
+            double* gam_n = gslot[(outer + 1) & 1];
             TRY(tn.apply_B(p, q));
             if (sw) {
                 k_mul<<<grid_for(N), TT, 0, st>>>(N, sw, q, q);
@@ -294,8 +332,23 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
             } else {
                 TRY(tn.apply_BT(r, s));
             }
-            TRY(tn.dot(m, s, s, &gam2, gam_d, qq_d, &qq));  // gam_d <- s.s for the next alpha
-            FEMI_CUDA(cudaMemcpy(&hds, tn.ds, sizeof(DevStats), cudaMemcpyDeviceToHost));  // stream synchronised above
+            TRY(tn.dot(m, s, s, nullptr, gam_n));  // s.s: the next alpha's numerator
+            // p = s + beta p before the host has looked (p is not read after the loop)
+            k_xpby_q<<<grid_for(m), TT, 0, st>>>(m, s, gam_n, gam_d, p); count_launches(1);
+            if (rb) {
+                FEMI_CUDA(cudaMemcpyAsync(&rb->gam2, gam_n, sizeof(double), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaMemcpyAsync(&rb->qq, qq_d, sizeof(double), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaMemcpyAsync(&rb->ds, tn.ds, sizeof(DevStats), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaStreamSynchronize(st));
+                gam2 = rb->gam2;
+                qq = rb->qq;
+                hds = rb->ds;
+            } else {
+                FEMI_CUDA(cudaMemcpyAsync(&gam2, gam_n, sizeof(double), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaMemcpyAsync(&qq, qq_d, sizeof(double), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaMemcpyAsync(&hds, tn.ds, sizeof(DevStats), cudaMemcpyDeviceToHost, st));
+                FEMI_CUDA(cudaStreamSynchronize(st));
+            }
             if (hds.status == FEMI_E_NONFINITE || hds.status == FEMI_E_NEG_CURVATURE) {
                 rc = (femi_status)hds.status;
                 goto out;
@@ -307,14 +360,10 @@ femi_status tonal_cgls(femi_system_s* S, const double* f, double* g, const femi_
                 rc = FEMI_E_NONFINITE;
                 goto out;
             }
-            if (relg < o.outer_rtol) {
-                gam = gam2;
-                break;
-            }
-            const double beta = gam2 / gam;
-            k_xpby<<<grid_for(m), TT, 0, st>>>(m, s, beta, p); count_launches(1);
             gam = gam2;
+            if (relg < o.outer_rtol) break;
         }
+
         rep->rel_grad_recursive = relg;
         rep->outer_iters = outer;
         TRY(tn.apply_B(g, u));

@@ -3,7 +3,7 @@
 # the driver's C5 bench line, the reference arm, C1-C4 / C6 / C3 variants, C5 loop timeline, the
 # graph-level launch list of the C5 timed region with DRAM bytes, the resident solver's phase
 # timers, and ncu --set full of k_raster_grp, k_gur/k_gt (standalone) and k_cgs (C4, C2).
-cd "$GRAFT_REPO_ROOT"; O=gpurun_out/ev; mkdir -p $O
+cd "$GRAFT_REPO_ROOT"; O=gpurun_out/${EVDIR:-ev}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu.txt 2>&1
 nproc >> $O/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
