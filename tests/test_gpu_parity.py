@@ -816,3 +816,28 @@ def test_resident_batch_with_empty_ctas():
     for b, (mk, un) in enumerate(items):
         O = oracle.inpaint(W, H, f, mk, un)
         assert np.abs(us[b].cpu().numpy() - O["u_vert"]).max() <= GREY_TOL, b
+
+
+@pytest.mark.gpu
+def test_resident_cluster_size_switch():
+    """One system solved alone (an 8-CTA cluster), then inside a 32-item batch (4-CTA clusters),
+    then alone again: the per-system halo tables are rebuilt for each cluster size and every
+    solve matches the oracle; the two single solves are bit-identical (same cluster size, same
+    fixed-order reductions)."""
+    c = make_config(2)
+    W, H = c["W"], c["H"]
+    f = dev(c["f"]).reshape(-1)
+    meshes = [femi.Mesh(W, H, c["masks"][b], c["unknowns"][b]) for b in range(32)]
+    systems = [femi.System(M) for M in meshes]
+    gs = [pipeline.mask_values(f, M.export()["vert_px"], s.n_u) for M, s in zip(meshes, systems)]
+    O = oracle.inpaint(W, H, c["f"], c["masks"][0], c["unknowns"][0])
+    u_a = torch.empty(systems[0].nv, dtype=torch.float64, device=DEV)
+    femi.inpaint_solve_batched([systems[0]], [gs[0]], [u_a], femi.cg_opts(rtol=1e-10))
+    us = [torch.empty(s.nv, dtype=torch.float64, device=DEV) for s in systems]
+    st, it, rel = femi.inpaint_solve_batched(systems, gs, us, femi.cg_opts(rtol=1e-10))
+    assert st == 0 and np.all(rel <= 1e-10)
+    u_b = torch.empty_like(u_a)
+    femi.inpaint_solve_batched([systems[0]], [gs[0]], [u_b], femi.cg_opts(rtol=1e-10))
+    for u in (u_a, us[0], u_b):
+        assert np.abs(u.cpu().numpy() - O["u_vert"]).max() <= GREY_TOL
+    assert torch.equal(u_a, u_b)
