@@ -58,7 +58,6 @@ struct LoopState {
     double rr;     // gamma = r^.r^ of that update's residual
     int32_t iters, active, started, need_rho;
     int32_t status;
-    int32_t rho_valid;  // k_gf: this kernel's partials include the residual monitor
 };
 
 struct RItem {
@@ -97,7 +96,6 @@ struct RItem {
     double* red;   // [reduction blocks] partials of the ordinary kernels
     CgState* st;
     LoopState* ls;  // graph mode (lean tail): ls[2]
-    double *r1, *w1, *s1;  // graph mode, fused iteration (k_gf): the second buffers of r, w, s
     // whole-solve resident kernel (k_cgs): per SELL entry the 16-bit index into the CTA's
     // extended vector (own rows | halo), per CTA the halo (canonical-internal rows it reads from
     // peers, ascending) and the send list (src row | peer << 12 | peer's halo slot << 16), both at
@@ -2554,352 +2552,6 @@ __global__ void __launch_bounds__(JNT, 1) k_gt(const RItem* __restrict__ items, 
     }
 }
 
-// Graph mode, FUSED iteration: ONE kernel per CG iteration does the update AND the next SpMV.
-// Update i needs alpha_i, beta_i, which come from the previous SpMV's global dots; the SpMV of
-// r_{i+1} needs the neighbours' r_{i+1}. Both are available inside one kernel because
-//  * every CTA reduces the previous kernel's per-CTA partials itself (fixed order: the same
-//    scalars in all CTAs) while its producer already streams the first tiles, and
-//  * a neighbour's r_{i+1} outside the tile is recomputed from the previous buffers --
-//    r_{i+1} = r_i - alpha (w_i + beta s_{i-1}), the owner's exact operation sequence, so
-//    bit-identical -- instead of waiting for its owner: r, w and s are double-buffered by
-//    iteration parity (read buffer `par`, write `par ^ 1`), p and x are own-row only.
-// Per tile (consumer warp = 32-row slice, lane = row): s = w + beta s ; p = r + beta p ;
-// r -= alpha s ; x += alpha p (+ the deferred alpha_{i-1} p_{i-1}, odd labels) -> r_{i+1} into
-// the staged r slice (named barrier) -> w = r + A^_off r (in-tile neighbours from shared
-// memory, others recomputed from three L2 gathers) -> the dots of r_{i+1}, w_{i+1}. Compared
-// with k_gur + k_gt: one kernel boundary and one pass over the CG vectors per iteration.
-constexpr int JNSF = 4;  // ring stages of k_gf (a stage carries 6 vector slices + the matrix tile)
-struct FStage {
-    double *r, *q, *w, *s, *p, *x;
-    double* val;
-    uint8_t* col;
-    uint8_t* meta;
-};
-__host__ __device__ inline size_t gf_stage_bytes(int maxe, int mb) {
-    return ((size_t)maxe * 12 + mb + 48 * kJdsRows + 127) & ~(size_t)127;
-}
-
-__global__ void __launch_bounds__(JNT, 1) k_gf(const RItem* __restrict__ items, double* __restrict__ part, int par,
-                                            cudaGraphConditionalHandle h) {
-    extern __shared__ __align__(128) unsigned char jsm[];
-    __shared__ __align__(8) uint64_t full[JNSF], empty[JNSF], ready[JNSF], scal;
-    __shared__ int2 tile_e[JNSF], tile_c[JNSF];
-    __shared__ double sc[3];  // alpha, beta, alpha_pend
-    __shared__ int si[4];     // active, iters, need_rho
-    const RItem& it = items[0];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tb = it.jpart[blockIdx.x], te = it.jpart[blockIdx.x + 1];
-    const int ntl = te - tb;
-    const int maxe = it.jmaxe, kmax = it.jkmax, mb = it.jmbytes;
-    const size_t stage_bytes = gf_stage_bytes(maxe, mb);
-    auto stage = [&](int k) {  // r | q | w | s | p | x | values | columns | lengths + diagonal offsets
-        unsigned char* b = jsm + (size_t)k * stage_bytes;
-        FStage q;
-        q.r = (double*)b;
-        q.q = q.r + kJdsRows;
-        q.w = q.q + kJdsRows;
-        q.s = q.w + kJdsRows;
-        q.p = q.s + kJdsRows;
-        q.x = q.p + kJdsRows;
-        q.val = q.x + kJdsRows;
-        q.col = (uint8_t*)(q.val + maxe);
-        q.meta = q.col + 4 * (size_t)maxe;
-        return q;
-    };
-    const double* __restrict__ Pin = part + 4 * (size_t)gridDim.x * par;
-    double* __restrict__ Pout = part + 4 * (size_t)gridDim.x * (par ^ 1);
-    const double* __restrict__ ra = par ? it.r1 : it.r;
-    const double* __restrict__ wa = par ? it.w1 : it.w;
-    const double* __restrict__ sa = par ? it.s1 : it.sv;
-    double* __restrict__ rb = par ? it.r : it.r1;
-    double* __restrict__ wb = par ? it.w : it.w1;
-    double* __restrict__ sbv = par ? it.sv : it.s1;
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < JNSF; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], JCW);
-            mbar_init(&ready[k], JCW);  // all slices of the stage's tile updated (r_{i+1} staged)
-        }
-        mbar_init(&scal, 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    // PDL: the matrix of the first tiles streams while the previous kernel finishes (see k_gt)
-    const bool live = *(volatile const int*)&it.ls[par].active;
-    const int npre = live ? min(min(g_pdl_pre, JNSF), ntl) : 0;
-    const uint64_t pol = matrix_policy();
-    if (warp == JCW && lane == 0) {
-        for (int i = 0; i < npre; ++i) {
-            const int t = tb + i;
-            const int e0 = it.jeb[t], e1 = it.jeb[t + 1], c0 = it.jcb[t], c1 = it.jcb[t + 1];
-            const FStage q = stage(i);
-            tile_e[i] = make_int2(e0, e1 - e0);
-            tile_c[i] = make_int2(c0, c1 - c0);
-            mbar_expect_tx(&full[i], (uint32_t)(e1 - e0) * 8u + (uint32_t)(c1 - c0) + (uint32_t)mb);
-            bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[i]);
-            if (e1 > e0) {
-                mat_g2s(q.val, it.jval + e0, 8u * (e1 - e0), &full[i], pol);
-                mat_g2s(q.col, it.jcol + c0, (uint32_t)(c1 - c0), &full[i], pol);
-            }
-        }
-    }
-    grid_dep_wait();
-    const LoopState L = it.ls[par];
-    if (!L.active) {  // finished earlier in this graph launch: no-op (keep the next slot inactive)
-        if (blockIdx.x == 0 && threadIdx.x == 0) it.ls[par ^ 1].active = 0;
-        if (warp == JCW && lane == 0)
-            for (int i = 0; i < npre; ++i) {
-                mbar_arrive(&full[i]);
-                mbar_wait(&full[i], 0);
-            }
-        return;
-    }
-    const bool nrho = !L.started || L.need_rho;  // the residual monitor's q stream (see cg_advance)
-    // this update's iteration label (odd: x += alpha p + alpha_{i-1} p_{i-1}) -- known before the
-    // reduction, so the producer streams x only when it moves
-    const bool xstep = ((L.started ? L.iters + 1 : L.iters) & 1) != 0;
-    const int nfirst = min(JNSF, ntl);  // stages issued before the scalars are known
-    const uint32_t vec_bytes = (uint32_t)(8 * kJdsRows) * ((nrho ? 5u : 4u) + (xstep ? 1u : 0u));
-    double v[3] = {0.0, 0.0, 0.0};
-    if (warp == JCW) {
-        // ---- producer: one elected lane streams the vector slices and the matrix of each tile
-        // into the ring, and writes each finished tile's r, s, p, w (x) back with bulk stores
-        if (lane == 0) {
-            double* __restrict__ pv = it.p;
-            double* __restrict__ xv = it.x;
-            auto load_vecs = [&](const FStage& q, int t, uint64_t* bar) {
-                const size_t o = (size_t)t * kJdsRows;
-                bulk_g2s(q.r, ra + o, 8 * kJdsRows, bar);
-                bulk_g2s(q.w, wa + o, 8 * kJdsRows, bar);
-                bulk_g2s(q.s, sa + o, 8 * kJdsRows, bar);
-                bulk_g2s(q.p, pv + o, 8 * kJdsRows, bar);
-                if (xstep) bulk_g2s(q.x, xv + o, 8 * kJdsRows, bar);
-                if (nrho) bulk_g2s(q.q, it.q + o, 8 * kJdsRows, bar);
-            };
-            auto store_vecs = [&](const FStage& q, int t) {
-                const size_t o = (size_t)t * kJdsRows;
-                bulk_s2g(rb + o, q.r, 8 * kJdsRows);
-                bulk_s2g(sbv + o, q.s, 8 * kJdsRows);
-                bulk_s2g(pv + o, q.p, 8 * kJdsRows);
-                bulk_s2g(wb + o, q.w, 8 * kJdsRows);
-                if (xstep) bulk_s2g(xv + o, q.x, 8 * kJdsRows);
-                bulk_commit();
-            };
-            for (int i = 0; i < npre; ++i) {
-                mbar_arrive_expect_tx(&full[i], vec_bytes);
-                load_vecs(stage(i), tb + i, &full[i]);
-            }
-            int e0 = npre < ntl ? it.jeb[tb + npre] : 0, c0 = npre < ntl ? it.jcb[tb + npre] : 0;
-            bool stopped = false;
-            for (int t = tb + npre, i = npre; t < te; ++t, ++i) {
-                const int k = i % JNSF;
-                const int e1 = it.jeb[t + 1], c1 = it.jcb[t + 1];
-                if (i == nfirst) {  // the ring is full: continue only if the recurrence goes on
-                    mbar_wait(&scal, 0);
-                    if (!*(volatile int*)&si[0]) {
-                        stopped = true;
-                        break;
-                    }
-                }
-                if (i >= JNSF) {  // stage k held tile t - JNSF: write it back, then refill
-                    mbar_wait(&empty[k], ((i / JNSF) - 1) & 1);
-                    store_vecs(stage(k), t - JNSF);
-                    bulk_wait_read<0>();
-                }
-                const FStage q = stage(k);
-                const int ne = e1 - e0, nc = c1 - c0;
-                tile_e[k] = make_int2(e0, ne);
-                tile_c[k] = make_int2(c0, nc);
-                mbar_arrive_expect_tx(&full[k], (uint32_t)ne * 8u + (uint32_t)nc + (uint32_t)mb + vec_bytes);
-                load_vecs(q, t, &full[k]);
-                bulk_g2s(q.meta, it.jmeta + (size_t)t * mb, (uint32_t)mb, &full[k]);
-                if (ne) {
-                    mat_g2s(q.val, it.jval + e0, 8u * ne, &full[k], pol);
-                    mat_g2s(q.col, it.jcol + c0, (uint32_t)nc, &full[k], pol);
-                }
-                e0 = e1;
-                c0 = c1;
-            }
-            if (!stopped) {
-                if (ntl <= nfirst) mbar_wait(&scal, 0);
-                if (*(volatile int*)&si[0]) {  // write back the tiles still in the ring
-                    for (int i = max(ntl - JNSF, 0); i < ntl; ++i) {
-                        const int k = i % JNSF;
-                        mbar_wait(&empty[k], (i / JNSF) & 1);
-                        store_vecs(stage(k), tb + i);
-                    }
-                }
-            }
-            bulk_wait_all<0>();  // the stores are complete before the kernel ends
-        }
-    } else {
-        // ---- consumer warp 0 reduces the previous SpMV's partials and advances the recurrence
-        if (warp == 0) {
-            // the order of cg_tail / k_gur (32 consecutive partials per warp sum, warp sums in
-            // sequence), so the scalars -- and the iterates -- equal the other graph paths' bit for bit
-            double g = 0.0, d = 0.0, rh = 0.0;
-            for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32) {
-                const int b = b0 + lane;
-                const bool ok = b < (int)gridDim.x;
-                const double g1 = warp_sum_d(ok ? __ldcg(Pin + 4 * b) : 0.0);
-                const double d1 = warp_sum_d(ok ? __ldcg(Pin + 4 * b + 1) : 0.0);
-                const double r1 = warp_sum_d(ok ? __ldcg(Pin + 4 * b + 2) : 0.0);
-                g += g1;
-                d += d1;
-                rh += r1;
-            }
-            if (lane == 0) {
-                const CgState* S = it.st;
-                const double tol2 = S->tol2, bn2 = S->bn2;
-                int active = 0, status = L.status, iters = L.iters;
-                double alpha = 0.0, beta = 0.0;
-                if (!L.started) {
-                    const bool fin = isfinite(g) && isfinite(bn2);
-                    active = (bn2 > 0.0 && rh > tol2 && fin && L.iters < S->max_iter) ? 1 : 0;
-                    if (!fin) status = FEMI_E_NONFINITE;
-                    if (active && !(d > 0.0)) {
-                        status = FEMI_E_NEG_CURVATURE;
-                        active = 0;
-                    }
-                    if (active) alpha = g / d;
-                } else {
-                    iters = L.iters + 1;
-                    if (!isfinite(g) || !isfinite(d)) {
-                        status = FEMI_E_NONFINITE;
-                    } else if (L.rho_valid && rh <= tol2) {
-                        // converged
-                    } else if (iters >= S->max_iter) {
-                        status = FEMI_E_NOT_CONVERGED;
-                    } else {
-                        beta = g / L.rr;
-                        const double den = d - beta * g / L.alpha;
-                        if (!(den > 0.0)) {
-                            status = FEMI_E_NEG_CURVATURE;
-                        } else {
-                            alpha = g / den;
-                            active = 1;
-                        }
-                    }
-                }
-                const bool deferred = L.started && (L.iters & 1) == 0;
-                sc[0] = alpha;
-                sc[1] = beta;
-                sc[2] = deferred ? L.alpha : 0.0;
-                si[0] = active;
-                si[1] = iters;
-                si[2] = (g * it.dmin <= 100.0 * tol2) ? 1 : 0;
-                if (blockIdx.x == 0) {
-                    LoopState N;
-                    N.alpha = alpha;
-                    N.rr = g;
-                    N.iters = iters;
-                    N.active = active;
-                    N.started = 1;
-                    N.need_rho = si[2];
-                    N.status = status;
-                    N.rho_valid = nrho ? 1 : 0;
-                    it.ls[par ^ 1] = N;
-                    if (!active) {
-                        CgState* Sw = it.st;
-                        Sw->iters = iters;
-                        Sw->status = status;
-                        Sw->active = 0;
-                        Sw->x_pend = deferred ? 1 : 0;
-                        Sw->alpha_pend = L.alpha;
-                        Sw->rr = g;
-                        if (h) cudaGraphSetConditional(h, 0u);
-                    }
-                }
-                mbar_arrive(&scal);
-            }
-            __syncwarp();
-        }
-        mbar_wait(&scal, 0);
-        const bool active = si[0] != 0;
-        if (!active) {  // converged / stopped: let the issued stages land, then leave
-            for (int i = 0; i < nfirst; ++i) mbar_wait(&full[i], 0);
-        } else {
-            const double alpha = sc[0], beta = sc[1], ap = sc[2];
-            const int rl = 32 * warp + lane;
-            // the update of tile j + 1 runs before the SpMV of tile j: a warp waits only for the
-            // other slices' updates of the tile it multiplies (ready[]), not in lockstep
-            auto update = [&](int i) {
-                const int k = i % JNSF;
-                mbar_wait(&full[k], (i / JNSF) & 1);
-                const FStage q = stage(k);
-                const double r0 = q.r[rl], w0 = q.w[rl], s0 = q.s[rl], p0 = q.p[rl];
-                const double s1 = fma(beta, s0, w0);
-                const double p1 = fma(beta, p0, r0);
-                q.r[rl] = fma(-alpha, s1, r0);  // r_{i+1}: written back and used by the in-tile gathers
-                q.s[rl] = s1;
-                q.p[rl] = p1;
-                if (xstep) q.x[rl] = fma(alpha, p1, fma(ap, p0, q.x[rl]));
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&ready[k]);
-            };
-            if (ntl > 0) update(0);
-            for (int t = tb, i = 0; t < te; ++t, ++i) {
-                const int k = i % JNSF;
-                if (t + 1 < te) update(i + 1);
-                mbar_wait(&ready[k], (i / JNSF) & 1);
-                const FStage q = stage(k);
-                const int64_t row = (int64_t)t * kJdsRows + rl;
-                const double r1 = q.r[rl];
-                // ---- w = r + A^_off r on r_{i+1}
-                const int len = q.meta[rl];
-                const uint16_t* doff = (const uint16_t*)(q.meta + kJdsRows) + warp * kmax;
-                const double qi = nrho ? q.q[rl] : 0.0;
-                const int Lk = __shfl_sync(0xffffffffu, len, 0);
-                const bool wide = tile_c[k].y > 2 * tile_e[k].y;
-                const int16_t* c16 = (const int16_t*)q.col;
-                const int32_t* c32 = (const int32_t*)q.col;
-                const int64_t tr0 = (int64_t)t * kJdsRows;
-                double acc = 0.0;
-                for (int k0 = 0; k0 < Lk; k0 += 8) {
-                    double vv[8], gv[8];
-                    int c[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const bool a = k0 + u < len;
-                        const int idx = (k0 + u < Lk ? doff[k0 + u] : 0) + lane;
-                        vv[u] = a ? q.val[idx] : 0.0;
-                        c[u] = a ? (wide ? c32[idx] : (int)c16[idx]) : rl;
-                        FEMI_DCHECK(!a || idx < tile_e[k].y, 3);
-                        FEMI_DCHECK((unsigned)c[u] < (unsigned)kJdsRows ||
-                                        (tr0 + c[u] >= 0 && tr0 + c[u] < (int64_t)it.ntile * kJdsRows),
-                                    3);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if ((unsigned)c[u] < (unsigned)kJdsRows) {
-                            gv[u] = q.r[c[u]];
-                        } else {  // outside the tile: the neighbour's r_{i+1}, recomputed
-                            const int64_t gi = tr0 + c[u];
-                            gv[u] = fma(-alpha, fma(beta, sa[gi], wa[gi]), ra[gi]);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = fma(vv[u], gv[u], acc);
-                }
-                const double y = r1 + acc;
-                q.w[rl] = y;  // w_{i+1} into the stage (the update of this row has used w_i)
-                fence_proxy_async();  // the stage's slices are read by the producer's bulk stores
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[k]);
-                if (row < it.n) {
-                    const double ru = r1 * qi;
-                    v[0] += r1 * r1;
-                    v[1] += y * r1;
-                    v[2] += ru * ru;
-                }
-            }
-        }
-    }
-    mbar_wait(&scal, 0);
-    if (!si[0]) return;  // uniform across the CTA (shared scalars)
-    cta_partials<JNT>(v, Pout + 4 * (size_t)blockIdx.x);
-}
-
 // ------------------------------------------------------------------ shared-matrix multi-RHS
 // NR <= 4 right-hand sides on ONE large system (colour channels): one CG
 // recurrence per RHS (own scalars, own convergence), but every iteration streams the matrix
@@ -3181,7 +2833,6 @@ struct GraphCache {
     bool item_dev_valid = false;
     int gs_blocks = 0, gx = 0, gt_blocks = 0;
     unsigned gt_smem = 0;  // > 0: the SpMV is the TMA-streamed k_gt (JDS layout); else SELL k_gs
-    unsigned gf_smem = 0;  // > 0: the fused iteration kernel k_gf fits
     int gt_ns = JNS;       // ring stages of k_gt (FEMI_JNS=8: the deeper ring when it fits)
     const void* mat_base = nullptr;  // the SpMV's matrix stream (one allocation) and its size
     size_t mat_bytes = 0;
@@ -3341,22 +2992,8 @@ femi_status build_graph(GraphCache& C, bool restart, cudaGraphExec_t* out, bool 
         const dim3 gu(gu_ctas);
         // inside the body, k_gu -> k_gt -> k_gu ... are programmatic edges (k_gt streams its
         // first matrix tiles while k_gu runs; each waits in grid_dep_wait for its inputs)
-        // FEMI_FUSED=1: one fused kernel per iteration (k_gf) instead of k_gur + k_gt -- measured
-        // slower at C5 (42.9 vs 33.3 us per iteration: one 544-thread CTA per SM carries the
-        // vector streams of the update through its TMA ring), kept as an experiment
-        static const bool fused = [] {
-            const char* e = std::getenv("FEMI_FUSED");
-            return e && e[0] == '1';
-        }();
         for (int k = 0; k < kUnroll; ++k) {
-            if (tma && fused && C.gf_smem > 0) {
-                // fused iteration: update + SpMV in one kernel (k_gf), parity k & 1
-                int par = k & 1;
-                void* a_gf[4] = {&di, &part, &par, &h};
-                if ((s = add_kernel_pdl(body, bprev ? &bprev : nullptr, (void*)k_gf, gsp, bsp, a_gf, &sn,
-                                        C.gf_smem)))
-                    return s;
-            } else if (tma) {
+            if (tma) {
                 // lean tail: k_gur (reduce the SpMV partials + update, body slot parity k & 1)
                 // -> k_gt (reads the scalars k_gur published in ls[(k + 1) & 1])
                 int par = k & 1, lsi = (k + 1) & 1, np = C.gt_blocks;
@@ -3463,33 +3100,14 @@ femi_status loop_prof_end(cudaStream_t st) {
     return FEMI_OK;
 }
 
-// Tiles -> k_gt CTAs: contiguous ranges, equal tile counts by default. FEMI_JPART_A=a weights
-// them by cost(tile) = a + stored entries instead. Measured at C5 (FEMI_CTA_PROF): under the
-// equal split the CTA times (14.7 .. 18.4 us) correlate 0.8 with the entry counts, yet the
-// cost-weighted split is slower (a = 5000: +0.02 ms per solve, 3700: +0.1, 2500: +0.19) --
-// the spread follows the image region, not the entry count -- so equal ranges stay.
+// Tiles -> k_gt CTAs: contiguous ranges of equal tile counts. (Measured at C5 with
+// FEMI_CTA_PROF: the CTA times correlate 0.8 with the entry counts, yet a split weighted by
+// cost(tile) = a + stored entries was slower for every a tried -- +0.02 to +0.19 ms per solve:
+// the spread follows the image region, not the entry count -- so it was removed.)
 femi_status tile_split(const femi_system_s* S, int nblocks, std::vector<int32_t>& jpart) {
     const int nt = S->jds_ntile;
     jpart.assign(nblocks + 1, 0);
-    const char* env = std::getenv("FEMI_JPART_A");
-    if (!env) {
-        for (int b = 0; b <= nblocks; ++b) jpart[b] = (int)((int64_t)nt * b / nblocks);
-        return FEMI_OK;
-    }
-    std::vector<int32_t> eb(nt + 1);
-    FEMI_CUDA(cudaMemcpy(eb.data(), S->jds_eb, sizeof(int32_t) * eb.size(), cudaMemcpyDeviceToHost));
-    const double A = std::atof(env);
-    jpart[nblocks] = nt;
-    const double total = A * nt + (double)eb[nt];
-    int t = 0;
-    for (int b = 1; b < nblocks; ++b) {
-        const double target = total * b / nblocks;
-        while (t < nt && A * (t + 1) + (double)eb[t + 1] <= target) ++t;
-        // nearer of the two boundaries around the target; every CTA keeps >= 1 tile
-        if (t < nt && target - (A * t + (double)eb[t]) > (A * (t + 1) + (double)eb[t + 1]) - target) ++t;
-        jpart[b] = std::max(jpart[b - 1] + 1, std::min(t, nt - (nblocks - b)));
-        t = jpart[b];
-    }
+    for (int b = 0; b <= nblocks; ++b) jpart[b] = (int)((int64_t)nt * b / nblocks);
     return FEMI_OK;
 }
 
@@ -3551,12 +3169,6 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
                                        (const void*)k_gt<false, false>})
                     FEMI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)(JNS * stage_bytes)));
-                const size_t gfb = JNSF * gf_stage_bytes(S->jds_maxe, S->jds_meta_bytes);
-                if (gfb + 4096 <= (size_t)optin) {
-                    C->gf_smem = (unsigned)gfb;
-                    FEMI_CUDA(cudaFuncSetAttribute((const void*)k_gf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)C->gf_smem));
-                }
                 femi_status ts = tile_split(S, C->gt_blocks, jpart);
                 if (ts != FEMI_OK) return ts;
             }
@@ -3565,7 +3177,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         const size_t bytes = al(sizeof(int32_t) * (jpart.size() + 1)) + al(sizeof(RItem)) + al(sizeof(CgState)) +
                              al(sizeof(LoopState) * 2) +
                              al(sizeof(unsigned) * 4) + al(sizeof(double) * 8 * pb) + al(sizeof(double) * C->gx) +
-                             9 * vb;
+                             6 * vb;
         FEMI_CUDA(cudaMalloc(&C->ws, bytes));
         char* cur = (char*)C->ws;
         auto take = [&](size_t x) {
@@ -3580,7 +3192,7 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         C->d_state = (CgState*)take(sizeof(CgState));
         LoopState* d_ls = (LoopState*)take(sizeof(LoopState) * 2);
         C->d_cnt = (unsigned*)take(sizeof(unsigned) * 4);
-        C->d_part = (double*)take(sizeof(double) * 8 * pb);  // two parities (k_gf)
+        C->d_part = (double*)take(sizeof(double) * 8 * pb);
         RItem& it = C->item;
         it.red = (double*)take(sizeof(double) * C->gx);
         it.b = (double*)take(vb);
@@ -3589,9 +3201,6 @@ femi_status graph_solve(femi_system_s* S, const double* g, const double* bin, do
         it.w = (double*)take(vb);
         it.p = (double*)take(vb);
         it.sv = (double*)take(vb);
-        it.r1 = (double*)take(vb);  // k_gf: second buffers of r, w, s
-        it.w1 = (double*)take(vb);
-        it.s1 = (double*)take(vb);
         C->mat_base = S->jds_val;
         C->mat_bytes = S->jds_block_bytes;
         if (g_l2pol_host == 3 && C->gt_smem > 0 && C->mat_bytes > 0) {
