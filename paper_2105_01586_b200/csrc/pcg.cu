@@ -3073,7 +3073,7 @@ femi_status loop_prof_end(cudaStream_t st) {
                 std::fprintf(stderr, "[femi cta] %d %.3f %.3f\n", b, (cp[2 * b] - t0) / 1e3, (cp[2 * b + 1] - t0) / 1e3);
     }
     double su = 0, sg = 0, g1 = 0, g2 = 0, c0 = 0, c1 = 0, c2 = 0, tA = 0, tB = 0;
-    int cnt = 0;
+    int cnt = 0, ctail = 0;  // ctail: iterations with last-CTA tail stamps (not the lean tail)
     for (int k = 1; k + 1 < kLoopProfMax; ++k) {
         const unsigned long long* a = &ts[4 * k];
         const unsigned long long* nx = &ts[4 * (k + 1)];
@@ -3085,18 +3085,24 @@ femi_status loop_prof_end(cudaStream_t st) {
         c0 += (double)t2[4 * k + 1] - (double)a[2];
         c1 += (double)t2[4 * k + 2] - (double)a[2];
         c2 += (double)t2[4 * k + 3] - (double)a[2];
-        tA += (double)t3[4 * k] - (double)a[2];
-        tB += (double)t3[4 * k + 1] - (double)a[2];
+        if (t3[4 * k] && t3[4 * k + 1]) {
+            tA += (double)t3[4 * k] - (double)a[2];
+            tB += (double)t3[4 * k + 1] - (double)a[2];
+            ++ctail;
+        }
         ++cnt;
     }
-    if (cnt)
+    if (cnt) {
         std::fprintf(stderr,
                      "[femi loop] %d iterations: k_gu span %.2f us, gap %.2f, SpMV span %.2f us, gap %.2f -> %.2f "
-                     "us/iteration | SpMV from first CTA start: first CTA done +%.2f, last CTA done +%.2f, last CTA "
-                     "arrival +%.2f, partials summed +%.2f, last CTA out +%.2f\n",
+                     "us/iteration | SpMV from first CTA start: first CTA done +%.2f, last CTA done +%.2f",
                      cnt, su / cnt / 1e3, g1 / cnt / 1e3, sg / cnt / 1e3, g2 / cnt / 1e3,
-                     (su + sg + g1 + g2) / cnt / 1e3, c0 / cnt / 1e3, c1 / cnt / 1e3, tA / cnt / 1e3, tB / cnt / 1e3,
-                     c2 / cnt / 1e3);
+                     (su + sg + g1 + g2) / cnt / 1e3, c0 / cnt / 1e3, c1 / cnt / 1e3);
+        if (ctail)  // last-CTA tail only (the lean tail has no arrival counter)
+            std::fprintf(stderr, ", last CTA arrival +%.2f, partials summed +%.2f", tA / ctail / 1e3,
+                         tB / ctail / 1e3);
+        std::fprintf(stderr, ", last CTA out +%.2f\n", c2 / cnt / 1e3);
+    }
     return FEMI_OK;
 }
 
