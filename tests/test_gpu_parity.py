@@ -484,8 +484,7 @@ np.save(sys.argv[2], R["u_vert"].cpu().numpy())
 
 def test_graph_mode_switches_bit_identical(tmp_path):
     """The graph-mode performance paths change timing, not arithmetic: programmatic dependent
-    launch, the in-tile shared-memory gathers and k_gur's 16-byte pair accesses on (default) or
-    off give bit-identical
+    launch and the in-tile shared-memory gathers on (default) or off give bit-identical
     solutions (deterministic fixed-order reductions). Separate processes: the switches are
     read once per process."""
     import os
@@ -493,7 +492,7 @@ def test_graph_mode_switches_bit_identical(tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for k, env_add in enumerate(({}, {"FEMI_NO_PDL": "1", "FEMI_SMEM_GATHER": "0", "FEMI_GUR_VEC": "0"})):
+    for k, env_add in enumerate(({}, {"FEMI_NO_PDL": "1", "FEMI_SMEM_GATHER": "0"})):
         out = str(tmp_path / f"u{k}.npy")
         env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root, out], check=True, env=env, timeout=600)
